@@ -1,0 +1,204 @@
+/* trims.h — C ABI of the B200-native TrIMS model store (libtrims.so).
+ *
+ * This is the drop-in boundary for the reference's load-and-serve path
+ * (SURVEY.md §8b). Plain pointers, sizes and ints only; every function
+ * returns 0 or a reference Errc value (proj/include/mrm/error.hpp:11-56;
+ * wire codes 1..7 unchanged) and never lets a C++ exception cross the ABI.
+ * trims_last_error() returns the thread's last failure message.
+ *
+ * Each entry point names the reference interface it replaces (file:line,
+ * relative to /root/reference). INTEGRATION.md shows how a maintainer binds
+ * it from the reference side (C++ TierBackend subclass / client SDK shim).
+ */
+#ifndef TRIMS_H
+#define TRIMS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- errors */
+
+/* error.cpp:5-38 errc_name */
+const char* trims_errc_name(int code);
+/* error.cpp:41-69 wire_code: collapse a fine code onto wire codes 1..7 */
+int trims_wire_code(int code);
+/* thread-local detail of the last non-zero return */
+const char* trims_last_error(void);
+/* library / device facts: cuda device count (0 on GPU-less hosts), SHA-NI use */
+int trims_device_count(void);
+int trims_sha_hw(void);
+
+/* ------------------------------------------------- artifact format (a1, a2, a7) */
+
+/* Sha256::of (proj/src/sha256.cpp:24-123) */
+int trims_sha256(const void* data, uint64_t n, uint8_t out[32]);
+
+/* model::read_manifest(path, full_verify) (model_format.cpp:370-409).
+ * json_out gets the canonical manifest JSON (nlohmann dump() bytes). */
+int trims_read_manifest(const char* path, int full_verify, char* json_out, uint64_t cap,
+                        uint8_t checksum_out[32], uint64_t* blob_bytes, uint64_t* blob_file_offset);
+
+/* model::manifest_from_json -> manifest_to_json round trip (model_format.cpp:179-229) */
+int trims_manifest_canonical(const char* json_in, char* json_out, uint64_t cap);
+
+/* model::make_manifest (model_format.cpp:158-177). decls: "name dtype d0,d1,...\n" */
+int trims_make_manifest(const char* ns, const char* name, const char* version, const char* decls,
+                        uint64_t workspace_bytes, char* json_out, uint64_t cap);
+
+/* model::write_model_file (model_format.cpp:293-305): blob = full blob_bytes
+ * (padding included) of the manifest. */
+int trims_write_model(const char* path, const char* manifest_json, const void* blob);
+
+/* shm::layout_for (shared_segment.cpp:63-95). kind 0 model, 1 layer, 2 block.
+ * Output lines "name segment offset length\n". */
+int trims_layout_for(const char* manifest_json, uint32_t kind, uint64_t block_bytes, char* out,
+                     uint64_t cap);
+
+/* The ingest plan (new: the reference keeps artifact bytes verbatim).
+ * flags bit0 = convert floating tensors to out_dtype, bit1 = KCRS->KRSC for
+ * 4-D tensors. out_dtype uses the manifest dtype codes: 0 f64 1 f32 2 f16
+ * 3 i8 4 bf16. Writes the resident manifest JSON. */
+#define TRIMS_PLAN_CONVERT 1u
+#define TRIMS_PLAN_PERMUTE_4D 2u
+int trims_resident_manifest(const char* src_json, uint32_t plan_flags, uint32_t out_dtype, char* json_out,
+                            uint64_t cap);
+
+/* ---------------------------------- synthetic weights (a12, K5), host side */
+
+/* bench::gen_catalog inner loop (catalog.cpp:143-154): n splitmix64 words of
+ * stream `stream_seed` starting at element k0 (multi-threaded). */
+int trims_fill_splitmix_host(uint64_t* dst, uint64_t n, uint64_t stream_seed, uint64_t k0);
+/* uniform fp32 init fmaf(hi-lo, u24*2^-24, lo) (our definition, K5) */
+int trims_fill_uniform_host(float* dst, uint64_t n, uint64_t stream_seed, uint64_t j0, float lo, float hi);
+/* bench::fnv1a (catalog.cpp:79-86) */
+uint64_t trims_fnv1a(const char* s);
+/* Client::touch (client.cpp:338-359) over a host blob + manifest */
+int trims_touch_host(const void* blob, const char* manifest_json, uint64_t* out);
+/* TRIMS block checksum over a host buffer (CPU twin of the device K4) */
+int trims_checksum_host(const void* p, uint64_t n, uint64_t word0, uint64_t* out);
+
+/* --------------------------------------------- the store (CacheCore + CudaTierBackend) */
+
+typedef struct trims_store trims_store;
+
+typedef struct trims_store_config {
+  uint64_t fast_capacity_bytes;  /* daemon.hpp:21 (HBM budget, logical bytes) */
+  uint64_t host_capacity_bytes;  /* daemon.hpp:22 (pinned DRAM budget) */
+  uint64_t disk_capacity_bytes;  /* daemon.hpp:24 */
+  uint32_t policy;               /* 0 LRU, 1 LCU (daemon.hpp:26) */
+  uint32_t eager_reclaim;        /* daemon.hpp:27 */
+  uint32_t full_verify;          /* daemon.hpp:32 */
+  int32_t device;                /* CUDA ordinal of this store's fast tier */
+  const char* disk_cache_dir;    /* daemon.hpp:23 */
+  uint32_t plan_flags;           /* TRIMS_PLAN_* (0 = bytes verbatim, reference behaviour) */
+  uint32_t out_dtype;            /* target dtype when TRIMS_PLAN_CONVERT */
+  uint64_t pinned_pool_bytes;    /* pre-pinned host pool (0 = host_capacity_bytes) */
+  uint32_t scan_disk;            /* register *.trms in disk_cache_dir at start (daemon.cpp:314-325) */
+  uint32_t read_threads;         /* parallel pread threads for disk -> pinned (0 = 8) */
+} trims_store_config;
+
+/* Reference outcomes (cache_core.hpp:36) + PEER_HIT for the multi-GPU directory. */
+enum { TRIMS_FAST_HIT = 0, TRIMS_HOST_HIT = 1, TRIMS_DISK_LOAD = 2, TRIMS_REMOTE_FETCH = 3, TRIMS_PEER_HIT = 4 };
+
+/* One open's result: PlacementResult (cache_core.hpp:48-57) + the exported
+ * segment (ExportedSegment cache_core.hpp:59-63 / wire ObjectRef
+ * wire_protocol.hpp:44-62) carrying a cuMem POSIX-fd instead of a shm name. */
+typedef struct trims_export {
+  uint64_t model_id;
+  uint32_t outcome;
+  int32_t device;
+  uint64_t generation;
+  uint64_t payload_bytes;         /* resident blob + JSON + 8 */
+  uint64_t resident_blob_bytes;
+  uint64_t alloc_bytes;           /* physical cuMem allocation (granularity-rounded) */
+  uint64_t weights_bytes;         /* artifact footprint (accounting unit) */
+  uint64_t workspace_bytes;
+  uint64_t ingest_checksum;       /* TRIMS block checksum of the resident blob */
+  uint64_t timings_ns[4];         /* fetch, disk_read, host_to_fast_copy, handle_export */
+  uint8_t manifest_digest[32];    /* SHA-256 of the resident manifest JSON */
+  void* dev_ptr;                  /* owner-process device address */
+  int32_t fd;                     /* owner-process fd of the allocation */
+  uint32_t n_objects;             /* layout_for(resident manifest, granularity) count */
+  char token[160];
+} trims_export;
+
+/* Daemon::Daemon (daemon.cpp:298-391) minus listeners: builds the backend
+ * and the core, optionally scans the disk cache. */
+int trims_store_create(const trims_store_config* cfg, trims_store** out);
+void trims_store_destroy(trims_store* s); /* Daemon::join: drop_all (daemon.cpp:597) */
+
+/* Daemon::handle_open -> CacheCore::open_model (daemon.cpp:452-476,
+ * cache_core.cpp:194-423). The logical clock advances per open. */
+int trims_store_open(trims_store* s, const char* ns, const char* name, const char* version,
+                     uint32_t gran_kind, uint64_t block_bytes, trims_export* out);
+/* CacheCore::close_model (cache_core.cpp:425-445) */
+int trims_store_close(trims_store* s, const char* ns, const char* name, const char* version,
+                      uint64_t* refcount_out);
+/* CacheCore::reclaim (cache_core.cpp:168-171); evicted keys as "ns/name@ver\n" */
+int trims_store_reclaim(trims_store* s, uint32_t tier, uint64_t bytes, uint32_t policy, char* out,
+                        uint64_t cap);
+/* CacheCore::register_disk_file (cache_core.cpp:474-485) */
+int trims_store_register_disk_file(trims_store* s, const char* ns, const char* name,
+                                   const char* version, const char* path, uint64_t bytes);
+/* CacheCore::drop_all (cache_core.cpp:512-529) */
+int trims_store_drop_all(trims_store* s);
+/* CacheCore::stats (cache_core.cpp:447-472) as a JSON document. */
+int trims_store_stats_json(trims_store* s, char* out, uint64_t cap);
+/* The resident manifest JSON of a fast-resident model. */
+int trims_store_resident_json(trims_store* s, uint64_t model_id, char* out, uint64_t cap);
+/* Last ingest of a model: h2d_ms, total_ms, read_ms, h2d_bytes, launches. */
+int trims_store_ingest_stats(trims_store* s, uint64_t model_id, double out5[5]);
+/* Per-tensor block checksums of a resident model (buckets = tensors + 1). */
+int trims_store_checksums(trims_store* s, uint64_t model_id, uint64_t* out, uint64_t cap, uint64_t* n);
+
+/* --------------------------------------------------- client attach (a5, a9) */
+
+typedef struct trims_import trims_import;
+/* Attachment::attach (shared_segment.cpp:212-245): map a segment exported by
+ * another (or this) process read-only. fd must be valid in the caller. The
+ * tail is validated (magic, generation, sealed, length) and the manifest
+ * digest re-checked (client.cpp:284-291). */
+int trims_import_open(int device, int fd, uint64_t alloc_bytes, uint64_t generation, uint64_t payload_bytes,
+                      const uint8_t digest[32], trims_import** out, void** dev_ptr);
+/* Resident manifest JSON carried by the imported segment (client.cpp:293-307). */
+int trims_import_manifest(trims_import* im, char* out, uint64_t cap);
+int trims_import_read_only(trims_import* im);
+/* Device-side integrity check of an attached segment: K4 over the resident
+ * blob, compared with the checksum sealed into the tail (Corrupt if not). */
+int trims_import_verify(trims_import* im, uint64_t* checksum_out);
+void trims_import_close(trims_import* im);
+
+/* ------------------------------------------- ingest kernels (K1..K5) raw */
+
+/* Pinned/pageable host raw blob -> resident blob on the device (what
+ * publish_fast runs; daemon.cpp:160-209 + new convert/permute/checksum). */
+int trims_ingest_host(int device, const void* host_blob, const char* src_json, uint32_t plan_flags,
+                      uint32_t out_dtype, void* dev_dst, uint64_t* checksum_out, double stats_out5[5]);
+/* HBM-resident raw blob -> resident blob, async on `stream` (cudaStream_t).
+ * Bucket sums are accumulated into d_sums (must be zeroed by the caller). */
+int trims_transform_device(int device, const void* dev_src, const char* src_json, uint32_t plan_flags,
+                           uint32_t out_dtype, void* dev_dst, unsigned long long* d_sums, void* stream);
+/* Roofline accounting of a plan: tiles, buckets, algorithmic read/write bytes. */
+int trims_plan_info(const char* src_json, uint32_t plan_flags, uint32_t out_dtype, uint64_t out4[4]);
+/* TRIMS block checksum of a device range (async, accumulates into *d_out). */
+int trims_checksum_device(const void* dev, uint64_t nbytes, uint64_t word0, unsigned long long* d_out,
+                          void* stream);
+/* K5 on device: splitmix words / uniform fp32 (bit-identical to the host fills). */
+int trims_fill_splitmix_device(uint64_t* dev, uint64_t n, uint64_t stream_seed, uint64_t k0, void* stream);
+int trims_fill_uniform_device(float* dev, uint64_t n, uint64_t stream_seed, uint64_t j0, float lo, float hi,
+                              void* stream);
+
+/* ------------------------------------------------------------ test hooks */
+
+/* Replays a decision trace through this library's CacheCore over an
+ * in-memory backend (the reference FakeBackend contract, oracle.cpp:14-91).
+ * Same spec / output text as oracle/ref_shim.cpp:ref_replay's "live" lines. */
+int trims_replay(const char* spec, char* out, uint64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRIMS_H */

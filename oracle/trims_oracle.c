@@ -135,7 +135,16 @@ void tro_f32_to_bf16(const uint32_t* src, uint64_t n, uint16_t* dst) {
 }
 
 void tro_f64_to_f32(const double* src, uint64_t n, float* dst) {
-  for (uint64_t i = 0; i < n; ++i) dst[i] = (float)src[i];
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t u;
+    memcpy(&u, &src[i], 8);
+    if ((u & 0x7fffffffffffffffull) > 0x7ff0000000000000ull) { /* NaN: canonical quiet, sign kept */
+      uint32_t q = (uint32_t)((u >> 32) & 0x80000000u) | 0x7fc00000u;
+      memcpy(&dst[i], &q, 4);
+    } else {
+      dst[i] = (float)src[i];
+    }
+  }
 }
 
 static uint16_t f64_to_bf16_1(uint64_t u) {

@@ -50,7 +50,7 @@ double tro_share_benefit(double bytes, double n_objects, double q, double o, dou
  * largest finite bf16 become +-Inf (IEEE RNE overflow). */
 uint16_t tro_f32_to_bf16_1(uint32_t bits);
 void tro_f32_to_bf16(const uint32_t* src, uint64_t n, uint16_t* dst);
-/* f64 -> f32 (IEEE RNE, the C cast) and f64 -> bf16 (via a single rounding
+/* f64 -> f32 (IEEE RNE, the C cast; NaN -> 0x7fc00000 | sign) and f64 -> bf16 (via a single rounding
  * from f64: round-to-nearest-even at bit 48 of the f64 mantissa after
  * rebasing the exponent; subnormal results flush per IEEE RNE). */
 void tro_f64_to_f32(const double* src, uint64_t n, float* dst);

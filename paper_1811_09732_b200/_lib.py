@@ -1,0 +1,178 @@
+"""ctypes binding of libtrims.so (include/trims.h).
+
+The library is built in-tree (``make -C paper_1811_09732_b200/csrc``, or
+``__graft_entry__.build()``). There is no fallback: importing the package
+without it raises, and every device entry point fails loudly on a host
+without a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtrims.so")
+
+
+class TrimsError(RuntimeError):
+    """A non-zero return of the C ABI; ``code`` is the reference Errc value."""
+
+    def __init__(self, code: int, name: str, detail: str):
+        super().__init__(f"{name}({code}): {detail}")
+        self.code = code
+        self.name = name
+        self.detail = detail
+
+
+# Errc values (proj/include/mrm/error.hpp:11-56), for callers that branch on them.
+class Errc:
+    NotFound = 1
+    TooLargeForFast = 2
+    NoEvictableSpace = 3
+    NotOpen = 4
+    Corrupt = 5
+    ProtocolError = 6
+    Internal = 7
+    LengthMismatch = 100
+    BadMagic = 101
+    UnsupportedVersion = 102
+    CorruptManifest = 103
+    ChecksumMismatch = 104
+    NoSuchSegment = 112
+    StaleGeneration = 113
+    NotSealed = 115
+    UnknownModel = 120
+    RemoteNotFound = 140
+    DaemonUnreachable = 150
+    ConnectionLost = 151
+    InvalidArgument = 160
+    CudaError = 170
+    OutOfDeviceMemory = 171
+    NoDevice = 173
+
+
+class StoreConfig(ctypes.Structure):
+    _fields_ = [
+        ("fast_capacity_bytes", ctypes.c_uint64),
+        ("host_capacity_bytes", ctypes.c_uint64),
+        ("disk_capacity_bytes", ctypes.c_uint64),
+        ("policy", ctypes.c_uint32),
+        ("eager_reclaim", ctypes.c_uint32),
+        ("full_verify", ctypes.c_uint32),
+        ("device", ctypes.c_int32),
+        ("disk_cache_dir", ctypes.c_char_p),
+        ("plan_flags", ctypes.c_uint32),
+        ("out_dtype", ctypes.c_uint32),
+        ("pinned_pool_bytes", ctypes.c_uint64),
+        ("scan_disk", ctypes.c_uint32),
+        ("read_threads", ctypes.c_uint32),
+    ]
+
+
+class Export(ctypes.Structure):
+    _fields_ = [
+        ("model_id", ctypes.c_uint64),
+        ("outcome", ctypes.c_uint32),
+        ("device", ctypes.c_int32),
+        ("generation", ctypes.c_uint64),
+        ("payload_bytes", ctypes.c_uint64),
+        ("resident_blob_bytes", ctypes.c_uint64),
+        ("alloc_bytes", ctypes.c_uint64),
+        ("weights_bytes", ctypes.c_uint64),
+        ("workspace_bytes", ctypes.c_uint64),
+        ("ingest_checksum", ctypes.c_uint64),
+        ("timings_ns", ctypes.c_uint64 * 4),
+        ("manifest_digest", ctypes.c_uint8 * 32),
+        ("dev_ptr", ctypes.c_void_p),
+        ("fd", ctypes.c_int32),
+        ("n_objects", ctypes.c_uint32),
+        ("token", ctypes.c_char * 160),
+    ]
+
+
+_c = ctypes
+_u64 = _c.c_uint64
+_u32 = _c.c_uint32
+_p = _c.c_void_p
+_s = _c.c_char_p
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "trims_errc_name": (_s, [_c.c_int]),
+    "trims_wire_code": (_c.c_int, [_c.c_int]),
+    "trims_last_error": (_s, []),
+    "trims_device_count": (_c.c_int, []),
+    "trims_sha_hw": (_c.c_int, []),
+    "trims_sha256": (_c.c_int, [_p, _u64, _p]),
+    "trims_read_manifest": (_c.c_int, [_s, _c.c_int, _s, _u64, _p, _c.POINTER(_u64), _c.POINTER(_u64)]),
+    "trims_manifest_canonical": (_c.c_int, [_s, _s, _u64]),
+    "trims_make_manifest": (_c.c_int, [_s, _s, _s, _s, _u64, _s, _u64]),
+    "trims_write_model": (_c.c_int, [_s, _s, _p]),
+    "trims_layout_for": (_c.c_int, [_s, _u32, _u64, _s, _u64]),
+    "trims_resident_manifest": (_c.c_int, [_s, _u32, _u32, _s, _u64]),
+    "trims_fill_splitmix_host": (_c.c_int, [_p, _u64, _u64, _u64]),
+    "trims_fill_uniform_host": (_c.c_int, [_p, _u64, _u64, _u64, _c.c_float, _c.c_float]),
+    "trims_fnv1a": (_u64, [_s]),
+    "trims_touch_host": (_c.c_int, [_p, _s, _c.POINTER(_u64)]),
+    "trims_checksum_host": (_c.c_int, [_p, _u64, _u64, _c.POINTER(_u64)]),
+    "trims_store_create": (_c.c_int, [_c.POINTER(StoreConfig), _c.POINTER(_p)]),
+    "trims_store_destroy": (None, [_p]),
+    "trims_store_open": (_c.c_int, [_p, _s, _s, _s, _u32, _u64, _c.POINTER(Export)]),
+    "trims_store_close": (_c.c_int, [_p, _s, _s, _s, _c.POINTER(_u64)]),
+    "trims_store_reclaim": (_c.c_int, [_p, _u32, _u64, _u32, _s, _u64]),
+    "trims_store_register_disk_file": (_c.c_int, [_p, _s, _s, _s, _s, _u64]),
+    "trims_store_drop_all": (_c.c_int, [_p]),
+    "trims_store_stats_json": (_c.c_int, [_p, _s, _u64]),
+    "trims_store_resident_json": (_c.c_int, [_p, _u64, _s, _u64]),
+    "trims_store_ingest_stats": (_c.c_int, [_p, _u64, _c.POINTER(_c.c_double)]),
+    "trims_store_checksums": (_c.c_int, [_p, _u64, _c.POINTER(_u64), _u64, _c.POINTER(_u64)]),
+    "trims_import_open": (_c.c_int, [_c.c_int, _c.c_int, _u64, _u64, _u64, _p, _c.POINTER(_p), _c.POINTER(_p)]),
+    "trims_import_manifest": (_c.c_int, [_p, _s, _u64]),
+    "trims_import_read_only": (_c.c_int, [_p]),
+    "trims_import_close": (None, [_p]),
+    "trims_import_verify": (_c.c_int, [_p, _c.POINTER(_u64)]),
+    "trims_ingest_host": (_c.c_int, [_c.c_int, _p, _s, _u32, _u32, _p, _c.POINTER(_u64), _c.POINTER(_c.c_double)]),
+    "trims_transform_device": (_c.c_int, [_c.c_int, _p, _s, _u32, _u32, _p, _p, _p]),
+    "trims_plan_info": (_c.c_int, [_s, _u32, _u32, _c.POINTER(_u64)]),
+    "trims_checksum_device": (_c.c_int, [_p, _u64, _u64, _p, _p]),
+    "trims_fill_splitmix_device": (_c.c_int, [_p, _u64, _u64, _u64, _p]),
+    "trims_fill_uniform_device": (_c.c_int, [_p, _u64, _u64, _u64, _c.c_float, _c.c_float, _p]),
+    "trims_replay": (_c.c_int, [_s, _s, _u64]),
+}
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is not built; run `make -C {os.path.join(HERE, 'csrc')}` "
+            "or `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise TrimsError(rc, lib.trims_errc_name(rc).decode(), lib.trims_last_error().decode())
+
+
+def text_call(fn, *args, cap: int = 1 << 20) -> str:
+    """Call an entry point whose last two args are (char* out, uint64 cap)."""
+    while True:
+        buf = ctypes.create_string_buffer(cap)
+        rc = fn(*args, buf, cap)
+        if rc == Errc.InvalidArgument and b"too small" in lib.trims_last_error() and cap < (1 << 30):
+            cap *= 8
+            continue
+        check(rc)
+        return buf.value.decode()
+
+
+def exported_symbols() -> list[str]:
+    return sorted(_SIGS)

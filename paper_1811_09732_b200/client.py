@@ -1,0 +1,301 @@
+"""Client SDK: open / close / touch / forward on shared (or private) weights.
+
+Mirrors proj/include/mrm/client.hpp:97-119 and proj/src/client.cpp:
+``open`` makes the rho = b/q - n(o+s) decision (client.cpp:16-18, 148-222),
+attaches the store's exported HBM segment read-only and slices it into
+device ``TensorView``s (client.cpp:243-315); it falls back to a private load
+(client.cpp:224-241) exactly where the reference does. ``touch`` is the
+reference's FNV-1a compute stand-in (client.cpp:338-359), kept as a parity
+check; the B200 compute on the shared weights is ``models.forward``.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import format as F
+from ._lib import Errc, TrimsError, check, lib
+
+SHARED, PRIVATE = "shared", "private"
+
+
+@dataclass
+class CostModelParams:
+    q: float = 200e6    # disk bytes/s      (client.cpp:70 kDefaultParams)
+    o: float = 2.5e-4   # export s/object
+    s: float = 2.5e-4   # attach s/object
+
+
+def share_benefit(nbytes: float, n_objects: float, p: CostModelParams) -> float:
+    """client.cpp:16-18."""
+    return nbytes / p.q - n_objects * (p.o + p.s)
+
+
+@dataclass
+class TensorView:
+    name: str
+    dims: list
+    dtype: str
+    layout: str
+    offset: int
+    nbytes: int
+    dev_ptr: int
+
+    def torch(self, device=None):
+        """Zero-copy torch view of the (read-only) device bytes."""
+        import torch
+        typestr = {"f64": "<f8", "f32": "<f4", "f16": "<f2", "i8": "|i1", "bf16": "<i2"}[self.dtype]
+
+        class _CAI:
+            pass
+
+        obj = _CAI()
+        obj.__cuda_array_interface__ = {"shape": tuple(int(d) for d in self.dims), "typestr": typestr,
+                                        "data": (int(self.dev_ptr), False), "version": 2, "strides": None}
+        t = torch.as_tensor(obj, device=device or f"cuda:{torch.cuda.current_device()}")
+        return t.view(torch.bfloat16) if self.dtype == "bf16" else t
+
+
+@dataclass
+class OpenTimings:  # client.hpp:53-57
+    rpc_s: float = 0.0
+    attach_s: float = 0.0
+    private_load_s: float = 0.0
+
+
+@dataclass
+class ModelView:
+    key: F.ModelKey
+    origin: str
+    fallback_reason: str
+    manifest_json: str              # resident manifest
+    base_ptr: int
+    tensors: list = field(default_factory=list)
+    model_id: int = 0
+    generation: int = 0
+    outcome: str = ""
+    export: object = None
+    timings: OpenTimings = field(default_factory=OpenTimings)
+    is_open: bool = True
+    _import: object = None          # trims_import* for imported mappings
+    _private: object = None         # owning torch buffer of a private view
+    _release: object = None
+
+    @property
+    def manifest(self) -> dict:
+        return json.loads(self.manifest_json)
+
+    def tensor(self, name: str) -> TensorView:
+        for t in self.tensors:
+            if t.name == name:
+                return t
+        raise KeyError(name)
+
+    def blob_bytes(self) -> int:
+        m = self.manifest
+        end = max((t["offset"] + t["nbytes"] for t in m["tensors"]), default=0)
+        return (end + 63) // 64 * 64
+
+
+def slice_tensors(manifest_json: str, base_ptr: int) -> list[TensorView]:
+    """client.cpp:60-65 with device pointers."""
+    out = []
+    for t in json.loads(manifest_json)["tensors"]:
+        out.append(TensorView(t["name"], t["dims"], t["dtype"], t.get("layout", "native"), t["offset"],
+                              t["nbytes"], base_ptr + t["offset"]))
+    return out
+
+
+class ImportCache:
+    """Per-process attach cache keyed by (token, generation): re-opening a hot
+    model skips the map + digest check (the reference caches manifests by
+    digest, client.cpp:293-307; we also keep the mapping)."""
+
+    def __init__(self):
+        self._maps = {}
+
+    def get(self, token: str, generation: int):
+        return self._maps.get((token, generation))
+
+    def put(self, token: str, generation: int, entry):
+        self._maps[(token, generation)] = entry
+
+    def clear(self):
+        for imp, _, _ in self._maps.values():
+            lib.trims_import_close(imp)
+        self._maps.clear()
+
+
+def import_segment(device: int, fd: int, alloc_bytes: int, generation: int, payload_bytes: int,
+                   digest: bytes):
+    """Attachment::attach (shared_segment.cpp:212-245) + digest check (client.cpp:284-291)."""
+    imp = ctypes.c_void_p()
+    ptr = ctypes.c_void_p()
+    dig = (ctypes.c_uint8 * 32).from_buffer_copy(bytes(digest))
+    check(lib.trims_import_open(device, fd, alloc_bytes, generation, payload_bytes, dig, ctypes.byref(imp),
+                                ctypes.byref(ptr)))
+    buf = ctypes.create_string_buffer(1 << 22)
+    check(lib.trims_import_manifest(imp, buf, len(buf)))
+    return imp, int(ptr.value), buf.value.decode()
+
+
+class Client:
+    """In-process client of a ``Store`` (or of a ``ipc.RemoteStore`` endpoint)."""
+
+    def __init__(self, store=None, model_dirs=(), granularity: int = F.MODEL, params: CostModelParams | None = None,
+                 disabled: bool | None = None, attach_via_import: bool = False, device: int = 0,
+                 plan_flags: int | None = None, out_dtype: str | None = None):
+        self.store = store
+        self.model_dirs = list(model_dirs)
+        env_dirs = os.environ.get("MRM_MODEL_DIR")  # client.cpp:81-91
+        if env_dirs:
+            self.model_dirs += [d for d in env_dirs.split(":") if d]
+        self.granularity = granularity
+        self.params = params
+        self.disabled = disabled if disabled is not None else os.environ.get("MRM_DISABLE") == "1"
+        self.attach_via_import = attach_via_import
+        self.device = device
+        opts = getattr(store, "opts", None)
+        self.plan_flags = plan_flags if plan_flags is not None else (opts.plan_flags if opts else 0)
+        self.out_dtype = out_dtype or (opts.convert_to if opts and opts.convert_to else "bf16")
+        self.imports = ImportCache()
+
+    # client.cpp:94-106
+    def resolve_local(self, key: F.ModelKey, local_path: str | None = None) -> str | None:
+        if local_path:
+            return local_path if os.path.exists(local_path) else None
+        for d in self.model_dirs:
+            p = os.path.join(d, key.filename)
+            if os.path.exists(p):
+                return p
+        return None
+
+    def open(self, key: F.ModelKey, force_private: bool = False, force_shared: bool = False,
+             granularity: int | None = None, params: CostModelParams | None = None,
+             local_path: str | None = None) -> ModelView:
+        """client.cpp:148-222."""
+        local = self.resolve_local(key, local_path)
+
+        def private(reason):
+            if not local:
+                raise TrimsError(Errc.NotFound, "NotFound", f"{key} (no daemon, no local artifact)")
+            return self.open_private(key, local, reason)
+
+        if force_private:
+            return private("forced")
+        if self.disabled:
+            return private("disabled")
+        if self.store is None:
+            return private("daemon_unreachable")
+        g = self.granularity if granularity is None else granularity
+        if local and not force_shared:
+            info = F.read_manifest(local)
+            b = os.path.getsize(local)
+            p = params or self.params or CostModelParams()
+            n = len(F.layout_for(info.manifest_json, g))
+            if share_benefit(b, n, p) <= 0:
+                if g == F.LAYER and share_benefit(b, 1, p) > 0:
+                    g = F.MODEL
+                else:
+                    return private("benefit_non_positive")
+        try:
+            return self.open_shared(key, g)
+        except TrimsError as e:
+            if local and e.code in (Errc.NotFound, Errc.RemoteNotFound, Errc.NoEvictableSpace,
+                                    Errc.TooLargeForFast, Errc.Internal, Errc.DaemonUnreachable,
+                                    Errc.ConnectionLost):
+                return self.open_private(key, local, "daemon_error")
+            raise
+
+    def open_shared(self, key: F.ModelKey, granularity: int = F.MODEL) -> ModelView:
+        """client.cpp:243-315: RPC, attach, digest, slice."""
+        t0 = time.perf_counter()
+        ex = self.store.open(key, granularity)
+        t1 = time.perf_counter()
+        token = ex.token.decode() if isinstance(ex.token, bytes) else ex.token
+        remote = getattr(ex, "remote", False)
+        if remote or self.attach_via_import:
+            hit = self.imports.get(token, ex.generation)
+            if hit is None:
+                fd = ex.fd if remote else os.dup(ex.fd)
+                try:
+                    imp, ptr, mjson = import_segment(ex.device, fd, ex.alloc_bytes, ex.generation, ex.payload_bytes,
+                                                     bytes(ex.manifest_digest))
+                finally:
+                    os.close(fd)
+                hit = (imp, ptr, mjson)
+                self.imports.put(token, ex.generation, hit)
+            elif remote and ex.fd >= 0:
+                os.close(ex.fd)
+            _, base, mjson = hit
+        else:
+            base = int(ex.dev_ptr)
+            mjson = self.store.resident_manifest(ex.model_id)
+            if F.sha256(mjson.encode()) != bytes(ex.manifest_digest):
+                raise TrimsError(Errc.Corrupt, "Corrupt", "manifest digest mismatch on attach")
+        view = ModelView(key, SHARED, "none", mjson, base, slice_tensors(mjson, base), ex.model_id, ex.generation,
+                         outcome=_outcome(ex.outcome), export=ex)
+        view.timings.rpc_s = t1 - t0
+        view.timings.attach_s = time.perf_counter() - t1
+        return view
+
+    def open_private(self, key: F.ModelKey, path: str, reason: str) -> ModelView:
+        """client.cpp:224-241: read the artifact and ingest it into private HBM
+        with the same plan, so shared and private views are byte-identical."""
+        import torch
+        t0 = time.perf_counter()
+        info = F.read_manifest(path)
+        if json.loads(info.manifest_json)["name"] != key.name:
+            raise TrimsError(Errc.Corrupt, "Corrupt", f"artifact at {path} holds another model")
+        host = torch.empty(max(info.blob_bytes, 1), dtype=torch.uint8, pin_memory=True)
+        with open(path, "rb") as f:
+            f.seek(info.blob_offset)
+            f.readinto(memoryview(host.numpy())[: info.blob_bytes])
+        rj = F.resident_manifest(info.manifest_json, self.plan_flags, self.out_dtype)
+        rb = json.loads(rj)
+        rbytes = max((t["offset"] + t["nbytes"] for t in rb["tensors"]), default=0)
+        rbytes = max((rbytes + 63) // 64 * 64, 1)
+        dev = torch.empty(rbytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+        cs = ctypes.c_uint64()
+        check(lib.trims_ingest_host(self.device, host.data_ptr(), info.manifest_json.encode(), self.plan_flags,
+                                    F.DTYPE_CODE[self.out_dtype], dev.data_ptr(), ctypes.byref(cs), None))
+        view = ModelView(key, PRIVATE, reason, rj, dev.data_ptr(), slice_tensors(rj, dev.data_ptr()))
+        view._private = dev
+        view.timings.private_load_s = time.perf_counter() - t0
+        return view
+
+    def close(self, view: ModelView) -> None:
+        """client.cpp:317-336: idempotent."""
+        if not view.is_open:
+            return
+        view.is_open = False
+        if view.origin == SHARED:
+            try:
+                self.store.close(view.key)
+            except TrimsError:
+                pass
+        view._private = None
+        view.tensors = []
+
+    def touch(self, view: ModelView) -> int:
+        """client.cpp:338-359 over a device->host copy of the view."""
+        import torch
+        n = view.blob_bytes()
+        host = torch.empty(max(n, 1), dtype=torch.uint8)
+        if n:
+            src = TensorView("blob", [n], "i8", "native", 0, n, view.base_ptr).torch(f"cuda:{self.device}")
+            host[:n].copy_(src.view(torch.uint8))
+        return F.touch_host(host.numpy()[:n], view.manifest_json)
+
+    def close_all_imports(self):
+        self.imports.clear()
+
+
+def _outcome(code: int) -> str:
+    from .store import outcome_name
+    return outcome_name(code)

@@ -1,0 +1,434 @@
+// backend.cu — Ingestor (pinned host / file -> HBM, copy-engine chunks
+// overlapped with the fused transform kernel) and CudaTierBackend.
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <filesystem>
+#include <thread>
+
+#include "backend.hpp"
+#include "cuda_util.hpp"
+#include "sha256.hpp"
+
+namespace trims {
+
+namespace fs = std::filesystem;
+
+void parallel_pread(int fd, uint8_t* dst, uint64_t len, uint64_t off, unsigned threads) {
+  auto worker = [&](uint64_t b, uint64_t e, bool* ok) {
+    while (b < e) {
+      ssize_t r = ::pread(fd, dst + b, size_t(std::min<uint64_t>(e - b, 64ull << 20)), off_t(off + b));
+      if (r <= 0) {
+        *ok = false;
+        return;
+      }
+      b += uint64_t(r);
+    }
+    *ok = true;
+  };
+  const uint64_t min_piece = 8ull << 20;
+  unsigned n = unsigned(std::clamp<uint64_t>(len / min_piece, 1, std::max(1u, threads)));
+  std::vector<std::thread> ts;
+  std::vector<char> oks(n, 0);
+  uint64_t piece = (len + n - 1) / n;
+  piece = (piece + 4095) / 4096 * 4096;
+  for (unsigned i = 1; i < n; ++i) {
+    uint64_t b = std::min<uint64_t>(len, i * piece), e = std::min<uint64_t>(len, (i + 1) * piece);
+    ts.emplace_back(worker, b, e, reinterpret_cast<bool*>(&oks[i]));
+  }
+  worker(0, std::min(len, piece), reinterpret_cast<bool*>(&oks[0]));
+  for (auto& t : ts) t.join();
+  for (char ok : oks)
+    if (!ok) raise(Errc::Corrupt, "blob truncated (short read)");
+}
+
+// ---------------------------------------------------------------------------
+// Ingestor
+
+Ingestor::Ingestor(int device) : device_(device) {
+  DeviceGuard g(device);
+  TRIMS_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device));
+  TRIMS_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+  TRIMS_CUDA(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking));
+  events_.resize(512);
+  for (auto& e : events_) TRIMS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto* e : {&t0_, &t1_, &c0_, &c1_}) TRIMS_CUDA(cudaEventCreate(e));
+  for (auto& e : bounce_ev_) TRIMS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
+Ingestor::~Ingestor() {
+  DeviceGuard g(device_);
+  for (auto& [k, p] : plans_) cudaFree(p->d_tiles);
+  for (auto e : events_) cudaEventDestroy(e);
+  for (auto e : {t0_, t1_, c0_, c1_}) cudaEventDestroy(e);
+  for (auto e : bounce_ev_) cudaEventDestroy(e);
+  if (staging_) cudaFree(staging_);
+  if (d_sums_) cudaFree(d_sums_);
+  if (h_sums_) cudaFreeHost(h_sums_);
+  for (auto* b : bounce_)
+    if (b) cudaFreeHost(b);
+  cudaStreamDestroy(copy_);
+  cudaStreamDestroy(compute_);
+}
+
+uint8_t* Ingestor::staging(uint64_t bytes) {
+  if (bytes > staging_cap_) {
+    if (staging_) TRIMS_CUDA(cudaFree(staging_));
+    staging_ = nullptr;
+    staging_cap_ = 0;
+    uint64_t cap = std::max<uint64_t>(bytes, 64ull << 20);
+    TRIMS_CUDA(cudaMalloc(&staging_, cap));
+    staging_cap_ = cap;
+  }
+  return staging_;
+}
+
+unsigned long long* Ingestor::sums(uint32_t n) {
+  if (n > sums_cap_) {
+    if (d_sums_) TRIMS_CUDA(cudaFree(d_sums_));
+    if (h_sums_) TRIMS_CUDA(cudaFreeHost(h_sums_));
+    uint32_t cap = std::max<uint32_t>(n, 1024);
+    TRIMS_CUDA(cudaMalloc(&d_sums_, cap * sizeof(unsigned long long)));
+    TRIMS_CUDA(cudaHostAlloc(&h_sums_, cap * sizeof(unsigned long long), cudaHostAllocDefault));
+    sums_cap_ = cap;
+  }
+  return d_sums_;
+}
+
+const ingest::TilePlan& Ingestor::plan_for(const fmt::Manifest& src, const fmt::Manifest& dst, bool identity,
+                                           const ingest::Tile** d_tiles) {
+  std::string key = (identity ? "I" : "T") + fmt::manifest_to_json(src) + "|" + fmt::manifest_to_json(dst);
+  auto it = plans_.find(key);
+  if (it == plans_.end()) {
+    auto cp = std::make_unique<CachedPlan>();
+    uint64_t chunk = std::max<uint64_t>(16ull << 20, src.blob_bytes / (events_.size() - 8) + 1);
+    cp->plan = ingest::build_tiles(src, dst, identity, chunk);
+    if (!cp->plan.tiles.empty()) {
+      size_t bytes = cp->plan.tiles.size() * sizeof(ingest::Tile);
+      TRIMS_CUDA(cudaMalloc(&cp->d_tiles, bytes));
+      TRIMS_CUDA(cudaMemcpy(cp->d_tiles, cp->plan.tiles.data(), bytes, cudaMemcpyHostToDevice));
+    }
+    if (plans_.size() > 64) {
+      for (auto& [k, p] : plans_) cudaFree(p->d_tiles);
+      plans_.clear();
+    }
+    it = plans_.emplace(std::move(key), std::move(cp)).first;
+  }
+  if (d_tiles) *d_tiles = it->second->d_tiles;
+  return it->second->plan;
+}
+
+uint64_t Ingestor::finish(const ingest::TilePlan& p, std::vector<uint64_t>* buckets) {
+  TRIMS_CUDA(cudaMemcpyAsync(h_sums_, d_sums_, p.buckets * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             compute_));
+  TRIMS_CUDA(cudaStreamSynchronize(compute_));
+  uint64_t total = 0;
+  if (buckets) buckets->assign(h_sums_, h_sums_ + p.buckets);
+  for (uint32_t i = 0; i < p.buckets; ++i) total += h_sums_[i];
+  return total;
+}
+
+uint64_t Ingestor::from_host(const uint8_t* host_blob, const fmt::Manifest& src, const fmt::Manifest& dst,
+                             bool identity, uint8_t* d_dst, std::vector<uint64_t>* buckets, IngestStats* st) {
+  std::lock_guard lk(mu_);
+  DeviceGuard g(device_);
+  const ingest::Tile* d_tiles = nullptr;
+  const ingest::TilePlan& p = plan_for(src, dst, identity, &d_tiles);
+  unsigned long long* ds = sums(p.buckets);
+  TRIMS_CUDA(cudaMemsetAsync(ds, 0, p.buckets * sizeof(unsigned long long), compute_));
+  uint8_t* raw = identity ? d_dst : staging(src.blob_bytes);
+  TRIMS_CUDA(cudaEventRecord(t0_, copy_));
+  TRIMS_CUDA(cudaStreamWaitEvent(copy_, t0_, 0));
+  uint32_t launches = 0;
+  for (size_t c = 0; c < p.chunks.size(); ++c) {
+    const auto& ch = p.chunks[c];
+    cudaEvent_t ev = events_[c % events_.size()];
+    TRIMS_CUDA(cudaMemcpyAsync(raw + ch.src_begin, host_blob + ch.src_begin, ch.src_end - ch.src_begin,
+                               cudaMemcpyHostToDevice, copy_));
+    TRIMS_CUDA(cudaEventRecord(ev, copy_));
+    TRIMS_CUDA(cudaStreamWaitEvent(compute_, ev, 0));
+    ingest::launch_transform(d_tiles + ch.tile_begin, ch.tile_end - ch.tile_begin, p.has_perm, raw, d_dst, ds,
+                             compute_, sms_);
+    ++launches;
+  }
+  TRIMS_CUDA(cudaEventRecord(t1_, copy_));
+  TRIMS_CUDA(cudaEventRecord(c1_, compute_));
+  uint64_t total = finish(p, buckets);
+  if (st) {
+    float ms = 0;
+    TRIMS_CUDA(cudaEventElapsedTime(&ms, t0_, t1_));
+    st->h2d_ms = ms;
+    TRIMS_CUDA(cudaEventElapsedTime(&ms, t0_, c1_));
+    st->total_ms = ms;
+    st->h2d_bytes = p.chunks.empty() ? 0 : p.chunks.back().src_end - p.chunks.front().src_begin;
+    st->launches = launches;
+  }
+  return total;
+}
+
+uint64_t Ingestor::from_file(int fd, uint64_t blob_file_off, const fmt::Manifest& src, const fmt::Manifest& dst,
+                             bool identity, uint8_t* d_dst, std::vector<uint64_t>* buckets, IngestStats* st) {
+  std::lock_guard lk(mu_);
+  DeviceGuard g(device_);
+  const ingest::Tile* d_tiles = nullptr;
+  const ingest::TilePlan& p = plan_for(src, dst, identity, &d_tiles);
+  uint64_t need = 0;
+  for (const auto& ch : p.chunks) need = std::max(need, ch.src_end - ch.src_begin);
+  if (need > bounce_cap_) {
+    for (auto*& b : bounce_) {
+      if (b) TRIMS_CUDA(cudaFreeHost(b));
+      b = nullptr;
+    }
+    bounce_cap_ = 0;
+    for (auto*& b : bounce_) TRIMS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&b), need, cudaHostAllocDefault));
+    bounce_cap_ = need;
+  }
+  unsigned long long* ds = sums(p.buckets);
+  TRIMS_CUDA(cudaMemsetAsync(ds, 0, p.buckets * sizeof(unsigned long long), compute_));
+  uint8_t* raw = identity ? d_dst : staging(src.blob_bytes);
+  TRIMS_CUDA(cudaEventRecord(t0_, copy_));
+  double read_ms = 0;
+  uint32_t launches = 0;
+  for (size_t c = 0; c < p.chunks.size(); ++c) {
+    const auto& ch = p.chunks[c];
+    const int slot = int(c & 1);
+    TRIMS_CUDA(cudaEventSynchronize(bounce_ev_[slot]));  // previous H2D out of this slot done
+    auto r0 = std::chrono::steady_clock::now();
+    parallel_pread(fd, bounce_[slot], ch.src_end - ch.src_begin, blob_file_off + ch.src_begin, 8);
+    read_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - r0).count();
+    cudaEvent_t ev = events_[c % events_.size()];
+    TRIMS_CUDA(cudaMemcpyAsync(raw + ch.src_begin, bounce_[slot], ch.src_end - ch.src_begin,
+                               cudaMemcpyHostToDevice, copy_));
+    TRIMS_CUDA(cudaEventRecord(ev, copy_));
+    TRIMS_CUDA(cudaEventRecord(bounce_ev_[slot], copy_));
+    TRIMS_CUDA(cudaStreamWaitEvent(compute_, ev, 0));
+    ingest::launch_transform(d_tiles + ch.tile_begin, ch.tile_end - ch.tile_begin, p.has_perm, raw, d_dst, ds,
+                             compute_, sms_);
+    ++launches;
+  }
+  TRIMS_CUDA(cudaEventRecord(t1_, copy_));
+  TRIMS_CUDA(cudaEventRecord(c1_, compute_));
+  uint64_t total = finish(p, buckets);
+  if (st) {
+    float ms = 0;
+    TRIMS_CUDA(cudaEventElapsedTime(&ms, t0_, t1_));
+    st->h2d_ms = ms;
+    TRIMS_CUDA(cudaEventElapsedTime(&ms, t0_, c1_));
+    st->total_ms = ms;
+    st->read_ms = read_ms;
+    st->h2d_bytes = p.chunks.empty() ? 0 : p.chunks.back().src_end - p.chunks.front().src_begin;
+    st->launches = launches;
+  }
+  return total;
+}
+
+void Ingestor::from_device(const uint8_t* d_src, const fmt::Manifest& src, const fmt::Manifest& dst,
+                           bool identity, uint8_t* d_dst, unsigned long long* d_sums, cudaStream_t stream) {
+  std::lock_guard lk(mu_);
+  DeviceGuard g(device_);
+  const ingest::Tile* d_tiles = nullptr;
+  const ingest::TilePlan& p = plan_for(src, dst, identity, &d_tiles);
+  ingest::launch_transform(d_tiles, uint32_t(p.tiles.size()), p.has_perm, d_src, d_dst, d_sums, stream, sms_);
+}
+
+// ---------------------------------------------------------------------------
+// CudaTierBackend
+
+CudaTierBackend::CudaTierBackend(BackendConfig cfg) : cfg_(std::move(cfg)), ing_(cfg_.device) {
+  DeviceGuard g(cfg_.device);
+  if (cfg_.pinned_pool_bytes) pool_ = std::make_unique<PinnedPool>(cfg_.pinned_pool_bytes);
+}
+
+CudaTierBackend::~CudaTierBackend() {
+  std::lock_guard lk(mu_);
+  fast_.clear();
+  for (auto& [id, h] : host_) free_host(h);
+  host_.clear();
+}
+
+// daemon.cpp:128-136
+Located CudaTierBackend::locate(const fmt::ModelKey& key) {
+  fs::path p = fs::path(cfg_.disk_cache_dir) / fmt::canonical_filename(key);
+  std::error_code ec;
+  if (fs::exists(p, ec)) return {Located::Kind::DiskCache, p.string(), uint64_t(fs::file_size(p, ec))};
+  return {Located::Kind::Absent, "", 0};
+}
+
+FetchResult CudaTierBackend::fetch_remote(const fmt::ModelKey& key) {
+  // The remote tier is outside the B200 hot path.
+  raise(Errc::RemoteNotFound, fmt::to_string(key));
+}
+
+// daemon.cpp:144-151
+fmt::Manifest CudaTierBackend::read_manifest(const fmt::ModelKey& key, const std::string& path) {
+  fmt::ArtifactInfo a = fmt::read_artifact_info(path, cfg_.full_verify);
+  if (a.manifest.key != key)
+    raise(Errc::Corrupt, "artifact at " + path + " holds " + fmt::to_string(a.manifest.key) + ", expected " +
+                             fmt::to_string(key));
+  return a.manifest;
+}
+
+void CudaTierBackend::free_host(HostBuf& h) {
+  if (!h.p) return;
+  if (h.pooled) pool_->free(h.p);
+  else cudaFreeHost(h.p);
+  h.p = nullptr;
+}
+
+// daemon.cpp:153-158: disk -> host tier, here straight into pinned memory.
+void CudaTierBackend::stage_host(uint64_t model_id, const fmt::Manifest& m, const std::string& path) {
+  int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
+  if (fd < 0) raise(Errc::NotFound, path);
+  HostBuf hb;
+  try {
+    uint8_t hdr[16];
+    if (::pread(fd, hdr, 16, 0) != 16) raise(Errc::Corrupt, "short read on " + path);
+    uint64_t mlen = 0;
+    for (int i = 0; i < 8; ++i) mlen |= uint64_t(hdr[8 + i]) << (8 * i);
+    const uint64_t off = fmt::blob_file_offset(mlen);
+    hb.bytes = m.blob_bytes;
+    if (pool_) hb.p = pool_->alloc(std::max<uint64_t>(hb.bytes, 1));
+    hb.pooled = hb.p != nullptr;
+    if (!hb.p) {
+      DeviceGuard g(cfg_.device);
+      TRIMS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hb.p), std::max<uint64_t>(hb.bytes, 1), cudaHostAllocPortable));
+    }
+    struct stat st {};
+    ::fstat(fd, &st);
+    if (uint64_t(st.st_size) < off + hb.bytes) raise(Errc::Corrupt, "blob truncated in " + path);
+    parallel_pread(fd, hb.p, hb.bytes, off, cfg_.read_threads);
+    if (cfg_.full_verify && Sha256::of(hb.p, hb.bytes) != m.checksum) raise(Errc::ChecksumMismatch, path);
+  } catch (...) {
+    ::close(fd);
+    free_host(hb);
+    throw;
+  }
+  ::close(fd);
+  std::lock_guard lk(mu_);
+  auto it = host_.find(model_id);
+  if (it != host_.end()) free_host(it->second);
+  host_[model_id] = hb;
+}
+
+const uint8_t* CudaTierBackend::host_buffer(uint64_t model_id, uint64_t* bytes) {
+  std::lock_guard lk(mu_);
+  auto it = host_.find(model_id);
+  if (it == host_.end()) return nullptr;
+  if (bytes) *bytes = it->second.bytes;
+  return it->second.p;
+}
+
+// daemon.cpp:160-209: build, fill and seal the fast-tier segment, then
+// export it. Payload = resident blob | manifest JSON | u64 LE jlen, then the
+// 64-byte SegTail.
+FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Manifest& m, bool from_host,
+                                              const std::string& path) {
+  auto rec = std::make_shared<FastRecord>();
+  rec->resident = fmt::resident_manifest(m, cfg_.plan);
+  rec->json = fmt::manifest_to_json(rec->resident);
+  const bool identity = cfg_.plan.identity();
+  const uint64_t rb = rec->resident.blob_bytes;
+  const uint64_t payload = rb + rec->json.size() + 8;
+  rec->seg = DeviceSegment::create(cfg_.device, payload + sizeof(SegTail));
+  rec->generation = next_gen_.fetch_add(1);
+
+  if (from_host) {
+    const uint8_t* src = nullptr;
+    {
+      std::lock_guard lk(mu_);
+      auto it = host_.find(model_id);
+      if (it == host_.end()) raise(Errc::Internal, "host buffer missing for publish");
+      if (it->second.bytes != m.blob_bytes) raise(Errc::Internal, "host buffer size mismatch");
+      src = it->second.p;  // single-flight pins the entry while loading
+    }
+    rec->checksum = ing_.from_host(src, m, rec->resident, identity, rec->seg.ptr(), &rec->bucket_sums, &rec->stats);
+  } else {
+    int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
+    if (fd < 0) raise(Errc::NotFound, path);
+    try {
+      uint8_t hdr[16];
+      if (::pread(fd, hdr, 16, 0) != 16) raise(Errc::Corrupt, "short read on " + path);
+      uint64_t mlen = 0;
+      for (int i = 0; i < 8; ++i) mlen |= uint64_t(hdr[8 + i]) << (8 * i);
+      rec->checksum = ing_.from_file(fd, fmt::blob_file_offset(mlen), m, rec->resident, identity, rec->seg.ptr(),
+                                     &rec->bucket_sums, &rec->stats);
+    } catch (...) {
+      ::close(fd);
+      throw;
+    }
+    ::close(fd);
+  }
+
+  // Tail: JSON, its length, the sealed SegTail.
+  std::vector<uint8_t> tail(rec->json.size() + 8 + sizeof(SegTail));
+  std::memcpy(tail.data(), rec->json.data(), rec->json.size());
+  uint64_t jlen = rec->json.size();
+  for (int i = 0; i < 8; ++i) tail[rec->json.size() + i] = uint8_t(jlen >> (8 * i));
+  SegTail t{};
+  t.magic = kSegMagic;
+  t.generation = rec->generation;
+  t.length = payload;
+  t.sealed = 1;
+  t.device = uint32_t(cfg_.device);
+  t.blob_bytes = rb;
+  t.checksum = rec->checksum;
+  std::memcpy(tail.data() + rec->json.size() + 8, &t, sizeof t);
+  {
+    DeviceGuard g(cfg_.device);
+    TRIMS_CUDA(cudaMemcpy(rec->seg.ptr() + rb, tail.data(), tail.size(), cudaMemcpyHostToDevice));
+  }
+
+  FastPublication pub;
+  ExportedSegment es;
+  es.token = "trims." + std::to_string(::getpid()) + "." + std::to_string(rec->generation) + "." + m.key.name;
+  es.generation = rec->generation;
+  es.length = payload;
+  es.device = cfg_.device;
+  es.dev_ptr = rec->seg.ptr();
+  es.fd = rec->seg.fd();
+  es.alloc_bytes = rec->seg.size();
+  es.resident_blob_bytes = rb;
+  es.ingest_checksum = rec->checksum;
+  pub.segments.push_back(es);
+  pub.manifest_digest = Sha256::of(rec->json.data(), rec->json.size());
+  std::lock_guard lk(mu_);
+  fast_[model_id] = std::move(rec);
+  return pub;
+}
+
+void CudaTierBackend::evict_fast(uint64_t model_id) {
+  std::shared_ptr<FastRecord> victim;
+  {
+    std::lock_guard lk(mu_);
+    auto it = fast_.find(model_id);
+    if (it == fast_.end()) return;
+    victim = std::move(it->second);
+    fast_.erase(it);
+  }
+  // Importers' mappings keep the physical memory alive (views survive).
+}
+
+void CudaTierBackend::evict_host(uint64_t model_id) {
+  std::lock_guard lk(mu_);
+  auto it = host_.find(model_id);
+  if (it == host_.end()) return;
+  free_host(it->second);
+  host_.erase(it);
+}
+
+void CudaTierBackend::evict_disk(const fmt::ModelKey&, const std::string& path) {
+  std::error_code ec;
+  fs::remove(path, ec);
+}
+
+std::shared_ptr<FastRecord> CudaTierBackend::fast_record(uint64_t model_id) {
+  std::lock_guard lk(mu_);
+  auto it = fast_.find(model_id);
+  return it == fast_.end() ? nullptr : it->second;
+}
+
+}  // namespace trims

@@ -1,0 +1,139 @@
+// backend.hpp — CudaTierBackend: the B200 implementation of the reference's
+// TierBackend plugin (proj/include/mrm/cache_core.hpp:76-98, implemented there
+// by ShmTierBackend, proj/src/daemon.cpp:120-224), and the Ingestor that
+// runs the disk -> pinned host -> HBM pipeline behind publish_fast.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "cache_core.hpp"
+#include "device_mem.hpp"
+#include "format.hpp"
+#include "ingest.hpp"
+
+namespace trims {
+
+struct IngestStats {
+  double h2d_ms{0};        // copy-engine time of the blob (first chunk start -> last chunk end)
+  double total_ms{0};      // ingest call wall time on the device (first copy -> last tile)
+  double read_ms{0};       // host file reads (from_file only)
+  uint64_t h2d_bytes{0};
+  uint32_t launches{0};    // transform kernel launches
+};
+
+// One per device. Serialises its own ingests (PCIe is the shared resource).
+class Ingestor {
+ public:
+  explicit Ingestor(int device);
+  ~Ingestor();
+  int device() const { return device_; }
+  int sm_count() const { return sms_; }
+
+  // Raw artifact blob in host memory (pinned for full PCIe rate) -> resident
+  // blob at d_dst. Returns the resident checksum; per-bucket sums optional.
+  uint64_t from_host(const uint8_t* host_blob, const fmt::Manifest& src, const fmt::Manifest& dst,
+                     bool identity, uint8_t* d_dst, std::vector<uint64_t>* buckets, IngestStats* st);
+  // Streams the blob from an artifact file through a pinned bounce ring
+  // (publish_fast without host staging, daemon.cpp:184-193).
+  uint64_t from_file(int fd, uint64_t blob_file_off, const fmt::Manifest& src, const fmt::Manifest& dst,
+                     bool identity, uint8_t* d_dst, std::vector<uint64_t>* buckets, IngestStats* st);
+  // Raw blob already in HBM -> resident blob (the HBM-resident transform).
+  // Asynchronous on `stream` when sums_out == nullptr (d_sums receives the bucket sums).
+  void from_device(const uint8_t* d_src, const fmt::Manifest& src, const fmt::Manifest& dst, bool identity,
+                   uint8_t* d_dst, unsigned long long* d_sums, cudaStream_t stream);
+  const ingest::TilePlan& plan_for(const fmt::Manifest& src, const fmt::Manifest& dst, bool identity,
+                                   const ingest::Tile** d_tiles);
+
+ private:
+  struct CachedPlan {
+    ingest::TilePlan plan;
+    ingest::Tile* d_tiles{nullptr};
+  };
+  uint8_t* staging(uint64_t bytes);
+  unsigned long long* sums(uint32_t n);
+  uint64_t finish(const ingest::TilePlan& p, std::vector<uint64_t>* buckets);
+
+  int device_{0}, sms_{148};
+  cudaStream_t copy_{}, compute_{};
+  std::vector<cudaEvent_t> events_;
+  cudaEvent_t t0_{}, t1_{}, c0_{}, c1_{};
+  uint8_t* staging_{nullptr};
+  uint64_t staging_cap_{0};
+  unsigned long long* d_sums_{nullptr};
+  unsigned long long* h_sums_{nullptr};
+  uint32_t sums_cap_{0};
+  uint8_t* bounce_[2]{};
+  uint64_t bounce_cap_{0};
+  cudaEvent_t bounce_ev_[2]{};
+  std::mutex mu_;
+  std::map<std::string, std::unique_ptr<CachedPlan>> plans_;
+};
+
+struct BackendConfig {
+  int device{0};
+  std::string disk_cache_dir;
+  bool full_verify{false};
+  fmt::Plan plan;
+  uint64_t pinned_pool_bytes{0};
+  unsigned read_threads{8};
+};
+
+// Fast-tier record of one published model.
+struct FastRecord {
+  DeviceSegment seg;
+  fmt::Manifest resident;
+  std::string json;
+  uint64_t generation{0};
+  uint64_t checksum{0};
+  std::vector<uint64_t> bucket_sums;
+  IngestStats stats;
+};
+
+class CudaTierBackend : public TierBackend {
+ public:
+  explicit CudaTierBackend(BackendConfig cfg);
+  ~CudaTierBackend() override;
+
+  Located locate(const fmt::ModelKey& key) override;
+  FetchResult fetch_remote(const fmt::ModelKey& key) override;
+  fmt::Manifest read_manifest(const fmt::ModelKey& key, const std::string& path) override;
+  void stage_host(uint64_t model_id, const fmt::Manifest& m, const std::string& path) override;
+  FastPublication publish_fast(uint64_t model_id, const fmt::Manifest& m, bool from_host,
+                               const std::string& path) override;
+  void evict_fast(uint64_t model_id) override;
+  void evict_host(uint64_t model_id) override;
+  void evict_disk(const fmt::ModelKey& key, const std::string& path) override;
+
+  std::shared_ptr<FastRecord> fast_record(uint64_t model_id);
+  const uint8_t* host_buffer(uint64_t model_id, uint64_t* bytes);
+  Ingestor& ingestor() { return ing_; }
+  const BackendConfig& config() const { return cfg_; }
+
+ private:
+  struct HostBuf {
+    uint8_t* p{nullptr};
+    uint64_t bytes{0};
+    bool pooled{false};
+  };
+  void free_host(HostBuf& h);
+
+  BackendConfig cfg_;
+  Ingestor ing_;
+  std::unique_ptr<PinnedPool> pool_;
+  std::mutex mu_;
+  std::map<uint64_t, HostBuf> host_;
+  std::map<uint64_t, std::shared_ptr<FastRecord>> fast_;
+  std::atomic<uint64_t> next_gen_{1};
+};
+
+// Multi-threaded pread of [off, off+len) into dst (page cache -> pinned).
+void parallel_pread(int fd, uint8_t* dst, uint64_t len, uint64_t off, unsigned threads);
+
+}  // namespace trims

@@ -1,0 +1,601 @@
+// capi.cu — the extern "C" boundary (include/trims.h). Every entry point
+// converts exceptions to reference Errc codes; nothing C++ crosses the ABI.
+#include <dirent.h>
+#include <sys/stat.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <filesystem>
+#include <memory>
+#include <sstream>
+#include <thread>
+
+#include "../../include/trims.h"
+#include "backend.hpp"
+#include "cache_core.hpp"
+#include "cuda_util.hpp"
+#include "format.hpp"
+#include "sha256.hpp"
+
+using namespace trims;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    g_last_error.clear();
+    return f();
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return int(e.code());
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return int(Errc::Internal);
+  } catch (...) {
+    g_last_error = "unknown exception";
+    return int(Errc::Internal);
+  }
+}
+
+int put(const std::string& s, char* out, uint64_t cap) {
+  if (!out || s.size() + 1 > cap) {
+    g_last_error = "output buffer too small (need " + std::to_string(s.size() + 1) + ")";
+    return int(Errc::InvalidArgument);
+  }
+  std::memcpy(out, s.data(), s.size());
+  out[s.size()] = '\0';
+  return 0;
+}
+
+std::vector<fmt::TensorDecl> parse_decls(const char* text) {
+  std::vector<fmt::TensorDecl> out;
+  std::istringstream is(text ? text : "");
+  std::string line;
+  while (std::getline(is, line)) {
+    if (line.empty()) continue;
+    std::istringstream ls(line);
+    std::string name, dt, dims;
+    ls >> name >> dt >> dims;
+    auto t = fmt::dtype_from_name(dt);
+    if (!t) raise(Errc::InvalidArgument, "dtype " + dt);
+    fmt::TensorDecl d{name, {}, *t};
+    size_t pos = 0;
+    while (pos < dims.size()) {
+      size_t c = dims.find(',', pos);
+      if (c == std::string::npos) c = dims.size();
+      d.dims.push_back(std::stoull(dims.substr(pos, c - pos)));
+      pos = c + 1;
+    }
+    out.push_back(std::move(d));
+  }
+  return out;
+}
+
+fmt::Plan make_plan(uint32_t flags, uint32_t out_dtype) {
+  fmt::Plan p;
+  p.convert = flags & TRIMS_PLAN_CONVERT;
+  p.permute_4d = flags & TRIMS_PLAN_PERMUTE_4D;
+  if (out_dtype > 4) raise(Errc::InvalidArgument, "out_dtype");
+  p.out_dtype = fmt::DType(out_dtype);
+  return p;
+}
+
+uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+template <class F>
+void parallel_for(uint64_t n, F&& f) {
+  unsigned t = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (n < (1u << 20)) t = 1;
+  std::vector<std::thread> ts;
+  uint64_t piece = (n + t - 1) / t;
+  for (unsigned i = 1; i < t; ++i) {
+    uint64_t b = std::min(n, i * piece), e = std::min(n, (i + 1) * piece);
+    ts.emplace_back([&, b, e] { f(b, e); });
+  }
+  f(0, std::min(n, piece));
+  for (auto& x : ts) x.join();
+}
+
+}  // namespace
+
+struct trims_store {
+  std::unique_ptr<CudaTierBackend> be;
+  std::unique_ptr<CacheCore> core;
+  std::atomic<uint64_t> clock{0};
+};
+
+struct trims_import {
+  std::unique_ptr<Import> map;
+  std::string json;
+  int device{0};
+  uint64_t blob_bytes{0};
+  uint64_t checksum{0};
+};
+
+extern "C" {
+
+const char* trims_errc_name(int code) { return errc_name(Errc(code)); }
+int trims_wire_code(int code) { return int(wire_code(Errc(code))); }
+const char* trims_last_error(void) { return g_last_error.c_str(); }
+
+int trims_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int trims_sha_hw(void) { return Sha256::hw_accelerated() ? 1 : 0; }
+
+int trims_sha256(const void* data, uint64_t n, uint8_t out[32]) {
+  return guard([&] {
+    auto d = Sha256::of(data, n);
+    std::memcpy(out, d.data(), 32);
+    return 0;
+  });
+}
+
+int trims_read_manifest(const char* path, int full_verify, char* json_out, uint64_t cap, uint8_t checksum_out[32],
+                        uint64_t* blob_bytes, uint64_t* blob_file_offset) {
+  return guard([&] {
+    fmt::ArtifactInfo a = fmt::read_artifact_info(path, full_verify != 0);
+    if (checksum_out) std::memcpy(checksum_out, a.manifest.checksum.data(), 32);
+    if (blob_bytes) *blob_bytes = a.manifest.blob_bytes;
+    if (blob_file_offset) *blob_file_offset = a.blob_offset;
+    return json_out ? put(fmt::manifest_to_json(a.manifest), json_out, cap) : 0;
+  });
+}
+
+int trims_manifest_canonical(const char* json_in, char* json_out, uint64_t cap) {
+  return guard([&] { return put(fmt::manifest_to_json(fmt::manifest_from_json(json_in)), json_out, cap); });
+}
+
+int trims_make_manifest(const char* ns, const char* name, const char* version, const char* decls,
+                        uint64_t workspace_bytes, char* json_out, uint64_t cap) {
+  return guard([&] {
+    fmt::Manifest m = fmt::make_manifest({ns, name, version}, parse_decls(decls), workspace_bytes);
+    return put(fmt::manifest_to_json(m), json_out, cap);
+  });
+}
+
+int trims_write_model(const char* path, const char* manifest_json, const void* blob) {
+  return guard([&] {
+    fmt::Manifest m = fmt::manifest_from_json(manifest_json);
+    static const uint8_t empty = 0;
+    fmt::write_artifact(path, m, blob ? static_cast<const uint8_t*>(blob) : &empty);
+    return 0;
+  });
+}
+
+int trims_layout_for(const char* manifest_json, uint32_t kind, uint64_t block_bytes, char* out, uint64_t cap) {
+  return guard([&] {
+    if (kind > 2) raise(Errc::InvalidArgument, "granularity kind");
+    fmt::Manifest m = fmt::manifest_from_json(manifest_json);
+    std::ostringstream os;
+    for (const auto& o : layout_for(m, {GranKind(kind), block_bytes}))
+      os << o.name << ' ' << o.segment_index << ' ' << o.offset << ' ' << o.length << '\n';
+    return put(os.str(), out, cap);
+  });
+}
+
+int trims_resident_manifest(const char* src_json, uint32_t plan_flags, uint32_t out_dtype, char* json_out,
+                            uint64_t cap) {
+  return guard([&] {
+    fmt::Manifest m = fmt::manifest_from_json(src_json);
+    return put(fmt::manifest_to_json(fmt::resident_manifest(m, make_plan(plan_flags, out_dtype))), json_out, cap);
+  });
+}
+
+int trims_fill_splitmix_host(uint64_t* dst, uint64_t n, uint64_t stream_seed, uint64_t k0) {
+  return guard([&] {
+    parallel_for(n, [&](uint64_t b, uint64_t e) {
+      for (uint64_t j = b; j < e; ++j) dst[j] = mix64(stream_seed + (k0 + j + 1) * 0x9e3779b97f4a7c15ull);
+    });
+    return 0;
+  });
+}
+
+int trims_fill_uniform_host(float* dst, uint64_t n, uint64_t stream_seed, uint64_t j0, float lo, float hi) {
+  return guard([&] {
+    const float span = hi - lo;
+    parallel_for(n, [&](uint64_t b, uint64_t e) {
+      for (uint64_t j = b; j < e; ++j) {
+        float u = float(mix64(stream_seed + (j0 + j + 1) * 0x9e3779b97f4a7c15ull) >> 40) * 0x1p-24f;
+        dst[j] = std::fma(span, u, lo);
+      }
+    });
+    return 0;
+  });
+}
+
+uint64_t trims_fnv1a(const char* s) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (; *s; ++s) {
+    h ^= uint8_t(*s);
+    h *= 0x100000001b3ull;
+  }
+  return h;
+}
+
+int trims_touch_host(const void* blob, const char* manifest_json, uint64_t* out) {
+  return guard([&] {
+    fmt::Manifest m = fmt::manifest_from_json(manifest_json);
+    const uint8_t* base = static_cast<const uint8_t*>(blob);
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (const auto& t : m.tensors) {
+      const uint8_t* p = base + t.offset;
+      uint64_t words = t.nbytes / 8;
+      for (uint64_t i = 0; i < words; ++i) {
+        uint64_t w;
+        std::memcpy(&w, p + 8 * i, 8);
+        h = (h ^ w) * 0x100000001b3ull;
+      }
+      for (uint64_t i = words * 8; i < t.nbytes; ++i) h = (h ^ p[i]) * 0x100000001b3ull;
+    }
+    *out = h;
+    return 0;
+  });
+}
+
+int trims_checksum_host(const void* p, uint64_t n, uint64_t word0, uint64_t* out) {
+  return guard([&] {
+    const uint8_t* b = static_cast<const uint8_t*>(p);
+    const uint64_t words = (n + 7) / 8;
+    std::atomic<uint64_t> total{0};
+    parallel_for(words, [&](uint64_t s, uint64_t e) {
+      uint64_t acc = 0;
+      for (uint64_t i = s; i < e; ++i) {
+        uint64_t w = 0;
+        std::memcpy(&w, b + 8 * i, std::min<uint64_t>(8, n - 8 * i));
+        acc += mix64(w ^ ((word0 + i + 1) * 0x9e3779b97f4a7c15ull));
+      }
+      total.fetch_add(acc);
+    });
+    *out = total.load();
+    return 0;
+  });
+}
+
+// ---------------------------------------------------------------- store
+
+int trims_store_create(const trims_store_config* cfg, trims_store** out) {
+  return guard([&] {
+    if (!cfg || !out) raise(Errc::InvalidArgument, "null argument");
+    if (!cfg->fast_capacity_bytes || !cfg->host_capacity_bytes || !cfg->disk_capacity_bytes)
+      raise(Errc::InvalidArgument, "capacities must be > 0");  // daemon.cpp:26-36
+    if (!cfg->disk_cache_dir || !*cfg->disk_cache_dir) raise(Errc::InvalidArgument, "disk_cache_dir must be set");
+    if (trims_device_count() <= cfg->device) raise(Errc::NoDevice, "no CUDA device " + std::to_string(cfg->device));
+    std::filesystem::create_directories(cfg->disk_cache_dir);
+    auto s = std::make_unique<trims_store>();
+    BackendConfig bc;
+    bc.device = cfg->device;
+    bc.disk_cache_dir = cfg->disk_cache_dir;
+    bc.full_verify = cfg->full_verify != 0;
+    bc.plan = make_plan(cfg->plan_flags, cfg->out_dtype);
+    bc.pinned_pool_bytes = cfg->pinned_pool_bytes ? cfg->pinned_pool_bytes : cfg->host_capacity_bytes;
+    bc.read_threads = cfg->read_threads ? cfg->read_threads : 8;
+    s->be = std::make_unique<CudaTierBackend>(bc);
+    CoreConfig cc{cfg->fast_capacity_bytes, cfg->host_capacity_bytes, cfg->disk_capacity_bytes,
+                  Policy(cfg->policy ? 1 : 0), cfg->eager_reclaim != 0};
+    s->core = std::make_unique<CacheCore>(cc, *s->be);
+    if (cfg->scan_disk) {  // daemon.cpp:314-325: name-sorted for deterministic seq numbers
+      std::vector<std::filesystem::path> files;
+      for (const auto& e : std::filesystem::directory_iterator(cfg->disk_cache_dir))
+        if (e.is_regular_file()) files.push_back(e.path());
+      std::sort(files.begin(), files.end());
+      for (const auto& p : files) {
+        auto key = fmt::key_from_filename(p.filename().string());
+        if (key) s->core->register_disk_file(*key, p.string(), std::filesystem::file_size(p));
+      }
+    }
+    *out = s.release();
+    return 0;
+  });
+}
+
+void trims_store_destroy(trims_store* s) {
+  if (!s) return;
+  try {
+    s->core->drop_all();
+  } catch (...) {
+  }
+  delete s;
+}
+
+int trims_store_open(trims_store* s, const char* ns, const char* name, const char* version, uint32_t gran_kind,
+                     uint64_t block_bytes, trims_export* out) {
+  return guard([&] {
+    if (gran_kind > 2) raise(Errc::InvalidArgument, "granularity kind");
+    uint64_t now = s->clock.fetch_add(1) + 1;  // daemon.cpp:457
+    PlacementResult r = s->core->open_model({ns, name, version}, {GranKind(gran_kind), block_bytes}, now);
+    std::memset(out, 0, sizeof *out);
+    out->model_id = r.model_id;
+    out->outcome = uint32_t(r.outcome);
+    out->weights_bytes = r.weights_bytes;
+    out->workspace_bytes = r.workspace_bytes;
+    out->timings_ns[0] = r.timings.fetch_ns;
+    out->timings_ns[1] = r.timings.disk_read_ns;
+    out->timings_ns[2] = r.timings.host_to_fast_copy_ns;
+    out->timings_ns[3] = r.timings.handle_export_ns;
+    std::memcpy(out->manifest_digest, r.manifest_digest.data(), 32);
+    out->fd = -1;
+    if (!r.segments.empty()) {
+      const ExportedSegment& es = r.segments[0];
+      out->device = es.device;
+      out->generation = es.generation;
+      out->payload_bytes = es.length;
+      out->resident_blob_bytes = es.resident_blob_bytes;
+      out->alloc_bytes = es.alloc_bytes;
+      out->ingest_checksum = es.ingest_checksum;
+      out->dev_ptr = es.dev_ptr;
+      out->fd = es.fd;
+      std::snprintf(out->token, sizeof out->token, "%s", es.token.c_str());
+    }
+    // objects of the resident blob at the requested granularity
+    if (auto rec = s->be->fast_record(r.model_id))
+      out->n_objects = uint32_t(layout_for(rec->resident, {GranKind(gran_kind), block_bytes}).size());
+    else
+      out->n_objects = uint32_t(r.layout.size());
+    return 0;
+  });
+}
+
+int trims_store_close(trims_store* s, const char* ns, const char* name, const char* version, uint64_t* rc) {
+  return guard([&] {
+    uint64_t v = s->core->close_model({ns, name, version});
+    if (rc) *rc = v;
+    return 0;
+  });
+}
+
+int trims_store_reclaim(trims_store* s, uint32_t tier, uint64_t bytes, uint32_t policy, char* out, uint64_t cap) {
+  return guard([&] {
+    if (tier > 2) raise(Errc::InvalidArgument, "tier");
+    auto ev = s->core->reclaim(Tier(tier), bytes, Policy(policy ? 1 : 0));
+    std::string txt;
+    for (const auto& k : ev) txt += fmt::to_string(k) + "\n";
+    return out ? put(txt, out, cap) : 0;
+  });
+}
+
+int trims_store_register_disk_file(trims_store* s, const char* ns, const char* name, const char* version,
+                                   const char* path, uint64_t bytes) {
+  return guard([&] {
+    s->core->register_disk_file({ns, name, version}, path, bytes);
+    return 0;
+  });
+}
+
+int trims_store_drop_all(trims_store* s) {
+  return guard([&] {
+    s->core->drop_all();
+    return 0;
+  });
+}
+
+int trims_store_stats_json(trims_store* s, char* out, uint64_t cap) {
+  return guard([&] {
+    StatsSnapshot st = s->core->stats();
+    std::ostringstream os;
+    os << "{\"tiers\":[";
+    for (int t = 0; t < kTiers; ++t) {
+      const auto& x = st.tiers[t];
+      os << (t ? "," : "") << "{\"hits\":" << x.hits << ",\"misses\":" << x.misses << ",\"evictions\":" << x.evictions
+         << ",\"used_bytes\":" << x.used_bytes << ",\"capacity_bytes\":" << x.capacity_bytes << "}";
+    }
+    os << "],\"models\":[";
+    for (size_t i = 0; i < st.models.size(); ++i) {
+      const auto& m = st.models[i];
+      os << (i ? "," : "") << "{\"key\":\"" << fmt::to_string(m.key) << "\",\"refcount\":" << m.refcount
+         << ",\"use_count\":" << m.use_count << ",\"last_access\":" << m.last_access
+         << ",\"residency\":" << int(m.residency) << "}";
+    }
+    os << "],\"open_requests\":" << st.open_requests << ",\"open_errors\":" << st.open_errors
+       << ",\"disk_reads\":" << st.disk_reads << ",\"remote_fetches\":" << st.remote_fetches
+       << ",\"fetch_ns\":" << st.cumulative.fetch_ns << ",\"disk_read_ns\":" << st.cumulative.disk_read_ns
+       << ",\"copy_ns\":" << st.cumulative.host_to_fast_copy_ns << ",\"export_ns\":" << st.cumulative.handle_export_ns
+       << "}";
+    return put(os.str(), out, cap);
+  });
+}
+
+int trims_store_resident_json(trims_store* s, uint64_t model_id, char* out, uint64_t cap) {
+  return guard([&] {
+    auto rec = s->be->fast_record(model_id);
+    if (!rec) raise(Errc::NotOpen, "model not fast-resident");
+    return put(rec->json, out, cap);
+  });
+}
+
+int trims_store_ingest_stats(trims_store* s, uint64_t model_id, double out5[5]) {
+  return guard([&] {
+    auto rec = s->be->fast_record(model_id);
+    if (!rec) raise(Errc::NotOpen, "model not fast-resident");
+    out5[0] = rec->stats.h2d_ms;
+    out5[1] = rec->stats.total_ms;
+    out5[2] = rec->stats.read_ms;
+    out5[3] = double(rec->stats.h2d_bytes);
+    out5[4] = rec->stats.launches;
+    return 0;
+  });
+}
+
+int trims_store_checksums(trims_store* s, uint64_t model_id, uint64_t* out, uint64_t cap, uint64_t* n) {
+  return guard([&] {
+    auto rec = s->be->fast_record(model_id);
+    if (!rec) raise(Errc::NotOpen, "model not fast-resident");
+    *n = rec->bucket_sums.size();
+    for (uint64_t i = 0; i < std::min<uint64_t>(cap, *n); ++i) out[i] = rec->bucket_sums[i];
+    return 0;
+  });
+}
+
+// ---------------------------------------------------------------- import
+
+int trims_import_open(int device, int fd, uint64_t alloc_bytes, uint64_t generation, uint64_t payload_bytes,
+                      const uint8_t digest[32], trims_import** out, void** dev_ptr) {
+  return guard([&] {
+    if (payload_bytes < 8 || payload_bytes + sizeof(SegTail) > alloc_bytes)
+      raise(Errc::NoSuchSegment, "segment shorter than its payload");
+    auto im = std::make_unique<trims_import>();
+    im->map.reset(Import::open(device, fd, alloc_bytes, /*read_only=*/true));
+    DeviceGuard g(device);
+    uint8_t tail[8 + sizeof(SegTail)];
+    TRIMS_CUDA(cudaMemcpy(tail, im->map->ptr() + payload_bytes - 8, sizeof tail, cudaMemcpyDeviceToHost));
+    uint64_t jlen = 0;
+    for (int i = 0; i < 8; ++i) jlen |= uint64_t(tail[i]) << (8 * i);
+    SegTail st;
+    std::memcpy(&st, tail + 8, sizeof st);
+    if (st.magic != kSegMagic) raise(Errc::NoSuchSegment, "bad segment tail");
+    if (st.generation != generation)
+      raise(Errc::StaleGeneration, "generation " + std::to_string(st.generation) + " != " + std::to_string(generation));
+    if (!st.sealed) raise(Errc::NotSealed, "segment not sealed");
+    if (st.length != payload_bytes || jlen + 8 > payload_bytes) raise(Errc::Corrupt, "segment length mismatch");
+    im->json.resize(jlen);
+    TRIMS_CUDA(cudaMemcpy(im->json.data(), im->map->ptr() + payload_bytes - 8 - jlen, jlen, cudaMemcpyDeviceToHost));
+    if (digest) {
+      auto d = Sha256::of(im->json.data(), im->json.size());
+      if (std::memcmp(d.data(), digest, 32) != 0) raise(Errc::Corrupt, "manifest digest mismatch on attach");
+    }
+    im->device = device;
+    im->blob_bytes = st.blob_bytes;
+    im->checksum = st.checksum;
+    if (dev_ptr) *dev_ptr = im->map->ptr();
+    *out = im.release();
+    return 0;
+  });
+}
+
+int trims_import_manifest(trims_import* im, char* out, uint64_t cap) {
+  return guard([&] { return put(im->json, out, cap); });
+}
+
+int trims_import_read_only(trims_import* im) { return im && im->map && im->map->read_only() ? 1 : 0; }
+
+int trims_import_verify(trims_import* im, uint64_t* checksum_out) {
+  return guard([&] {
+    DeviceGuard g(im->device);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, im->device);
+    unsigned long long* d = nullptr;
+    TRIMS_CUDA(cudaMalloc(&d, sizeof *d));
+    unsigned long long h = 0;
+    try {
+      TRIMS_CUDA(cudaMemset(d, 0, sizeof *d));
+      ingest::launch_checksum(im->map->ptr(), im->blob_bytes, 0, d, nullptr, sms);
+      TRIMS_CUDA(cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost));
+    } catch (...) {
+      cudaFree(d);
+      throw;
+    }
+    cudaFree(d);
+    if (checksum_out) *checksum_out = h;
+    if (h != im->checksum) raise(Errc::Corrupt, "resident blob checksum mismatch on attach");
+    return 0;
+  });
+}
+
+void trims_import_close(trims_import* im) {
+  try {
+    delete im;
+  } catch (...) {
+  }
+}
+
+// ---------------------------------------------------------------- raw ingest
+
+namespace {
+std::mutex g_ing_mu;
+std::map<int, std::unique_ptr<Ingestor>> g_ing;
+Ingestor& ingestor(int device) {
+  std::lock_guard lk(g_ing_mu);
+  auto& p = g_ing[device];
+  if (!p) p = std::make_unique<Ingestor>(device);
+  return *p;
+}
+}  // namespace
+
+int trims_ingest_host(int device, const void* host_blob, const char* src_json, uint32_t plan_flags,
+                      uint32_t out_dtype, void* dev_dst, uint64_t* checksum_out, double stats_out5[5]) {
+  return guard([&] {
+    fmt::Manifest src = fmt::manifest_from_json(src_json);
+    fmt::Plan plan = make_plan(plan_flags, out_dtype);
+    fmt::Manifest dst = fmt::resident_manifest(src, plan);
+    IngestStats st;
+    uint64_t c = ingestor(device).from_host(static_cast<const uint8_t*>(host_blob), src, dst, plan.identity(),
+                                            static_cast<uint8_t*>(dev_dst), nullptr, &st);
+    if (checksum_out) *checksum_out = c;
+    if (stats_out5) {
+      stats_out5[0] = st.h2d_ms;
+      stats_out5[1] = st.total_ms;
+      stats_out5[2] = st.read_ms;
+      stats_out5[3] = double(st.h2d_bytes);
+      stats_out5[4] = st.launches;
+    }
+    return 0;
+  });
+}
+
+int trims_transform_device(int device, const void* dev_src, const char* src_json, uint32_t plan_flags,
+                           uint32_t out_dtype, void* dev_dst, unsigned long long* d_sums, void* stream) {
+  return guard([&] {
+    fmt::Manifest src = fmt::manifest_from_json(src_json);
+    fmt::Plan plan = make_plan(plan_flags, out_dtype);
+    fmt::Manifest dst = fmt::resident_manifest(src, plan);
+    ingestor(device).from_device(static_cast<const uint8_t*>(dev_src), src, dst, plan.identity(),
+                                 static_cast<uint8_t*>(dev_dst), d_sums, static_cast<cudaStream_t>(stream));
+    return 0;
+  });
+}
+
+int trims_plan_info(const char* src_json, uint32_t plan_flags, uint32_t out_dtype, uint64_t out4[4]) {
+  return guard([&] {
+    fmt::Manifest src = fmt::manifest_from_json(src_json);
+    fmt::Plan plan = make_plan(plan_flags, out_dtype);
+    fmt::Manifest dst = fmt::resident_manifest(src, plan);
+    ingest::TilePlan p = ingest::build_tiles(src, dst, plan.identity());
+    out4[0] = p.tiles.size();
+    out4[1] = p.buckets;
+    out4[2] = p.algo_read_bytes;
+    out4[3] = p.algo_write_bytes;
+    return 0;
+  });
+}
+
+int trims_checksum_device(const void* dev, uint64_t nbytes, uint64_t word0, unsigned long long* d_out, void* stream) {
+  return guard([&] {
+    int dev_id = 0, sms = 148;
+    cudaGetDevice(&dev_id);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev_id);
+    ingest::launch_checksum(static_cast<const uint8_t*>(dev), nbytes, word0, d_out, static_cast<cudaStream_t>(stream),
+                            sms);
+    return 0;
+  });
+}
+
+int trims_fill_splitmix_device(uint64_t* dev, uint64_t n, uint64_t stream_seed, uint64_t k0, void* stream) {
+  return guard([&] {
+    ingest::launch_fill_splitmix(dev, n, stream_seed, k0, static_cast<cudaStream_t>(stream));
+    return 0;
+  });
+}
+
+int trims_fill_uniform_device(float* dev, uint64_t n, uint64_t stream_seed, uint64_t j0, float lo, float hi,
+                              void* stream) {
+  return guard([&] {
+    ingest::launch_fill_uniform(dev, n, stream_seed, j0, lo, hi, static_cast<cudaStream_t>(stream));
+    return 0;
+  });
+}
+
+}  // extern "C"

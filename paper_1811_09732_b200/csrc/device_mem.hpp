@@ -1,0 +1,127 @@
+// device_mem.hpp — the physical tiers on B200.
+//
+//  * DeviceSegment: one fast-tier (HBM) object. A cuMem VMM allocation
+//    (2 MiB granularity) created exportable as a POSIX fd — the B200
+//    replacement for the reference's named shm segment
+//    (proj/src/shared_segment.cpp:115-191). Importers map it read-only
+//    (cuMemSetAccess PROT_READ = the reference's mprotect "seal"), and the
+//    physical memory lives until the last mapping goes, so readers' views
+//    survive owner eviction exactly like attached shm views do.
+//  * PinnedPool: the host tier — page-locked DRAM carved first-fit in 2 MiB
+//    granules, so staged blobs DMA at full PCIe rate (the reference's
+//    std::vector host buffers, daemon.cpp:153-158, are pageable).
+//  * Import: the client-side attach (shared_segment.cpp:212-245).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "errc.hpp"
+
+namespace trims {
+
+// Driver entry points resolved through the runtime (no link-time libcuda
+// dependency, so the library loads on GPU-less build hosts).
+struct Driver {
+  decltype(&cuMemCreate) MemCreate{};
+  decltype(&cuMemRelease) MemRelease{};
+  decltype(&cuMemAddressReserve) MemAddressReserve{};
+  decltype(&cuMemAddressFree) MemAddressFree{};
+  decltype(&cuMemMap) MemMap{};
+  decltype(&cuMemUnmap) MemUnmap{};
+  decltype(&cuMemSetAccess) MemSetAccess{};
+  decltype(&cuMemExportToShareableHandle) MemExportToShareableHandle{};
+  decltype(&cuMemImportFromShareableHandle) MemImportFromShareableHandle{};
+  decltype(&cuMemGetAllocationGranularity) MemGetAllocationGranularity{};
+  decltype(&cuGetErrorString) GetErrorString{};
+  static const Driver& get();
+};
+
+void cu_check(CUresult r, const char* what);
+
+// Segment tail written after the payload (blob | JSON | u64 jlen): the
+// reference's 64-byte SegHeader (shared_segment.cpp:21-30) moved to the end
+// so the resident blob starts at the allocation base (TMA/vector alignment).
+struct SegTail {
+  uint64_t magic;       // "TRMSEGB2"
+  uint64_t generation;
+  uint64_t length;      // payload bytes
+  uint32_t sealed;
+  uint32_t device;
+  uint64_t blob_bytes;  // resident blob bytes
+  uint64_t checksum;    // TRIMS block checksum of the resident blob
+  uint64_t reserved[2];
+};
+static_assert(sizeof(SegTail) == 64, "tail is 64 bytes");
+inline constexpr uint64_t kSegMagic = 0x32424745534d5254ull;  // "TRMSEGB2" little-endian
+
+class DeviceSegment {
+ public:
+  DeviceSegment() = default;
+  DeviceSegment(const DeviceSegment&) = delete;
+  DeviceSegment& operator=(const DeviceSegment&) = delete;
+  DeviceSegment(DeviceSegment&& o) noexcept { *this = std::move(o); }
+  DeviceSegment& operator=(DeviceSegment&& o) noexcept;
+  ~DeviceSegment() { release(); }
+
+  // bytes = payload + tail; rounded up to the allocation granularity.
+  static DeviceSegment create(int device, uint64_t bytes);
+  void release();
+  uint8_t* ptr() const { return reinterpret_cast<uint8_t*>(va_); }
+  uint64_t size() const { return size_; }
+  int fd() const { return fd_; }
+  int device() const { return device_; }
+
+ private:
+  CUdeviceptr va_{0};
+  uint64_t size_{0};
+  CUmemGenericAllocationHandle handle_{0};
+  int fd_{-1};
+  int device_{0};
+};
+
+// Client-side read-only mapping of an exported segment.
+class Import {
+ public:
+  Import() = default;
+  Import(const Import&) = delete;
+  Import& operator=(const Import&) = delete;
+  ~Import();
+  // fd must be valid in this process (SCM_RIGHTS / pidfd_getfd / same process).
+  static Import* open(int device, int fd, uint64_t alloc_bytes, bool read_only);
+  uint8_t* ptr() const { return reinterpret_cast<uint8_t*>(va_); }
+  uint64_t size() const { return size_; }
+  bool read_only() const { return read_only_; }
+
+ private:
+  CUdeviceptr va_{0};
+  uint64_t size_{0};
+  bool read_only_{false};
+};
+
+class PinnedPool {
+ public:
+  explicit PinnedPool(uint64_t bytes);
+  ~PinnedPool();
+  PinnedPool(const PinnedPool&) = delete;
+  PinnedPool& operator=(const PinnedPool&) = delete;
+  // Returns nullptr when no extent fits (caller may fall back).
+  uint8_t* alloc(uint64_t bytes);
+  void free(uint8_t* p);
+  uint64_t capacity() const { return cap_; }
+
+ private:
+  static constexpr uint64_t kGranule = 2ull << 20;
+  uint8_t* base_{nullptr};
+  uint64_t cap_{0};
+  std::mutex mu_;
+  std::map<uint64_t, uint64_t> free_;   // offset -> bytes
+  std::map<uint64_t, uint64_t> used_;   // offset -> bytes
+};
+
+}  // namespace trims

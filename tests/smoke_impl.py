@@ -1,0 +1,49 @@
+"""__graft_entry__.smoke(): one small load-and-serve pass on cuda:0 checked
+against the oracle (the reference's own trailer/touch + the CPU transform)."""
+import os
+import tempfile
+
+import numpy as np
+
+
+def run_smoke() -> None:
+    import torch
+
+    import oracle
+    from paper_1811_09732_b200 import catalog as C
+    from paper_1811_09732_b200 import format as F
+    from paper_1811_09732_b200.client import Client, TensorView
+    from paper_1811_09732_b200.store import Store, StoreOptions
+    from tests.golden_data import load
+    from tests.gpu_util import expected_resident
+
+    assert torch.cuda.is_available(), "smoke needs cuda:0"
+    g = {e["name"]: e for e in load("catalog.json.gz")["tiny_seed1"]}
+    with tempfile.TemporaryDirectory(prefix="trims-smoke-") as d:
+        # 1. identity path: catalog model, disk -> pinned -> HBM, bytes == reference trailer
+        C.gen_catalog("tiny", d, seed=1, only=["alexnet"])
+        with Store(StoreOptions(disk_cache_dir=d, fast_capacity_bytes=64 << 20, host_capacity_bytes=64 << 20)) as s:
+            cli = Client(s)
+            v = cli.open(F.ModelKey("zoo", "alexnet", "1.0.0"), force_shared=True)
+            n = v.blob_bytes()
+            blob = TensorView("b", [n], "i8", "native", 0, n, v.base_ptr).torch().view(torch.uint8).cpu().numpy()
+            assert F.sha256(blob).hex() == g["alexnet"]["trailer"], "resident bytes differ from the reference blob"
+            assert cli.touch(v) == g["alexnet"]["touch"], "touch differs from the reference"
+            assert v.export.ingest_checksum == oracle.port().block_checksum(blob)
+            cli.close(v)
+        # 2. converting path: real-shape AlexNet fp32 -> bf16 KRSC, bit-exact vs the CPU oracle
+        arch = C.ARCHS["alexnet"]()
+        C.write_arch(arch, d, seed=1)
+        src_json, src_blob = C.arch_blob(arch, seed=1)
+        opts = StoreOptions(disk_cache_dir=d, fast_capacity_bytes=1 << 30, host_capacity_bytes=1 << 30,
+                            convert_to="bf16", permute_4d=True)
+        with Store(opts) as s:
+            cli = Client(s)
+            v = cli.open(C.arch_key(arch), force_shared=True)
+            n = v.blob_bytes()
+            got = TensorView("b", [n], "i8", "native", 0, n, v.base_ptr).torch().view(torch.uint8).cpu().numpy()
+            want = expected_resident(src_json, src_blob, v.manifest_json)
+            assert np.array_equal(got, want), "converted resident blob differs from the oracle"
+            assert v.export.ingest_checksum == oracle.port().block_checksum(want)
+            cli.close(v)
+    print("smoke ok")
