@@ -132,7 +132,7 @@ def run_ours(args):
     import torch
 
     from paper_1811_09732_b200 import format as F
-    from paper_1811_09732_b200._lib import check, lib
+    from paper_1811_09732_b200.ingest import IngestPlan
 
     world, rank, local = dist_setup(args.gpus)
     dev = local
@@ -140,22 +140,22 @@ def run_ours(args):
     work = tempfile.mkdtemp(prefix=f"trims-bench-{rank}-")
     arch, path, src_json, blob = make_artifact(work)
     flags = F.PLAN_CONVERT | F.PLAN_PERMUTE_4D
-    res_json = F.resident_manifest(src_json, flags, "bf16")
-    info = F.plan_info(src_json, flags, "bf16")
+    plan = IngestPlan(src_json, flags, "bf16", dev)
+    res_json = plan.resident_json
+    info = {"buckets": plan.buckets, "read_bytes": plan.read_bytes, "write_bytes": plan.write_bytes}
     src_bytes = blob.size
     rb = json.loads(res_json)
-    res_bytes = (max(t["offset"] + t["nbytes"] for t in rb["tensors"]) + 63) // 64 * 64
+    res_bytes = plan.resident_bytes
 
     d_src = torch.from_numpy(blob).to(f"cuda:{dev}")
     d_dst = torch.empty(res_bytes, dtype=torch.uint8, device=f"cuda:{dev}")
     d_sums = torch.zeros(info["buckets"], dtype=torch.int64, device=f"cuda:{dev}")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
     stream = torch.cuda.Stream(device=dev)
-    src_c = src_json.encode()
+    launches = [0]
 
     def transform():
-        check(lib.trims_transform_device(dev, d_src.data_ptr(), src_c, flags, 4, d_dst.data_ptr(),
-                                         d_sums.data_ptr(), ctypes.c_void_p(stream.cuda_stream)))
+        launches[0] += plan.transform(d_src.data_ptr(), d_dst.data_ptr(), d_sums.data_ptr(), stream.cuda_stream)
 
     # ---- value: HBM-resident transform
     with torch.cuda.stream(stream):
@@ -165,6 +165,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier(world)
     total_ms = 0.0
+    launches[0] = 0
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(dev) as clocks:
         with torch.cuda.stream(stream):
@@ -183,10 +184,8 @@ def run_ours(args):
 
     # ---- e2e: pinned host buffer through the C ABI (H2D + transform + D2H checksums)
     host = torch.from_numpy(blob).pin_memory()
-    cs = ctypes.c_uint64()
-    st = (ctypes.c_double * 5)()
     for _ in range(args.warmup):
-        check(lib.trims_ingest_host(dev, host.data_ptr(), src_c, flags, 4, d_dst.data_ptr(), ctypes.byref(cs), st))
+        cs, st = plan.ingest_host(host.data_ptr(), d_dst.data_ptr())
     torch.cuda.synchronize()
     barrier(world)
     e2e_ms = 0.0
@@ -195,17 +194,17 @@ def run_ours(args):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        check(lib.trims_ingest_host(dev, host.data_ptr(), src_c, flags, 4, d_dst.data_ptr(), ctypes.byref(cs), st))
+        cs, st = plan.ingest_host(host.data_ptr(), d_dst.data_ptr())   # H2D + transform + D2H checksums
         e2e_ms += (time.perf_counter() - t0) * 1e3
-        launches_e2e += int(st[4])
+        launches_e2e += st["launches"]
     barrier(world)
     e2e_max = barrier_max(e2e_ms, world)
     e2e_value = world * args.steps * src_bytes / (e2e_max / 1e3) / 1e9
-    h2d_gbs = src_bytes / (st[0] / 1e3) / 1e9 if st[0] > 0 else None
+    h2d_gbs = src_bytes / (st["h2d_ms"] / 1e3) / 1e9 if st["h2d_ms"] > 0 else None
 
     # ---- parity spot check of the timed output (checksum vs the value path)
     want = int(d_sums.cpu().numpy().view("uint64").sum(dtype="uint64"))
-    assert cs.value == want, "e2e and device-resident ingest disagree"
+    assert cs == want, "e2e and device-resident ingest disagree"
 
     # ---- store latencies (rank 0): cold / warm(host) / hot(HBM) opens
     lat = store_latencies(work, arch, dev) if rank == 0 else None
@@ -227,7 +226,7 @@ def run_ours(args):
                      "frac": round(achieved / hbm_peak, 4), "traffic": None,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                      "algorithmic_bytes_per_launch": algo, "kernel": "transform_kernel"},
-        "gpu_launches": args.steps + launches_e2e,
+        "gpu_launches": launches[0] + launches_e2e,
         "clocks": clocks.summary(),
         "latency_ms": lat,
     }

@@ -181,6 +181,18 @@ int trims_ingest_host(int device, const void* host_blob, const char* src_json, u
  * Bucket sums are accumulated into d_sums (must be zeroed by the caller). */
 int trims_transform_device(int device, const void* dev_src, const char* src_json, uint32_t plan_flags,
                            uint32_t out_dtype, void* dev_dst, unsigned long long* d_sums, void* stream);
+/* Compiled ingest plans: the tile table is built and uploaded once, so the
+ * per-call host cost of the two entry points below is a few microseconds. */
+typedef struct trims_plan trims_plan;
+int trims_plan_create(int device, const char* src_json, uint32_t plan_flags, uint32_t out_dtype, trims_plan** out);
+void trims_plan_destroy(trims_plan* p);
+/* tiles, buckets, algo read bytes, algo write bytes, src blob, resident blob, chunks, dtype-pair mask */
+int trims_plan_describe(trims_plan* p, uint64_t out8[8]);
+int trims_plan_resident_json(trims_plan* p, char* out, uint64_t cap);
+int trims_plan_transform(trims_plan* p, const void* dev_src, void* dev_dst, unsigned long long* d_sums, void* stream,
+                         uint32_t* launches);
+int trims_plan_ingest_host(trims_plan* p, const void* host_blob, void* dev_dst, uint64_t* checksum_out,
+                           double stats_out5[5]);
 /* Roofline accounting of a plan: tiles, buckets, algorithmic read/write bytes. */
 int trims_plan_info(const char* src_json, uint32_t plan_flags, uint32_t out_dtype, uint64_t out4[4]);
 /* TRIMS block checksum of a device range (async, accumulates into *d_out). */

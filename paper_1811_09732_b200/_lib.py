@@ -134,6 +134,12 @@ _SIGS = {
     "trims_ingest_host": (_c.c_int, [_c.c_int, _p, _s, _u32, _u32, _p, _c.POINTER(_u64), _c.POINTER(_c.c_double)]),
     "trims_transform_device": (_c.c_int, [_c.c_int, _p, _s, _u32, _u32, _p, _p, _p]),
     "trims_plan_info": (_c.c_int, [_s, _u32, _u32, _c.POINTER(_u64)]),
+    "trims_plan_create": (_c.c_int, [_c.c_int, _s, _u32, _u32, _c.POINTER(_p)]),
+    "trims_plan_destroy": (None, [_p]),
+    "trims_plan_describe": (_c.c_int, [_p, _c.POINTER(_u64)]),
+    "trims_plan_resident_json": (_c.c_int, [_p, _s, _u64]),
+    "trims_plan_transform": (_c.c_int, [_p, _p, _p, _p, _p, _c.POINTER(_u32)]),
+    "trims_plan_ingest_host": (_c.c_int, [_p, _p, _p, _c.POINTER(_u64), _c.POINTER(_c.c_double)]),
     "trims_checksum_device": (_c.c_int, [_p, _u64, _u64, _p, _p]),
     "trims_fill_splitmix_device": (_c.c_int, [_p, _u64, _u64, _u64, _p]),
     "trims_fill_uniform_device": (_c.c_int, [_p, _u64, _u64, _u64, _c.c_float, _c.c_float, _p]),

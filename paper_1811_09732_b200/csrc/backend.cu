@@ -61,8 +61,7 @@ Ingestor::Ingestor(int device) : device_(device) {
 }
 
 Ingestor::~Ingestor() {
-  DeviceGuard g(device_);
-  for (auto& [k, p] : plans_) cudaFree(p->d_tiles);
+  DeviceGuard g(device_, /*nothrow=*/true);
   for (auto e : events_) cudaEventDestroy(e);
   for (auto e : {t0_, t1_, c0_, c1_}) cudaEventDestroy(e);
   for (auto e : bounce_ev_) cudaEventDestroy(e);
@@ -99,27 +98,29 @@ unsigned long long* Ingestor::sums(uint32_t n) {
   return d_sums_;
 }
 
-const ingest::TilePlan& Ingestor::plan_for(const fmt::Manifest& src, const fmt::Manifest& dst, bool identity,
-                                           const ingest::Tile** d_tiles) {
-  std::string key = (identity ? "I" : "T") + fmt::manifest_to_json(src) + "|" + fmt::manifest_to_json(dst);
-  auto it = plans_.find(key);
-  if (it == plans_.end()) {
-    auto cp = std::make_unique<CachedPlan>();
-    uint64_t chunk = std::max<uint64_t>(16ull << 20, src.blob_bytes / (events_.size() - 8) + 1);
-    cp->plan = ingest::build_tiles(src, dst, identity, chunk);
-    if (!cp->plan.tiles.empty()) {
-      size_t bytes = cp->plan.tiles.size() * sizeof(ingest::Tile);
-      TRIMS_CUDA(cudaMalloc(&cp->d_tiles, bytes));
-      TRIMS_CUDA(cudaMemcpy(cp->d_tiles, cp->plan.tiles.data(), bytes, cudaMemcpyHostToDevice));
-    }
-    if (plans_.size() > 64) {
-      for (auto& [k, p] : plans_) cudaFree(p->d_tiles);
-      plans_.clear();
-    }
-    it = plans_.emplace(std::move(key), std::move(cp)).first;
+IngestPlan::~IngestPlan() {
+  if (d_tiles) {
+    DeviceGuard g(device, /*nothrow=*/true);
+    cudaFree(d_tiles);
   }
-  if (d_tiles) *d_tiles = it->second->d_tiles;
-  return it->second->plan;
+}
+
+std::shared_ptr<IngestPlan> Ingestor::compile(const fmt::Manifest& src, const fmt::Plan& plan) {
+  DeviceGuard g(device_);
+  auto p = std::make_shared<IngestPlan>();
+  p->device = device_;
+  p->src = src;
+  p->dst = fmt::resident_manifest(src, plan);
+  p->dst_json = fmt::manifest_to_json(p->dst);
+  p->identity = plan.identity();
+  const uint64_t chunk = std::max<uint64_t>(16ull << 20, src.blob_bytes / (events_.size() - 8) + 1);
+  p->plan = ingest::build_tiles(p->src, p->dst, p->identity, chunk);
+  if (!p->plan.tiles.empty()) {
+    const size_t bytes = p->plan.tiles.size() * sizeof(ingest::Tile);
+    TRIMS_CUDA(cudaMalloc(&p->d_tiles, bytes));
+    TRIMS_CUDA(cudaMemcpy(p->d_tiles, p->plan.tiles.data(), bytes, cudaMemcpyHostToDevice));
+  }
+  return p;
 }
 
 uint64_t Ingestor::finish(const ingest::TilePlan& p, std::vector<uint64_t>* buckets) {
@@ -132,17 +133,15 @@ uint64_t Ingestor::finish(const ingest::TilePlan& p, std::vector<uint64_t>* buck
   return total;
 }
 
-uint64_t Ingestor::from_host(const uint8_t* host_blob, const fmt::Manifest& src, const fmt::Manifest& dst,
-                             bool identity, uint8_t* d_dst, std::vector<uint64_t>* buckets, IngestStats* st) {
+uint64_t Ingestor::from_host(const IngestPlan& ip, const uint8_t* host_blob, uint8_t* d_dst,
+                             std::vector<uint64_t>* buckets, IngestStats* st) {
   std::lock_guard lk(mu_);
   DeviceGuard g(device_);
-  const ingest::Tile* d_tiles = nullptr;
-  const ingest::TilePlan& p = plan_for(src, dst, identity, &d_tiles);
+  const ingest::TilePlan& p = ip.plan;
   unsigned long long* ds = sums(p.buckets);
   TRIMS_CUDA(cudaMemsetAsync(ds, 0, p.buckets * sizeof(unsigned long long), compute_));
-  uint8_t* raw = identity ? d_dst : staging(src.blob_bytes);
+  uint8_t* raw = ip.identity ? d_dst : staging(ip.src.blob_bytes);
   TRIMS_CUDA(cudaEventRecord(t0_, copy_));
-  TRIMS_CUDA(cudaStreamWaitEvent(copy_, t0_, 0));
   uint32_t launches = 0;
   for (size_t c = 0; c < p.chunks.size(); ++c) {
     const auto& ch = p.chunks[c];
@@ -151,9 +150,8 @@ uint64_t Ingestor::from_host(const uint8_t* host_blob, const fmt::Manifest& src,
                                cudaMemcpyHostToDevice, copy_));
     TRIMS_CUDA(cudaEventRecord(ev, copy_));
     TRIMS_CUDA(cudaStreamWaitEvent(compute_, ev, 0));
-    ingest::launch_transform(d_tiles + ch.tile_begin, ch.tile_end - ch.tile_begin, p.has_perm, raw, d_dst, ds,
-                             compute_, sms_);
-    ++launches;
+    launches += ingest::launch_transform(ip.d_tiles + ch.tile_begin, ch.tile_end - ch.tile_begin, ch.pairs,
+                                         p.has_perm, raw, d_dst, ds, compute_, sms_);
   }
   TRIMS_CUDA(cudaEventRecord(t1_, copy_));
   TRIMS_CUDA(cudaEventRecord(c1_, compute_));
@@ -170,12 +168,11 @@ uint64_t Ingestor::from_host(const uint8_t* host_blob, const fmt::Manifest& src,
   return total;
 }
 
-uint64_t Ingestor::from_file(int fd, uint64_t blob_file_off, const fmt::Manifest& src, const fmt::Manifest& dst,
-                             bool identity, uint8_t* d_dst, std::vector<uint64_t>* buckets, IngestStats* st) {
+uint64_t Ingestor::from_file(const IngestPlan& ip, int fd, uint64_t blob_file_off, uint8_t* d_dst,
+                             std::vector<uint64_t>* buckets, IngestStats* st) {
   std::lock_guard lk(mu_);
   DeviceGuard g(device_);
-  const ingest::Tile* d_tiles = nullptr;
-  const ingest::TilePlan& p = plan_for(src, dst, identity, &d_tiles);
+  const ingest::TilePlan& p = ip.plan;
   uint64_t need = 0;
   for (const auto& ch : p.chunks) need = std::max(need, ch.src_end - ch.src_begin);
   if (need > bounce_cap_) {
@@ -189,7 +186,7 @@ uint64_t Ingestor::from_file(int fd, uint64_t blob_file_off, const fmt::Manifest
   }
   unsigned long long* ds = sums(p.buckets);
   TRIMS_CUDA(cudaMemsetAsync(ds, 0, p.buckets * sizeof(unsigned long long), compute_));
-  uint8_t* raw = identity ? d_dst : staging(src.blob_bytes);
+  uint8_t* raw = ip.identity ? d_dst : staging(ip.src.blob_bytes);
   TRIMS_CUDA(cudaEventRecord(t0_, copy_));
   double read_ms = 0;
   uint32_t launches = 0;
@@ -206,9 +203,8 @@ uint64_t Ingestor::from_file(int fd, uint64_t blob_file_off, const fmt::Manifest
     TRIMS_CUDA(cudaEventRecord(ev, copy_));
     TRIMS_CUDA(cudaEventRecord(bounce_ev_[slot], copy_));
     TRIMS_CUDA(cudaStreamWaitEvent(compute_, ev, 0));
-    ingest::launch_transform(d_tiles + ch.tile_begin, ch.tile_end - ch.tile_begin, p.has_perm, raw, d_dst, ds,
-                             compute_, sms_);
-    ++launches;
+    launches += ingest::launch_transform(ip.d_tiles + ch.tile_begin, ch.tile_end - ch.tile_begin, ch.pairs,
+                                         p.has_perm, raw, d_dst, ds, compute_, sms_);
   }
   TRIMS_CUDA(cudaEventRecord(t1_, copy_));
   TRIMS_CUDA(cudaEventRecord(c1_, compute_));
@@ -226,13 +222,11 @@ uint64_t Ingestor::from_file(int fd, uint64_t blob_file_off, const fmt::Manifest
   return total;
 }
 
-void Ingestor::from_device(const uint8_t* d_src, const fmt::Manifest& src, const fmt::Manifest& dst,
-                           bool identity, uint8_t* d_dst, unsigned long long* d_sums, cudaStream_t stream) {
-  std::lock_guard lk(mu_);
+uint32_t Ingestor::from_device(const IngestPlan& ip, const uint8_t* d_src, uint8_t* d_dst,
+                               unsigned long long* d_sums, cudaStream_t stream) {
   DeviceGuard g(device_);
-  const ingest::Tile* d_tiles = nullptr;
-  const ingest::TilePlan& p = plan_for(src, dst, identity, &d_tiles);
-  ingest::launch_transform(d_tiles, uint32_t(p.tiles.size()), p.has_perm, d_src, d_dst, d_sums, stream, sms_);
+  return ingest::launch_transform(ip.d_tiles, uint32_t(ip.plan.tiles.size()), ip.plan.pairs, ip.plan.has_perm, d_src,
+                                  d_dst, d_sums, stream, sms_);
 }
 
 // ---------------------------------------------------------------------------
@@ -322,15 +316,26 @@ const uint8_t* CudaTierBackend::host_buffer(uint64_t model_id, uint64_t* bytes) 
   return it->second.p;
 }
 
+std::shared_ptr<IngestPlan> CudaTierBackend::plan_for(uint64_t model_id, const fmt::Manifest& m) {
+  {
+    std::lock_guard lk(mu_);
+    auto it = plans_.find(model_id);
+    if (it != plans_.end()) return it->second;
+  }
+  auto p = ing_.compile(m, cfg_.plan);
+  std::lock_guard lk(mu_);
+  return plans_.emplace(model_id, std::move(p)).first->second;
+}
+
 // daemon.cpp:160-209: build, fill and seal the fast-tier segment, then
 // export it. Payload = resident blob | manifest JSON | u64 LE jlen, then the
 // 64-byte SegTail.
 FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Manifest& m, bool from_host,
                                               const std::string& path) {
   auto rec = std::make_shared<FastRecord>();
-  rec->resident = fmt::resident_manifest(m, cfg_.plan);
-  rec->json = fmt::manifest_to_json(rec->resident);
-  const bool identity = cfg_.plan.identity();
+  std::shared_ptr<IngestPlan> plan = plan_for(model_id, m);
+  rec->resident = plan->dst;
+  rec->json = plan->dst_json;
   const uint64_t rb = rec->resident.blob_bytes;
   const uint64_t payload = rb + rec->json.size() + 8;
   rec->seg = DeviceSegment::create(cfg_.device, payload + sizeof(SegTail));
@@ -345,7 +350,7 @@ FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Mani
       if (it->second.bytes != m.blob_bytes) raise(Errc::Internal, "host buffer size mismatch");
       src = it->second.p;  // single-flight pins the entry while loading
     }
-    rec->checksum = ing_.from_host(src, m, rec->resident, identity, rec->seg.ptr(), &rec->bucket_sums, &rec->stats);
+    rec->checksum = ing_.from_host(*plan, src, rec->seg.ptr(), &rec->bucket_sums, &rec->stats);
   } else {
     int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
     if (fd < 0) raise(Errc::NotFound, path);
@@ -354,8 +359,8 @@ FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Mani
       if (::pread(fd, hdr, 16, 0) != 16) raise(Errc::Corrupt, "short read on " + path);
       uint64_t mlen = 0;
       for (int i = 0; i < 8; ++i) mlen |= uint64_t(hdr[8 + i]) << (8 * i);
-      rec->checksum = ing_.from_file(fd, fmt::blob_file_offset(mlen), m, rec->resident, identity, rec->seg.ptr(),
-                                     &rec->bucket_sums, &rec->stats);
+      rec->checksum = ing_.from_file(*plan, fd, fmt::blob_file_offset(mlen), rec->seg.ptr(), &rec->bucket_sums,
+                                     &rec->stats);
     } catch (...) {
       ::close(fd);
       throw;

@@ -28,6 +28,18 @@ struct IngestStats {
   uint32_t launches{0};    // transform kernel launches
 };
 
+// A compiled ingest plan: tiles + chunks on the host, the tile table in HBM.
+// Built once per (artifact manifest, plan) and reused by every ingest of it.
+struct IngestPlan {
+  fmt::Manifest src, dst;
+  bool identity{false};
+  ingest::TilePlan plan;
+  ingest::Tile* d_tiles{nullptr};
+  int device{0};
+  std::string dst_json;
+  ~IngestPlan();
+};
+
 // One per device. Serialises its own ingests (PCIe is the shared resource).
 class Ingestor {
  public:
@@ -36,26 +48,22 @@ class Ingestor {
   int device() const { return device_; }
   int sm_count() const { return sms_; }
 
+  std::shared_ptr<IngestPlan> compile(const fmt::Manifest& src, const fmt::Plan& plan);
+
   // Raw artifact blob in host memory (pinned for full PCIe rate) -> resident
   // blob at d_dst. Returns the resident checksum; per-bucket sums optional.
-  uint64_t from_host(const uint8_t* host_blob, const fmt::Manifest& src, const fmt::Manifest& dst,
-                     bool identity, uint8_t* d_dst, std::vector<uint64_t>* buckets, IngestStats* st);
+  uint64_t from_host(const IngestPlan& p, const uint8_t* host_blob, uint8_t* d_dst, std::vector<uint64_t>* buckets,
+                     IngestStats* st);
   // Streams the blob from an artifact file through a pinned bounce ring
   // (publish_fast without host staging, daemon.cpp:184-193).
-  uint64_t from_file(int fd, uint64_t blob_file_off, const fmt::Manifest& src, const fmt::Manifest& dst,
-                     bool identity, uint8_t* d_dst, std::vector<uint64_t>* buckets, IngestStats* st);
-  // Raw blob already in HBM -> resident blob (the HBM-resident transform).
-  // Asynchronous on `stream` when sums_out == nullptr (d_sums receives the bucket sums).
-  void from_device(const uint8_t* d_src, const fmt::Manifest& src, const fmt::Manifest& dst, bool identity,
-                   uint8_t* d_dst, unsigned long long* d_sums, cudaStream_t stream);
-  const ingest::TilePlan& plan_for(const fmt::Manifest& src, const fmt::Manifest& dst, bool identity,
-                                   const ingest::Tile** d_tiles);
+  uint64_t from_file(const IngestPlan& p, int fd, uint64_t blob_file_off, uint8_t* d_dst,
+                     std::vector<uint64_t>* buckets, IngestStats* st);
+  // Raw blob already in HBM -> resident blob (the HBM-resident transform),
+  // asynchronous on `stream`; bucket sums accumulate into d_sums.
+  uint32_t from_device(const IngestPlan& p, const uint8_t* d_src, uint8_t* d_dst, unsigned long long* d_sums,
+                       cudaStream_t stream);
 
  private:
-  struct CachedPlan {
-    ingest::TilePlan plan;
-    ingest::Tile* d_tiles{nullptr};
-  };
   uint8_t* staging(uint64_t bytes);
   unsigned long long* sums(uint32_t n);
   uint64_t finish(const ingest::TilePlan& p, std::vector<uint64_t>* buckets);
@@ -73,7 +81,6 @@ class Ingestor {
   uint64_t bounce_cap_{0};
   cudaEvent_t bounce_ev_[2]{};
   std::mutex mu_;
-  std::map<std::string, std::unique_ptr<CachedPlan>> plans_;
 };
 
 struct BackendConfig {
@@ -124,12 +131,15 @@ class CudaTierBackend : public TierBackend {
   };
   void free_host(HostBuf& h);
 
+  std::shared_ptr<IngestPlan> plan_for(uint64_t model_id, const fmt::Manifest& m);
+
   BackendConfig cfg_;
   Ingestor ing_;
   std::unique_ptr<PinnedPool> pool_;
   std::mutex mu_;
   std::map<uint64_t, HostBuf> host_;
   std::map<uint64_t, std::shared_ptr<FastRecord>> fast_;
+  std::map<uint64_t, std::shared_ptr<IngestPlan>> plans_;  // model_id -> compiled plan (manifests are immutable)
   std::atomic<uint64_t> next_gen_{1};
 };
 

@@ -515,33 +515,112 @@ void trims_import_close(trims_import* im) {
 // ---------------------------------------------------------------- raw ingest
 
 namespace {
+// Raw-ingest engines live for the process: they are never destroyed at exit
+// (static destructors would run after the CUDA driver has shut down).
 std::mutex g_ing_mu;
-std::map<int, std::unique_ptr<Ingestor>> g_ing;
+std::map<int, Ingestor*>* g_ing = new std::map<int, Ingestor*>();
 Ingestor& ingestor(int device) {
   std::lock_guard lk(g_ing_mu);
-  auto& p = g_ing[device];
-  if (!p) p = std::make_unique<Ingestor>(device);
+  Ingestor*& p = (*g_ing)[device];
+  if (!p) p = new Ingestor(device);
   return *p;
 }
 }  // namespace
 
+namespace {
+// Plans compiled for the convenience (JSON-in) entry points, keyed by the
+// exact request; callers on a hot path hold a trims_plan instead.
+std::mutex g_plan_mu;
+std::map<std::string, std::shared_ptr<IngestPlan>>* g_plans = new std::map<std::string, std::shared_ptr<IngestPlan>>();
+std::shared_ptr<IngestPlan> cached_plan(int device, const char* src_json, uint32_t flags, uint32_t out_dtype) {
+  std::string key = std::to_string(device) + ":" + std::to_string(flags) + ":" + std::to_string(out_dtype) + ":" + src_json;
+  {
+    std::lock_guard lk(g_plan_mu);
+    auto it = g_plans->find(key);
+    if (it != g_plans->end()) return it->second;
+  }
+  auto p = ingestor(device).compile(fmt::manifest_from_json(src_json), make_plan(flags, out_dtype));
+  std::lock_guard lk(g_plan_mu);
+  if (g_plans->size() > 32) g_plans->clear();
+  return g_plans->emplace(std::move(key), std::move(p)).first->second;
+}
+
+void put_stats(const IngestStats& st, double* out5) {
+  if (!out5) return;
+  out5[0] = st.h2d_ms;
+  out5[1] = st.total_ms;
+  out5[2] = st.read_ms;
+  out5[3] = double(st.h2d_bytes);
+  out5[4] = st.launches;
+}
+}  // namespace
+
+struct trims_plan {
+  std::shared_ptr<IngestPlan> p;
+};
+
+int trims_plan_create(int device, const char* src_json, uint32_t plan_flags, uint32_t out_dtype, trims_plan** out) {
+  return guard([&] {
+    auto h = std::make_unique<trims_plan>();
+    h->p = ingestor(device).compile(fmt::manifest_from_json(src_json), make_plan(plan_flags, out_dtype));
+    *out = h.release();
+    return 0;
+  });
+}
+
+void trims_plan_destroy(trims_plan* p) { delete p; }
+
+int trims_plan_describe(trims_plan* p, uint64_t out8[8]) {
+  return guard([&] {
+    const auto& t = p->p->plan;
+    out8[0] = t.tiles.size();
+    out8[1] = t.buckets;
+    out8[2] = t.algo_read_bytes;
+    out8[3] = t.algo_write_bytes;
+    out8[4] = p->p->src.blob_bytes;
+    out8[5] = p->p->dst.blob_bytes;
+    out8[6] = t.chunks.size();
+    out8[7] = t.pairs;
+    return 0;
+  });
+}
+
+int trims_plan_resident_json(trims_plan* p, char* out, uint64_t cap) {
+  return guard([&] { return put(p->p->dst_json, out, cap); });
+}
+
+int trims_plan_transform(trims_plan* p, const void* dev_src, void* dev_dst, unsigned long long* d_sums, void* stream,
+                         uint32_t* launches) {
+  return guard([&] {
+    uint32_t n = ingestor(p->p->device).from_device(*p->p, static_cast<const uint8_t*>(dev_src),
+                                                    static_cast<uint8_t*>(dev_dst), d_sums,
+                                                    static_cast<cudaStream_t>(stream));
+    if (launches) *launches = n;
+    return 0;
+  });
+}
+
+int trims_plan_ingest_host(trims_plan* p, const void* host_blob, void* dev_dst, uint64_t* checksum_out,
+                           double stats_out5[5]) {
+  return guard([&] {
+    IngestStats st;
+    uint64_t c = ingestor(p->p->device).from_host(*p->p, static_cast<const uint8_t*>(host_blob),
+                                                  static_cast<uint8_t*>(dev_dst), nullptr, &st);
+    if (checksum_out) *checksum_out = c;
+    put_stats(st, stats_out5);
+    return 0;
+  });
+}
+
 int trims_ingest_host(int device, const void* host_blob, const char* src_json, uint32_t plan_flags,
                       uint32_t out_dtype, void* dev_dst, uint64_t* checksum_out, double stats_out5[5]) {
   return guard([&] {
-    fmt::Manifest src = fmt::manifest_from_json(src_json);
-    fmt::Plan plan = make_plan(plan_flags, out_dtype);
-    fmt::Manifest dst = fmt::resident_manifest(src, plan);
+    auto p = cached_plan(device, src_json, plan_flags, out_dtype);
     IngestStats st;
-    uint64_t c = ingestor(device).from_host(static_cast<const uint8_t*>(host_blob), src, dst, plan.identity(),
-                                            static_cast<uint8_t*>(dev_dst), nullptr, &st);
+    uint64_t c = ingestor(device).from_host(*p, static_cast<const uint8_t*>(host_blob), static_cast<uint8_t*>(dev_dst),
+                                            nullptr, &st);
     if (checksum_out) *checksum_out = c;
-    if (stats_out5) {
-      stats_out5[0] = st.h2d_ms;
-      stats_out5[1] = st.total_ms;
-      stats_out5[2] = st.read_ms;
-      stats_out5[3] = double(st.h2d_bytes);
-      stats_out5[4] = st.launches;
-    }
+    put_stats(st, stats_out5);
     return 0;
   });
 }
@@ -549,11 +628,9 @@ int trims_ingest_host(int device, const void* host_blob, const char* src_json, u
 int trims_transform_device(int device, const void* dev_src, const char* src_json, uint32_t plan_flags,
                            uint32_t out_dtype, void* dev_dst, unsigned long long* d_sums, void* stream) {
   return guard([&] {
-    fmt::Manifest src = fmt::manifest_from_json(src_json);
-    fmt::Plan plan = make_plan(plan_flags, out_dtype);
-    fmt::Manifest dst = fmt::resident_manifest(src, plan);
-    ingestor(device).from_device(static_cast<const uint8_t*>(dev_src), src, dst, plan.identity(),
-                                 static_cast<uint8_t*>(dev_dst), d_sums, static_cast<cudaStream_t>(stream));
+    auto p = cached_plan(device, src_json, plan_flags, out_dtype);
+    ingestor(device).from_device(*p, static_cast<const uint8_t*>(dev_src), static_cast<uint8_t*>(dev_dst), d_sums,
+                                 static_cast<cudaStream_t>(stream));
     return 0;
   });
 }

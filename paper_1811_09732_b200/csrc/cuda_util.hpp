@@ -21,11 +21,19 @@
 namespace trims {
 
 // RAII device guard: the C-ABI may be entered from any host thread.
+// nothrow=true for destructors (teardown may run after driver shutdown).
 struct DeviceGuard {
   int prev{-1};
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) TRIMS_CUDA(cudaSetDevice(dev));
+  explicit DeviceGuard(int dev, bool nothrow = false) {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      cudaGetLastError();
+      prev = -1;
+    }
+    if (prev != dev) {
+      cudaError_t e = cudaSetDevice(dev);
+      if (e != cudaSuccess && !nothrow) TRIMS_CUDA(e);
+      if (e != cudaSuccess) cudaGetLastError();
+    }
   }
   ~DeviceGuard() {
     int cur = -1;

@@ -20,7 +20,8 @@ constexpr uint64_t kGold = 0x9e3779b97f4a7c15ull;
 constexpr int kThreads = 256;
 constexpr uint32_t kElemTile = 8192;          // elements per OP_CVT tile
 constexpr uint32_t kHashTile = 64u << 10;     // bytes per OP_HASH tile
-constexpr uint32_t kPermSmem = 48u << 10;     // smem budget of one OP_PERM tile
+constexpr uint32_t kPermSmem = 24u << 10;     // smem budget of one OP_PERM tile (8 CTAs/SM fit)
+constexpr int kUnroll = 4;                    // 128-bit loads in flight per thread
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -169,23 +170,33 @@ __device__ uint64_t tile_cvt(const Tile& t, const uint8_t* src, uint8_t* dst) {
   const uint64_t gw0 = t.dst_off >> 3;
   const uint32_t words = t.dst_bytes >> 3, n = t.n_elem;
   uint64_t acc = 0;
-  for (uint32_t w = threadIdx.x; w < words; w += kThreads) {
-    const uint32_t e0 = w * EPW;
-    uint64_t word = 0;
-    if (e0 + EPW <= n) {
-      ST v[EPW];
-      load_vec<ST, EPW>(s + uint64_t(e0) * SS, v);
+  // kUnroll independent 128-bit loads in flight per thread before any use.
+  for (uint32_t base = threadIdx.x; base < words; base += kThreads * kUnroll) {
+    ST v[kUnroll][EPW];
 #pragma unroll
-      for (int q = 0; q < EPW; ++q) word |= uint64_t(cvt<S, D>(v[q])) << (8 * DS * q);
-    } else if (e0 < n) {
-      for (int q = 0; q < EPW && e0 + q < n; ++q) {
-        ST x;
-        memcpy(&x, s + uint64_t(e0 + q) * SS, SS);
-        word |= uint64_t(cvt<S, D>(x)) << (8 * DS * q);
-      }
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t e0 = (base + u * kThreads) * EPW;
+      if (e0 + EPW <= n) load_vec<ST, EPW>(s + uint64_t(e0) * SS, v[u]);
     }
-    d[w] = word;
-    acc += word_hash(word, gw0 + w);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t w = base + u * kThreads;
+      if (w >= words) break;
+      const uint32_t e0 = w * EPW;
+      uint64_t word = 0;
+      if (e0 + EPW <= n) {
+#pragma unroll
+        for (int q = 0; q < EPW; ++q) word |= uint64_t(cvt<S, D>(v[u][q])) << (8 * DS * q);
+      } else if (e0 < n) {
+        for (int q = 0; q < EPW && e0 + q < n; ++q) {
+          ST x;
+          memcpy(&x, s + uint64_t(e0 + q) * SS, SS);
+          word |= uint64_t(cvt<S, D>(x)) << (8 * DS * q);
+        }
+      }
+      d[w] = word;
+      acc += word_hash(word, gw0 + w);
+    }
   }
   return acc;
 }
@@ -199,25 +210,70 @@ __device__ uint64_t tile_perm(const Tile& t, const uint8_t* src, uint8_t* dst, u
   const uint8_t* s = src + t.src_off;
   DT* sm = reinterpret_cast<DT*>(smem);
   const uint32_t n = t.n_elem, C = t.C, RS = t.RS, CRS = C * RS;
+  const bool gather = t.pad_ != 0;  // slice too large for smem: read the source directly
   // phase 1: coalesced vector loads in source order -> converted in smem
-  const uint32_t groups = n / EPW;
-  for (uint32_t g = threadIdx.x; g < groups; g += kThreads) {
-    ST v[EPW];
-    load_vec<ST, EPW>(s + uint64_t(g) * EPW * SS, v);
+  const uint32_t groups = gather ? 0 : n / EPW;
+  for (uint32_t base = threadIdx.x; base < groups; base += kThreads * kUnroll) {
+    ST v[kUnroll][EPW];
 #pragma unroll
-    for (int q = 0; q < EPW; ++q) sm[g * EPW + q] = cvt<S, D>(v[q]);
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t g = base + u * kThreads;
+      if (g < groups) load_vec<ST, EPW>(s + uint64_t(g) * EPW * SS, v[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t g = base + u * kThreads;
+      if (g < groups) {  // one packed 8-byte shared store per group
+        uint64_t word = 0;
+#pragma unroll
+        for (int q = 0; q < EPW; ++q) word |= uint64_t(cvt<S, D>(v[u][q])) << (8 * DS * q);
+        reinterpret_cast<uint64_t*>(sm)[g] = word;
+      }
+    }
   }
-  for (uint32_t e = groups * EPW + threadIdx.x; e < n; e += kThreads) {
+  for (uint32_t e = groups * EPW + threadIdx.x; !gather && e < n; e += kThreads) {
     ST x;
     memcpy(&x, s + uint64_t(e) * SS, SS);
     sm[e] = cvt<S, D>(x);
   }
   __syncthreads();
-  // phase 2: resident order o = (k*RS + rs)*C + c; one word per thread step
+  auto elem = [&](uint32_t i) -> DT {
+    if (!gather) return sm[i];
+    ST x;
+    memcpy(&x, s + uint64_t(i) * SS, SS);
+    return cvt<S, D>(x);
+  };
+  // phase 2: resident order o = (k*RS + rs)*C + c
   uint64_t* d = reinterpret_cast<uint64_t*>(dst + t.dst_off);
   const uint64_t gw0 = t.dst_off >> 3;
   const uint32_t words = t.dst_bytes >> 3;
   uint64_t acc = 0;
+  if (!gather && (C * DS) % 8 == 0) {
+    // Row path: one warp per output row (k, rs) of C contiguous elements, so
+    // the only division is per row; lanes write consecutive words.
+    const uint32_t wpr = C / EPW, rows = (n / CRS) * RS;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (uint32_t row = warp; row < rows; row += kThreads / 32) {
+      const uint32_t k = row / RS, rs = row - k * RS;
+      const DT* col = sm + k * CRS + rs;
+      uint64_t* drow = d + uint64_t(row) * wpr;
+      const uint64_t gwr = gw0 + uint64_t(row) * wpr;
+      for (uint32_t wi = lane; wi < wpr; wi += 32) {
+        const DT* e = col + wi * EPW * RS;
+        uint64_t word = 0;
+#pragma unroll
+        for (int q = 0; q < EPW; ++q) word |= uint64_t(e[q * RS]) << (8 * DS * q);
+        drow[wi] = word;
+        acc += word_hash(word, gwr + wi);
+      }
+    }
+    for (uint32_t w = n * DS / 8 + threadIdx.x; w < words; w += kThreads) {  // trailing pad
+      d[w] = 0;
+      acc += word_hash(0, gw0 + w);
+    }
+    __syncthreads();  // smem reuse by the next tile
+    return acc;
+  }
   for (uint32_t w = threadIdx.x; w < words; w += kThreads) {
     uint32_t o = w * EPW;
     uint64_t word = 0;
@@ -225,7 +281,7 @@ __device__ uint64_t tile_perm(const Tile& t, const uint8_t* src, uint8_t* dst, u
       uint32_t k = o / CRS, rem = o - k * CRS, rs = rem / C, c = rem - rs * C;
 #pragma unroll
       for (int q = 0; q < EPW; ++q) {
-        if (o + q < n) word |= uint64_t(sm[k * CRS + c * RS + rs]) << (8 * DS * q);
+        if (o + q < n) word |= uint64_t(elem(k * CRS + c * RS + rs)) << (8 * DS * q);
         if (++c == C) {
           c = 0;
           if (++rs == RS) {
@@ -242,30 +298,10 @@ __device__ uint64_t tile_perm(const Tile& t, const uint8_t* src, uint8_t* dst, u
   return acc;
 }
 
+// One specialisation per (source dtype, resident dtype) pair keeps register
+// pressure at what that pair needs; tiles of other pairs in the same range are
+// skipped (the host launches one kernel per pair present, usually exactly one).
 template <int S, int D>
-__device__ uint64_t dispatch_op(const Tile& t, const uint8_t* src, uint8_t* dst, uint8_t* smem) {
-  return t.op == OP_PERM ? tile_perm<S, D>(t, src, dst, smem) : tile_cvt<S, D>(t, src, dst);
-}
-
-__device__ uint64_t run_tile(const Tile& t, const uint8_t* src, uint8_t* dst, uint8_t* smem) {
-  if (t.op == OP_HASH) return tile_hash(t, dst);
-  const int pair = t.sdt * 8 + t.ddt;
-  switch (pair) {
-    case 0 * 8 + 0: return dispatch_op<0, 0>(t, src, dst, smem);
-    case 1 * 8 + 1: return dispatch_op<1, 1>(t, src, dst, smem);
-    case 2 * 8 + 2: return dispatch_op<2, 2>(t, src, dst, smem);
-    case 3 * 8 + 3: return dispatch_op<3, 3>(t, src, dst, smem);
-    case 4 * 8 + 4: return dispatch_op<4, 4>(t, src, dst, smem);
-    case 1 * 8 + 4: return dispatch_op<1, 4>(t, src, dst, smem);
-    case 0 * 8 + 1: return dispatch_op<0, 1>(t, src, dst, smem);
-    case 0 * 8 + 4: return dispatch_op<0, 4>(t, src, dst, smem);
-    case 2 * 8 + 1: return dispatch_op<2, 1>(t, src, dst, smem);
-    case 2 * 8 + 4: return dispatch_op<2, 4>(t, src, dst, smem);
-    case 4 * 8 + 1: return dispatch_op<4, 1>(t, src, dst, smem);
-    default: return 0;
-  }
-}
-
 __global__ void __launch_bounds__(kThreads) transform_kernel(const Tile* __restrict__ tiles, uint32_t ntiles,
                                                              const uint8_t* __restrict__ src,
                                                              uint8_t* __restrict__ dst,
@@ -274,9 +310,41 @@ __global__ void __launch_bounds__(kThreads) transform_kernel(const Tile* __restr
   __shared__ unsigned long long red[kThreads / 32];
   for (uint32_t i = blockIdx.x; i < ntiles; i += gridDim.x) {
     const Tile t = tiles[i];
-    uint64_t acc = run_tile(t, src, dst, smem);
+    if (t.op == OP_HASH || t.sdt != S || t.ddt != D) continue;  // block-uniform
+    uint64_t acc = t.op == OP_PERM ? tile_perm<S, D>(t, src, dst, smem) : tile_cvt<S, D>(t, src, dst);
     acc = block_sum(acc, red);
     if (threadIdx.x == 0) atomicAdd(&sums[t.tensor], (unsigned long long)acc);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) hash_tiles_kernel(const Tile* __restrict__ tiles, uint32_t ntiles,
+                                                              const uint8_t* __restrict__ dst,
+                                                              unsigned long long* __restrict__ sums) {
+  __shared__ unsigned long long red[kThreads / 32];
+  for (uint32_t i = blockIdx.x; i < ntiles; i += gridDim.x) {
+    const Tile t = tiles[i];
+    if (t.op != OP_HASH) continue;
+    uint64_t acc = block_sum(tile_hash(t, dst), red);
+    if (threadIdx.x == 0) atomicAdd(&sums[t.tensor], (unsigned long long)acc);
+  }
+}
+
+using TransformFn = void (*)(const Tile*, uint32_t, const uint8_t*, uint8_t*, unsigned long long*);
+
+TransformFn pair_kernel(int s, int d) {
+  switch (s * 8 + d) {
+    case 0 * 8 + 0: return transform_kernel<0, 0>;
+    case 1 * 8 + 1: return transform_kernel<1, 1>;
+    case 2 * 8 + 2: return transform_kernel<2, 2>;
+    case 3 * 8 + 3: return transform_kernel<3, 3>;
+    case 4 * 8 + 4: return transform_kernel<4, 4>;
+    case 1 * 8 + 4: return transform_kernel<1, 4>;
+    case 0 * 8 + 1: return transform_kernel<0, 1>;
+    case 0 * 8 + 4: return transform_kernel<0, 4>;
+    case 2 * 8 + 1: return transform_kernel<2, 1>;
+    case 2 * 8 + 4: return transform_kernel<2, 4>;
+    case 4 * 8 + 1: return transform_kernel<4, 1>;
+    default: return nullptr;
   }
 }
 
@@ -367,14 +435,16 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
       const uint64_t ss = fmt::element_size(s.dtype), ds = fmt::element_size(d.dtype);
       const uint64_t n = s.nbytes / ss, end = extent_end(i);
       p.algo_read_bytes += s.nbytes;
-      const bool perm = d.layout == fmt::Layout::KRSC && s.layout == fmt::Layout::Native;
+      // 1x1 kernels: KCRS and KRSC are the same byte order -> elementwise tile.
+      const bool perm = d.layout == fmt::Layout::KRSC && s.layout == fmt::Layout::Native &&
+                        s.dims[2] * s.dims[3] > 1;
       if (perm) {
         const uint64_t K = s.dims[0], C = s.dims[1], RS = s.dims[2] * s.dims[3], CRS = C * RS;
         uint64_t g = 1;
         while ((g * CRS * ds) % 8) ++g;
-        if (g * CRS * ds > kPermSmem)
-          raise(Errc::InvalidArgument, "conv slice " + s.name + " exceeds the permute tile budget");
-        while (2 * g * CRS * ds <= kPermSmem / 2 && g * 2 <= K) g *= 2;
+        // slices too large for shared memory are gathered straight from HBM
+        const bool gather = g * CRS * ds > kPermSmem;
+        while (!gather && 2 * g * CRS * ds <= kPermSmem && g * 2 <= K) g *= 2;
         p.has_perm = true;
         for (uint64_t k0 = 0; k0 < K; k0 += g) {
           uint64_t kn = std::min(g, K - k0);
@@ -389,6 +459,7 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
           t.ddt = uint8_t(d.dtype);
           t.C = uint32_t(C);
           t.RS = uint32_t(RS);
+          t.pad_ = gather ? 1 : 0;
           p.tiles.push_back(t);
         }
       } else {
@@ -415,33 +486,44 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
     uint64_t ss = fmt::element_size(fmt::DType(t.sdt));
     return t.src_off + uint64_t(t.n_elem) * ss;
   };
+  auto pair_bit = [](const Tile& t) { return t.op == OP_HASH ? kHashPairBit : 1ull << (t.sdt * 8 + t.ddt); };
   uint32_t b = 0;
   while (b < p.tiles.size()) {
-    uint64_t s0 = p.tiles[b].src_off, s1 = src_end(p.tiles[b]);
+    uint64_t s0 = p.tiles[b].src_off, s1 = src_end(p.tiles[b]), pairs = pair_bit(p.tiles[b]);
     uint32_t e = b + 1;
     while (e < p.tiles.size() && s1 - s0 < chunk_bytes) {
       s1 = std::max(s1, src_end(p.tiles[e]));
+      pairs |= pair_bit(p.tiles[e]);
       ++e;
     }
-    p.chunks.push_back({b, e, s0, s1});
+    p.chunks.push_back({b, e, s0, s1, pairs});
+    p.pairs |= pairs;
     b = e;
   }
   return p;
 }
 
-void launch_transform(const Tile* d_tiles, uint32_t ntiles, bool has_perm, const uint8_t* src, uint8_t* dst,
-                      unsigned long long* d_sums, cudaStream_t stream, int sm_count) {
-  if (!ntiles) return;
-  const size_t smem = has_perm ? kPermSmem : 0;
-  static bool attr_set = false;
-  if (has_perm && !attr_set) {
-    TRIMS_CUDA(cudaFuncSetAttribute(transform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPermSmem)));
-    attr_set = true;
+uint32_t launch_transform(const Tile* d_tiles, uint32_t ntiles, uint64_t pairs, bool has_perm, const uint8_t* src,
+                          uint8_t* dst, unsigned long long* d_sums, cudaStream_t stream, int sm_count) {
+  if (!ntiles) return 0;
+  const uint32_t grid = std::min<uint32_t>(ntiles, uint32_t(sm_count * 8));
+  uint32_t launches = 0;
+  if (pairs & kHashPairBit) {
+    hash_tiles_kernel<<<grid, kThreads, 0, stream>>>(d_tiles, ntiles, dst, d_sums);
+    TRIMS_CUDA(cudaGetLastError());
+    ++launches;
   }
-  const int per_sm = has_perm ? 4 : 8;
-  const uint32_t grid = std::min<uint32_t>(ntiles, uint32_t(sm_count * per_sm));
-  transform_kernel<<<grid, kThreads, smem, stream>>>(d_tiles, ntiles, src, dst, d_sums);
-  TRIMS_CUDA(cudaGetLastError());
+  for (int bit = 0; bit < 64; ++bit) {
+    if (bit == 63 || !(pairs & (1ull << bit))) continue;
+    TransformFn fn = pair_kernel(bit / 8, bit % 8);
+    if (!fn) raise(Errc::InvalidArgument, "unsupported dtype pair in plan");
+    const size_t smem = has_perm ? kPermSmem : 0;
+    if (has_perm) TRIMS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPermSmem)));
+    fn<<<grid, kThreads, smem, stream>>>(d_tiles, ntiles, src, dst, d_sums);
+    TRIMS_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  return launches;
 }
 
 void launch_checksum(const uint8_t* p, uint64_t nbytes, uint64_t word0, unsigned long long* d_out,

@@ -36,8 +36,10 @@ struct TilePlan {
   struct Chunk {
     uint32_t tile_begin, tile_end;
     uint64_t src_begin, src_end;
+    uint64_t pairs;  // dtype pairs present (bit s*8+d), kHashPairBit for OP_HASH
   };
   std::vector<Chunk> chunks;
+  uint64_t pairs{0};
   uint32_t buckets{0};     // checksum buckets (ntensors + 1)
   bool identity{false};    // resident == source bytes: tiles only hash
   bool has_perm{false};
@@ -49,10 +51,14 @@ struct TilePlan {
 TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool identity,
                      uint64_t chunk_bytes = 16ull << 20);
 
-// Persistent tile kernel over tiles [0, ntiles) of `d_tiles` (device copy).
-// Per-bucket checksums are atomically accumulated into d_sums (mod 2^64).
-void launch_transform(const Tile* d_tiles, uint32_t ntiles, bool has_perm, const uint8_t* src,
-                      uint8_t* dst, unsigned long long* d_sums, cudaStream_t stream, int sm_count);
+inline constexpr uint64_t kHashPairBit = 1ull << 63;
+
+// Persistent tile kernels over tiles [0, ntiles) of `d_tiles` (device copy):
+// one launch per dtype pair in `pairs` (+ one hash launch). Per-bucket
+// checksums are atomically accumulated into d_sums (mod 2^64). Returns the
+// number of kernel launches issued.
+uint32_t launch_transform(const Tile* d_tiles, uint32_t ntiles, uint64_t pairs, bool has_perm, const uint8_t* src,
+                          uint8_t* dst, unsigned long long* d_sums, cudaStream_t stream, int sm_count);
 
 // Checksum of an arbitrary device range (word0 = global index of its first word).
 void launch_checksum(const uint8_t* p, uint64_t nbytes, uint64_t word0, unsigned long long* d_out,

@@ -1,0 +1,39 @@
+"""Runs only the HBM-resident transform (for ncu / quick timing):
+    python scripts/prof_transform.py [arch] [reps] [plan_flags]"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_1811_09732_b200 import catalog as C
+from paper_1811_09732_b200.ingest import IngestPlan
+
+arch = sys.argv[1] if len(sys.argv) > 1 else "resnet50"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+flags = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+src_json, blob = C.arch_blob(C.ARCHS[arch](), seed=1)
+plan = IngestPlan(src_json, flags, "bf16")
+d_src = torch.from_numpy(blob).cuda()
+d_dst = torch.empty(plan.resident_bytes, dtype=torch.uint8, device="cuda")
+d_sums = torch.zeros(plan.buckets, dtype=torch.int64, device="cuda")
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+s = torch.cuda.current_stream()
+for i in range(reps):
+    d_sums.zero_()
+    plan.transform(d_src.data_ptr(), d_dst.data_ptr(), d_sums.data_ptr(), s.cuda_stream)
+torch.cuda.synchronize()
+tot = 0.0
+for i in range(10):
+    flush.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    plan.transform(d_src.data_ptr(), d_dst.data_ptr(), d_sums.data_ptr(), s.cuda_stream)
+    e1.record()
+    torch.cuda.synchronize()
+    tot += e0.elapsed_time(e1)
+ms = tot / 10
+print(json.dumps({"arch": arch, "flags": flags, "tiles": plan.tiles, "ms": round(ms, 4),
+                  "GBps_algo": round((plan.read_bytes + plan.write_bytes) / ms / 1e6, 1),
+                  "GBps_src": round(plan.src_bytes / ms / 1e6, 1)}))

@@ -70,7 +70,7 @@ def test_dtype_matrix_with_special_values(torch, flags, out_dtype):
     specials64 = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, -np.nan, 1e-310, -1e-310, 1e300, -1e300,
                            3.4e38, 3.5e38, 1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8, 2 ** -133, 2 ** -134, 5e-324], np.float64)
     nan_payload = np.array([0x7ff0000000000001, 0xfff4000000000000], np.uint64).view(np.float64)
-    x64 = np.concatenate([specials64, nan_payload, rng.standard_normal(997) * 10 ** rng.integers(-40, 40, 997)])
+    x64 = np.concatenate([specials64, nan_payload, rng.standard_normal(997) * 10.0 ** rng.integers(-40, 40, 997)])
     x32 = np.concatenate([specials64.astype(np.float32), rng.standard_normal(1003).astype(np.float32)])
     x16 = np.concatenate([np.array([0, 0x8000, 0x7c00, 0xfc00, 0x7e01, 0x0001, 0x03ff, 0x8001], np.uint16),
                           rng.integers(0, 65536, 995, dtype=np.uint16)])

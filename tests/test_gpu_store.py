@@ -112,7 +112,7 @@ def test_converting_store_bit_exact_and_import_path(tmp_path):
                         convert_to="bf16", permute_4d=True)
     with Store(opts) as s:
         k = C.arch_key(arch)
-        direct = Client(s)
+        direct = Client(s, model_dirs=[d])
         via_fd = Client(s, attach_via_import=True)
         a = direct.open(k, force_shared=True)
         b = via_fd.open(k, force_shared=True)
