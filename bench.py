@@ -280,6 +280,7 @@ def store_latencies(work: str, arch, dev: int) -> dict:
             cli.close(v)
         out["warm_open_host_resident"] = round(statistics.median(ts[1:]), 3)
         out["hot_open_hbm_resident"] = round(statistics.median(hs[1:]), 4)
+        out["last_publish_breakdown_ms"] = {k: round(x, 3) for k, x in s.ingest_stats(v.model_id).items()}
     return out
 
 

@@ -149,8 +149,9 @@ int trims_store_drop_all(trims_store* s);
 int trims_store_stats_json(trims_store* s, char* out, uint64_t cap);
 /* The resident manifest JSON of a fast-resident model. */
 int trims_store_resident_json(trims_store* s, uint64_t model_id, char* out, uint64_t cap);
-/* Last ingest of a model: h2d_ms, total_ms, read_ms, h2d_bytes, launches. */
-int trims_store_ingest_stats(trims_store* s, uint64_t model_id, double out5[5]);
+/* Last ingest of a model: h2d_ms, total_ms, read_ms, h2d_bytes, launches,
+ * segment alloc_ms (cuMem create/map/export), seal_ms (tail + digest). */
+int trims_store_ingest_stats(trims_store* s, uint64_t model_id, double out7[7]);
 /* Per-tensor block checksums of a resident model (buckets = tensors + 1). */
 int trims_store_checksums(trims_store* s, uint64_t model_id, uint64_t* out, uint64_t cap, uint64_t* n);
 
@@ -186,7 +187,8 @@ int trims_transform_device(int device, const void* dev_src, const char* src_json
 typedef struct trims_plan trims_plan;
 int trims_plan_create(int device, const char* src_json, uint32_t plan_flags, uint32_t out_dtype, trims_plan** out);
 void trims_plan_destroy(trims_plan* p);
-/* tiles, buckets, algo read bytes, algo write bytes, src blob, resident blob, chunks, dtype-pair mask */
+/* tiles, buckets, algo read bytes, algo write bytes, src blob, resident blob, chunks,
+ * kernel launches per HBM-resident transform */
 int trims_plan_describe(trims_plan* p, uint64_t out8[8]);
 int trims_plan_resident_json(trims_plan* p, char* out, uint64_t cap);
 int trims_plan_transform(trims_plan* p, const void* dev_src, void* dev_dst, unsigned long long* d_sums, void* stream,

@@ -168,7 +168,7 @@ def check(rc: int) -> None:
         raise TrimsError(rc, lib.trims_errc_name(rc).decode(), lib.trims_last_error().decode())
 
 
-def text_call(fn, *args, cap: int = 1 << 20) -> str:
+def text_call(fn, *args, cap: int = 1 << 16) -> str:
     """Call an entry point whose last two args are (char* out, uint64 cap)."""
     while True:
         buf = ctypes.create_string_buffer(cap)

@@ -126,8 +126,8 @@ class ImportCache:
         self._maps[(token, generation)] = entry
 
     def clear(self):
-        for imp, _, _ in self._maps.values():
-            lib.trims_import_close(imp)
+        for entry in self._maps.values():
+            lib.trims_import_close(entry[0])
         self._maps.clear()
 
 
@@ -164,6 +164,7 @@ class Client:
         self.plan_flags = plan_flags if plan_flags is not None else (opts.plan_flags if opts else 0)
         self.out_dtype = out_dtype or (opts.convert_to if opts and opts.convert_to else "bf16")
         self.imports = ImportCache()
+        self._local = {}  # (model_id, generation) -> (resident json, digest, tensor views)
 
     # client.cpp:94-106
     def resolve_local(self, key: F.ModelKey, local_path: str | None = None) -> str | None:
@@ -219,26 +220,36 @@ class Client:
         t1 = time.perf_counter()
         token = ex.token.decode() if isinstance(ex.token, bytes) else ex.token
         remote = getattr(ex, "remote", False)
+        digest = bytes(ex.manifest_digest)
         if remote or self.attach_via_import:
             hit = self.imports.get(token, ex.generation)
             if hit is None:
                 fd = ex.fd if remote else os.dup(ex.fd)
                 try:
                     imp, ptr, mjson = import_segment(ex.device, fd, ex.alloc_bytes, ex.generation, ex.payload_bytes,
-                                                     bytes(ex.manifest_digest))
+                                                     digest)
                 finally:
                     os.close(fd)
-                hit = (imp, ptr, mjson)
+                hit = (imp, ptr, mjson, digest, slice_tensors(mjson, ptr))
                 self.imports.put(token, ex.generation, hit)
             elif remote and ex.fd >= 0:
                 os.close(ex.fd)
-            _, base, mjson = hit
+            _, base, mjson, seen, tensors = hit
         else:
+            # same process: the segment is already mapped; the manifest is
+            # fetched, digest-checked and sliced once per (model, generation)
             base = int(ex.dev_ptr)
-            mjson = self.store.resident_manifest(ex.model_id)
-            if F.sha256(mjson.encode()) != bytes(ex.manifest_digest):
-                raise TrimsError(Errc.Corrupt, "Corrupt", "manifest digest mismatch on attach")
-        view = ModelView(key, SHARED, "none", mjson, base, slice_tensors(mjson, base), ex.model_id, ex.generation,
+            hit = self._local.get((ex.model_id, ex.generation))
+            if hit is None:
+                mjson = self.store.resident_manifest(ex.model_id)
+                if F.sha256(mjson.encode()) != digest:
+                    raise TrimsError(Errc.Corrupt, "Corrupt", "manifest digest mismatch on attach")
+                hit = (mjson, digest, slice_tensors(mjson, base))
+                self._local[(ex.model_id, ex.generation)] = hit
+            mjson, seen, tensors = hit
+        if seen != digest:
+            raise TrimsError(Errc.Corrupt, "Corrupt", "manifest digest mismatch on attach")
+        view = ModelView(key, SHARED, "none", mjson, base, list(tensors), ex.model_id, ex.generation,
                          outcome=_outcome(ex.outcome), export=ex)
         view.timings.rpc_s = t1 - t0
         view.timings.attach_s = time.perf_counter() - t1

@@ -99,9 +99,10 @@ unsigned long long* Ingestor::sums(uint32_t n) {
 }
 
 IngestPlan::~IngestPlan() {
-  if (d_tiles) {
+  if (d_tiles || d_tiles_k) {
     DeviceGuard g(device, /*nothrow=*/true);
-    cudaFree(d_tiles);
+    if (d_tiles) cudaFree(d_tiles);
+    if (d_tiles_k) cudaFree(d_tiles_k);
   }
 }
 
@@ -119,6 +120,8 @@ std::shared_ptr<IngestPlan> Ingestor::compile(const fmt::Manifest& src, const fm
     const size_t bytes = p->plan.tiles.size() * sizeof(ingest::Tile);
     TRIMS_CUDA(cudaMalloc(&p->d_tiles, bytes));
     TRIMS_CUDA(cudaMemcpy(p->d_tiles, p->plan.tiles.data(), bytes, cudaMemcpyHostToDevice));
+    TRIMS_CUDA(cudaMalloc(&p->d_tiles_k, bytes));
+    TRIMS_CUDA(cudaMemcpy(p->d_tiles_k, p->plan.tiles_by_kernel.data(), bytes, cudaMemcpyHostToDevice));
   }
   return p;
 }
@@ -150,8 +153,7 @@ uint64_t Ingestor::from_host(const IngestPlan& ip, const uint8_t* host_blob, uin
                                cudaMemcpyHostToDevice, copy_));
     TRIMS_CUDA(cudaEventRecord(ev, copy_));
     TRIMS_CUDA(cudaStreamWaitEvent(compute_, ev, 0));
-    launches += ingest::launch_transform(ip.d_tiles + ch.tile_begin, ch.tile_end - ch.tile_begin, ch.pairs,
-                                         p.has_perm, raw, d_dst, ds, compute_, sms_);
+    launches += ingest::launch_groups(ip.d_tiles, ch.groups, raw, d_dst, ds, compute_, sms_);
   }
   TRIMS_CUDA(cudaEventRecord(t1_, copy_));
   TRIMS_CUDA(cudaEventRecord(c1_, compute_));
@@ -203,8 +205,7 @@ uint64_t Ingestor::from_file(const IngestPlan& ip, int fd, uint64_t blob_file_of
     TRIMS_CUDA(cudaEventRecord(ev, copy_));
     TRIMS_CUDA(cudaEventRecord(bounce_ev_[slot], copy_));
     TRIMS_CUDA(cudaStreamWaitEvent(compute_, ev, 0));
-    launches += ingest::launch_transform(ip.d_tiles + ch.tile_begin, ch.tile_end - ch.tile_begin, ch.pairs,
-                                         p.has_perm, raw, d_dst, ds, compute_, sms_);
+    launches += ingest::launch_groups(ip.d_tiles, ch.groups, raw, d_dst, ds, compute_, sms_);
   }
   TRIMS_CUDA(cudaEventRecord(t1_, copy_));
   TRIMS_CUDA(cudaEventRecord(c1_, compute_));
@@ -225,7 +226,7 @@ uint64_t Ingestor::from_file(const IngestPlan& ip, int fd, uint64_t blob_file_of
 uint32_t Ingestor::from_device(const IngestPlan& ip, const uint8_t* d_src, uint8_t* d_dst,
                                unsigned long long* d_sums, cudaStream_t stream) {
   DeviceGuard g(device_);
-  return ingest::launch_transform(ip.d_tiles, uint32_t(ip.plan.tiles.size()), ip.plan.pairs, ip.plan.has_perm, d_src,
+  return ingest::launch_groups(ip.d_tiles_k, ip.plan.groups, d_src,
                                   d_dst, d_sums, stream, sms_);
 }
 
@@ -338,7 +339,9 @@ FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Mani
   rec->json = plan->dst_json;
   const uint64_t rb = rec->resident.blob_bytes;
   const uint64_t payload = rb + rec->json.size() + 8;
+  auto a0 = std::chrono::steady_clock::now();
   rec->seg = DeviceSegment::create(cfg_.device, payload + sizeof(SegTail));
+  const double alloc_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a0).count();
   rec->generation = next_gen_.fetch_add(1);
 
   if (from_host) {
@@ -369,6 +372,7 @@ FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Mani
   }
 
   // Tail: JSON, its length, the sealed SegTail.
+  auto s0 = std::chrono::steady_clock::now();
   std::vector<uint8_t> tail(rec->json.size() + 8 + sizeof(SegTail));
   std::memcpy(tail.data(), rec->json.data(), rec->json.size());
   uint64_t jlen = rec->json.size();
@@ -400,6 +404,8 @@ FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Mani
   es.ingest_checksum = rec->checksum;
   pub.segments.push_back(es);
   pub.manifest_digest = Sha256::of(rec->json.data(), rec->json.size());
+  rec->stats.alloc_ms = alloc_ms;
+  rec->stats.seal_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - s0).count();
   std::lock_guard lk(mu_);
   fast_[model_id] = std::move(rec);
   return pub;

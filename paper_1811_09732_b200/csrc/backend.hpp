@@ -26,6 +26,8 @@ struct IngestStats {
   double read_ms{0};       // host file reads (from_file only)
   uint64_t h2d_bytes{0};
   uint32_t launches{0};    // transform kernel launches
+  double alloc_ms{0};      // publish_fast: cuMem create/map/export of the segment
+  double seal_ms{0};       // publish_fast: tail (JSON + SegTail) write + digest
 };
 
 // A compiled ingest plan: tiles + chunks on the host, the tile table in HBM.
@@ -34,7 +36,8 @@ struct IngestPlan {
   fmt::Manifest src, dst;
   bool identity{false};
   ingest::TilePlan plan;
-  ingest::Tile* d_tiles{nullptr};
+  ingest::Tile* d_tiles{nullptr};    // chunk-major table (pipelined H2D ingest)
+  ingest::Tile* d_tiles_k{nullptr};  // kernel-grouped table (HBM-resident transform)
   int device{0};
   std::string dst_json;
   ~IngestPlan();

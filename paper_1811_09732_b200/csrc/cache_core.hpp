@@ -98,7 +98,7 @@ class TierBackend {
 struct PlacementResult {
   Outcome outcome{Outcome::FastHit};
   uint64_t model_id{0};
-  fmt::Manifest manifest;  // artifact manifest
+  std::shared_ptr<const fmt::Manifest> manifest;  // artifact manifest (shared, immutable)
   uint64_t weights_bytes{0}, workspace_bytes{0};
   std::vector<ExportedSegment> segments;
   std::vector<ObjectSpan> layout;
@@ -156,7 +156,7 @@ class CacheCore {
   struct Entry {
     fmt::ModelKey key;
     uint64_t model_id{0}, seq{0};
-    std::optional<fmt::Manifest> manifest;
+    std::shared_ptr<const fmt::Manifest> manifest;
     uint32_t refcount{0};
     uint64_t last_access{0}, use_count{0};
     bool in_fast{false}, in_host{false}, on_disk{false}, loading{false};

@@ -341,11 +341,12 @@ int trims_store_open(trims_store* s, const char* ns, const char* name, const cha
       out->fd = es.fd;
       std::snprintf(out->token, sizeof out->token, "%s", es.token.c_str());
     }
-    // objects of the resident blob at the requested granularity
-    if (auto rec = s->be->fast_record(r.model_id))
-      out->n_objects = uint32_t(layout_for(rec->resident, {GranKind(gran_kind), block_bytes}).size());
-    else
-      out->n_objects = uint32_t(r.layout.size());
+    // objects of the resident blob at the requested granularity (count only)
+    const uint64_t rbb = out->resident_blob_bytes;
+    if (rbb == 0) out->n_objects = 1;
+    else if (gran_kind == 0) out->n_objects = 1;
+    else if (gran_kind == 1) out->n_objects = uint32_t(r.manifest->tensors.size());
+    else out->n_objects = uint32_t((rbb + block_bytes - 1) / block_bytes);
     return 0;
   });
 }
@@ -417,7 +418,8 @@ int trims_store_resident_json(trims_store* s, uint64_t model_id, char* out, uint
   });
 }
 
-int trims_store_ingest_stats(trims_store* s, uint64_t model_id, double out5[5]) {
+int trims_store_ingest_stats(trims_store* s, uint64_t model_id, double out7[7]) {
+  double* out5 = out7;
   return guard([&] {
     auto rec = s->be->fast_record(model_id);
     if (!rec) raise(Errc::NotOpen, "model not fast-resident");
@@ -426,6 +428,8 @@ int trims_store_ingest_stats(trims_store* s, uint64_t model_id, double out5[5]) 
     out5[2] = rec->stats.read_ms;
     out5[3] = double(rec->stats.h2d_bytes);
     out5[4] = rec->stats.launches;
+    out7[5] = rec->stats.alloc_ms;
+    out7[6] = rec->stats.seal_ms;
     return 0;
   });
 }
@@ -580,7 +584,7 @@ int trims_plan_describe(trims_plan* p, uint64_t out8[8]) {
     out8[4] = p->p->src.blob_bytes;
     out8[5] = p->p->dst.blob_bytes;
     out8[6] = t.chunks.size();
-    out8[7] = t.pairs;
+    out8[7] = t.groups.size();  // kernel launches of one HBM-resident transform
     return 0;
   });
 }

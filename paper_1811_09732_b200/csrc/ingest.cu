@@ -18,10 +18,12 @@ namespace {
 
 constexpr uint64_t kGold = 0x9e3779b97f4a7c15ull;
 constexpr int kThreads = 256;
-constexpr uint32_t kElemTile = 8192;          // elements per OP_CVT tile
 constexpr uint32_t kHashTile = 64u << 10;     // bytes per OP_HASH tile
-constexpr uint32_t kPermSmem = 24u << 10;     // smem budget of one OP_PERM tile (8 CTAs/SM fit)
-constexpr int kUnroll = 4;                    // 128-bit loads in flight per thread
+constexpr uint32_t kPermSmem = 24u << 10;     // smem of the direct (non-TMA) permute path
+constexpr int kUnroll = 4;                    // 128-bit loads in flight per thread (direct paths)
+constexpr int kStages = 3;                    // TMA ring depth
+constexpr uint32_t kStageBytes = 32u << 10;   // raw source bytes per staged tile
+constexpr uint32_t kStageAlloc = kStageBytes + 128;  // + 16-byte realignment slack, 128-aligned stages
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -329,7 +331,179 @@ __global__ void __launch_bounds__(kThreads) hash_tiles_kernel(const Tile* __rest
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged variant (the production path): each persistent CTA streams its
+// tiles' raw source bytes into a kStages-deep shared-memory ring with 1-D bulk
+// async copies (cp.async.bulk, mbarrier complete_tx), and converts / permutes
+// straight out of shared memory while the next tiles are in flight.
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "TRIMS_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra TRIMS_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int S, int D>
+__global__ void __launch_bounds__(kThreads) transform_tma_kernel(const Tile* __restrict__ tiles, uint32_t ntiles,
+                                                                 const uint8_t* __restrict__ src,
+                                                                 uint8_t* __restrict__ dst,
+                                                                 unsigned long long* __restrict__ sums) {
+  using ST = typename Bits<S>::T;
+  using DT = typename Bits<D>::T;
+  constexpr int DS = esize<D>(), SS = esize<S>(), EPW = 8 / DS;
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ Tile staged[kStages];
+  __shared__ unsigned long long red[kThreads / 32];
+
+  const uint32_t first = blockIdx.x, stride = gridDim.x;
+  const uint32_t mine = first < ntiles ? (ntiles - first + stride - 1) / stride : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](uint32_t j) {  // thread 0: stage tile j of this CTA
+    const int s = int(j % kStages);
+    const Tile t = tiles[first + j * stride];
+    staged[s] = t;
+    const uint64_t b = t.src_off & ~15ull, e = (t.src_off + uint64_t(t.n_elem) * SS + 15) & ~15ull;
+    mbar_expect_tx(&full[s], uint32_t(e - b));
+    bulk_g2s(ring + s * kStageAlloc, src + b, uint32_t(e - b), &full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (uint32_t j = 0; j < mine && j < uint32_t(kStages); ++j) issue(j);
+
+  for (uint32_t j = 0; j < mine; ++j) {
+    const int s = int(j % kStages);
+    mbar_wait(&full[s], (j / kStages) & 1);
+    const Tile t = staged[s];
+    const uint8_t* raw = ring + s * kStageAlloc + (t.src_off & 15);
+    const ST* rs_elems = reinterpret_cast<const ST*>(raw);
+    uint64_t* d = reinterpret_cast<uint64_t*>(dst + t.dst_off);
+    const uint64_t gw0 = t.dst_off >> 3;
+    const uint32_t words = t.dst_bytes >> 3, n = t.n_elem;
+    uint64_t acc = 0;
+    if (t.op == OP_CVT) {
+      const bool vec = ((t.src_off & 15) % (EPW * SS)) == 0;
+      for (uint32_t w = threadIdx.x; w < words; w += kThreads) {
+        const uint32_t e0 = w * EPW;
+        uint64_t word = 0;
+        if (e0 + EPW <= n && vec) {
+          ST v[EPW];
+          if constexpr (EPW * SS >= 16) {
+#pragma unroll
+            for (int i = 0; i < EPW * SS / 16; ++i)
+              reinterpret_cast<uint4*>(v)[i] = reinterpret_cast<const uint4*>(rs_elems + e0)[i];
+          } else if constexpr (EPW * SS == 8) {
+            *reinterpret_cast<uint2*>(v) = *reinterpret_cast<const uint2*>(rs_elems + e0);
+          } else {
+#pragma unroll
+            for (int q = 0; q < EPW; ++q) v[q] = rs_elems[e0 + q];
+          }
+#pragma unroll
+          for (int q = 0; q < EPW; ++q) word |= uint64_t(cvt<S, D>(v[q])) << (8 * DS * q);
+        } else {
+          for (int q = 0; q < EPW && e0 + q < n; ++q) word |= uint64_t(cvt<S, D>(rs_elems[e0 + q])) << (8 * DS * q);
+        }
+        d[w] = word;
+        acc += word_hash(word, gw0 + w);
+      }
+    } else {  // OP_PERM: source [g][C][RS] in smem -> resident [g][RS][C]
+      const uint32_t C = t.C, RS = t.RS, CRS = C * RS;
+      if ((C * DS) % 8 == 0) {
+        const uint32_t wpr = C / EPW, rows = (n / CRS) * RS;
+        const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (uint32_t row = warp; row < rows; row += kThreads / 32) {
+          const uint32_t k = row / RS, r = row - k * RS;
+          const ST* col = rs_elems + k * CRS + r;
+          uint64_t* drow = d + uint64_t(row) * wpr;
+          const uint64_t gwr = gw0 + uint64_t(row) * wpr;
+          for (uint32_t wi = lane; wi < wpr; wi += 32) {
+            const ST* e = col + wi * EPW * RS;
+            uint64_t word = 0;
+#pragma unroll
+            for (int q = 0; q < EPW; ++q) word |= uint64_t(cvt<S, D>(e[q * RS])) << (8 * DS * q);
+            drow[wi] = word;
+            acc += word_hash(word, gwr + wi);
+          }
+        }
+      } else {
+        for (uint32_t w = threadIdx.x; w < n * DS / 8; w += kThreads) {
+          uint32_t o = w * EPW, k = o / CRS, rem = o - k * CRS, r = rem / C, c = rem - r * C;
+          uint64_t word = 0;
+#pragma unroll
+          for (int q = 0; q < EPW; ++q) {
+            word |= uint64_t(cvt<S, D>(rs_elems[k * CRS + c * RS + r])) << (8 * DS * q);
+            if (++c == C) {
+              c = 0;
+              if (++r == RS) {
+                r = 0;
+                ++k;
+              }
+            }
+          }
+          d[w] = word;
+          acc += word_hash(word, gw0 + w);
+        }
+      }
+      for (uint32_t w = n * DS / 8 + threadIdx.x; w < words; w += kThreads) {  // tail: partial word + pad
+        const uint32_t o = w * EPW;
+        uint64_t word = 0;
+        for (int q = 0; q < EPW && o + q < n; ++q) {
+          uint32_t oo = o + q, k = oo / CRS, rem = oo - k * CRS, r = rem / C, c = rem - r * C;
+          word |= uint64_t(cvt<S, D>(rs_elems[k * CRS + c * RS + r])) << (8 * DS * q);
+        }
+        d[w] = word;
+        acc += word_hash(word, gw0 + w);
+      }
+    }
+    acc = block_sum(acc, red);  // its barriers also retire every read of ring stage s
+    if (threadIdx.x == 0) {
+      atomicAdd(&sums[t.tensor], (unsigned long long)acc);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async overwrite
+      if (j + kStages < mine) issue(j + kStages);
+    }
+  }
+}
+
 using TransformFn = void (*)(const Tile*, uint32_t, const uint8_t*, uint8_t*, unsigned long long*);
+
+TransformFn pair_tma_kernel(int s, int d) {
+  switch (s * 8 + d) {
+    case 0 * 8 + 0: return transform_tma_kernel<0, 0>;
+    case 1 * 8 + 1: return transform_tma_kernel<1, 1>;
+    case 2 * 8 + 2: return transform_tma_kernel<2, 2>;
+    case 3 * 8 + 3: return transform_tma_kernel<3, 3>;
+    case 4 * 8 + 4: return transform_tma_kernel<4, 4>;
+    case 1 * 8 + 4: return transform_tma_kernel<1, 4>;
+    case 0 * 8 + 1: return transform_tma_kernel<0, 1>;
+    case 0 * 8 + 4: return transform_tma_kernel<0, 4>;
+    case 2 * 8 + 1: return transform_tma_kernel<2, 1>;
+    case 2 * 8 + 4: return transform_tma_kernel<2, 4>;
+    case 4 * 8 + 1: return transform_tma_kernel<4, 1>;
+    default: return nullptr;
+  }
+}
 
 TransformFn pair_kernel(int s, int d) {
   switch (s * 8 + d) {
@@ -408,6 +582,7 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
   p.buckets = uint32_t(nt + 1);
   if (src.tensors.size() != nt) raise(Errc::InvalidArgument, "plan tensor count mismatch");
   auto extent_end = [&](size_t i) { return i + 1 < nt ? dst.tensors[i + 1].offset : dst.blob_bytes; };
+  std::vector<Tile> tiles;
 
   if (identity) {
     auto hash_range = [&](uint64_t b, uint64_t e, uint32_t bucket) {
@@ -417,13 +592,12 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
         t.dst_bytes = uint32_t(std::min<uint64_t>(kHashTile, e - off));
         t.tensor = bucket;
         t.op = OP_HASH;
-        p.tiles.push_back(t);
+        tiles.push_back(t);
       }
     };
     if (nt && dst.tensors[0].offset > 0) hash_range(0, dst.tensors[0].offset, uint32_t(nt));
     for (size_t i = 0; i < nt; ++i) hash_range(dst.tensors[i].offset, extent_end(i), uint32_t(i));
     p.algo_read_bytes = dst.blob_bytes;
-    p.algo_write_bytes = 0;
   } else {
     for (size_t i = 0; i < nt; ++i) {
       const auto& s = src.tensors[i];
@@ -442,12 +616,12 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
         const uint64_t K = s.dims[0], C = s.dims[1], RS = s.dims[2] * s.dims[3], CRS = C * RS;
         uint64_t g = 1;
         while ((g * CRS * ds) % 8) ++g;
-        // slices too large for shared memory are gathered straight from HBM
-        const bool gather = g * CRS * ds > kPermSmem;
-        while (!gather && 2 * g * CRS * ds <= kPermSmem && g * 2 <= K) g *= 2;
+        // a slice group whose raw bytes exceed a ring stage is gathered straight from HBM
+        const bool gather = g * CRS * ss > kStageBytes;
+        while (!gather && 2 * g * CRS * ss <= kStageBytes && g * 2 <= K) g *= 2;
         p.has_perm = true;
         for (uint64_t k0 = 0; k0 < K; k0 += g) {
-          uint64_t kn = std::min(g, K - k0);
+          const uint64_t kn = std::min(g, K - k0);
           Tile t{};
           t.op = OP_PERM;
           t.src_off = s.offset + k0 * CRS * ss;
@@ -460,11 +634,12 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
           t.C = uint32_t(C);
           t.RS = uint32_t(RS);
           t.pad_ = gather ? 1 : 0;
-          p.tiles.push_back(t);
+          tiles.push_back(t);
         }
       } else {
-        for (uint64_t e0 = 0; e0 < n; e0 += kElemTile) {
-          uint64_t cnt = std::min<uint64_t>(kElemTile, n - e0);
+        const uint64_t per = kStageBytes / ss;  // one ring stage of source per tile
+        for (uint64_t e0 = 0; e0 < n; e0 += per) {
+          const uint64_t cnt = std::min<uint64_t>(per, n - e0);
           Tile t{};
           t.op = OP_CVT;
           t.src_off = s.offset + e0 * ss;
@@ -474,52 +649,69 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
           t.tensor = uint32_t(i);
           t.sdt = uint8_t(s.dtype);
           t.ddt = uint8_t(d.dtype);
-          p.tiles.push_back(t);
+          tiles.push_back(t);
         }
       }
     }
     p.algo_write_bytes = dst.blob_bytes;
   }
-  // Chunks: consecutive tiles until their source span reaches chunk_bytes.
-  auto src_end = [&](const Tile& t) -> uint64_t {
+
+  auto src_end = [](const Tile& t) -> uint64_t {
     if (t.op == OP_HASH) return t.src_off + t.dst_bytes;
-    uint64_t ss = fmt::element_size(fmt::DType(t.sdt));
-    return t.src_off + uint64_t(t.n_elem) * ss;
+    return t.src_off + uint64_t(t.n_elem) * fmt::element_size(fmt::DType(t.sdt));
   };
-  auto pair_bit = [](const Tile& t) { return t.op == OP_HASH ? kHashPairBit : 1ull << (t.sdt * 8 + t.ddt); };
+  // kernel key: hash | (TMA ring or gather) x dtype pair
+  auto kind_of = [](const Tile& t) -> uint8_t { return t.op == OP_HASH ? 0 : (t.pad_ ? 2 : 1); };
+  auto key_of = [&](const Tile& t) { return uint32_t(kind_of(t)) << 16 | uint32_t(t.sdt) << 8 | t.ddt; };
+  auto group_range = [&](std::vector<Tile>& v, uint32_t b, uint32_t e, std::vector<Group>& out) {
+    std::stable_sort(v.begin() + b, v.begin() + e, [&](const Tile& x, const Tile& y) { return key_of(x) < key_of(y); });
+    for (uint32_t i = b; i < e;) {
+      uint32_t j = i + 1;
+      while (j < e && key_of(v[j]) == key_of(v[i])) ++j;
+      out.push_back({i, j, kind_of(v[i]), v[i].sdt, v[i].ddt});
+      i = j;
+    }
+  };
+  // Chunks: consecutive (source-ordered) tiles until their span reaches chunk_bytes.
   uint32_t b = 0;
-  while (b < p.tiles.size()) {
-    uint64_t s0 = p.tiles[b].src_off, s1 = src_end(p.tiles[b]), pairs = pair_bit(p.tiles[b]);
+  while (b < tiles.size()) {
+    uint64_t s0 = tiles[b].src_off, s1 = src_end(tiles[b]);
     uint32_t e = b + 1;
-    while (e < p.tiles.size() && s1 - s0 < chunk_bytes) {
-      s1 = std::max(s1, src_end(p.tiles[e]));
-      pairs |= pair_bit(p.tiles[e]);
+    while (e < tiles.size() && s1 - s0 < chunk_bytes) {
+      s1 = std::max(s1, src_end(tiles[e]));
       ++e;
     }
-    p.chunks.push_back({b, e, s0, s1, pairs});
-    p.pairs |= pairs;
+    p.chunks.push_back({b, e, s0, s1, {}});
     b = e;
   }
+  p.tiles = tiles;
+  for (auto& ch : p.chunks) group_range(p.tiles, ch.tile_begin, ch.tile_end, ch.groups);
+  p.tiles_by_kernel = tiles;
+  group_range(p.tiles_by_kernel, 0, uint32_t(tiles.size()), p.groups);
   return p;
 }
 
-uint32_t launch_transform(const Tile* d_tiles, uint32_t ntiles, uint64_t pairs, bool has_perm, const uint8_t* src,
-                          uint8_t* dst, unsigned long long* d_sums, cudaStream_t stream, int sm_count) {
-  if (!ntiles) return 0;
-  const uint32_t grid = std::min<uint32_t>(ntiles, uint32_t(sm_count * 8));
+uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, const uint8_t* src, uint8_t* dst,
+                       unsigned long long* d_sums, cudaStream_t stream, int sm_count) {
   uint32_t launches = 0;
-  if (pairs & kHashPairBit) {
-    hash_tiles_kernel<<<grid, kThreads, 0, stream>>>(d_tiles, ntiles, dst, d_sums);
-    TRIMS_CUDA(cudaGetLastError());
-    ++launches;
-  }
-  for (int bit = 0; bit < 64; ++bit) {
-    if (bit == 63 || !(pairs & (1ull << bit))) continue;
-    TransformFn fn = pair_kernel(bit / 8, bit % 8);
-    if (!fn) raise(Errc::InvalidArgument, "unsupported dtype pair in plan");
-    const size_t smem = has_perm ? kPermSmem : 0;
-    if (has_perm) TRIMS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPermSmem)));
-    fn<<<grid, kThreads, smem, stream>>>(d_tiles, ntiles, src, dst, d_sums);
+  for (const Group& g : groups) {
+    const uint32_t n = g.end - g.begin;
+    if (!n) continue;
+    const Tile* t = d_tiles + g.begin;
+    if (g.kind == 0) {
+      hash_tiles_kernel<<<std::min<uint32_t>(n, sm_count * 8), kThreads, 0, stream>>>(t, n, dst, d_sums);
+    } else if (g.kind == 1) {
+      TransformFn fn = pair_tma_kernel(g.sdt, g.ddt);
+      if (!fn) raise(Errc::InvalidArgument, "unsupported dtype pair in plan");
+      const int smem = kStages * kStageAlloc;
+      TRIMS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      fn<<<std::min<uint32_t>(n, sm_count * 2), kThreads, smem, stream>>>(t, n, src, dst, d_sums);
+    } else {
+      TransformFn fn = pair_kernel(g.sdt, g.ddt);
+      if (!fn) raise(Errc::InvalidArgument, "unsupported dtype pair in plan");
+      TRIMS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPermSmem)));
+      fn<<<std::min<uint32_t>(n, sm_count * 4), kThreads, kPermSmem, stream>>>(t, n, src, dst, d_sums);
+    }
     TRIMS_CUDA(cudaGetLastError());
     ++launches;
   }

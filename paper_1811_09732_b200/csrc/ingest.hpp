@@ -1,8 +1,8 @@
 // ingest.hpp — the weight-ingest transform: staged raw artifact blob ->
 // resident blob (dtype convert, KCRS->KRSC permute, zero padding) with the
 // TRIMS block checksum of every resident word fused in (K2+K3+K4 of
-// SURVEY.md §2). Work is cut into tiles on the host; one persistent kernel
-// launch processes a tile range.
+// SURVEY.md §2). Work is cut into tiles on the host; persistent kernels
+// stream tile ranges through a TMA-fed shared-memory ring.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -24,22 +24,32 @@ struct Tile {
   uint32_t dst_bytes;  // resident bytes written (and hashed) by this tile
   uint32_t n_elem;     // source elements consumed (OP_CVT / OP_PERM)
   uint32_t tensor;     // checksum bucket (resident tensor index; ntensors = leading pad)
-  uint8_t op, sdt, ddt, pad_;
+  uint8_t op, sdt, ddt, pad_;  // pad_ = 1: slice too large for the TMA ring (direct-gather kernel)
   uint32_t C, RS;      // OP_PERM geometry: n_elem / (C*RS) k-slices
 };
 static_assert(sizeof(Tile) == 40, "tile layout");
 
+// A contiguous tile range handled by one kernel: kind 0 hash, 1 TMA ring, 2 gather.
+struct Group {
+  uint32_t begin, end;
+  uint8_t kind, sdt, ddt;
+};
+
 struct TilePlan {
+  // Chunk-major tile table (tiles grouped by kernel within each chunk).
   std::vector<Tile> tiles;
-  // Pipeline chunks: [tile_begin, tile_end) with the source byte span the
-  // chunk's tiles read, so the H2D of chunk c can overlap tiles of chunk c-1.
+  // Pipeline chunks: the source byte span their tiles read, so the H2D of
+  // chunk c+1 overlaps the kernels of chunk c.
   struct Chunk {
     uint32_t tile_begin, tile_end;
     uint64_t src_begin, src_end;
-    uint64_t pairs;  // dtype pairs present (bit s*8+d), kHashPairBit for OP_HASH
+    std::vector<Group> groups;  // ranges inside `tiles`
   };
   std::vector<Chunk> chunks;
-  uint64_t pairs{0};
+  // Whole-plan table sorted by kernel (one launch per group) for the
+  // HBM-resident transform.
+  std::vector<Tile> tiles_by_kernel;
+  std::vector<Group> groups;
   uint32_t buckets{0};     // checksum buckets (ntensors + 1)
   bool identity{false};    // resident == source bytes: tiles only hash
   bool has_perm{false};
@@ -51,14 +61,11 @@ struct TilePlan {
 TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool identity,
                      uint64_t chunk_bytes = 16ull << 20);
 
-inline constexpr uint64_t kHashPairBit = 1ull << 63;
-
-// Persistent tile kernels over tiles [0, ntiles) of `d_tiles` (device copy):
-// one launch per dtype pair in `pairs` (+ one hash launch). Per-bucket
-// checksums are atomically accumulated into d_sums (mod 2^64). Returns the
-// number of kernel launches issued.
-uint32_t launch_transform(const Tile* d_tiles, uint32_t ntiles, uint64_t pairs, bool has_perm, const uint8_t* src,
-                          uint8_t* dst, unsigned long long* d_sums, cudaStream_t stream, int sm_count);
+// Launches one persistent kernel per group over `d_tiles` (device copy of the
+// table the groups index). Per-bucket checksums accumulate atomically into
+// d_sums (mod 2^64). Returns the number of kernel launches.
+uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, const uint8_t* src, uint8_t* dst,
+                       unsigned long long* d_sums, cudaStream_t stream, int sm_count);
 
 // Checksum of an arbitrary device range (word0 = global index of its first word).
 void launch_checksum(const uint8_t* p, uint64_t nbytes, uint64_t word0, unsigned long long* d_out,

@@ -111,10 +111,10 @@ class Store:
         return text_call(lambda o, c: lib.trims_store_resident_json(self._h, model_id, o, c), cap=1 << 22)
 
     def ingest_stats(self, model_id: int) -> dict:
-        out = (ctypes.c_double * 5)()
+        out = (ctypes.c_double * 7)()
         check(lib.trims_store_ingest_stats(self._h, model_id, out))
         return {"h2d_ms": out[0], "total_ms": out[1], "read_ms": out[2], "h2d_bytes": int(out[3]),
-                "launches": int(out[4])}
+                "launches": int(out[4]), "alloc_ms": out[5], "seal_ms": out[6]}
 
     def checksums(self, model_id: int) -> list[int]:
         cap = 1 << 16

@@ -129,19 +129,22 @@ def test_converting_store_bit_exact_and_import_path(tmp_path):
         via_fd.close_all_imports()
 
 
-def _child_attach(sock_fd: int, device: int, alloc: int, gen: int, payload: int, digest: bytes, q):
-    import socket as so
-    s = so.socket(fileno=sock_fd)
-    msg, fds, _, _ = so.recv_fds(s, 16, 1)
-    from paper_1811_09732_b200._lib import lib
-    import ctypes
-    imp, ptr, mj = import_segment(device, fds[0], alloc, gen, payload, digest)
-    os.close(fds[0])
-    cs = ctypes.c_uint64()
-    rc = lib.trims_import_verify(imp, ctypes.byref(cs))
-    ro = lib.trims_import_read_only(imp)
-    q.put((rc, cs.value, ro, len(mj)))
-    lib.trims_import_close(imp)
+def _child_attach(conn, device: int, alloc: int, gen: int, payload: int, digest: bytes, q):
+    try:
+        import ctypes
+        from multiprocessing.reduction import recv_handle
+
+        from paper_1811_09732_b200._lib import lib
+        fd = recv_handle(conn)  # SCM_RIGHTS over the pipe: the fd of the cuMem allocation
+        imp, ptr, mj = import_segment(device, fd, alloc, gen, payload, digest)
+        os.close(fd)
+        cs = ctypes.c_uint64()
+        rc = lib.trims_import_verify(imp, ctypes.byref(cs))
+        ro = lib.trims_import_read_only(imp)
+        q.put((rc, cs.value, ro, len(mj)))
+        lib.trims_import_close(imp)
+    except Exception as e:  # report instead of dying silently
+        q.put((-1, repr(e), 0, 0))
 
 
 def test_multiprocess_one_copy(tiny_dir):
@@ -152,16 +155,17 @@ def test_multiprocess_one_copy(tiny_dir):
     with Store(StoreOptions(disk_cache_dir=tiny_dir, fast_capacity_bytes=64 * MB, host_capacity_bytes=64 * MB)) as s:
         q = ctx.Queue()
         procs, exps = [], []
+        from multiprocessing.reduction import send_handle
         for i in range(8):
             ex = s.open(key("vgg16"))
             exps.append(ex)
-            a, b = socket.socketpair()
-            p = ctx.Process(target=_child_attach, args=(b.fileno(), ex.device, ex.alloc_bytes, ex.generation,
+            parent, child = ctx.Pipe()
+            p = ctx.Process(target=_child_attach, args=(child, ex.device, ex.alloc_bytes, ex.generation,
                                                         ex.payload_bytes, bytes(ex.manifest_digest), q))
             p.start()
-            socket.send_fds(a, [b"fd"], [ex.fd])
-            procs.append((p, a, b))
-        res = [q.get(timeout=120) for _ in procs]
+            send_handle(parent, ex.fd, p.pid)
+            procs.append((p, parent, child))
+        res = [q.get(timeout=180) for _ in procs]
         for p, a, b in procs:
             p.join(60)
             a.close()
