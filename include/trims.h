@@ -98,6 +98,7 @@ typedef struct trims_store_config {
   uint64_t pinned_pool_bytes;    /* pre-pinned host pool (0 = host_capacity_bytes) */
   uint32_t scan_disk;            /* register *.trms in disk_cache_dir at start (daemon.cpp:314-325) */
   uint32_t read_threads;         /* parallel pread threads for disk -> pinned (0 = 8) */
+  uint64_t arena_bytes;          /* HBM arena of the fast tier: 0 = auto, 1 = off (one cuMem allocation per model) */
 } trims_store_config;
 
 /* Reference outcomes (cache_core.hpp:36) + PEER_HIT for the multi-GPU directory. */
@@ -120,9 +121,10 @@ typedef struct trims_export {
   uint64_t timings_ns[4];         /* fetch, disk_read, host_to_fast_copy, handle_export */
   uint8_t manifest_digest[32];    /* SHA-256 of the resident manifest JSON */
   void* dev_ptr;                  /* owner-process device address */
-  int32_t fd;                     /* owner-process fd of the allocation */
+  int32_t fd;                     /* owner-process fd of the allocation (the arena, or a dedicated segment) */
   uint32_t n_objects;             /* layout_for(resident manifest, granularity) count */
-  char token[160];
+  char token[160];                /* names the allocation: one token per arena */
+  uint64_t segment_offset;        /* segment start inside that allocation */
 } trims_export;
 
 /* Daemon::Daemon (daemon.cpp:298-391) minus listeners: builds the backend
@@ -158,18 +160,22 @@ int trims_store_checksums(trims_store* s, uint64_t model_id, uint64_t* out, uint
 /* --------------------------------------------------- client attach (a5, a9) */
 
 typedef struct trims_import trims_import;
-/* Attachment::attach (shared_segment.cpp:212-245): map a segment exported by
- * another (or this) process read-only. fd must be valid in the caller. The
- * tail is validated (magic, generation, sealed, length) and the manifest
- * digest re-checked (client.cpp:284-291). */
-int trims_import_open(int device, int fd, uint64_t alloc_bytes, uint64_t generation, uint64_t payload_bytes,
-                      const uint8_t digest[32], trims_import** out, void** dev_ptr);
-/* Resident manifest JSON carried by the imported segment (client.cpp:293-307). */
-int trims_import_manifest(trims_import* im, char* out, uint64_t cap);
+/* Maps an allocation exported by another (or this) process read-only — the
+ * device side of Attachment::attach (shared_segment.cpp:212-245). fd must be
+ * valid in the caller (SCM_RIGHTS / same process). With the arena, a client
+ * maps once and attaches every model by offset. */
+int trims_import_open(int device, int fd, uint64_t alloc_bytes, trims_import** out, void** base);
+/* Attaches one model segment of a mapping: validates the tail (magic,
+ * generation -> StaleGeneration, sealed, length), re-checks the manifest
+ * digest (client.cpp:284-291), returns the device pointer and the resident
+ * manifest JSON (client.cpp:293-307). */
+int trims_import_attach(trims_import* im, uint64_t offset, uint64_t generation, uint64_t payload_bytes,
+                        const uint8_t digest[32], void** dev_ptr, char* json_out, uint64_t cap);
 int trims_import_read_only(trims_import* im);
 /* Device-side integrity check of an attached segment: K4 over the resident
  * blob, compared with the checksum sealed into the tail (Corrupt if not). */
-int trims_import_verify(trims_import* im, uint64_t* checksum_out);
+int trims_import_verify(trims_import* im, uint64_t offset, uint64_t generation, uint64_t payload_bytes,
+                        uint64_t* checksum_out);
 void trims_import_close(trims_import* im);
 
 /* ------------------------------------------- ingest kernels (K1..K5) raw */

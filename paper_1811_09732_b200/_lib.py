@@ -66,6 +66,7 @@ class StoreConfig(ctypes.Structure):
         ("pinned_pool_bytes", ctypes.c_uint64),
         ("scan_disk", ctypes.c_uint32),
         ("read_threads", ctypes.c_uint32),
+        ("arena_bytes", ctypes.c_uint64),
     ]
 
 
@@ -87,6 +88,7 @@ class Export(ctypes.Structure):
         ("fd", ctypes.c_int32),
         ("n_objects", ctypes.c_uint32),
         ("token", ctypes.c_char * 160),
+        ("segment_offset", ctypes.c_uint64),
     ]
 
 
@@ -126,11 +128,11 @@ _SIGS = {
     "trims_store_resident_json": (_c.c_int, [_p, _u64, _s, _u64]),
     "trims_store_ingest_stats": (_c.c_int, [_p, _u64, _c.POINTER(_c.c_double)]),
     "trims_store_checksums": (_c.c_int, [_p, _u64, _c.POINTER(_u64), _u64, _c.POINTER(_u64)]),
-    "trims_import_open": (_c.c_int, [_c.c_int, _c.c_int, _u64, _u64, _u64, _p, _c.POINTER(_p), _c.POINTER(_p)]),
-    "trims_import_manifest": (_c.c_int, [_p, _s, _u64]),
+    "trims_import_open": (_c.c_int, [_c.c_int, _c.c_int, _u64, _c.POINTER(_p), _c.POINTER(_p)]),
+    "trims_import_attach": (_c.c_int, [_p, _u64, _u64, _u64, _p, _c.POINTER(_p), _s, _u64]),
     "trims_import_read_only": (_c.c_int, [_p]),
     "trims_import_close": (None, [_p]),
-    "trims_import_verify": (_c.c_int, [_p, _c.POINTER(_u64)]),
+    "trims_import_verify": (_c.c_int, [_p, _u64, _u64, _u64, _c.POINTER(_u64)]),
     "trims_ingest_host": (_c.c_int, [_c.c_int, _p, _s, _u32, _u32, _p, _c.POINTER(_u64), _c.POINTER(_c.c_double)]),
     "trims_transform_device": (_c.c_int, [_c.c_int, _p, _s, _u32, _u32, _p, _p, _p]),
     "trims_plan_info": (_c.c_int, [_s, _u32, _u32, _c.POINTER(_u64)]),

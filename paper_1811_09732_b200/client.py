@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import format as F
-from ._lib import Errc, TrimsError, check, lib
+from ._lib import Errc, TrimsError, check, lib, text_call
 
 SHARED, PRIVATE = "shared", "private"
 
@@ -112,36 +112,51 @@ def slice_tensors(manifest_json: str, base_ptr: int) -> list[TensorView]:
 
 
 class ImportCache:
-    """Per-process attach cache keyed by (token, generation): re-opening a hot
-    model skips the map + digest check (the reference caches manifests by
-    digest, client.cpp:293-307; we also keep the mapping)."""
+    """Per-process attach state. One read-only mapping per exported allocation
+    (token: the store's arena, or a dedicated segment), and per attached model
+    (token, offset, generation) its manifest + views, so re-opening a hot
+    model costs neither a map nor a digest check (the reference caches
+    manifests by digest, client.cpp:293-307)."""
 
     def __init__(self):
-        self._maps = {}
-
-    def get(self, token: str, generation: int):
-        return self._maps.get((token, generation))
-
-    def put(self, token: str, generation: int, entry):
-        self._maps[(token, generation)] = entry
+        self.maps = {}    # token -> (trims_import*, base)
+        self.models = {}  # (token, offset, generation) -> (ptr, json, digest, views)
 
     def clear(self):
-        for entry in self._maps.values():
-            lib.trims_import_close(entry[0])
-        self._maps.clear()
+        for imp, _ in self.maps.values():
+            lib.trims_import_close(imp)
+        self.maps.clear()
+        self.models.clear()
 
 
-def import_segment(device: int, fd: int, alloc_bytes: int, generation: int, payload_bytes: int,
-                   digest: bytes):
-    """Attachment::attach (shared_segment.cpp:212-245) + digest check (client.cpp:284-291)."""
+def map_allocation(device: int, fd: int, alloc_bytes: int):
+    """Map an exported allocation read-only (shared_segment.cpp:212-232)."""
     imp = ctypes.c_void_p()
+    base = ctypes.c_void_p()
+    check(lib.trims_import_open(device, fd, alloc_bytes, ctypes.byref(imp), ctypes.byref(base)))
+    return imp, int(base.value)
+
+
+def attach_segment(imp, offset: int, generation: int, payload_bytes: int, digest: bytes):
+    """Validate one model segment of a mapping (tail, generation, seal) and its
+    manifest digest (client.cpp:284-291); returns (device ptr, resident JSON)."""
     ptr = ctypes.c_void_p()
     dig = (ctypes.c_uint8 * 32).from_buffer_copy(bytes(digest))
-    check(lib.trims_import_open(device, fd, alloc_bytes, generation, payload_bytes, dig, ctypes.byref(imp),
-                                ctypes.byref(ptr)))
-    buf = ctypes.create_string_buffer(1 << 22)
-    check(lib.trims_import_manifest(imp, buf, len(buf)))
-    return imp, int(ptr.value), buf.value.decode()
+    json_txt = text_call(lambda o, c: lib.trims_import_attach(imp, offset, generation, payload_bytes, dig,
+                                                               ctypes.byref(ptr), o, c))
+    return int(ptr.value), json_txt
+
+
+def import_segment(device: int, fd: int, alloc_bytes: int, offset: int, generation: int, payload_bytes: int,
+                   digest: bytes):
+    """map_allocation + attach_segment in one call (used by one-shot importers)."""
+    imp, _ = map_allocation(device, fd, alloc_bytes)
+    try:
+        ptr, js = attach_segment(imp, offset, generation, payload_bytes, digest)
+    except Exception:
+        lib.trims_import_close(imp)
+        raise
+    return imp, ptr, js
 
 
 class Client:
@@ -222,19 +237,25 @@ class Client:
         remote = getattr(ex, "remote", False)
         digest = bytes(ex.manifest_digest)
         if remote or self.attach_via_import:
-            hit = self.imports.get(token, ex.generation)
+            mkey = (token, ex.segment_offset, ex.generation)
+            hit = self.imports.models.get(mkey)
             if hit is None:
-                fd = ex.fd if remote else os.dup(ex.fd)
-                try:
-                    imp, ptr, mjson = import_segment(ex.device, fd, ex.alloc_bytes, ex.generation, ex.payload_bytes,
-                                                     digest)
-                finally:
-                    os.close(fd)
-                hit = (imp, ptr, mjson, digest, slice_tensors(mjson, ptr))
-                self.imports.put(token, ex.generation, hit)
+                mapping = self.imports.maps.get(token)
+                if mapping is None:
+                    fd = ex.fd if remote else os.dup(ex.fd)
+                    try:
+                        mapping = map_allocation(ex.device, fd, ex.alloc_bytes)
+                    finally:
+                        os.close(fd)
+                    self.imports.maps[token] = mapping
+                elif remote and ex.fd >= 0:
+                    os.close(ex.fd)
+                ptr, mjson = attach_segment(mapping[0], ex.segment_offset, ex.generation, ex.payload_bytes, digest)
+                hit = (ptr, mjson, digest, slice_tensors(mjson, ptr))
+                self.imports.models[mkey] = hit
             elif remote and ex.fd >= 0:
                 os.close(ex.fd)
-            _, base, mjson, seen, tensors = hit
+            base, mjson, seen, tensors = hit
         else:
             # same process: the segment is already mapped; the manifest is
             # fetched, digest-checked and sliced once per (model, generation)

@@ -236,6 +236,7 @@ uint32_t Ingestor::from_device(const IngestPlan& ip, const uint8_t* d_src, uint8
 CudaTierBackend::CudaTierBackend(BackendConfig cfg) : cfg_(std::move(cfg)), ing_(cfg_.device) {
   DeviceGuard g(cfg_.device);
   if (cfg_.pinned_pool_bytes) pool_ = std::make_unique<PinnedPool>(cfg_.pinned_pool_bytes);
+  if (cfg_.arena_bytes) arena_ = std::make_unique<DeviceArena>(cfg_.device, cfg_.arena_bytes);
 }
 
 CudaTierBackend::~CudaTierBackend() {
@@ -340,7 +341,15 @@ FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Mani
   const uint64_t rb = rec->resident.blob_bytes;
   const uint64_t payload = rb + rec->json.size() + 8;
   auto a0 = std::chrono::steady_clock::now();
-  rec->seg = DeviceSegment::create(cfg_.device, payload + sizeof(SegTail));
+  uint64_t off = 0, reserved = 0;
+  if (arena_ && arena_->alloc(payload + sizeof(SegTail), &off, &reserved)) {
+    rec->arena = arena_.get();
+    rec->offset = off;
+    rec->reserved = reserved;
+  } else {
+    rec->seg = DeviceSegment::create(cfg_.device, payload + sizeof(SegTail));
+  }
+  uint8_t* const base = rec->base();
   const double alloc_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a0).count();
   rec->generation = next_gen_.fetch_add(1);
 
@@ -353,7 +362,7 @@ FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Mani
       if (it->second.bytes != m.blob_bytes) raise(Errc::Internal, "host buffer size mismatch");
       src = it->second.p;  // single-flight pins the entry while loading
     }
-    rec->checksum = ing_.from_host(*plan, src, rec->seg.ptr(), &rec->bucket_sums, &rec->stats);
+    rec->checksum = ing_.from_host(*plan, src, base, &rec->bucket_sums, &rec->stats);
   } else {
     int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
     if (fd < 0) raise(Errc::NotFound, path);
@@ -362,7 +371,7 @@ FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Mani
       if (::pread(fd, hdr, 16, 0) != 16) raise(Errc::Corrupt, "short read on " + path);
       uint64_t mlen = 0;
       for (int i = 0; i < 8; ++i) mlen |= uint64_t(hdr[8 + i]) << (8 * i);
-      rec->checksum = ing_.from_file(*plan, fd, fmt::blob_file_offset(mlen), rec->seg.ptr(), &rec->bucket_sums,
+      rec->checksum = ing_.from_file(*plan, fd, fmt::blob_file_offset(mlen), base, &rec->bucket_sums,
                                      &rec->stats);
     } catch (...) {
       ::close(fd);
@@ -388,7 +397,7 @@ FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Mani
   std::memcpy(tail.data() + rec->json.size() + 8, &t, sizeof t);
   {
     DeviceGuard g(cfg_.device);
-    TRIMS_CUDA(cudaMemcpy(rec->seg.ptr() + rb, tail.data(), tail.size(), cudaMemcpyHostToDevice));
+    TRIMS_CUDA(cudaMemcpy(base + rb, tail.data(), tail.size(), cudaMemcpyHostToDevice));
   }
 
   FastPublication pub;
@@ -397,9 +406,11 @@ FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Mani
   es.generation = rec->generation;
   es.length = payload;
   es.device = cfg_.device;
-  es.dev_ptr = rec->seg.ptr();
-  es.fd = rec->seg.fd();
-  es.alloc_bytes = rec->seg.size();
+  es.dev_ptr = base;
+  es.fd = rec->arena ? rec->arena->fd() : rec->seg.fd();
+  es.alloc_bytes = rec->arena ? rec->arena->size() : rec->seg.size();
+  es.offset = rec->offset;
+  if (rec->arena) es.token = "trims." + std::to_string(::getpid()) + ".arena" + std::to_string(cfg_.device);
   es.resident_blob_bytes = rb;
   es.ingest_checksum = rec->checksum;
   pub.segments.push_back(es);

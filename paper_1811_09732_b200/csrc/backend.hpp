@@ -93,11 +93,19 @@ struct BackendConfig {
   fmt::Plan plan;
   uint64_t pinned_pool_bytes{0};
   unsigned read_threads{8};
+  uint64_t arena_bytes{0};  // HBM arena for the fast tier (0 = one cuMem allocation per model)
 };
 
-// Fast-tier record of one published model.
+// Fast-tier record of one published model: a range of the arena, or a
+// dedicated segment when the arena has no fitting extent.
 struct FastRecord {
-  DeviceSegment seg;
+  DeviceSegment seg;             // dedicated allocation (arena == nullptr)
+  DeviceArena* arena{nullptr};   // arena range [offset, offset + reserved)
+  uint64_t offset{0}, reserved{0};
+  uint8_t* base() const { return arena ? arena->base() + offset : seg.ptr(); }
+  ~FastRecord() {
+    if (arena) arena->free(offset);
+  }
   fmt::Manifest resident;
   std::string json;
   uint64_t generation{0};
@@ -139,6 +147,7 @@ class CudaTierBackend : public TierBackend {
   BackendConfig cfg_;
   Ingestor ing_;
   std::unique_ptr<PinnedPool> pool_;
+  std::unique_ptr<DeviceArena> arena_;
   std::mutex mu_;
   std::map<uint64_t, HostBuf> host_;
   std::map<uint64_t, std::shared_ptr<FastRecord>> fast_;

@@ -57,6 +57,7 @@ struct ExportedSegment {
   void* dev_ptr{nullptr};     // owner-process address
   int fd{-1};                 // owner-process POSIX fd of the allocation (-1: none)
   uint64_t alloc_bytes{0};    // physical allocation (granularity-rounded)
+  uint64_t offset{0};         // segment offset inside that allocation (arena ranges)
   uint8_t ipc_handle[64]{};   // cudaIpcMemHandle_t bytes (legacy import path)
   uint64_t resident_blob_bytes{0};
   uint64_t ingest_checksum{0};  // TRIMS block checksum of the resident blob

@@ -114,10 +114,7 @@ struct trims_store {
 
 struct trims_import {
   std::unique_ptr<Import> map;
-  std::string json;
   int device{0};
-  uint64_t blob_bytes{0};
-  uint64_t checksum{0};
 };
 
 extern "C" {
@@ -284,6 +281,10 @@ int trims_store_create(const trims_store_config* cfg, trims_store** out) {
     bc.plan = make_plan(cfg->plan_flags, cfg->out_dtype);
     bc.pinned_pool_bytes = cfg->pinned_pool_bytes ? cfg->pinned_pool_bytes : cfg->host_capacity_bytes;
     bc.read_threads = cfg->read_threads ? cfg->read_threads : 8;
+    // arena: 0 = auto (capacity + 1/16 + 64 MiB for per-segment rounding and tails), 1 = off
+    bc.arena_bytes = cfg->arena_bytes == 1 ? 0
+                     : cfg->arena_bytes ? cfg->arena_bytes
+                                        : cfg->fast_capacity_bytes + cfg->fast_capacity_bytes / 16 + (64ull << 20);
     s->be = std::make_unique<CudaTierBackend>(bc);
     CoreConfig cc{cfg->fast_capacity_bytes, cfg->host_capacity_bytes, cfg->disk_capacity_bytes,
                   Policy(cfg->policy ? 1 : 0), cfg->eager_reclaim != 0};
@@ -339,6 +340,7 @@ int trims_store_open(trims_store* s, const char* ns, const char* name, const cha
       out->ingest_checksum = es.ingest_checksum;
       out->dev_ptr = es.dev_ptr;
       out->fd = es.fd;
+      out->segment_offset = es.offset;
       std::snprintf(out->token, sizeof out->token, "%s", es.token.c_str());
     }
     // objects of the resident blob at the requested granularity (count only)
@@ -446,48 +448,65 @@ int trims_store_checksums(trims_store* s, uint64_t model_id, uint64_t* out, uint
 
 // ---------------------------------------------------------------- import
 
-int trims_import_open(int device, int fd, uint64_t alloc_bytes, uint64_t generation, uint64_t payload_bytes,
-                      const uint8_t digest[32], trims_import** out, void** dev_ptr) {
+int trims_import_open(int device, int fd, uint64_t alloc_bytes, trims_import** out, void** base) {
   return guard([&] {
-    if (payload_bytes < 8 || payload_bytes + sizeof(SegTail) > alloc_bytes)
-      raise(Errc::NoSuchSegment, "segment shorter than its payload");
     auto im = std::make_unique<trims_import>();
     im->map.reset(Import::open(device, fd, alloc_bytes, /*read_only=*/true));
-    DeviceGuard g(device);
-    uint8_t tail[8 + sizeof(SegTail)];
-    TRIMS_CUDA(cudaMemcpy(tail, im->map->ptr() + payload_bytes - 8, sizeof tail, cudaMemcpyDeviceToHost));
-    uint64_t jlen = 0;
-    for (int i = 0; i < 8; ++i) jlen |= uint64_t(tail[i]) << (8 * i);
-    SegTail st;
-    std::memcpy(&st, tail + 8, sizeof st);
-    if (st.magic != kSegMagic) raise(Errc::NoSuchSegment, "bad segment tail");
-    if (st.generation != generation)
-      raise(Errc::StaleGeneration, "generation " + std::to_string(st.generation) + " != " + std::to_string(generation));
-    if (!st.sealed) raise(Errc::NotSealed, "segment not sealed");
-    if (st.length != payload_bytes || jlen + 8 > payload_bytes) raise(Errc::Corrupt, "segment length mismatch");
-    im->json.resize(jlen);
-    TRIMS_CUDA(cudaMemcpy(im->json.data(), im->map->ptr() + payload_bytes - 8 - jlen, jlen, cudaMemcpyDeviceToHost));
-    if (digest) {
-      auto d = Sha256::of(im->json.data(), im->json.size());
-      if (std::memcmp(d.data(), digest, 32) != 0) raise(Errc::Corrupt, "manifest digest mismatch on attach");
-    }
     im->device = device;
-    im->blob_bytes = st.blob_bytes;
-    im->checksum = st.checksum;
-    if (dev_ptr) *dev_ptr = im->map->ptr();
+    if (base) *base = im->map->ptr();
     *out = im.release();
     return 0;
   });
 }
 
-int trims_import_manifest(trims_import* im, char* out, uint64_t cap) {
-  return guard([&] { return put(im->json, out, cap); });
+namespace {
+// Reads and validates the tail of the segment at `offset` (shared_segment.cpp:
+// 233-237 checks: magic, generation, sealed, length) and returns it with the JSON.
+SegTail read_tail(trims_import* im, uint64_t offset, uint64_t generation, uint64_t payload_bytes, std::string* json) {
+  if (payload_bytes < 8 || offset + payload_bytes + sizeof(SegTail) > im->map->size())
+    raise(Errc::NoSuchSegment, "segment outside the mapped allocation");
+  DeviceGuard g(im->device);
+  uint8_t tail[8 + sizeof(SegTail)];
+  TRIMS_CUDA(cudaMemcpy(tail, im->map->ptr() + offset + payload_bytes - 8, sizeof tail, cudaMemcpyDeviceToHost));
+  uint64_t jlen = 0;
+  for (int i = 0; i < 8; ++i) jlen |= uint64_t(tail[i]) << (8 * i);
+  SegTail st;
+  std::memcpy(&st, tail + 8, sizeof st);
+  if (st.magic != kSegMagic) raise(Errc::NoSuchSegment, "bad segment tail");
+  if (st.generation != generation)
+    raise(Errc::StaleGeneration, "generation " + std::to_string(st.generation) + " != " + std::to_string(generation));
+  if (!st.sealed) raise(Errc::NotSealed, "segment not sealed");
+  if (st.length != payload_bytes || jlen + 8 > payload_bytes || st.blob_bytes + jlen + 8 != payload_bytes)
+    raise(Errc::Corrupt, "segment length mismatch");
+  if (json) {
+    json->resize(jlen);
+    TRIMS_CUDA(cudaMemcpy(json->data(), im->map->ptr() + offset + payload_bytes - 8 - jlen, jlen,
+                          cudaMemcpyDeviceToHost));
+  }
+  return st;
+}
+}  // namespace
+
+int trims_import_attach(trims_import* im, uint64_t offset, uint64_t generation, uint64_t payload_bytes,
+                        const uint8_t digest[32], void** dev_ptr, char* json_out, uint64_t cap) {
+  return guard([&] {
+    std::string json;
+    read_tail(im, offset, generation, payload_bytes, &json);
+    if (digest) {
+      auto d = Sha256::of(json.data(), json.size());
+      if (std::memcmp(d.data(), digest, 32) != 0) raise(Errc::Corrupt, "manifest digest mismatch on attach");
+    }
+    if (dev_ptr) *dev_ptr = im->map->ptr() + offset;
+    return json_out ? put(json, json_out, cap) : 0;
+  });
 }
 
 int trims_import_read_only(trims_import* im) { return im && im->map && im->map->read_only() ? 1 : 0; }
 
-int trims_import_verify(trims_import* im, uint64_t* checksum_out) {
+int trims_import_verify(trims_import* im, uint64_t offset, uint64_t generation, uint64_t payload_bytes,
+                        uint64_t* checksum_out) {
   return guard([&] {
+    SegTail st = read_tail(im, offset, generation, payload_bytes, nullptr);
     DeviceGuard g(im->device);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, im->device);
@@ -496,7 +515,7 @@ int trims_import_verify(trims_import* im, uint64_t* checksum_out) {
     unsigned long long h = 0;
     try {
       TRIMS_CUDA(cudaMemset(d, 0, sizeof *d));
-      ingest::launch_checksum(im->map->ptr(), im->blob_bytes, 0, d, nullptr, sms);
+      ingest::launch_checksum(im->map->ptr() + offset, st.blob_bytes, 0, d, nullptr, sms);
       TRIMS_CUDA(cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost));
     } catch (...) {
       cudaFree(d);
@@ -504,7 +523,7 @@ int trims_import_verify(trims_import* im, uint64_t* checksum_out) {
     }
     cudaFree(d);
     if (checksum_out) *checksum_out = h;
-    if (h != im->checksum) raise(Errc::Corrupt, "resident blob checksum mismatch on attach");
+    if (h != st.checksum) raise(Errc::Corrupt, "resident blob checksum mismatch on attach");
     return 0;
   });
 }

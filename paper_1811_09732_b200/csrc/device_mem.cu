@@ -176,6 +176,56 @@ Import::~Import() {
   }
 }
 
+DeviceArena::DeviceArena(int device, uint64_t bytes) {
+  seg_ = DeviceSegment::create(device, std::max<uint64_t>(bytes, kGranule));
+  free_[0] = seg_.size();
+}
+
+bool DeviceArena::alloc(uint64_t bytes, uint64_t* offset, uint64_t* reserved) {
+  const uint64_t need = std::max<uint64_t>(kGranule, (bytes + kGranule - 1) / kGranule * kGranule);
+  std::lock_guard lk(mu_);
+  for (auto it = free_.begin(); it != free_.end(); ++it) {
+    if (it->second < need) continue;
+    const uint64_t off = it->first, len = it->second;
+    free_.erase(it);
+    if (len > need) free_[off + need] = len - need;
+    used_[off] = need;
+    *offset = off;
+    *reserved = need;
+    return true;
+  }
+  return false;
+}
+
+void DeviceArena::free(uint64_t off) {
+  std::lock_guard lk(mu_);
+  auto u = used_.find(off);
+  if (u == used_.end()) return;
+  uint64_t len = u->second;
+  used_.erase(u);
+  auto next = free_.lower_bound(off);
+  if (next != free_.end() && next->first == off + len) {
+    len += next->second;
+    free_.erase(next);
+  }
+  auto it = free_.lower_bound(off);
+  if (it != free_.begin()) {
+    auto prev = std::prev(it);
+    if (prev->first + prev->second == off) {
+      prev->second += len;
+      return;
+    }
+  }
+  free_[off] = len;
+}
+
+uint64_t DeviceArena::free_bytes() {
+  std::lock_guard lk(mu_);
+  uint64_t f = 0;
+  for (auto& [o, l] : free_) f += l;
+  return f;
+}
+
 PinnedPool::PinnedPool(uint64_t bytes) {
   cap_ = (bytes + kGranule - 1) / kGranule * kGranule;
   if (!cap_) return;

@@ -85,6 +85,30 @@ class DeviceSegment {
   int device_{0};
 };
 
+// The fast tier's HBM arena: ONE exportable cuMem allocation sized to the
+// tier's capacity, carved first-fit into model segments. Publishing a model
+// costs no driver allocation call, and a client process maps the arena once
+// (one fd, read-only) and then reaches every model by offset. Reuse of a
+// freed range is detected by importers through the tail's generation
+// (the reference's StaleGeneration check, shared_segment.cpp:233-237).
+class DeviceArena {
+ public:
+  static constexpr uint64_t kGranule = 64ull << 10;
+  DeviceArena(int device, uint64_t bytes);
+  // Returns false when no free extent fits (caller falls back to a dedicated segment).
+  bool alloc(uint64_t bytes, uint64_t* offset, uint64_t* reserved);
+  void free(uint64_t offset);
+  uint8_t* base() const { return seg_.ptr(); }
+  uint64_t size() const { return seg_.size(); }
+  int fd() const { return seg_.fd(); }
+  uint64_t free_bytes();
+
+ private:
+  DeviceSegment seg_;
+  std::mutex mu_;
+  std::map<uint64_t, uint64_t> free_, used_;
+};
+
 // Client-side read-only mapping of an exported segment.
 class Import {
  public:

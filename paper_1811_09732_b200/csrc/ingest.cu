@@ -24,6 +24,8 @@ constexpr int kUnroll = 4;                    // 128-bit loads in flight per thr
 constexpr int kStages = 3;                    // TMA ring depth
 constexpr uint32_t kStageBytes = 32u << 10;   // raw source bytes per staged tile
 constexpr uint32_t kStageAlloc = kStageBytes + 128;  // + 16-byte realignment slack, 128-aligned stages
+constexpr int kConsumerWarps = 16;                  // TMA kernel: 1 producer warp + 16 consumer warps
+constexpr int kTmaThreads = 32 * (kConsumerWarps + 1);
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -362,82 +364,98 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32
                : "memory");
 }
 
+// Warp-specialised: warp 0 is the producer (one elected lane issues the bulk
+// copies and recycles ring stages through `empty` mbarriers); kConsumerWarps
+// warps convert / permute / hash straight out of shared memory. No CTA-wide
+// barrier on the steady path: every consumer warp reduces its checksum with
+// shuffles and adds it with one atomic per tile.
 template <int S, int D>
-__global__ void __launch_bounds__(kThreads) transform_tma_kernel(const Tile* __restrict__ tiles, uint32_t ntiles,
-                                                                 const uint8_t* __restrict__ src,
-                                                                 uint8_t* __restrict__ dst,
-                                                                 unsigned long long* __restrict__ sums) {
+__global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* __restrict__ tiles, uint32_t ntiles,
+                                                                    const uint8_t* __restrict__ src,
+                                                                    uint8_t* __restrict__ dst,
+                                                                    unsigned long long* __restrict__ sums) {
   using ST = typename Bits<S>::T;
-  using DT = typename Bits<D>::T;
   constexpr int DS = esize<D>(), SS = esize<S>(), EPW = 8 / DS;
+  constexpr uint32_t kC = kConsumerWarps * 32;  // consumer threads
   extern __shared__ __align__(128) uint8_t ring[];
-  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ Tile staged[kStages];
-  __shared__ unsigned long long red[kThreads / 32];
 
   const uint32_t first = blockIdx.x, stride = gridDim.x;
   const uint32_t mine = first < ntiles ? (ntiles - first + stride - 1) / stride : 0;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  auto issue = [&](uint32_t j) {  // thread 0: stage tile j of this CTA
-    const int s = int(j % kStages);
-    const Tile t = tiles[first + j * stride];
-    staged[s] = t;
-    const uint64_t b = t.src_off & ~15ull, e = (t.src_off + uint64_t(t.n_elem) * SS + 15) & ~15ull;
-    mbar_expect_tx(&full[s], uint32_t(e - b));
-    bulk_g2s(ring + s * kStageAlloc, src + b, uint32_t(e - b), &full[s]);
-  };
-  if (threadIdx.x == 0)
-    for (uint32_t j = 0; j < mine && j < uint32_t(kStages); ++j) issue(j);
 
+  if (warp == 0) {  // ---------------- producer
+    if (lane == 0) {
+      for (uint32_t j = 0; j < mine; ++j) {
+        const int s = int(j % kStages);
+        if (j >= uint32_t(kStages)) mbar_wait(&empty[s], ((j / kStages) - 1) & 1);
+        const Tile t = tiles[first + j * stride];
+        staged[s] = t;
+        const uint64_t b = t.src_off & ~15ull, e = (t.src_off + uint64_t(t.n_elem) * SS + 15) & ~15ull;
+        mbar_expect_tx(&full[s], uint32_t(e - b));
+        bulk_g2s(ring + s * kStageAlloc, src + b, uint32_t(e - b), &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers
+  const uint32_t ct = threadIdx.x - 32, cw = warp - 1;
   for (uint32_t j = 0; j < mine; ++j) {
     const int s = int(j % kStages);
     mbar_wait(&full[s], (j / kStages) & 1);
     const Tile t = staged[s];
-    const uint8_t* raw = ring + s * kStageAlloc + (t.src_off & 15);
-    const ST* rs_elems = reinterpret_cast<const ST*>(raw);
+    const ST* el = reinterpret_cast<const ST*>(ring + s * kStageAlloc + (t.src_off & 15));
     uint64_t* d = reinterpret_cast<uint64_t*>(dst + t.dst_off);
     const uint64_t gw0 = t.dst_off >> 3;
     const uint32_t words = t.dst_bytes >> 3, n = t.n_elem;
     uint64_t acc = 0;
     if (t.op == OP_CVT) {
       const bool vec = ((t.src_off & 15) % (EPW * SS)) == 0;
-      for (uint32_t w = threadIdx.x; w < words; w += kThreads) {
+#pragma unroll 2
+      for (uint32_t w = ct; w < words; w += kC) {
         const uint32_t e0 = w * EPW;
         uint64_t word = 0;
         if (e0 + EPW <= n && vec) {
           ST v[EPW];
           if constexpr (EPW * SS >= 16) {
 #pragma unroll
-            for (int i = 0; i < EPW * SS / 16; ++i)
-              reinterpret_cast<uint4*>(v)[i] = reinterpret_cast<const uint4*>(rs_elems + e0)[i];
+            for (int i = 0; i < EPW * SS / 16; ++i) reinterpret_cast<uint4*>(v)[i] = reinterpret_cast<const uint4*>(el + e0)[i];
           } else if constexpr (EPW * SS == 8) {
-            *reinterpret_cast<uint2*>(v) = *reinterpret_cast<const uint2*>(rs_elems + e0);
+            *reinterpret_cast<uint2*>(v) = *reinterpret_cast<const uint2*>(el + e0);
           } else {
 #pragma unroll
-            for (int q = 0; q < EPW; ++q) v[q] = rs_elems[e0 + q];
+            for (int q = 0; q < EPW; ++q) v[q] = el[e0 + q];
           }
 #pragma unroll
           for (int q = 0; q < EPW; ++q) word |= uint64_t(cvt<S, D>(v[q])) << (8 * DS * q);
         } else {
-          for (int q = 0; q < EPW && e0 + q < n; ++q) word |= uint64_t(cvt<S, D>(rs_elems[e0 + q])) << (8 * DS * q);
+          for (int q = 0; q < EPW && e0 + q < n; ++q) word |= uint64_t(cvt<S, D>(el[e0 + q])) << (8 * DS * q);
         }
         d[w] = word;
         acc += word_hash(word, gw0 + w);
       }
     } else {  // OP_PERM: source [g][C][RS] in smem -> resident [g][RS][C]
       const uint32_t C = t.C, RS = t.RS, CRS = C * RS;
+      uint32_t body = 0;  // words written by the fast paths below
       if ((C * DS) % 8 == 0) {
         const uint32_t wpr = C / EPW, rows = (n / CRS) * RS;
-        const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        for (uint32_t row = warp; row < rows; row += kThreads / 32) {
+        body = rows * wpr;
+        for (uint32_t row = cw; row < rows; row += kConsumerWarps) {
           const uint32_t k = row / RS, r = row - k * RS;
-          const ST* col = rs_elems + k * CRS + r;
+          const ST* col = el + k * CRS + r;
           uint64_t* drow = d + uint64_t(row) * wpr;
           const uint64_t gwr = gw0 + uint64_t(row) * wpr;
+#pragma unroll 2
           for (uint32_t wi = lane; wi < wpr; wi += 32) {
             const ST* e = col + wi * EPW * RS;
             uint64_t word = 0;
@@ -447,13 +465,14 @@ __global__ void __launch_bounds__(kThreads) transform_tma_kernel(const Tile* __r
             acc += word_hash(word, gwr + wi);
           }
         }
-      } else {
-        for (uint32_t w = threadIdx.x; w < n * DS / 8; w += kThreads) {
-          uint32_t o = w * EPW, k = o / CRS, rem = o - k * CRS, r = rem / C, c = rem - r * C;
-          uint64_t word = 0;
-#pragma unroll
-          for (int q = 0; q < EPW; ++q) {
-            word |= uint64_t(cvt<S, D>(rs_elems[k * CRS + c * RS + r])) << (8 * DS * q);
+      }
+      for (uint32_t w = body + ct; w < words; w += kC) {  // generic path, partial word, pad
+        const uint32_t o = w * EPW;
+        uint64_t word = 0;
+        if (o < n) {
+          uint32_t k = o / CRS, rem = o - k * CRS, r = rem / C, c = rem - r * C;
+          for (int q = 0; q < EPW && o + q < n; ++q) {
+            word |= uint64_t(cvt<S, D>(el[k * CRS + c * RS + r])) << (8 * DS * q);
             if (++c == C) {
               c = 0;
               if (++r == RS) {
@@ -462,26 +481,18 @@ __global__ void __launch_bounds__(kThreads) transform_tma_kernel(const Tile* __r
               }
             }
           }
-          d[w] = word;
-          acc += word_hash(word, gw0 + w);
-        }
-      }
-      for (uint32_t w = n * DS / 8 + threadIdx.x; w < words; w += kThreads) {  // tail: partial word + pad
-        const uint32_t o = w * EPW;
-        uint64_t word = 0;
-        for (int q = 0; q < EPW && o + q < n; ++q) {
-          uint32_t oo = o + q, k = oo / CRS, rem = oo - k * CRS, r = rem / C, c = rem - r * C;
-          word |= uint64_t(cvt<S, D>(rs_elems[k * CRS + c * RS + r])) << (8 * DS * q);
         }
         d[w] = word;
         acc += word_hash(word, gw0 + w);
       }
     }
-    acc = block_sum(acc, red);  // its barriers also retire every read of ring stage s
-    if (threadIdx.x == 0) {
-      atomicAdd(&sums[t.tensor], (unsigned long long)acc);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async overwrite
-      if (j + kStages < mine) issue(j + kStages);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __syncwarp();  // every lane's shared-memory reads of stage s are done
+    if (lane == 0) {
+      if (acc) atomicAdd(&sums[t.tensor], (unsigned long long)acc);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async overwrite
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
     }
   }
 }
@@ -705,7 +716,7 @@ uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, co
       if (!fn) raise(Errc::InvalidArgument, "unsupported dtype pair in plan");
       const int smem = kStages * kStageAlloc;
       TRIMS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      fn<<<std::min<uint32_t>(n, sm_count * 2), kThreads, smem, stream>>>(t, n, src, dst, d_sums);
+      fn<<<std::min<uint32_t>(n, sm_count * 2), kTmaThreads, smem, stream>>>(t, n, src, dst, d_sums);
     } else {
       TransformFn fn = pair_kernel(g.sdt, g.ddt);
       if (!fn) raise(Errc::InvalidArgument, "unsupported dtype pair in plan");

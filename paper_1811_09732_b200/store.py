@@ -37,6 +37,7 @@ class StoreOptions:
     pinned_pool_bytes: int = 0         # 0 = host_capacity_bytes
     scan_disk: bool = True
     read_threads: int = 8
+    arena_bytes: int = 0               # 0 = auto (fast capacity + slack), 1 = one allocation per model
 
     @property
     def plan_flags(self) -> int:
@@ -61,6 +62,7 @@ class Store:
         cfg.pinned_pool_bytes = opts.pinned_pool_bytes
         cfg.scan_disk = int(opts.scan_disk)
         cfg.read_threads = opts.read_threads
+        cfg.arena_bytes = opts.arena_bytes
         h = ctypes.c_void_p()
         check(lib.trims_store_create(ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h

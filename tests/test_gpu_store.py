@@ -129,17 +129,17 @@ def test_converting_store_bit_exact_and_import_path(tmp_path):
         via_fd.close_all_imports()
 
 
-def _child_attach(conn, device: int, alloc: int, gen: int, payload: int, digest: bytes, q):
+def _child_attach(conn, device: int, alloc: int, offset: int, gen: int, payload: int, digest: bytes, q):
     try:
         import ctypes
         from multiprocessing.reduction import recv_handle
 
         from paper_1811_09732_b200._lib import lib
         fd = recv_handle(conn)  # SCM_RIGHTS over the pipe: the fd of the cuMem allocation
-        imp, ptr, mj = import_segment(device, fd, alloc, gen, payload, digest)
+        imp, ptr, mj = import_segment(device, fd, alloc, offset, gen, payload, digest)
         os.close(fd)
         cs = ctypes.c_uint64()
-        rc = lib.trims_import_verify(imp, ctypes.byref(cs))
+        rc = lib.trims_import_verify(imp, offset, gen, payload, ctypes.byref(cs))
         ro = lib.trims_import_read_only(imp)
         q.put((rc, cs.value, ro, len(mj)))
         lib.trims_import_close(imp)
@@ -160,8 +160,9 @@ def test_multiprocess_one_copy(tiny_dir):
             ex = s.open(key("vgg16"))
             exps.append(ex)
             parent, child = ctx.Pipe()
-            p = ctx.Process(target=_child_attach, args=(child, ex.device, ex.alloc_bytes, ex.generation,
-                                                        ex.payload_bytes, bytes(ex.manifest_digest), q))
+            p = ctx.Process(target=_child_attach, args=(child, ex.device, ex.alloc_bytes, ex.segment_offset,
+                                                        ex.generation, ex.payload_bytes, bytes(ex.manifest_digest),
+                                                        q))
             p.start()
             send_handle(parent, ex.fd, p.pid)
             procs.append((p, parent, child))
@@ -194,4 +195,39 @@ def test_views_survive_eviction(tiny_dir):
         n = v.blob_bytes()
         t = TensorView("b", [n], "i8", "native", 0, n, v.base_ptr).torch("cuda:0").view(torch.uint8).cpu().numpy()
         assert F.sha256(t).hex() == g["googlenet"]["trailer"]
+        cli.close_all_imports()
+
+
+def test_arena_reuse_is_detected_as_stale_generation(tiny_dir):
+    """A freed arena range re-used by another model: attaching with the old
+    generation fails with StaleGeneration (shared_segment.cpp:233-237)."""
+    from paper_1811_09732_b200.client import attach_segment, map_allocation
+    from paper_1811_09732_b200._lib import lib
+    with Store(StoreOptions(disk_cache_dir=tiny_dir, fast_capacity_bytes=5 * MB, host_capacity_bytes=64 * MB)) as s:
+        a = s.open(key("alexnet"))
+        s.close(key("alexnet"))
+        fd = os.dup(a.fd)
+        imp, base = map_allocation(a.device, fd, a.alloc_bytes)
+        os.close(fd)
+        ptr, js = attach_segment(imp, a.segment_offset, a.generation, a.payload_bytes, bytes(a.manifest_digest))
+        assert ptr == base + a.segment_offset and json.loads(js)["name"] == "alexnet"
+        b = s.open(key("googlenet"))  # 5 MB tier: alexnet (3.7 MB) is evicted, its range reused
+        assert b.segment_offset == a.segment_offset and b.generation != a.generation
+        with pytest.raises(TrimsError) as ei:
+            attach_segment(imp, a.segment_offset, a.generation, a.payload_bytes, bytes(a.manifest_digest))
+        assert ei.value.code == Errc.StaleGeneration
+        lib.trims_import_close(imp)
+        s.close(key("googlenet"))
+
+
+def test_dedicated_segments_without_arena(tiny_dir):
+    import torch
+    g = {e["name"]: e for e in load("catalog.json.gz")["tiny_seed1"]}
+    with Store(StoreOptions(disk_cache_dir=tiny_dir, fast_capacity_bytes=64 * MB, host_capacity_bytes=64 * MB,
+                            arena_bytes=1)) as s:
+        cli = Client(s, attach_via_import=True)
+        v = cli.open(key("squeezenet-v1.1"), force_shared=True)
+        assert v.export.segment_offset == 0
+        assert F.sha256(d2h(v, torch)).hex() == g["squeezenet-v1.1"]["trailer"]
+        cli.close(v)
         cli.close_all_imports()
