@@ -125,7 +125,7 @@ double tro_share_benefit(double bytes, double n_objects, double q, double o, dou
 /* ---------------- conversions (our definition; parity unpinned) ---------------- */
 
 uint16_t tro_f32_to_bf16_1(uint32_t u) {
-  if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)(((u >> 16) & 0x8000u) | 0x7fc0u);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)0x7fffu; /* canonical NaN */
   uint32_t lsb = (u >> 16) & 1u;
   return (uint16_t)((u + 0x7fffu + lsb) >> 16);
 }
@@ -150,7 +150,7 @@ void tro_f64_to_f32(const double* src, uint64_t n, float* dst) {
 static uint16_t f64_to_bf16_1(uint64_t u) {
   uint16_t sign = (uint16_t)((u >> 48) & 0x8000u);
   uint64_t e = (u >> 52) & 0x7ff, m = u & ((1ull << 52) - 1);
-  if (e == 0x7ff) return m ? (uint16_t)(sign | 0x7fc0u) : (uint16_t)(sign | 0x7f80u);
+  if (e == 0x7ff) return m ? (uint16_t)0x7fffu : (uint16_t)(sign | 0x7f80u);
   if (e == 0) return sign; /* f64 subnormals are far below bf16's range */
   int64_t eb = (int64_t)e - 1023 + 127;
   if (eb >= 255) return (uint16_t)(sign | 0x7f80u);

@@ -45,9 +45,10 @@ double tro_share_benefit(double bytes, double n_objects, double q, double o, dou
 
 /* ---- transforms with no reference counterpart (parity unpinned) ---- */
 
-/* fp32 -> bf16, round-to-nearest-even. NaN -> quiet NaN keeping the sign
- * (0x7fc0 | sign); +-Inf and +-0 preserved; values that round past the
- * largest finite bf16 become +-Inf (IEEE RNE overflow). */
+/* fp32 -> bf16, round-to-nearest-even. NaN -> the canonical bf16 NaN 0x7fff
+ * (what B200's cvt.rn.bf16x2.f32 produces; scripts/probe_cvt.cu); +-Inf and
+ * +-0 preserved; values that round past the largest finite bf16 become +-Inf
+ * (IEEE RNE overflow). f64 -> bf16 uses the same NaN encoding. */
 uint16_t tro_f32_to_bf16_1(uint32_t bits);
 void tro_f32_to_bf16(const uint32_t* src, uint64_t n, uint16_t* dst);
 /* f64 -> f32 (IEEE RNE, the C cast; NaN -> 0x7fc00000 | sign) and f64 -> bf16 (via a single rounding

@@ -7,7 +7,9 @@
 // conversions are integer-defined so they are bit-identical to the CPU oracle
 // (oracle/trims_oracle.c) — no reliance on hardware NaN canonicalisation.
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
+#include <string>
 
 #include "cuda_util.hpp"
 #include "ingest.hpp"
@@ -43,15 +45,26 @@ template <> struct Bits<3> { using T = uint8_t; };
 template <> struct Bits<4> { using T = uint16_t; };
 template <int DT> constexpr int esize() { return int(sizeof(typename Bits<DT>::T)); }
 
+// bf16 NaN encoding is the canonical 0x7fff: what the B200 cvt.rn.bf16x2.f32
+// instruction produces (probed: scripts/probe_cvt.cu, 4M values, no other
+// difference from integer RNE), so the hardware pair-convert below and these
+// scalar integer paths agree bit for bit.
 __device__ __forceinline__ uint16_t f32_to_bf16(uint32_t u) {
-  if ((u & 0x7fffffffu) > 0x7f800000u) return uint16_t(((u >> 16) & 0x8000u) | 0x7fc0u);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return uint16_t(0x7fffu);
   return uint16_t((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+}
+
+// Two fp32 -> packed bf16x2 (x0 in the low half) in one instruction.
+__device__ __forceinline__ uint32_t f32x2_to_bf16x2(uint32_t x0, uint32_t x1) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float(x1)), "f"(__uint_as_float(x0)));
+  return r;
 }
 
 __device__ __forceinline__ uint16_t f64_to_bf16(uint64_t u) {
   uint16_t sign = uint16_t((u >> 48) & 0x8000u);
   uint64_t e = (u >> 52) & 0x7ff, m = u & ((1ull << 52) - 1);
-  if (e == 0x7ff) return m ? uint16_t(sign | 0x7fc0u) : uint16_t(sign | 0x7f80u);
+  if (e == 0x7ff) return m ? uint16_t(0x7fffu) : uint16_t(sign | 0x7f80u);
   if (e == 0) return sign;
   int64_t eb = int64_t(e) - 1023 + 127;
   if (eb >= 255) return uint16_t(sign | 0x7f80u);
@@ -214,7 +227,8 @@ __device__ uint64_t tile_perm(const Tile& t, const uint8_t* src, uint8_t* dst, u
   const uint8_t* s = src + t.src_off;
   DT* sm = reinterpret_cast<DT*>(smem);
   const uint32_t n = t.n_elem, C = t.C, RS = t.RS, CRS = C * RS;
-  const bool gather = t.pad_ != 0;  // slice too large for smem: read the source directly
+  // slice group too large for this path's smem: read the source directly
+  const bool gather = t.pad_ != 0 || uint64_t(n) * DS > kPermSmem;
   // phase 1: coalesced vector loads in source order -> converted in smem
   const uint32_t groups = gather ? 0 : n / EPW;
   for (uint32_t base = threadIdx.x; base < groups; base += kThreads * kUnroll) {
@@ -364,6 +378,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32
                : "memory");
 }
 
+// One resident word from EPW source elements (element 0 in the low bits).
+template <int S, int D, int N>
+__device__ __forceinline__ uint64_t pack_word(const typename Bits<S>::T (&v)[N]) {
+  if constexpr (S == 1 && D == 4 && N == 4) {
+    return uint64_t(f32x2_to_bf16x2(v[0], v[1])) | (uint64_t(f32x2_to_bf16x2(v[2], v[3])) << 32);
+  } else {
+    uint64_t word = 0;
+#pragma unroll
+    for (int q = 0; q < N; ++q) word |= uint64_t(cvt<S, D>(v[q])) << (8 * esize<D>() * q);
+    return word;
+  }
+}
+
 // Warp-specialised: warp 0 is the producer (one elected lane issues the bulk
 // copies and recycles ring stages through `empty` mbarriers); kConsumerWarps
 // warps convert / permute / hash straight out of shared memory. No CTA-wide
@@ -436,8 +463,7 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
 #pragma unroll
             for (int q = 0; q < EPW; ++q) v[q] = el[e0 + q];
           }
-#pragma unroll
-          for (int q = 0; q < EPW; ++q) word |= uint64_t(cvt<S, D>(v[q])) << (8 * DS * q);
+          word = pack_word<S, D>(v);
         } else {
           for (int q = 0; q < EPW && e0 + q < n; ++q) word |= uint64_t(cvt<S, D>(el[e0 + q])) << (8 * DS * q);
         }
@@ -458,9 +484,10 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
 #pragma unroll 2
           for (uint32_t wi = lane; wi < wpr; wi += 32) {
             const ST* e = col + wi * EPW * RS;
-            uint64_t word = 0;
+            ST v[EPW];
 #pragma unroll
-            for (int q = 0; q < EPW; ++q) word |= uint64_t(cvt<S, D>(e[q * RS])) << (8 * DS * q);
+            for (int q = 0; q < EPW; ++q) v[q] = e[q * RS];
+            const uint64_t word = pack_word<S, D>(v);
             drow[wi] = word;
             acc += word_hash(word, gwr + wi);
           }
@@ -671,8 +698,21 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
     if (t.op == OP_HASH) return t.src_off + t.dst_bytes;
     return t.src_off + uint64_t(t.n_elem) * fmt::element_size(fmt::DType(t.sdt));
   };
-  // kernel key: hash | (TMA ring or gather) x dtype pair
-  auto kind_of = [](const Tile& t) -> uint8_t { return t.op == OP_HASH ? 0 : (t.pad_ ? 2 : 1); };
+  // kernel key: hash | (TMA ring or direct) x dtype pair. TRIMS_CVT_PATH /
+  // TRIMS_PERM_PATH = "direct" | "tma" select the kernel per op (A/B switch).
+  static const bool cvt_direct = [] {
+    const char* e = std::getenv("TRIMS_CVT_PATH");
+    return e && std::string(e) == "direct";
+  }();
+  static const bool perm_direct = [] {
+    const char* e = std::getenv("TRIMS_PERM_PATH");
+    return e && std::string(e) == "direct";
+  }();
+  auto kind_of = [](const Tile& t) -> uint8_t {
+    if (t.op == OP_HASH) return 0;
+    if (t.pad_) return 2;
+    return (t.op == OP_CVT ? cvt_direct : perm_direct) ? 2 : 1;
+  };
   auto key_of = [&](const Tile& t) { return uint32_t(kind_of(t)) << 16 | uint32_t(t.sdt) << 8 | t.ddt; };
   auto group_range = [&](std::vector<Tile>& v, uint32_t b, uint32_t e, std::vector<Group>& out) {
     std::stable_sort(v.begin() + b, v.begin() + e, [&](const Tile& x, const Tile& y) { return key_of(x) < key_of(y); });

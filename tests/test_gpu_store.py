@@ -211,13 +211,13 @@ def test_arena_reuse_is_detected_as_stale_generation(tiny_dir):
         os.close(fd)
         ptr, js = attach_segment(imp, a.segment_offset, a.generation, a.payload_bytes, bytes(a.manifest_digest))
         assert ptr == base + a.segment_offset and json.loads(js)["name"] == "alexnet"
-        b = s.open(key("googlenet"))  # 5 MB tier: alexnet (3.7 MB) is evicted, its range reused
+        b = s.open(key("resnet50"))  # 3.7 + 1.5 MB > 5 MB: alexnet evicted, its range reused
         assert b.segment_offset == a.segment_offset and b.generation != a.generation
         with pytest.raises(TrimsError) as ei:
             attach_segment(imp, a.segment_offset, a.generation, a.payload_bytes, bytes(a.manifest_digest))
         assert ei.value.code == Errc.StaleGeneration
         lib.trims_import_close(imp)
-        s.close(key("googlenet"))
+        s.close(key("resnet50"))
 
 
 def test_dedicated_segments_without_arena(tiny_dir):
