@@ -431,7 +431,15 @@ void CudaTierBackend::evict_fast(uint64_t model_id) {
     victim = std::move(it->second);
     fast_.erase(it);
   }
-  // Importers' mappings keep the physical memory alive (views survive).
+  if (victim->arena) {
+    // The range returns to the arena: scrub the sealed tail so an importer
+    // holding the old (offset, generation) can never validate it again, even
+    // when the next occupant is shorter and leaves these bytes untouched.
+    DeviceGuard g(cfg_.device, /*nothrow=*/true);
+    const uint64_t payload = victim->resident.blob_bytes + victim->json.size() + 8;
+    cudaMemset(victim->base() + payload, 0, sizeof(SegTail));
+  }
+  // A dedicated segment's physical memory lives on in importers' mappings.
 }
 
 void CudaTierBackend::evict_host(uint64_t model_id) {

@@ -23,9 +23,29 @@ constexpr int kThreads = 256;
 constexpr uint32_t kHashTile = 64u << 10;     // bytes per OP_HASH tile
 constexpr uint32_t kPermSmem = 24u << 10;     // smem of the direct (non-TMA) permute path
 constexpr int kUnroll = 4;                    // 128-bit loads in flight per thread (direct paths)
-constexpr int kStages = 3;                    // TMA ring depth
-constexpr uint32_t kStageBytes = 32u << 10;   // raw source bytes per staged tile
-constexpr uint32_t kStageAlloc = kStageBytes + 128;  // + 16-byte realignment slack, 128-aligned stages
+constexpr int kMaxStages = 16;                // TMA ring depth limit (runtime depth <= this)
+
+// TMA ring geometry (host side): stage bytes = raw source bytes per tile,
+// depth, CTAs per SM. Defaults tuned on B200; TRIMS_TMA_{STAGE_KB,STAGES,CTAS}
+// override them for sweeps (scripts/prof_transform.py).
+struct RingCfg {
+  uint32_t stage_bytes, stages, ctas_per_sm;
+  uint32_t stage_alloc() const { return stage_bytes + 128; }  // + 16-byte realignment slack, 128-aligned
+};
+const RingCfg& ring_cfg() {
+  static const RingCfg c = [] {
+    auto env = [](const char* k, uint32_t d) {
+      const char* v = std::getenv(k);
+      return v ? uint32_t(std::strtoul(v, nullptr, 10)) : d;
+    };
+    // 64 KiB x 3 stages x 1 CTA/SM won the sweep (scripts/sweep_ring.sh): the
+    // per-tile fixed cost dominates below 32 KiB stages.
+    RingCfg r{env("TRIMS_TMA_STAGE_KB", 64) << 10, env("TRIMS_TMA_STAGES", 3), env("TRIMS_TMA_CTAS", 1)};
+    r.stages = std::max(2u, std::min<uint32_t>(r.stages, kMaxStages));
+    return r;
+  }();
+  return c;
+}
 constexpr int kConsumerWarps = 16;                  // TMA kernel: 1 producer warp + 16 consumer warps
 constexpr int kTmaThreads = 32 * (kConsumerWarps + 1);
 
@@ -349,7 +369,7 @@ __global__ void __launch_bounds__(kThreads) hash_tiles_kernel(const Tile* __rest
 
 // ---------------------------------------------------------------------------
 // TMA-staged variant (the production path): each persistent CTA streams its
-// tiles' raw source bytes into a kStages-deep shared-memory ring with 1-D bulk
+// tiles' raw source bytes into a multi-stage shared-memory ring with 1-D bulk
 // async copies (cp.async.bulk, mbarrier complete_tx), and converts / permutes
 // straight out of shared memory while the next tiles are in flight.
 
@@ -400,19 +420,20 @@ template <int S, int D>
 __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* __restrict__ tiles, uint32_t ntiles,
                                                                     const uint8_t* __restrict__ src,
                                                                     uint8_t* __restrict__ dst,
-                                                                    unsigned long long* __restrict__ sums) {
+                                                                    unsigned long long* __restrict__ sums,
+                                                                    uint32_t stages, uint32_t stage_alloc) {
   using ST = typename Bits<S>::T;
   constexpr int DS = esize<D>(), SS = esize<S>(), EPW = 8 / DS;
   constexpr uint32_t kC = kConsumerWarps * 32;  // consumer threads
   extern __shared__ __align__(128) uint8_t ring[];
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-  __shared__ Tile staged[kStages];
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+  __shared__ Tile staged[kMaxStages];
 
   const uint32_t first = blockIdx.x, stride = gridDim.x;
   const uint32_t mine = first < ntiles ? (ntiles - first + stride - 1) / stride : 0;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (uint32_t s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
     }
@@ -422,14 +443,16 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
 
   if (warp == 0) {  // ---------------- producer
     if (lane == 0) {
+      Tile next = mine ? tiles[first] : Tile{};
       for (uint32_t j = 0; j < mine; ++j) {
-        const int s = int(j % kStages);
-        if (j >= uint32_t(kStages)) mbar_wait(&empty[s], ((j / kStages) - 1) & 1);
-        const Tile t = tiles[first + j * stride];
+        const uint32_t s = j % stages;
+        const Tile t = next;
+        if (j + 1 < mine) next = tiles[first + (j + 1) * stride];  // descriptor prefetch overlaps the wait
+        if (j >= stages) mbar_wait(&empty[s], ((j / stages) - 1) & 1);
         staged[s] = t;
         const uint64_t b = t.src_off & ~15ull, e = (t.src_off + uint64_t(t.n_elem) * SS + 15) & ~15ull;
         mbar_expect_tx(&full[s], uint32_t(e - b));
-        bulk_g2s(ring + s * kStageAlloc, src + b, uint32_t(e - b), &full[s]);
+        bulk_g2s(ring + s * stage_alloc, src + b, uint32_t(e - b), &full[s]);
       }
     }
     return;
@@ -438,10 +461,10 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
   // ---------------- consumers
   const uint32_t ct = threadIdx.x - 32, cw = warp - 1;
   for (uint32_t j = 0; j < mine; ++j) {
-    const int s = int(j % kStages);
-    mbar_wait(&full[s], (j / kStages) & 1);
+    const uint32_t s = j % stages;
+    mbar_wait(&full[s], (j / stages) & 1);
     const Tile t = staged[s];
-    const ST* el = reinterpret_cast<const ST*>(ring + s * kStageAlloc + (t.src_off & 15));
+    const ST* el = reinterpret_cast<const ST*>(ring + s * stage_alloc + (t.src_off & 15));
     uint64_t* d = reinterpret_cast<uint64_t*>(dst + t.dst_off);
     const uint64_t gw0 = t.dst_off >> 3;
     const uint32_t words = t.dst_bytes >> 3, n = t.n_elem;
@@ -518,15 +541,15 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
     __syncwarp();  // every lane's shared-memory reads of stage s are done
     if (lane == 0) {
       if (acc) atomicAdd(&sums[t.tensor], (unsigned long long)acc);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async overwrite
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
     }
   }
 }
 
 using TransformFn = void (*)(const Tile*, uint32_t, const uint8_t*, uint8_t*, unsigned long long*);
+using TmaFn = void (*)(const Tile*, uint32_t, const uint8_t*, uint8_t*, unsigned long long*, uint32_t, uint32_t);
 
-TransformFn pair_tma_kernel(int s, int d) {
+TmaFn pair_tma_kernel(int s, int d) {
   switch (s * 8 + d) {
     case 0 * 8 + 0: return transform_tma_kernel<0, 0>;
     case 1 * 8 + 1: return transform_tma_kernel<1, 1>;
@@ -655,8 +678,9 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
         uint64_t g = 1;
         while ((g * CRS * ds) % 8) ++g;
         // a slice group whose raw bytes exceed a ring stage is gathered straight from HBM
-        const bool gather = g * CRS * ss > kStageBytes;
-        while (!gather && 2 * g * CRS * ss <= kStageBytes && g * 2 <= K) g *= 2;
+        const uint64_t stage = ring_cfg().stage_bytes;
+        const bool gather = g * CRS * ss > stage;
+        while (!gather && 2 * g * CRS * ss <= stage && g * 2 <= K) g *= 2;
         p.has_perm = true;
         for (uint64_t k0 = 0; k0 < K; k0 += g) {
           const uint64_t kn = std::min(g, K - k0);
@@ -675,7 +699,7 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
           tiles.push_back(t);
         }
       } else {
-        const uint64_t per = kStageBytes / ss;  // one ring stage of source per tile
+        const uint64_t per = ring_cfg().stage_bytes / ss;  // one ring stage of source per tile
         for (uint64_t e0 = 0; e0 < n; e0 += per) {
           const uint64_t cnt = std::min<uint64_t>(per, n - e0);
           Tile t{};
@@ -700,9 +724,9 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
   };
   // kernel key: hash | (TMA ring or direct) x dtype pair. TRIMS_CVT_PATH /
   // TRIMS_PERM_PATH = "direct" | "tma" select the kernel per op (A/B switch).
-  static const bool cvt_direct = [] {
+  static const bool cvt_direct = [] {  // default: elementwise tiles take the direct-load kernel
     const char* e = std::getenv("TRIMS_CVT_PATH");
-    return e && std::string(e) == "direct";
+    return !(e && std::string(e) == "tma");
   }();
   static const bool perm_direct = [] {
     const char* e = std::getenv("TRIMS_PERM_PATH");
@@ -752,11 +776,13 @@ uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, co
     if (g.kind == 0) {
       hash_tiles_kernel<<<std::min<uint32_t>(n, sm_count * 8), kThreads, 0, stream>>>(t, n, dst, d_sums);
     } else if (g.kind == 1) {
-      TransformFn fn = pair_tma_kernel(g.sdt, g.ddt);
+      TmaFn fn = pair_tma_kernel(g.sdt, g.ddt);
       if (!fn) raise(Errc::InvalidArgument, "unsupported dtype pair in plan");
-      const int smem = kStages * kStageAlloc;
+      const RingCfg& rc = ring_cfg();
+      const int smem = int(rc.stages * rc.stage_alloc());
       TRIMS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      fn<<<std::min<uint32_t>(n, sm_count * 2), kTmaThreads, smem, stream>>>(t, n, src, dst, d_sums);
+      fn<<<std::min<uint32_t>(n, sm_count * rc.ctas_per_sm), kTmaThreads, smem, stream>>>(t, n, src, dst, d_sums,
+                                                                                          rc.stages, rc.stage_alloc());
     } else {
       TransformFn fn = pair_kernel(g.sdt, g.ddt);
       if (!fn) raise(Errc::InvalidArgument, "unsupported dtype pair in plan");
