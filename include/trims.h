@@ -211,6 +211,16 @@ int trims_fill_splitmix_device(uint64_t* dev, uint64_t n, uint64_t stream_seed, 
 int trims_fill_uniform_device(float* dev, uint64_t n, uint64_t stream_seed, uint64_t j0, float lo, float hi,
                               void* stream);
 
+/* ------------------------------------------- forward pass (K7, K8) */
+
+/* K7: D[M,N] = relu?(A[M,K] . B[N,K]^T * scale[n] + bias[n] + residual[m,n]),
+ * bf16 operands (row strides lda/ldb/ldd/ldr in elements, 16-byte aligned),
+ * fp32 accumulation in TMEM via tcgen05.mma; scale/bias/residual nullable.
+ * bn = output tile width 64/128/256 or 0 (auto). Async on `stream`. */
+int trims_gemm_bf16(const void* A, uint64_t M, uint64_t K, uint64_t lda, const void* B, uint64_t N, uint64_t ldb,
+                    void* D, uint64_t ldd, const float* scale, const float* bias, const void* residual, uint64_t ldr,
+                    int relu, int bn, void* stream);
+
 /* ------------------------------------------------------------ test hooks */
 
 /* Replays a decision trace through this library's CacheCore over an

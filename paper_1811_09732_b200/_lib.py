@@ -146,6 +146,8 @@ _SIGS = {
     "trims_fill_splitmix_device": (_c.c_int, [_p, _u64, _u64, _u64, _p]),
     "trims_fill_uniform_device": (_c.c_int, [_p, _u64, _u64, _u64, _c.c_float, _c.c_float, _p]),
     "trims_replay": (_c.c_int, [_s, _s, _u64]),
+    "trims_gemm_bf16": (_c.c_int, [_p, _u64, _u64, _u64, _p, _u64, _u64, _p, _u64, _p, _p, _p, _u64, _c.c_int,
+                                   _c.c_int, _p]),
 }
 
 

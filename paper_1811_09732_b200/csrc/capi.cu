@@ -16,6 +16,7 @@
 #include "cache_core.hpp"
 #include "cuda_util.hpp"
 #include "format.hpp"
+#include "gemm.hpp"
 #include "sha256.hpp"
 
 using namespace trims;
@@ -686,6 +687,17 @@ int trims_checksum_device(const void* dev, uint64_t nbytes, uint64_t word0, unsi
 int trims_fill_splitmix_device(uint64_t* dev, uint64_t n, uint64_t stream_seed, uint64_t k0, void* stream) {
   return guard([&] {
     ingest::launch_fill_splitmix(dev, n, stream_seed, k0, static_cast<cudaStream_t>(stream));
+    return 0;
+  });
+}
+
+int trims_gemm_bf16(const void* A, uint64_t M, uint64_t K, uint64_t lda, const void* B, uint64_t N, uint64_t ldb,
+                    void* D, uint64_t ldd, const float* scale, const float* bias, const void* residual, uint64_t ldr,
+                    int relu, int bn, void* stream) {
+  return guard([&] {
+    gemm::Epilogue e{static_cast<uint16_t*>(D), ldd, scale, bias, static_cast<const uint16_t*>(residual), ldr,
+                     relu != 0};
+    gemm::launch({A, M, K, lda}, {B, N, K, ldb}, e, static_cast<cudaStream_t>(stream), bn);
     return 0;
   });
 }

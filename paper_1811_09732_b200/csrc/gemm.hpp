@@ -1,0 +1,34 @@
+// gemm.hpp — host interface of the tcgen05 GEMM (K7).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace trims::gemm {
+
+// A K-major bf16 operand: `rows` rows of `k` elements, row stride `ld`
+// elements (ld*2 must be a multiple of 16 bytes; TMA zero-fills k..ceil64(k)).
+struct Operand {
+  const void* ptr;
+  uint64_t rows, k, ld;
+};
+
+// out[m, n] = relu?(acc * scale[n] + bias[n] + residual[m, n]) as bf16.
+struct Epilogue {
+  uint16_t* out;
+  uint64_t ldo;
+  const float* scale{nullptr};
+  const float* bias{nullptr};
+  const uint16_t* residual{nullptr};
+  uint64_t ldr{0};
+  bool relu{false};
+};
+
+CUtensorMap make_tmap(const void* ptr, uint64_t rows, uint64_t k, uint64_t ld, uint32_t box_rows);
+int pick_bn(uint64_t M, uint64_t N, int sms);
+// D = epi(A . B^T); bn = 0 picks the tile width.
+void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn = 0);
+
+}  // namespace trims::gemm

@@ -1,0 +1,41 @@
+"""K7 tcgen05 GEMM (bf16 in, fp32 TMEM accumulate, fused epilogue) vs a plain
+PyTorch fp32 reference of the same op. Tolerance: the output is rounded to
+bf16 once, so |out - ref| <= 2^-8 |ref| + 1e-3 * max|ref| (one bf16 ulp of
+the value plus fp32 summation-order noise)."""
+import pytest
+
+from paper_1811_09732_b200._lib import check, lib
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("M,N,K,bn", [
+    (128, 64, 64, 64), (256, 128, 128, 128), (300, 200, 96, 64), (1000, 256, 576, 256),
+    (49, 2048, 512, 64), (3136, 64, 576, 64), (17, 1000, 4096, 128), (777, 384, 2304, 128),
+    (512, 512, 1024, 256),
+])
+@pytest.mark.parametrize("epi", ["plain", "full"])
+def test_gemm_matches_fp32_reference(M, N, K, bn, epi):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    D = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    scale = bias = res = None
+    ref = A.float() @ B.float().T
+    if epi == "full":
+        scale = torch.rand(N, device="cuda", generator=g) + 0.5
+        bias = torch.randn(N, device="cuda", generator=g)
+        res = torch.randn(M, N, device="cuda", generator=g).to(torch.bfloat16)
+        ref = torch.relu(ref * scale + bias + res.float())
+    check(lib.trims_gemm_bf16(A.data_ptr(), M, K, K, B.data_ptr(), N, K, D.data_ptr(), N,
+                              scale.data_ptr() if scale is not None else None,
+                              bias.data_ptr() if bias is not None else None,
+                              res.data_ptr() if res is not None else None, N, int(epi == "full"), bn,
+                              torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    out = D.float()
+    assert torch.isfinite(out).all()
+    err = (out - ref).abs()
+    tol = ref.abs() * 2 ** -8 + 1e-3 * ref.abs().max()
+    assert (err <= tol).all(), f"max err {err.max().item()} (ref max {ref.abs().max().item()})"
