@@ -221,6 +221,23 @@ int trims_gemm_bf16(const void* A, uint64_t M, uint64_t K, uint64_t lda, const v
                     void* D, uint64_t ldd, const float* scale, const float* bias, const void* residual, uint64_t ldr,
                     int relu, int bn, void* stream);
 
+/* The compute on shared weights (replaces Client::touch, client.cpp:338-359):
+ * a CNN bound to a resident manifest whose bf16 KRSC weights start at
+ * `weights` (an attached segment). arch_text: one layer per line (written by
+ * paper_1811_09732_b200/models.py). The net owns its workspace, an fp32 NCHW
+ * input buffer and an fp32 logits buffer. */
+typedef struct trims_net trims_net;
+int trims_net_create(int device, const char* arch_text, const char* resident_json, const void* weights, int batch,
+                     trims_net** out);
+void trims_net_destroy(trims_net* net);
+int trims_net_buffers(trims_net* net, void** input, void** logits, int* classes, int* input_hw);
+/* One forward pass, async on `stream`; use_graph replays a captured CUDA graph. */
+int trims_net_run(trims_net* net, void* stream, int use_graph);
+/* flops per forward, kernel launches per forward, workspace bytes */
+int trims_net_info(trims_net* net, double out3[3]);
+/* row softmax of fp32 logits [M, N] (device pointers) */
+int trims_softmax(const float* in, float* out, int M, int N, void* stream);
+
 /* ------------------------------------------------------------ test hooks */
 
 /* Replays a decision trace through this library's CacheCore over an

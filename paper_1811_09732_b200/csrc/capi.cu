@@ -17,6 +17,7 @@
 #include "cuda_util.hpp"
 #include "format.hpp"
 #include "gemm.hpp"
+#include "nn.hpp"
 #include "sha256.hpp"
 
 using namespace trims;
@@ -698,6 +699,62 @@ int trims_gemm_bf16(const void* A, uint64_t M, uint64_t K, uint64_t lda, const v
     gemm::Epilogue e{static_cast<uint16_t*>(D), ldd, scale, bias, static_cast<const uint16_t*>(residual), ldr,
                      relu != 0};
     gemm::launch({A, M, K, lda}, {B, N, K, ldb}, e, static_cast<cudaStream_t>(stream), bn);
+    return 0;
+  });
+}
+
+struct trims_net {
+  std::unique_ptr<nn::Net> net;
+};
+
+int trims_net_create(int device, const char* arch_text, const char* resident_json, const void* weights, int batch,
+                     trims_net** out) {
+  return guard([&] {
+    if (batch < 1) raise(Errc::InvalidArgument, "batch must be >= 1");
+    auto h = std::make_unique<trims_net>();
+    h->net = std::make_unique<nn::Net>(device, arch_text, fmt::manifest_from_json(resident_json),
+                                       static_cast<const uint8_t*>(weights), batch);
+    *out = h.release();
+    return 0;
+  });
+}
+
+void trims_net_destroy(trims_net* net) {
+  try {
+    delete net;
+  } catch (...) {
+  }
+}
+
+int trims_net_buffers(trims_net* net, void** input, void** logits, int* classes, int* input_hw) {
+  return guard([&] {
+    if (input) *input = net->net->input();
+    if (logits) *logits = net->net->logits();
+    if (classes) *classes = net->net->classes();
+    if (input_hw) *input_hw = net->net->input_hw();
+    return 0;
+  });
+}
+
+int trims_net_run(trims_net* net, void* stream, int use_graph) {
+  return guard([&] {
+    net->net->run(static_cast<cudaStream_t>(stream), use_graph != 0);
+    return 0;
+  });
+}
+
+int trims_net_info(trims_net* net, double out3[3]) {
+  return guard([&] {
+    out3[0] = net->net->flops();
+    out3[1] = net->net->launches();
+    out3[2] = double(net->net->workspace_bytes());
+    return 0;
+  });
+}
+
+int trims_softmax(const float* in, float* out, int M, int N, void* stream) {
+  return guard([&] {
+    nn::softmax(in, out, M, N, static_cast<cudaStream_t>(stream));
     return 0;
   });
 }

@@ -173,7 +173,7 @@ EncodeTiled encode_fn() {
 }
 
 template <int BN, int STAGES>
-void launch_bn(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream) {
+void run_bn(const Prepared& p, cudaStream_t stream) {
   constexpr size_t smem = size_t(STAGES) * (BM * BK * 2 + BN * BK * 2) + 1024;
   static bool attr = false;
   if (!attr) {
@@ -181,10 +181,9 @@ void launch_bn(const Operand& A, const Operand& B, const Epilogue& e, cudaStream
                                     int(smem)));
     attr = true;
   }
-  CUtensorMap ta = make_tmap(A.ptr, A.rows, A.k, A.ld, BM);
-  CUtensorMap tb = make_tmap(B.ptr, B.rows, B.k, B.ld, BN);
-  dim3 grid((A.rows + BM - 1) / BM, (B.rows + BN - 1) / BN);
-  gemm_tc_kernel<BN, STAGES><<<grid, kThreads, smem, stream>>>(ta, tb, e.out, int(A.rows), int(B.rows), int(A.k),
+  const Epilogue& e = p.e;
+  dim3 grid(unsigned((p.M + BM - 1) / BM), unsigned((p.N + BN - 1) / BN));
+  gemm_tc_kernel<BN, STAGES><<<grid, kThreads, smem, stream>>>(p.ta, p.tb, e.out, int(p.M), int(p.N), int(p.K),
                                                                 int(e.ldo), e.scale, e.bias, e.residual, int(e.ldr),
                                                                 e.relu ? 1 : 0);
   TRIMS_CUDA(cudaGetLastError());
@@ -216,7 +215,7 @@ int pick_bn(uint64_t M, uint64_t N, int sms) {
   return 64;
 }
 
-void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn) {
+Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn) {
   if (A.k != B.k) raise(Errc::InvalidArgument, "GEMM K mismatch");
   if (!bn) {
     int dev = 0, sms = 148;
@@ -224,12 +223,28 @@ void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     bn = pick_bn(A.rows, B.rows, sms);
   }
-  switch (bn) {
-    case 64: launch_bn<64, 6>(A, B, e, stream); break;
-    case 128: launch_bn<128, 5>(A, B, e, stream); break;
-    case 256: launch_bn<256, 4>(A, B, e, stream); break;
-    default: raise(Errc::InvalidArgument, "BN must be 64, 128 or 256");
+  if (bn != 64 && bn != 128 && bn != 256) raise(Errc::InvalidArgument, "BN must be 64, 128 or 256");
+  Prepared p;
+  p.ta = make_tmap(A.ptr, A.rows, A.k, A.ld, BM);
+  p.tb = make_tmap(B.ptr, B.rows, B.k, B.ld, uint32_t(bn));
+  p.M = A.rows;
+  p.N = B.rows;
+  p.K = A.k;
+  p.bn = bn;
+  p.e = e;
+  return p;
+}
+
+void run(const Prepared& p, cudaStream_t stream) {
+  switch (p.bn) {
+    case 64: run_bn<64, 6>(p, stream); break;
+    case 128: run_bn<128, 5>(p, stream); break;
+    default: run_bn<256, 4>(p, stream); break;
   }
+}
+
+void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn) {
+  run(prepare(A, B, e, bn), stream);
 }
 
 }  // namespace trims::gemm

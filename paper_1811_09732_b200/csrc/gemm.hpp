@@ -28,6 +28,17 @@ struct Epilogue {
 
 CUtensorMap make_tmap(const void* ptr, uint64_t rows, uint64_t k, uint64_t ld, uint32_t box_rows);
 int pick_bn(uint64_t M, uint64_t N, int sms);
+
+// A GEMM with its tensor maps encoded once (the executor builds these at
+// bind time so a forward pass costs only kernel launches).
+struct Prepared {
+  CUtensorMap ta, tb;
+  uint64_t M{0}, N{0}, K{0};
+  int bn{128};
+  Epilogue e;
+};
+Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn = 0);
+void run(const Prepared& p, cudaStream_t stream);
 // D = epi(A . B^T); bn = 0 picks the tile width.
 void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn = 0);
 

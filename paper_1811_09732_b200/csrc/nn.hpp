@@ -1,0 +1,71 @@
+// nn.hpp — forward-pass kernels (K8) and the network executor that runs a
+// CNN on weights lent by the store (K7 GEMMs + K8 layers, CUDA-graph replay).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "format.hpp"
+#include "gemm.hpp"
+
+namespace trims::nn {
+
+void input_prep(const float* in_nchw, uint16_t* out_nhwc, int N, int C, int H, int W, cudaStream_t s);
+void im2col(const uint16_t* in, uint16_t* A, int N, int H, int W, int Ctot, int c_off, int Cg, int R, int S, int stride,
+            int pad, int P, int Q, int Kp, cudaStream_t s);
+void maxpool(const uint16_t* in, uint16_t* out, int N, int H, int W, int C, int k, int stride, int pad, int P, int Q,
+             cudaStream_t s);
+void avgpool_global(const uint16_t* in, uint16_t* out, int N, int HW, int C, cudaStream_t s);
+void flatten_nchw(const uint16_t* in, uint16_t* out, int N, int HW, int C, cudaStream_t s);
+void gemv(const uint16_t* x, int M, int K, const uint16_t* W, int N, const float* bias, bool relu, uint16_t* out_bf,
+          float* out_f32, int ldo, int sms, cudaStream_t s);
+void bn_fold(const uint16_t* gamma, const uint16_t* beta, const uint16_t* mean, const uint16_t* var, float eps, int C,
+             float* scale, float* shift, cudaStream_t s);
+void bf16_to_f32(const uint16_t* in, float* out, int n, cudaStream_t s);
+void pad_rows(const uint16_t* in, int rows, int k, uint16_t* out, int kp, cudaStream_t s);
+void softmax(const float* in, float* out, int M, int N, cudaStream_t s);
+
+// One bound network: an architecture (text, one layer per line, written by
+// paper_1811_09732_b200/models.py) over a resident manifest whose bf16 KRSC
+// weights live at `weights` (the store's segment, mapped read-only), plus a
+// private workspace: activations, im2col scratch, folded BN parameters.
+class Net {
+ public:
+  Net(int device, const std::string& arch, const fmt::Manifest& resident, const uint8_t* weights, int batch);
+  ~Net();
+  float* input() const { return input_; }    // fp32 NCHW [batch, 3, H, W]
+  float* logits() const { return logits_; }  // fp32 [batch, classes]
+  int classes() const { return classes_; }
+  int input_hw() const { return in_hw_; }
+  // One forward pass on `stream`; with use_graph the launch sequence is
+  // captured once into a CUDA graph and replayed.
+  void run(cudaStream_t stream, bool use_graph);
+  double flops() const { return flops_; }
+  uint32_t launches() const { return launches_; }
+  uint64_t workspace_bytes() const { return ws_bytes_; }
+
+ private:
+  struct Step;
+  void record(cudaStream_t stream);
+  uint8_t* alloc(uint64_t bytes);
+
+  int device_, batch_, sms_{148};
+  int in_hw_{224}, in_c_{3}, classes_{1000};
+  std::vector<std::unique_ptr<Step>> steps_;
+  std::vector<void*> owned_;
+  float* input_{nullptr};
+  float* logits_{nullptr};
+  double flops_{0};
+  uint32_t launches_{0};
+  uint64_t ws_bytes_{0};
+  cudaGraph_t graph_{nullptr};
+  cudaGraphExec_t exec_{nullptr};
+  cudaStream_t capture_stream_{nullptr};
+};
+
+}  // namespace trims::nn

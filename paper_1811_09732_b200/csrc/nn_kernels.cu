@@ -1,0 +1,290 @@
+// nn_kernels.cu — K8: the bandwidth-bound layers of the forward pass on the
+// shared weights (NHWC bf16 activations): input layout/precision prep,
+// im2col feeding the tcgen05 GEMM, max/avg pooling, NHWC->NCHW flatten for
+// torchvision-ordered FC weights, the small-batch FC GEMV, batch-norm
+// folding into per-channel fp32 scale/shift, and softmax.
+#include <cuda_bf16.h>
+
+#include "cuda_util.hpp"
+#include "nn.hpp"
+
+namespace trims::nn {
+
+namespace {
+
+__device__ __forceinline__ float bf(uint16_t v) { return __uint_as_float(uint32_t(v) << 16); }
+__device__ __forceinline__ uint16_t to_bf(float x) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(0.f), "f"(x));
+  return uint16_t(r & 0xffffu);
+}
+
+inline unsigned blocks(uint64_t n, unsigned t = 256) { return unsigned(std::min<uint64_t>((n + t - 1) / t, 1u << 20)); }
+
+__global__ void input_prep_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int N, int C, int H, int W) {
+  const uint64_t total = uint64_t(N) * H * W * C;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
+    const int c = int(i % C);
+    uint64_t r = i / C;
+    const int w = int(r % W);
+    r /= W;
+    const int h = int(r % H);
+    const int n = int(r / H);
+    out[i] = to_bf(in[((uint64_t(n) * C + c) * H + h) * W + w]);
+  }
+}
+
+// A[m, (r*S + s)*Cg + c] = in[n, p*stride - pad + r, q*stride - pad + s, c_off + c]; zero outside / in padding cols.
+__global__ void im2col_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ A, int N, int H, int W, int Ctot,
+                              int c_off, int Cg, int R, int S, int stride, int pad, int P, int Q, int Kp) {
+  const int RSC = R * S * Cg;
+  const bool vec = (Cg % 8 == 0) && (Ctot % 8 == 0) && (c_off % 8 == 0) && (Kp % 8 == 0);
+  const uint64_t M = uint64_t(N) * P * Q;
+  if (vec) {
+    const int cols8 = Kp / 8;
+    const uint64_t total = M * cols8;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+      const int col = int(i % cols8) * 8;
+      const uint64_t m = i / cols8;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (col < RSC) {
+        const int c = col % Cg, rs = col / Cg, s = rs % S, r = rs / S;
+        const int q = int(m % Q), p = int((m / Q) % P), n = int(m / (uint64_t(P) * Q));
+        const int y = p * stride - pad + r, x = q * stride - pad + s;
+        if (y >= 0 && y < H && x >= 0 && x < W)
+          v = *reinterpret_cast<const uint4*>(in + ((uint64_t(n) * H + y) * W + x) * Ctot + c_off + c);
+      }
+      *reinterpret_cast<uint4*>(A + m * Kp + col) = v;
+    }
+  } else {
+    const uint64_t total = M * Kp;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+      const int col = int(i % Kp);
+      const uint64_t m = i / Kp;
+      uint16_t v = 0;
+      if (col < RSC) {
+        const int c = col % Cg, rs = col / Cg, s = rs % S, r = rs / S;
+        const int q = int(m % Q), p = int((m / Q) % P), n = int(m / (uint64_t(P) * Q));
+        const int y = p * stride - pad + r, x = q * stride - pad + s;
+        if (y >= 0 && y < H && x >= 0 && x < W) v = in[((uint64_t(n) * H + y) * W + x) * Ctot + c_off + c];
+      }
+      A[i] = v;
+    }
+  }
+}
+
+__global__ void maxpool_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, int N, int H, int W, int C,
+                               int k, int stride, int pad, int P, int Q) {
+  const int C8 = C / 8;
+  const uint64_t total = uint64_t(N) * P * Q * C8;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
+    const int c = int(i % C8) * 8;
+    uint64_t r = i / C8;
+    const int q = int(r % Q);
+    r /= Q;
+    const int p = int(r % P);
+    const int n = int(r / P);
+    float m[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m[j] = -INFINITY;
+    for (int dy = 0; dy < k; ++dy) {
+      const int y = p * stride - pad + dy;
+      if (y < 0 || y >= H) continue;
+      for (int dx = 0; dx < k; ++dx) {
+        const int x = q * stride - pad + dx;
+        if (x < 0 || x >= W) continue;
+        const uint4 v = *reinterpret_cast<const uint4*>(in + ((uint64_t(n) * H + y) * W + x) * C + c);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          m[2 * j] = fmaxf(m[2 * j], bf(uint16_t(w[j] & 0xffff)));
+          m[2 * j + 1] = fmaxf(m[2 * j + 1], bf(uint16_t(w[j] >> 16)));
+        }
+      }
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = uint32_t(to_bf(m[2 * j])) | (uint32_t(to_bf(m[2 * j + 1])) << 16);
+    *reinterpret_cast<uint4*>(out + i * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+__global__ void avgpool_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, int N, int HW, int C) {
+  const uint64_t total = uint64_t(N) * C;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
+    const int c = int(i % C);
+    const int n = int(i / C);
+    float s = 0.f;
+    for (int j = 0; j < HW; ++j) s += bf(in[(uint64_t(n) * HW + j) * C + c]);
+    out[i] = to_bf(s / float(HW));
+  }
+}
+
+__global__ void flatten_nchw_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, int N, int HW, int C) {
+  const uint64_t total = uint64_t(N) * HW * C;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
+    const int hw = int(i % HW);
+    uint64_t r = i / HW;
+    const int c = int(r % C);
+    const int n = int(r / C);
+    out[i] = in[(uint64_t(n) * HW + hw) * C + c];
+  }
+}
+
+// Small-batch FC: out[m, n] = relu?(sum_k x[m,k] W[n,k] + bias[n]). One warp
+// per output row n, 128-bit weight loads streamed once (HBM-bound).
+template <int MB>
+__global__ void __launch_bounds__(256) gemv_kernel(const uint16_t* __restrict__ x, int M, int K,
+                                                   const uint16_t* __restrict__ Wt, int N, const float* __restrict__ bias,
+                                                   int relu, uint16_t* __restrict__ out_bf, float* __restrict__ out_f32,
+                                                   int ldo) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int n = warp; n < N; n += nwarps) {
+    float acc[MB];
+#pragma unroll
+    for (int m = 0; m < MB; ++m) acc[m] = 0.f;
+    const uint16_t* wr = Wt + uint64_t(n) * K;
+    for (int k = lane * 8; k < K; k += 32 * 8) {
+      const uint4 wv = __ldg(reinterpret_cast<const uint4*>(wr + k));
+      const uint32_t w[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+      for (int m = 0; m < MB; ++m) {
+        if (m >= M) break;
+        const uint4 xv = __ldg(reinterpret_cast<const uint4*>(x + uint64_t(m) * K + k));
+        const uint32_t xx[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc[m] = fmaf(bf(uint16_t(w[j] & 0xffff)), bf(uint16_t(xx[j] & 0xffff)), acc[m]);
+          acc[m] = fmaf(bf(uint16_t(w[j] >> 16)), bf(uint16_t(xx[j] >> 16)), acc[m]);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MB; ++m) {
+      if (m >= M) break;
+      float v = acc[m];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) {
+        if (bias) v += bias[n];
+        if (relu) v = fmaxf(v, 0.f);
+        if (out_f32) out_f32[uint64_t(m) * ldo + n] = v;
+        else out_bf[uint64_t(m) * ldo + n] = to_bf(v);
+      }
+    }
+  }
+}
+
+__global__ void bn_fold_kernel(const uint16_t* gamma, const uint16_t* beta, const uint16_t* mean, const uint16_t* var,
+                               float eps, int C, float* scale, float* shift) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const float s = bf(gamma[c]) / sqrtf(bf(var[c]) + eps);
+  scale[c] = s;
+  shift[c] = bf(beta[c]) - bf(mean[c]) * s;
+}
+
+__global__ void bf16_to_f32_kernel(const uint16_t* in, float* out, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = bf(in[i]);
+}
+
+__global__ void pad_rows_kernel(const uint16_t* in, int rows, int k, uint16_t* out, int kp) {
+  const uint64_t total = uint64_t(rows) * kp;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
+    const int col = int(i % kp);
+    const uint64_t r = i / kp;
+    out[i] = col < k ? in[r * k + col] : uint16_t(0);
+  }
+}
+
+__global__ void softmax_kernel(const float* in, float* out, int M, int N) {
+  const int m = blockIdx.x;
+  if (m >= M) return;
+  __shared__ float red[32];
+  const float* x = in + uint64_t(m) * N;
+  float mx = -INFINITY;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) mx = fmaxf(mx, x[i]);
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = -INFINITY;
+  for (int w = 0; w < int(blockDim.x >> 5); ++w) mx = fmaxf(mx, red[w]);
+  __syncthreads();
+  float s = 0.f;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) s += __expf(x[i] - mx);
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  s = 0.f;
+  for (int w = 0; w < int(blockDim.x >> 5); ++w) s += red[w];
+  for (int i = threadIdx.x; i < N; i += blockDim.x) out[uint64_t(m) * N + i] = __expf(x[i] - mx) / s;
+}
+
+}  // namespace
+
+void input_prep(const float* in, uint16_t* out, int N, int C, int H, int W, cudaStream_t s) {
+  input_prep_kernel<<<blocks(uint64_t(N) * C * H * W), 256, 0, s>>>(in, out, N, C, H, W);
+  TRIMS_CUDA(cudaGetLastError());
+}
+
+void im2col(const uint16_t* in, uint16_t* A, int N, int H, int W, int Ctot, int c_off, int Cg, int R, int S, int stride,
+            int pad, int P, int Q, int Kp, cudaStream_t s) {
+  const uint64_t work = uint64_t(N) * P * Q * ((Cg % 8 == 0 && Ctot % 8 == 0 && c_off % 8 == 0 && Kp % 8 == 0) ? Kp / 8 : Kp);
+  im2col_kernel<<<blocks(work), 256, 0, s>>>(in, A, N, H, W, Ctot, c_off, Cg, R, S, stride, pad, P, Q, Kp);
+  TRIMS_CUDA(cudaGetLastError());
+}
+
+void maxpool(const uint16_t* in, uint16_t* out, int N, int H, int W, int C, int k, int stride, int pad, int P, int Q,
+             cudaStream_t s) {
+  if (C % 8) raise(Errc::InvalidArgument, "maxpool needs C % 8 == 0");
+  maxpool_kernel<<<blocks(uint64_t(N) * P * Q * C / 8), 256, 0, s>>>(in, out, N, H, W, C, k, stride, pad, P, Q);
+  TRIMS_CUDA(cudaGetLastError());
+}
+
+void avgpool_global(const uint16_t* in, uint16_t* out, int N, int HW, int C, cudaStream_t s) {
+  avgpool_kernel<<<blocks(uint64_t(N) * C), 256, 0, s>>>(in, out, N, HW, C);
+  TRIMS_CUDA(cudaGetLastError());
+}
+
+void flatten_nchw(const uint16_t* in, uint16_t* out, int N, int HW, int C, cudaStream_t s) {
+  flatten_nchw_kernel<<<blocks(uint64_t(N) * HW * C), 256, 0, s>>>(in, out, N, HW, C);
+  TRIMS_CUDA(cudaGetLastError());
+}
+
+void gemv(const uint16_t* x, int M, int K, const uint16_t* W, int N, const float* bias, bool relu, uint16_t* out_bf,
+          float* out_f32, int ldo, int sms, cudaStream_t s) {
+  if (K % 8) raise(Errc::InvalidArgument, "gemv needs K % 8 == 0");
+  const unsigned grid = unsigned(std::min<int>((N + 7) / 8, sms * 8));
+  if (M <= 1) gemv_kernel<1><<<grid, 256, 0, s>>>(x, M, K, W, N, bias, relu, out_bf, out_f32, ldo);
+  else if (M <= 4) gemv_kernel<4><<<grid, 256, 0, s>>>(x, M, K, W, N, bias, relu, out_bf, out_f32, ldo);
+  else if (M <= 8) gemv_kernel<8><<<grid, 256, 0, s>>>(x, M, K, W, N, bias, relu, out_bf, out_f32, ldo);
+  else raise(Errc::InvalidArgument, "gemv is for M <= 8");
+  TRIMS_CUDA(cudaGetLastError());
+}
+
+void bn_fold(const uint16_t* gamma, const uint16_t* beta, const uint16_t* mean, const uint16_t* var, float eps, int C,
+             float* scale, float* shift, cudaStream_t s) {
+  bn_fold_kernel<<<(C + 255) / 256, 256, 0, s>>>(gamma, beta, mean, var, eps, C, scale, shift);
+  TRIMS_CUDA(cudaGetLastError());
+}
+
+void bf16_to_f32(const uint16_t* in, float* out, int n, cudaStream_t s) {
+  bf16_to_f32_kernel<<<(n + 255) / 256, 256, 0, s>>>(in, out, n);
+  TRIMS_CUDA(cudaGetLastError());
+}
+
+void pad_rows(const uint16_t* in, int rows, int k, uint16_t* out, int kp, cudaStream_t s) {
+  pad_rows_kernel<<<blocks(uint64_t(rows) * kp), 256, 0, s>>>(in, rows, k, out, kp);
+  TRIMS_CUDA(cudaGetLastError());
+}
+
+void softmax(const float* in, float* out, int M, int N, cudaStream_t s) {
+  softmax_kernel<<<M, 256, 0, s>>>(in, out, M, N);
+  TRIMS_CUDA(cudaGetLastError());
+}
+
+}  // namespace trims::nn

@@ -1,0 +1,90 @@
+"""Inference on shared weights: the B200 compute step of load-and-serve.
+
+The reference's compute stand-in is ``Client::touch`` (client.cpp:338-359), an
+FNV-1a pass over the weight bytes. Here a client binds the store-lent resident
+weights (bf16, conv filters KRSC) to a native network executor (csrc/net.cu):
+tcgen05 GEMMs for every conv/FC contraction (im2col for k>1), bandwidth-bound
+pooling/flatten/GEMV kernels, batch-norm folded at bind time into per-channel
+fp32 epilogue scale/shift (the shared weights are never modified), and the
+whole forward replayed as one CUDA graph.
+"""
+from __future__ import annotations
+
+import ctypes
+
+from . import catalog as C
+from ._lib import check, lib
+
+
+def arch_text(arch: C.Arch) -> str:
+    lines = [f"input hw={arch.input_hw} c=3"]
+    for l in arch.layers:
+        if l.kind == "conv":
+            lines.append(f"conv name={l.name} cin={l.cin} cout={l.cout} k={l.k} stride={l.stride} pad={l.pad} "
+                         f"groups={l.groups} bias={int(l.bias)} bn={int(l.bn)} relu={int(l.relu)} src={l.src} "
+                         f"res={l.res} out={l.out}")
+        elif l.kind == "pool_max":
+            lines.append(f"pool_max k={l.k} stride={l.stride} pad={l.pad} out={l.out}")
+        elif l.kind == "pool_avg":
+            lines.append(f"pool_avg k={l.k}")
+        elif l.kind == "flatten":
+            lines.append("flatten")
+        elif l.kind == "fc":
+            lines.append(f"fc name={l.name} cin={l.cin} cout={l.cout} bias={int(l.bias)} relu={int(l.relu)}")
+        else:
+            raise ValueError(l.kind)
+    return "\n".join(lines) + "\n"
+
+
+class BoundNet:
+    """A network executor over one attached model view (weights stay shared)."""
+
+    def __init__(self, view, arch: C.Arch | str, batch: int = 1, device: int = 0):
+        arch = C.ARCHS[arch]() if isinstance(arch, str) else arch
+        self.arch, self.batch, self.device, self.view = arch, batch, device, view
+        h = ctypes.c_void_p()
+        check(lib.trims_net_create(device, arch_text(arch).encode(), view.manifest_json.encode(), view.base_ptr, batch,
+                                   ctypes.byref(h)))
+        self._h = h
+        inp, lg = ctypes.c_void_p(), ctypes.c_void_p()
+        classes, hw = ctypes.c_int(), ctypes.c_int()
+        check(lib.trims_net_buffers(h, ctypes.byref(inp), ctypes.byref(lg), ctypes.byref(classes), ctypes.byref(hw)))
+        self.input_ptr, self.logits_ptr = int(inp.value), int(lg.value)
+        self.classes, self.input_hw = classes.value, hw.value
+        info = (ctypes.c_double * 3)()
+        check(lib.trims_net_info(h, info))
+        self.flops, self.launches, self.workspace_bytes = info[0], int(info[1]), int(info[2])
+
+    def input_view(self):
+        """Zero-copy torch view of the net's fp32 NCHW input buffer."""
+        from .client import TensorView
+        n = self.batch * 3 * self.input_hw * self.input_hw
+        return TensorView("input", [self.batch, 3, self.input_hw, self.input_hw], "f32", "native", 0, n * 4,
+                          self.input_ptr).torch(f"cuda:{self.device}")
+
+    def logits_view(self):
+        from .client import TensorView
+        return TensorView("logits", [self.batch, self.classes], "f32", "native", 0, self.batch * self.classes * 4,
+                          self.logits_ptr).torch(f"cuda:{self.device}")
+
+    def run(self, stream=None, graph: bool = True) -> None:
+        check(lib.trims_net_run(self._h, stream, int(graph)))
+
+    def forward(self, x, graph: bool = True):
+        """x: fp32 NCHW (any device). Returns the fp32 logits on the GPU."""
+        import torch
+        self.input_view().copy_(x)
+        s = torch.cuda.current_stream(self.device)
+        self.run(s.cuda_stream, graph)
+        return self.logits_view()
+
+    def close(self):
+        if self._h:
+            lib.trims_net_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
