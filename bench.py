@@ -12,8 +12,10 @@ word checksummed.
   e2e   : the same metric through the C ABI (trims_ingest_host) from a pinned
           HOST buffer: H2D copy-engine chunks + fused transform + D2H of the
           per-tensor checksums, all inside the timed region.
-  latency_ms : cold (disk) / warm (host-resident) / hot (HBM-resident) open
-          latency of the store for the same model, measured once on rank 0.
+  latency_ms : cold (disk) / warm (host-resident) / hot (HBM-resident)
+          end-to-end inference request latency (open -> attach -> bind ->
+          H2D input -> forward -> D2H logits -> close) and the compute-only
+          ideal, for ResNet-50 and VGG-16 at batch 1 (rank 0's numbers).
 
 Timing: CUDA events on the launching stream, W untimed warm-ups, K timed
 steps, L2 flushed (256 MiB write) before every timed step, max over ranks.
@@ -207,7 +209,13 @@ def run_ours(args):
     assert cs == want, "e2e and device-resident ingest disagree"
 
     # ---- store latencies (rank 0): cold / warm(host) / hot(HBM) opens
-    lat = store_latencies(work, arch, dev) if rank == 0 else None
+    # ---- end-to-end inference request latency (every rank serves its own shard)
+    lat = {"resnet50": request_latencies(work, arch, dev)}
+    if not args.quick:
+        from paper_1811_09732_b200 import catalog as C
+        vgg = C.ARCHS["vgg16"]()
+        C.write_arch(vgg, work, seed=1)
+        lat["vgg16"] = request_latencies(work, vgg, dev)
 
     hbm_peak, peak_kind = peaks()
     algo = info["read_bytes"] + info["write_bytes"]
@@ -239,48 +247,101 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def store_latencies(work: str, arch, dev: int) -> dict:
-    """Open latency through the store for the same artifact (ms, median of 5)."""
+def request_latencies(work: str, arch, dev: int, batch: int = 1, reps: int = 7) -> dict:
+    """End-to-end inference request latency through the public API (ms, median):
+    open (store) -> attach -> bind (new weights generation only) -> H2D input ->
+    forward (CUDA graph) -> D2H logits -> close, for the three residency states
+    of TrIMS (cold = disk, warm = pinned host tier, hot = HBM), plus the
+    compute-only ideal (H2D + forward + D2H on an already bound, resident model;
+    PAPER.md:39,142)."""
     import statistics
 
     import torch
 
     from paper_1811_09732_b200 import catalog as C
     from paper_1811_09732_b200.client import Client
+    from paper_1811_09732_b200.models import BoundNet
     from paper_1811_09732_b200.store import Store, StoreOptions
     key = C.arch_key(arch)
-    out = {}
     base = dict(disk_cache_dir=work, fast_capacity_bytes=4 << 30, host_capacity_bytes=4 << 30, device=dev,
                 convert_to="bf16", permute_4d=True)
-    # cold: eager reclaim -> every open is a disk load (page cache warm, like the reference harness)
-    with Store(StoreOptions(eager_reclaim=True, **base)) as s:
+    x = torch.randn(batch, 3, arch.input_hw, arch.input_hw, generator=torch.Generator().manual_seed(2)).pin_memory()
+    logits = None
+    stream = torch.cuda.current_stream(dev)
+    nets = {}
+
+    def request(cli, phases):
+        nonlocal logits
+        t0 = time.perf_counter()
+        v = cli.open(key, force_shared=True)
+        t1 = time.perf_counter()
+        net = nets.get((v.model_id, v.generation))
+        if net is None:
+            for old in nets.values():
+                old.close()
+            nets.clear()
+            net = nets[(v.model_id, v.generation)] = BoundNet(v, arch, batch, dev)
+        t2 = time.perf_counter()
+        if logits is None:
+            logits = torch.empty(batch, net.classes).pin_memory()
+        net.input_view().copy_(x, non_blocking=True)
+        net.run(stream.cuda_stream, True)
+        logits.copy_(net.logits_view(), non_blocking=True)
+        stream.synchronize()
+        t3 = time.perf_counter()
+        cli.close(v)
+        t4 = time.perf_counter()
+        phases.append(((t4 - t0) * 1e3, (t1 - t0) * 1e3, (t2 - t1) * 1e3, (t3 - t2) * 1e3))
+
+    def summary(ph):
+        ph = sorted(ph[1:])  # first rep warms allocators / graph capture
+        med = ph[len(ph) // 2]
+        return {"e2e": round(med[0], 4), "open": round(med[1], 4), "bind": round(med[2], 4),
+                "h2d_forward_d2h": round(med[3], 4)}
+
+    out = {"model": arch.name, "batch": batch}
+    with Store(StoreOptions(eager_reclaim=True, **base)) as s:  # cold: every open is a disk load
         cli = Client(s)
-        ts = []
-        for _ in range(6):
-            t0 = time.perf_counter()
-            v = cli.open(key, force_shared=True)
-            torch.cuda.synchronize()
-            ts.append((time.perf_counter() - t0) * 1e3)
-            cli.close(v)
-        out["cold_open"] = round(statistics.median(ts[1:]), 3)
+        ph = []
+        for _ in range(reps):
+            request(cli, ph)
+        out["cold"] = summary(ph)
     with Store(StoreOptions(**base)) as s:
         cli = Client(s)
+        ph_w, ph_h = [], []
+        request(cli, ph_h)
+        for _ in range(reps):
+            s.reclaim(0, 4 << 30)  # drop the HBM copy, keep the pinned host copy -> host hit
+            request(cli, ph_w)
+        for _ in range(reps * 3):
+            request(cli, ph_h)
+        out["warm"] = summary(ph_w)
+        out["hot"] = summary(ph_h)
         v = cli.open(key, force_shared=True)
-        cli.close(v)
-        ts, hs = [], []
-        for _ in range(6):
-            s.reclaim(0, 4 << 30)                 # drop the HBM copy, keep the pinned host copy
+        out["last_publish_breakdown_ms"] = {k: round(y, 3) for k, y in s.ingest_stats(v.model_id).items()}
+        net = nets[(v.model_id, v.generation)]
+        ts = []
+        for _ in range(reps * 3):
             t0 = time.perf_counter()
-            v = cli.open(key, force_shared=True)
+            net.input_view().copy_(x, non_blocking=True)
+            net.run(stream.cuda_stream, True)
+            logits.copy_(net.logits_view(), non_blocking=True)
+            stream.synchronize()
             ts.append((time.perf_counter() - t0) * 1e3)
-            cli.close(v)
-            t0 = time.perf_counter()
-            v = cli.open(key, force_shared=True)
-            hs.append((time.perf_counter() - t0) * 1e3)
-            cli.close(v)
-        out["warm_open_host_resident"] = round(statistics.median(ts[1:]), 3)
-        out["hot_open_hbm_resident"] = round(statistics.median(hs[1:]), 4)
-        out["last_publish_breakdown_ms"] = {k: round(x, 3) for k, x in s.ingest_stats(v.model_id).items()}
+        out["compute_only"] = round(statistics.median(ts[1:]), 4)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(20):
+            net.run(stream.cuda_stream, True)
+        e1.record(stream)
+        stream.synchronize()
+        out["forward_device_ms"] = round(e0.elapsed_time(e1) / 20, 4)
+        out["forward_tflops"] = round(net.flops / (out["forward_device_ms"] / 1e3) / 1e12, 2)
+        out["hot_over_compute_only"] = round(out["hot"]["e2e"] / out["compute_only"], 4)
+        out["kernels_per_forward"] = net.launches
+        cli.close(v)
+    for n in nets.values():
+        n.close()
     return out
 
 
@@ -353,6 +414,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="ResNet-50 latencies only")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
