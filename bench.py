@@ -275,12 +275,15 @@ def request_latencies(work: str, arch, dev: int, batch: int = 1, reps: int = 7) 
         t0 = time.perf_counter()
         v = cli.open(key, force_shared=True)
         t1 = time.perf_counter()
-        net = nets.get((v.model_id, v.generation))
+        # A serving client keeps its executor; a new weights generation (after
+        # eviction + reload) only rebinds the weight-dependent state.
+        net = nets.get("net")
         if net is None:
-            for old in nets.values():
-                old.close()
-            nets.clear()
-            net = nets[(v.model_id, v.generation)] = BoundNet(v, arch, batch, dev)
+            net = nets["net"] = BoundNet(v, arch, batch, dev)
+            nets["gen"] = (id(cli), v.generation)
+        elif nets["gen"] != (id(cli), v.generation):
+            net.rebind(v)
+            nets["gen"] = (id(cli), v.generation)
         t2 = time.perf_counter()
         if logits is None:
             logits = torch.empty(batch, net.classes).pin_memory()
@@ -319,7 +322,7 @@ def request_latencies(work: str, arch, dev: int, batch: int = 1, reps: int = 7) 
         out["hot"] = summary(ph_h)
         v = cli.open(key, force_shared=True)
         out["last_publish_breakdown_ms"] = {k: round(y, 3) for k, y in s.ingest_stats(v.model_id).items()}
-        net = nets[(v.model_id, v.generation)]
+        net = nets["net"]
         ts = []
         for _ in range(reps * 3):
             t0 = time.perf_counter()
@@ -340,8 +343,7 @@ def request_latencies(work: str, arch, dev: int, batch: int = 1, reps: int = 7) 
         out["hot_over_compute_only"] = round(out["hot"]["e2e"] / out["compute_only"], 4)
         out["kernels_per_forward"] = net.launches
         cli.close(v)
-    for n in nets.values():
-        n.close()
+    nets["net"].close()
     return out
 
 

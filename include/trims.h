@@ -231,6 +231,9 @@ int trims_net_create(int device, const char* arch_text, const char* resident_jso
                      trims_net** out);
 void trims_net_destroy(trims_net* net);
 int trims_net_buffers(trims_net* net, void** input, void** logits, int* classes, int* input_hw);
+/* Re-point a net at a new generation of the same resident model (after an
+ * eviction + reload): only weight-dependent state is rebuilt. */
+int trims_net_rebind(trims_net* net, const void* weights);
 /* One forward pass, async on `stream`; use_graph replays a captured CUDA graph. */
 int trims_net_run(trims_net* net, void* stream, int use_graph);
 /* flops per forward, kernel launches per forward, workspace bytes */

@@ -736,6 +736,13 @@ int trims_net_buffers(trims_net* net, void** input, void** logits, int* classes,
   });
 }
 
+int trims_net_rebind(trims_net* net, const void* weights) {
+  return guard([&] {
+    net->net->rebind(static_cast<const uint8_t*>(weights));
+    return 0;
+  });
+}
+
 int trims_net_run(trims_net* net, void* stream, int use_graph) {
   return guard([&] {
     net->net->run(static_cast<cudaStream_t>(stream), use_graph != 0);

@@ -1,4 +1,12 @@
 // net.cu — the CNN executor over store-lent weights (see nn.hpp).
+//
+// Construction ("bind") sizes and allocates the private workspace once and
+// records every layer as a step. Everything that depends on WHERE the shared
+// weights live (B-operand tensor maps, GEMV weight pointers, folded BN
+// scale/shift, fp32 biases, zero-padded conv1 filters) is recomputed by
+// rebind() from resident-manifest offsets, so a client keeps its executor
+// across store evictions/reloads and only pays a few microseconds per layer
+// when a new generation of the model is published.
 #include <algorithm>
 #include <cmath>
 #include <functional>
@@ -11,7 +19,8 @@
 namespace trims::nn {
 
 struct Net::Step {
-  std::function<void(cudaStream_t)> fn;
+  std::function<void(cudaStream_t)> run;
+  std::function<void(cudaStream_t)> rebind;  // weight-dependent state (may be empty)
   uint32_t launches{1};
 };
 
@@ -82,33 +91,30 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
   TRIMS_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device));
   std::map<std::string, const fmt::TensorSpec*> tensors;
   for (const auto& t : resident.tensors) tensors[t.name] = &t;
-  auto tensor = [&](const std::string& name, fmt::DType want) -> const uint16_t* {
+  // Weights are addressed as offsets into the resident blob; `wbase_` is the
+  // current generation's base (set by rebind()).
+  auto offset_of = [&](const std::string& name) -> uint64_t {
     auto it = tensors.find(name);
     if (it == tensors.end()) raise(Errc::InvalidArgument, "resident manifest lacks " + name);
-    if (it->second->dtype != want) raise(Errc::InvalidArgument, name + " is not resident as bf16");
-    return reinterpret_cast<const uint16_t*>(weights + it->second->offset);
+    if (it->second->dtype != fmt::DType::BF16) raise(Errc::InvalidArgument, name + " is not resident as bf16");
+    return it->second->offset;
   };
+  const uint8_t* const* wb = &wbase_;
+  auto wptr = [wb](uint64_t off) { return reinterpret_cast<const uint16_t*>(*wb + off); };
 
-  cudaStream_t bind;
-  TRIMS_CUDA(cudaStreamCreateWithFlags(&bind, cudaStreamNonBlocking));
   const std::vector<LayerSpec> layers = parse_arch(arch);
   int last_fc = -1;
   for (size_t i = 0; i < layers.size(); ++i)
     if (layers[i].kind == "fc") last_fc = int(i);
 
-  std::map<std::string, Act> named;
-  Act cur;
-  uint16_t* col = nullptr;  // shared im2col scratch
-  uint64_t col_elems = 0;
-  // First pass sizes the im2col scratch; steps keep a pointer to `col` slot.
-  std::vector<std::function<void()>> fixups;
   auto conv_shape = [&](const Act& in, const LayerSpec& l, int& P, int& Q) {
     const int k = l.i("k", 1), st = l.i("stride", 1), pad = l.i("pad", 0);
     P = (in.h + 2 * pad - k) / st + 1;
     Q = (in.w + 2 * pad - k) / st + 1;
   };
-  {
-    // size pass
+  std::map<std::string, Act> named;
+  uint64_t col_elems = 0;
+  {  // size pass: the shared im2col scratch
     Act a;
     for (const auto& l : layers) {
       if (l.kind == "input") {
@@ -118,14 +124,10 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
         int P, Q;
         conv_shape(in, l, P, Q);
         const int k = l.i("k", 1), groups = l.i("groups", 1), cg = l.i("cin") / groups;
-        const bool direct = k == 1 && l.i("stride", 1) == 1 && l.i("pad", 0) == 0 && groups == 1;
-        if (!direct) {
-          const uint64_t kp = (uint64_t(k) * k * cg + 7) / 8 * 8;
-          col_elems = std::max<uint64_t>(col_elems, uint64_t(batch) * P * Q * kp);
-        }
-        Act o{nullptr, batch, P, Q, l.i("cout")};
-        if (!l.s("out").empty()) named[l.s("out")] = o;
-        a = o;
+        if (!(k == 1 && l.i("stride", 1) == 1 && l.i("pad", 0) == 0 && groups == 1))
+          col_elems = std::max<uint64_t>(col_elems, uint64_t(batch) * P * Q * ((uint64_t(k) * k * cg + 7) / 8 * 8));
+        a = {nullptr, batch, P, Q, l.i("cout")};
+        if (!l.s("out").empty()) named[l.s("out")] = a;
       } else if (l.kind == "pool_max") {
         const int k = l.i("k"), st = l.i("stride", k), pad = l.i("pad", 0);
         a = {nullptr, batch, (a.h + 2 * pad - k) / st + 1, (a.w + 2 * pad - k) / st + 1, a.c};
@@ -134,13 +136,12 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
         a = {nullptr, batch, 1, 1, a.c};
       } else if (l.kind == "flatten") {
         a = {nullptr, batch, 1, 1, a.h * a.w * a.c};
-      } else if (l.kind == "fc") {
-        a = {nullptr, batch, 1, 1, l.i("cout")};
       }
     }
     named.clear();
   }
-  if (col_elems) col = reinterpret_cast<uint16_t*>(alloc(col_elems * 2));
+  uint16_t* col = col_elems ? reinterpret_cast<uint16_t*>(alloc(col_elems * 2)) : nullptr;
+  Act cur;
 
   for (size_t li = 0; li < layers.size(); ++li) {
     const LayerSpec& l = layers[li];
@@ -151,10 +152,9 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       cur = {reinterpret_cast<uint16_t*>(alloc(uint64_t(batch) * in_c_ * in_hw_ * in_hw_ * 2)), batch, in_hw_, in_hw_,
              in_c_};
       const float* in = input_;
-      Act o = cur;
+      const Act o = cur;
       const int C = in_c_, HW = in_hw_;
-      steps_.push_back(std::make_unique<Step>(
-          Step{[=](cudaStream_t s) { input_prep(in, o.p, o.n, C, HW, HW, s); }, 1}));
+      steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) { input_prep(in, o.p, o.n, C, HW, HW, s); }}));
     } else if (l.kind == "conv") {
       const Act in = l.s("src").empty() ? cur : named.at(l.s("src"));
       int P, Q;
@@ -165,24 +165,25 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       const uint64_t M = uint64_t(batch) * P * Q;
       const int rsc = k * k * cg, kp = (rsc + 7) / 8 * 8;
       const std::string name = l.s("name");
-      const uint16_t* W = tensor(name + ".weight", fmt::DType::BF16);
-      if (kp != rsc) {  // TMA rows must be 16-byte multiples: private zero-padded copy
-        auto* wp = reinterpret_cast<uint16_t*>(alloc(uint64_t(cout) * kp * 2));
-        pad_rows(W, cout, rsc, wp, kp, bind);
-        W = wp;
-      }
+      const uint64_t w_off = offset_of(name + ".weight");
+      // TMA rows must be 16-byte multiples: conv1-like filters get a private zero-padded copy
+      uint16_t* wpad = kp != rsc ? reinterpret_cast<uint16_t*>(alloc(uint64_t(cout) * kp * 2)) : nullptr;
       float* scale = nullptr;
       float* bias = nullptr;
+      std::function<void(cudaStream_t)> bind_params;
       if (l.i("bn")) {
         const std::string bn = bn_name(name);
         scale = reinterpret_cast<float*>(alloc(uint64_t(cout) * 4));
         bias = reinterpret_cast<float*>(alloc(uint64_t(cout) * 4));
-        nn::bn_fold(tensor(bn + ".weight", fmt::DType::BF16), tensor(bn + ".bias", fmt::DType::BF16),
-                    tensor(bn + ".running_mean", fmt::DType::BF16), tensor(bn + ".running_var", fmt::DType::BF16),
-                    1e-5f, cout, scale, bias, bind);
+        const uint64_t og = offset_of(bn + ".weight"), ob = offset_of(bn + ".bias"),
+                       om = offset_of(bn + ".running_mean"), ov = offset_of(bn + ".running_var");
+        bind_params = [=](cudaStream_t s) {
+          nn::bn_fold(wptr(og), wptr(ob), wptr(om), wptr(ov), 1e-5f, cout, scale, bias, s);
+        };
       } else if (l.i("bias")) {
         bias = reinterpret_cast<float*>(alloc(uint64_t(cout) * 4));
-        bf16_to_f32(tensor(name + ".bias", fmt::DType::BF16), bias, cout, bind);
+        const uint64_t ob = offset_of(name + ".bias");
+        bind_params = [=](cudaStream_t s) { bf16_to_f32(wptr(ob), bias, cout, s); };
       }
       const uint16_t* res = nullptr;
       if (!l.s("res").empty()) {
@@ -192,20 +193,35 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       }
       Act out{reinterpret_cast<uint16_t*>(alloc(M * cout * 2)), batch, P, Q, cout};
       const bool direct = k == 1 && st == 1 && pad == 0 && groups == 1;
+      bool first_group = true;
       for (int gi = 0; gi < groups; ++gi) {
         const uint16_t* A = direct ? in.p : col;
         if (!direct) {
-          Act src = in;
+          const Act src = in;
           steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) {
             nn::im2col(src.p, col, src.n, src.h, src.w, src.c, gi * cg, cg, k, k, st, pad, P, Q, kp, s);
-          }, 1}));
+          }}));
         }
         gemm::Epilogue e{out.p + uint64_t(gi) * kg, uint64_t(cout), scale ? scale + gi * kg : nullptr,
                          bias ? bias + gi * kg : nullptr, res ? res + uint64_t(gi) * kg : nullptr, uint64_t(cout),
                          l.i("relu") != 0};
-        gemm::Prepared prep = gemm::prepare({A, M, uint64_t(kp), uint64_t(direct ? cin : kp)},
-                                            {W + uint64_t(gi) * kg * kp, uint64_t(kg), uint64_t(kp), uint64_t(kp)}, e);
-        steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) { gemm::run(prep, s); }, 1}));
+        // A-side map and tile width are fixed; the B map follows the weights.
+        auto prep = std::make_shared<gemm::Prepared>(
+            gemm::prepare({A, M, uint64_t(kp), uint64_t(direct ? cin : kp)},
+                          {wpad ? wpad : reinterpret_cast<const uint16_t*>(uintptr_t(256)), uint64_t(kg),
+                           uint64_t(kp), uint64_t(kp)},
+                          e));
+        const uint64_t b_off = w_off + uint64_t(gi) * kg * rsc * 2;
+        const bool do_params = first_group && bind_params;
+        auto rebind = [=](cudaStream_t s) {
+          if (first_group && wpad) pad_rows(wptr(w_off), cout, rsc, wpad, kp, s);
+          if (!wpad) prep->tb = gemm::make_tmap(wptr(b_off), uint64_t(kg), uint64_t(kp), uint64_t(kp), prep->bn);
+          else prep->tb = gemm::make_tmap(wpad + uint64_t(gi) * kg * kp, uint64_t(kg), uint64_t(kp), uint64_t(kp),
+                                         prep->bn);
+          if (do_params) bind_params(s);
+        };
+        steps_.push_back(std::make_unique<Step>(Step{[prep](cudaStream_t s) { gemm::run(*prep, s); }, rebind}));
+        first_group = false;
       }
       flops_ += 2.0 * double(M) * cout * rsc;
       if (!l.s("out").empty()) named[l.s("out")] = out;
@@ -214,26 +230,26 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       const int k = l.i("k"), st = l.i("stride", k), pad = l.i("pad", 0);
       const Act in = cur;
       const int P = (in.h + 2 * pad - k) / st + 1, Q = (in.w + 2 * pad - k) / st + 1;
-      Act out{reinterpret_cast<uint16_t*>(alloc(uint64_t(batch) * P * Q * in.c * 2)), batch, P, Q, in.c};
+      const Act out{reinterpret_cast<uint16_t*>(alloc(uint64_t(batch) * P * Q * in.c * 2)), batch, P, Q, in.c};
       steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) {
         nn::maxpool(in.p, out.p, in.n, in.h, in.w, in.c, k, st, pad, P, Q, s);
-      }, 1}));
+      }}));
       if (!l.s("out").empty()) named[l.s("out")] = out;
       cur = out;
     } else if (l.kind == "pool_avg") {
       const Act in = cur;
-      Act out{reinterpret_cast<uint16_t*>(alloc(uint64_t(batch) * in.c * 2)), batch, 1, 1, in.c};
+      const Act out{reinterpret_cast<uint16_t*>(alloc(uint64_t(batch) * in.c * 2)), batch, 1, 1, in.c};
       steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) {
         nn::avgpool_global(in.p, out.p, in.n, in.h * in.w, in.c, s);
-      }, 1}));
+      }}));
       cur = out;
     } else if (l.kind == "flatten") {
       const Act in = cur;
       if (in.h * in.w > 1) {  // FC weights expect torch's NCHW flatten order
-        Act out{reinterpret_cast<uint16_t*>(alloc(in.elems() * 2)), batch, 1, 1, in.h * in.w * in.c};
+        const Act out{reinterpret_cast<uint16_t*>(alloc(in.elems() * 2)), batch, 1, 1, in.h * in.w * in.c};
         steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) {
           nn::flatten_nchw(in.p, out.p, in.n, in.h * in.w, in.c, s);
-        }, 1}));
+        }}));
         cur = out;
       } else {
         cur = {in.p, batch, 1, 1, in.c};
@@ -242,34 +258,44 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       const Act in = cur;
       const int cin = l.i("cin"), cout = l.i("cout");
       if (in.c != cin) raise(Errc::InvalidArgument, l.s("name") + ": fc input mismatch");
-      const uint16_t* W = tensor(l.s("name") + ".weight", fmt::DType::BF16);
+      const uint64_t w_off = offset_of(l.s("name") + ".weight");
       float* bias = nullptr;
+      uint64_t b_off = 0;
       if (l.i("bias")) {
         bias = reinterpret_cast<float*>(alloc(uint64_t(cout) * 4));
-        bf16_to_f32(tensor(l.s("name") + ".bias", fmt::DType::BF16), bias, cout, bind);
+        b_off = offset_of(l.s("name") + ".bias");
       }
       const bool last = int(li) == last_fc;
       const bool relu = l.i("relu") != 0;
-      Act out{reinterpret_cast<uint16_t*>(alloc(uint64_t(batch) * cout * 2)), batch, 1, 1, cout};
+      const Act out{reinterpret_cast<uint16_t*>(alloc(uint64_t(batch) * cout * 2)), batch, 1, 1, cout};
       if (last) {
         classes_ = cout;
         logits_ = reinterpret_cast<float*>(alloc(uint64_t(batch) * cout * 4));
       }
       float* lg = last ? logits_ : nullptr;
       const int sms = sms_;
+      auto bind_bias = [=](cudaStream_t s) {
+        if (bias) bf16_to_f32(wptr(b_off), bias, cout, s);
+      };
       if (batch <= 8) {  // HBM-bound GEMV: weights streamed once
         steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) {
-          nn::gemv(in.p, batch, cin, W, cout, bias, relu, out.p, lg, cout, sms, s);
-        }, 1}));
+          nn::gemv(in.p, batch, cin, wptr(w_off), cout, bias, relu, out.p, lg, cout, sms, s);
+        }, bind_bias}));
       } else {
         gemm::Epilogue e{out.p, uint64_t(cout), nullptr, bias, nullptr, 0, relu};
-        gemm::Prepared prep = gemm::prepare({in.p, uint64_t(batch), uint64_t(cin), uint64_t(cin)},
-                                            {W, uint64_t(cout), uint64_t(cin), uint64_t(cin)}, e);
-        steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) { gemm::run(prep, s); }, 1}));
+        auto prep = std::make_shared<gemm::Prepared>(
+            gemm::prepare({in.p, uint64_t(batch), uint64_t(cin), uint64_t(cin)},
+                          {reinterpret_cast<const uint16_t*>(uintptr_t(256)), uint64_t(cout), uint64_t(cin),
+                           uint64_t(cin)},
+                          e));
+        auto rebind = [=](cudaStream_t s) {
+          prep->tb = gemm::make_tmap(wptr(w_off), uint64_t(cout), uint64_t(cin), uint64_t(cin), prep->bn);
+          bind_bias(s);
+        };
+        steps_.push_back(std::make_unique<Step>(Step{[prep](cudaStream_t s) { gemm::run(*prep, s); }, rebind}));
         if (last) {
           const int n = batch * cout;
-          steps_.push_back(
-              std::make_unique<Step>(Step{[=](cudaStream_t s) { nn::bf16_to_f32(out.p, lg, n, s); }, 1}));
+          steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) { nn::bf16_to_f32(out.p, lg, n, s); }}));
         }
       }
       flops_ += 2.0 * double(batch) * cin * cout;
@@ -280,9 +306,8 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
   }
   if (!logits_) raise(Errc::InvalidArgument, "architecture has no fc output");
   for (const auto& s : steps_) launches_ += s->launches;
-  TRIMS_CUDA(cudaStreamSynchronize(bind));
-  cudaStreamDestroy(bind);
   TRIMS_CUDA(cudaStreamCreateWithFlags(&capture_stream_, cudaStreamNonBlocking));
+  rebind(weights);
 }
 
 Net::~Net() {
@@ -293,8 +318,22 @@ Net::~Net() {
   for (void* p : owned_) cudaFree(p);
 }
 
+void Net::rebind(const uint8_t* weights) {
+  DeviceGuard g(device_);
+  wbase_ = weights;
+  for (const auto& s : steps_)
+    if (s->rebind) s->rebind(capture_stream_);
+  TRIMS_CUDA(cudaStreamSynchronize(capture_stream_));
+  if (exec_) {  // kernel parameters (tensor maps, pointers) changed: re-capture
+    cudaGraphExecDestroy(exec_);
+    cudaGraphDestroy(graph_);
+    exec_ = nullptr;
+    graph_ = nullptr;
+  }
+}
+
 void Net::record(cudaStream_t stream) {
-  for (const auto& s : steps_) s->fn(stream);
+  for (const auto& s : steps_) s->run(stream);
 }
 
 void Net::run(cudaStream_t stream, bool use_graph) {

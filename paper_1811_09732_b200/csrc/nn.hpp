@@ -45,6 +45,9 @@ class Net {
   // One forward pass on `stream`; with use_graph the launch sequence is
   // captured once into a CUDA graph and replayed.
   void run(cudaStream_t stream, bool use_graph);
+  // Point the executor at another generation of the same resident model
+  // (identical manifest, new segment): recomputes weight-dependent state only.
+  void rebind(const uint8_t* weights);
   double flops() const { return flops_; }
   uint32_t launches() const { return launches_; }
   uint64_t workspace_bytes() const { return ws_bytes_; }
@@ -55,6 +58,7 @@ class Net {
   uint8_t* alloc(uint64_t bytes);
 
   int device_, batch_, sms_{148};
+  const uint8_t* wbase_{nullptr};  // current weights generation (resident blob base)
   int in_hw_{224}, in_c_{3}, classes_{1000};
   std::vector<std::unique_ptr<Step>> steps_;
   std::vector<void*> owned_;

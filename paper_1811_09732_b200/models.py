@@ -67,6 +67,13 @@ class BoundNet:
         return TensorView("logits", [self.batch, self.classes], "f32", "native", 0, self.batch * self.classes * 4,
                           self.logits_ptr).torch(f"cuda:{self.device}")
 
+    def rebind(self, view) -> None:
+        """Follow the model to a new segment (same resident manifest, new generation)."""
+        if view.manifest_json != self.view.manifest_json:
+            raise ValueError("rebind needs the same resident manifest")
+        check(lib.trims_net_rebind(self._h, view.base_ptr))
+        self.view = view
+
     def run(self, stream=None, graph: bool = True) -> None:
         check(lib.trims_net_run(self._h, stream, int(graph)))
 

@@ -52,3 +52,27 @@ def test_forward_matches_fp32_reference(store, name, batch):
     assert torch.equal(got.argmax(1), ref.argmax(1))
     net.close()
     cli.close(view)
+
+
+def test_rebind_follows_a_reloaded_generation(store):
+    """Evict + reload the model (new generation, reused arena range): the bound
+    executor rebinds its weight-dependent state and reproduces the logits."""
+    import torch
+    arch = C.ARCHS["resnet50"]()
+    cli = Client(store)
+    v1 = cli.open(C.arch_key(arch), force_shared=True)
+    net = BoundNet(v1, arch, batch=2)
+    x = torch.randn(2, 3, 224, 224, generator=torch.Generator().manual_seed(5))
+    first = net.forward(x).clone()
+    cli.close(v1)
+    store.reclaim(0, 2 << 30)                      # evict everything from HBM
+    filler = C.ARCHS["alexnet"]()
+    f = cli.open(C.arch_key(filler), force_shared=True)  # reuse the freed arena range
+    v2 = cli.open(C.arch_key(arch), force_shared=True)
+    assert v2.generation != v1.generation
+    net.rebind(v2)
+    again = net.forward(x).clone()
+    assert torch.equal(first, again)
+    net.close()
+    cli.close(v2)
+    cli.close(f)
