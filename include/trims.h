@@ -127,6 +127,30 @@ typedef struct trims_export {
   uint64_t segment_offset;        /* segment start inside that allocation */
 } trims_export;
 
+/* ---- The TierBackend seam itself (cache_core.hpp:76-98): the eight virtuals
+ * of the reference's plugin, implemented by CudaTierBackend, for a reference
+ * CacheCore/daemon to drive directly (INTEGRATION.md shows the adapter).
+ * Manifests cross as their canonical JSON; the trailer checksum separately. */
+typedef struct trims_backend trims_backend;
+int trims_backend_create(const trims_store_config* cfg, trims_backend** out);
+void trims_backend_destroy(trims_backend* b);
+/* ShmTierBackend::locate (daemon.cpp:128-136); NotFound when absent (no remote tier). */
+int trims_backend_locate(trims_backend* b, const char* ns, const char* name, const char* version, char* path_out,
+                         uint64_t cap, uint64_t* file_bytes);
+/* ShmTierBackend::read_manifest (daemon.cpp:144-151) */
+int trims_backend_read_manifest(trims_backend* b, const char* ns, const char* name, const char* version,
+                                const char* path, char* json_out, uint64_t cap, uint8_t checksum_out[32]);
+/* ShmTierBackend::stage_host (daemon.cpp:153-158): disk -> pinned host tier */
+int trims_backend_stage_host(trims_backend* b, uint64_t model_id, const char* manifest_json,
+                             const uint8_t checksum[32], const char* path);
+/* ShmTierBackend::publish_fast (daemon.cpp:160-209): -> HBM arena segment, exported */
+int trims_backend_publish_fast(trims_backend* b, uint64_t model_id, const char* manifest_json, int from_host,
+                               const char* path, trims_export* out);
+/* ShmTierBackend::evict_fast/host/disk (daemon.cpp:211-224) */
+int trims_backend_evict_fast(trims_backend* b, uint64_t model_id);
+int trims_backend_evict_host(trims_backend* b, uint64_t model_id);
+int trims_backend_evict_disk(trims_backend* b, const char* path);
+
 /* Daemon::Daemon (daemon.cpp:298-391) minus listeners: builds the backend
  * and the core, optionally scans the disk cache. */
 int trims_store_create(const trims_store_config* cfg, trims_store** out);

@@ -44,6 +44,8 @@ def build(ref: bool | None = None) -> None:
     targets = ["port"]
     if ref or (ref is None and os.path.isdir("/root/reference/proj")):
         targets.append("ref")
+        if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_1811_09732_b200", "libtrims.so")):
+            targets.append("integration")  # reference CacheCore over the B200 backend
     subprocess.run(["make", "-s", "-C", HERE, "-j8", *targets], check=True)
 
 

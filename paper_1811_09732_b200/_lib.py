@@ -117,6 +117,15 @@ _SIGS = {
     "trims_fnv1a": (_u64, [_s]),
     "trims_touch_host": (_c.c_int, [_p, _s, _c.POINTER(_u64)]),
     "trims_checksum_host": (_c.c_int, [_p, _u64, _u64, _c.POINTER(_u64)]),
+    "trims_backend_create": (_c.c_int, [_c.POINTER(StoreConfig), _c.POINTER(_p)]),
+    "trims_backend_destroy": (None, [_p]),
+    "trims_backend_locate": (_c.c_int, [_p, _s, _s, _s, _s, _u64, _c.POINTER(_u64)]),
+    "trims_backend_read_manifest": (_c.c_int, [_p, _s, _s, _s, _s, _s, _u64, _p]),
+    "trims_backend_stage_host": (_c.c_int, [_p, _u64, _s, _p, _s]),
+    "trims_backend_publish_fast": (_c.c_int, [_p, _u64, _s, _c.c_int, _s, _c.POINTER(Export)]),
+    "trims_backend_evict_fast": (_c.c_int, [_p, _u64]),
+    "trims_backend_evict_host": (_c.c_int, [_p, _u64]),
+    "trims_backend_evict_disk": (_c.c_int, [_p, _s]),
     "trims_store_create": (_c.c_int, [_c.POINTER(StoreConfig), _c.POINTER(_p)]),
     "trims_store_destroy": (None, [_p]),
     "trims_store_open": (_c.c_int, [_p, _s, _s, _s, _u32, _u64, _c.POINTER(Export)]),

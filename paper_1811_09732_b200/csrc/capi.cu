@@ -267,27 +267,133 @@ int trims_checksum_host(const void* p, uint64_t n, uint64_t word0, uint64_t* out
 
 // ---------------------------------------------------------------- store
 
+namespace {
+// DaemonConfig validation (daemon.cpp:26-36) + the B200 backend settings.
+BackendConfig backend_config(const trims_store_config* cfg) {
+  if (!cfg) raise(Errc::InvalidArgument, "null argument");
+  if (!cfg->fast_capacity_bytes || !cfg->host_capacity_bytes || !cfg->disk_capacity_bytes)
+    raise(Errc::InvalidArgument, "capacities must be > 0");
+  if (!cfg->disk_cache_dir || !*cfg->disk_cache_dir) raise(Errc::InvalidArgument, "disk_cache_dir must be set");
+  if (trims_device_count() <= cfg->device) raise(Errc::NoDevice, "no CUDA device " + std::to_string(cfg->device));
+  std::filesystem::create_directories(cfg->disk_cache_dir);
+  BackendConfig bc;
+  bc.device = cfg->device;
+  bc.disk_cache_dir = cfg->disk_cache_dir;
+  bc.full_verify = cfg->full_verify != 0;
+  bc.plan = make_plan(cfg->plan_flags, cfg->out_dtype);
+  bc.pinned_pool_bytes = cfg->pinned_pool_bytes ? cfg->pinned_pool_bytes : cfg->host_capacity_bytes;
+  bc.read_threads = cfg->read_threads ? cfg->read_threads : 8;
+  // arena: 0 = auto (capacity + 1/16 + 64 MiB for per-segment rounding and tails), 1 = off
+  bc.arena_bytes = cfg->arena_bytes == 1 ? 0
+                   : cfg->arena_bytes ? cfg->arena_bytes
+                                      : cfg->fast_capacity_bytes + cfg->fast_capacity_bytes / 16 + (64ull << 20);
+  return bc;
+}
+
+void fill_export(const ExportedSegment& es, trims_export* out) {
+  out->device = es.device;
+  out->generation = es.generation;
+  out->payload_bytes = es.length;
+  out->resident_blob_bytes = es.resident_blob_bytes;
+  out->alloc_bytes = es.alloc_bytes;
+  out->ingest_checksum = es.ingest_checksum;
+  out->dev_ptr = es.dev_ptr;
+  out->fd = es.fd;
+  out->segment_offset = es.offset;
+  std::snprintf(out->token, sizeof out->token, "%s", es.token.c_str());
+}
+}  // namespace
+
+struct trims_backend {
+  std::unique_ptr<CudaTierBackend> be;
+};
+
+int trims_backend_create(const trims_store_config* cfg, trims_backend** out) {
+  return guard([&] {
+    auto b = std::make_unique<trims_backend>();
+    b->be = std::make_unique<CudaTierBackend>(backend_config(cfg));
+    *out = b.release();
+    return 0;
+  });
+}
+
+void trims_backend_destroy(trims_backend* b) {
+  try {
+    delete b;
+  } catch (...) {
+  }
+}
+
+int trims_backend_locate(trims_backend* b, const char* ns, const char* name, const char* version, char* path_out,
+                         uint64_t cap, uint64_t* file_bytes) {
+  return guard([&] {
+    Located l = b->be->locate({ns, name, version});
+    if (l.kind == Located::Kind::Absent) raise(Errc::NotFound, std::string(ns) + "/" + name + "@" + version);
+    if (file_bytes) *file_bytes = l.file_bytes;
+    return put(l.path, path_out, cap);
+  });
+}
+
+int trims_backend_read_manifest(trims_backend* b, const char* ns, const char* name, const char* version,
+                                const char* path, char* json_out, uint64_t cap, uint8_t checksum_out[32]) {
+  return guard([&] {
+    fmt::Manifest m = b->be->read_manifest({ns, name, version}, path);
+    if (checksum_out) std::memcpy(checksum_out, m.checksum.data(), 32);
+    return put(fmt::manifest_to_json(m), json_out, cap);
+  });
+}
+
+int trims_backend_stage_host(trims_backend* b, uint64_t model_id, const char* manifest_json,
+                             const uint8_t checksum[32], const char* path) {
+  return guard([&] {
+    fmt::Manifest m = fmt::manifest_from_json(manifest_json);
+    if (checksum) std::memcpy(m.checksum.data(), checksum, 32);
+    b->be->stage_host(model_id, m, path);
+    return 0;
+  });
+}
+
+int trims_backend_publish_fast(trims_backend* b, uint64_t model_id, const char* manifest_json, int from_host,
+                               const char* path, trims_export* out) {
+  return guard([&] {
+    FastPublication pub = b->be->publish_fast(model_id, fmt::manifest_from_json(manifest_json), from_host != 0,
+                                              path ? path : "");
+    std::memset(out, 0, sizeof *out);
+    out->model_id = model_id;
+    out->outcome = TRIMS_DISK_LOAD;
+    std::memcpy(out->manifest_digest, pub.manifest_digest.data(), 32);
+    fill_export(pub.segments.at(0), out);
+    out->n_objects = 1;
+    return 0;
+  });
+}
+
+int trims_backend_evict_fast(trims_backend* b, uint64_t model_id) {
+  return guard([&] {
+    b->be->evict_fast(model_id);
+    return 0;
+  });
+}
+
+int trims_backend_evict_host(trims_backend* b, uint64_t model_id) {
+  return guard([&] {
+    b->be->evict_host(model_id);
+    return 0;
+  });
+}
+
+int trims_backend_evict_disk(trims_backend* b, const char* path) {
+  return guard([&] {
+    b->be->evict_disk({}, path);
+    return 0;
+  });
+}
+
 int trims_store_create(const trims_store_config* cfg, trims_store** out) {
   return guard([&] {
-    if (!cfg || !out) raise(Errc::InvalidArgument, "null argument");
-    if (!cfg->fast_capacity_bytes || !cfg->host_capacity_bytes || !cfg->disk_capacity_bytes)
-      raise(Errc::InvalidArgument, "capacities must be > 0");  // daemon.cpp:26-36
-    if (!cfg->disk_cache_dir || !*cfg->disk_cache_dir) raise(Errc::InvalidArgument, "disk_cache_dir must be set");
-    if (trims_device_count() <= cfg->device) raise(Errc::NoDevice, "no CUDA device " + std::to_string(cfg->device));
-    std::filesystem::create_directories(cfg->disk_cache_dir);
+    if (!out) raise(Errc::InvalidArgument, "null argument");
     auto s = std::make_unique<trims_store>();
-    BackendConfig bc;
-    bc.device = cfg->device;
-    bc.disk_cache_dir = cfg->disk_cache_dir;
-    bc.full_verify = cfg->full_verify != 0;
-    bc.plan = make_plan(cfg->plan_flags, cfg->out_dtype);
-    bc.pinned_pool_bytes = cfg->pinned_pool_bytes ? cfg->pinned_pool_bytes : cfg->host_capacity_bytes;
-    bc.read_threads = cfg->read_threads ? cfg->read_threads : 8;
-    // arena: 0 = auto (capacity + 1/16 + 64 MiB for per-segment rounding and tails), 1 = off
-    bc.arena_bytes = cfg->arena_bytes == 1 ? 0
-                     : cfg->arena_bytes ? cfg->arena_bytes
-                                        : cfg->fast_capacity_bytes + cfg->fast_capacity_bytes / 16 + (64ull << 20);
-    s->be = std::make_unique<CudaTierBackend>(bc);
+    s->be = std::make_unique<CudaTierBackend>(backend_config(cfg));
     CoreConfig cc{cfg->fast_capacity_bytes, cfg->host_capacity_bytes, cfg->disk_capacity_bytes,
                   Policy(cfg->policy ? 1 : 0), cfg->eager_reclaim != 0};
     s->core = std::make_unique<CacheCore>(cc, *s->be);
@@ -332,19 +438,7 @@ int trims_store_open(trims_store* s, const char* ns, const char* name, const cha
     out->timings_ns[3] = r.timings.handle_export_ns;
     std::memcpy(out->manifest_digest, r.manifest_digest.data(), 32);
     out->fd = -1;
-    if (!r.segments.empty()) {
-      const ExportedSegment& es = r.segments[0];
-      out->device = es.device;
-      out->generation = es.generation;
-      out->payload_bytes = es.length;
-      out->resident_blob_bytes = es.resident_blob_bytes;
-      out->alloc_bytes = es.alloc_bytes;
-      out->ingest_checksum = es.ingest_checksum;
-      out->dev_ptr = es.dev_ptr;
-      out->fd = es.fd;
-      out->segment_offset = es.offset;
-      std::snprintf(out->token, sizeof out->token, "%s", es.token.c_str());
-    }
+    if (!r.segments.empty()) fill_export(r.segments[0], out);
     // objects of the resident blob at the requested granularity (count only)
     const uint64_t rbb = out->resident_blob_bytes;
     if (rbb == 0) out->n_objects = 1;
