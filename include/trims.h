@@ -99,6 +99,14 @@ typedef struct trims_store_config {
   uint32_t scan_disk;            /* register *.trms in disk_cache_dir at start (daemon.cpp:314-325) */
   uint32_t read_threads;         /* parallel pread threads for disk -> pinned (0 = 8) */
   uint64_t arena_bytes;          /* HBM arena of the fast tier: 0 = auto, 1 = off (one cuMem allocation per model) */
+  /* Multi-GPU (no reference counterpart — the reference runs
+   * one daemon per node): one store per GPU process, all sharing a node-local
+   * residency directory. A fast-tier miss whose model is sealed on a peer GPU
+   * is served by an NVLink pull of the peer's segment (TRIMS_PEER_HIT). */
+  const char* directory;         /* /dev/shm name shared by the node's stores; NULL = single GPU */
+  int32_t rank;                  /* this store's row in the directory */
+  int32_t world;                 /* stores on the node */
+  uint32_t directory_slots;      /* per-rank slots (0 = 1024) */
 } trims_store_config;
 
 /* Reference outcomes (cache_core.hpp:36) + PEER_HIT for the multi-GPU directory. */
@@ -180,6 +188,31 @@ int trims_store_resident_json(trims_store* s, uint64_t model_id, char* out, uint
 int trims_store_ingest_stats(trims_store* s, uint64_t model_id, double out7[7]);
 /* Per-tensor block checksums of a resident model (buckets = tensors + 1). */
 int trims_store_checksums(trims_store* s, uint64_t model_id, uint64_t* out, uint64_t cap, uint64_t* n);
+/* Is the model fast-resident in this store (no state change)? */
+int trims_store_fast_resident(trims_store* s, const char* ns, const char* name, const char* version, int* out);
+
+/* ------------------------------------------- multi-GPU residency directory */
+
+/* One sealed fast-tier segment as published for peers. */
+typedef struct trims_dir_coords {
+  int32_t rank, device, pid, fd;  /* owner rank / GPU / process, and its fd of the exportable allocation */
+  uint32_t arena, reserved;       /* arena: the allocation outlives the segment */
+  uint64_t alloc_bytes, offset;   /* allocation size; segment offset inside it */
+  uint64_t payload_bytes, resident_blob_bytes, generation, checksum;
+} trims_dir_coords;
+
+typedef struct trims_dir trims_dir;
+/* Create or attach the node directory `name` for world x slots; clears `rank`'s row. */
+int trims_dir_open(const char* name, int world, int rank, uint32_t slots, trims_dir** out);
+void trims_dir_close(trims_dir* d); /* clears this rank's row */
+int trims_dir_unlink(const char* name);
+int trims_dir_publish(trims_dir* d, const char* ns, const char* name, const char* version, const trims_dir_coords* c);
+int trims_dir_retract(trims_dir* d, const char* ns, const char* name, const char* version);
+/* Other ranks' live copies, best peer first (rendezvous order). */
+int trims_dir_holders(trims_dir* d, const char* ns, const char* name, const char* version, trims_dir_coords* out,
+                      uint64_t cap, uint64_t* n);
+/* Rendezvous weight of (key "ns/name@version", rank). */
+uint64_t trims_peer_score(const char* key, int rank);
 
 /* --------------------------------------------------- client attach (a5, a9) */
 
@@ -271,6 +304,16 @@ int trims_softmax(const float* in, float* out, int M, int N, void* stream);
  * in-memory backend (the reference FakeBackend contract, oracle.cpp:14-91).
  * Same spec / output text as oracle/ref_shim.cpp:ref_replay's "live" lines. */
 int trims_replay(const char* spec, char* out, uint64_t cap);
+
+/* One rank of a simulated node: the same CacheCore + open_with_peers as a
+ * store, over the in-memory backend of trims_replay, publishing to a real
+ * directory. spec = the "cfg" and "model" lines of a replay spec. step: kind
+ * 'o' (open through the directory) or 'c' (close) of model i at clock `now`;
+ * writes "<outcome> <fast_used> <host_used> <refcount> <peer_rank>". */
+typedef struct trims_simcore trims_simcore;
+int trims_simcore_create(const char* spec, const char* directory, int world, int rank, trims_simcore** out);
+void trims_simcore_destroy(trims_simcore* c);
+int trims_simcore_step(trims_simcore* c, char kind, uint32_t model, uint64_t now, char* out, uint64_t cap);
 
 #ifdef __cplusplus
 }

@@ -124,24 +124,23 @@ class _World:
         return True
 
 
-def simulate(cfg: SimConfig, models: list[SimModel], trace: list[tuple[str, int]]) -> list[SimEvent]:
-    """simulator.cpp:131-254. trace items are ("o"|"c", model_index)."""
-    w = _World(cfg, models)
-    events = []
-    for step, (kind, i) in enumerate(trace):
-        now = step + 1
-        m = models[i]
+class Core(_World):
+    """One store's decision state, stepped one op at a time (simulate() below
+    is the reference loop over it). Op kinds: "o" open, "c" close, and the
+    multi-GPU extension "p": open with a peer copy available."""
+
+    def step(self, kind: str, i: int, now: int) -> SimEvent:
+        cfg, m, w = self.cfg, self.models[i], self
         ev = SimEvent(FAST_HIT, 0, 0, 0)
 
         def finish():
             ev.fast_used, ev.host_used, ev.refcount = w.used[0], w.used[1], w.rc[i]
-            events.append(ev)
+            return ev
 
         if kind == "c":
             if not w.has[i] or w.rc[i] == 0:
                 ev.outcome = ERR_NOT_OPEN
-                finish()
-                continue
+                return finish()
             w.rc[i] -= 1
             if cfg.eager_reclaim and w.rc[i] == 0:
                 if w.res[0][i]:
@@ -150,16 +149,33 @@ def simulate(cfg: SimConfig, models: list[SimModel], trace: list[tuple[str, int]
                 if w.res[1][i]:
                     w.drop(1, i)
                     ev.evicted_host.append(i)
-            finish()
-            continue
+            return finish()
 
         if w.has[i] and w.res[0][i]:
             w.rc[i] += 1
             w.last[i] = now
             w.uses[i] += 1
             ev.outcome = FAST_HIT
-            finish()
-            continue
+            return finish()
+
+        if kind == "p":
+            # PeerHit (builder-defined, paper_1811_09732_b200/csrc/cache_core.cpp
+            # open_model with a PeerSource): fast-tier admission only; host and
+            # disk tiers untouched.
+            w.touch_entry(i)
+            if m.weights_bytes > cfg.fast_capacity:
+                ev.outcome = ERR_TOO_LARGE
+                return finish()
+            if not w.reclaim(0, m.weights_bytes, ev.evicted_fast, i):
+                ev.outcome = ERR_NO_EVICTABLE
+                return finish()
+            w.used[0] += m.weights_bytes
+            w.res[0][i] = True
+            w.rc[i] += 1
+            w.last[i] = now
+            w.uses[i] += 1
+            ev.outcome = PEER_HIT
+            return finish()
 
         host_hit = w.has[i] and w.res[1][i]
         fetched = False
@@ -167,8 +183,7 @@ def simulate(cfg: SimConfig, models: list[SimModel], trace: list[tuple[str, int]
             have_disk = w.has[i] and w.res[2][i]
             if not have_disk and not m.on_remote:
                 ev.outcome = ERR_NOT_FOUND
-                finish()
-                continue
+                return finish()
             fetched = not have_disk
         w.touch_entry(i)
 
@@ -184,14 +199,12 @@ def simulate(cfg: SimConfig, models: list[SimModel], trace: list[tuple[str, int]
             if temp_file:
                 ev.evicted_disk.append(i)
             ev.outcome = ERR_TOO_LARGE
-            finish()
-            continue
+            return finish()
         if not w.reclaim(0, m.weights_bytes, ev.evicted_fast, i):
             if temp_file:
                 ev.evicted_disk.append(i)
             ev.outcome = ERR_NO_EVICTABLE
-            finish()
-            continue
+            return finish()
         w.used[0] += m.weights_bytes
 
         staged = False
@@ -208,8 +221,67 @@ def simulate(cfg: SimConfig, models: list[SimModel], trace: list[tuple[str, int]
         w.last[i] = now
         w.uses[i] += 1
         ev.outcome = HOST_HIT if host_hit else (REMOTE_FETCH if fetched else DISK_LOAD)
-        finish()
-    return events
+        return finish()
+
+
+def simulate(cfg: SimConfig, models: list[SimModel], trace: list[tuple[str, int]]) -> list[SimEvent]:
+    """simulator.cpp:131-254. trace items are ("o"|"c", model_index); "p"
+    (peer copy available) is the multi-GPU extension."""
+    core = Core(cfg, models)
+    return [core.step(kind, i, step + 1) for step, (kind, i) in enumerate(trace)]
+
+
+# --- N > 1 (builder-defined extension, SURVEY.md §8e) -----------------------
+
+_GOLD = 0x9E3779B97F4A7C15
+_M64 = (1 << 64) - 1
+
+
+def _mix64(z: int) -> int:
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def _fnv1a(s: str) -> int:
+    h = 0xCBF29CE484222325
+    for c in s.encode():
+        h = ((h ^ c) * 0x100000001B3) & _M64
+    return h
+
+
+def peer_score(key: str, rank: int) -> int:
+    """Rendezvous weight of (key, rank) (csrc/directory.cpp:peer_score)."""
+    return _mix64(_fnv1a(key) ^ (((rank + 1) * _GOLD) & _M64))
+
+
+def trace_key(i: int) -> str:
+    """Key string of model i in a replay spec (csrc/replay.cpp FakeBackend::key_of)."""
+    return f"trace/m{i}@1"
+
+
+def simulate_cluster(cfg: SimConfig, models: list[SimModel], world: int,
+                     trace: list[tuple[int, str, int]]) -> list[tuple[SimEvent, int]]:
+    """N stores (one per GPU) sharing a residency directory; trace items are
+    (rank, "o"|"c", model). An open at rank r of a model that is not
+    fast-resident at r, is fast-resident on another rank, and whose artifact
+    is on r's disk tier, is a PeerHit served by the holder with the highest
+    peer_score; anything else is the single-store step. Returns (event, peer
+    rank or -1) per op. With world == 1 this is simulate() exactly."""
+    cores = [Core(cfg, models) for _ in range(world)]
+    out = []
+    for step, (r, kind, i) in enumerate(trace):
+        w = cores[r]
+        peer = -1
+        if kind == "o" and not (w.has[i] and w.res[0][i]) and w.has[i] and w.res[2][i]:
+            holders = [h for h in range(world) if h != r and cores[h].has[i] and cores[h].res[0][i]]
+            if holders:
+                peer = max(holders, key=lambda h: peer_score(trace_key(i), h))
+        ev = w.step("p" if peer >= 0 else kind, i, step + 1)
+        if ev.outcome != PEER_HIT:
+            peer = -1
+        out.append((ev, peer))
+    return out
 
 
 def spec_text(cfg: SimConfig, models: list[SimModel], trace: list[tuple[str, int]]) -> str:

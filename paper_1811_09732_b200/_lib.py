@@ -67,6 +67,27 @@ class StoreConfig(ctypes.Structure):
         ("scan_disk", ctypes.c_uint32),
         ("read_threads", ctypes.c_uint32),
         ("arena_bytes", ctypes.c_uint64),
+        ("directory", ctypes.c_char_p),
+        ("rank", ctypes.c_int32),
+        ("world", ctypes.c_int32),
+        ("directory_slots", ctypes.c_uint32),
+    ]
+
+
+class DirCoords(ctypes.Structure):
+    _fields_ = [
+        ("rank", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("pid", ctypes.c_int32),
+        ("fd", ctypes.c_int32),
+        ("arena", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
+        ("alloc_bytes", ctypes.c_uint64),
+        ("offset", ctypes.c_uint64),
+        ("payload_bytes", ctypes.c_uint64),
+        ("resident_blob_bytes", ctypes.c_uint64),
+        ("generation", ctypes.c_uint64),
+        ("checksum", ctypes.c_uint64),
     ]
 
 
@@ -137,6 +158,17 @@ _SIGS = {
     "trims_store_resident_json": (_c.c_int, [_p, _u64, _s, _u64]),
     "trims_store_ingest_stats": (_c.c_int, [_p, _u64, _c.POINTER(_c.c_double)]),
     "trims_store_checksums": (_c.c_int, [_p, _u64, _c.POINTER(_u64), _u64, _c.POINTER(_u64)]),
+    "trims_store_fast_resident": (_c.c_int, [_p, _s, _s, _s, _c.POINTER(_c.c_int)]),
+    "trims_dir_open": (_c.c_int, [_s, _c.c_int, _c.c_int, _u32, _c.POINTER(_p)]),
+    "trims_dir_close": (None, [_p]),
+    "trims_dir_unlink": (_c.c_int, [_s]),
+    "trims_dir_publish": (_c.c_int, [_p, _s, _s, _s, _c.POINTER(DirCoords)]),
+    "trims_dir_retract": (_c.c_int, [_p, _s, _s, _s]),
+    "trims_dir_holders": (_c.c_int, [_p, _s, _s, _s, _c.POINTER(DirCoords), _u64, _c.POINTER(_u64)]),
+    "trims_peer_score": (_u64, [_s, _c.c_int]),
+    "trims_simcore_create": (_c.c_int, [_s, _s, _c.c_int, _c.c_int, _c.POINTER(_p)]),
+    "trims_simcore_destroy": (None, [_p]),
+    "trims_simcore_step": (_c.c_int, [_p, _c.c_char, _u32, _u64, _s, _u64]),
     "trims_import_open": (_c.c_int, [_c.c_int, _c.c_int, _u64, _c.POINTER(_p), _c.POINTER(_p)]),
     "trims_import_attach": (_c.c_int, [_p, _u64, _u64, _u64, _p, _c.POINTER(_p), _s, _u64]),
     "trims_import_read_only": (_c.c_int, [_p]),

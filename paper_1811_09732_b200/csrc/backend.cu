@@ -230,6 +230,29 @@ uint32_t Ingestor::from_device(const IngestPlan& ip, const uint8_t* d_src, uint8
                                   d_dst, d_sums, stream, sms_);
 }
 
+uint64_t Ingestor::pull(const IngestPlan& ip, const uint8_t* d_src, uint8_t* d_dst, std::vector<uint64_t>* buckets,
+                        IngestStats* st) {
+  if (!ip.identity) raise(Errc::Internal, "peer pull needs an identity plan");
+  std::lock_guard lk(mu_);
+  DeviceGuard g(device_);
+  const ingest::TilePlan& p = ip.plan;
+  unsigned long long* ds = sums(p.buckets);
+  TRIMS_CUDA(cudaMemsetAsync(ds, 0, p.buckets * sizeof(unsigned long long), compute_));
+  TRIMS_CUDA(cudaEventRecord(c0_, compute_));
+  const uint32_t launches = ingest::launch_pull(ip.d_tiles_k, p.groups, d_src, d_dst, ds, compute_, sms_);
+  TRIMS_CUDA(cudaEventRecord(c1_, compute_));
+  const uint64_t total = finish(p, buckets);
+  if (st) {
+    float ms = 0;
+    TRIMS_CUDA(cudaEventElapsedTime(&ms, c0_, c1_));
+    st->total_ms = ms;
+    st->h2d_ms = 0;
+    st->h2d_bytes = 0;
+    st->launches = launches;
+  }
+  return total;
+}
+
 // ---------------------------------------------------------------------------
 // CudaTierBackend
 
@@ -329,59 +352,26 @@ std::shared_ptr<IngestPlan> CudaTierBackend::plan_for(uint64_t model_id, const f
   return plans_.emplace(model_id, std::move(p)).first->second;
 }
 
-// daemon.cpp:160-209: build, fill and seal the fast-tier segment, then
-// export it. Payload = resident blob | manifest JSON | u64 LE jlen, then the
-// 64-byte SegTail.
-FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Manifest& m, bool from_host,
-                                              const std::string& path) {
-  auto rec = std::make_shared<FastRecord>();
-  std::shared_ptr<IngestPlan> plan = plan_for(model_id, m);
-  rec->resident = plan->dst;
-  rec->json = plan->dst_json;
-  const uint64_t rb = rec->resident.blob_bytes;
-  const uint64_t payload = rb + rec->json.size() + 8;
+void CudaTierBackend::place(FastRecord& rec, uint64_t payload) {
   auto a0 = std::chrono::steady_clock::now();
   uint64_t off = 0, reserved = 0;
   if (arena_ && arena_->alloc(payload + sizeof(SegTail), &off, &reserved)) {
-    rec->arena = arena_.get();
-    rec->offset = off;
-    rec->reserved = reserved;
+    rec.arena = arena_.get();
+    rec.offset = off;
+    rec.reserved = reserved;
   } else {
-    rec->seg = DeviceSegment::create(cfg_.device, payload + sizeof(SegTail));
+    rec.seg = DeviceSegment::create(cfg_.device, payload + sizeof(SegTail));
   }
-  uint8_t* const base = rec->base();
-  const double alloc_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a0).count();
-  rec->generation = next_gen_.fetch_add(1);
+  rec.stats.alloc_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a0).count();
+  rec.generation = next_gen_.fetch_add(1);
+}
 
-  if (from_host) {
-    const uint8_t* src = nullptr;
-    {
-      std::lock_guard lk(mu_);
-      auto it = host_.find(model_id);
-      if (it == host_.end()) raise(Errc::Internal, "host buffer missing for publish");
-      if (it->second.bytes != m.blob_bytes) raise(Errc::Internal, "host buffer size mismatch");
-      src = it->second.p;  // single-flight pins the entry while loading
-    }
-    rec->checksum = ing_.from_host(*plan, src, base, &rec->bucket_sums, &rec->stats);
-  } else {
-    int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
-    if (fd < 0) raise(Errc::NotFound, path);
-    try {
-      uint8_t hdr[16];
-      if (::pread(fd, hdr, 16, 0) != 16) raise(Errc::Corrupt, "short read on " + path);
-      uint64_t mlen = 0;
-      for (int i = 0; i < 8; ++i) mlen |= uint64_t(hdr[8 + i]) << (8 * i);
-      rec->checksum = ing_.from_file(*plan, fd, fmt::blob_file_offset(mlen), base, &rec->bucket_sums,
-                                     &rec->stats);
-    } catch (...) {
-      ::close(fd);
-      throw;
-    }
-    ::close(fd);
-  }
-
-  // Tail: JSON, its length, the sealed SegTail.
+// Tail: JSON, its length, the sealed SegTail; then the export record.
+FastPublication CudaTierBackend::seal(uint64_t model_id, std::shared_ptr<FastRecord> rec, const fmt::Manifest& m) {
   auto s0 = std::chrono::steady_clock::now();
+  uint8_t* const base = rec->base();
+  const uint64_t rb = rec->resident.blob_bytes;
+  const uint64_t payload = rb + rec->json.size() + 8;
   std::vector<uint8_t> tail(rec->json.size() + 8 + sizeof(SegTail));
   std::memcpy(tail.data(), rec->json.data(), rec->json.size());
   uint64_t jlen = rec->json.size();
@@ -415,11 +405,120 @@ FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Mani
   es.ingest_checksum = rec->checksum;
   pub.segments.push_back(es);
   pub.manifest_digest = Sha256::of(rec->json.data(), rec->json.size());
-  rec->stats.alloc_ms = alloc_ms;
+  rec->key = m.key;
   rec->stats.seal_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - s0).count();
+  if (cfg_.directory) {
+    DirCoords c;
+    c.device = cfg_.device;
+    c.pid = int32_t(::getpid());
+    c.fd = es.fd;
+    c.arena = rec->arena ? 1 : 0;
+    c.alloc_bytes = es.alloc_bytes;
+    c.offset = es.offset;
+    c.payload_bytes = payload;
+    c.resident_blob_bytes = rb;
+    c.generation = rec->generation;
+    c.checksum = rec->checksum;
+    cfg_.directory->publish(m.key, c);  // only after the tail is sealed
+  }
   std::lock_guard lk(mu_);
   fast_[model_id] = std::move(rec);
   return pub;
+}
+
+// daemon.cpp:160-209: the fast-tier (HBM) segment holds the RESIDENT blob
+// (converted / permuted per the plan), then its JSON manifest and the
+// 64-byte SegTail.
+FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Manifest& m, bool from_host,
+                                              const std::string& path) {
+  auto rec = std::make_shared<FastRecord>();
+  std::shared_ptr<IngestPlan> plan = plan_for(model_id, m);
+  rec->resident = plan->dst;
+  rec->json = plan->dst_json;
+  place(*rec, rec->resident.blob_bytes + rec->json.size() + 8);
+  uint8_t* const base = rec->base();
+  const double alloc_ms = rec->stats.alloc_ms;
+
+  if (from_host) {
+    const uint8_t* src = nullptr;
+    {
+      std::lock_guard lk(mu_);
+      auto it = host_.find(model_id);
+      if (it == host_.end()) raise(Errc::Internal, "host buffer missing for publish");
+      if (it->second.bytes != m.blob_bytes) raise(Errc::Internal, "host buffer size mismatch");
+      src = it->second.p;  // single-flight pins the entry while loading
+    }
+    rec->checksum = ing_.from_host(*plan, src, base, &rec->bucket_sums, &rec->stats);
+  } else {
+    int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
+    if (fd < 0) raise(Errc::NotFound, path);
+    try {
+      uint8_t hdr[16];
+      if (::pread(fd, hdr, 16, 0) != 16) raise(Errc::Corrupt, "short read on " + path);
+      uint64_t mlen = 0;
+      for (int i = 0; i < 8; ++i) mlen |= uint64_t(hdr[8 + i]) << (8 * i);
+      rec->checksum = ing_.from_file(*plan, fd, fmt::blob_file_offset(mlen), base, &rec->bucket_sums,
+                                     &rec->stats);
+    } catch (...) {
+      ::close(fd);
+      throw;
+    }
+    ::close(fd);
+  }
+  rec->stats.alloc_ms = alloc_ms;
+  return seal(model_id, std::move(rec), m);
+}
+
+// Multi-GPU extension: fill this GPU's fast tier from a peer's
+// sealed segment. One fused kernel pulls the resident blob over NVLink and
+// hashes it; the peer's tail must show the same sealed generation before and
+// after the pull (a seqlock: an eviction scrubs the tail before the range can
+// be reused), and the pulled checksum must equal the one the peer sealed.
+FastPublication CudaTierBackend::publish_from_peer(uint64_t model_id, const fmt::Manifest& m, const PeerSource& src) {
+  auto rec = std::make_shared<FastRecord>();
+  std::shared_ptr<IngestPlan> plan = plan_for(model_id, m);
+  rec->resident = plan->dst;
+  rec->json = plan->dst_json;
+  const uint64_t rb = rec->resident.blob_bytes;
+  const uint64_t payload = rb + rec->json.size() + 8;
+  if (!src.payload || src.resident_blob_bytes != rb || src.payload_bytes != payload)
+    raise(Errc::InvalidArgument, "peer segment of " + fmt::to_string(m.key) + " has a different resident layout " +
+                                     "(stores must share the ingest plan)");
+  DeviceGuard g(cfg_.device);
+  auto read_tail = [&](std::string* json) {
+    SegTail t{};
+    TRIMS_CUDA(cudaMemcpy(&t, src.payload + payload, sizeof t, cudaMemcpyDefault));
+    if (t.magic != kSegMagic || !t.sealed || t.generation != src.generation || t.length != payload ||
+        t.blob_bytes != rb)
+      raise(Errc::StaleGeneration, "peer segment of " + fmt::to_string(m.key) + " changed (generation " +
+                                       std::to_string(src.generation) + ")");
+    if (json) {
+      json->resize(rec->json.size());
+      TRIMS_CUDA(cudaMemcpy(json->data(), src.payload + rb, json->size(), cudaMemcpyDefault));
+    }
+  };
+  std::string peer_json;
+  read_tail(&peer_json);
+  if (peer_json != rec->json) raise(Errc::InvalidArgument, "peer resident manifest differs (plan mismatch)");
+  place(*rec, payload);
+  std::shared_ptr<IngestPlan> ident = pull_plan_for(model_id, rec->resident);
+  rec->checksum = ing_.pull(*ident, src.payload, rec->base(), &rec->bucket_sums, &rec->stats);
+  read_tail(nullptr);
+  if (rec->checksum != src.checksum)
+    raise(Errc::ChecksumMismatch, "peer pull of " + fmt::to_string(m.key) + ": checksum " +
+                                      std::to_string(rec->checksum) + " != sealed " + std::to_string(src.checksum));
+  return seal(model_id, std::move(rec), m);
+}
+
+std::shared_ptr<IngestPlan> CudaTierBackend::pull_plan_for(uint64_t model_id, const fmt::Manifest& resident) {
+  {
+    std::lock_guard lk(mu_);
+    auto it = pull_plans_.find(model_id);
+    if (it != pull_plans_.end()) return it->second;
+  }
+  std::shared_ptr<IngestPlan> p = ing_.compile(resident, fmt::Plan{});
+  std::lock_guard lk(mu_);
+  return pull_plans_.emplace(model_id, std::move(p)).first->second;
 }
 
 void CudaTierBackend::evict_fast(uint64_t model_id) {
@@ -431,6 +530,7 @@ void CudaTierBackend::evict_fast(uint64_t model_id) {
     victim = std::move(it->second);
     fast_.erase(it);
   }
+  if (cfg_.directory) cfg_.directory->retract(victim->key);  // before the scrub: peers stop choosing it
   if (victim->arena) {
     // The range returns to the arena: scrub the sealed tail so an importer
     // holding the old (offset, generation) can never validate it again, even
@@ -438,6 +538,7 @@ void CudaTierBackend::evict_fast(uint64_t model_id) {
     DeviceGuard g(cfg_.device, /*nothrow=*/true);
     const uint64_t payload = victim->resident.blob_bytes + victim->json.size() + 8;
     cudaMemset(victim->base() + payload, 0, sizeof(SegTail));
+    cudaStreamSynchronize(cudaStreamLegacy);  // scrubbed before the range can be reallocated
   }
   // A dedicated segment's physical memory lives on in importers' mappings.
 }

@@ -15,6 +15,7 @@
 
 #include "cache_core.hpp"
 #include "device_mem.hpp"
+#include "directory.hpp"
 #include "format.hpp"
 #include "ingest.hpp"
 
@@ -65,6 +66,10 @@ class Ingestor {
   // asynchronous on `stream`; bucket sums accumulate into d_sums.
   uint32_t from_device(const IngestPlan& p, const uint8_t* d_src, uint8_t* d_dst, unsigned long long* d_sums,
                        cudaStream_t stream);
+  // Peer pull: an identity plan's resident bytes from `d_src` (a peer GPU's
+  // segment mapped here) to d_dst, copied and hashed by one fused kernel.
+  uint64_t pull(const IngestPlan& p, const uint8_t* d_src, uint8_t* d_dst, std::vector<uint64_t>* buckets,
+                IngestStats* st);
 
  private:
   uint8_t* staging(uint64_t bytes);
@@ -94,6 +99,7 @@ struct BackendConfig {
   uint64_t pinned_pool_bytes{0};
   unsigned read_threads{8};
   uint64_t arena_bytes{0};  // HBM arena for the fast tier (0 = one cuMem allocation per model)
+  std::shared_ptr<Directory> directory;  // multi-GPU: publish sealed segments for peers (null = single GPU)
 };
 
 // Fast-tier record of one published model: a range of the arena, or a
@@ -106,6 +112,7 @@ struct FastRecord {
   ~FastRecord() {
     if (arena) arena->free(offset);
   }
+  fmt::ModelKey key;
   fmt::Manifest resident;
   std::string json;
   uint64_t generation{0};
@@ -128,6 +135,7 @@ class CudaTierBackend : public TierBackend {
   void evict_fast(uint64_t model_id) override;
   void evict_host(uint64_t model_id) override;
   void evict_disk(const fmt::ModelKey& key, const std::string& path) override;
+  FastPublication publish_from_peer(uint64_t model_id, const fmt::Manifest& m, const PeerSource& src) override;
 
   std::shared_ptr<FastRecord> fast_record(uint64_t model_id);
   const uint8_t* host_buffer(uint64_t model_id, uint64_t* bytes);
@@ -143,6 +151,9 @@ class CudaTierBackend : public TierBackend {
   void free_host(HostBuf& h);
 
   std::shared_ptr<IngestPlan> plan_for(uint64_t model_id, const fmt::Manifest& m);
+  std::shared_ptr<IngestPlan> pull_plan_for(uint64_t model_id, const fmt::Manifest& resident);
+  void place(FastRecord& rec, uint64_t payload);  // arena range or dedicated segment + generation
+  FastPublication seal(uint64_t model_id, std::shared_ptr<FastRecord> rec, const fmt::Manifest& m);
 
   BackendConfig cfg_;
   Ingestor ing_;
@@ -152,6 +163,7 @@ class CudaTierBackend : public TierBackend {
   std::map<uint64_t, HostBuf> host_;
   std::map<uint64_t, std::shared_ptr<FastRecord>> fast_;
   std::map<uint64_t, std::shared_ptr<IngestPlan>> plans_;  // model_id -> compiled plan (manifests are immutable)
+  std::map<uint64_t, std::shared_ptr<IngestPlan>> pull_plans_;  // model_id -> identity plan of the resident blob
   std::atomic<uint64_t> next_gen_{1};
 };
 

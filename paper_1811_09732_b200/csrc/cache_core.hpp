@@ -79,6 +79,17 @@ struct FetchResult {
   uint64_t file_bytes{0};
 };
 
+// Multi-GPU extension: a sealed fast-tier copy of the model on
+// a peer GPU, mapped into this process and readable from this device. The
+// open becomes a PeerHit: the manifest comes with the source, no disk or host
+// tier is touched, and the backend pulls the resident segment over NVLink.
+struct PeerSource {
+  std::shared_ptr<const fmt::Manifest> manifest;  // artifact manifest of the model
+  int rank{-1}, device{-1};
+  const uint8_t* payload{nullptr};  // peer segment base (resident blob | JSON | jlen | SegTail)
+  uint64_t payload_bytes{0}, resident_blob_bytes{0}, generation{0}, checksum{0};
+};
+
 // The plugin boundary, same eight operations and threading contract as the
 // reference: everything but evict_* is called outside the core lock; evict_*
 // runs under it and must not block long.
@@ -94,6 +105,9 @@ class TierBackend {
   virtual void evict_fast(uint64_t model_id) = 0;
   virtual void evict_host(uint64_t model_id) = 0;
   virtual void evict_disk(const fmt::ModelKey& key, const std::string& path) = 0;
+  // Extension, not part of the reference's eight: fill the fast tier from a
+  // peer's sealed segment. The default refuses.
+  virtual FastPublication publish_from_peer(uint64_t model_id, const fmt::Manifest& m, const PeerSource& src);
 };
 
 struct PlacementResult {
@@ -120,6 +134,7 @@ struct StatsSnapshot {
   TierStats tiers[kTiers];
   std::vector<ModelStats> models;
   uint64_t open_requests{0}, open_errors{0}, disk_reads{0}, remote_fetches{0};
+  uint64_t peer_hits{0};  // multi-GPU extension
   PhaseTimings cumulative;
 };
 
@@ -140,7 +155,10 @@ std::vector<Candidate> evict_candidates(Policy p, std::vector<Candidate> c);
 class CacheCore {
  public:
   CacheCore(CoreConfig cfg, TierBackend& backend);
-  PlacementResult open_model(const fmt::ModelKey& key, const Granularity& g, uint64_t now);
+  // `peer` (multi-GPU extension): a peer copy to serve a fast-tier miss from;
+  // nullptr is exactly the reference's open.
+  PlacementResult open_model(const fmt::ModelKey& key, const Granularity& g, uint64_t now,
+                             const PeerSource* peer = nullptr);
   uint64_t close_model(const fmt::ModelKey& key);
   std::vector<fmt::ModelKey> reclaim(Tier t, uint64_t bytes_needed, Policy p);
   StatsSnapshot stats() const;
@@ -190,7 +208,7 @@ class CacheCore {
   uint64_t next_seq_{1}, next_id_{1};
   uint64_t used_[kTiers]{};
   uint64_t hits_[kTiers]{}, misses_[kTiers]{}, evictions_[kTiers]{};
-  uint64_t opens_{0}, open_errors_{0}, disk_reads_{0}, remote_fetches_{0};
+  uint64_t opens_{0}, open_errors_{0}, disk_reads_{0}, remote_fetches_{0}, peer_hits_{0};
   PhaseTimings cumulative_;
 };
 

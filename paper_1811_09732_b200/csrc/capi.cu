@@ -2,6 +2,8 @@
 // converts exceptions to reference Errc codes; nothing C++ crosses the ABI.
 #include <dirent.h>
 #include <sys/stat.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -15,6 +17,7 @@
 #include "backend.hpp"
 #include "cache_core.hpp"
 #include "cuda_util.hpp"
+#include "directory.hpp"
 #include "format.hpp"
 #include "gemm.hpp"
 #include "nn.hpp"
@@ -112,6 +115,82 @@ struct trims_store {
   std::unique_ptr<CudaTierBackend> be;
   std::unique_ptr<CacheCore> core;
   std::atomic<uint64_t> clock{0};
+  // multi-GPU
+  std::shared_ptr<Directory> dir;
+  PeerCounters peers;
+  std::mutex peer_mu;
+  std::map<std::tuple<int, int, uint64_t>, std::shared_ptr<Import>> peer_arenas;  // (pid, fd, bytes) -> mapping
+  std::map<fmt::ModelKey, std::shared_ptr<const fmt::Manifest>> manifests;
+
+  // The peer path needs the artifact's manifest from this store's own disk
+  // cache (same rule as oracle/simulator.py simulate_cluster); parsed once.
+  std::shared_ptr<const fmt::Manifest> manifest_for(const fmt::ModelKey& key) {
+    Located l = be->locate(key);
+    if (l.kind != Located::Kind::DiskCache) return nullptr;
+    {
+      std::lock_guard lk(peer_mu);
+      auto it = manifests.find(key);
+      if (it != manifests.end()) return it->second;
+    }
+    auto m = std::make_shared<const fmt::Manifest>(be->read_manifest(key, l.path));
+    std::lock_guard lk(peer_mu);
+    return manifests.emplace(key, std::move(m)).first->second;
+  }
+
+  // Map a peer's exportable allocation into this process with read access for
+  // this store's device: the fd is taken from the owner with pidfd_getfd.
+  std::shared_ptr<Import> map_peer(const DirCoords& c) {
+    const auto k = std::make_tuple(c.pid, c.fd, c.alloc_bytes);
+    if (c.arena) {
+      std::lock_guard lk(peer_mu);
+      auto it = peer_arenas.find(k);
+      if (it != peer_arenas.end()) return it->second;
+    }
+    const int pidfd = int(::syscall(SYS_pidfd_open, c.pid, 0));
+    if (pidfd < 0) raise(Errc::NoSuchSegment, "peer rank " + std::to_string(c.rank) + " (pid " + std::to_string(c.pid) + ") is gone");
+    const int fd = int(::syscall(SYS_pidfd_getfd, pidfd, c.fd, 0));
+    const int err = errno;
+    ::close(pidfd);
+    if (fd < 0) raise(Errc::NoSuchSegment, "pidfd_getfd from rank " + std::to_string(c.rank) + ": " + std::strerror(err));
+    std::shared_ptr<Import> imp;
+    try {
+      imp.reset(Import::open(be->config().device, fd, c.alloc_bytes, /*read_only=*/true));
+    } catch (...) {
+      ::close(fd);
+      throw;
+    }
+    ::close(fd);
+    if (c.arena) {
+      std::lock_guard lk(peer_mu);
+      peer_arenas.emplace(k, imp);
+    }
+    return imp;
+  }
+
+  PlacementResult open(const fmt::ModelKey& key, const Granularity& g, uint64_t now, int* peer_rank) {
+    return open_with_peers(
+        *core, dir.get(), key, g, now, [this](const fmt::ModelKey& k) { return manifest_for(k); },
+        [this](const DirCoords& c, std::shared_ptr<void>* hold) {
+          std::shared_ptr<Import> imp = map_peer(c);
+          *hold = imp;
+          PeerSource src;
+          src.rank = c.rank;
+          src.device = c.device;
+          src.payload = imp->ptr() + c.offset;
+          src.payload_bytes = c.payload_bytes;
+          src.resident_blob_bytes = c.resident_blob_bytes;
+          src.generation = c.generation;
+          src.checksum = c.checksum;
+          if (c.offset + c.payload_bytes + sizeof(SegTail) > imp->size())
+            raise(Errc::NoSuchSegment, "peer segment outside its allocation");
+          return src;
+        },
+        &peers, peer_rank);
+  }
+};
+
+struct trims_dir {
+  std::unique_ptr<Directory> d;
 };
 
 struct trims_import {
@@ -393,7 +472,13 @@ int trims_store_create(const trims_store_config* cfg, trims_store** out) {
   return guard([&] {
     if (!out) raise(Errc::InvalidArgument, "null argument");
     auto s = std::make_unique<trims_store>();
-    s->be = std::make_unique<CudaTierBackend>(backend_config(cfg));
+    BackendConfig bc = backend_config(cfg);
+    if (cfg->directory && *cfg->directory) {
+      s->dir = Directory::open(cfg->directory, cfg->world, cfg->rank,
+                               cfg->directory_slots ? cfg->directory_slots : 1024);
+      bc.directory = s->dir;
+    }
+    s->be = std::make_unique<CudaTierBackend>(std::move(bc));
     CoreConfig cc{cfg->fast_capacity_bytes, cfg->host_capacity_bytes, cfg->disk_capacity_bytes,
                   Policy(cfg->policy ? 1 : 0), cfg->eager_reclaim != 0};
     s->core = std::make_unique<CacheCore>(cc, *s->be);
@@ -426,7 +511,7 @@ int trims_store_open(trims_store* s, const char* ns, const char* name, const cha
   return guard([&] {
     if (gran_kind > 2) raise(Errc::InvalidArgument, "granularity kind");
     uint64_t now = s->clock.fetch_add(1) + 1;  // daemon.cpp:457
-    PlacementResult r = s->core->open_model({ns, name, version}, {GranKind(gran_kind), block_bytes}, now);
+    PlacementResult r = s->open({ns, name, version}, {GranKind(gran_kind), block_bytes}, now, nullptr);
     std::memset(out, 0, sizeof *out);
     out->model_id = r.model_id;
     out->outcome = uint32_t(r.outcome);
@@ -503,7 +588,9 @@ int trims_store_stats_json(trims_store* s, char* out, uint64_t cap) {
        << ",\"disk_reads\":" << st.disk_reads << ",\"remote_fetches\":" << st.remote_fetches
        << ",\"fetch_ns\":" << st.cumulative.fetch_ns << ",\"disk_read_ns\":" << st.cumulative.disk_read_ns
        << ",\"copy_ns\":" << st.cumulative.host_to_fast_copy_ns << ",\"export_ns\":" << st.cumulative.handle_export_ns
-       << "}";
+       << ",\"peer_hits\":" << st.peer_hits << ",\"peer_attempts\":" << s->peers.attempts.load()
+       << ",\"peer_fallbacks\":" << s->peers.fallbacks.load() << ",\"rank\":" << (s->dir ? s->dir->rank() : 0)
+       << ",\"world\":" << (s->dir ? s->dir->world() : 1) << "}";
     return put(os.str(), out, cap);
   });
 }
@@ -541,6 +628,74 @@ int trims_store_checksums(trims_store* s, uint64_t model_id, uint64_t* out, uint
     return 0;
   });
 }
+
+int trims_store_fast_resident(trims_store* s, const char* ns, const char* name, const char* version, int* out) {
+  return guard([&] {
+    if (!s || !out) raise(Errc::InvalidArgument, "null argument");
+    *out = s->core->fast_resident({ns, name, version}) ? 1 : 0;
+    return 0;
+  });
+}
+
+// ------------------------------------------------------------- directory
+
+static_assert(sizeof(trims_dir_coords) == sizeof(DirCoords), "trims_dir_coords mirrors DirCoords");
+
+int trims_dir_open(const char* name, int world, int rank, uint32_t slots, trims_dir** out) {
+  return guard([&] {
+    if (!name || !out) raise(Errc::InvalidArgument, "null argument");
+    auto d = std::make_unique<trims_dir>();
+    d->d = Directory::open(name, world, rank, slots ? slots : 1024);
+    *out = d.release();
+    return 0;
+  });
+}
+
+void trims_dir_close(trims_dir* d) {
+  try {
+    delete d;
+  } catch (...) {
+  }
+}
+
+int trims_dir_unlink(const char* name) {
+  return guard([&] {
+    if (!name) raise(Errc::InvalidArgument, "null argument");
+    Directory::unlink(name);
+    return 0;
+  });
+}
+
+int trims_dir_publish(trims_dir* d, const char* ns, const char* name, const char* version, const trims_dir_coords* c) {
+  return guard([&] {
+    if (!d || !c) raise(Errc::InvalidArgument, "null argument");
+    DirCoords dc;
+    std::memcpy(&dc, c, sizeof dc);
+    d->d->publish({ns, name, version}, dc);
+    return 0;
+  });
+}
+
+int trims_dir_retract(trims_dir* d, const char* ns, const char* name, const char* version) {
+  return guard([&] {
+    if (!d) raise(Errc::InvalidArgument, "null argument");
+    d->d->retract({ns, name, version});
+    return 0;
+  });
+}
+
+int trims_dir_holders(trims_dir* d, const char* ns, const char* name, const char* version, trims_dir_coords* out,
+                      uint64_t cap, uint64_t* n) {
+  return guard([&] {
+    if (!d || !n) raise(Errc::InvalidArgument, "null argument");
+    std::vector<DirCoords> hs = d->d->holders({ns, name, version});
+    *n = hs.size();
+    for (uint64_t i = 0; i < std::min<uint64_t>(cap, hs.size()); ++i) std::memcpy(&out[i], &hs[i], sizeof hs[i]);
+    return 0;
+  });
+}
+
+uint64_t trims_peer_score(const char* key, int rank) { return peer_score(key ? key : "", rank); }
 
 // ---------------------------------------------------------------- import
 

@@ -196,6 +196,53 @@ __device__ uint64_t tile_hash(const Tile& t, const uint8_t* dst) {
   return acc;
 }
 
+// OP_HASH tile of a peer pull: copy the resident bytes from `src` (a peer
+// GPU's sealed segment, mapped into this device over NVLink) to `dst` and hash
+// them in the same pass. Four 16-byte loads in flight per thread to cover the
+// NVLink round trip.
+__device__ uint64_t tile_pull(const Tile& t, const uint8_t* src, uint8_t* dst) {
+  const uint8_t* s = src + t.dst_off;
+  uint8_t* d = dst + t.dst_off;
+  const uint64_t gw0 = t.dst_off >> 3;
+  const uint32_t words = t.dst_bytes >> 3;
+  uint64_t acc = 0;
+  if ((t.dst_off & 15) == 0) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(s);
+    uint4* d4 = reinterpret_cast<uint4*>(d);
+    const uint32_t pairs = words >> 1;
+    uint32_t i = threadIdx.x;
+    for (; i + 3 * kThreads < pairs; i += 4 * kThreads) {
+      uint4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] = __ldcs(s4 + i + u * kThreads);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t j = i + u * kThreads;
+        d4[j] = q[u];
+        acc += word_hash((uint64_t(q[u].y) << 32) | q[u].x, gw0 + 2 * j) +
+               word_hash((uint64_t(q[u].w) << 32) | q[u].z, gw0 + 2 * j + 1);
+      }
+    }
+    for (; i < pairs; i += kThreads) {
+      const uint4 q = __ldcs(s4 + i);
+      d4[i] = q;
+      acc += word_hash((uint64_t(q.y) << 32) | q.x, gw0 + 2 * i) + word_hash((uint64_t(q.w) << 32) | q.z, gw0 + 2 * i + 1);
+    }
+    if ((words & 1) && threadIdx.x == 0) {
+      const unsigned long long a = reinterpret_cast<const unsigned long long*>(s)[words - 1];
+      reinterpret_cast<unsigned long long*>(d)[words - 1] = a;
+      acc += word_hash(a, gw0 + words - 1);
+    }
+  } else {
+    for (uint32_t i = threadIdx.x; i < words; i += kThreads) {
+      const unsigned long long a = reinterpret_cast<const unsigned long long*>(s)[i];
+      reinterpret_cast<unsigned long long*>(d)[i] = a;
+      acc += word_hash(a, gw0 + i);
+    }
+  }
+  return acc;
+}
+
 // OP_CVT: elementwise convert S -> D; one resident word per thread step.
 template <int S, int D>
 __device__ uint64_t tile_cvt(const Tile& t, const uint8_t* src, uint8_t* dst) {
@@ -363,6 +410,19 @@ __global__ void __launch_bounds__(kThreads) hash_tiles_kernel(const Tile* __rest
     const Tile t = tiles[i];
     if (t.op != OP_HASH) continue;
     uint64_t acc = block_sum(tile_hash(t, dst), red);
+    if (threadIdx.x == 0) atomicAdd(&sums[t.tensor], (unsigned long long)acc);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) pull_tiles_kernel(const Tile* __restrict__ tiles, uint32_t ntiles,
+                                                              const uint8_t* __restrict__ src,
+                                                              uint8_t* __restrict__ dst,
+                                                              unsigned long long* __restrict__ sums) {
+  __shared__ unsigned long long red[kThreads / 32];
+  for (uint32_t i = blockIdx.x; i < ntiles; i += gridDim.x) {
+    const Tile t = tiles[i];
+    if (t.op != OP_HASH) continue;
+    uint64_t acc = block_sum(tile_pull(t, src, dst), red);
     if (threadIdx.x == 0) atomicAdd(&sums[t.tensor], (unsigned long long)acc);
   }
 }
@@ -789,6 +849,21 @@ uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, co
       TRIMS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPermSmem)));
       fn<<<std::min<uint32_t>(n, sm_count * 4), kThreads, kPermSmem, stream>>>(t, n, src, dst, d_sums);
     }
+    TRIMS_CUDA(cudaGetLastError());
+    ++launches;
+  }
+  return launches;
+}
+
+uint32_t launch_pull(const Tile* d_tiles, const std::vector<Group>& groups, const uint8_t* src, uint8_t* dst,
+                     unsigned long long* d_sums, cudaStream_t stream, int sm_count) {
+  uint32_t launches = 0;
+  for (const Group& g : groups) {
+    const uint32_t n = g.end - g.begin;
+    if (!n) continue;
+    if (g.kind != 0) raise(Errc::InvalidArgument, "peer pull needs an identity (hash-only) plan");
+    pull_tiles_kernel<<<std::min<uint32_t>(n, sm_count * 8), kThreads, 0, stream>>>(d_tiles + g.begin, n, src, dst,
+                                                                                    d_sums);
     TRIMS_CUDA(cudaGetLastError());
     ++launches;
   }

@@ -67,6 +67,11 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
 uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, const uint8_t* src, uint8_t* dst,
                        unsigned long long* d_sums, cudaStream_t stream, int sm_count);
 
+// Peer pull over an identity plan's hash groups: copies src -> dst (src is a
+// peer GPU's resident segment) and hashes the copied bytes in the same pass.
+uint32_t launch_pull(const Tile* d_tiles, const std::vector<Group>& groups, const uint8_t* src, uint8_t* dst,
+                     unsigned long long* d_sums, cudaStream_t stream, int sm_count);
+
 // Checksum of an arbitrary device range (word0 = global index of its first word).
 void launch_checksum(const uint8_t* p, uint64_t nbytes, uint64_t word0, unsigned long long* d_out,
                      cudaStream_t stream, int sm_count);

@@ -10,6 +10,7 @@
 
 #include "../../include/trims.h"
 #include "cache_core.hpp"
+#include "directory.hpp"
 
 using namespace trims;
 
@@ -49,28 +50,47 @@ class FakeBackend : public TierBackend {
     FastPublication p;
     ExportedSegment s;
     s.token = "fake-seg-" + std::to_string(id);
-    s.generation = 1;
+    s.generation = ++gen_;
     s.length = m.blob_bytes;
     p.segments.push_back(s);
+    if (dir) {
+      DirCoords c;
+      c.generation = s.generation;
+      c.payload_bytes = s.length;
+      dir->publish(m.key, c);
+    }
     return p;
   }
-  void evict_fast(uint64_t id) override { record(id, ev_fast); }
+  FastPublication publish_from_peer(uint64_t id, const fmt::Manifest& m, const PeerSource&) override {
+    return publish_fast(id, m, false, "");
+  }
+  void evict_fast(uint64_t id) override {
+    uint32_t i = record(id, ev_fast);
+    if (dir && i != ~0u) dir->retract(key_of(i));
+  }
   void evict_host(uint64_t id) override { record(id, ev_host); }
   void evict_disk(const fmt::ModelKey& k, const std::string&) override {
     uint32_t i = index_of(k);
     present_[i] = false;
     ev_disk.push_back(i);
   }
+  std::shared_ptr<const fmt::Manifest> manifest_if_on_disk(uint32_t i) {
+    if (!present_[i]) return nullptr;
+    return std::make_shared<const fmt::Manifest>(read_manifest(key_of(i), ""));
+  }
   std::vector<uint32_t> ev_fast, ev_host, ev_disk;
+  Directory* dir{nullptr};
 
  private:
-  void record(uint64_t id, std::vector<uint32_t>& v) {
+  uint32_t record(uint64_t id, std::vector<uint32_t>& v) {
     for (uint32_t i = 0; i < id_.size(); ++i)
       if (id_[i] == id) {
         v.push_back(i);
-        return;
+        return i;
       }
+    return ~0u;
   }
+  uint64_t gen_{0};
   std::vector<Model> models_;
   std::vector<bool> present_;
   std::vector<uint64_t> id_;
@@ -83,13 +103,9 @@ std::string list(std::vector<uint32_t>& v) {
   return s.empty() ? "-" : s;
 }
 
-}  // namespace
 
-extern "C" int trims_replay(const char* spec, char* out, uint64_t cap) {
-  try {
-    CoreConfig cfg;
-    std::vector<Model> models;
-    std::vector<std::pair<char, uint32_t>> ops;
+void parse_spec(const char* spec, CoreConfig& cfg, std::vector<Model>& models,
+                std::vector<std::pair<char, uint32_t>>& ops) {
     std::istringstream is(spec);
     std::string tag;
     while (is >> tag) {
@@ -112,6 +128,30 @@ extern "C" int trims_replay(const char* spec, char* out, uint64_t cap) {
         ops.push_back({k[0], i});
       }
     }
+}
+
+int error_outcome(Errc c) {
+  switch (c) {
+    case Errc::NotFound:
+    case Errc::RemoteNotFound: return 100;
+    case Errc::TooLargeForFast: return 101;
+    case Errc::NoEvictableSpace: return 102;
+    case Errc::NotOpen:
+    case Errc::UnknownModel: return 103;
+    default: return 199;
+  }
+}
+
+}  // namespace
+
+// Op kinds: 'o' open, 'c' close, 'p' open with a peer copy available (the
+// multi-GPU extension; oracle/simulator.py Core.step 'p').
+extern "C" int trims_replay(const char* spec, char* out, uint64_t cap) {
+  try {
+    CoreConfig cfg;
+    std::vector<Model> models;
+    std::vector<std::pair<char, uint32_t>> ops;
+    parse_spec(spec, cfg, models, ops);
     FakeBackend be(models);
     CacheCore core(cfg, be);
     for (uint32_t i = 0; i < models.size(); ++i)
@@ -121,18 +161,17 @@ extern "C" int trims_replay(const char* spec, char* out, uint64_t cap) {
       auto key = FakeBackend::key_of(ops[s].second);
       int outcome = 0;
       try {
-        if (ops[s].first == 'o') outcome = int(core.open_model(key, {}, s + 1).outcome);
-        else core.close_model(key);
-      } catch (const Error& e) {
-        switch (e.code()) {
-          case Errc::NotFound:
-          case Errc::RemoteNotFound: outcome = 100; break;
-          case Errc::TooLargeForFast: outcome = 101; break;
-          case Errc::NoEvictableSpace: outcome = 102; break;
-          case Errc::NotOpen:
-          case Errc::UnknownModel: outcome = 103; break;
-          default: outcome = 199; break;
+        if (ops[s].first == 'o') {
+          outcome = int(core.open_model(key, {}, s + 1).outcome);
+        } else if (ops[s].first == 'p') {
+          PeerSource src;
+          src.manifest = std::make_shared<const fmt::Manifest>(be.read_manifest(key, ""));
+          outcome = int(core.open_model(key, {}, s + 1, &src).outcome);
+        } else {
+          core.close_model(key);
         }
+      } catch (const Error& e) {
+        outcome = error_outcome(e.code());
         if (ops[s].first == 'c') outcome = 103;
       }
       os << "live " << s << ' ' << outcome << ' ' << core.used_bytes(Tier::Fast) << ' ' << core.used_bytes(Tier::Host)
@@ -148,6 +187,87 @@ extern "C" int trims_replay(const char* spec, char* out, uint64_t cap) {
     std::string txt = os.str();
     if (txt.size() + 1 > cap) return int(Errc::InvalidArgument);
     std::memcpy(out, txt.data(), txt.size() + 1);
+    return 0;
+  } catch (const Error& e) {
+    return int(e.code());
+  } catch (...) {
+    return int(Errc::Internal);
+  }
+}
+
+struct trims_simcore {
+  CoreConfig cfg;
+  std::vector<Model> models;
+  std::unique_ptr<FakeBackend> be;
+  std::unique_ptr<CacheCore> core;
+  std::unique_ptr<Directory> dir;
+  PeerCounters ctr;
+};
+
+extern "C" int trims_simcore_create(const char* spec, const char* directory, int world, int rank,
+                                    trims_simcore** out) {
+  try {
+    if (!spec || !out) return int(Errc::InvalidArgument);
+    auto c = std::make_unique<trims_simcore>();
+    std::vector<std::pair<char, uint32_t>> ops;
+    parse_spec(spec, c->cfg, c->models, ops);
+    c->be = std::make_unique<FakeBackend>(c->models);
+    if (directory && *directory) {
+      c->dir = Directory::open(directory, world, rank, 1024);
+      c->be->dir = c->dir.get();
+    }
+    c->core = std::make_unique<CacheCore>(c->cfg, *c->be);
+    for (uint32_t i = 0; i < c->models.size(); ++i)
+      if (c->models[i].on_disk)
+        c->core->register_disk_file(FakeBackend::key_of(i), "fake://" + std::to_string(i), c->models[i].file_bytes);
+    *out = c.release();
+    return 0;
+  } catch (const Error& e) {
+    return int(e.code());
+  } catch (...) {
+    return int(Errc::Internal);
+  }
+}
+
+extern "C" void trims_simcore_destroy(trims_simcore* c) {
+  if (!c) return;
+  c->core.reset();  // before the backend and the directory
+  delete c;
+}
+
+extern "C" int trims_simcore_step(trims_simcore* c, char kind, uint32_t model, uint64_t now, char* out,
+                                  uint64_t cap) {
+  try {
+    if (!c || model >= c->models.size()) return int(Errc::InvalidArgument);
+    const auto key = FakeBackend::key_of(model);
+    int outcome = 0, peer = -1;
+    try {
+      if (kind == 'o') {
+        PlacementResult r = open_with_peers(
+            *c->core, c->dir.get(), key, {}, now,
+            [&](const fmt::ModelKey&) { return c->be->manifest_if_on_disk(model); },
+            [&](const DirCoords& d, std::shared_ptr<void>*) {
+              PeerSource s;
+              s.rank = d.rank;
+              s.generation = d.generation;
+              return s;
+            },
+            &c->ctr, &peer);
+        outcome = int(r.outcome);
+      } else {
+        c->core->close_model(key);
+      }
+    } catch (const Error& e) {
+      outcome = kind == 'c' ? 103 : error_outcome(e.code());
+    }
+    c->be->ev_fast.clear();
+    c->be->ev_host.clear();
+    c->be->ev_disk.clear();
+    std::string line = std::to_string(outcome) + ' ' + std::to_string(c->core->used_bytes(Tier::Fast)) + ' ' +
+                       std::to_string(c->core->used_bytes(Tier::Host)) + ' ' +
+                       std::to_string(c->core->refcount(key)) + ' ' + std::to_string(peer);
+    if (line.size() + 1 > cap) return int(Errc::InvalidArgument);
+    std::memcpy(out, line.c_str(), line.size() + 1);
     return 0;
   } catch (const Error& e) {
     return int(e.code());

@@ -38,6 +38,11 @@ class StoreOptions:
     scan_disk: bool = True
     read_threads: int = 8
     arena_bytes: int = 0               # 0 = auto (fast capacity + slack), 1 = one allocation per model
+    # multi-GPU: stores of one node share a residency directory
+    directory: str | None = None       # /dev/shm name; None = single GPU
+    rank: int = 0
+    world: int = 1
+    directory_slots: int = 0           # 0 = 1024 per rank
 
     @property
     def plan_flags(self) -> int:
@@ -63,6 +68,11 @@ class Store:
         cfg.scan_disk = int(opts.scan_disk)
         cfg.read_threads = opts.read_threads
         cfg.arena_bytes = opts.arena_bytes
+        self._dirname = opts.directory.encode() if opts.directory else None
+        cfg.directory = self._dirname
+        cfg.rank = opts.rank
+        cfg.world = opts.world
+        cfg.directory_slots = opts.directory_slots
         h = ctypes.c_void_p()
         check(lib.trims_store_create(ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h
@@ -90,6 +100,11 @@ class Store:
         ex = Export()
         check(lib.trims_store_open(self._h, *key.b(), granularity, block_bytes, ctypes.byref(ex)))
         return ex
+
+    def fast_resident(self, key: F.ModelKey) -> bool:
+        out = ctypes.c_int()
+        check(lib.trims_store_fast_resident(self._h, *key.b(), ctypes.byref(out)))
+        return bool(out.value)
 
     def close(self, key: F.ModelKey) -> int:
         rc = ctypes.c_uint64()

@@ -1,0 +1,25 @@
+#!/bin/bash
+# One GPU-box pass: gpu tests, a bench line, the ncu launch list of the bench
+# command, and one full ncu capture of the transform kernel.
+# usage: bash scripts/gpu_round.sh <tag> [tests|bench|ncu ...]
+tag=${1:-r01}; shift
+what=${@:-tests bench ncu}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/${tag}_smi.txt 2>&1
+for w in $what; do
+  case $w in
+    tests)
+      timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/${tag}_pytest_gpu.log 2>&1
+      echo "pytest exit $?" >> gpurun_out/${tag}_pytest_gpu.log ;;
+    bench)
+      timeout 900 python bench.py > gpurun_out/${tag}_bench.jsonl 2> gpurun_out/${tag}_bench.err ;;
+    ncu)
+      timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
+        --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 3 --warmup 3 --quick --no-cpu-baseline \
+        > gpurun_out/${tag}_ncu_bench.log 2>&1
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:transform -c 2 \
+        -f -o gpurun_out/${tag}_transform python scripts/prof_transform.py resnet50 1 \
+        > gpurun_out/${tag}_ncu_transform.log 2>&1 ;;
+  esac
+done
+ls -la gpurun_out
