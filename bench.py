@@ -182,6 +182,7 @@ def run_ours(args):
     barrier(world)
     max_ms = barrier_max(total_ms, world)
     kernel_ms = total_ms / args.steps
+    info["launches_per_step"] = launches[0] // max(1, args.steps)
     value = world * args.steps * src_bytes / (max_ms / 1e3) / 1e9
 
     # ---- e2e: pinned host buffer through the C ABI (H2D + transform + D2H checksums)
@@ -231,9 +232,12 @@ def run_ours(args):
                 "d2h_bytes_per_step": info["buckets"] * 8, "ms_per_step": round(e2e_max / args.steps, 4),
                 "h2d_gbs_copy_engine": round(h2d_gbs, 2) if h2d_gbs else None},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                     "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                     "frac": round(achieved / hbm_peak, 4), **ncu_traffic(),
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                     "algorithmic_bytes_per_launch": algo, "kernel": "transform_kernel"},
+                     "algorithmic_bytes_per_launch": algo,
+                     "kernel": "transform step = transform_tma_kernel (KCRS->KRSC tiles) || transform_kernel "
+                               "(elementwise tiles), one launch each, concurrent",
+                     "launches_per_step": info["launches_per_step"]},
         "gpu_launches": launches[0] + launches_e2e,
         "clocks": clocks.summary(),
         "latency_ms": lat,
@@ -245,6 +249,18 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def ncu_traffic() -> dict:
+    """DRAM bytes (read + write) of one transform step from the newest committed
+    `ncu --set full` summary (profiles/*_ncu_transform.json, written by
+    scripts/ncu_summary.py); null when none is committed."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_transform.json")), key=os.path.getmtime)
+    if not files:
+        return {"traffic": None}
+    doc = json.load(open(files[-1]))
+    return {"traffic": int(doc["step"]["dram_bytes"]), "traffic_source": os.path.relpath(files[-1], ROOT)}
 
 
 def request_latencies(work: str, arch, dev: int, batch: int = 1, reps: int = 7) -> dict:

@@ -54,6 +54,9 @@ Ingestor::Ingestor(int device) : device_(device) {
   TRIMS_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device));
   TRIMS_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
   TRIMS_CUDA(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking));
+  TRIMS_CUDA(cudaStreamCreateWithFlags(&side_.stream, cudaStreamNonBlocking));
+  TRIMS_CUDA(cudaEventCreateWithFlags(&side_.fork, cudaEventDisableTiming));
+  TRIMS_CUDA(cudaEventCreateWithFlags(&side_.join, cudaEventDisableTiming));
   events_.resize(512);
   for (auto& e : events_) TRIMS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto* e : {&t0_, &t1_, &c0_, &c1_}) TRIMS_CUDA(cudaEventCreate(e));
@@ -72,6 +75,9 @@ Ingestor::~Ingestor() {
     if (b) cudaFreeHost(b);
   cudaStreamDestroy(copy_);
   cudaStreamDestroy(compute_);
+  cudaStreamDestroy(side_.stream);
+  cudaEventDestroy(side_.fork);
+  cudaEventDestroy(side_.join);
 }
 
 uint8_t* Ingestor::staging(uint64_t bytes) {
@@ -153,7 +159,7 @@ uint64_t Ingestor::from_host(const IngestPlan& ip, const uint8_t* host_blob, uin
                                cudaMemcpyHostToDevice, copy_));
     TRIMS_CUDA(cudaEventRecord(ev, copy_));
     TRIMS_CUDA(cudaStreamWaitEvent(compute_, ev, 0));
-    launches += ingest::launch_groups(ip.d_tiles, ch.groups, raw, d_dst, ds, compute_, sms_);
+    launches += ingest::launch_groups(ip.d_tiles, ch.groups, raw, d_dst, ds, compute_, sms_, &side_);
   }
   TRIMS_CUDA(cudaEventRecord(t1_, copy_));
   TRIMS_CUDA(cudaEventRecord(c1_, compute_));
@@ -205,7 +211,7 @@ uint64_t Ingestor::from_file(const IngestPlan& ip, int fd, uint64_t blob_file_of
     TRIMS_CUDA(cudaEventRecord(ev, copy_));
     TRIMS_CUDA(cudaEventRecord(bounce_ev_[slot], copy_));
     TRIMS_CUDA(cudaStreamWaitEvent(compute_, ev, 0));
-    launches += ingest::launch_groups(ip.d_tiles, ch.groups, raw, d_dst, ds, compute_, sms_);
+    launches += ingest::launch_groups(ip.d_tiles, ch.groups, raw, d_dst, ds, compute_, sms_, &side_);
   }
   TRIMS_CUDA(cudaEventRecord(t1_, copy_));
   TRIMS_CUDA(cudaEventRecord(c1_, compute_));
@@ -225,9 +231,9 @@ uint64_t Ingestor::from_file(const IngestPlan& ip, int fd, uint64_t blob_file_of
 
 uint32_t Ingestor::from_device(const IngestPlan& ip, const uint8_t* d_src, uint8_t* d_dst,
                                unsigned long long* d_sums, cudaStream_t stream) {
+  std::lock_guard lk(mu_);  // side_ is shared
   DeviceGuard g(device_);
-  return ingest::launch_groups(ip.d_tiles_k, ip.plan.groups, d_src,
-                                  d_dst, d_sums, stream, sms_);
+  return ingest::launch_groups(ip.d_tiles_k, ip.plan.groups, d_src, d_dst, d_sums, stream, sms_, &side_);
 }
 
 uint64_t Ingestor::pull(const IngestPlan& ip, const uint8_t* d_src, uint8_t* d_dst, std::vector<uint64_t>* buckets,

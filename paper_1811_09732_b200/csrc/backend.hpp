@@ -78,6 +78,7 @@ class Ingestor {
 
   int device_{0}, sms_{148};
   cudaStream_t copy_{}, compute_{};
+  ingest::SideStream side_;  // concurrent direct-path groups (fork/join off compute_ or the caller's stream)
   std::vector<cudaEvent_t> events_;
   cudaEvent_t t0_{}, t1_{}, c0_{}, c1_{};
   uint8_t* staging_{nullptr};

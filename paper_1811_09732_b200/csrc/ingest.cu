@@ -695,6 +695,37 @@ bool supported_pair(fmt::DType s, fmt::DType d) {
 }  // namespace
 
 TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool identity, uint64_t chunk_bytes) {
+  // kernel key: hash | (TMA ring or direct) x dtype pair. TRIMS_CVT_PATH /
+  // TRIMS_PERM_PATH = "direct" | "tma" select the kernel per op (A/B switch).
+  static const bool cvt_direct = [] {  // default: elementwise tiles take the direct-load kernel
+    const char* e = std::getenv("TRIMS_CVT_PATH");
+    return !(e && std::string(e) == "tma");
+  }();
+  static const bool perm_direct = [] {
+    const char* e = std::getenv("TRIMS_PERM_PATH");
+    return e && std::string(e) == "direct";
+  }();
+  // Elementwise tiles on the direct path: enough tiles for ~4 waves of the
+  // direct grid (148 SMs x 4 CTAs) so the last wave is not half empty, but
+  // 16..64 KiB of source each so the per-tile reduction stays noise (A/B in
+  // profiles/r01_transform_ab.log). TRIMS_CVT_TILE_KB (source KiB) overrides.
+  static const uint64_t cvt_tile_env = [] {
+    const char* e = std::getenv("TRIMS_CVT_TILE_KB");
+    return e ? uint64_t(std::max(1, std::atoi(e))) << 10 : 0;
+  }();
+  uint64_t cvt_src_bytes = 0;
+  for (size_t i = 0; i < src.tensors.size() && i < dst.tensors.size(); ++i) {
+    const auto& s = src.tensors[i];
+    const auto& d = dst.tensors[i];
+    const bool perm = d.layout == fmt::Layout::KRSC && s.layout == fmt::Layout::Native && s.dims.size() == 4 &&
+                      s.dims[2] * s.dims[3] > 1;
+    if (!perm) cvt_src_bytes += s.nbytes;
+  }
+  uint64_t cvt_tile = cvt_tile_env;
+  if (!cvt_tile) {
+    cvt_tile = 16u << 10;
+    while (cvt_tile < (64u << 10) && cvt_src_bytes / cvt_tile > 148ull * 4 * 4) cvt_tile *= 2;
+  }
   TilePlan p;
   p.identity = identity;
   p.src_bytes = src.blob_bytes;
@@ -759,7 +790,7 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
           tiles.push_back(t);
         }
       } else {
-        const uint64_t per = ring_cfg().stage_bytes / ss;  // one ring stage of source per tile
+        const uint64_t per = (cvt_direct ? cvt_tile : ring_cfg().stage_bytes) / ss;
         for (uint64_t e0 = 0; e0 < n; e0 += per) {
           const uint64_t cnt = std::min<uint64_t>(per, n - e0);
           Tile t{};
@@ -782,16 +813,6 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
     if (t.op == OP_HASH) return t.src_off + t.dst_bytes;
     return t.src_off + uint64_t(t.n_elem) * fmt::element_size(fmt::DType(t.sdt));
   };
-  // kernel key: hash | (TMA ring or direct) x dtype pair. TRIMS_CVT_PATH /
-  // TRIMS_PERM_PATH = "direct" | "tma" select the kernel per op (A/B switch).
-  static const bool cvt_direct = [] {  // default: elementwise tiles take the direct-load kernel
-    const char* e = std::getenv("TRIMS_CVT_PATH");
-    return !(e && std::string(e) == "tma");
-  }();
-  static const bool perm_direct = [] {
-    const char* e = std::getenv("TRIMS_PERM_PATH");
-    return e && std::string(e) == "direct";
-  }();
   auto kind_of = [](const Tile& t) -> uint8_t {
     if (t.op == OP_HASH) return 0;
     if (t.pad_) return 2;
@@ -803,7 +824,9 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
     for (uint32_t i = b; i < e;) {
       uint32_t j = i + 1;
       while (j < e && key_of(v[j]) == key_of(v[i])) ++j;
-      out.push_back({i, j, kind_of(v[i]), v[i].sdt, v[i].ddt});
+      uint8_t smem = 0;
+      for (uint32_t k = i; k < j; ++k) smem |= v[k].op == OP_PERM && !v[k].pad_;
+      out.push_back({i, j, kind_of(v[i]), v[i].sdt, v[i].ddt, smem});
       i = j;
     }
   };
@@ -827,30 +850,50 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
 }
 
 uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, const uint8_t* src, uint8_t* dst,
-                       unsigned long long* d_sums, cudaStream_t stream, int sm_count) {
+                       unsigned long long* d_sums, cudaStream_t stream, int sm_count, const SideStream* side) {
+  // With a side stream, the direct-path groups run concurrently with the TMA
+  // ring groups: the ring kernel holds one CTA and ~200 KB of shared memory
+  // per SM, the smem-free direct CTAs fill the remaining warps and registers.
+  bool has_tma = false, has_direct = false;
+  for (const Group& g : groups) {
+    has_tma |= g.kind == 1 && g.end > g.begin;
+    has_direct |= g.kind == 2 && g.end > g.begin;
+  }
+  static const bool serial = std::getenv("TRIMS_TRANSFORM_SERIAL") != nullptr;  // A/B switch
+  const bool fork = !serial && side && side->stream && has_tma && has_direct;
+  if (fork) {
+    TRIMS_CUDA(cudaEventRecord(side->fork, stream));
+    TRIMS_CUDA(cudaStreamWaitEvent(side->stream, side->fork, 0));
+  }
   uint32_t launches = 0;
   for (const Group& g : groups) {
     const uint32_t n = g.end - g.begin;
     if (!n) continue;
     const Tile* t = d_tiles + g.begin;
+    cudaStream_t st = fork && g.kind == 2 ? side->stream : stream;
     if (g.kind == 0) {
-      hash_tiles_kernel<<<std::min<uint32_t>(n, sm_count * 8), kThreads, 0, stream>>>(t, n, dst, d_sums);
+      hash_tiles_kernel<<<std::min<uint32_t>(n, sm_count * 8), kThreads, 0, st>>>(t, n, dst, d_sums);
     } else if (g.kind == 1) {
       TmaFn fn = pair_tma_kernel(g.sdt, g.ddt);
       if (!fn) raise(Errc::InvalidArgument, "unsupported dtype pair in plan");
       const RingCfg& rc = ring_cfg();
       const int smem = int(rc.stages * rc.stage_alloc());
       TRIMS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      fn<<<std::min<uint32_t>(n, sm_count * rc.ctas_per_sm), kTmaThreads, smem, stream>>>(t, n, src, dst, d_sums,
-                                                                                          rc.stages, rc.stage_alloc());
+      fn<<<std::min<uint32_t>(n, sm_count * rc.ctas_per_sm), kTmaThreads, smem, st>>>(t, n, src, dst, d_sums,
+                                                                                      rc.stages, rc.stage_alloc());
     } else {
       TransformFn fn = pair_kernel(g.sdt, g.ddt);
       if (!fn) raise(Errc::InvalidArgument, "unsupported dtype pair in plan");
+      const uint32_t smem = g.smem ? uint32_t(kPermSmem) : 0;
       TRIMS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPermSmem)));
-      fn<<<std::min<uint32_t>(n, sm_count * 4), kThreads, kPermSmem, stream>>>(t, n, src, dst, d_sums);
+      fn<<<std::min<uint32_t>(n, sm_count * 4), kThreads, smem, st>>>(t, n, src, dst, d_sums);
     }
     TRIMS_CUDA(cudaGetLastError());
     ++launches;
+  }
+  if (fork) {
+    TRIMS_CUDA(cudaEventRecord(side->join, side->stream));
+    TRIMS_CUDA(cudaStreamWaitEvent(stream, side->join, 0));
   }
   return launches;
 }

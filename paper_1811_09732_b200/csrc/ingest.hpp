@@ -33,6 +33,7 @@ static_assert(sizeof(Tile) == 40, "tile layout");
 struct Group {
   uint32_t begin, end;
   uint8_t kind, sdt, ddt;
+  uint8_t smem;  // a direct-path group holding smem-staged OP_PERM tiles
 };
 
 struct TilePlan {
@@ -64,8 +65,14 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
 // Launches one persistent kernel per group over `d_tiles` (device copy of the
 // table the groups index). Per-bucket checksums accumulate atomically into
 // d_sums (mod 2^64). Returns the number of kernel launches.
+// Optional second stream for concurrent groups (fork/join through the events).
+struct SideStream {
+  cudaStream_t stream{nullptr};
+  cudaEvent_t fork{nullptr}, join{nullptr};
+};
 uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, const uint8_t* src, uint8_t* dst,
-                       unsigned long long* d_sums, cudaStream_t stream, int sm_count);
+                       unsigned long long* d_sums, cudaStream_t stream, int sm_count,
+                       const SideStream* side = nullptr);
 
 // Peer pull over an identity plan's hash groups: copies src -> dst (src is a
 // peer GPU's resident segment) and hashes the copied bytes in the same pass.

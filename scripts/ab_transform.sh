@@ -1,0 +1,8 @@
+#!/bin/bash
+# A/B of transform variants (env switches) on resnet50 / vgg16.
+for arch in resnet50 vgg16; do
+  for v in "A=1" "TRIMS_TRANSFORM_SERIAL=1" "TRIMS_CVT_TILE_KB=64" "TRIMS_CVT_TILE_KB=8" "TRIMS_CVT_TILE_KB=32" "TRIMS_TRANSFORM_SERIAL=1 TRIMS_CVT_TILE_KB=64"; do
+    echo -n "$arch [$v] "
+    env $v python scripts/prof_transform.py $arch 3 3
+  done
+done
