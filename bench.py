@@ -35,6 +35,9 @@ import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# TRIMS_BENCH_SHARED_GPU=1: run N ranks on cuda:0 over gloo (tests the N>1 code
+# path on a one-GPU box; its numbers are not scaling numbers).
+SHARED_GPU = os.environ.get("TRIMS_BENCH_SHARED_GPU") == "1"
 sys.path.insert(0, ROOT)
 
 METRIC = "end-to-end inference latency cold/warm/hot (ms) + weight-ingest GB/s at 1/2/4/8 B200"
@@ -101,8 +104,12 @@ def dist_setup(n_gpus: int):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if SHARED_GPU:  # code-path test of N>1 on one GPU: every rank on cuda:0, gloo plumbing
+            local = 0
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     return world, rank, local
 
 
@@ -111,7 +118,7 @@ def barrier_max(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if SHARED_GPU else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -218,6 +225,8 @@ def run_ours(args):
         C.write_arch(vgg, work, seed=1)
         lat["vgg16"] = request_latencies(work, vgg, dev)
 
+    peer = peer_serve(work, arch, dev, rank, world, args.steps) if world > 1 else None
+
     hbm_peak, peak_kind = peaks()
     algo = info["read_bytes"] + info["write_bytes"]
     achieved = algo / (kernel_ms / 1e3) / 1e9
@@ -242,6 +251,8 @@ def run_ours(args):
         "clocks": clocks.summary(),
         "latency_ms": lat,
     }
+    if peer:
+        line["peer_serve"] = peer
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(src_json, blob, res_json)
     if rank == 0:
@@ -249,6 +260,56 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def peer_serve(work: str, arch, dev: int, rank: int, world: int, steps: int) -> dict:
+    """N>1: NVLink peer serve through the public store API.
+    Every rank holds its own model p<rank> (disk load, sealed, published in the
+    node directory); each step every rank opens its neighbour's p<rank+1> —
+    a PeerHit: one fused pull+checksum kernel reads the neighbour's sealed
+    segment over NVLink — then evicts that replica again. All ranks pull at
+    once, so this is the ring-neighbour NVLink load. Reports the pull kernel
+    throughput (resident bytes / kernel time) and the open latency."""
+    import dataclasses
+    import statistics
+
+    from paper_1811_09732_b200 import catalog as C
+    from paper_1811_09732_b200.store import Store, StoreOptions
+
+    d = os.path.join(work, "peer")
+    own = dataclasses.replace(arch, name=f"{arch.name}-p{rank}")
+    nb = dataclasses.replace(arch, name=f"{arch.name}-p{(rank + 1) % world}")
+    C.write_arch(own, d, seed=1)
+    C.write_arch(nb, d, seed=1)
+    name = f"trims.bench.{os.environ.get('MASTER_PORT', '0')}"
+    cap = 4 << 30
+    opts = StoreOptions(disk_cache_dir=d, fast_capacity_bytes=cap, host_capacity_bytes=1 << 30,
+                        convert_to="bf16", permute_4d=True, directory=name, rank=rank, world=world, device=dev,
+                        scan_disk=False)
+    gbs, open_ms, outcomes = [], [], []
+    with Store(opts) as s:
+        mine = s.open(C.arch_key(own))
+        barrier(world)
+        for i in range(steps + 1):
+            t0 = time.perf_counter()
+            ex = s.open(C.arch_key(nb))
+            dt = (time.perf_counter() - t0) * 1e3
+            st = s.ingest_stats(ex.model_id)
+            outcomes.append(int(ex.outcome))
+            if i:  # the first pull maps the neighbour's arena
+                open_ms.append(dt)
+                gbs.append(ex.resident_blob_bytes / (st["total_ms"] / 1e3) / 1e9)
+            s.close(C.arch_key(nb))
+            s.reclaim(0, cap - mine.weights_bytes)  # evict the replica (own copy is open)
+            barrier(world)
+        stats = s.stats()
+        barrier(world)
+    med = statistics.median(gbs) if gbs else 0.0
+    return {"pull_GBps_median": round(med, 1), "pull_GBps_min_over_ranks": round(-barrier_max(-med, world), 1),
+            "open_ms_median": round(statistics.median(open_ms), 3) if open_ms else None,
+            "resident_bytes": int(ex.resident_blob_bytes), "outcomes": sorted(set(outcomes)),
+            "peer_hits": stats["peer_hits"], "peer_fallbacks": stats["peer_fallbacks"],
+            "note": "outcome 4 = PeerHit" + ("; shared-GPU mode pulls within one HBM" if SHARED_GPU else "")}
 
 
 def ncu_traffic() -> dict:

@@ -13,6 +13,10 @@ for w in $what; do
       echo "pytest exit $?" >> gpurun_out/${tag}_pytest_gpu.log ;;
     bench)
       timeout 900 python bench.py > gpurun_out/${tag}_bench.jsonl 2> gpurun_out/${tag}_bench.err ;;
+    multi)
+      TRIMS_BENCH_SHARED_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+        --master-addr 127.0.0.1 --master-port 29611 bench.py --gpus 2 --steps 5 --warmup 3 --quick \
+        > gpurun_out/${tag}_bench_shared2.jsonl 2> gpurun_out/${tag}_bench_shared2.err ;;
     ncu)
       timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
         --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 3 --warmup 3 --quick --no-cpu-baseline \
