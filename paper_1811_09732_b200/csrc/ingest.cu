@@ -136,6 +136,20 @@ __device__ __forceinline__ typename Bits<D>::T cvt(typename Bits<S>::T x) {
   else return 0;  // unreachable: build_tiles rejects other pairs
 }
 
+// One resident word from EPW source elements (the pair-convert instruction
+// for fp32 -> bf16).
+template <int S, int D, int N>
+__device__ __forceinline__ uint64_t pack_word(const typename Bits<S>::T (&v)[N]) {
+  if constexpr (S == 1 && D == 4 && N == 4) {
+    return uint64_t(f32x2_to_bf16x2(v[0], v[1])) | (uint64_t(f32x2_to_bf16x2(v[2], v[3])) << 32);
+  } else {
+    uint64_t word = 0;
+#pragma unroll
+    for (int q = 0; q < N; ++q) word |= uint64_t(cvt<S, D>(v[q])) << (8 * esize<D>() * q);
+    return word;
+  }
+}
+
 // Load N elements of type T starting at p (p aligned to N*sizeof(T)) with
 // the widest vector loads available (16 B), read-only path.
 template <typename T, int N>
@@ -158,6 +172,29 @@ __device__ __forceinline__ void load_vec(const uint8_t* p, T (&v)[N]) {
     for (int i = 0; i < N; ++i) v[i] = reinterpret_cast<const T*>(p)[i];
   }
 }
+
+// Per-warp checksum accumulator that flushes (warp reduce + one atomic) only
+// when the bucket changes: a CTA's consecutive tiles mostly belong to the same
+// large tensor, so the atomics on a hot bucket stay few.
+struct WarpSum {
+  uint32_t bucket{~0u};
+  uint64_t acc{0};
+  __device__ __forceinline__ void flush(unsigned long long* sums) {
+    if (bucket == ~0u) return;
+    uint64_t v = acc;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&sums[bucket], (unsigned long long)v);
+    acc = 0;
+  }
+  __device__ __forceinline__ void add(uint32_t b, uint64_t v, unsigned long long* sums) {
+    if (b != bucket) {  // warp-uniform
+      flush(sums);
+      bucket = b;
+    }
+    acc += v;
+  }
+};
 
 __device__ __forceinline__ uint64_t block_sum(uint64_t v, unsigned long long* red) {
 #pragma unroll
@@ -243,9 +280,12 @@ __device__ uint64_t tile_pull(const Tile& t, const uint8_t* src, uint8_t* dst) {
   return acc;
 }
 
-// OP_CVT: elementwise convert S -> D; one resident word per thread step.
+// OP_CVT: elementwise convert S -> D; one resident word per thread step,
+// kCvtUnroll independent 128-bit loads in flight per thread.
+constexpr int kCvtUnroll = 8;
 template <int S, int D>
 __device__ uint64_t tile_cvt(const Tile& t, const uint8_t* src, uint8_t* dst) {
+  constexpr int kUnroll = kCvtUnroll;
   using ST = typename Bits<S>::T;
   using DT = typename Bits<D>::T;
   constexpr int DS = esize<D>(), SS = esize<S>(), EPW = 8 / DS;
@@ -269,8 +309,7 @@ __device__ uint64_t tile_cvt(const Tile& t, const uint8_t* src, uint8_t* dst) {
       const uint32_t e0 = w * EPW;
       uint64_t word = 0;
       if (e0 + EPW <= n) {
-#pragma unroll
-        for (int q = 0; q < EPW; ++q) word |= uint64_t(cvt<S, D>(v[u][q])) << (8 * DS * q);
+        word = pack_word<S, D>(v[u]);
       } else if (e0 < n) {
         for (int q = 0; q < EPW && e0 + q < n; ++q) {
           ST x;
@@ -387,19 +426,26 @@ __device__ uint64_t tile_perm(const Tile& t, const uint8_t* src, uint8_t* dst, u
 // pressure at what that pair needs; tiles of other pairs in the same range are
 // skipped (the host launches one kernel per pair present, usually exactly one).
 template <int S, int D>
-__global__ void __launch_bounds__(kThreads) transform_kernel(const Tile* __restrict__ tiles, uint32_t ntiles,
+__global__ void __launch_bounds__(kThreads, 3) transform_kernel(const Tile* __restrict__ tiles, uint32_t ntiles,
                                                              const uint8_t* __restrict__ src,
                                                              uint8_t* __restrict__ dst,
                                                              unsigned long long* __restrict__ sums) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ unsigned long long red[kThreads / 32];
+  Tile next = blockIdx.x < ntiles ? tiles[blockIdx.x] : Tile{};
+  WarpSum ws;
   for (uint32_t i = blockIdx.x; i < ntiles; i += gridDim.x) {
-    const Tile t = tiles[i];
+    const Tile t = next;
+    if (i + gridDim.x < ntiles) next = tiles[i + gridDim.x];  // descriptor prefetch
     if (t.op == OP_HASH || t.sdt != S || t.ddt != D) continue;  // block-uniform
-    uint64_t acc = t.op == OP_PERM ? tile_perm<S, D>(t, src, dst, smem) : tile_cvt<S, D>(t, src, dst);
-    acc = block_sum(acc, red);
-    if (threadIdx.x == 0) atomicAdd(&sums[t.tensor], (unsigned long long)acc);
+    if (t.op == OP_PERM) {
+      const uint64_t acc = block_sum(tile_perm<S, D>(t, src, dst, smem), red);
+      if (threadIdx.x == 0) atomicAdd(&sums[t.tensor], (unsigned long long)acc);
+    } else {  // no CTA barrier: warps run ahead into the next tile
+      ws.add(t.tensor, tile_cvt<S, D>(t, src, dst), sums);
+    }
   }
+  ws.flush(sums);
 }
 
 __global__ void __launch_bounds__(kThreads) hash_tiles_kernel(const Tile* __restrict__ tiles, uint32_t ntiles,
@@ -459,17 +505,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32
 }
 
 // One resident word from EPW source elements (element 0 in the low bits).
-template <int S, int D, int N>
-__device__ __forceinline__ uint64_t pack_word(const typename Bits<S>::T (&v)[N]) {
-  if constexpr (S == 1 && D == 4 && N == 4) {
-    return uint64_t(f32x2_to_bf16x2(v[0], v[1])) | (uint64_t(f32x2_to_bf16x2(v[2], v[3])) << 32);
-  } else {
-    uint64_t word = 0;
-#pragma unroll
-    for (int q = 0; q < N; ++q) word |= uint64_t(cvt<S, D>(v[q])) << (8 * esize<D>() * q);
-    return word;
-  }
-}
 
 // Warp-specialised: warp 0 is the producer (one elected lane issues the bulk
 // copies and recycles ring stages through `empty` mbarriers); kConsumerWarps
@@ -520,6 +555,7 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
 
   // ---------------- consumers
   const uint32_t ct = threadIdx.x - 32, cw = warp - 1;
+  WarpSum ws;
   for (uint32_t j = 0; j < mine; ++j) {
     const uint32_t s = j % stages;
     mbar_wait(&full[s], (j / stages) & 1);
@@ -596,14 +632,12 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
         acc += word_hash(word, gw0 + w);
       }
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    ws.add(t.tensor, acc, sums);
     __syncwarp();  // every lane's shared-memory reads of stage s are done
-    if (lane == 0) {
-      if (acc) atomicAdd(&sums[t.tensor], (unsigned long long)acc);
+    if (lane == 0)
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
-    }
   }
+  ws.flush(sums);
 }
 
 using TransformFn = void (*)(const Tile*, uint32_t, const uint8_t*, uint8_t*, unsigned long long*);
@@ -886,7 +920,9 @@ uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, co
       if (!fn) raise(Errc::InvalidArgument, "unsupported dtype pair in plan");
       const uint32_t smem = g.smem ? uint32_t(kPermSmem) : 0;
       TRIMS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPermSmem)));
-      fn<<<std::min<uint32_t>(n, sm_count * 4), kThreads, smem, st>>>(t, n, src, dst, d_sums);
+      int per_sm = 0;  // persistent grid = exactly the resident CTAs
+      TRIMS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
+      fn<<<std::min<uint32_t>(n, sm_count * std::max(1, per_sm)), kThreads, smem, st>>>(t, n, src, dst, d_sums);
     }
     TRIMS_CUDA(cudaGetLastError());
     ++launches;
