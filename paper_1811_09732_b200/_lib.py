@@ -11,7 +11,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtrims.so")
+# TRIMS_LIB: an A/B variant build of the same library (scripts/ab_transform.sh)
+LIB_PATH = os.environ.get("TRIMS_LIB") or os.path.join(HERE, "libtrims.so")
 
 
 class TrimsError(RuntimeError):

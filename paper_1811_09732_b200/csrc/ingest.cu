@@ -46,7 +46,10 @@ const RingCfg& ring_cfg() {
   }();
   return c;
 }
-constexpr int kConsumerWarps = 16;                  // TMA kernel: 1 producer warp + 16 consumer warps
+#ifndef TRIMS_CONSUMER_WARPS
+#define TRIMS_CONSUMER_WARPS 16
+#endif
+constexpr int kConsumerWarps = TRIMS_CONSUMER_WARPS;  // TMA kernel: 1 producer warp + consumer warps
 constexpr int kTmaThreads = 32 * (kConsumerWarps + 1);
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -148,6 +151,13 @@ __device__ __forceinline__ uint64_t pack_word(const typename Bits<S>::T (&v)[N])
     for (int q = 0; q < N; ++q) word |= uint64_t(cvt<S, D>(v[q])) << (8 * esize<D>() * q);
     return word;
   }
+}
+
+// One element S -> D; fp32 -> bf16 through the (probed) hardware convert.
+template <int S, int D>
+__device__ __forceinline__ typename Bits<D>::T cvt1(typename Bits<S>::T x) {
+  if constexpr (S == 1 && D == 4) return uint16_t(f32x2_to_bf16x2(x, 0u));
+  else return cvt<S, D>(x);
 }
 
 // Load N elements of type T starting at p (p aligned to N*sizeof(T)) with
@@ -592,24 +602,30 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
     } else {  // OP_PERM: source [g][C][RS] in smem -> resident [g][RS][C]
       const uint32_t C = t.C, RS = t.RS, CRS = C * RS;
       uint32_t body = 0;  // words written by the fast paths below
-      if ((C * DS) % 8 == 0) {
-        const uint32_t wpr = C / EPW, rows = (n / CRS) * RS;
-        body = rows * wpr;
-        for (uint32_t row = cw; row < rows; row += kConsumerWarps) {
-          const uint32_t k = row / RS, r = row - k * RS;
-          const ST* col = el + k * CRS + r;
-          uint64_t* drow = d + uint64_t(row) * wpr;
-          const uint64_t gwr = gw0 + uint64_t(row) * wpr;
+      if ((C * DS) % 8 == 0 && RS > 1) {
+        // Flattened (row, word) items, 32 consecutive words per warp step:
+        // full lanes even when a row is shorter than a warp (C = 64). Each lane
+        // gathers its EPW elements (source stride RS) in an order rotated by
+        // lane/8, which makes the four shared loads of a step hit 32 distinct
+        // banks for odd RS (3x3, 5x5, 7x7) instead of 8.
+        const uint32_t wpr = C / EPW, rows = (n / CRS) * RS, items = rows * wpr;
+        body = items;
+        const bool pow2 = (wpr & (wpr - 1)) == 0;
+        const uint32_t sh = __ffs(wpr) - 1, rs_magic = 0xffffffffu / RS + 1;  // k = ceil(2^32/RS)*row >> 32
+        const uint32_t rot = (lane >> 3) & (EPW - 1);
 #pragma unroll 2
-          for (uint32_t wi = lane; wi < wpr; wi += 32) {
-            const ST* e = col + wi * EPW * RS;
-            ST v[EPW];
+        for (uint32_t it = cw * 32 + lane; it < items; it += kC) {
+          const uint32_t row = pow2 ? it >> sh : it / wpr, wi = it - row * wpr;
+          const uint32_t k = __umulhi(row, rs_magic), r = row - k * RS;
+          const ST* e = el + k * CRS + r + wi * EPW * RS;
+          uint64_t word = 0;
 #pragma unroll
-            for (int q = 0; q < EPW; ++q) v[q] = e[q * RS];
-            const uint64_t word = pack_word<S, D>(v);
-            drow[wi] = word;
-            acc += word_hash(word, gwr + wi);
+          for (int q = 0; q < EPW; ++q) {
+            const uint32_t qq = (q + rot) & (EPW - 1);
+            word |= uint64_t(cvt1<S, D>(e[qq * RS])) << (8 * DS * qq);
           }
+          d[it] = word;
+          acc += word_hash(word, gw0 + it);
         }
       }
       for (uint32_t w = body + ct; w < words; w += kC) {  // generic path, partial word, pad
@@ -731,9 +747,9 @@ bool supported_pair(fmt::DType s, fmt::DType d) {
 TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool identity, uint64_t chunk_bytes) {
   // kernel key: hash | (TMA ring or direct) x dtype pair. TRIMS_CVT_PATH /
   // TRIMS_PERM_PATH = "direct" | "tma" select the kernel per op (A/B switch).
-  static const bool cvt_direct = [] {  // default: elementwise tiles take the direct-load kernel
+  static const bool cvt_direct = [] {  // default: elementwise tiles ride the TMA ring too (one launch)
     const char* e = std::getenv("TRIMS_CVT_PATH");
-    return !(e && std::string(e) == "tma");
+    return e && std::string(e) == "direct";
   }();
   static const bool perm_direct = [] {
     const char* e = std::getenv("TRIMS_PERM_PATH");
@@ -805,7 +821,8 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
         // a slice group whose raw bytes exceed a ring stage is gathered straight from HBM
         const uint64_t stage = ring_cfg().stage_bytes;
         const bool gather = g * CRS * ss > stage;
-        while (!gather && 2 * g * CRS * ss <= stage && g * 2 <= K) g *= 2;
+        // as many whole aligned slice groups as fill one ring stage
+        if (!gather) g = std::max<uint64_t>(g, std::min<uint64_t>(K, stage / (g * CRS * ss) * g));
         p.has_perm = true;
         for (uint64_t k0 = 0; k0 < K; k0 += g) {
           const uint64_t kn = std::min(g, K - k0);
