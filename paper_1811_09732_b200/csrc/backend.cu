@@ -57,6 +57,8 @@ Ingestor::Ingestor(int device) : device_(device) {
   TRIMS_CUDA(cudaStreamCreateWithFlags(&side_.stream, cudaStreamNonBlocking));
   TRIMS_CUDA(cudaEventCreateWithFlags(&side_.fork, cudaEventDisableTiming));
   TRIMS_CUDA(cudaEventCreateWithFlags(&side_.join, cudaEventDisableTiming));
+  TRIMS_CUDA(cudaMalloc(&side_.sched, 2 * ingest::kSchedSlots * sizeof(unsigned int)));
+  TRIMS_CUDA(cudaMemset(side_.sched, 0, 2 * ingest::kSchedSlots * sizeof(unsigned int)));
   events_.resize(512);
   for (auto& e : events_) TRIMS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto* e : {&t0_, &t1_, &c0_, &c1_}) TRIMS_CUDA(cudaEventCreate(e));
@@ -78,6 +80,7 @@ Ingestor::~Ingestor() {
   cudaStreamDestroy(side_.stream);
   cudaEventDestroy(side_.fork);
   cudaEventDestroy(side_.join);
+  cudaFree(side_.sched);
 }
 
 uint8_t* Ingestor::staging(uint64_t bytes) {

@@ -514,62 +514,24 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32
                : "memory");
 }
 
-// One resident word from EPW source elements (element 0 in the low bits).
-
-// Warp-specialised: warp 0 is the producer (one elected lane issues the bulk
-// copies and recycles ring stages through `empty` mbarriers); kConsumerWarps
-// warps convert / permute / hash straight out of shared memory. No CTA-wide
-// barrier on the steady path: every consumer warp reduces its checksum with
-// shuffles and adds it with one atomic per tile.
+// Consumer warps of transform_tma_kernel: wait for a staged tile, convert /
+// permute it out of shared memory, store + hash the resident words, hand the
+// stage back.
 template <int S, int D>
-__global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* __restrict__ tiles, uint32_t ntiles,
-                                                                    const uint8_t* __restrict__ src,
-                                                                    uint8_t* __restrict__ dst,
-                                                                    unsigned long long* __restrict__ sums,
-                                                                    uint32_t stages, uint32_t stage_alloc) {
+__device__ __forceinline__ void consume_tiles(const uint8_t* ring, uint64_t* full, uint64_t* empty, const Tile* staged,
+                                              uint8_t* __restrict__ dst, unsigned long long* __restrict__ sums,
+                                              uint32_t stages, uint32_t stage_alloc) {
   using ST = typename Bits<S>::T;
   constexpr int DS = esize<D>(), SS = esize<S>(), EPW = 8 / DS;
   constexpr uint32_t kC = kConsumerWarps * 32;  // consumer threads
-  extern __shared__ __align__(128) uint8_t ring[];
-  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
-  __shared__ Tile staged[kMaxStages];
-
-  const uint32_t first = blockIdx.x, stride = gridDim.x;
-  const uint32_t mine = first < ntiles ? (ntiles - first + stride - 1) / stride : 0;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (uint32_t s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == 0) {  // ---------------- producer
-    if (lane == 0) {
-      Tile next = mine ? tiles[first] : Tile{};
-      for (uint32_t j = 0; j < mine; ++j) {
-        const uint32_t s = j % stages;
-        const Tile t = next;
-        if (j + 1 < mine) next = tiles[first + (j + 1) * stride];  // descriptor prefetch overlaps the wait
-        if (j >= stages) mbar_wait(&empty[s], ((j / stages) - 1) & 1);
-        staged[s] = t;
-        const uint64_t b = t.src_off & ~15ull, e = (t.src_off + uint64_t(t.n_elem) * SS + 15) & ~15ull;
-        mbar_expect_tx(&full[s], uint32_t(e - b));
-        bulk_g2s(ring + s * stage_alloc, src + b, uint32_t(e - b), &full[s]);
-      }
-    }
-    return;
-  }
-
-  // ---------------- consumers
   const uint32_t ct = threadIdx.x - 32, cw = warp - 1;
   WarpSum ws;
-  for (uint32_t j = 0; j < mine; ++j) {
+  for (uint32_t j = 0;; ++j) {
     const uint32_t s = j % stages;
     mbar_wait(&full[s], (j / stages) & 1);
     const Tile t = staged[s];
+    if (t.op == OP_END) break;
     const ST* el = reinterpret_cast<const ST*>(ring + s * stage_alloc + (t.src_off & 15));
     uint64_t* d = reinterpret_cast<uint64_t*>(dst + t.dst_off);
     const uint64_t gw0 = t.dst_off >> 3;
@@ -656,8 +618,87 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
   ws.flush(sums);
 }
 
+// Warp-specialised: warp 0 is the producer (one elected lane issues the bulk
+// copies and recycles ring stages through `empty` mbarriers); kConsumerWarps
+// warps convert / permute / hash straight out of shared memory. No CTA-wide
+// barrier on the steady path: every consumer warp reduces its checksum with
+// shuffles and adds it with one atomic per tile.
+template <int S, int D>
+__global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* __restrict__ tiles, uint32_t ntiles,
+                                                                    const uint8_t* __restrict__ src,
+                                                                    uint8_t* __restrict__ dst,
+                                                                    unsigned long long* __restrict__ sums,
+                                                                    uint32_t stages, uint32_t stage_alloc,
+                                                                    unsigned int* __restrict__ sched) {
+  using ST = typename Bits<S>::T;
+  constexpr int DS = esize<D>(), SS = esize<S>(), EPW = 8 / DS;
+  constexpr uint32_t kC = kConsumerWarps * 32;  // consumer threads
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
+  __shared__ Tile staged[kMaxStages];
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {  // ---------------- producer
+    if (lane == 0) {
+      // Dynamic tile order: tickets from a per-launch device counter, one
+      // ticket ahead so the descriptor load overlaps the ring wait; tiles are
+      // sorted large-first (build_tiles), so the small ones fill the tail.
+      // The first tile is static (blockIdx.x); the next ticket's atomic is in
+      // flight together with the first descriptor load.
+      const bool dyn = sched != nullptr;
+      uint32_t ti = blockIdx.x;
+      uint32_t tn = dyn ? gridDim.x + atomicAdd(&sched[0], 1u) : ti + gridDim.x;
+      Tile next = ti < ntiles ? tiles[ti] : Tile{};
+      for (uint32_t j = 0;; ++j) {
+        const uint32_t s = j % stages;
+        const uint32_t cur = ti;
+        const Tile t = next;
+        if (cur < ntiles) {
+          ti = tn;
+          if (ti < ntiles) {
+            next = tiles[ti];
+            tn = dyn ? gridDim.x + atomicAdd(&sched[0], 1u) : ti + gridDim.x;
+          }
+        }
+        if (j >= stages) mbar_wait(&empty[s], ((j / stages) - 1) & 1);
+        if (cur >= ntiles) {  // end marker: consumers leave
+          staged[s].op = OP_END;
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+          break;
+        }
+        staged[s] = t;
+        const uint64_t b = t.src_off & ~15ull, e = (t.src_off + uint64_t(t.n_elem) * SS + 15) & ~15ull;
+        mbar_expect_tx(&full[s], uint32_t(e - b));
+        bulk_g2s(ring + s * stage_alloc, src + b, uint32_t(e - b), &full[s]);
+      }
+    }
+  } else {
+    consume_tiles<S, D>(ring, full, empty, staged, dst, sums, stages, stage_alloc);
+  }
+  __syncthreads();
+  if (sched && threadIdx.x == 0) {  // the last CTA re-arms the counter slot for the next launch
+    __threadfence();
+    if (atomicAdd(&sched[1], 1u) == gridDim.x - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+      __threadfence();
+    }
+  }
+}
+
+
 using TransformFn = void (*)(const Tile*, uint32_t, const uint8_t*, uint8_t*, unsigned long long*);
-using TmaFn = void (*)(const Tile*, uint32_t, const uint8_t*, uint8_t*, unsigned long long*, uint32_t, uint32_t);
+using TmaFn = void (*)(const Tile*, uint32_t, const uint8_t*, uint8_t*, unsigned long long*, uint32_t, uint32_t,
+                       unsigned int*);
 
 TmaFn pair_tma_kernel(int s, int d) {
   switch (s * 8 + d) {
@@ -897,11 +938,17 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
   for (auto& ch : p.chunks) group_range(p.tiles, ch.tile_begin, ch.tile_end, ch.groups);
   p.tiles_by_kernel = tiles;
   group_range(p.tiles_by_kernel, 0, uint32_t(tiles.size()), p.groups);
+  // TRIMS_TILE_LPT=1: largest tiles first (A/B: source order measured faster,
+  // profiles/r01_transform_ab_sched.log)
+  static const bool lpt = std::getenv("TRIMS_TILE_LPT") && std::atoi(std::getenv("TRIMS_TILE_LPT"));
+  for (const Group& g : p.groups)
+    if (lpt) std::stable_sort(p.tiles_by_kernel.begin() + g.begin, p.tiles_by_kernel.begin() + g.end,
+                     [](const Tile& x, const Tile& y) { return x.dst_bytes > y.dst_bytes; });
   return p;
 }
 
 uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, const uint8_t* src, uint8_t* dst,
-                       unsigned long long* d_sums, cudaStream_t stream, int sm_count, const SideStream* side) {
+                       unsigned long long* d_sums, cudaStream_t stream, int sm_count, SideStream* side) {
   // With a side stream, the direct-path groups run concurrently with the TMA
   // ring groups: the ring kernel holds one CTA and ~200 KB of shared memory
   // per SM, the smem-free direct CTAs fill the remaining warps and registers.
@@ -930,8 +977,14 @@ uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, co
       const RingCfg& rc = ring_cfg();
       const int smem = int(rc.stages * rc.stage_alloc());
       TRIMS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      fn<<<std::min<uint32_t>(n, sm_count * rc.ctas_per_sm), kTmaThreads, smem, st>>>(t, n, src, dst, d_sums,
-                                                                                      rc.stages, rc.stage_alloc());
+      if (!side || !side->sched) raise(Errc::Internal, "TMA transform launch without a scheduler slot");
+      static const bool dynamic = [] {  // A/B switch: TRIMS_TILE_SCHED=static
+        const char* e = std::getenv("TRIMS_TILE_SCHED");
+        return !(e && std::string(e) == "static");
+      }();
+      unsigned int* slot = dynamic ? side->sched + 2 * (side->sched_next++ % kSchedSlots) : nullptr;
+      fn<<<std::min<uint32_t>(n, sm_count * rc.ctas_per_sm), kTmaThreads, smem, st>>>(
+          t, n, src, dst, d_sums, rc.stages, rc.stage_alloc(), slot);
     } else {
       TransformFn fn = pair_kernel(g.sdt, g.ddt);
       if (!fn) raise(Errc::InvalidArgument, "unsupported dtype pair in plan");

@@ -14,7 +14,7 @@
 
 namespace trims::ingest {
 
-enum Op : uint8_t { OP_HASH = 0, OP_CVT = 1, OP_PERM = 2 };
+enum Op : uint8_t { OP_HASH = 0, OP_CVT = 1, OP_PERM = 2, OP_END = 0xff };
 
 // 40 bytes. dst_off/dst_bytes are multiples of 8 so every tile owns whole
 // checksum words; the last tile of a tensor extends over its trailing pad.
@@ -65,14 +65,20 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
 // Launches one persistent kernel per group over `d_tiles` (device copy of the
 // table the groups index). Per-bucket checksums accumulate atomically into
 // d_sums (mod 2^64). Returns the number of kernel launches.
-// Optional second stream for concurrent groups (fork/join through the events).
+// Launch context of an Ingestor: an optional second stream for concurrent
+// groups (fork/join through the events), and a ring of tile-scheduler
+// counters in device memory for the TMA kernel's dynamic (work-stealing) tile
+// order. Each launch takes the next slot; the kernel's last CTA re-zeroes it,
+// so stream-ordered reuse is safe (slots >> launches in flight).
 struct SideStream {
   cudaStream_t stream{nullptr};
   cudaEvent_t fork{nullptr}, join{nullptr};
+  unsigned int* sched{nullptr};  // kSchedSlots x {next ticket, CTAs done}
+  uint32_t sched_next{0};
 };
+inline constexpr uint32_t kSchedSlots = 256;
 uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, const uint8_t* src, uint8_t* dst,
-                       unsigned long long* d_sums, cudaStream_t stream, int sm_count,
-                       const SideStream* side = nullptr);
+                       unsigned long long* d_sums, cudaStream_t stream, int sm_count, SideStream* side);
 
 // Peer pull over an identity plan's hash groups: copies src -> dst (src is a
 // peer GPU's resident segment) and hashes the copied bytes in the same pass.

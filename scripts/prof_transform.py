@@ -24,16 +24,16 @@ for i in range(reps):
     d_sums.zero_()
     plan.transform(d_src.data_ptr(), d_dst.data_ptr(), d_sums.data_ptr(), s.cuda_stream)
 torch.cuda.synchronize()
-tot = 0.0
-for i in range(10):
+times = []
+for i in range(int(os.environ.get("PROF_ITERS", "40"))):
     flush.zero_()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     plan.transform(d_src.data_ptr(), d_dst.data_ptr(), d_sums.data_ptr(), s.cuda_stream)
     e1.record()
     torch.cuda.synchronize()
-    tot += e0.elapsed_time(e1)
-ms = tot / 10
+    times.append(e0.elapsed_time(e1))
+ms = sorted(times)[len(times) // 2]  # median
 print(json.dumps({"arch": arch, "flags": flags, "tiles": plan.tiles, "ms": round(ms, 4),
                   "GBps_algo": round((plan.read_bytes + plan.write_bytes) / ms / 1e6, 1),
                   "GBps_src": round(plan.src_bytes / ms / 1e6, 1)}))
