@@ -224,6 +224,12 @@ def run_ours(args):
         vgg = C.ARCHS["vgg16"]()
         C.write_arch(vgg, work, seed=1)
         lat["vgg16"] = request_latencies(work, vgg, dev)
+        alex = C.ARCHS["alexnet"]()
+        C.write_arch(alex, work, seed=1)
+        lat["alexnet"] = request_latencies(work, alex, dev)  # BASELINE configs[0]: AlexNet cold then hot
+
+    # ---- BASELINE configs[1]: 16 client processes on one shared HBM copy
+    shared = None if args.quick else shared_clients(work, arch, dev, n_clients=16, n_reqs=args.steps * 5)
 
     peer = peer_serve(work, arch, dev, rank, world, args.steps) if world > 1 else None
 
@@ -253,6 +259,8 @@ def run_ours(args):
     }
     if peer:
         line["peer_serve"] = peer
+    if shared:
+        line["shared_clients"] = shared
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(src_json, blob, res_json)
     if rank == 0:
@@ -310,6 +318,34 @@ def peer_serve(work: str, arch, dev: int, rank: int, world: int, steps: int) -> 
             "resident_bytes": int(ex.resident_blob_bytes), "outcomes": sorted(set(outcomes)),
             "peer_hits": stats["peer_hits"], "peer_fallbacks": stats["peer_fallbacks"],
             "note": "outcome 4 = PeerHit" + ("; shared-GPU mode pulls within one HBM" if SHARED_GPU else "")}
+
+
+def shared_clients(work: str, arch, dev: int, n_clients: int, n_reqs: int) -> dict:
+    """BASELINE configs[1]: ResNet-50 loaded once into this process's store;
+    `n_clients` spawned client processes map the exported arena read-only,
+    bind an executor on the shared weights and serve batch-1 requests at once
+    (paper_1811_09732_b200/sharing.py). Reports per-request latency
+    percentiles, aggregate requests/s, weight copies in HBM and disk reads."""
+    import numpy as np
+
+    from paper_1811_09732_b200 import catalog as C
+    from paper_1811_09732_b200.models import arch_text
+    from paper_1811_09732_b200.sharing import SharedModel, run_clients
+    from paper_1811_09732_b200.store import Store, StoreOptions
+
+    opts = StoreOptions(disk_cache_dir=work, fast_capacity_bytes=2 << 30, host_capacity_bytes=1 << 30,
+                        convert_to="bf16", permute_4d=True, device=dev, scan_disk=False)
+    with Store(opts) as s:
+        ex = s.open(C.arch_key(arch))
+        r = run_clients(SharedModel.from_export(ex, arch_text(arch)), ex.fd, n_clients, n_reqs)
+        st = s.stats()
+        s.close(C.arch_key(arch))
+    logits = r.pop("logits")
+    r["identical_logits_across_clients"] = all(np.array_equal(logits[0], l) for l in logits)
+    r["hbm_weight_copies"] = round(st["tiers"][0]["used_bytes"] / ex.weights_bytes, 4)
+    r["disk_reads"] = st["disk_reads"]
+    r["model"] = arch.name
+    return r
 
 
 def ncu_traffic() -> dict:

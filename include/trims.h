@@ -295,6 +295,10 @@ int trims_net_rebind(trims_net* net, const void* weights);
 int trims_net_run(trims_net* net, void* stream, int use_graph);
 /* flops per forward, kernel launches per forward, workspace bytes */
 int trims_net_info(trims_net* net, double out3[3]);
+/* One request end to end on `stream`: host input (fp32 NCHW, batch x 3 x H x W)
+ * -> device, forward, logits (fp32 batch x classes) -> host, synchronised.
+ * Pinned host buffers give the full PCIe rate. */
+int trims_net_forward_host(trims_net* net, const float* host_input, float* host_logits, void* stream, int use_graph);
 /* row softmax of fp32 logits [M, N] (device pointers) */
 int trims_softmax(const float* in, float* out, int M, int N, void* stream);
 

@@ -999,6 +999,19 @@ int trims_net_run(trims_net* net, void* stream, int use_graph) {
   });
 }
 
+int trims_net_forward_host(trims_net* net, const float* host_input, float* host_logits, void* stream, int use_graph) {
+  return guard([&] {
+    if (!net || !host_input || !host_logits) raise(Errc::InvalidArgument, "null argument");
+    DeviceGuard g(net->net->device());
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TRIMS_CUDA(cudaMemcpyAsync(net->net->input(), host_input, net->net->input_bytes(), cudaMemcpyHostToDevice, st));
+    net->net->run(st, use_graph != 0);
+    TRIMS_CUDA(cudaMemcpyAsync(host_logits, net->net->logits(), net->net->logits_bytes(), cudaMemcpyDeviceToHost, st));
+    TRIMS_CUDA(cudaStreamSynchronize(st));
+    return 0;
+  });
+}
+
 int trims_net_info(trims_net* net, double out3[3]) {
   return guard([&] {
     out3[0] = net->net->flops();

@@ -42,6 +42,9 @@ class Net {
   float* logits() const { return logits_; }  // fp32 [batch, classes]
   int classes() const { return classes_; }
   int input_hw() const { return in_hw_; }
+  uint64_t input_bytes() const { return uint64_t(batch_) * in_c_ * in_hw_ * in_hw_ * sizeof(float); }
+  uint64_t logits_bytes() const { return uint64_t(batch_) * classes_ * sizeof(float); }
+  int device() const { return device_; }
   // One forward pass on `stream`; with use_graph the launch sequence is
   // captured once into a CUDA graph and replayed.
   void run(cudaStream_t stream, bool use_graph);

@@ -1,0 +1,128 @@
+"""Many client processes serving inference from ONE HBM-resident copy of a
+model (BASELINE configs[1]: ResNet-50, 16 concurrent clients sharing one copy
+via IPC; the reference's acceptance C4, proj/tests/acceptance.cpp:76-153).
+
+The store process owns the weights (a sealed segment of its cuMem arena). Each
+client process receives the arena's POSIX fd over a Unix pipe (SCM_RIGHTS,
+what the reference daemon's UDS would carry), maps it read-only
+(trims_import_open), validates the segment tail + manifest digest
+(trims_import_attach), binds an executor on the shared weights
+(trims_net_create) and serves requests with trims_net_forward_host (input
+H2D -> CUDA-graph forward -> logits D2H). No weight byte is copied per client.
+
+Clients use only the C ABI through ctypes (no torch), so a client process
+costs a CUDA context plus its activation workspace.
+"""
+from __future__ import annotations
+
+import ctypes
+import multiprocessing as mp
+import time
+from dataclasses import dataclass
+from multiprocessing.reduction import recv_handle, send_handle
+
+import numpy as np
+
+
+@dataclass
+class SharedModel:
+    """What a client needs to attach one exported model (ObjectRef +
+    manifest digest of the reference's OpenResponse, wire_protocol.hpp:44-62)."""
+    device: int
+    alloc_bytes: int
+    offset: int
+    generation: int
+    payload_bytes: int
+    digest: bytes
+    arch_text: str
+
+    @classmethod
+    def from_export(cls, ex, arch_text: str) -> "SharedModel":
+        return cls(ex.device, ex.alloc_bytes, ex.segment_offset, ex.generation, ex.payload_bytes,
+                   bytes(ex.manifest_digest), arch_text)
+
+
+def _client_main(conn, sm: SharedModel, batch: int, n_reqs: int, seed: int) -> None:
+    try:
+        from ._lib import check, lib
+        from .client import import_segment
+        fd = recv_handle(conn)
+        t0 = time.perf_counter()
+        imp, ptr, res_json = import_segment(sm.device, fd, sm.alloc_bytes, sm.offset, sm.generation,
+                                            sm.payload_bytes, sm.digest)
+        net = ctypes.c_void_p()
+        check(lib.trims_net_create(sm.device, sm.arch_text.encode(), res_json.encode(), ptr, batch,
+                                   ctypes.byref(net)))
+        classes, hw = ctypes.c_int(), ctypes.c_int()
+        check(lib.trims_net_buffers(net, None, None, ctypes.byref(classes), ctypes.byref(hw)))
+        attach_ms = (time.perf_counter() - t0) * 1e3
+        x = np.random.default_rng(seed).standard_normal((batch, 3, hw.value, hw.value)).astype(np.float32)
+        y = np.empty((batch, classes.value), np.float32)
+        check(lib.trims_net_forward_host(net, x.ctypes.data, y.ctypes.data, None, 1))  # warm-up + graph capture
+        conn.send(("ready", attach_ms))
+        assert conn.recv() == "go"
+        lat = []
+        t_first = time.perf_counter()
+        for _ in range(n_reqs):
+            t = time.perf_counter()
+            check(lib.trims_net_forward_host(net, x.ctypes.data, y.ctypes.data, None, 1))
+            lat.append((time.perf_counter() - t) * 1e3)
+        t_last = time.perf_counter()
+        conn.send(("done", lat, t_first, t_last, y.copy()))
+        lib.trims_net_destroy(net)
+        lib.trims_import_close(imp)
+    except Exception as e:  # reported to the store process
+        conn.send(("error", repr(e)))
+    finally:
+        conn.close()
+
+
+def run_clients(sm: SharedModel, fd: int, n_clients: int = 16, n_reqs: int = 20, batch: int = 1,
+                seed: int = 2, timeout_s: float = 600.0) -> dict:
+    """Spawn `n_clients` processes on the shared model; all start serving at
+    once. Returns per-request latency percentiles (ms), aggregate requests/s
+    over the common serving window, attach cost, and every client's logits
+    of the last request (same input in every client)."""
+    ctx = mp.get_context("spawn")
+    procs, conns = [], []
+    for i in range(n_clients):
+        parent, child = ctx.Pipe()
+        p = ctx.Process(target=_client_main, args=(child, sm, batch, n_reqs, seed), daemon=True)
+        p.start()
+        send_handle(parent, fd, p.pid)
+        procs.append(p)
+        conns.append(parent)
+    try:
+        attach = []
+        for c in conns:
+            if not c.poll(timeout_s):
+                raise TimeoutError("client did not become ready")
+            msg = c.recv()
+            if msg[0] != "ready":
+                raise RuntimeError(f"client failed: {msg}")
+            attach.append(msg[1])
+        for c in conns:
+            c.send("go")
+        lat, starts, ends, logits = [], [], [], []
+        for c in conns:
+            if not c.poll(timeout_s):
+                raise TimeoutError("client did not finish")
+            msg = c.recv()
+            if msg[0] != "done":
+                raise RuntimeError(f"client failed: {msg}")
+            lat += msg[1]
+            starts.append(msg[2])
+            ends.append(msg[3])
+            logits.append(msg[4])
+    finally:
+        for p in procs:
+            p.join(30)
+            if p.is_alive():
+                p.kill()
+    lat.sort()
+    pct = lambda q: lat[min(len(lat) - 1, max(0, int(np.ceil(q * len(lat))) - 1))]  # nearest rank
+    window = max(ends) - min(starts)
+    return {"clients": n_clients, "requests": len(lat), "batch": batch,
+            "p50_ms": round(pct(0.50), 3), "p99_ms": round(pct(0.99), 3), "max_ms": round(lat[-1], 3),
+            "requests_per_s": round(len(lat) / window, 1),
+            "attach_ms_median": round(float(np.median(attach)), 2), "logits": logits}
