@@ -29,6 +29,8 @@ int trims_wire_code(int code);
 const char* trims_last_error(void);
 /* library / device facts: cuda device count (0 on GPU-less hosts), SHA-NI use */
 int trims_device_count(void);
+/* Create the device's primary context ahead of the first open/attach. */
+int trims_device_init(int device);
 int trims_sha_hw(void);
 
 /* ------------------------------------------------- artifact format (a1, a2, a7) */

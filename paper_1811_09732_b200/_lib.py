@@ -126,6 +126,7 @@ _SIGS = {
     "trims_wire_code": (_c.c_int, [_c.c_int]),
     "trims_last_error": (_s, []),
     "trims_device_count": (_c.c_int, []),
+    "trims_device_init": (_c.c_int, [_c.c_int]),
     "trims_sha_hw": (_c.c_int, []),
     "trims_sha256": (_c.c_int, [_p, _u64, _p]),
     "trims_read_manifest": (_c.c_int, [_s, _c.c_int, _s, _u64, _p, _c.POINTER(_u64), _c.POINTER(_u64)]),

@@ -213,6 +213,15 @@ int trims_device_count(void) {
   return n;
 }
 
+int trims_device_init(int device) {
+  return guard([&] {
+    if (device < 0 || device >= trims_device_count()) raise(Errc::NoDevice, "no CUDA device " + std::to_string(device));
+    TRIMS_CUDA(cudaSetDevice(device));
+    TRIMS_CUDA(cudaFree(nullptr));  // creates the primary context now, not inside the first open
+    return 0;
+  });
+}
+
 int trims_sha_hw(void) { return Sha256::hw_accelerated() ? 1 : 0; }
 
 int trims_sha256(const void* data, uint64_t n, uint8_t out[32]) {

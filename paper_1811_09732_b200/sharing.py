@@ -46,6 +46,7 @@ def _client_main(conn, sm: SharedModel, batch: int, n_reqs: int, seed: int) -> N
     try:
         from ._lib import check, lib
         from .client import import_segment
+        check(lib.trims_device_init(sm.device))  # context creation is not part of the attach
         fd = recv_handle(conn)
         t0 = time.perf_counter()
         imp, ptr, res_json = import_segment(sm.device, fd, sm.alloc_bytes, sm.offset, sm.generation,
