@@ -230,6 +230,8 @@ def run_ours(args):
 
     # ---- BASELINE configs[1]: 16 client processes on one shared HBM copy
     shared = None if args.quick else shared_clients(work, arch, dev, n_clients=16, n_reqs=args.steps * 5)
+    # ---- BASELINE configs[2] + [4]: 37-model mix / FaaS traces under memory pressure
+    mix = None if args.quick else mix_traces(dev, rank, world)
 
     peer = peer_serve(work, arch, dev, rank, world, args.steps) if world > 1 else None
 
@@ -261,6 +263,8 @@ def run_ours(args):
         line["peer_serve"] = peer
     if shared:
         line["shared_clients"] = shared
+    if mix:
+        line["traces"] = mix
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(src_json, blob, res_json)
     if rank == 0:
@@ -346,6 +350,74 @@ def shared_clients(work: str, arch, dev: int, n_clients: int, n_reqs: int) -> di
     r["disk_reads"] = st["disk_reads"]
     r["model"] = arch.name
     return r
+
+
+CATALOG_DIR = "/tmp/trims-bench-small37-seed1"
+
+
+def small37_catalog(rank: int, world: int) -> tuple[str, list, int]:
+    """The reference's small37 catalog (seed 1, byte-identical to its
+    gen_catalog), generated once per node into a shared directory."""
+    from paper_1811_09732_b200 import catalog as C
+    models, div = C.catalog("small37")
+    total = sum(C.scaled_weights_bytes(m, div) for m in models)
+    keys = [C.catalog_key(m) for m in models]
+    want = {k.filename for k in keys}
+    have = set(os.listdir(CATALOG_DIR)) if os.path.isdir(CATALOG_DIR) else set()
+    if rank == 0 and not want <= have:
+        C.gen_catalog("small37", CATALOG_DIR, seed=1)
+    barrier(world)
+    return CATALOG_DIR, keys, total
+
+
+def mix_traces(dev: int, rank: int, world: int, n_requests: int = 1000) -> dict:
+    """BASELINE configs[2] (37-model mix under memory pressure, LRU) and
+    configs[4] (FaaS trace, Zipf over model ids), through the public store API.
+    The harness's oversubscription contract (harness.cpp:448-452): each GPU's
+    fast tier holds half the catalog's weights, host = catalog + 1 MB. Every
+    request: open (force shared) -> GPU compute over every weight byte (the
+    block-checksum pass, touch's role) -> close. The global trace is split
+    round-robin over the ranks; with N > 1 the node directory turns misses
+    into NVLink PeerHits. Baseline: a private load per model (file -> HBM,
+    then the same compute), the reference harness's no-daemon baseline."""
+    import numpy as np
+    import torch
+
+    from paper_1811_09732_b200 import workload as W
+    from paper_1811_09732_b200.store import Store, StoreOptions
+
+    cat, keys, total = small37_catalog(rank, world)
+    touch = W.DeviceTouch(dev)
+    # private (no-store) baseline: read the artifact, upload, compute
+    from paper_1811_09732_b200 import format as F
+    base = {}
+    for k in keys:
+        path = os.path.join(cat, k.filename)
+        t0 = time.perf_counter()
+        info = F.read_manifest(path)
+        blob = np.fromfile(path, dtype=np.uint8, count=info.blob_bytes, offset=info.blob_offset)
+        d = torch.from_numpy(blob).to(f"cuda:{dev}")
+        touch(d.data_ptr(), d.numel())
+        base[k] = time.perf_counter() - t0
+        del d, blob
+    out = {"catalog": "small37 seed 1", "models": len(keys), "catalog_weight_bytes": total,
+           "fast_capacity_per_gpu": total // 2, "policy": "LRU", "requests_total": n_requests}
+    traces = {"pareto_reference_stream": W.pareto_trace(42, n_requests, len(keys)),
+              "faas_zipf_s1.1": W.zipf_trace(42, n_requests, len(keys), 1.1)}
+    name = f"trims.mix.{os.environ.get('MASTER_PORT', '0')}"
+    for tname, tr in traces.items():
+        opts = StoreOptions(disk_cache_dir=cat, fast_capacity_bytes=max(total // 2, 1 << 20),
+                            host_capacity_bytes=total + (1 << 20), disk_capacity_bytes=total * 8 + (64 << 20),
+                            device=dev, scan_disk=True, directory=name if world > 1 else None, rank=rank,
+                            world=world)
+        with Store(opts) as s:
+            barrier(world)
+            r = W.run_trace(s, keys, tr[rank::world], dev, private_baseline=base)
+            barrier(world)
+        r["hit_rate_min_over_ranks"] = round(-barrier_max(-r["fast_hit_rate"], world), 4)
+        r["p99_ms_max_over_ranks"] = round(barrier_max(r["p99_ms"], world), 3)
+        out[tname] = r
+    return out
 
 
 def ncu_traffic() -> dict:

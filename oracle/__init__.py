@@ -165,6 +165,11 @@ class _Ref:
         L.ref_run_oracle.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, _u64p]
         L.ref_ingest.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
         L.ref_latency.argtypes = [ctypes.c_char_p] * 5 + [ctypes.c_int, ctypes.POINTER(ctypes.c_double), _u64p]
+        L.ref_pareto_trace.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_double, ctypes.c_double,
+                                       ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32)]
+        L.ref_trace.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint32,
+                                ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(ctypes.c_double),
+                                _u64p]
         self.L = L
 
     @staticmethod
@@ -248,6 +253,21 @@ class _Ref:
         d = dict(zip(names, list(out)))
         d["touch"] = t.value
         return d
+
+    def pareto_trace(self, seed: int, n: int, alpha: float, x_m: float, active: int) -> list[int]:
+        out = (ctypes.c_uint32 * n)()
+        self._check(self.L.ref_pareto_trace(seed, n, alpha, x_m, active, out), "pareto_trace")
+        return list(out)
+
+    def trace(self, dir: str, names: list[str], trace: list[int], fast: int, host: int, disk: int):
+        n = len(trace)
+        tr = (ctypes.c_uint32 * n)(*trace)
+        out = (ctypes.c_double * n)()
+        st = (ctypes.c_uint64 * 5)()
+        self._check(self.L.ref_trace(dir.encode(), "\n".join(names).encode(), tr, n, fast, host, disk, out, st),
+                    "trace")
+        return list(out), dict(zip(("fast_hits", "fast_misses", "fast_evictions", "open_errors", "disk_reads"),
+                                   list(st)))
 
 
 _port = None

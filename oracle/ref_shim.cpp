@@ -11,6 +11,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
+#include <random>
 #include <cstdio>
 #include <cstring>
 #include <filesystem>
@@ -22,6 +24,7 @@
 #include "mrm/bench/catalog.hpp"
 #include "mrm/bench/oracle.hpp"
 #include "mrm/bench/simulator.hpp"
+#include "mrm/bench/stats_math.hpp"
 #include "mrm/cache_core.hpp"
 #include "mrm/client.hpp"
 #include "mrm/daemon.hpp"
@@ -440,4 +443,65 @@ int ref_latency(const char* dir, const char* ns, const char* name, const char* v
   });
 }
 
+// The reference worker's request stream (harness.cpp:294-300,
+// tools/mrm_bench.cpp:107-116): mt19937_64(seed), uniform_real over
+// (nextafter(0,1), 1), model = pareto_rank(u, alpha, x_m, active) - 1.
+int ref_pareto_trace(uint64_t seed, uint32_t n, double alpha, double x_m, uint32_t active, uint32_t* out) {
+  return guarded([&] {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> uni(std::nextafter(0.0, 1.0), 1.0);
+    for (uint32_t i = 0; i < n; ++i) out[i] = uint32_t(bench::pareto_rank(uni(rng), alpha, x_m, active) - 1);
+    return 0;
+  });
+}
+
+// A request trace through the UNMODIFIED reference daemon + client (the
+// harness worker loop, harness.cpp:297-322): open(force_shared) -> touch ->
+// close per request, catalog keys zoo/<name>@1.0.0 in `dir`. names: one model
+// name per line, trace: indices into names. out_s: per-request e2e seconds.
+// stats: fast hits, fast misses, fast evictions, open_errors, disk_reads.
+int ref_trace(const char* dir, const char* names_c, const uint32_t* trace, uint32_t n, uint64_t fast_cap,
+              uint64_t host_cap, uint64_t disk_cap, double* out_s, uint64_t* stats) {
+  return guarded([&] {
+    std::vector<model::ModelKey> keys;
+    std::istringstream is(names_c);
+    std::string nm;
+    while (is >> nm) keys.push_back({"zoo", nm, "1.0.0"});
+    daemon::DaemonConfig cfg;
+    cfg.listen_path = "/tmp/mrm-refshim-trace-" + std::to_string(::getpid()) + ".sock";
+    cfg.disk_cache_dir = dir;
+    cfg.startup_calibration = false;
+    cfg.workspace_headroom_fraction = 1.0;
+    cfg.fast_capacity_bytes = fast_cap;
+    cfg.host_capacity_bytes = host_cap;
+    cfg.disk_capacity_bytes = disk_cap;
+    daemon::Daemon dmn(cfg);
+    dmn.start();
+    client::ClientConfig cc;
+    cc.endpoint = cfg.listen_path;
+    cc.model_dirs = {dir};
+    client::Client cli(cc);
+    client::OpenOptions opts;
+    opts.force_shared = true;
+    for (uint32_t i = 0; i < n; ++i) {
+      auto t0 = std::chrono::steady_clock::now();
+      client::ModelView v = cli.open(keys.at(trace[i]), opts);
+      cli.touch(v);
+      auto t1 = std::chrono::steady_clock::now();
+      cli.close(v);
+      out_s[i] = std::chrono::duration<double>(t1 - t0).count();
+    }
+    cache::StatsSnapshot st = dmn.stats();
+    stats[0] = st.tiers[0].hits;
+    stats[1] = st.tiers[0].misses;
+    stats[2] = st.tiers[0].evictions;
+    stats[3] = st.open_errors;
+    stats[4] = st.disk_reads;
+    dmn.request_stop();
+    dmn.join();
+    return 0;
+  });
+}
+
 }  // extern "C"
+

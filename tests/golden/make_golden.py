@@ -173,8 +173,23 @@ def main() -> None:
             json.dump(traces, f)
         run = R.run_oracle(60, 2025, 24, 800)
         json.dump({"run_oracle_seed2025_60x24x800": run}, open(os.path.join(OUT, "oracle_run.json"), "w"))
+    pareto_golden(R)
     print("golden vectors written to", OUT)
 
 
+def pareto_golden(R) -> None:
+    """The reference worker's request streams (mt19937_64 + libstdc++
+    uniform_real + pareto_rank), for workload.pareto_trace."""
+    cases = []
+    for seed, n, active, alpha in [(42, 1000, 37, 1.0), (1, 400, 10, 1.0), (42001127, 1000, 37, 1.0),
+                                   (7, 300, 8, 2.5)]:
+        cases.append({"seed": seed, "n": n, "active": active, "alpha": alpha, "x_m": 1.0,
+                      "trace": R.pareto_trace(seed, n, alpha, 1.0, active)})
+    json.dump(cases, open(os.path.join(OUT, "pareto_trace.json"), "w"))
+
+
 if __name__ == "__main__":
-    main()
+    if "--pareto-only" in sys.argv:
+        pareto_golden(oracle.ref())
+    else:
+        main()
