@@ -577,6 +577,7 @@ def run_reference(args):
         r = R.latency(work, (key.ns, key.name, key.version), mode, 3)
         lat[f"{mode}_open"] = round(r["open_s"] * 1e3, 3)
         lat[f"{mode}_e2e_with_touch"] = round(r["end_to_end_s"] * 1e3, 3)
+    traces = None if args.quick else reference_traces(R)
     cores = 1
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
@@ -591,7 +592,28 @@ def run_reference(args):
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "latency_ms": lat,
     }
+    if traces:
+        line["traces"] = traces
     print(json.dumps(line), flush=True)
+
+
+def reference_traces(R, n: int = 150) -> dict:
+    """configs[2]/[4] through the UNMODIFIED reference daemon + client
+    (oracle ref_trace: open force-shared -> touch -> close), same catalog,
+    capacities and request streams as ours; a bounded sample (the first `n`
+    requests) because every request touches the weights on one CPU core."""
+    from paper_1811_09732_b200 import workload as W
+    cat, keys, total = small37_catalog(0, 1)
+    names = [k.name for k in keys]
+    out = {"catalog": "small37 seed 1", "fast_capacity": total // 2, "sample_requests": n}
+    for tname, tr in (("pareto_reference_stream", W.pareto_trace(42, 1000, len(keys))[:n]),
+                      ("faas_zipf_s1.1", W.zipf_trace(42, 1000, len(keys), 1.1)[:n])):
+        lat, st = R.trace(cat, names, tr, max(total // 2, 1 << 20), total + (1 << 20), total * 8 + (64 << 20))
+        acc = st["fast_hits"] + st["fast_misses"]
+        out[tname] = {"requests": n, "fast_hit_rate": round(st["fast_hits"] / max(1, acc), 4),
+                      "p50_ms": round(W.percentile(lat, 50) * 1e3, 3), "p99_ms": round(W.percentile(lat, 99) * 1e3, 3),
+                      "mean_ms": round(sum(lat) / len(lat) * 1e3, 3), "evictions": st["fast_evictions"]}
+    return out
 
 
 def main():
