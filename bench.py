@@ -18,7 +18,9 @@ word checksummed.
           ideal, for ResNet-50 and VGG-16 at batch 1 (rank 0's numbers).
 
 Timing: CUDA events on the launching stream, W untimed warm-ups, K timed
-steps, L2 flushed (256 MiB write) before every timed step, max over ranks.
+steps, L2 flushed before every timed step (256 MiB write + 256 MiB read of a
+second buffer, so no dirty lines are written back inside the timed region),
+max over ranks.
 ``--impl reference`` times the reference's own CPU path (oracle/_ref, built
 from /root/reference) on the same artifact and config.
 """
@@ -160,6 +162,13 @@ def run_ours(args):
     d_dst = torch.empty(res_bytes, dtype=torch.uint8, device=f"cuda:{dev}")
     d_sums = torch.zeros(info["buckets"], dtype=torch.int64, device=f"cuda:{dev}")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+    flush_r = torch.ones(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+
+    def flush_l2():
+        # write 256 MiB (> the 126 MB L2: evicts everything), then read another
+        # 256 MiB so the dirty lines are written back outside the timed region
+        flush.zero_()
+        flush_r.view(torch.int64).sum()
     stream = torch.cuda.Stream(device=dev)
     launches = [0]
 
@@ -179,7 +188,7 @@ def run_ours(args):
     with ClockSampler(dev) as clocks:
         with torch.cuda.stream(stream):
             for i in range(args.steps):
-                flush.zero_()                    # L2 flush outside the timed events
+                flush_l2()                       # L2 flush outside the timed events
                 d_sums.zero_()
                 ev[i][0].record(stream)
                 transform()
@@ -201,7 +210,7 @@ def run_ours(args):
     e2e_ms = 0.0
     launches_e2e = 0
     for i in range(args.steps):
-        flush.zero_()
+        flush_l2()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         cs, st = plan.ingest_host(host.data_ptr(), d_dst.data_ptr())   # H2D + transform + D2H checksums
@@ -243,7 +252,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8/fp32->bf16", "data": "synthetic (seeded uniform init)",
         "config": {"workload": WORKLOAD, "artifact_bytes": src_bytes, "resident_bytes": res_bytes,
-                   "tensors": len(rb["tensors"]), "l2": "flushed (256 MiB write) before every timed step",
+                   "tensors": len(rb["tensors"]), "l2": "flushed before every timed step (256 MiB write, then 256 MiB read of another buffer)",
                    "parallelism": f"store shard per GPU x{world}"},
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": src_bytes,
                 "d2h_bytes_per_step": info["buckets"] * 8, "ms_per_step": round(e2e_max / args.steps, 4),
@@ -252,8 +261,8 @@ def run_ours(args):
                      "frac": round(achieved / hbm_peak, 4), **ncu_traffic(),
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                      "algorithmic_bytes_per_launch": algo,
-                     "kernel": "transform step = transform_tma_kernel (KCRS->KRSC tiles) || transform_kernel "
-                               "(elementwise tiles), one launch each, concurrent",
+                     "kernel": "transform_tma_kernel<f32,bf16>: one persistent launch per step (KCRS->KRSC + "
+                               "elementwise tiles; static LPT bins + dynamic tail)",
                      "launches_per_step": info["launches_per_step"]},
         "gpu_launches": launches[0] + launches_e2e,
         "clocks": clocks.summary(),
@@ -425,7 +434,7 @@ def ncu_traffic() -> dict:
     `ncu --set full` summary (profiles/*_ncu_transform.json, written by
     scripts/ncu_summary.py); null when none is committed."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_transform.json")), key=os.path.getmtime)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_transform.json")))  # newest round tag last
     if not files:
         return {"traffic": None}
     doc = json.load(open(files[-1]))
@@ -619,7 +628,7 @@ def reference_traces(R, n: int = 150) -> dict:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -210,13 +210,20 @@ void tro_permute_kcrs_krsc(const void* src, uint64_t K, uint64_t C, uint64_t R, 
         }
 }
 
+/* per-position odd key of the block checksum (trims_oracle.h) */
+static uint64_t tro_checksum_key(uint64_t g) {
+  uint32_t t = (uint32_t)g * 0x9e3779b1u;
+  uint32_t klo = (t ^ (t >> 16)) | 1u, khi = t * 0xc2b2ae3du;
+  return ((uint64_t)khi << 32) | klo;
+}
+
 uint64_t tro_block_checksum(const uint8_t* p, uint64_t nbytes, uint64_t word0) {
   uint64_t sum = 0, words = (nbytes + 7) / 8;
   for (uint64_t i = 0; i < words; ++i) {
     uint64_t w = 0;
     uint64_t take = (nbytes - 8 * i) < 8 ? (nbytes - 8 * i) : 8;
     memcpy(&w, p + 8 * i, take);
-    sum += mix64(w ^ ((word0 + i + 1) * GOLDEN));
+    sum += w * tro_checksum_key(word0 + i);
   }
   return sum;
 }

@@ -64,10 +64,14 @@ void tro_permute_kcrs_krsc(const void* src, uint64_t K, uint64_t C, uint64_t R, 
                            uint64_t esize, void* dst);
 
 /* TRIMS block checksum (our definition, fused into the GPU ingest): the
- * region is read as LE u64 words w_i (tail zero-padded to 8 bytes), i counted
- * from `word0`; result = sum_i mix64(w_i ^ ((i+1) * 0x9e3779b97f4a7c15))
- * mod 2^64, mix64 = the splitmix64 finaliser. Additive over disjoint word
- * ranges, so a blob's checksum is the sum of its objects' checksums. */
+ * region is read as LE u64 words w_g (tail zero-padded to 8 bytes), g counted
+ * from `word0`; result = sum_g w_g * K(g) mod 2^64, a multilinear hash with an
+ * odd per-position key: t = (u32)g * 0x9e3779b1, K(g) = (t*0xc2b2ae3d) << 32
+ * | ((t ^ t >> 16) | 1) (keys repeat every 2^32 words = 32 GiB). Any change
+ * of a single word changes the sum (odd key); position enters through K.
+ * Additive over disjoint word ranges, so a blob's checksum is the sum of its
+ * objects' checksums. On the GPU it costs ~8 integer instructions per word
+ * (32-bit IMADs), where a splitmix finaliser per word cost ~30. */
 uint64_t tro_block_checksum(const uint8_t* p, uint64_t nbytes, uint64_t word0);
 
 /* Synthetic real-valued init (our definition): element j of a tensor whose

@@ -124,13 +124,17 @@ std::shared_ptr<IngestPlan> Ingestor::compile(const fmt::Manifest& src, const fm
   p->dst_json = fmt::manifest_to_json(p->dst);
   p->identity = plan.identity();
   const uint64_t chunk = std::max<uint64_t>(16ull << 20, src.blob_bytes / (events_.size() - 8) + 1);
-  p->plan = ingest::build_tiles(p->src, p->dst, p->identity, chunk);
+  p->plan = ingest::build_tiles(p->src, p->dst, p->identity, chunk, sms_);
   if (!p->plan.tiles.empty()) {
-    const size_t bytes = p->plan.tiles.size() * sizeof(ingest::Tile);
-    TRIMS_CUDA(cudaMalloc(&p->d_tiles, bytes));
-    TRIMS_CUDA(cudaMemcpy(p->d_tiles, p->plan.tiles.data(), bytes, cudaMemcpyHostToDevice));
-    TRIMS_CUDA(cudaMalloc(&p->d_tiles_k, bytes));
-    TRIMS_CUDA(cudaMemcpy(p->d_tiles_k, p->plan.tiles_by_kernel.data(), bytes, cudaMemcpyHostToDevice));
+    // each table is followed by the bin offsets of its static schedules
+    auto upload = [](ingest::Tile** d, const std::vector<ingest::Tile>& t, const std::vector<uint32_t>& bins) {
+      const size_t tb = t.size() * sizeof(ingest::Tile), bb = bins.size() * sizeof(uint32_t);
+      TRIMS_CUDA(cudaMalloc(d, tb + bb));
+      TRIMS_CUDA(cudaMemcpy(*d, t.data(), tb, cudaMemcpyHostToDevice));
+      if (bb) TRIMS_CUDA(cudaMemcpy(reinterpret_cast<uint8_t*>(*d) + tb, bins.data(), bb, cudaMemcpyHostToDevice));
+    };
+    upload(&p->d_tiles, p->plan.tiles, p->plan.bins);
+    upload(&p->d_tiles_k, p->plan.tiles_by_kernel, p->plan.bins_k);
   }
   return p;
 }

@@ -344,7 +344,7 @@ int trims_checksum_host(const void* p, uint64_t n, uint64_t word0, uint64_t* out
       for (uint64_t i = s; i < e; ++i) {
         uint64_t w = 0;
         std::memcpy(&w, b + 8 * i, std::min<uint64_t>(8, n - 8 * i));
-        acc += mix64(w ^ ((word0 + i + 1) * 0x9e3779b97f4a7c15ull));
+        acc += ingest::checksum_term(w, word0 + i);
       }
       total.fetch_add(acc);
     });

@@ -7,6 +7,7 @@
 // conversions are integer-defined so they are bit-identical to the CPU oracle
 // (oracle/trims_oracle.c) — no reliance on hardware NaN canonicalisation.
 #include <algorithm>
+#include <queue>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -51,13 +52,15 @@ const RingCfg& ring_cfg() {
 #endif
 constexpr int kConsumerWarps = TRIMS_CONSUMER_WARPS;  // TMA kernel: 1 producer warp + consumer warps
 constexpr int kTmaThreads = 32 * (kConsumerWarps + 1);
+constexpr uint32_t kDescCap = 384;
+constexpr int kDefaultTailPct = 15;  // dynamic share of a TMA group's tile cost  // static-schedule descriptors staged in smem per batch (18 KiB)
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
   z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
   return z ^ (z >> 31);
 }
-__device__ __forceinline__ uint64_t word_hash(uint64_t w, uint64_t gw) { return mix64(w ^ ((gw + 1) * kGold)); }
+__device__ __forceinline__ uint64_t word_hash(uint64_t w, uint64_t gw) { return checksum_term(w, gw); }
 
 // dtype codes are fmt::DType: F64=0 F32=1 F16=2 I8=3 BF16=4
 template <int DT> struct Bits;
@@ -514,6 +517,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32
                : "memory");
 }
 
+// 64-bit warp sum from three 32-bit redux.sync adds (16 + 16 + 32 bits): the
+// low pieces cannot overflow 32 lanes, the high piece only matters mod 2^32.
+__device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
+  const uint32_t l = __reduce_add_sync(0xffffffffu, uint32_t(v) & 0xffffu);
+  const uint32_t m = __reduce_add_sync(0xffffffffu, uint32_t(v) >> 16);
+  const uint32_t h = __reduce_add_sync(0xffffffffu, uint32_t(v >> 32));
+  return uint64_t(l) + (uint64_t(m) << 16) + (uint64_t(h) << 32);
+}
+
+// EPW source elements at stride `stride` (shared memory) -> one resident word;
+// fp32 -> bf16 through the pair-convert instruction.
+template <int S, int D, int EPW>
+__device__ __forceinline__ uint64_t gather_word(const typename Bits<S>::T* e, uint32_t stride) {
+  typename Bits<S>::T v[EPW];
+#pragma unroll
+  for (int q = 0; q < EPW; ++q) v[q] = e[q * stride];
+  return pack_word<S, D, EPW>(v);
+}
+
 // Consumer warps of transform_tma_kernel: wait for a staged tile, convert /
 // permute it out of shared memory, store + hash the resident words, hand the
 // stage back.
@@ -526,10 +548,11 @@ __device__ __forceinline__ void consume_tiles(const uint8_t* ring, uint64_t* ful
   constexpr uint32_t kC = kConsumerWarps * 32;  // consumer threads
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t ct = threadIdx.x - 32, cw = warp - 1;
-  WarpSum ws;
-  for (uint32_t j = 0;; ++j) {
-    const uint32_t s = j % stages;
-    mbar_wait(&full[s], (j / stages) & 1);
+  uint32_t bucket = ~0u;  // per-warp checksum accumulator, flushed when the tensor changes
+  uint64_t wacc = 0;
+  uint32_t s = 0, phase = 0;
+  for (;;) {
+    mbar_wait(&full[s], phase);
     const Tile t = staged[s];
     if (t.op == OP_END) break;
     const ST* el = reinterpret_cast<const ST*>(ring + s * stage_alloc + (t.src_off & 15));
@@ -539,53 +562,65 @@ __device__ __forceinline__ void consume_tiles(const uint8_t* ring, uint64_t* ful
     uint64_t acc = 0;
     if (t.op == OP_CVT) {
       const bool vec = ((t.src_off & 15) % (EPW * SS)) == 0;
-#pragma unroll 2
-      for (uint32_t w = ct; w < words; w += kC) {
+      const uint32_t full_words = vec ? n / EPW : 0;
+#pragma unroll 4
+      for (uint32_t w = ct; w < full_words; w += kC) {
+        ST v[EPW];
+        if constexpr (EPW * SS >= 16) {
+#pragma unroll
+          for (int i = 0; i < EPW * SS / 16; ++i) reinterpret_cast<uint4*>(v)[i] = reinterpret_cast<const uint4*>(el + w * EPW)[i];
+        } else if constexpr (EPW * SS == 8) {
+          *reinterpret_cast<uint2*>(v) = *reinterpret_cast<const uint2*>(el + w * EPW);
+        } else {
+#pragma unroll
+          for (int q = 0; q < EPW; ++q) v[q] = el[w * EPW + q];
+        }
+        const uint64_t word = pack_word<S, D, EPW>(v);
+        d[w] = word;
+        acc += word_hash(word, gw0 + w);
+      }
+      for (uint32_t w = full_words + ct; w < words; w += kC) {  // partial word, trailing pad
         const uint32_t e0 = w * EPW;
         uint64_t word = 0;
-        if (e0 + EPW <= n && vec) {
-          ST v[EPW];
-          if constexpr (EPW * SS >= 16) {
-#pragma unroll
-            for (int i = 0; i < EPW * SS / 16; ++i) reinterpret_cast<uint4*>(v)[i] = reinterpret_cast<const uint4*>(el + e0)[i];
-          } else if constexpr (EPW * SS == 8) {
-            *reinterpret_cast<uint2*>(v) = *reinterpret_cast<const uint2*>(el + e0);
-          } else {
-#pragma unroll
-            for (int q = 0; q < EPW; ++q) v[q] = el[e0 + q];
-          }
-          word = pack_word<S, D>(v);
-        } else {
-          for (int q = 0; q < EPW && e0 + q < n; ++q) word |= uint64_t(cvt<S, D>(el[e0 + q])) << (8 * DS * q);
-        }
+        for (int q = 0; q < EPW && e0 + q < n; ++q) word |= uint64_t(cvt<S, D>(el[e0 + q])) << (8 * DS * q);
         d[w] = word;
         acc += word_hash(word, gw0 + w);
       }
     } else {  // OP_PERM: source [g][C][RS] in smem -> resident [g][RS][C]
       const uint32_t C = t.C, RS = t.RS, CRS = C * RS;
+      const uint32_t wpr = (C * DS) / 8, rows = t.rows;
+      const uint32_t rs_magic = t.rs_magic;  // k = row / RS = umulhi(row, ceil(2^32/RS))
       uint32_t body = 0;  // words written by the fast paths below
-      if ((C * DS) % 8 == 0 && RS > 1) {
-        // Flattened (row, word) items, 32 consecutive words per warp step:
-        // full lanes even when a row is shorter than a warp (C = 64). Each lane
-        // gathers its EPW elements (source stride RS) in an order rotated by
-        // lane/8, which makes the four shared loads of a step hit 32 distinct
-        // banks for odd RS (3x3, 5x5, 7x7) instead of 8.
-        const uint32_t wpr = C / EPW, rows = (n / CRS) * RS, items = rows * wpr;
-        body = items;
-        const bool pow2 = (wpr & (wpr - 1)) == 0;
-        const uint32_t sh = __ffs(wpr) - 1, rs_magic = 0xffffffffu / RS + 1;  // k = ceil(2^32/RS)*row >> 32
-        const uint32_t rot = (lane >> 3) & (EPW - 1);
+      if ((C * DS) % 8 == 0 && RS > 1 && (wpr & 7) == 0) {
+        // Units of 4 rows x 8 words: lane (lane>>3, lane&7) takes row 4u'+lane>>3,
+        // word 8o+lane&7. For odd RS the 32 lanes of one shared load then hit 32
+        // distinct banks (row offsets 0..3 + multiples of 4), with no rotation,
+        // so the EPW loads pack straight into pair converts.
+        const uint32_t oct = wpr >> 3, units = ((rows + 3) >> 2) * oct;
+        const bool pow2 = (oct & (oct - 1)) == 0;
+        const uint32_t sh = __ffs(oct) - 1, oct_magic = pow2 ? 0u : 0xffffffffu / oct + 1;
+        const uint32_t g = lane >> 3, o = lane & 7;
+        body = rows * wpr;
 #pragma unroll 2
-        for (uint32_t it = cw * 32 + lane; it < items; it += kC) {
-          const uint32_t row = pow2 ? it >> sh : it / wpr, wi = it - row * wpr;
-          const uint32_t k = __umulhi(row, rs_magic), r = row - k * RS;
-          const ST* e = el + k * CRS + r + wi * EPW * RS;
-          uint64_t word = 0;
-#pragma unroll
-          for (int q = 0; q < EPW; ++q) {
-            const uint32_t qq = (q + rot) & (EPW - 1);
-            word |= uint64_t(cvt1<S, D>(e[qq * RS])) << (8 * DS * qq);
+        for (uint32_t u = cw; u < units; u += kConsumerWarps) {
+          const uint32_t q4 = pow2 ? u >> sh : __umulhi(u, oct_magic);
+          const uint32_t row = 4 * q4 + g, wi = 8 * (u - q4 * oct) + o;
+          if (row < rows) {
+            const uint32_t k = __umulhi(row, rs_magic), r = row - k * RS;
+            const uint64_t word = gather_word<S, D, EPW>(el + k * CRS + r + wi * EPW * RS, RS);
+            const uint32_t it = row * wpr + wi;
+            d[it] = word;
+            acc += word_hash(word, gw0 + it);
           }
+        }
+      } else if ((C * DS) % 8 == 0 && RS > 1) {
+        // Flattened (row, word) items, 32 consecutive words per warp step.
+        const uint32_t items = rows * wpr;
+        body = items;
+        for (uint32_t it = ct; it < items; it += kC) {
+          const uint32_t row = it / wpr, wi = it - row * wpr;
+          const uint32_t k = __umulhi(row, rs_magic), r = row - k * RS;
+          const uint64_t word = gather_word<S, D, EPW>(el + k * CRS + r + wi * EPW * RS, RS);
           d[it] = word;
           acc += word_hash(word, gw0 + it);
         }
@@ -610,12 +645,27 @@ __device__ __forceinline__ void consume_tiles(const uint8_t* ring, uint64_t* ful
         acc += word_hash(word, gw0 + w);
       }
     }
-    ws.add(t.tensor, acc, sums);
+    if (t.tensor != bucket) {  // warp-uniform
+      if (bucket != ~0u) {
+        const uint64_t v = warp_sum64(wacc);
+        if (lane == 0 && v) atomicAdd(&sums[bucket], (unsigned long long)v);
+      }
+      bucket = t.tensor;
+      wacc = 0;
+    }
+    wacc += acc;
     __syncwarp();  // every lane's shared-memory reads of stage s are done
     if (lane == 0)
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])) : "memory");
+    if (++s == stages) {
+      s = 0;
+      phase ^= 1;
+    }
   }
-  ws.flush(sums);
+  if (bucket != ~0u) {
+    const uint64_t v = warp_sum64(wacc);
+    if (lane == 0 && v) atomicAdd(&sums[bucket], (unsigned long long)v);
+  }
 }
 
 // Warp-specialised: warp 0 is the producer (one elected lane issues the bulk
@@ -629,13 +679,15 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
                                                                     uint8_t* __restrict__ dst,
                                                                     unsigned long long* __restrict__ sums,
                                                                     uint32_t stages, uint32_t stage_alloc,
-                                                                    unsigned int* __restrict__ sched) {
+                                                                    unsigned int* __restrict__ sched,
+                                                                    const uint32_t* __restrict__ bins) {
   using ST = typename Bits<S>::T;
   constexpr int DS = esize<D>(), SS = esize<S>(), EPW = 8 / DS;
   constexpr uint32_t kC = kConsumerWarps * 32;  // consumer threads
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ Tile staged[kMaxStages];
+  __shared__ __align__(16) Tile descs[kDescCap];  // static schedule: this CTA's descriptors
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -648,38 +700,57 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
   __syncthreads();
 
   if (warp == 0) {  // ---------------- producer
-    if (lane == 0) {
-      // Dynamic tile order: tickets from a per-launch device counter, one
-      // ticket ahead so the descriptor load overlaps the ring wait; tiles are
-      // sorted large-first (build_tiles), so the small ones fill the tail.
-      // The first tile is static (blockIdx.x); the next ticket's atomic is in
-      // flight together with the first descriptor load.
-      const bool dyn = sched != nullptr;
-      uint32_t ti = blockIdx.x;
-      uint32_t tn = dyn ? gridDim.x + atomicAdd(&sched[0], 1u) : ti + gridDim.x;
-      Tile next = ti < ntiles ? tiles[ti] : Tile{};
-      for (uint32_t j = 0;; ++j) {
-        const uint32_t s = j % stages;
-        const uint32_t cur = ti;
-        const Tile t = next;
-        if (cur < ntiles) {
-          ti = tn;
-          if (ti < ntiles) {
-            next = tiles[ti];
-            tn = dyn ? gridDim.x + atomicAdd(&sched[0], 1u) : ti + gridDim.x;
-          }
-        }
-        if (j >= stages) mbar_wait(&empty[s], ((j / stages) - 1) & 1);
-        if (cur >= ntiles) {  // end marker: consumers leave
-          staged[s].op = OP_END;
-          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
-          break;
-        }
-        staged[s] = t;
-        const uint64_t b = t.src_off & ~15ull, e = (t.src_off + uint64_t(t.n_elem) * SS + 15) & ~15ull;
-        mbar_expect_tx(&full[s], uint32_t(e - b));
-        bulk_g2s(ring + s * stage_alloc, src + b, uint32_t(e - b), &full[s]);
+    uint32_t s = 0, round = 0;  // ring slot, and how many times the ring has wrapped
+    auto push = [&](const Tile& t) {  // lane 0: stage t's raw bytes into slot s
+      if (round) mbar_wait(&empty[s], (round - 1) & 1);
+      staged[s] = t;
+      const uint64_t b = t.src_off & ~15ull, e = (t.src_off + uint64_t(t.n_elem) * SS + 15) & ~15ull;
+      mbar_expect_tx(&full[s], uint32_t(e - b));
+      bulk_g2s(ring + s * stage_alloc, src + b, uint32_t(e - b), &full[s]);
+      if (++s == stages) {
+        s = 0;
+        ++round;
       }
+    };
+    uint32_t tail0 = 0;
+    if (bins) {
+      // Static part: this CTA's bin, balanced on the host. Its descriptors are
+      // copied into shared memory by the whole warp (one round trip per
+      // kDescCap tiles), so issuing a tile never waits on a global load.
+      const uint32_t b0 = bins[blockIdx.x], b1 = bins[blockIdx.x + 1];
+      tail0 = bins[gridDim.x];
+      for (uint32_t base = b0; base < b1; base += kDescCap) {
+        const uint32_t cnt = min(kDescCap, b1 - base);
+        const uint4* g4 = reinterpret_cast<const uint4*>(tiles + base);
+        uint4* s4 = reinterpret_cast<uint4*>(descs);
+        constexpr uint32_t kW = sizeof(Tile) / 16;
+        for (uint32_t i = lane; i < cnt * kW; i += 32) s4[i] = g4[i];
+        __syncwarp();
+        if (lane == 0)
+          for (uint32_t j = 0; j < cnt; ++j) push(descs[j]);
+        __syncwarp();
+      }
+    }
+    if (lane == 0) {
+      if (sched && tail0 < ntiles) {
+        // Dynamic part: tiles [tail0, ntiles) handed out by a per-launch
+        // ticket counter, so CTAs that ran slow take fewer of them. The next
+        // ticket and its descriptor are fetched while the ring waits.
+        uint32_t ti = tail0 + atomicAdd(&sched[0], 1u);
+        Tile next = ti < ntiles ? tiles[ti] : Tile{};
+        while (ti < ntiles) {
+          const Tile t = next;
+          ti = tail0 + atomicAdd(&sched[0], 1u);
+          if (ti < ntiles) next = tiles[ti];
+          push(t);
+        }
+      } else if (!bins) {  // no schedule at all: static round robin
+        for (uint32_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) push(tiles[ti]);
+      }
+      // end marker: consumers leave
+      if (round) mbar_wait(&empty[s], (round - 1) & 1);
+      staged[s].op = OP_END;
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
     }
   } else {
     consume_tiles<S, D>(ring, full, empty, staged, dst, sums, stages, stage_alloc);
@@ -698,7 +769,7 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
 
 using TransformFn = void (*)(const Tile*, uint32_t, const uint8_t*, uint8_t*, unsigned long long*);
 using TmaFn = void (*)(const Tile*, uint32_t, const uint8_t*, uint8_t*, unsigned long long*, uint32_t, uint32_t,
-                       unsigned int*);
+                       unsigned int*, const uint32_t*);
 
 TmaFn pair_tma_kernel(int s, int d) {
   switch (s * 8 + d) {
@@ -783,9 +854,64 @@ bool supported_pair(fmt::DType s, fmt::DType d) {
          (s == DType::F16 && d == DType::BF16) || (s == DType::BF16 && d == DType::F32);
 }
 
+// One group's tiles -> nb bins (LPT: largest cost first onto the least loaded
+// bin), written back bin-major in the group's range; appends nb+1 offsets
+// (relative to g.begin) to `bins`. Tiles keep source order inside a bin.
+void schedule_bins(std::vector<Tile>& table, Group& g, uint32_t grid, std::vector<uint32_t>& bins,
+                   uint32_t table_words) {
+  constexpr uint64_t kFixed = 8u << 10;  // per-tile charge in byte-equivalents
+  const uint32_t n = g.end - g.begin, nb = std::min(n, grid);
+  std::vector<uint32_t> order(n);
+  std::vector<uint64_t> cost(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    const Tile& t = table[g.begin + i];
+    order[i] = i;
+    cost[i] = kFixed + t.dst_bytes + uint64_t(t.n_elem) * fmt::element_size(fmt::DType(t.sdt));
+  }
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cost[a] > cost[b]; });
+  // The smallest tiles worth `tail_pct` % of the cost form the dynamic tail
+  // (TRIMS_TILE_TAIL, percent), handed out by tickets after the static bins.
+  static const uint64_t tail_pct = [] {
+    const char* e = std::getenv("TRIMS_TILE_TAIL");
+    return e ? uint64_t(std::clamp(std::atoi(e), 0, 100)) : uint64_t(kDefaultTailPct);
+  }();
+  uint64_t total = 0;
+  for (uint64_t c : cost) total += c;
+  uint32_t head = n;
+  for (uint64_t acc = 0; head > 0 && (acc + cost[order[head - 1]]) * 100 <= total * tail_pct; --head)
+    acc += cost[order[head - 1]];
+  using Load = std::pair<uint64_t, uint32_t>;
+  std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+  for (uint32_t b = 0; b < nb; ++b) heap.push({0, b});
+  std::vector<uint32_t> bin_of(n, nb);  // nb = the dynamic tail
+  for (uint32_t k = 0; k < head; ++k) {
+    const uint32_t i = order[k];
+    Load l = heap.top();
+    heap.pop();
+    bin_of[i] = l.second;
+    heap.push({l.first + cost[i], l.second});
+  }
+  std::vector<uint32_t> start(nb + 2, 0);
+  for (uint32_t i = 0; i < n; ++i) ++start[bin_of[i] + 1];
+  for (uint32_t b = 0; b <= nb; ++b) start[b + 1] += start[b];
+  std::vector<Tile> out(n);
+  std::vector<uint32_t> fill(start.begin(), start.end() - 1);
+  for (uint32_t i = 0; i < n; ++i) out[fill[bin_of[i]]++] = table[g.begin + i];
+  // tail in largest-first order: the small ones fill the end
+  std::vector<uint32_t> tail_order;
+  for (uint32_t k = head; k < n; ++k) tail_order.push_back(order[k]);
+  for (uint32_t k = 0; k < tail_order.size(); ++k) out[start[nb] + k] = table[g.begin + tail_order[k]];
+  std::copy(out.begin(), out.end(), table.begin() + g.begin);
+  g.bin_base = table_words + uint32_t(bins.size());
+  g.nbins = nb;
+  g.tail = n - start[nb];
+  bins.insert(bins.end(), start.begin(), start.end() - 1);  // nb+1 offsets; bins[nb] = tail start
+}
+
 }  // namespace
 
-TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool identity, uint64_t chunk_bytes) {
+TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool identity, uint64_t chunk_bytes,
+                     int sm_count) {
   // kernel key: hash | (TMA ring or direct) x dtype pair. TRIMS_CVT_PATH /
   // TRIMS_PERM_PATH = "direct" | "tma" select the kernel per op (A/B switch).
   static const bool cvt_direct = [] {  // default: elementwise tiles ride the TMA ring too (one launch)
@@ -878,6 +1004,8 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
           t.ddt = uint8_t(d.dtype);
           t.C = uint32_t(C);
           t.RS = uint32_t(RS);
+          t.rows = uint32_t(kn * RS);
+          t.rs_magic = uint32_t(0xffffffffu / RS + 1);
           t.pad_ = gather ? 1 : 0;
           tiles.push_back(t);
         }
@@ -944,6 +1072,24 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
   for (const Group& g : p.groups)
     if (lpt) std::stable_sort(p.tiles_by_kernel.begin() + g.begin, p.tiles_by_kernel.begin() + g.end,
                      [](const Tile& x, const Tile& y) { return x.dst_bytes > y.dst_bytes; });
+  // Static schedule of the TMA groups (default; TRIMS_TILE_SCHED=dynamic uses
+  // the ticket counter): greedy largest-cost-first bin packing onto one bin
+  // per CTA, cost = bytes moved + a fixed per-tile charge.
+  static const bool dyn = [] {
+    const char* e = std::getenv("TRIMS_TILE_SCHED");
+    return e && std::string(e) == "dynamic";
+  }();
+  if (!dyn) {
+    const uint32_t grid = uint32_t(std::max(1, sm_count)) * ring_cfg().ctas_per_sm;
+    auto schedule = [&](std::vector<Tile>& table, std::vector<Group>& gs, std::vector<uint32_t>& bins) {
+      for (Group& g : gs) {
+        if (g.kind != 1 || g.end <= g.begin) continue;
+        schedule_bins(table, g, grid, bins, uint32_t(table.size() * (sizeof(Tile) / 4)));
+      }
+    };
+    for (auto& ch : p.chunks) schedule(p.tiles, ch.groups, p.bins);
+    schedule(p.tiles_by_kernel, p.groups, p.bins_k);
+  }
   return p;
 }
 
@@ -982,9 +1128,15 @@ uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, co
         const char* e = std::getenv("TRIMS_TILE_SCHED");
         return !(e && std::string(e) == "static");
       }();
-      unsigned int* slot = dynamic ? side->sched + 2 * (side->sched_next++ % kSchedSlots) : nullptr;
-      fn<<<std::min<uint32_t>(n, sm_count * rc.ctas_per_sm), kTmaThreads, smem, st>>>(
-          t, n, src, dst, d_sums, rc.stages, rc.stage_alloc(), slot);
+      if (g.nbins) {  // static schedule: one CTA per bin (+ dynamic tail)
+        const uint32_t* bins = reinterpret_cast<const uint32_t*>(d_tiles) + g.bin_base;
+        unsigned int* slot = g.tail ? side->sched + 2 * (side->sched_next++ % kSchedSlots) : nullptr;
+        fn<<<g.nbins, kTmaThreads, smem, st>>>(t, n, src, dst, d_sums, rc.stages, rc.stage_alloc(), slot, bins);
+      } else {
+        unsigned int* slot = dynamic ? side->sched + 2 * (side->sched_next++ % kSchedSlots) : nullptr;
+        fn<<<std::min<uint32_t>(n, sm_count * rc.ctas_per_sm), kTmaThreads, smem, st>>>(
+            t, n, src, dst, d_sums, rc.stages, rc.stage_alloc(), slot, nullptr);
+      }
     } else {
       TransformFn fn = pair_kernel(g.sdt, g.ddt);
       if (!fn) raise(Errc::InvalidArgument, "unsupported dtype pair in plan");

@@ -14,9 +14,21 @@
 
 namespace trims::ingest {
 
+// TRIMS block checksum term of resident word w at global word index g
+// (oracle/trims_oracle.h: tro_block_checksum): w * K(g) mod 2^64 with an odd
+// per-position key, so every single-word change moves the sum. Four 32-bit
+// IMADs + three key ops per word on the GPU; the region checksum is the sum of
+// its words' terms (additive over disjoint ranges).
+__host__ __device__ __forceinline__ uint64_t checksum_term(uint64_t w, uint64_t g) {
+  const uint32_t t = uint32_t(g) * 0x9e3779b1u;
+  const uint32_t klo = (t ^ (t >> 16)) | 1u, khi = t * 0xc2b2ae3du;
+  const uint32_t lo = uint32_t(w), hi = uint32_t(w >> 32);
+  return uint64_t(lo) * klo + (uint64_t(lo * khi + hi * klo) << 32);
+}
+
 enum Op : uint8_t { OP_HASH = 0, OP_CVT = 1, OP_PERM = 2, OP_END = 0xff };
 
-// 40 bytes. dst_off/dst_bytes are multiples of 8 so every tile owns whole
+// 48 bytes. dst_off/dst_bytes are multiples of 8 so every tile owns whole
 // checksum words; the last tile of a tensor extends over its trailing pad.
 struct Tile {
   uint64_t src_off;    // byte offset in the staged raw blob
@@ -26,14 +38,22 @@ struct Tile {
   uint32_t tensor;     // checksum bucket (resident tensor index; ntensors = leading pad)
   uint8_t op, sdt, ddt, pad_;  // pad_ = 1: slice too large for the TMA ring (direct-gather kernel)
   uint32_t C, RS;      // OP_PERM geometry: n_elem / (C*RS) k-slices
+  uint32_t rows;       // OP_PERM: resident rows (k, rs) in the tile = n_elem / C
+  uint32_t rs_magic;   // OP_PERM: ceil(2^32 / RS), so row / RS = umulhi(row, rs_magic)
 };
-static_assert(sizeof(Tile) == 40, "tile layout");
+static_assert(sizeof(Tile) == 48, "tile layout");
 
 // A contiguous tile range handled by one kernel: kind 0 hash, 1 TMA ring, 2 gather.
 struct Group {
   uint32_t begin, end;
   uint8_t kind, sdt, ddt;
   uint8_t smem;  // a direct-path group holding smem-staged OP_PERM tiles
+  // TMA groups: static schedule. The group's tiles are stored bin-major (one
+  // bin per CTA, balanced on the host); bin b is tiles [bins[b], bins[b+1])
+  // of the group, bins = (const uint32_t*)table + bin_base. nbins = 0: none.
+  // The last `tail` tiles of the group (after the bins) are handed out
+  // dynamically by a ticket counter once a CTA's bin is done.
+  uint32_t bin_base{0}, nbins{0}, tail{0};
 };
 
 struct TilePlan {
@@ -51,6 +71,9 @@ struct TilePlan {
   // HBM-resident transform.
   std::vector<Tile> tiles_by_kernel;
   std::vector<Group> groups;
+  // Bin offsets of the static schedules, stored right after each tile table
+  // on the device (Group::bin_base counts u32 words from the table start).
+  std::vector<uint32_t> bins, bins_k;
   uint32_t buckets{0};     // checksum buckets (ntensors + 1)
   bool identity{false};    // resident == source bytes: tiles only hash
   bool has_perm{false};
@@ -59,8 +82,9 @@ struct TilePlan {
 };
 
 // src: the artifact manifest; dst: resident_manifest(src, plan).
+// sm_count sizes the static schedule of the TMA groups (one bin per CTA).
 TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool identity,
-                     uint64_t chunk_bytes = 16ull << 20);
+                     uint64_t chunk_bytes = 16ull << 20, int sm_count = 148);
 
 // Launches one persistent kernel per group over `d_tiles` (device copy of the
 // table the groups index). Per-bucket checksums accumulate atomically into

@@ -57,9 +57,11 @@ def full(rep, tag, name):
         kernels.append(k)
     doc = {"source": os.path.relpath(rep, ROOT), "command": "see scripts/gpu_round.sh (ncu --set full)",
            "kernels": kernels,
-           "step": {"launches": len(kernels),
-                    "duration_us": sum(k["gpu__time_duration.sum"] for k in kernels),
-                    "dram_bytes": sum(k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"] for k in kernels)}}
+           # one transform step = one launch: per-launch means over the captured launches
+           "step": {"launches_captured": len(kernels),
+                    "duration_us": sum(k["gpu__time_duration.sum"] for k in kernels) / max(1, len(kernels)),
+                    "dram_bytes": sum(k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"] for k in kernels)
+                    / max(1, len(kernels))}}
     path = os.path.join(ROOT, "profiles", f"{tag}_ncu_{name}.json")
     json.dump(doc, open(path, "w"), indent=1)
     print("wrote", path)

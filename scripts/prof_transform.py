@@ -19,6 +19,18 @@ d_src = torch.from_numpy(blob).cuda()
 d_dst = torch.empty(plan.resident_bytes, dtype=torch.uint8, device="cuda")
 d_sums = torch.zeros(plan.buckets, dtype=torch.int64, device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+flush_r = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
+flush_mode = os.environ.get("PROF_FLUSH", "writeread")  # write | writeread | none
+
+
+def flush_l2():
+    # write 256 MiB (evicts everything), then read another 256 MiB so the
+    # dirty lines are written back before the timed region starts
+    if flush_mode != "none":
+        flush.zero_()
+    if flush_mode == "writeread":
+        flush_r.view(torch.int64).sum()
+
 s = torch.cuda.current_stream()
 for i in range(reps):
     d_sums.zero_()
@@ -26,14 +38,15 @@ for i in range(reps):
 torch.cuda.synchronize()
 times = []
 for i in range(int(os.environ.get("PROF_ITERS", "40"))):
-    flush.zero_()
+    flush_l2()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     plan.transform(d_src.data_ptr(), d_dst.data_ptr(), d_sums.data_ptr(), s.cuda_stream)
     e1.record()
     torch.cuda.synchronize()
     times.append(e0.elapsed_time(e1))
-ms = sorted(times)[len(times) // 2]  # median
-print(json.dumps({"arch": arch, "flags": flags, "tiles": plan.tiles, "ms": round(ms, 4),
+# event ticks are ~2 us on this box: report the mean (quantisation averages out)
+ms = sum(times) / len(times)
+print(json.dumps({"arch": arch, "flags": flags, "flush": flush_mode, "tiles": plan.tiles, "ms": round(ms, 4), "ms_median": round(sorted(times)[len(times) // 2], 4),
                   "GBps_algo": round((plan.read_bytes + plan.write_bytes) / ms / 1e6, 1),
                   "GBps_src": round(plan.src_bytes / ms / 1e6, 1)}))
