@@ -126,15 +126,14 @@ std::shared_ptr<IngestPlan> Ingestor::compile(const fmt::Manifest& src, const fm
   const uint64_t chunk = std::max<uint64_t>(16ull << 20, src.blob_bytes / (events_.size() - 8) + 1);
   p->plan = ingest::build_tiles(p->src, p->dst, p->identity, chunk, sms_);
   if (!p->plan.tiles.empty()) {
-    // each table is followed by the bin offsets of its static schedules
-    auto upload = [](ingest::Tile** d, const std::vector<ingest::Tile>& t, const std::vector<uint32_t>& bins) {
-      const size_t tb = t.size() * sizeof(ingest::Tile), bb = bins.size() * sizeof(uint32_t);
-      TRIMS_CUDA(cudaMalloc(d, tb + bb));
-      TRIMS_CUDA(cudaMemcpy(*d, t.data(), tb, cudaMemcpyHostToDevice));
-      if (bb) TRIMS_CUDA(cudaMemcpy(reinterpret_cast<uint8_t*>(*d) + tb, bins.data(), bb, cudaMemcpyHostToDevice));
+    // the device images: scheduled groups' bins padded to a common stride
+    auto upload = [](ingest::Tile** d, const std::vector<ingest::Tile>& t) {
+      const size_t tb = std::max<size_t>(1, t.size()) * sizeof(ingest::Tile);
+      TRIMS_CUDA(cudaMalloc(d, tb));
+      if (!t.empty()) TRIMS_CUDA(cudaMemcpy(*d, t.data(), t.size() * sizeof(ingest::Tile), cudaMemcpyHostToDevice));
     };
-    upload(&p->d_tiles, p->plan.tiles, p->plan.bins);
-    upload(&p->d_tiles_k, p->plan.tiles_by_kernel, p->plan.bins_k);
+    upload(&p->d_tiles, p->plan.dev_tiles);
+    upload(&p->d_tiles_k, p->plan.dev_tiles_k);
   }
   return p;
 }

@@ -680,7 +680,8 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
                                                                     unsigned long long* __restrict__ sums,
                                                                     uint32_t stages, uint32_t stage_alloc,
                                                                     unsigned int* __restrict__ sched,
-                                                                    const uint32_t* __restrict__ bins) {
+                                                                    uint32_t ticket_base, uint32_t stride,
+                                                                    uint32_t tail0) {
   using ST = typename Bits<S>::T;
   constexpr int DS = esize<D>(), SS = esize<S>(), EPW = 8 / DS;
   constexpr uint32_t kC = kConsumerWarps * 32;  // consumer threads
@@ -712,39 +713,43 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
         ++round;
       }
     };
-    uint32_t tail0 = 0;
-    if (bins) {
-      // Static part: this CTA's bin, balanced on the host. Its descriptors are
-      // copied into shared memory by the whole warp (one round trip per
-      // kDescCap tiles), so issuing a tile never waits on a global load.
-      const uint32_t b0 = bins[blockIdx.x], b1 = bins[blockIdx.x + 1];
-      tail0 = bins[gridDim.x];
-      for (uint32_t base = b0; base < b1; base += kDescCap) {
-        const uint32_t cnt = min(kDescCap, b1 - base);
-        const uint4* g4 = reinterpret_cast<const uint4*>(tiles + base);
+    if (stride) {
+      // Static part: this CTA's bin (balanced on the host) sits at
+      // blockIdx.x * stride, padded with OP_END. Its descriptors are copied
+      // into shared memory by the whole warp in one round trip per kDescCap
+      // entries, so issuing a tile never waits on a global load.
+      const Tile* mine = tiles + size_t(blockIdx.x) * stride;
+      bool more = true;
+      for (uint32_t base = 0; more && base < stride; base += kDescCap) {
+        const uint32_t cnt = min(kDescCap, stride - base);
+        const uint4* g4 = reinterpret_cast<const uint4*>(mine + base);
         uint4* s4 = reinterpret_cast<uint4*>(descs);
         constexpr uint32_t kW = sizeof(Tile) / 16;
         for (uint32_t i = lane; i < cnt * kW; i += 32) s4[i] = g4[i];
         __syncwarp();
-        if (lane == 0)
-          for (uint32_t j = 0; j < cnt; ++j) push(descs[j]);
+        if (lane == 0) {
+          uint32_t j = 0;
+          for (; j < cnt && descs[j].op != OP_END; ++j) push(descs[j]);
+          more = j == cnt;
+        }
+        more = __shfl_sync(0xffffffffu, more, 0);
         __syncwarp();
       }
     }
     if (lane == 0) {
       if (sched && tail0 < ntiles) {
-        // Dynamic part: tiles [tail0, ntiles) handed out by a per-launch
-        // ticket counter, so CTAs that ran slow take fewer of them. The next
-        // ticket and its descriptor are fetched while the ring waits.
-        uint32_t ti = tail0 + atomicAdd(&sched[0], 1u);
+        // Dynamic part: tiles [tail0, ntiles) handed out by a ticket counter,
+        // so CTAs that ran slow take fewer of them. The next ticket and its
+        // descriptor are fetched while the ring waits.
+        uint32_t ti = tail0 + (atomicAdd(sched, 1u) - ticket_base);
         Tile next = ti < ntiles ? tiles[ti] : Tile{};
         while (ti < ntiles) {
           const Tile t = next;
-          ti = tail0 + atomicAdd(&sched[0], 1u);
+          ti = tail0 + (atomicAdd(sched, 1u) - ticket_base);
           if (ti < ntiles) next = tiles[ti];
           push(t);
         }
-      } else if (!bins) {  // no schedule at all: static round robin
+      } else if (!stride) {  // no schedule at all: static round robin
         for (uint32_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) push(tiles[ti]);
       }
       // end marker: consumers leave
@@ -755,21 +760,11 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
   } else {
     consume_tiles<S, D>(ring, full, empty, staged, dst, sums, stages, stage_alloc);
   }
-  __syncthreads();
-  if (sched && threadIdx.x == 0) {  // the last CTA re-arms the counter slot for the next launch
-    __threadfence();
-    if (atomicAdd(&sched[1], 1u) == gridDim.x - 1) {
-      sched[0] = 0;
-      sched[1] = 0;
-      __threadfence();
-    }
-  }
 }
-
 
 using TransformFn = void (*)(const Tile*, uint32_t, const uint8_t*, uint8_t*, unsigned long long*);
 using TmaFn = void (*)(const Tile*, uint32_t, const uint8_t*, uint8_t*, unsigned long long*, uint32_t, uint32_t,
-                       unsigned int*, const uint32_t*);
+                       unsigned int*, uint32_t, uint32_t, uint32_t);
 
 TmaFn pair_tma_kernel(int s, int d) {
   switch (s * 8 + d) {
@@ -855,10 +850,10 @@ bool supported_pair(fmt::DType s, fmt::DType d) {
 }
 
 // One group's tiles -> nb bins (LPT: largest cost first onto the least loaded
-// bin), written back bin-major in the group's range; appends nb+1 offsets
-// (relative to g.begin) to `bins`. Tiles keep source order inside a bin.
-void schedule_bins(std::vector<Tile>& table, Group& g, uint32_t grid, std::vector<uint32_t>& bins,
-                   uint32_t table_words) {
+// bin) plus a dynamic tail of the smallest tiles, written back in the group's
+// range as [bin 0 | bin 1 | ... | tail]; bin sizes go to `bin_sizes`. Tiles
+// keep source order inside a bin, the tail is largest first.
+void schedule_bins(std::vector<Tile>& table, Group& g, uint32_t grid, std::vector<uint32_t>& bin_sizes) {
   constexpr uint64_t kFixed = 8u << 10;  // per-tile charge in byte-equivalents
   const uint32_t n = g.end - g.begin, nb = std::min(n, grid);
   std::vector<uint32_t> order(n);
@@ -897,15 +892,44 @@ void schedule_bins(std::vector<Tile>& table, Group& g, uint32_t grid, std::vecto
   std::vector<Tile> out(n);
   std::vector<uint32_t> fill(start.begin(), start.end() - 1);
   for (uint32_t i = 0; i < n; ++i) out[fill[bin_of[i]]++] = table[g.begin + i];
-  // tail in largest-first order: the small ones fill the end
-  std::vector<uint32_t> tail_order;
-  for (uint32_t k = head; k < n; ++k) tail_order.push_back(order[k]);
-  for (uint32_t k = 0; k < tail_order.size(); ++k) out[start[nb] + k] = table[g.begin + tail_order[k]];
+  for (uint32_t k = head; k < n; ++k) out[start[nb] + (k - head)] = table[g.begin + order[k]];
   std::copy(out.begin(), out.end(), table.begin() + g.begin);
-  g.bin_base = table_words + uint32_t(bins.size());
   g.nbins = nb;
   g.tail = n - start[nb];
-  bins.insert(bins.end(), start.begin(), start.end() - 1);  // nb+1 offsets; bins[nb] = tail start
+  g.bin_first = uint32_t(bin_sizes.size());
+  for (uint32_t b = 0; b < nb; ++b) bin_sizes.push_back(start[b + 1] - start[b]);
+}
+
+// Device image of a tile table: every group's range in order; a scheduled
+// group's bins are padded with OP_END entries to a common stride, so CTA b
+// finds its bin at b * stride without a lookup (one global round trip to
+// fetch its descriptors), followed by the tail.
+std::vector<Tile> device_image(const std::vector<Tile>& table, std::vector<Group*> groups,
+                               const std::vector<uint32_t>& bin_sizes) {
+  std::vector<Tile> dev;
+  Tile pad{};
+  pad.op = OP_END;
+  for (Group* g : groups) {
+    g->dev_begin = uint32_t(dev.size());
+    if (!g->nbins) {
+      dev.insert(dev.end(), table.begin() + g->begin, table.begin() + g->end);
+      g->dev_count = g->end - g->begin;
+      continue;
+    }
+    uint32_t stride = 1;
+    for (uint32_t b = 0; b < g->nbins; ++b) stride = std::max(stride, bin_sizes[g->bin_first + b] + 1);
+    g->stride = stride;
+    uint32_t at = g->begin;
+    for (uint32_t b = 0; b < g->nbins; ++b) {
+      const uint32_t sz = bin_sizes[g->bin_first + b];
+      dev.insert(dev.end(), table.begin() + at, table.begin() + at + sz);
+      dev.insert(dev.end(), stride - sz, pad);
+      at += sz;
+    }
+    dev.insert(dev.end(), table.begin() + at, table.begin() + g->end);  // tail
+    g->dev_count = uint32_t(dev.size()) - g->dev_begin;
+  }
+  return dev;
 }
 
 }  // namespace
@@ -1079,17 +1103,20 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
     const char* e = std::getenv("TRIMS_TILE_SCHED");
     return e && std::string(e) == "dynamic";
   }();
-  if (!dyn) {
-    const uint32_t grid = uint32_t(std::max(1, sm_count)) * ring_cfg().ctas_per_sm;
-    auto schedule = [&](std::vector<Tile>& table, std::vector<Group>& gs, std::vector<uint32_t>& bins) {
-      for (Group& g : gs) {
-        if (g.kind != 1 || g.end <= g.begin) continue;
-        schedule_bins(table, g, grid, bins, uint32_t(table.size() * (sizeof(Tile) / 4)));
-      }
-    };
-    for (auto& ch : p.chunks) schedule(p.tiles, ch.groups, p.bins);
-    schedule(p.tiles_by_kernel, p.groups, p.bins_k);
+  const uint32_t grid = uint32_t(std::max(1, sm_count)) * ring_cfg().ctas_per_sm;
+  std::vector<uint32_t> sizes, sizes_k;
+  std::vector<Group*> gp, gp_k;
+  for (auto& ch : p.chunks)
+    for (Group& g : ch.groups) {
+      if (!dyn && g.kind == 1 && g.end > g.begin) schedule_bins(p.tiles, g, grid, sizes);
+      gp.push_back(&g);
+    }
+  for (Group& g : p.groups) {
+    if (!dyn && g.kind == 1 && g.end > g.begin) schedule_bins(p.tiles_by_kernel, g, grid, sizes_k);
+    gp_k.push_back(&g);
   }
+  p.dev_tiles = device_image(p.tiles, gp, sizes);
+  p.dev_tiles_k = device_image(p.tiles_by_kernel, gp_k, sizes_k);
   return p;
 }
 
@@ -1111,9 +1138,9 @@ uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, co
   }
   uint32_t launches = 0;
   for (const Group& g : groups) {
-    const uint32_t n = g.end - g.begin;
+    const uint32_t n = g.dev_count;
     if (!n) continue;
-    const Tile* t = d_tiles + g.begin;
+    const Tile* t = d_tiles + g.dev_begin;
     cudaStream_t st = fork && g.kind == 2 ? side->stream : stream;
     if (g.kind == 0) {
       hash_tiles_kernel<<<std::min<uint32_t>(n, sm_count * 8), kThreads, 0, st>>>(t, n, dst, d_sums);
@@ -1128,14 +1155,25 @@ uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, co
         const char* e = std::getenv("TRIMS_TILE_SCHED");
         return !(e && std::string(e) == "static");
       }();
+      // Ticket counters are never reset: a launch draws exactly (dynamic
+      // tiles + CTAs) tickets (every CTA ends on one failing draw), so the
+      // host advances the slot's base by that and passes it in.
+      auto take_slot = [&](uint32_t dyn_tiles, uint32_t ctas, unsigned int** slot, uint32_t* base) {
+        const uint32_t k = side->sched_next++ % kSchedSlots;
+        *slot = side->sched + 2 * k;
+        *base = side->sched_base[k];
+        side->sched_base[k] += dyn_tiles + ctas;
+      };
+      unsigned int* slot = nullptr;
+      uint32_t base = 0;
       if (g.nbins) {  // static schedule: one CTA per bin (+ dynamic tail)
-        const uint32_t* bins = reinterpret_cast<const uint32_t*>(d_tiles) + g.bin_base;
-        unsigned int* slot = g.tail ? side->sched + 2 * (side->sched_next++ % kSchedSlots) : nullptr;
-        fn<<<g.nbins, kTmaThreads, smem, st>>>(t, n, src, dst, d_sums, rc.stages, rc.stage_alloc(), slot, bins);
+        if (g.tail) take_slot(g.tail, g.nbins, &slot, &base);
+        fn<<<g.nbins, kTmaThreads, smem, st>>>(t, n, src, dst, d_sums, rc.stages, rc.stage_alloc(), slot, base,
+                                               g.stride, g.nbins * g.stride);
       } else {
-        unsigned int* slot = dynamic ? side->sched + 2 * (side->sched_next++ % kSchedSlots) : nullptr;
-        fn<<<std::min<uint32_t>(n, sm_count * rc.ctas_per_sm), kTmaThreads, smem, st>>>(
-            t, n, src, dst, d_sums, rc.stages, rc.stage_alloc(), slot, nullptr);
+        const uint32_t ctas = std::min<uint32_t>(n, sm_count * rc.ctas_per_sm);
+        if (dynamic) take_slot(n, ctas, &slot, &base);
+        fn<<<ctas, kTmaThreads, smem, st>>>(t, n, src, dst, d_sums, rc.stages, rc.stage_alloc(), slot, base, 0u, 0u);
       }
     } else {
       TransformFn fn = pair_kernel(g.sdt, g.ddt);
@@ -1163,8 +1201,8 @@ uint32_t launch_pull(const Tile* d_tiles, const std::vector<Group>& groups, cons
     const uint32_t n = g.end - g.begin;
     if (!n) continue;
     if (g.kind != 0) raise(Errc::InvalidArgument, "peer pull needs an identity (hash-only) plan");
-    pull_tiles_kernel<<<std::min<uint32_t>(n, sm_count * 8), kThreads, 0, stream>>>(d_tiles + g.begin, n, src, dst,
-                                                                                    d_sums);
+    pull_tiles_kernel<<<std::min<uint32_t>(n, sm_count * 8), kThreads, 0, stream>>>(d_tiles + g.dev_begin, n, src,
+                                                                                    dst, d_sums);
     TRIMS_CUDA(cudaGetLastError());
     ++launches;
   }

@@ -49,11 +49,13 @@ struct Group {
   uint8_t kind, sdt, ddt;
   uint8_t smem;  // a direct-path group holding smem-staged OP_PERM tiles
   // TMA groups: static schedule. The group's tiles are stored bin-major (one
-  // bin per CTA, balanced on the host); bin b is tiles [bins[b], bins[b+1])
-  // of the group, bins = (const uint32_t*)table + bin_base. nbins = 0: none.
-  // The last `tail` tiles of the group (after the bins) are handed out
-  // dynamically by a ticket counter once a CTA's bin is done.
-  uint32_t bin_base{0}, nbins{0}, tail{0};
+  // bin per CTA, balanced on the host; nbins = 0: none), then the `tail`
+  // smallest tiles, handed out dynamically by a ticket counter once a CTA's
+  // bin is done. bin_first indexes the plan's bin sizes.
+  uint32_t nbins{0}, tail{0}, bin_first{0};
+  // Where the group lives in the device image of its table (bins padded to
+  // `stride` entries each, see device_image in ingest.cu).
+  uint32_t dev_begin{0}, dev_count{0}, stride{0};
 };
 
 struct TilePlan {
@@ -71,9 +73,8 @@ struct TilePlan {
   // HBM-resident transform.
   std::vector<Tile> tiles_by_kernel;
   std::vector<Group> groups;
-  // Bin offsets of the static schedules, stored right after each tile table
-  // on the device (Group::bin_base counts u32 words from the table start).
-  std::vector<uint32_t> bins, bins_k;
+  // Device images of the two tables (what d_tiles / d_tiles_k hold).
+  std::vector<Tile> dev_tiles, dev_tiles_k;
   uint32_t buckets{0};     // checksum buckets (ntensors + 1)
   bool identity{false};    // resident == source bytes: tiles only hash
   bool has_perm{false};
@@ -97,8 +98,9 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
 struct SideStream {
   cudaStream_t stream{nullptr};
   cudaEvent_t fork{nullptr}, join{nullptr};
-  unsigned int* sched{nullptr};  // kSchedSlots x {next ticket, CTAs done}
+  unsigned int* sched{nullptr};  // kSchedSlots x {ticket counter, unused}
   uint32_t sched_next{0};
+  uint32_t sched_base[256]{};    // per slot: the counter value the next launch starts from
 };
 inline constexpr uint32_t kSchedSlots = 256;
 uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, const uint8_t* src, uint8_t* dst,
