@@ -24,7 +24,7 @@ using namespace trims::sm100;
 
 namespace {
 
-constexpr int BM = 128, BK = 64, kThreads = 256;
+constexpr int BM = 128, BK = 64, kThreads = 256, kMaxSplits = 4;
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
@@ -34,21 +34,40 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 __device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
 
+// Shared-memory plan of one CTA: the TMA ring, then the epilogue operands
+// (residual tile, folded-BN scale and bias) prefetched during the mainloop.
+template <int BN, int STAGES>
+struct Smem {
+  static constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t RES_LD = BN + 8;  // bf16 elements per residual row (+16 B: spreads banks)
+  static constexpr uint32_t RING = STAGES * STAGE_BYTES;
+  static constexpr uint32_t RES = RING, RES_BYTES = BM * RES_LD * 2;
+  static constexpr uint32_t SCALE = RES + RES_BYTES, BIAS = SCALE + BN * 4;
+  static constexpr uint32_t TOTAL = BIAS + BN * 4 + 1024;  // + 1 KiB realignment slack
+};
+
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, uint16_t* D,
                    int M, int N, int K, int ldd, const float* __restrict__ scale, const float* __restrict__ bias,
-                   const uint16_t* __restrict__ res, int ldr, int relu) {
-  constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
+                   const uint16_t* __restrict__ res, int ldr, int relu, float* __restrict__ ws,
+                   unsigned int* __restrict__ ctr, int kper) {
+  using L = Smem<BN, STAGES>;
   constexpr uint32_t TMEM_COLS = BN;  // 64 / 128 / 256: powers of two >= 32
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], accum_full;
   __shared__ uint32_t tmem_base;
+  __shared__ int last_split;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint16_t* s_res = reinterpret_cast<uint16_t*>(smem + L::RES);
+  float* s_scale = reinterpret_cast<float*>(smem + L::SCALE);
+  float* s_bias = reinterpret_cast<float*>(smem + L::BIAS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int splits = gridDim.z, z = blockIdx.z;
   const int kblocks = (K + BK - 1) / BK;
+  const int kb0 = z * kper, kb1 = min(kblocks, kb0 + kper);  // this split's k-blocks
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -64,89 +83,165 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();  // the next layer's CTAs may start their prologue now
   const uint32_t tmem = tmem_base;
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const int s = kb % STAGES;
-        if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
-        uint8_t* sa = smem + s * STAGE_BYTES;
-        mbar_expect_tx(&full[s], STAGE_BYTES);
+      // Weights (B) do not depend on the previous kernel: the first stages'
+      // B tiles are requested before waiting on it, the activations after.
+      const int pre = min(STAGES, kb1 - kb0);
+      for (int i = 0; i < pre; ++i) {
+        uint8_t* sa = smem + i * L::STAGE_BYTES;
+        mbar_expect_tx(&full[i], L::STAGE_BYTES);
+        tma_load_2d(sa + L::A_BYTES, &tmB, (kb0 + i) * BK, n0, &full[i]);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) tma_load_2d(smem + i * L::STAGE_BYTES, &tmA, (kb0 + i) * BK, m0, &full[i]);
+      for (int kb = kb0 + pre, i = pre; kb < kb1; ++kb, ++i) {
+        const int s = i % STAGES;
+        mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
+        uint8_t* sa = smem + s * L::STAGE_BYTES;
+        mbar_expect_tx(&full[s], L::STAGE_BYTES);
         tma_load_2d(sa, &tmA, kb * BK, m0, &full[s]);
-        tma_load_2d(sa + A_BYTES, &tmB, kb * BK, n0, &full[s]);
+        tma_load_2d(sa + L::A_BYTES, &tmB, kb * BK, n0, &full[s]);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer
       constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const int s = kb % STAGES;
-        mbar_wait(&full[s], (kb / STAGES) & 1);
+      for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
+        const int s = i % STAGES;
+        mbar_wait(&full[s], (i / STAGES) & 1);
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + s * STAGE_BYTES), sb = sa + A_BYTES;
+        const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES), sb = sa + L::A_BYTES;
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)
-          mma_bf16(tmem, smem_desc_sw128(sa + k * 32), smem_desc_sw128(sb + k * 32), idesc, (kb | k) != 0);
+          mma_bf16(tmem, smem_desc_sw128(sa + k * 32), smem_desc_sw128(sb + k * 32), idesc, (i | k) != 0);
         mma_commit(&empty[s]);  // the stage is free once these MMAs have read it
       }
       mma_commit(&accum_full);
     }
-  } else if (warp >= 4) {  // ---- epilogue: TMEM -> registers -> bf16 global
-    mbar_wait(&accum_full, 0);
-    tc_fence_after();
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = m0 + q * 32 + lane;
-    uint16_t* drow = D + size_t(row) * ldd;
-    const uint16_t* rrow = res ? res + size_t(row) * ldr : nullptr;
-    const bool vec_ok = (ldd % 8 == 0) && (!res || ldr % 8 == 0);
+  } else if (warp < 4) {  // ---- epilogue operands -> smem, during the mainloop
+    const int t = threadIdx.x - 64;  // 64 threads
+#pragma unroll
+    for (int j = t; j < BN; j += 64) {
+      const int n = n0 + j;
+      s_scale[j] = (scale && n < N) ? __ldg(scale + n) : 1.f;
+      s_bias[j] = (bias && n < N) ? __ldg(bias + n) : 0.f;
+    }
+    pdl_wait();
+    if (res) {  // residual tile, 16-byte pieces (ldr % 8 == 0 checked on the host), 8 loads in flight
+      constexpr int PR = BN / 8, PIECES = BM * PR / 64, BATCH = PIECES < 8 ? PIECES : 8;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t r[16];
-      tmem_ld16(tmem + (uint32_t(q * 32) << 16) + uint32_t(c0), r);
-      const int n = n0 + c0;
-      if (row >= M || n >= N) continue;
-      float v[16];
+      for (int b = 0; b < PIECES; b += BATCH) {
+        uint4 v[BATCH];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int nj = n + j;
-        float x = __uint_as_float(r[j]);
-        if (nj < N) {
-          if (scale) x *= __ldg(scale + nj);
-          if (bias) x += __ldg(bias + nj);
-        }
-        v[j] = x;
-      }
-      if (vec_ok && n + 16 <= N) {
-        if (rrow) {
-          const uint4* rp = reinterpret_cast<const uint4*>(rrow + n);
-          uint4 a = rp[0], b = rp[1];
-          const uint32_t rw[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            v[2 * j] += bf16_lo(rw[j]);
-            v[2 * j + 1] += bf16_hi(rw[j]);
+        for (int u = 0; u < BATCH; ++u) {
+          const int i = t + (b + u) * 64, r = i / PR, c = (i - r * PR) * 8;
+          v[u] = make_uint4(0, 0, 0, 0);
+          if (m0 + r < M && n0 + c + 8 <= N) {
+            v[u] = *reinterpret_cast<const uint4*>(res + size_t(m0 + r) * ldr + n0 + c);
+          } else if (m0 + r < M) {
+            for (int q = 0; q < 8 && n0 + c + q < N; ++q)
+              reinterpret_cast<uint16_t*>(&v[u])[q] = res[size_t(m0 + r) * ldr + n0 + c + q];
           }
         }
+#pragma unroll
+        for (int u = 0; u < BATCH; ++u) {
+          const int i = t + (b + u) * 64, r = i / PR, c = (i - r * PR) * 8;
+          *reinterpret_cast<uint4*>(s_res + r * L::RES_LD + c) = v[u];
+        }
+      }
+    }
+    asm volatile("bar.arrive 1, 192;" ::: "memory");  // operands ready for warps 4-7
+  } else {  // ---- epilogue: TMEM -> registers -> bf16 global
+    pdl_wait();
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int rl = q * 32 + lane, row = m0 + rl;
+    const uint32_t tq = tmem + (uint32_t(q * 32) << 16);
+    mbar_wait(&accum_full, 0);
+    tc_fence_after();
+    bool finish = true;
+    float* part = nullptr;
+    if (splits > 1) {
+      // Deterministic split-K: every split stores its fp32 partial tile
+      // (column-major, so a warp's stores are coalesced); the last split to
+      // arrive sums all partials in split order and runs the epilogue.
+      const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+      part = ws + size_t(tile) * splits * BN * BM;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(tq + uint32_t(c0), r);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) __stcg(part + (size_t(z) * BN + c0 + j) * BM + rl, __uint_as_float(r[j]));
+      }
+      __threadfence();
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (threadIdx.x == 128) last_split = atomicAdd(&ctr[tile], 1u) == unsigned(splits - 1);
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      finish = last_split;
+      if (finish) {
+        __threadfence();
+        if (threadIdx.x == 128) ctr[tile] = 0;  // re-armed for the next launch
+      }
+    }
+    asm volatile("bar.sync 1, 192;" ::: "memory");  // residual / scale / bias in smem
+    if (finish) {
+      uint16_t* drow = D + size_t(row) * ldd;
+      const bool vec_ok = (ldd % 8 == 0);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        if (splits > 1) {  // every split's 16 values in flight, then summed in split order
+          float pv[kMaxSplits][16];
+#pragma unroll
+          for (int zz = 0; zz < kMaxSplits; ++zz)
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              pv[zz][j] = zz < splits ? __ldcg(part + (size_t(zz) * BN + c0 + j) * BM + rl) : 0.f;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            v[j] = pv[0][j];
+#pragma unroll
+            for (int zz = 1; zz < kMaxSplits; ++zz)
+              if (zz < splits) v[j] += pv[zz][j];
+          }
+        } else {
+          uint32_t r[16];
+          tmem_ld16(tq + uint32_t(c0), r);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+        }
+        const int n = n0 + c0;
+        if (row >= M || n >= N) continue;
+        const uint4* rp = reinterpret_cast<const uint4*>(s_res + rl * L::RES_LD + c0);
+        const uint4 ra = res ? rp[0] : make_uint4(0, 0, 0, 0), rb = res ? rp[1] : make_uint4(0, 0, 0, 0);
+        const uint32_t rw[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
         uint32_t o[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          float a = v[2 * j], b = v[2 * j + 1];
+          float a = v[2 * j] * s_scale[c0 + 2 * j] + s_bias[c0 + 2 * j];
+          float b = v[2 * j + 1] * s_scale[c0 + 2 * j + 1] + s_bias[c0 + 2 * j + 1];
+          if (res) {
+            a += bf16_lo(rw[j]);
+            b += bf16_hi(rw[j]);
+          }
           if (relu) {
             a = fmaxf(a, 0.f);
             b = fmaxf(b, 0.f);
           }
           o[j] = pack_bf16x2(a, b);
         }
-        uint4* dp = reinterpret_cast<uint4*>(drow + n);
-        dp[0] = make_uint4(o[0], o[1], o[2], o[3]);
-        dp[1] = make_uint4(o[4], o[5], o[6], o[7]);
-      } else {
-        for (int j = 0; j < 16 && n + j < N; ++j) {
-          float x = v[j];
-          if (rrow) x += __uint_as_float(uint32_t(rrow[n + j]) << 16);
-          if (relu) x = fmaxf(x, 0.f);
-          drow[n + j] = uint16_t(pack_bf16x2(x, 0.f) & 0xffffu);
+        if (vec_ok && n + 16 <= N) {
+          uint4* dp = reinterpret_cast<uint4*>(drow + n);
+          dp[0] = make_uint4(o[0], o[1], o[2], o[3]);
+          dp[1] = make_uint4(o[4], o[5], o[6], o[7]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (n + j < N) drow[n + j] = uint16_t(o[j >> 1] >> (16 * (j & 1)));
         }
       }
     }
@@ -174,7 +269,8 @@ EncodeTiled encode_fn() {
 
 template <int BN, int STAGES>
 void run_bn(const Prepared& p, cudaStream_t stream) {
-  constexpr size_t smem = size_t(STAGES) * (BM * BK * 2 + BN * BK * 2) + 1024;
+  constexpr size_t smem = Smem<BN, STAGES>::TOTAL;
+  static_assert(smem <= 227 * 1024, "GEMM shared memory");
   static bool attr = false;
   if (!attr) {
     TRIMS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -182,11 +278,11 @@ void run_bn(const Prepared& p, cudaStream_t stream) {
     attr = true;
   }
   const Epilogue& e = p.e;
-  dim3 grid(unsigned((p.M + BM - 1) / BM), unsigned((p.N + BN - 1) / BN));
-  gemm_tc_kernel<BN, STAGES><<<grid, kThreads, smem, stream>>>(p.ta, p.tb, e.out, int(p.M), int(p.N), int(p.K),
-                                                                int(e.ldo), e.scale, e.bias, e.residual, int(e.ldr),
-                                                                e.relu ? 1 : 0);
-  TRIMS_CUDA(cudaGetLastError());
+  const int kblocks = int((p.K + BK - 1) / BK);
+  const int kper = (kblocks + p.splits - 1) / p.splits;
+  dim3 grid(unsigned((p.M + BM - 1) / BM), unsigned((p.N + BN - 1) / BN), unsigned(p.splits));
+  launch_pdl(gemm_tc_kernel<BN, STAGES>, grid, dim3(kThreads), smem, stream, p.ta, p.tb, e.out, int(p.M), int(p.N),
+             int(p.K), int(e.ldo), e.scale, e.bias, e.residual, int(e.ldr), e.relu ? 1 : 0, p.ws, p.ctr, kper);
 }
 
 }  // namespace
@@ -224,6 +320,8 @@ Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn) 
     bn = pick_bn(A.rows, B.rows, sms);
   }
   if (bn != 64 && bn != 128 && bn != 256) raise(Errc::InvalidArgument, "BN must be 64, 128 or 256");
+  if (e.residual && (e.ldr % 8 || reinterpret_cast<uintptr_t>(e.residual) % 16))
+    raise(Errc::InvalidArgument, "GEMM residual rows must be 16-byte aligned");
   Prepared p;
   p.ta = make_tmap(A.ptr, A.rows, A.k, A.ld, BM);
   p.tb = make_tmap(B.ptr, B.rows, B.k, B.ld, uint32_t(bn));
@@ -236,11 +334,31 @@ Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn) 
 }
 
 void run(const Prepared& p, cudaStream_t stream) {
+  if (p.splits > 1 && (!p.ws || !p.ctr)) raise(Errc::InvalidArgument, "split-K GEMM without a workspace");
   switch (p.bn) {
     case 64: run_bn<64, 6>(p, stream); break;
     case 128: run_bn<128, 5>(p, stream); break;
-    default: run_bn<256, 4>(p, stream); break;
+    default: run_bn<256, 3>(p, stream); break;
   }
+}
+
+int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms) {
+  // Split K only when the output tiles leave most SMs idle and each split
+  // keeps >= 8 k-blocks; the last split reduces all partials, so at most 4.
+  const uint64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn), kb = (K + BK - 1) / BK;
+  int s = 1;
+  while (s < 4 && tiles * uint64_t(s * 2) <= uint64_t(sms) && kb / uint64_t(s * 2) >= 8) s *= 2;
+  return s;
+}
+
+uint64_t workspace_bytes(const Prepared& p) {
+  if (p.splits <= 1) return 0;
+  const uint64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + p.bn - 1) / p.bn);
+  return tiles * uint64_t(p.splits) * uint64_t(p.bn) * BM * 4;
+}
+
+uint64_t counter_count(const Prepared& p) {
+  return p.splits <= 1 ? 0 : ((p.M + BM - 1) / BM) * ((p.N + p.bn - 1) / p.bn);
 }
 
 void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn) {

@@ -36,9 +36,18 @@ struct Prepared {
   uint64_t M{0}, N{0}, K{0};
   int bn{128};
   Epilogue e;
+  // Split-K (grid.z = splits): fp32 partial tiles in `ws`, one arrival
+  // counter per output tile in `ctr` (zeroed once; the last split re-arms it).
+  int splits{1};
+  float* ws{nullptr};
+  unsigned int* ctr{nullptr};
 };
 Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn = 0);
 void run(const Prepared& p, cudaStream_t stream);
+// Split count for a GEMM shape on `sms` SMs, and the workspace it needs.
+int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms);
+uint64_t workspace_bytes(const Prepared& p);
+uint64_t counter_count(const Prepared& p);
 // D = epi(A . B^T); bn = 0 picks the tile width.
 void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn = 0);
 

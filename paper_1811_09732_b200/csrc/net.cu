@@ -75,6 +75,15 @@ std::string bn_name(const std::string& conv) {
   return b;
 }
 
+// TRIMS_SPLITK=0 turns split-K off (A/B switch).
+bool splitk_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TRIMS_SPLITK");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
 }  // namespace
 
 uint8_t* Net::alloc(uint64_t bytes) {
@@ -142,6 +151,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
   }
   uint16_t* col = col_elems ? reinterpret_cast<uint16_t*>(alloc(col_elems * 2)) : nullptr;
   Act cur;
+  std::vector<std::shared_ptr<gemm::Prepared>> gemms;  // split-K workspace is shared (layers run in order)
 
   for (size_t li = 0; li < layers.size(); ++li) {
     const LayerSpec& l = layers[li];
@@ -211,6 +221,8 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
                           {wpad ? wpad : reinterpret_cast<const uint16_t*>(uintptr_t(256)), uint64_t(kg),
                            uint64_t(kp), uint64_t(kp)},
                           e));
+        if (splitk_enabled()) prep->splits = gemm::pick_splits(M, uint64_t(kg), uint64_t(kp), prep->bn, sms_);
+        gemms.push_back(prep);
         const uint64_t b_off = w_off + uint64_t(gi) * kg * rsc * 2;
         const bool do_params = first_group && bind_params;
         auto rebind = [=](cudaStream_t s) {
@@ -305,6 +317,21 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
     }
   }
   if (!logits_) raise(Errc::InvalidArgument, "architecture has no fc output");
+  uint64_t ws_need = 0, ctr_need = 0;
+  for (const auto& g : gemms) {
+    ws_need = std::max(ws_need, gemm::workspace_bytes(*g));
+    ctr_need = std::max(ctr_need, gemm::counter_count(*g));
+  }
+  if (ws_need) {
+    float* ws = reinterpret_cast<float*>(alloc(ws_need));
+    auto* ctr = reinterpret_cast<unsigned int*>(alloc(ctr_need * 4));
+    TRIMS_CUDA(cudaMemset(ctr, 0, ctr_need * 4));
+    for (const auto& g : gemms)
+      if (g->splits > 1) {
+        g->ws = ws;
+        g->ctr = ctr;
+      }
+  }
   for (const auto& s : steps_) launches_ += s->launches;
   TRIMS_CUDA(cudaStreamCreateWithFlags(&capture_stream_, cudaStreamNonBlocking));
   rebind(weights);

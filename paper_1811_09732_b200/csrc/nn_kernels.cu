@@ -22,6 +22,8 @@ __device__ __forceinline__ uint16_t to_bf(float x) {
 inline unsigned blocks(uint64_t n, unsigned t = 256) { return unsigned(std::min<uint64_t>((n + t - 1) / t, 1u << 20)); }
 
 __global__ void input_prep_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int N, int C, int H, int W) {
+  pdl_wait();  // reads the previous layer's output / writes shared scratch
+  pdl_trigger();
   const uint64_t total = uint64_t(N) * H * W * C;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
     const int c = int(i % C);
@@ -37,6 +39,8 @@ __global__ void input_prep_kernel(const float* __restrict__ in, uint16_t* __rest
 // A[m, (r*S + s)*Cg + c] = in[n, p*stride - pad + r, q*stride - pad + s, c_off + c]; zero outside / in padding cols.
 __global__ void im2col_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ A, int N, int H, int W, int Ctot,
                               int c_off, int Cg, int R, int S, int stride, int pad, int P, int Q, int Kp) {
+  pdl_wait();  // reads the previous layer's output / writes shared scratch
+  pdl_trigger();
   const int RSC = R * S * Cg;
   const bool vec = (Cg % 8 == 0) && (Ctot % 8 == 0) && (c_off % 8 == 0) && (Kp % 8 == 0);
   const uint64_t M = uint64_t(N) * P * Q;
@@ -58,25 +62,32 @@ __global__ void im2col_kernel(const uint16_t* __restrict__ in, uint16_t* __restr
       *reinterpret_cast<uint4*>(A + m * Kp + col) = v;
     }
   } else {
-    const uint64_t total = M * Kp;
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-      const int col = int(i % Kp);
-      const uint64_t m = i / Kp;
-      uint16_t v = 0;
-      if (col < RSC) {
-        const int c = col % Cg, rs = col / Cg, s = rs % S, r = rs / S;
-        const int q = int(m % Q), p = int((m / Q) % P), n = int(m / (uint64_t(P) * Q));
-        const int y = p * stride - pad + r, x = q * stride - pad + s;
-        if (y >= 0 && y < H && x >= 0 && x < W) v = in[((uint64_t(n) * H + y) * W + x) * Ctot + c_off + c];
+    // Narrow channel groups (conv1: Cg = 3): one thread per (row m, filter
+    // row r) copies the S*Cg contiguous NHWC elements of that tap row (zero
+    // outside the image); the r = R-1 thread also zeroes the K padding.
+    const uint32_t rows = uint32_t(M) * R, SC = S * Cg;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
+      const uint32_t m = i / R, r = i - m * R;
+      const uint32_t q = m % Q, pn = m / Q, p = pn % P, n = pn / P;
+      const int y = int(p) * stride - pad + int(r), x0 = int(q) * stride - pad;
+      uint16_t* dst = A + uint64_t(m) * Kp + r * SC;
+      const bool yok = y >= 0 && y < H;
+      const uint16_t* srow = in + (uint64_t(n) * H + (yok ? y : 0)) * W * Ctot + c_off;
+      for (int s = 0; s < S; ++s) {
+        const int x = x0 + s;
+        const bool ok = yok && x >= 0 && x < W;
+        for (int c = 0; c < Cg; ++c) dst[s * Cg + c] = ok ? srow[uint64_t(x) * Ctot + c] : uint16_t(0);
       }
-      A[i] = v;
+      if (r == uint32_t(R - 1))
+        for (int c = RSC; c < Kp; ++c) A[uint64_t(m) * Kp + c] = 0;
     }
   }
 }
 
 __global__ void maxpool_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, int N, int H, int W, int C,
                                int k, int stride, int pad, int P, int Q) {
+  pdl_wait();  // reads the previous layer's output / writes shared scratch
+  pdl_trigger();
   const int C8 = C / 8;
   const uint64_t total = uint64_t(N) * P * Q * C8;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
@@ -112,6 +123,32 @@ __global__ void maxpool_kernel(const uint16_t* __restrict__ in, uint16_t* __rest
 }
 
 __global__ void avgpool_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, int N, int HW, int C) {
+  pdl_wait();  // reads the previous layer's output / writes shared scratch
+  pdl_trigger();
+  if (C % 8 == 0) {  // 8 channels per thread, 128-bit loads, 7 in flight
+    const uint32_t C8 = C / 8, total = uint32_t(N) * C8;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+      const uint32_t n = i / C8, c = (i - n * C8) * 8;
+      const uint16_t* base = in + uint64_t(n) * HW * C + c;
+      float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 7
+      for (int j = 0; j < HW; ++j) {
+        const uint4 v = *reinterpret_cast<const uint4*>(base + uint64_t(j) * C);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          s[2 * q] += bf(uint16_t(w[q] & 0xffff));
+          s[2 * q + 1] += bf(uint16_t(w[q] >> 16));
+        }
+      }
+      uint32_t o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        o[q] = uint32_t(to_bf(s[2 * q] / float(HW))) | (uint32_t(to_bf(s[2 * q + 1] / float(HW))) << 16);
+      *reinterpret_cast<uint4*>(out + uint64_t(n) * C + c) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    return;
+  }
   const uint64_t total = uint64_t(N) * C;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
     const int c = int(i % C);
@@ -123,6 +160,8 @@ __global__ void avgpool_kernel(const uint16_t* __restrict__ in, uint16_t* __rest
 }
 
 __global__ void flatten_nchw_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, int N, int HW, int C) {
+  pdl_wait();  // reads the previous layer's output / writes shared scratch
+  pdl_trigger();
   const uint64_t total = uint64_t(N) * HW * C;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
     const int hw = int(i % HW);
@@ -140,6 +179,8 @@ __global__ void __launch_bounds__(256) gemv_kernel(const uint16_t* __restrict__ 
                                                    const uint16_t* __restrict__ Wt, int N, const float* __restrict__ bias,
                                                    int relu, uint16_t* __restrict__ out_bf, float* __restrict__ out_f32,
                                                    int ldo) {
+  pdl_wait();  // reads the previous layer's output / writes shared scratch
+  pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int n = warp; n < N; n += nwarps) {
@@ -147,6 +188,7 @@ __global__ void __launch_bounds__(256) gemv_kernel(const uint16_t* __restrict__ 
 #pragma unroll
     for (int m = 0; m < MB; ++m) acc[m] = 0.f;
     const uint16_t* wr = Wt + uint64_t(n) * K;
+#pragma unroll 4
     for (int k = lane * 8; k < K; k += 32 * 8) {
       const uint4 wv = __ldg(reinterpret_cast<const uint4*>(wr + k));
       const uint32_t w[4] = {wv.x, wv.y, wv.z, wv.w};
@@ -188,6 +230,8 @@ __global__ void bn_fold_kernel(const uint16_t* gamma, const uint16_t* beta, cons
 }
 
 __global__ void bf16_to_f32_kernel(const uint16_t* in, float* out, int n) {
+  pdl_wait();  // reads the previous layer's output / writes shared scratch
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = bf(in[i]);
 }
@@ -202,6 +246,8 @@ __global__ void pad_rows_kernel(const uint16_t* in, int rows, int k, uint16_t* o
 }
 
 __global__ void softmax_kernel(const float* in, float* out, int M, int N) {
+  pdl_wait();  // reads the previous layer's output / writes shared scratch
+  pdl_trigger();
   const int m = blockIdx.x;
   if (m >= M) return;
   __shared__ float red[32];
@@ -227,31 +273,31 @@ __global__ void softmax_kernel(const float* in, float* out, int M, int N) {
 }  // namespace
 
 void input_prep(const float* in, uint16_t* out, int N, int C, int H, int W, cudaStream_t s) {
-  input_prep_kernel<<<blocks(uint64_t(N) * C * H * W), 256, 0, s>>>(in, out, N, C, H, W);
+  launch_pdl(input_prep_kernel, dim3(blocks(uint64_t(N) * C * H * W)), dim3(256), 0, s, in, out, N, C, H, W);
   TRIMS_CUDA(cudaGetLastError());
 }
 
 void im2col(const uint16_t* in, uint16_t* A, int N, int H, int W, int Ctot, int c_off, int Cg, int R, int S, int stride,
             int pad, int P, int Q, int Kp, cudaStream_t s) {
-  const uint64_t work = uint64_t(N) * P * Q * ((Cg % 8 == 0 && Ctot % 8 == 0 && c_off % 8 == 0 && Kp % 8 == 0) ? Kp / 8 : Kp);
-  im2col_kernel<<<blocks(work), 256, 0, s>>>(in, A, N, H, W, Ctot, c_off, Cg, R, S, stride, pad, P, Q, Kp);
+  const uint64_t work = uint64_t(N) * P * Q * ((Cg % 8 == 0 && Ctot % 8 == 0 && c_off % 8 == 0 && Kp % 8 == 0) ? Kp / 8 : R);
+  launch_pdl(im2col_kernel, dim3(blocks(work)), dim3(256), 0, s, in, A, N, H, W, Ctot, c_off, Cg, R, S, stride, pad, P, Q, Kp);
   TRIMS_CUDA(cudaGetLastError());
 }
 
 void maxpool(const uint16_t* in, uint16_t* out, int N, int H, int W, int C, int k, int stride, int pad, int P, int Q,
              cudaStream_t s) {
   if (C % 8) raise(Errc::InvalidArgument, "maxpool needs C % 8 == 0");
-  maxpool_kernel<<<blocks(uint64_t(N) * P * Q * C / 8), 256, 0, s>>>(in, out, N, H, W, C, k, stride, pad, P, Q);
+  launch_pdl(maxpool_kernel, dim3(blocks(uint64_t(N) * P * Q * C / 8)), dim3(256), 0, s, in, out, N, H, W, C, k, stride, pad, P, Q);
   TRIMS_CUDA(cudaGetLastError());
 }
 
 void avgpool_global(const uint16_t* in, uint16_t* out, int N, int HW, int C, cudaStream_t s) {
-  avgpool_kernel<<<blocks(uint64_t(N) * C), 256, 0, s>>>(in, out, N, HW, C);
+  launch_pdl(avgpool_kernel, dim3(blocks(uint64_t(N) * C / (C % 8 ? 1 : 8), 64)), dim3(64), 0, s, in, out, N, HW, C);
   TRIMS_CUDA(cudaGetLastError());
 }
 
 void flatten_nchw(const uint16_t* in, uint16_t* out, int N, int HW, int C, cudaStream_t s) {
-  flatten_nchw_kernel<<<blocks(uint64_t(N) * HW * C), 256, 0, s>>>(in, out, N, HW, C);
+  launch_pdl(flatten_nchw_kernel, dim3(blocks(uint64_t(N) * HW * C)), dim3(256), 0, s, in, out, N, HW, C);
   TRIMS_CUDA(cudaGetLastError());
 }
 
@@ -259,31 +305,31 @@ void gemv(const uint16_t* x, int M, int K, const uint16_t* W, int N, const float
           float* out_f32, int ldo, int sms, cudaStream_t s) {
   if (K % 8) raise(Errc::InvalidArgument, "gemv needs K % 8 == 0");
   const unsigned grid = unsigned(std::min<int>((N + 7) / 8, sms * 8));
-  if (M <= 1) gemv_kernel<1><<<grid, 256, 0, s>>>(x, M, K, W, N, bias, relu, out_bf, out_f32, ldo);
-  else if (M <= 4) gemv_kernel<4><<<grid, 256, 0, s>>>(x, M, K, W, N, bias, relu, out_bf, out_f32, ldo);
-  else if (M <= 8) gemv_kernel<8><<<grid, 256, 0, s>>>(x, M, K, W, N, bias, relu, out_bf, out_f32, ldo);
+  if (M <= 1) launch_pdl(gemv_kernel<1>, dim3(grid), dim3(256), 0, s, x, M, K, W, N, bias, relu, out_bf, out_f32, ldo);
+  else if (M <= 4) launch_pdl(gemv_kernel<4>, dim3(grid), dim3(256), 0, s, x, M, K, W, N, bias, relu, out_bf, out_f32, ldo);
+  else if (M <= 8) launch_pdl(gemv_kernel<8>, dim3(grid), dim3(256), 0, s, x, M, K, W, N, bias, relu, out_bf, out_f32, ldo);
   else raise(Errc::InvalidArgument, "gemv is for M <= 8");
   TRIMS_CUDA(cudaGetLastError());
 }
 
 void bn_fold(const uint16_t* gamma, const uint16_t* beta, const uint16_t* mean, const uint16_t* var, float eps, int C,
              float* scale, float* shift, cudaStream_t s) {
-  bn_fold_kernel<<<(C + 255) / 256, 256, 0, s>>>(gamma, beta, mean, var, eps, C, scale, shift);
+  bn_fold_kernel<<<(C + 255) / 256, 256, 0, s>>>(gamma, beta, mean, var, eps, C, scale, shift);  // bind time: no PDL
   TRIMS_CUDA(cudaGetLastError());
 }
 
 void bf16_to_f32(const uint16_t* in, float* out, int n, cudaStream_t s) {
-  bf16_to_f32_kernel<<<(n + 255) / 256, 256, 0, s>>>(in, out, n);
+  launch_pdl(bf16_to_f32_kernel, dim3((n + 255) / 256), dim3(256), 0, s, in, out, n);
   TRIMS_CUDA(cudaGetLastError());
 }
 
 void pad_rows(const uint16_t* in, int rows, int k, uint16_t* out, int kp, cudaStream_t s) {
-  pad_rows_kernel<<<blocks(uint64_t(rows) * kp), 256, 0, s>>>(in, rows, k, out, kp);
+  pad_rows_kernel<<<blocks(uint64_t(rows) * kp), 256, 0, s>>>(in, rows, k, out, kp);  // bind time: no PDL
   TRIMS_CUDA(cudaGetLastError());
 }
 
 void softmax(const float* in, float* out, int M, int N, cudaStream_t s) {
-  softmax_kernel<<<M, 256, 0, s>>>(in, out, M, N);
+  launch_pdl(softmax_kernel, dim3(M), dim3(256), 0, s, in, out, M, N);
   TRIMS_CUDA(cudaGetLastError());
 }
 
