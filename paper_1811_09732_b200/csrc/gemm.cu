@@ -24,7 +24,7 @@ using namespace trims::sm100;
 
 namespace {
 
-constexpr int BM = 128, BK = 64, kThreads = 256, kMaxSplits = 4;
+constexpr int BM = 128, BK = 64, kThreads = 256, kMaxSplits = 8;
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
@@ -50,14 +50,12 @@ template <int BN, int STAGES>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, uint16_t* D,
                    int M, int N, int K, int ldd, const float* __restrict__ scale, const float* __restrict__ bias,
-                   const uint16_t* __restrict__ res, int ldr, int relu, float* __restrict__ ws,
-                   unsigned int* __restrict__ ctr, int kper) {
+                   const uint16_t* __restrict__ res, int ldr, int relu, int kper, const ConvGeom cg) {
   using L = Smem<BN, STAGES>;
   constexpr uint32_t TMEM_COLS = BN;  // 64 / 128 / 256: powers of two >= 32
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], accum_full;
   __shared__ uint32_t tmem_base;
-  __shared__ int last_split;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint16_t* s_res = reinterpret_cast<uint16_t*>(smem + L::RES);
   float* s_scale = reinterpret_cast<float*>(smem + L::SCALE);
@@ -68,6 +66,71 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int splits = gridDim.z, z = blockIdx.z;
   const int kblocks = (K + BK - 1) / BK;
   const int kb0 = z * kper, kb1 = min(kblocks, kb0 + kper);  // this split's k-blocks
+  // Implicit conv: this tile = image ti, output rows [th*hbox, +hbox), cols [tw*wbox, +wbox).
+  int ti = 0, th = 0, tw = 0;
+  if (cg.impl) {
+    tw = blockIdx.x % cg.tiles_w;
+    th = (blockIdx.x / cg.tiles_w) % cg.tiles_h;
+    ti = blockIdx.x / (cg.tiles_w * cg.tiles_h);
+  }
+  const int wbox = 1 << cg.wbox_log2;
+  // Global output row of tile row rl, or -1 outside the output.
+  auto row_of = [&](int rl) -> int {
+    if (!cg.impl) return m0 + rl < M ? m0 + rl : -1;
+    const int h = th * cg.hbox + (rl >> cg.wbox_log2), w = tw * wbox + (rl & (wbox - 1));
+    return (h < cg.P && w < cg.Q) ? (ti * cg.P + h) * cg.Q + w : -1;
+  };
+  // Epilogue of tile columns [c_begin, c_end) for tile row rl: fetch(c0, v)
+  // yields the 16 fp32 accumulators of columns c0..c0+15; then scale, bias,
+  // residual (smem), ReLU, bf16, 32-byte stores.
+  auto store_cols = [&](int c_begin, int c_end, int rl, auto&& fetch) {
+    const int row = row_of(rl);
+    uint16_t* drow = D + size_t(row < 0 ? 0 : row) * ldd;
+    const bool vec_ok = (ldd % 8 == 0);
+#pragma unroll 1
+    for (int c0 = c_begin; c0 < c_end; c0 += 16) {
+      float v[16];
+      fetch(c0, v);
+      const int n = n0 + c0;
+      if (row < 0 || n >= N) continue;
+      const uint4* rp = reinterpret_cast<const uint4*>(s_res + rl * L::RES_LD + c0);
+      const uint4 ra = res ? rp[0] : make_uint4(0, 0, 0, 0), rb = res ? rp[1] : make_uint4(0, 0, 0, 0);
+      const uint32_t rw[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+      uint32_t o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float a = v[2 * j] * s_scale[c0 + 2 * j] + s_bias[c0 + 2 * j];
+        float b = v[2 * j + 1] * s_scale[c0 + 2 * j + 1] + s_bias[c0 + 2 * j + 1];
+        if (res) {
+          a += bf16_lo(rw[j]);
+          b += bf16_hi(rw[j]);
+        }
+        if (relu) {
+          a = fmaxf(a, 0.f);
+          b = fmaxf(b, 0.f);
+        }
+        o[j] = pack_bf16x2(a, b);
+      }
+      if (vec_ok && n + 16 <= N) {
+        uint4* dp = reinterpret_cast<uint4*>(drow + n);
+        dp[0] = make_uint4(o[0], o[1], o[2], o[3]);
+        dp[1] = make_uint4(o[4], o[5], o[6], o[7]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (n + j < N) drow[n + j] = uint16_t(o[j >> 1] >> (16 * (j & 1)));
+      }
+    }
+  };
+  auto load_a = [&](void* dst, int kb, uint64_t* bar) {
+    if (cg.impl) {
+      const int rs = kb / cg.cblocks, cb = kb - rs * cg.cblocks, r = rs / cg.S, s = rs - r * cg.S;
+      tma_load_4d(dst, &tmA, cb * BK, tw * wbox * cg.stride - cg.pad + s, th * cg.hbox * cg.stride - cg.pad + r, ti,
+                  bar);
+    } else {
+      tma_load_2d(dst, &tmA, kb * BK, m0, bar);
+    }
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -97,13 +160,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(sa + L::A_BYTES, &tmB, (kb0 + i) * BK, n0, &full[i]);
       }
       pdl_wait();
-      for (int i = 0; i < pre; ++i) tma_load_2d(smem + i * L::STAGE_BYTES, &tmA, (kb0 + i) * BK, m0, &full[i]);
+      for (int i = 0; i < pre; ++i) load_a(smem + i * L::STAGE_BYTES, kb0 + i, &full[i]);
       for (int kb = kb0 + pre, i = pre; kb < kb1; ++kb, ++i) {
         const int s = i % STAGES;
         mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
         uint8_t* sa = smem + s * L::STAGE_BYTES;
         mbar_expect_tx(&full[s], L::STAGE_BYTES);
-        tma_load_2d(sa, &tmA, kb * BK, m0, &full[s]);
+        load_a(sa, kb, &full[s]);
         tma_load_2d(sa + L::A_BYTES, &tmB, kb * BK, n0, &full[s]);
       }
     }
@@ -138,13 +201,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint4 v[BATCH];
 #pragma unroll
         for (int u = 0; u < BATCH; ++u) {
-          const int i = t + (b + u) * 64, r = i / PR, c = (i - r * PR) * 8;
+          const int i = t + (b + u) * 64, r = i / PR, c = (i - r * PR) * 8, gr = row_of(r);
           v[u] = make_uint4(0, 0, 0, 0);
-          if (m0 + r < M && n0 + c + 8 <= N) {
-            v[u] = *reinterpret_cast<const uint4*>(res + size_t(m0 + r) * ldr + n0 + c);
-          } else if (m0 + r < M) {
+          if (gr >= 0 && n0 + c + 8 <= N) {
+            v[u] = *reinterpret_cast<const uint4*>(res + size_t(gr) * ldr + n0 + c);
+          } else if (gr >= 0) {
             for (int q = 0; q < 8 && n0 + c + q < N; ++q)
-              reinterpret_cast<uint16_t*>(&v[u])[q] = res[size_t(m0 + r) * ldr + n0 + c + q];
+              reinterpret_cast<uint16_t*>(&v[u])[q] = res[size_t(gr) * ldr + n0 + c + q];
           }
         }
 #pragma unroll
@@ -158,93 +221,61 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {  // ---- epilogue: TMEM -> registers -> bf16 global
     pdl_wait();
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int rl = q * 32 + lane, row = m0 + rl;
+    const int rl = q * 32 + lane;
     const uint32_t tq = tmem + (uint32_t(q * 32) << 16);
     mbar_wait(&accum_full, 0);
     tc_fence_after();
-    bool finish = true;
-    float* part = nullptr;
     if (splits > 1) {
-      // Deterministic split-K: every split stores its fp32 partial tile
-      // (column-major, so a warp's stores are coalesced); the last split to
-      // arrive sums all partials in split order and runs the epilogue.
-      const int tile = blockIdx.y * gridDim.x + blockIdx.x;
-      part = ws + size_t(tile) * splits * BN * BM;
+      // Split-K: park this split's fp32 partial tile in the (now idle) ring,
+      // column-major so a warp's accesses are contiguous.
+      float* part = reinterpret_cast<float*>(smem);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16) {
         uint32_t r[16];
         tmem_ld16(tq + uint32_t(c0), r);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) __stcg(part + (size_t(z) * BN + c0 + j) * BM + rl, __uint_as_float(r[j]));
+        for (int j = 0; j < 16; ++j) part[(c0 + j) * BM + rl] = __uint_as_float(r[j]);
       }
-      __threadfence();
-      asm volatile("bar.sync 2, 128;" ::: "memory");
-      if (threadIdx.x == 128) last_split = atomicAdd(&ctr[tile], 1u) == unsigned(splits - 1);
-      asm volatile("bar.sync 2, 128;" ::: "memory");
-      finish = last_split;
-      if (finish) {
-        __threadfence();
-        if (threadIdx.x == 128) ctr[tile] = 0;  // re-armed for the next launch
-      }
+    } else {
+      asm volatile("bar.sync 1, 192;" ::: "memory");  // residual / scale / bias in smem
+      store_cols(0, BN, rl, [&](int c0, float (&v)[16]) {
+        uint32_t r[16];
+        tmem_ld16(tq + uint32_t(c0), r);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+      });
     }
-    asm volatile("bar.sync 1, 192;" ::: "memory");  // residual / scale / bias in smem
-    if (finish) {
-      uint16_t* drow = D + size_t(row) * ldd;
-      const bool vec_ok = (ldd % 8 == 0);
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-        if (splits > 1) {  // every split's 16 values in flight, then summed in split order
-          float pv[kMaxSplits][16];
+  }
+  if (splits > 1) {
+    // The splits of a tile form one thread-block cluster. After a cluster
+    // barrier, split z reduces columns [z*BN/S, (z+1)*BN/S) of the tile by
+    // reading every split's partial from distributed shared memory in split
+    // order (deterministic), and runs the epilogue for that slice.
+    cluster_sync();
+    if (warp >= 4) {
+      const int rl = (warp & 3) * 32 + lane, cols = BN / splits, cbeg = z * cols;
+      const uint32_t local = smem_u32(smem);
+      asm volatile("bar.sync 1, 192;" ::: "memory");
+      store_cols(cbeg, cbeg + cols, rl, [&](int c0, float (&v)[16]) {
+        float pv[kMaxSplits][16];
 #pragma unroll
-          for (int zz = 0; zz < kMaxSplits; ++zz)
+        for (int zz = 0; zz < kMaxSplits; ++zz) {
+          if (zz < splits) {
+            const uint32_t base = map_shared_rank(local, uint32_t(zz));
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              pv[zz][j] = zz < splits ? __ldcg(part + (size_t(zz) * BN + c0 + j) * BM + rl) : 0.f;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            v[j] = pv[0][j];
-#pragma unroll
-            for (int zz = 1; zz < kMaxSplits; ++zz)
-              if (zz < splits) v[j] += pv[zz][j];
+            for (int j = 0; j < 16; ++j) pv[zz][j] = ld_dsmem_f32(base + uint32_t(((c0 + j) * BM + rl) * 4));
           }
-        } else {
-          uint32_t r[16];
-          tmem_ld16(tq + uint32_t(c0), r);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
         }
-        const int n = n0 + c0;
-        if (row >= M || n >= N) continue;
-        const uint4* rp = reinterpret_cast<const uint4*>(s_res + rl * L::RES_LD + c0);
-        const uint4 ra = res ? rp[0] : make_uint4(0, 0, 0, 0), rb = res ? rp[1] : make_uint4(0, 0, 0, 0);
-        const uint32_t rw[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-        uint32_t o[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float a = v[2 * j] * s_scale[c0 + 2 * j] + s_bias[c0 + 2 * j];
-          float b = v[2 * j + 1] * s_scale[c0 + 2 * j + 1] + s_bias[c0 + 2 * j + 1];
-          if (res) {
-            a += bf16_lo(rw[j]);
-            b += bf16_hi(rw[j]);
-          }
-          if (relu) {
-            a = fmaxf(a, 0.f);
-            b = fmaxf(b, 0.f);
-          }
-          o[j] = pack_bf16x2(a, b);
-        }
-        if (vec_ok && n + 16 <= N) {
-          uint4* dp = reinterpret_cast<uint4*>(drow + n);
-          dp[0] = make_uint4(o[0], o[1], o[2], o[3]);
-          dp[1] = make_uint4(o[4], o[5], o[6], o[7]);
-        } else {
+        for (int j = 0; j < 16; ++j) {
+          v[j] = pv[0][j];
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (n + j < N) drow[n + j] = uint16_t(o[j >> 1] >> (16 * (j & 1)));
+          for (int zz = 1; zz < kMaxSplits; ++zz)
+            if (zz < splits) v[j] += pv[zz][j];
         }
-      }
+      });
     }
+    cluster_sync();  // no split leaves while its partial may still be read
   }
   tc_fence_before();
   __syncthreads();
@@ -271,18 +302,33 @@ template <int BN, int STAGES>
 void run_bn(const Prepared& p, cudaStream_t stream) {
   constexpr size_t smem = Smem<BN, STAGES>::TOTAL;
   static_assert(smem <= 227 * 1024, "GEMM shared memory");
-  static bool attr = false;
-  if (!attr) {
+  static bool smem_set = false;
+  if (!smem_set) {
     TRIMS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(smem)));
-    attr = true;
+    smem_set = true;
   }
   const Epilogue& e = p.e;
   const int kblocks = int((p.K + BK - 1) / BK);
   const int kper = (kblocks + p.splits - 1) / p.splits;
-  dim3 grid(unsigned((p.M + BM - 1) / BM), unsigned((p.N + BN - 1) / BN), unsigned(p.splits));
-  launch_pdl(gemm_tc_kernel<BN, STAGES>, grid, dim3(kThreads), smem, stream, p.ta, p.tb, e.out, int(p.M), int(p.N),
-             int(p.K), int(e.ldo), e.scale, e.bias, e.residual, int(e.ldr), e.relu ? 1 : 0, p.ws, p.ctr, kper);
+  dim3 grid(unsigned(tile_rows(p) / BM), unsigned((p.N + BN - 1) / BN), unsigned(p.splits));
+  // PDL always; split-K launches the splits of a tile as one (1, 1, S) cluster
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = unsigned(p.splits);
+  cfg.attrs = attr;
+  cfg.numAttrs = p.splits > 1 ? 2 : 1;
+  TRIMS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES>, p.ta, p.tb, e.out, int(p.M), int(p.N), int(p.K),
+                                int(e.ldo), e.scale, e.bias, e.residual, int(e.ldr), e.relu ? 1 : 0, kper, p.g));
 }
 
 }  // namespace
@@ -334,7 +380,8 @@ Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn) 
 }
 
 void run(const Prepared& p, cudaStream_t stream) {
-  if (p.splits > 1 && (!p.ws || !p.ctr)) raise(Errc::InvalidArgument, "split-K GEMM without a workspace");
+  if (p.splits < 1 || p.splits > kMaxSplits || (p.bn / p.splits) % 16)
+    raise(Errc::InvalidArgument, "GEMM split count");
   switch (p.bn) {
     case 64: run_bn<64, 6>(p, stream); break;
     case 128: run_bn<128, 5>(p, stream); break;
@@ -343,22 +390,58 @@ void run(const Prepared& p, cudaStream_t stream) {
 }
 
 int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms) {
-  // Split K only when the output tiles leave most SMs idle and each split
-  // keeps >= 8 k-blocks; the last split reduces all partials, so at most 4.
+  // Split K only while the output tiles leave most SMs idle, each split keeps
+  // >= 4 k-blocks and every split's column slice of the tile is >= 16 wide.
   const uint64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn), kb = (K + BK - 1) / BK;
   int s = 1;
-  while (s < 4 && tiles * uint64_t(s * 2) <= uint64_t(sms) && kb / uint64_t(s * 2) >= 8) s *= 2;
+  while (s < kMaxSplits && bn / (s * 2) >= 16 && tiles * uint64_t(s * 2) <= uint64_t(sms) && kb / uint64_t(s * 2) >= 4)
+    s *= 2;
   return s;
 }
 
-uint64_t workspace_bytes(const Prepared& p) {
-  if (p.splits <= 1) return 0;
-  const uint64_t tiles = ((p.M + BM - 1) / BM) * ((p.N + p.bn - 1) / p.bn);
-  return tiles * uint64_t(p.splits) * uint64_t(p.bn) * BM * 4;
+uint64_t tile_rows(const Prepared& p) {
+  if (p.g.impl) return uint64_t(p.g.N) * p.g.tiles_h * p.g.tiles_w * BM;
+  return (p.M + BM - 1) / BM * BM;
 }
 
-uint64_t counter_count(const Prepared& p) {
-  return p.splits <= 1 ? 0 : ((p.M + BM - 1) / BM) * ((p.N + p.bn - 1) / p.bn);
+ConvGeom conv_geom(int N, int H, int W, int C, int R, int S, int stride, int pad, int P, int Q) {
+  ConvGeom g;
+  g.impl = 1;
+  g.N = N, g.H = H, g.W = W, g.C = C, g.R = R, g.S = S, g.stride = stride, g.pad = pad, g.P = P, g.Q = Q;
+  int wl = 0;
+  while ((1 << wl) < Q && wl < 7) ++wl;   // Wbox = next power of two >= Q, at most 128
+  while ((1 << wl) * stride > 256) --wl;  // TMA box dims are <= 256 elements
+  while ((BM >> wl) * stride > 256) ++wl;
+  g.wbox_log2 = wl;
+  g.hbox = BM >> wl;
+  g.tiles_w = (Q + (1 << wl) - 1) >> wl;
+  g.tiles_h = (P + g.hbox - 1) / g.hbox;
+  g.cblocks = C / BK;
+  return g;
+}
+
+Prepared prepare_conv(const void* act, const ConvGeom& g, const Operand& B, const Epilogue& e, int bn) {
+  if (!g.impl || g.C % BK || g.hbox * g.stride > 256) raise(Errc::InvalidArgument, "implicit conv geometry");
+  if (B.k != uint64_t(g.R) * g.S * g.C) raise(Errc::InvalidArgument, "implicit conv K mismatch");
+  const uint64_t M = uint64_t(g.N) * g.P * g.Q;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  Prepared p = prepare({act, M, B.k, B.k}, B, e, bn ? bn : pick_bn(uint64_t(g.N) * g.tiles_h * g.tiles_w * BM, B.rows,
+                                                                     sms));
+  // replace the A map: 4-D NHWC, box {64 ch, Wbox, Hbox, 1} at element strides {1, st, st, 1}
+  CUtensorMap m;
+  cuuint64_t dims[4] = {cuuint64_t(g.C), cuuint64_t(g.W), cuuint64_t(g.H), cuuint64_t(g.N)};
+  cuuint64_t strides[3] = {cuuint64_t(g.C) * 2, cuuint64_t(g.W) * g.C * 2, cuuint64_t(g.H) * g.W * g.C * 2};
+  cuuint32_t box[4] = {uint32_t(BK), uint32_t((1 << g.wbox_log2) * g.stride), uint32_t(g.hbox * g.stride), 1};
+  cuuint32_t estr[4] = {1, uint32_t(g.stride), uint32_t(g.stride), 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(act), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cu_check(r, "cuTensorMapEncodeTiled (conv)");
+  p.ta = m;
+  p.g = g;
+  return p;
 }
 
 void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn) {

@@ -27,6 +27,18 @@ struct Epilogue {
 };
 
 CUtensorMap make_tmap(const void* ptr, uint64_t rows, uint64_t k, uint64_t ld, uint32_t box_rows);
+
+// Implicit-GEMM convolution geometry: A is read straight from the NHWC bf16
+// activation [N][H][W][C] by 4-D TMA boxes of 64 channels x Wbox x Hbox output
+// pixels (tap-shifted, stride via TMA element strides, padding = OOB zero
+// fill); an M tile is a Hbox x Wbox block of one image's output (Wbox*Hbox =
+// 128). K order = (r, s, c), the resident KRSC weight order. Needs C % 64 == 0.
+struct ConvGeom {
+  int impl{0};
+  int N, H, W, C, R, S, stride, pad, P, Q;
+  int wbox_log2, hbox, tiles_w, tiles_h, cblocks;
+};
+ConvGeom conv_geom(int N, int H, int W, int C, int R, int S, int stride, int pad, int P, int Q);
 int pick_bn(uint64_t M, uint64_t N, int sms);
 
 // A GEMM with its tensor maps encoded once (the executor builds these at
@@ -36,18 +48,19 @@ struct Prepared {
   uint64_t M{0}, N{0}, K{0};
   int bn{128};
   Epilogue e;
-  // Split-K (grid.z = splits): fp32 partial tiles in `ws`, one arrival
-  // counter per output tile in `ctr` (zeroed once; the last split re-arms it).
+  // Split-K (grid.z = splits, one (1,1,splits) cluster per output tile):
+  // the splits reduce their fp32 partials through distributed shared memory.
   int splits{1};
-  float* ws{nullptr};
-  unsigned int* ctr{nullptr};
+  ConvGeom g{};  // g.impl: A is the implicit im2col of an NHWC activation
 };
 Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn = 0);
+// Implicit-GEMM conv: `act` = NHWC input, B = [Cout][R*S*C] KRSC weights.
+Prepared prepare_conv(const void* act, const ConvGeom& g, const Operand& B, const Epilogue& e, int bn = 0);
+// Output-tile rows of a prepared GEMM (M rounded up to whole tiles).
+uint64_t tile_rows(const Prepared& p);
 void run(const Prepared& p, cudaStream_t stream);
-// Split count for a GEMM shape on `sms` SMs, and the workspace it needs.
+// Split count for a GEMM shape on `sms` SMs.
 int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms);
-uint64_t workspace_bytes(const Prepared& p);
-uint64_t counter_count(const Prepared& p);
 // D = epi(A . B^T); bn = 0 picks the tile width.
 void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn = 0);
 

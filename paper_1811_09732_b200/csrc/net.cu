@@ -75,6 +75,26 @@ std::string bn_name(const std::string& conv) {
   return b;
 }
 
+// TRIMS_IMPLICIT_CONV=0 goes back to im2col + GEMM (A/B switch).
+bool implicit_enabled();
+
+// The first conv builds its columns from the fp32 input directly when it
+// would im2col anyway (not 1x1/stride 1, not implicit, one group).
+bool first_conv_fusable(const LayerSpec& l) {
+  const int k = l.i("k", 1), groups = l.i("groups", 1);
+  const bool direct = k == 1 && l.i("stride", 1) == 1 && l.i("pad", 0) == 0 && groups == 1;
+  const bool implicit = !direct && groups == 1 && l.i("cin") % 64 == 0 && implicit_enabled();
+  return !direct && !implicit && groups == 1;
+}
+
+bool implicit_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TRIMS_IMPLICIT_CONV");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
 // TRIMS_SPLITK=0 turns split-K off (A/B switch).
 bool splitk_enabled() {
   static const bool on = [] {
@@ -133,7 +153,9 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
         int P, Q;
         conv_shape(in, l, P, Q);
         const int k = l.i("k", 1), groups = l.i("groups", 1), cg = l.i("cin") / groups;
-        if (!(k == 1 && l.i("stride", 1) == 1 && l.i("pad", 0) == 0 && groups == 1))
+        const bool direct = k == 1 && l.i("stride", 1) == 1 && l.i("pad", 0) == 0 && groups == 1;
+        const bool implicit = !direct && groups == 1 && l.i("cin") % 64 == 0 && implicit_enabled();
+        if (!direct && !implicit)
           col_elems = std::max<uint64_t>(col_elems, uint64_t(batch) * P * Q * ((uint64_t(k) * k * cg + 7) / 8 * 8));
         a = {nullptr, batch, P, Q, l.i("cout")};
         if (!l.s("out").empty()) named[l.s("out")] = a;
@@ -151,7 +173,6 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
   }
   uint16_t* col = col_elems ? reinterpret_cast<uint16_t*>(alloc(col_elems * 2)) : nullptr;
   Act cur;
-  std::vector<std::shared_ptr<gemm::Prepared>> gemms;  // split-K workspace is shared (layers run in order)
 
   for (size_t li = 0; li < layers.size(); ++li) {
     const LayerSpec& l = layers[li];
@@ -164,7 +185,12 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       const float* in = input_;
       const Act o = cur;
       const int C = in_c_, HW = in_hw_;
-      steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) { input_prep(in, o.p, o.n, C, HW, HW, s); }}));
+      // A first conv that im2cols the input reads the fp32 NCHW input itself
+      // (im2col_input); otherwise the input is converted to NHWC bf16 here.
+      const bool fused = li + 1 < layers.size() && layers[li + 1].kind == "conv" && layers[li + 1].s("src").empty() &&
+                         first_conv_fusable(layers[li + 1]);
+      if (!fused)
+        steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) { input_prep(in, o.p, o.n, C, HW, HW, s); }}));
     } else if (l.kind == "conv") {
       const Act in = l.s("src").empty() ? cur : named.at(l.s("src"));
       int P, Q;
@@ -203,26 +229,36 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       }
       Act out{reinterpret_cast<uint16_t*>(alloc(M * cout * 2)), batch, P, Q, cout};
       const bool direct = k == 1 && st == 1 && pad == 0 && groups == 1;
+      // Implicit GEMM (A read from the NHWC activation by 4-D TMA, no im2col
+      // pass) whenever the channels tile by 64.
+      const bool implicit = !direct && groups == 1 && cin % 64 == 0 && implicit_enabled();
       bool first_group = true;
       for (int gi = 0; gi < groups; ++gi) {
         const uint16_t* A = direct ? in.p : col;
-        if (!direct) {
+        if (!direct && !implicit) {
           const Act src = in;
-          steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) {
-            nn::im2col(src.p, col, src.n, src.h, src.w, src.c, gi * cg, cg, k, k, st, pad, P, Q, kp, s);
-          }}));
+          if (li == 1 && layers[0].kind == "input" && l.s("src").empty() && first_conv_fusable(l)) {
+            const float* x = input_;
+            steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) {
+              nn::im2col_input(x, col, src.n, src.c, src.h, src.w, k, k, st, pad, P, Q, kp, s);
+            }}));
+          } else {
+            steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) {
+              nn::im2col(src.p, col, src.n, src.h, src.w, src.c, gi * cg, cg, k, k, st, pad, P, Q, kp, s);
+            }}));
+          }
         }
         gemm::Epilogue e{out.p + uint64_t(gi) * kg, uint64_t(cout), scale ? scale + gi * kg : nullptr,
                          bias ? bias + gi * kg : nullptr, res ? res + uint64_t(gi) * kg : nullptr, uint64_t(cout),
                          l.i("relu") != 0};
         // A-side map and tile width are fixed; the B map follows the weights.
+        const gemm::Operand Bop{wpad ? wpad : reinterpret_cast<const uint16_t*>(uintptr_t(256)), uint64_t(kg),
+                                uint64_t(kp), uint64_t(kp)};
         auto prep = std::make_shared<gemm::Prepared>(
-            gemm::prepare({A, M, uint64_t(kp), uint64_t(direct ? cin : kp)},
-                          {wpad ? wpad : reinterpret_cast<const uint16_t*>(uintptr_t(256)), uint64_t(kg),
-                           uint64_t(kp), uint64_t(kp)},
-                          e));
-        if (splitk_enabled()) prep->splits = gemm::pick_splits(M, uint64_t(kg), uint64_t(kp), prep->bn, sms_);
-        gemms.push_back(prep);
+            implicit ? gemm::prepare_conv(in.p, gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q), Bop, e)
+                     : gemm::prepare({A, M, uint64_t(kp), uint64_t(direct ? cin : kp)}, Bop, e));
+        if (splitk_enabled())
+          prep->splits = gemm::pick_splits(gemm::tile_rows(*prep), uint64_t(kg), uint64_t(kp), prep->bn, sms_);
         const uint64_t b_off = w_off + uint64_t(gi) * kg * rsc * 2;
         const bool do_params = first_group && bind_params;
         auto rebind = [=](cudaStream_t s) {
@@ -317,21 +353,6 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
     }
   }
   if (!logits_) raise(Errc::InvalidArgument, "architecture has no fc output");
-  uint64_t ws_need = 0, ctr_need = 0;
-  for (const auto& g : gemms) {
-    ws_need = std::max(ws_need, gemm::workspace_bytes(*g));
-    ctr_need = std::max(ctr_need, gemm::counter_count(*g));
-  }
-  if (ws_need) {
-    float* ws = reinterpret_cast<float*>(alloc(ws_need));
-    auto* ctr = reinterpret_cast<unsigned int*>(alloc(ctr_need * 4));
-    TRIMS_CUDA(cudaMemset(ctr, 0, ctr_need * 4));
-    for (const auto& g : gemms)
-      if (g->splits > 1) {
-        g->ws = ws;
-        g->ctr = ctr;
-      }
-  }
   for (const auto& s : steps_) launches_ += s->launches;
   TRIMS_CUDA(cudaStreamCreateWithFlags(&capture_stream_, cudaStreamNonBlocking));
   rebind(weights);
@@ -371,7 +392,15 @@ void Net::run(cudaStream_t stream, bool use_graph) {
   }
   if (!exec_) {
     TRIMS_CUDA(cudaStreamBeginCapture(capture_stream_, cudaStreamCaptureModeThreadLocal));
-    record(capture_stream_);
+    try {
+      record(capture_stream_);
+    } catch (...) {  // close the capture so the stream stays usable, report the launch error
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(capture_stream_, &g);
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      throw;
+    }
     TRIMS_CUDA(cudaStreamEndCapture(capture_stream_, &graph_));
     TRIMS_CUDA(cudaGraphInstantiate(&exec_, graph_, 0));
   }

@@ -21,6 +21,11 @@ void im2col(const uint16_t* in, uint16_t* A, int N, int H, int W, int Ctot, int 
 void maxpool(const uint16_t* in, uint16_t* out, int N, int H, int W, int C, int k, int stride, int pad, int P, int Q,
              cudaStream_t s);
 void avgpool_global(const uint16_t* in, uint16_t* out, int N, int HW, int C, cudaStream_t s);
+// im2col straight from the fp32 NCHW network input (the first conv): fuses the
+// input layout/precision prep into the column build. Columns in (r, s, c)
+// order, zero beyond R*S*C up to Kp (Kp % 8 == 0).
+void im2col_input(const float* in_nchw, uint16_t* A, int N, int C, int H, int W, int R, int S, int stride, int pad,
+                  int P, int Q, int Kp, cudaStream_t s);
 void flatten_nchw(const uint16_t* in, uint16_t* out, int N, int HW, int C, cudaStream_t s);
 void gemv(const uint16_t* x, int M, int K, const uint16_t* W, int N, const float* bias, bool relu, uint16_t* out_bf,
           float* out_f32, int ldo, int sms, cudaStream_t s);

@@ -122,40 +122,64 @@ __global__ void maxpool_kernel(const uint16_t* __restrict__ in, uint16_t* __rest
   }
 }
 
-__global__ void avgpool_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, int N, int HW, int C) {
-  pdl_wait();  // reads the previous layer's output / writes shared scratch
+// Global average pool: one block per (image, 64 channels); 8 threads of
+// 8 channels x 32 pixel slices, 128-bit loads, shared-memory reduction.
+__global__ void __launch_bounds__(256) avgpool_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out,
+                                                      int N, int HW, int C) {
+  pdl_wait();  // reads the previous layer's output
   pdl_trigger();
-  if (C % 8 == 0) {  // 8 channels per thread, 128-bit loads, 7 in flight
-    const uint32_t C8 = C / 8, total = uint32_t(N) * C8;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-      const uint32_t n = i / C8, c = (i - n * C8) * 8;
-      const uint16_t* base = in + uint64_t(n) * HW * C + c;
-      float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll 7
-      for (int j = 0; j < HW; ++j) {
-        const uint4 v = *reinterpret_cast<const uint4*>(base + uint64_t(j) * C);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  __shared__ float red[32][65];
+  const int groups = (C + 63) / 64, n = blockIdx.x / groups, c0 = (blockIdx.x - n * groups) * 64;
+  const int cg = threadIdx.x & 7, sl = threadIdx.x >> 3, c = c0 + cg * 8;
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c + 8 <= C && C % 8 == 0) {
+    for (int j = sl; j < HW; j += 32) {
+      const uint4 v = *reinterpret_cast<const uint4*>(in + (uint64_t(n) * HW + j) * C + c);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          s[2 * q] += bf(uint16_t(w[q] & 0xffff));
-          s[2 * q + 1] += bf(uint16_t(w[q] >> 16));
-        }
+      for (int q = 0; q < 4; ++q) {
+        s[2 * q] += bf(uint16_t(w[q] & 0xffff));
+        s[2 * q + 1] += bf(uint16_t(w[q] >> 16));
       }
-      uint32_t o[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        o[q] = uint32_t(to_bf(s[2 * q] / float(HW))) | (uint32_t(to_bf(s[2 * q + 1] / float(HW))) << 16);
-      *reinterpret_cast<uint4*>(out + uint64_t(n) * C + c) = make_uint4(o[0], o[1], o[2], o[3]);
     }
-    return;
+  } else {
+    for (int j = sl; j < HW; j += 32)
+      for (int q = 0; q < 8 && c + q < C; ++q) s[q] += bf(in[(uint64_t(n) * HW + j) * C + c + q]);
   }
-  const uint64_t total = uint64_t(N) * C;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
-    const int c = int(i % C);
-    const int n = int(i / C);
-    float s = 0.f;
-    for (int j = 0; j < HW; ++j) s += bf(in[(uint64_t(n) * HW + j) * C + c]);
-    out[i] = to_bf(s / float(HW));
+#pragma unroll
+  for (int q = 0; q < 8; ++q) red[sl][cg * 8 + q] = s[q];
+  __syncthreads();
+  if (threadIdx.x < 64 && c0 + int(threadIdx.x) < C) {
+    float t = 0.f;
+    for (int k = 0; k < 32; ++k) t += red[k][threadIdx.x];
+    out[uint64_t(n) * C + c0 + threadIdx.x] = to_bf(t / float(HW));
+  }
+}
+
+// A[m, (r*S + s)*C + c] = bf16(in[n, c, y, x]) for the first conv, 8 columns
+// (one 16-byte store) per thread.
+__global__ void im2col_input_kernel(const float* __restrict__ in, uint16_t* __restrict__ A, int N, int C, int H, int W,
+                                    int R, int S, int stride, int pad, int P, int Q, int Kp) {
+  pdl_wait();  // the input H2D / previous forward's readers of A
+  pdl_trigger();
+  const int RSC = R * S * C, cols8 = Kp / 8;
+  const uint32_t total = uint32_t(N) * P * Q * cols8;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t m = i / cols8, col = (i - m * cols8) * 8;
+    const uint32_t q = m % Q, pn = m / Q, p = pn % P, n = pn / P;
+    uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int k = int(col) + e;
+      float v = 0.f;
+      if (k < RSC) {
+        const int rs = k / C, c = k - rs * C, r = rs / S, sx = rs - r * S;
+        const int y = int(p) * stride - pad + r, x = int(q) * stride - pad + sx;
+        if (y >= 0 && y < H && x >= 0 && x < W) v = __ldg(in + ((uint64_t(n) * C + c) * H + y) * W + x);
+      }
+      o[e >> 1] |= uint32_t(to_bf(v)) << (16 * (e & 1));
+    }
+    *reinterpret_cast<uint4*>(A + uint64_t(m) * Kp + col) = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -284,6 +308,13 @@ void im2col(const uint16_t* in, uint16_t* A, int N, int H, int W, int Ctot, int 
   TRIMS_CUDA(cudaGetLastError());
 }
 
+void im2col_input(const float* in, uint16_t* A, int N, int C, int H, int W, int R, int S, int stride, int pad, int P,
+                  int Q, int Kp, cudaStream_t s) {
+  if (Kp % 8) raise(Errc::InvalidArgument, "im2col_input needs Kp % 8 == 0");
+  launch_pdl(im2col_input_kernel, dim3(blocks(uint64_t(N) * P * Q * (Kp / 8))), dim3(256), 0, s, in, A, N, C, H, W, R,
+             S, stride, pad, P, Q, Kp);
+}
+
 void maxpool(const uint16_t* in, uint16_t* out, int N, int H, int W, int C, int k, int stride, int pad, int P, int Q,
              cudaStream_t s) {
   if (C % 8) raise(Errc::InvalidArgument, "maxpool needs C % 8 == 0");
@@ -292,7 +323,7 @@ void maxpool(const uint16_t* in, uint16_t* out, int N, int H, int W, int C, int 
 }
 
 void avgpool_global(const uint16_t* in, uint16_t* out, int N, int HW, int C, cudaStream_t s) {
-  launch_pdl(avgpool_kernel, dim3(blocks(uint64_t(N) * C / (C % 8 ? 1 : 8), 64)), dim3(64), 0, s, in, out, N, HW, C);
+  launch_pdl(avgpool_kernel, dim3(unsigned(N * ((C + 63) / 64))), dim3(256), 0, s, in, out, N, HW, C);
   TRIMS_CUDA(cudaGetLastError());
 }
 
