@@ -66,6 +66,12 @@ class Ingestor {
   // asynchronous on `stream`; bucket sums accumulate into d_sums.
   uint32_t from_device(const IngestPlan& p, const uint8_t* d_src, uint8_t* d_dst, unsigned long long* d_sums,
                        cudaStream_t stream);
+  // Raw blob already uploaded to d_raw (ready once `ready` fires) -> resident
+  // blob at d_dst: the transform (or, for an identity plan, the fused copy +
+  // hash), then the checksums. Used by a publish whose stage_host streamed
+  // the blob to the device while reading it.
+  uint64_t from_staged(const IngestPlan& p, const uint8_t* d_raw, cudaEvent_t ready, uint8_t* d_dst,
+                       std::vector<uint64_t>* buckets, IngestStats* st);
   // Peer pull: an identity plan's resident bytes from `d_src` (a peer GPU's
   // segment mapped here) to d_dst, copied and hashed by one fused kernel.
   uint64_t pull(const IngestPlan& p, const uint8_t* d_src, uint8_t* d_dst, std::vector<uint64_t>* buckets,
@@ -166,6 +172,20 @@ class CudaTierBackend : public TierBackend {
   std::map<uint64_t, std::shared_ptr<IngestPlan>> plans_;  // model_id -> compiled plan (manifests are immutable)
   std::map<uint64_t, std::shared_ptr<IngestPlan>> pull_plans_;  // model_id -> identity plan of the resident blob
   std::atomic<uint64_t> next_gen_{1};
+
+  // Cold-path overlap: stage_host reads the artifact in chunks into the
+  // pinned host tier and uploads each chunk to `pre_raw_` while reading the
+  // next, so the publish_fast that follows (same open, same thread) only
+  // transforms. One model at a time owns the buffer (pre_owner_); a
+  // concurrent cold open takes the plain path.
+  static constexpr uint64_t kNoOwner = ~0ull;
+  std::atomic<uint64_t> pre_owner_{kNoOwner};
+  uint8_t* pre_raw_{nullptr};
+  uint64_t pre_cap_{0};
+  cudaStream_t pre_stream_{nullptr};
+  cudaEvent_t pre_t0_{nullptr}, pre_done_{nullptr};
+  double pre_read_ms_{0};
+  void release_prestage(uint64_t model_id);
 };
 
 // Multi-threaded pread of [off, off+len) into dst (page cache -> pinned).
