@@ -213,9 +213,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
         bias = reinterpret_cast<float*>(alloc(uint64_t(cout) * 4));
         const uint64_t og = offset_of(bn + ".weight"), ob = offset_of(bn + ".bias"),
                        om = offset_of(bn + ".running_mean"), ov = offset_of(bn + ".running_var");
-        bind_params = [=](cudaStream_t s) {
-          nn::bn_fold(wptr(og), wptr(ob), wptr(om), wptr(ov), 1e-5f, cout, scale, bias, s);
-        };
+        folds_.push_back({og, ob, om, ov, scale, bias, cout});  // folded in one batched launch per rebind
       } else if (l.i("bias")) {
         bias = reinterpret_cast<float*>(alloc(uint64_t(cout) * 4));
         const uint64_t ob = offset_of(name + ".bias");
@@ -354,6 +352,8 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
   }
   if (!logits_) raise(Errc::InvalidArgument, "architecture has no fc output");
   for (const auto& s : steps_) launches_ += s->launches;
+  for (const auto& f : folds_) max_fold_c_ = std::max(max_fold_c_, f.C);
+  if (!folds_.empty()) d_jobs_ = reinterpret_cast<FoldJob*>(alloc(folds_.size() * sizeof(FoldJob)));
   TRIMS_CUDA(cudaStreamCreateWithFlags(&capture_stream_, cudaStreamNonBlocking));
   rebind(weights);
 }
@@ -371,13 +371,48 @@ void Net::rebind(const uint8_t* weights) {
   wbase_ = weights;
   for (const auto& s : steps_)
     if (s->rebind) s->rebind(capture_stream_);
-  TRIMS_CUDA(cudaStreamSynchronize(capture_stream_));
-  if (exec_) {  // kernel parameters (tensor maps, pointers) changed: re-capture
-    cudaGraphExecDestroy(exec_);
-    cudaGraphDestroy(graph_);
-    exec_ = nullptr;
-    graph_ = nullptr;
+  if (!folds_.empty()) {
+    std::vector<FoldJob> jobs;
+    jobs.reserve(folds_.size());
+    auto w = [&](uint64_t off) { return reinterpret_cast<const uint16_t*>(wbase_ + off); };
+    for (const auto& f : folds_) jobs.push_back({w(f.og), w(f.ob), w(f.om), w(f.ov), f.scale, f.shift, f.C, 0});
+    TRIMS_CUDA(cudaMemcpyAsync(d_jobs_, jobs.data(), jobs.size() * sizeof(FoldJob), cudaMemcpyHostToDevice,
+                               capture_stream_));
+    nn::bn_fold_batched(d_jobs_, int(jobs.size()), max_fold_c_, 1e-5f, capture_stream_);
   }
+  TRIMS_CUDA(cudaStreamSynchronize(capture_stream_));
+  // Kernel parameters (tensor maps, pointers) changed: re-record the graph
+  // and update the instantiated one in place (same topology) instead of
+  // instantiating a new executable graph.
+  if (exec_) capture_graph();
+}
+
+void Net::capture_graph() {
+  cudaGraph_t g = nullptr;
+  TRIMS_CUDA(cudaStreamBeginCapture(capture_stream_, cudaStreamCaptureModeThreadLocal));
+  try {
+    record(capture_stream_);
+  } catch (...) {  // close the capture so the stream stays usable, report the launch error
+    cudaStreamEndCapture(capture_stream_, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    throw;
+  }
+  TRIMS_CUDA(cudaStreamEndCapture(capture_stream_, &g));
+  if (exec_) {
+    cudaGraphExecUpdateResultInfo info{};
+    if (cudaGraphExecUpdate(exec_, g, &info) == cudaSuccess) {
+      if (graph_) cudaGraphDestroy(graph_);
+      graph_ = g;
+      return;
+    }
+    cudaGetLastError();  // topology changed: fall back to a fresh instantiation
+    cudaGraphExecDestroy(exec_);
+    exec_ = nullptr;
+  }
+  if (graph_) cudaGraphDestroy(graph_);
+  graph_ = g;
+  TRIMS_CUDA(cudaGraphInstantiate(&exec_, graph_, 0));
 }
 
 void Net::record(cudaStream_t stream) {
@@ -390,20 +425,7 @@ void Net::run(cudaStream_t stream, bool use_graph) {
     record(stream);
     return;
   }
-  if (!exec_) {
-    TRIMS_CUDA(cudaStreamBeginCapture(capture_stream_, cudaStreamCaptureModeThreadLocal));
-    try {
-      record(capture_stream_);
-    } catch (...) {  // close the capture so the stream stays usable, report the launch error
-      cudaGraph_t g = nullptr;
-      cudaStreamEndCapture(capture_stream_, &g);
-      if (g) cudaGraphDestroy(g);
-      cudaGetLastError();
-      throw;
-    }
-    TRIMS_CUDA(cudaStreamEndCapture(capture_stream_, &graph_));
-    TRIMS_CUDA(cudaGraphInstantiate(&exec_, graph_, 0));
-  }
+  if (!exec_) capture_graph();
   TRIMS_CUDA(cudaGraphLaunch(exec_, stream));
 }
 

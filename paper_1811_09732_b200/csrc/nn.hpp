@@ -29,6 +29,13 @@ void im2col_input(const float* in_nchw, uint16_t* A, int N, int C, int H, int W,
 void flatten_nchw(const uint16_t* in, uint16_t* out, int N, int HW, int C, cudaStream_t s);
 void gemv(const uint16_t* x, int M, int K, const uint16_t* W, int N, const float* bias, bool relu, uint16_t* out_bf,
           float* out_f32, int ldo, int sms, cudaStream_t s);
+// Batched BN fold at bind time: every BN layer of a network in one launch.
+struct FoldJob {
+  const uint16_t *gamma, *beta, *mean, *var;
+  float *scale, *shift;
+  int C, pad_;
+};
+void bn_fold_batched(const FoldJob* d_jobs, int njobs, int max_c, float eps, cudaStream_t s);
 void bn_fold(const uint16_t* gamma, const uint16_t* beta, const uint16_t* mean, const uint16_t* var, float eps, int C,
              float* scale, float* shift, cudaStream_t s);
 void bf16_to_f32(const uint16_t* in, float* out, int n, cudaStream_t s);
@@ -78,6 +85,17 @@ class Net {
   cudaGraph_t graph_{nullptr};
   cudaGraphExec_t exec_{nullptr};
   cudaStream_t capture_stream_{nullptr};
+  // BN folds of every layer, batched into one launch per rebind: offsets of
+  // gamma/beta/mean/var in the resident blob + destination buffers.
+  struct Fold {
+    uint64_t og, ob, om, ov;
+    float *scale, *shift;
+    int C;
+  };
+  std::vector<Fold> folds_;
+  FoldJob* d_jobs_{nullptr};
+  int max_fold_c_{0};
+  void capture_graph();
 };
 
 }  // namespace trims::nn

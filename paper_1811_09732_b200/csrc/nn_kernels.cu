@@ -244,6 +244,15 @@ __global__ void __launch_bounds__(256) gemv_kernel(const uint16_t* __restrict__ 
   }
 }
 
+__global__ void bn_fold_batched_kernel(const FoldJob* __restrict__ jobs, float eps) {
+  const FoldJob j = jobs[blockIdx.y];
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= j.C) return;
+  const float s = bf(j.gamma[c]) / sqrtf(bf(j.var[c]) + eps);
+  j.scale[c] = s;
+  j.shift[c] = bf(j.beta[c]) - bf(j.mean[c]) * s;
+}
+
 __global__ void bn_fold_kernel(const uint16_t* gamma, const uint16_t* beta, const uint16_t* mean, const uint16_t* var,
                                float eps, int C, float* scale, float* shift) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -340,6 +349,12 @@ void gemv(const uint16_t* x, int M, int K, const uint16_t* W, int N, const float
   else if (M <= 4) launch_pdl(gemv_kernel<4>, dim3(grid), dim3(256), 0, s, x, M, K, W, N, bias, relu, out_bf, out_f32, ldo);
   else if (M <= 8) launch_pdl(gemv_kernel<8>, dim3(grid), dim3(256), 0, s, x, M, K, W, N, bias, relu, out_bf, out_f32, ldo);
   else raise(Errc::InvalidArgument, "gemv is for M <= 8");
+  TRIMS_CUDA(cudaGetLastError());
+}
+
+void bn_fold_batched(const FoldJob* d_jobs, int njobs, int max_c, float eps, cudaStream_t s) {
+  if (!njobs) return;
+  bn_fold_batched_kernel<<<dim3((max_c + 255) / 256, njobs), 256, 0, s>>>(d_jobs, eps);  // bind time: no PDL
   TRIMS_CUDA(cudaGetLastError());
 }
 
