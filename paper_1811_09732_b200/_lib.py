@@ -224,10 +224,19 @@ def check(rc: int) -> None:
         raise TrimsError(rc, lib.trims_errc_name(rc).decode(), lib.trims_last_error().decode())
 
 
+_TEXT_BUFS: dict = {}
+
+
 def text_call(fn, *args, cap: int = 1 << 16) -> str:
-    """Call an entry point whose last two args are (char* out, uint64 cap)."""
+    """Call an entry point whose last two args are (char* out, uint64 cap).
+    Output buffers are reused per size (allocating and zeroing a fresh
+    multi-MiB buffer per call cost more than the call)."""
+    import threading
     while True:
-        buf = ctypes.create_string_buffer(cap)
+        k = (threading.get_ident(), cap)
+        buf = _TEXT_BUFS.get(k)
+        if buf is None:
+            buf = _TEXT_BUFS[k] = ctypes.create_string_buffer(cap)
         rc = fn(*args, buf, cap)
         if rc == Errc.InvalidArgument and b"too small" in lib.trims_last_error() and cap < (1 << 30):
             cap *= 8

@@ -102,13 +102,21 @@ class ModelView:
         return (end + 63) // 64 * 64
 
 
+_PARSED: dict = {}  # manifest JSON -> parsed tensor records (manifests are immutable)
+
+
 def slice_tensors(manifest_json: str, base_ptr: int) -> list[TensorView]:
-    """client.cpp:60-65 with device pointers."""
-    out = []
-    for t in json.loads(manifest_json)["tensors"]:
-        out.append(TensorView(t["name"], t["dims"], t["dtype"], t.get("layout", "native"), t["offset"],
-                              t["nbytes"], base_ptr + t["offset"]))
-    return out
+    """client.cpp:60-65 with device pointers; the parse is cached per manifest
+    (client.cpp:293-307 caches it by digest), so a new generation of a model
+    only re-bases the views."""
+    recs = _PARSED.get(manifest_json)
+    if recs is None:
+        recs = [(t["name"], t["dims"], t["dtype"], t.get("layout", "native"), t["offset"], t["nbytes"])
+                for t in json.loads(manifest_json)["tensors"]]
+        if len(_PARSED) > 256:
+            _PARSED.clear()
+        _PARSED[manifest_json] = recs
+    return [TensorView(n, d, dt, lay, off, nb, base_ptr + off) for n, d, dt, lay, off, nb in recs]
 
 
 class ImportCache:
