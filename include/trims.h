@@ -304,6 +304,24 @@ int trims_net_forward_host(trims_net* net, const float* host_input, float* host_
 /* row softmax of fp32 logits [M, N] (device pointers) */
 int trims_softmax(const float* in, float* out, int M, int N, void* stream);
 
+/* ------------------------------------------------------------ daemon
+ * The wire-protocol server (proj/src/daemon.cpp:398-560 over
+ * proj/src/wire_protocol.cpp's frozen v1 frames): serves OpenRequest /
+ * CloseRequest / StatsRequest for `store` on endpoint "unix:<path>" (or a bare
+ * path) / "tcp:<ipv4>:<port>", one thread per connection; handles still open
+ * when a connection drops are closed. OpenResponse objects tile the resident
+ * blob; each ObjectRef token is "<allocation>?dev=&alloc=&seg=&payload=" and,
+ * on Unix sockets, the allocation's fd rides the frame (SCM_RIGHTS).
+ * Replaces mrm::daemon::Daemon::start/request_stop/join (daemon.hpp:77-131). */
+typedef struct trims_server trims_server;
+int trims_server_start(trims_store* store, const char* endpoint, trims_server** out);
+void trims_server_stop(trims_server* s);
+uint64_t trims_server_frames_served(trims_server* s);
+/* v1 codec (wire_protocol.hpp:151-158 encode/decode) over a one-line text
+ * form of a message, for parity tests against the reference's codec. */
+int trims_wire_encode_text(const char* text, uint8_t* out, uint64_t cap, uint64_t* n);
+int trims_wire_decode_text(const uint8_t* frame, uint64_t n, char* out, uint64_t cap);
+
 /* ------------------------------------------------------------ test hooks */
 
 /* Replays a decision trace through this library's CacheCore over an

@@ -170,7 +170,27 @@ class _Ref:
         L.ref_trace.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint32,
                                 ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(ctypes.c_double),
                                 _u64p]
+        L.ref_wire_encode_text.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_uint64, _u64p]
+        L.ref_wire_decode_text.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_uint64]
+        L.ref_wire_request.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_uint64]
         self.L = L
+
+    # wire_protocol.cpp:319-357 through the shim's text form; (rc, value)
+    def wire_encode(self, text: str):
+        buf = ctypes.create_string_buffer(1 << 20)
+        n = ctypes.c_uint64()
+        rc = self.L.ref_wire_encode_text(text.encode(), buf, len(buf), ctypes.byref(n))
+        return rc, (buf.raw[: n.value] if rc == 0 else None)
+
+    def wire_decode(self, frame: bytes):
+        out = ctypes.create_string_buffer(max(1 << 16, 4 * len(frame)))
+        rc = self.L.ref_wire_decode_text(frame, len(frame), out, len(out))
+        return rc, (out.value.decode() if rc == 0 else None)
+
+    def wire_request(self, endpoint: str, text: str):
+        out = ctypes.create_string_buffer(1 << 20)
+        rc = self.L.ref_wire_request(endpoint.encode(), text.encode(), out, len(out))
+        return rc, (out.value.decode() if rc == 0 else None)
 
     @staticmethod
     def _check(rc: int, what: str) -> None:

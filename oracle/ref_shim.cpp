@@ -31,6 +31,7 @@
 #include "mrm/model_format.hpp"
 #include "mrm/sha256.hpp"
 #include "mrm/shared_segment.hpp"
+#include "mrm/wire_protocol.hpp"
 
 using namespace mrm;
 namespace fs = std::filesystem;
@@ -99,6 +100,201 @@ bench::CatalogSpec filtered(const char* catalog, const char* only_model) {
 
 double secs_since(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// ---- wire protocol text form (the same one-line form as our
+// trims_wire_encode_text / trims_wire_decode_text, csrc/wire.cpp)
+std::string wesc(const std::string& s) {
+  std::string o;
+  for (unsigned char c : s) {
+    if (c <= ' ' || c == '%' || c >= 0x7f) {
+      char h[4];
+      std::snprintf(h, sizeof h, "%%%02X", c);
+      o += h;
+    } else {
+      o += char(c);
+    }
+  }
+  return o.empty() ? "%" : o;
+}
+
+std::string wunesc(const std::string& s) {
+  if (s == "%") return "";
+  std::string o;
+  for (size_t i = 0; i < s.size(); ++i) {
+    if (s[i] == '%' && i + 2 < s.size()) {
+      o += char(std::stoi(s.substr(i + 1, 2), nullptr, 16));
+      i += 2;
+    } else {
+      o += s[i];
+    }
+  }
+  return o;
+}
+
+std::string wf64(double v) {
+  char b[40];
+  std::snprintf(b, sizeof b, "%.17g", v);
+  return b;
+}
+
+wire::Message wire_from_text(const std::string& text) {
+  std::istringstream is(text);
+  std::string kind;
+  is >> kind;
+  auto s = [&] {
+    std::string t;
+    if (!(is >> t)) throw std::runtime_error("message text ends early");
+    return wunesc(t);
+  };
+  auto u = [&] { return std::stoull(s()); };
+  auto d = [&] { return std::stod(s()); };
+  auto gran = [&](uint64_t kind_v, uint64_t block) {
+    shm::ShareGranularity g;
+    g.kind = shm::GranularityKind(kind_v);
+    if (g.kind == shm::GranularityKind::Block) g.block_bytes = block;
+    return g;
+  };
+  if (kind == "open") {
+    wire::OpenRequest m;
+    m.protocol_version = uint16_t(u());
+    m.ns = s();
+    m.name = s();
+    m.version = s();
+    const uint64_t k = u(), b = u();
+    m.granularity = gran(k, b);
+    m.client_id = u();
+    return m;
+  }
+  if (kind == "openresp") {
+    wire::OpenResponse m;
+    m.model_id = u();
+    m.handle_id = u();
+    m.footprint.weights_bytes = u();
+    m.footprint.workspace_bytes = u();
+    m.footprint.total_bytes = u();
+    const uint64_t c = u();
+    for (uint64_t i = 0; i < c; ++i) {
+      wire::ObjectRef o;
+      o.name = s();
+      o.segment_token = s();
+      o.generation = u();
+      o.offset = u();
+      o.length = u();
+      m.objects.push_back(o);
+    }
+    const std::string h = s();
+    for (int i = 0; i < 32; ++i) m.manifest_digest[size_t(i)] = uint8_t(std::stoi(h.substr(size_t(2 * i), 2), nullptr, 16));
+    return m;
+  }
+  if (kind == "close") {
+    wire::CloseRequest m;
+    m.protocol_version = uint16_t(u());
+    m.model_id = u();
+    m.handle_id = u();
+    return m;
+  }
+  if (kind == "closeresp") {
+    wire::CloseResponse m;
+    m.model_id = u();
+    m.refcount = u();
+    return m;
+  }
+  if (kind == "stats") {
+    wire::StatsRequest m;
+    m.protocol_version = uint16_t(u());
+    return m;
+  }
+  if (kind == "statsresp") {
+    wire::StatsResponse m;
+    for (auto& t : m.tiers) {
+      t.hits = u();
+      t.misses = u();
+      t.evictions = u();
+      t.used_bytes = u();
+      t.capacity_bytes = u();
+    }
+    const uint64_t c = u();
+    for (uint64_t i = 0; i < c; ++i) {
+      wire::ModelStatsMsg r;
+      r.ns = s();
+      r.name = s();
+      r.version = s();
+      r.refcount = u();
+      r.use_count = u();
+      r.residency = uint8_t(u());
+      m.models.push_back(r);
+    }
+    m.open_requests = u();
+    m.open_errors = u();
+    m.disk_reads = u();
+    m.remote_fetches = u();
+    m.fetch_ns = u();
+    m.disk_read_ns = u();
+    m.copy_ns = u();
+    m.export_ns = u();
+    m.workspace_headroom = d();
+    m.has_calibration = u() != 0;
+    if (m.has_calibration) {
+      m.calib_q = d();
+      m.calib_o = d();
+      m.calib_s = d();
+    }
+    return m;
+  }
+  if (kind == "error") {
+    wire::ErrorMsg m;
+    m.code = uint16_t(u());
+    m.detail = s();
+    return m;
+  }
+  throw std::runtime_error("unknown message kind " + kind);
+}
+
+std::string wire_to_text(const wire::Message& msg) {
+  std::ostringstream os;
+  auto hex = [](const Digest& dg) {
+    std::string h;
+    char b[3];
+    for (uint8_t x : dg) {
+      std::snprintf(b, sizeof b, "%02x", x);
+      h += b;
+    }
+    return h;
+  };
+  if (const auto* m = std::get_if<wire::OpenRequest>(&msg)) {
+    const bool blk = m->granularity.kind == shm::GranularityKind::Block;
+    os << "open " << m->protocol_version << ' ' << wesc(m->ns) << ' ' << wesc(m->name) << ' ' << wesc(m->version)
+       << ' ' << int(m->granularity.kind) << ' ' << (blk ? m->granularity.block_bytes : 0) << ' ' << m->client_id;
+  } else if (const auto* m = std::get_if<wire::OpenResponse>(&msg)) {
+    os << "openresp " << m->model_id << ' ' << m->handle_id << ' ' << m->footprint.weights_bytes << ' '
+       << m->footprint.workspace_bytes << ' ' << m->footprint.total_bytes << ' ' << m->objects.size();
+    for (const auto& o : m->objects)
+      os << ' ' << wesc(o.name) << ' ' << wesc(o.segment_token) << ' ' << o.generation << ' ' << o.offset << ' '
+         << o.length;
+    os << ' ' << hex(m->manifest_digest);
+  } else if (const auto* m = std::get_if<wire::CloseRequest>(&msg)) {
+    os << "close " << m->protocol_version << ' ' << m->model_id << ' ' << m->handle_id;
+  } else if (const auto* m = std::get_if<wire::CloseResponse>(&msg)) {
+    os << "closeresp " << m->model_id << ' ' << m->refcount;
+  } else if (const auto* m = std::get_if<wire::StatsRequest>(&msg)) {
+    os << "stats " << m->protocol_version;
+  } else if (const auto* m = std::get_if<wire::StatsResponse>(&msg)) {
+    os << "statsresp";
+    for (const auto& t : m->tiers)
+      os << ' ' << t.hits << ' ' << t.misses << ' ' << t.evictions << ' ' << t.used_bytes << ' ' << t.capacity_bytes;
+    os << ' ' << m->models.size();
+    for (const auto& r : m->models)
+      os << ' ' << wesc(r.ns) << ' ' << wesc(r.name) << ' ' << wesc(r.version) << ' ' << r.refcount << ' '
+         << r.use_count << ' ' << int(r.residency);
+    os << ' ' << m->open_requests << ' ' << m->open_errors << ' ' << m->disk_reads << ' ' << m->remote_fetches << ' '
+       << m->fetch_ns << ' ' << m->disk_read_ns << ' ' << m->copy_ns << ' ' << m->export_ns << ' '
+       << wf64(m->workspace_headroom) << ' ' << (m->has_calibration ? 1 : 0);
+    if (m->has_calibration) os << ' ' << wf64(m->calib_q) << ' ' << wf64(m->calib_o) << ' ' << wf64(m->calib_s);
+  } else if (const auto* m = std::get_if<wire::ErrorMsg>(&msg)) {
+    os << "error " << m->code << ' ' << wesc(m->detail);
+  }
+  return os.str();
 }
 
 }  // namespace
@@ -500,6 +696,30 @@ int ref_trace(const char* dir, const char* names_c, const uint32_t* trace, uint3
     dmn.request_stop();
     dmn.join();
     return 0;
+  });
+}
+
+// wire_protocol.cpp:319-357 encode/decode through the text form
+int ref_wire_encode_text(const char* text, uint8_t* out, uint64_t cap, uint64_t* n) {
+  return guarded([&] {
+    std::vector<uint8_t> f = wire::encode(wire_from_text(text));
+    *n = f.size();
+    if (f.size() > cap) return -2;
+    std::memcpy(out, f.data(), f.size());
+    return 0;
+  });
+}
+
+int ref_wire_decode_text(const uint8_t* frame, uint64_t n, char* out, uint64_t cap) {
+  return guarded([&] { return put_text(wire_to_text(wire::decode({frame, size_t(n)})), out, cap); });
+}
+
+// One request over the reference FramedSocket (wire_protocol.cpp:395-492) to a
+// daemon at `endpoint`; the reply's text form in `out`.
+int ref_wire_request(const char* endpoint, const char* text, char* out, uint64_t cap) {
+  return guarded([&] {
+    wire::FramedSocket sock = wire::FramedSocket::connect(wire::parse_endpoint(endpoint));
+    return put_text(wire_to_text(sock.request(wire_from_text(text))), out, cap);
   });
 }
 

@@ -139,6 +139,11 @@ _SIGS = {
     "trims_fill_uniform_host": (_c.c_int, [_p, _u64, _u64, _u64, _c.c_float, _c.c_float]),
     "trims_fnv1a": (_u64, [_s]),
     "trims_touch_host": (_c.c_int, [_p, _s, _c.POINTER(_u64)]),
+    "trims_server_start": (_c.c_int, [_p, _c.c_char_p, _c.POINTER(_p)]),
+    "trims_server_stop": (None, [_p]),
+    "trims_server_frames_served": (_u64, [_p]),
+    "trims_wire_encode_text": (_c.c_int, [_c.c_char_p, _p, _u64, _c.POINTER(_u64)]),
+    "trims_wire_decode_text": (_c.c_int, [_p, _u64, _c.c_char_p, _u64]),
     "trims_checksum_host": (_c.c_int, [_p, _u64, _u64, _c.POINTER(_u64)]),
     "trims_backend_create": (_c.c_int, [_c.POINTER(StoreConfig), _c.POINTER(_p)]),
     "trims_backend_destroy": (None, [_p]),

@@ -22,6 +22,7 @@
 #include "gemm.hpp"
 #include "nn.hpp"
 #include "sha256.hpp"
+#include "store_api.hpp"
 
 using namespace trims;
 
@@ -1046,3 +1047,23 @@ int trims_fill_uniform_device(float* dev, uint64_t n, uint64_t stream_seed, uint
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ store_api
+// (store_api.hpp: the surface the wire daemon drives)
+
+namespace trims::store_api {
+
+PlacementResult open(trims_store* s, const fmt::ModelKey& key, const Granularity& g) {
+  const uint64_t now = s->clock.fetch_add(1) + 1;  // daemon.cpp:457
+  return s->open(key, g, now, nullptr);
+}
+
+uint64_t close(trims_store* s, const fmt::ModelKey& key) { return s->core->close_model(key); }
+
+StatsSnapshot stats(trims_store* s) { return s->core->stats(); }
+
+std::shared_ptr<FastRecord> fast_record(trims_store* s, uint64_t model_id) { return s->be->fast_record(model_id); }
+
+void set_last_error(const std::string& what) { g_last_error = what; }
+
+}  // namespace trims::store_api

@@ -174,6 +174,7 @@ def main() -> None:
         run = R.run_oracle(60, 2025, 24, 800)
         json.dump({"run_oracle_seed2025_60x24x800": run}, open(os.path.join(OUT, "oracle_run.json"), "w"))
     pareto_golden(R)
+    wire_golden(R)
     print("golden vectors written to", OUT)
 
 
@@ -188,8 +189,70 @@ def pareto_golden(R) -> None:
     json.dump(cases, open(os.path.join(OUT, "pareto_trace.json"), "w"))
 
 
+# v1 wire messages (text form of csrc/wire.hpp / oracle/ref_shim.cpp) covering
+# every message type, each granularity, escapes, lists and calibration.
+WIRE_MESSAGES = [
+    "open 1 zoo resnet50 1.0.0 0 0 7",
+    "open 1 zoo vgg16 1.0.0 1 0 0",
+    "open 1 zoo vgg16-s4 1.0.0 2 4194304 18446744073709551615",
+    "open 1 my%20ns n%25ame v%C3%A9 2 64 1",
+    "openresp 1 2 98000000 4000000 102000000 1 resnet50 trims.77.arena0?dev=0&alloc=4362076160&seg=0&payload=51248352 1 "
+    "0 51220352 " + "0f" * 32,
+    "openresp 9 10 64 0 64 3 a t 5 0 64 b t 5 64 64 c t 5 128 64 " + "00" * 32,
+    "openresp 0 0 0 0 0 0 " + "ff" * 32,
+    "close 1 5 9",
+    "closeresp 5 2",
+    "stats 1",
+    "statsresp " + " ".join(str(i * 1000003) for i in range(20)) + " 2 zoo m 1.0 2 3 5 zoo n 2.0 0 1 4 "
+    "1 2 3 4 5 6 7 8 0.25 1 1.5 0.0625 3.5",
+    "statsresp " + " ".join("0" for _ in range(20)) + " 0 0 0 0 0 0 0 0 0 0.125 0",
+    "error 4 handle%2017%20not%20open",
+    "error 7 %",
+]
+
+
+def wire_golden(R) -> None:
+    """Reference-encoded v1 frames and the reference decoder's verdict on a
+    set of malformed frames (error code, or its text form)."""
+    msgs = []
+    for t in WIRE_MESSAGES:
+        rc, frame = R.wire_encode(t)
+        assert rc == 0, t
+        msgs.append({"text": t, "frame": frame.hex()})
+    rng = np.random.default_rng(20251017)
+    bad = []
+    base = [bytes.fromhex(m["frame"]) for m in msgs]
+    hand = [b"", b"\x01\x00", b"\x00\x00\x00\x00\x01", b"\x02\x00\x00\x00\x01\x02\x00",
+            (16 << 20 | 1).to_bytes(4, "little") + b"\x01", b"\x00\x00\x00\x00\x42",
+            b"\x02\x00\x00\x00\x05\x01\x00", b"\x03\x00\x00\x00\x05\x01\x00\x00"]
+    for f in hand:
+        bad.append(f)
+    for _ in range(400):  # mutations of valid frames: flips, truncations, extensions, length edits
+        f = bytearray(base[int(rng.integers(len(base)))])
+        op = int(rng.integers(4))
+        if op == 0 and len(f) > 5:
+            i = int(rng.integers(5, len(f)))
+            f[i] ^= 1 << int(rng.integers(8))
+        elif op == 1:
+            f = f[: int(rng.integers(len(f)))]
+        elif op == 2:
+            f += bytes(rng.integers(0, 256, int(rng.integers(1, 9)), dtype=np.uint8))
+        else:
+            delta = int(rng.integers(-3, 4))
+            n = max(0, int.from_bytes(f[:4], "little") + delta)
+            f[:4] = n.to_bytes(4, "little")
+        bad.append(bytes(f))
+    cases = []
+    for f in bad:
+        rc, text = R.wire_decode(f)
+        cases.append({"frame": f.hex(), "rc": rc, "text": text})
+    json.dump({"messages": msgs, "decode_cases": cases}, open(os.path.join(OUT, "wire.json"), "w"), indent=0)
+
+
 if __name__ == "__main__":
     if "--pareto-only" in sys.argv:
         pareto_golden(oracle.ref())
+    elif "--wire-only" in sys.argv:
+        wire_golden(oracle.ref())
     else:
         main()
