@@ -345,8 +345,17 @@ CudaTierBackend::CudaTierBackend(BackendConfig cfg) : cfg_(std::move(cfg)), ing_
   if (cfg_.pinned_pool_bytes) pool_ = std::make_unique<PinnedPool>(cfg_.pinned_pool_bytes);
   if (cfg_.arena_bytes) arena_ = std::make_unique<DeviceArena>(cfg_.device, cfg_.arena_bytes);
   TRIMS_CUDA(cudaStreamCreateWithFlags(&pre_stream_, cudaStreamNonBlocking));
+  cudaMemPoolProps pp{};
+  pp.allocType = cudaMemAllocationTypePinned;
+  pp.location.type = cudaMemLocationTypeDevice;
+  pp.location.id = cfg_.device;
+  TRIMS_CUDA(cudaMemPoolCreate(&pre_pool_, &pp));
+  uint64_t keep = ~0ull;
+  TRIMS_CUDA(cudaMemPoolSetAttribute(pre_pool_, cudaMemPoolAttrReleaseThreshold, &keep));
   TRIMS_CUDA(cudaEventCreate(&pre_t0_));
   TRIMS_CUDA(cudaEventCreate(&pre_done_));
+  TRIMS_CUDA(cudaEventCreateWithFlags(&pre_used_, cudaEventDisableTiming));
+  TRIMS_CUDA(cudaEventRecord(pre_used_, pre_stream_));
 }
 
 CudaTierBackend::~CudaTierBackend() {
@@ -356,13 +365,23 @@ CudaTierBackend::~CudaTierBackend() {
   host_.clear();
   DeviceGuard g(cfg_.device, /*nothrow=*/true);
   if (pre_stream_) cudaStreamSynchronize(pre_stream_);
-  if (pre_raw_) cudaFree(pre_raw_);
+  if (pre_raw_) cudaFreeAsync(pre_raw_, pre_stream_);
+  if (pre_stream_) cudaStreamSynchronize(pre_stream_);
+  if (pre_pool_) cudaMemPoolDestroy(pre_pool_);
   if (pre_stream_) cudaStreamDestroy(pre_stream_);
   if (pre_t0_) cudaEventDestroy(pre_t0_);
   if (pre_done_) cudaEventDestroy(pre_done_);
+  if (pre_used_) cudaEventDestroy(pre_used_);
 }
 
 void CudaTierBackend::release_prestage(uint64_t model_id) {
+  if (pre_owner_.load() != model_id) return;
+  if (pre_raw_) {  // back to the pool once the transform that read it is done (stream-ordered)
+    DeviceGuard g(cfg_.device, /*nothrow=*/true);
+    cudaStreamWaitEvent(pre_stream_, pre_used_, 0);
+    cudaFreeAsync(pre_raw_, pre_stream_);
+    pre_raw_ = nullptr;
+  }
   uint64_t want = model_id;
   pre_owner_.compare_exchange_strong(want, kNoOwner);
 }
@@ -422,14 +441,10 @@ void CudaTierBackend::stage_host(uint64_t model_id, const fmt::Manifest& m, cons
       // Read chunk c into the host tier while chunk c-1 uploads to the device.
       try {
         DeviceGuard g(cfg_.device);
-        if (hb.bytes > pre_cap_) {
-          TRIMS_CUDA(cudaStreamSynchronize(pre_stream_));
-          if (pre_raw_) TRIMS_CUDA(cudaFree(pre_raw_));
-          pre_raw_ = nullptr;
-          pre_cap_ = 0;
-          TRIMS_CUDA(cudaMalloc(&pre_raw_, hb.bytes));
-          pre_cap_ = hb.bytes;
-        }
+        // stream-ordered from a pool that keeps its memory: a cold open of
+        // any size reuses the blocks of earlier ones (no device-wide sync,
+        // no re-mapping)
+        TRIMS_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&pre_raw_), hb.bytes, pre_pool_, pre_stream_));
         auto r0 = std::chrono::steady_clock::now();
         TRIMS_CUDA(cudaEventRecord(pre_t0_, pre_stream_));
         parallel_pread_upload(fd, hb.p, pre_raw_, hb.bytes, off, cfg_.read_threads, cfg_.device, pre_stream_);
@@ -566,6 +581,7 @@ FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Mani
     // stage_host already streamed the raw blob to pre_raw_: transform only
     try {
       rec->checksum = ing_.from_staged(*plan, pre_raw_, pre_done_, base, &rec->bucket_sums, &rec->stats);
+      TRIMS_CUDA(cudaEventRecord(pre_used_, pre_stream_));  // from_staged returned: the reads are done
       float ms = 0;
       TRIMS_CUDA(cudaEventElapsedTime(&ms, pre_t0_, pre_done_));
       rec->stats.h2d_ms = ms;  // overlapped with the file read

@@ -180,10 +180,10 @@ class CudaTierBackend : public TierBackend {
   // concurrent cold open takes the plain path.
   static constexpr uint64_t kNoOwner = ~0ull;
   std::atomic<uint64_t> pre_owner_{kNoOwner};
-  uint8_t* pre_raw_{nullptr};
-  uint64_t pre_cap_{0};
+  uint8_t* pre_raw_{nullptr};      // from pre_pool_, owned by pre_owner_ until its publish
+  cudaMemPool_t pre_pool_{nullptr};
   cudaStream_t pre_stream_{nullptr};
-  cudaEvent_t pre_t0_{nullptr}, pre_done_{nullptr};
+  cudaEvent_t pre_t0_{nullptr}, pre_done_{nullptr}, pre_used_{nullptr};
   double pre_read_ms_{0};
   void release_prestage(uint64_t model_id);
 };

@@ -22,6 +22,8 @@ struct Net::Step {
   std::function<void(cudaStream_t)> run;
   std::function<void(cudaStream_t)> rebind;  // weight-dependent state (may be empty)
   uint32_t launches{1};
+  int branch{-1};  // >= 0: runs on the side stream as independent branch #branch
+  std::vector<int> joins;  // branches whose output this step reads: wait for them first
 };
 
 namespace {
@@ -91,6 +93,19 @@ bool implicit_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("TRIMS_IMPLICIT_CONV");
     return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
+// TRIMS_BRANCHES=1 runs independent branches on a side stream. Off by
+// default: the fork/join edges cost ResNet-50 more than the overlap gains
+// (0.336 vs 0.315 ms per forward, profiles/r02a_forward_ab.log), because the
+// shortcut GEMM then waits for its producer's full completion instead of a
+// programmatic edge.
+bool branches_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TRIMS_BRANCHES");
+    return e && std::string(e) == "1";
   }();
   return on;
 }
@@ -174,8 +189,21 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
   uint16_t* col = col_elems ? reinterpret_cast<uint16_t*>(alloc(col_elems * 2)) : nullptr;
   Act cur;
 
+  std::map<std::string, int> branch_of;  // named output -> side branch producing it
   for (size_t li = 0; li < layers.size(); ++li) {
     const LayerSpec& l = layers[li];
+    const size_t first_step = steps_.size();
+    std::vector<int> joins;
+    for (const char* ref : {"src", "res"}) {
+      auto it = branch_of.find(l.s(ref));
+      if (it != branch_of.end()) {
+        joins.push_back(it->second);
+        branch_of.erase(it);
+      }
+    }
+    auto attach_joins = [&] {
+      if (!joins.empty() && steps_.size() > first_step) steps_[first_step]->joins = joins;
+    };
     if (l.kind == "input") {
       in_hw_ = l.i("hw");
       in_c_ = l.i("c", 3);
@@ -230,6 +258,12 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       // Implicit GEMM (A read from the NHWC activation by 4-D TMA, no im2col
       // pass) whenever the channels tile by 64.
       const bool implicit = !direct && groups == 1 && cin % 64 == 0 && implicit_enabled();
+      // A conv whose output only feeds a later layer by name (the next layer
+      // reads its own `src`, e.g. ResNet's downsample shortcut) is an
+      // independent branch: it runs on a side stream concurrently with the
+      // main path and is joined by the first layer that references it.
+      const bool branch = branches_enabled() && groups == 1 && (direct || implicit) && !l.s("out").empty() &&
+                          li + 1 < layers.size() && !layers[li + 1].s("src").empty();
       bool first_group = true;
       for (int gi = 0; gi < groups; ++gi) {
         const uint16_t* A = direct ? in.p : col;
@@ -267,11 +301,13 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
           if (do_params) bind_params(s);
         };
         steps_.push_back(std::make_unique<Step>(Step{[prep](cudaStream_t s) { gemm::run(*prep, s); }, rebind}));
+        if (branch) steps_.back()->branch = nbranches_;
         first_group = false;
       }
       flops_ += 2.0 * double(M) * cout * rsc;
+      if (branch) branch_of[l.s("out")] = nbranches_++;
       if (!l.s("out").empty()) named[l.s("out")] = out;
-      cur = out;
+      if (!branch) cur = out;
     } else if (l.kind == "pool_max") {
       const int k = l.i("k"), st = l.i("stride", k), pad = l.i("pad", 0);
       const Act in = cur;
@@ -349,12 +385,21 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
     } else {
       raise(Errc::InvalidArgument, "unknown layer kind " + l.kind);
     }
+    attach_joins();
   }
+  if (!branch_of.empty()) raise(Errc::InvalidArgument, "a branch output is never consumed");
   if (!logits_) raise(Errc::InvalidArgument, "architecture has no fc output");
   for (const auto& s : steps_) launches_ += s->launches;
   for (const auto& f : folds_) max_fold_c_ = std::max(max_fold_c_, f.C);
   if (!folds_.empty()) d_jobs_ = reinterpret_cast<FoldJob*>(alloc(folds_.size() * sizeof(FoldJob)));
   TRIMS_CUDA(cudaStreamCreateWithFlags(&capture_stream_, cudaStreamNonBlocking));
+  if (nbranches_) {
+    TRIMS_CUDA(cudaStreamCreateWithFlags(&side_stream_, cudaStreamNonBlocking));
+    fork_ev_.resize(size_t(nbranches_));
+    join_ev_.resize(size_t(nbranches_));
+    for (auto* v : {&fork_ev_, &join_ev_})
+      for (auto& e : *v) TRIMS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   rebind(weights);
 }
 
@@ -363,6 +408,9 @@ Net::~Net() {
   if (exec_) cudaGraphExecDestroy(exec_);
   if (graph_) cudaGraphDestroy(graph_);
   if (capture_stream_) cudaStreamDestroy(capture_stream_);
+  if (side_stream_) cudaStreamDestroy(side_stream_);
+  for (auto* v : {&fork_ev_, &join_ev_})
+    for (auto e : *v) cudaEventDestroy(e);
   for (void* p : owned_) cudaFree(p);
 }
 
@@ -416,7 +464,18 @@ void Net::capture_graph() {
 }
 
 void Net::record(cudaStream_t stream) {
-  for (const auto& s : steps_) s->run(stream);
+  for (const auto& s : steps_) {
+    for (int j : s->joins) TRIMS_CUDA(cudaStreamWaitEvent(stream, join_ev_[size_t(j)], 0));
+    if (s->branch >= 0) {  // fork: the side stream starts from the main stream's current point
+      const size_t b = size_t(s->branch);
+      TRIMS_CUDA(cudaEventRecord(fork_ev_[b], stream));
+      TRIMS_CUDA(cudaStreamWaitEvent(side_stream_, fork_ev_[b], 0));
+      s->run(side_stream_);
+      TRIMS_CUDA(cudaEventRecord(join_ev_[b], side_stream_));
+    } else {
+      s->run(stream);
+    }
+  }
 }
 
 void Net::run(cudaStream_t stream, bool use_graph) {

@@ -85,6 +85,10 @@ class Net {
   cudaGraph_t graph_{nullptr};
   cudaGraphExec_t exec_{nullptr};
   cudaStream_t capture_stream_{nullptr};
+  // independent branches (ResNet shortcuts) run on a side stream, fork/join by events
+  int nbranches_{0};
+  cudaStream_t side_stream_{nullptr};
+  std::vector<cudaEvent_t> fork_ev_, join_ev_;
   // BN folds of every layer, batched into one launch per rebind: offsets of
   // gamma/beta/mean/var in the resident blob + destination buffers.
   struct Fold {
