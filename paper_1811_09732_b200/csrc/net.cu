@@ -359,7 +359,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       auto bind_bias = [=](cudaStream_t s) {
         if (bias) bf16_to_f32(wptr(b_off), bias, cout, s);
       };
-      if (batch <= 8) {  // HBM-bound GEMV: weights streamed once
+      if (batch <= 8 && cin % 256 == 0) {  // HBM-bound GEMV: weights streamed once
         steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) {
           nn::gemv(in.p, batch, cin, wptr(w_off), cout, bias, relu, out.p, lg, cout, sms, s);
         }, bind_bias}));

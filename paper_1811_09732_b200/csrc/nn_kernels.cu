@@ -5,6 +5,8 @@
 // folding into per-channel fp32 scale/shift, and softmax.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "cuda_util.hpp"
 #include "nn.hpp"
 
@@ -196,51 +198,94 @@ __global__ void flatten_nchw_kernel(const uint16_t* __restrict__ in, uint16_t* _
   }
 }
 
-// Small-batch FC: out[m, n] = relu?(sum_k x[m,k] W[n,k] + bias[n]). One warp
-// per output row n, 128-bit weight loads streamed once (HBM-bound).
-template <int MB>
+// Small-batch FC: out[m, n] = relu?(sum_k x[m,k] W[n,k] + bias[n]), HBM-bound
+// on the weights, which are streamed exactly once. A block owns R consecutive
+// rows, i.e. one contiguous R*K region of W, and its 8 warps sweep that region
+// linearly in 512-byte pieces (warp w takes pieces w, w+8, ...), 16 pieces in
+// flight per lane: each block is one sequential DRAM stream, not R*8
+// interleaved row streams (measured: the per-row mapping capped at ~3.3 TB/s).
+// A piece never straddles rows (K % 256 == 0); a warp flushes its running sum
+// when its row changes, into a per-(row, warp) slot summed in a fixed order.
+// The head of the block's region is prefetched into L2 before waiting on the
+// previous layer.
+constexpr int kGemvRows = 8;
+template <int MB, int kGemvUnroll>
 __global__ void __launch_bounds__(256) gemv_kernel(const uint16_t* __restrict__ x, int M, int K,
                                                    const uint16_t* __restrict__ Wt, int N, const float* __restrict__ bias,
                                                    int relu, uint16_t* __restrict__ out_bf, float* __restrict__ out_f32,
-                                                   int ldo) {
-  pdl_wait();  // reads the previous layer's output / writes shared scratch
+                                                   int ldo, int R) {
+  __shared__ float red[kGemvRows][8][MB];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * R, rows = min(R, N - n0);
+  const int ppr = K / 256, pieces = rows * ppr;  // 256-element pieces per row / in the block
+  const uint16_t* base = Wt + uint64_t(n0) * K;
+  for (int i = threadIdx.x; i < kGemvRows * 8 * MB; i += blockDim.x) reinterpret_cast<float*>(red)[i] = 0.f;
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = uint32_t(min(pieces, 128)) * 512;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base), "r"(bytes) : "memory");
+  }
+  pdl_wait();  // x is the previous layer's output
   pdl_trigger();
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int n = warp; n < N; n += nwarps) {
-    float acc[MB];
+  __syncthreads();
+  float acc[MB];
 #pragma unroll
-    for (int m = 0; m < MB; ++m) acc[m] = 0.f;
-    const uint16_t* wr = Wt + uint64_t(n) * K;
-#pragma unroll 4
-    for (int k = lane * 8; k < K; k += 32 * 8) {
-      const uint4 wv = __ldg(reinterpret_cast<const uint4*>(wr + k));
-      const uint32_t w[4] = {wv.x, wv.y, wv.z, wv.w};
-#pragma unroll
-      for (int m = 0; m < MB; ++m) {
-        if (m >= M) break;
-        const uint4 xv = __ldg(reinterpret_cast<const uint4*>(x + uint64_t(m) * K + k));
-        const uint32_t xx[4] = {xv.x, xv.y, xv.z, xv.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          acc[m] = fmaf(bf(uint16_t(w[j] & 0xffff)), bf(uint16_t(xx[j] & 0xffff)), acc[m]);
-          acc[m] = fmaf(bf(uint16_t(w[j] >> 16)), bf(uint16_t(xx[j] >> 16)), acc[m]);
-        }
-      }
-    }
+  for (int m = 0; m < MB; ++m) acc[m] = 0.f;
+  int cur = 0;  // block-local row of the running sums
+  auto flush = [&](int next) {
 #pragma unroll
     for (int m = 0; m < MB; ++m) {
-      if (m >= M) break;
       float v = acc[m];
 #pragma unroll
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) {
-        if (bias) v += bias[n];
-        if (relu) v = fmaxf(v, 0.f);
-        if (out_f32) out_f32[uint64_t(m) * ldo + n] = v;
-        else out_bf[uint64_t(m) * ldo + n] = to_bf(v);
+      if (lane == 0) red[cur][warp][m] += v;
+      acc[m] = 0.f;
+    }
+    cur = next;
+  };
+  auto fma8 = [&](const uint4 wv, int col) {
+    const uint32_t w[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+    for (int m = 0; m < MB; ++m) {
+      if (m >= M) break;
+      const uint4 xv = __ldg(reinterpret_cast<const uint4*>(x + uint64_t(m) * K + col));
+      const uint32_t xx[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[m] = fmaf(bf(uint16_t(w[j] & 0xffff)), bf(uint16_t(xx[j] & 0xffff)), acc[m]);
+        acc[m] = fmaf(bf(uint16_t(w[j] >> 16)), bf(uint16_t(xx[j] >> 16)), acc[m]);
       }
     }
+  };
+  for (int p0 = warp; p0 < pieces; p0 += 8 * kGemvUnroll) {  // kGemvUnroll pieces of this warp per step
+    uint4 wv[kGemvUnroll];
+#pragma unroll
+    for (int u = 0; u < kGemvUnroll; ++u) {
+      const int p = p0 + 8 * u;
+      if (p < pieces)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(wv[u].x), "=r"(wv[u].y), "=r"(wv[u].z), "=r"(wv[u].w)
+                     : "l"(base + uint64_t(p) * 256 + lane * 8));
+    }
+#pragma unroll
+    for (int u = 0; u < kGemvUnroll; ++u) {
+      const int p = p0 + 8 * u;
+      if (p >= pieces) break;
+      const int row = p / ppr;  // warp-uniform
+      if (row != cur) flush(row);
+      fma8(wv[u], (p - row * ppr) * 256 + lane * 8);
+    }
+  }
+  flush(0);
+  __syncthreads();
+  if (threadIdx.x >= rows) return;
+  const int r = threadIdx.x, n = n0 + r;
+  for (int m = 0; m < M && m < MB; ++m) {
+    float v = 0.f;
+    for (int w = 0; w < 8; ++w) v += red[r][w][m];  // fixed order: deterministic
+    if (bias) v += bias[n];
+    if (relu) v = fmaxf(v, 0.f);
+    if (out_f32) out_f32[uint64_t(m) * ldo + n] = v;
+    else out_bf[uint64_t(m) * ldo + n] = to_bf(v);
   }
 }
 
@@ -343,12 +388,30 @@ void flatten_nchw(const uint16_t* in, uint16_t* out, int N, int HW, int C, cudaS
 
 void gemv(const uint16_t* x, int M, int K, const uint16_t* W, int N, const float* bias, bool relu, uint16_t* out_bf,
           float* out_f32, int ldo, int sms, cudaStream_t s) {
-  if (K % 8) raise(Errc::InvalidArgument, "gemv needs K % 8 == 0");
-  const unsigned grid = unsigned(std::min<int>((N + 7) / 8, sms * 8));
-  if (M <= 1) launch_pdl(gemv_kernel<1>, dim3(grid), dim3(256), 0, s, x, M, K, W, N, bias, relu, out_bf, out_f32, ldo);
-  else if (M <= 4) launch_pdl(gemv_kernel<4>, dim3(grid), dim3(256), 0, s, x, M, K, W, N, bias, relu, out_bf, out_f32, ldo);
-  else if (M <= 8) launch_pdl(gemv_kernel<8>, dim3(grid), dim3(256), 0, s, x, M, K, W, N, bias, relu, out_bf, out_f32, ldo);
-  else raise(Errc::InvalidArgument, "gemv is for M <= 8");
+  if (K % 256) raise(Errc::InvalidArgument, "gemv needs K % 256 == 0");
+  // rows per block: 8, or fewer when that leaves fewer than 2 blocks per SM
+  // (TRIMS_GEMV_R / TRIMS_GEMV_U override rows per block / loads in flight)
+  static const int r_env = std::getenv("TRIMS_GEMV_R") ? std::atoi(std::getenv("TRIMS_GEMV_R")) : 0;
+  static const int u_env = std::getenv("TRIMS_GEMV_U") ? std::atoi(std::getenv("TRIMS_GEMV_U")) : 8;
+  int R = kGemvRows;
+  while (R > 2 && (N + R - 1) / R < 2 * sms) R /= 2;
+  if (r_env >= 1 && r_env <= kGemvRows) R = r_env;
+  const unsigned grid = unsigned((N + R - 1) / R);
+  auto go = [&](auto k) { launch_pdl(k, dim3(grid), dim3(256), 0, s, x, M, K, W, N, bias, relu, out_bf, out_f32, ldo, R); };
+  if (M > 8) raise(Errc::InvalidArgument, "gemv is for M <= 8");
+  if (u_env == 4) {
+    if (M <= 1) go(gemv_kernel<1, 4>);
+    else if (M <= 4) go(gemv_kernel<4, 4>);
+    else go(gemv_kernel<8, 4>);
+  } else if (u_env == 16) {
+    if (M <= 1) go(gemv_kernel<1, 16>);
+    else if (M <= 4) go(gemv_kernel<4, 16>);
+    else go(gemv_kernel<8, 16>);
+  } else {
+    if (M <= 1) go(gemv_kernel<1, 8>);
+    else if (M <= 4) go(gemv_kernel<4, 8>);
+    else go(gemv_kernel<8, 8>);
+  }
   TRIMS_CUDA(cudaGetLastError());
 }
 
