@@ -242,7 +242,12 @@ def run_ours(args):
     # ---- BASELINE configs[2] + [4]: 37-model mix / FaaS traces under memory pressure
     mix = None if args.quick else mix_traces(dev, rank, world)
 
-    peer = peer_serve(work, arch, dev, rank, world, args.steps) if world > 1 else None
+    peer = None
+    if world > 1:
+        try:
+            peer = peer_serve(work, arch, dev, rank, world, args.steps)
+        except Exception as e:  # report, keep the rest of the line (the driver needs it)
+            peer = {"error": repr(e)[:300]}
 
     hbm_peak, peak_kind = peaks()
     algo = info["read_bytes"] + info["write_bytes"]
