@@ -96,7 +96,10 @@ Ingestor::Ingestor(int device) : device_(device) {
   TRIMS_CUDA(cudaEventCreateWithFlags(&side_.fork, cudaEventDisableTiming));
   TRIMS_CUDA(cudaEventCreateWithFlags(&side_.join, cudaEventDisableTiming));
   TRIMS_CUDA(cudaMalloc(&side_.sched, 2 * ingest::kSchedSlots * sizeof(unsigned int)));
-  TRIMS_CUDA(cudaMemset(side_.sched, 0, 2 * ingest::kSchedSlots * sizeof(unsigned int)));
+  // ordered before every launch of this Ingestor: compute_ is a non-blocking
+  // stream, so a legacy-stream memset would not be
+  TRIMS_CUDA(cudaMemsetAsync(side_.sched, 0, 2 * ingest::kSchedSlots * sizeof(unsigned int), compute_));
+  TRIMS_CUDA(cudaStreamSynchronize(compute_));
   events_.resize(512);
   for (auto& e : events_) TRIMS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (auto* e : {&t0_, &t1_, &c0_, &c1_}) TRIMS_CUDA(cudaEventCreate(e));
@@ -172,6 +175,10 @@ std::shared_ptr<IngestPlan> Ingestor::compile(const fmt::Manifest& src, const fm
     };
     upload(&p->d_tiles, p->plan.dev_tiles);
     upload(&p->d_tiles_k, p->plan.dev_tiles_k);
+    // A pageable-memory cudaMemcpy may return before its DMA lands, and the
+    // ingest kernels run on non-blocking streams that do not order after the
+    // legacy stream: wait for the tables here (a cold open once raced this).
+    TRIMS_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
   }
   return p;
 }
@@ -526,6 +533,7 @@ FastPublication CudaTierBackend::seal(uint64_t model_id, std::shared_ptr<FastRec
   {
     DeviceGuard g(cfg_.device);
     TRIMS_CUDA(cudaMemcpy(base + rb, tail.data(), tail.size(), cudaMemcpyHostToDevice));
+    TRIMS_CUDA(cudaStreamSynchronize(cudaStreamLegacy));  // sealed before anyone can see the segment
   }
 
   FastPublication pub;
