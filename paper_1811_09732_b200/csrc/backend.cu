@@ -352,6 +352,7 @@ CudaTierBackend::CudaTierBackend(BackendConfig cfg) : cfg_(std::move(cfg)), ing_
   if (cfg_.pinned_pool_bytes) pool_ = std::make_unique<PinnedPool>(cfg_.pinned_pool_bytes);
   if (cfg_.arena_bytes) arena_ = std::make_unique<DeviceArena>(cfg_.device, cfg_.arena_bytes);
   TRIMS_CUDA(cudaStreamCreateWithFlags(&pre_stream_, cudaStreamNonBlocking));
+  TRIMS_CUDA(cudaStreamCreateWithFlags(&d2h_stream_, cudaStreamNonBlocking));
   cudaMemPoolProps pp{};
   pp.allocType = cudaMemAllocationTypePinned;
   pp.location.type = cudaMemLocationTypeDevice;
@@ -376,6 +377,7 @@ CudaTierBackend::~CudaTierBackend() {
   if (pre_stream_) cudaStreamSynchronize(pre_stream_);
   if (pre_pool_) cudaMemPoolDestroy(pre_pool_);
   if (pre_stream_) cudaStreamDestroy(pre_stream_);
+  if (d2h_stream_) cudaStreamDestroy(d2h_stream_);
   if (pre_t0_) cudaEventDestroy(pre_t0_);
   if (pre_done_) cudaEventDestroy(pre_done_);
   if (pre_used_) cudaEventDestroy(pre_used_);
@@ -416,6 +418,11 @@ fmt::Manifest CudaTierBackend::read_manifest(const fmt::ModelKey& key, const std
 }
 
 void CudaTierBackend::free_host(HostBuf& h) {
+  if (h.ready) {  // a resident-form D2H may still be writing it
+    cudaEventSynchronize(h.ready);
+    cudaEventDestroy(h.ready);
+    h.ready = nullptr;
+  }
   if (!h.p) return;
   if (h.pooled) pool_->free(h.p);
   else cudaFreeHost(h.p);
@@ -602,14 +609,26 @@ FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Mani
     release_prestage(model_id);
   } else if (from_host) {
     const uint8_t* src = nullptr;
+    bool resident = false;
+    cudaEvent_t ready = nullptr;
     {
       std::lock_guard lk(mu_);
       auto it = host_.find(model_id);
       if (it == host_.end()) raise(Errc::Internal, "host buffer missing for publish");
       if (it->second.bytes != m.blob_bytes) raise(Errc::Internal, "host buffer size mismatch");
       src = it->second.p;  // single-flight pins the entry while loading
+      resident = it->second.resident;
+      ready = it->second.ready;
     }
-    rec->checksum = ing_.from_host(*plan, src, base, &rec->bucket_sums, &rec->stats);
+    if (resident) {
+      // The host tier already holds the resident blob: copy it straight into
+      // the segment and hash it (the identity plan of the resident manifest).
+      if (ready) TRIMS_CUDA(cudaEventSynchronize(ready));
+      std::shared_ptr<IngestPlan> ident = pull_plan_for(model_id, rec->resident);
+      rec->checksum = ing_.from_host(*ident, src, base, &rec->bucket_sums, &rec->stats);
+    } else {
+      rec->checksum = ing_.from_host(*plan, src, base, &rec->bucket_sums, &rec->stats);
+    }
   } else {
     int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
     if (fd < 0) raise(Errc::NotFound, path);
@@ -627,7 +646,23 @@ FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Mani
     ::close(fd);
   }
   rec->stats.alloc_ms = alloc_ms;
+  if (cfg_.resident_host_tier && !plan->identity) to_resident_form(model_id, *rec, *plan);
   return seal(model_id, std::move(rec), m);
+}
+
+// Replace a staged raw host copy with the resident blob just published
+// (async D2H on its own stream; evictions of either tier wait for it).
+void CudaTierBackend::to_resident_form(uint64_t model_id, const FastRecord& rec, const IngestPlan& plan) {
+  std::lock_guard lk(mu_);
+  auto it = host_.find(model_id);
+  if (it == host_.end() || it->second.resident || rec.resident.blob_bytes > it->second.bytes) return;
+  HostBuf& hb = it->second;
+  DeviceGuard g(cfg_.device);
+  if (!hb.ready) TRIMS_CUDA(cudaEventCreateWithFlags(&hb.ready, cudaEventDisableTiming));
+  TRIMS_CUDA(cudaMemcpyAsync(hb.p, rec.base(), rec.resident.blob_bytes, cudaMemcpyDeviceToHost, d2h_stream_));
+  TRIMS_CUDA(cudaEventRecord(hb.ready, d2h_stream_));
+  hb.resident = true;
+  (void)plan;
 }
 
 // Multi-GPU extension: fill this GPU's fast tier from a peer's
@@ -690,6 +725,11 @@ void CudaTierBackend::evict_fast(uint64_t model_id) {
     if (it == fast_.end()) return;
     victim = std::move(it->second);
     fast_.erase(it);
+  }
+  {
+    std::lock_guard lk(mu_);  // a resident-form D2H may still be reading the segment
+    auto h = host_.find(model_id);
+    if (h != host_.end() && h->second.ready) cudaEventSynchronize(h->second.ready);
   }
   if (cfg_.directory) cfg_.directory->retract(victim->key);  // before the scrub: peers stop choosing it
   if (victim->arena) {

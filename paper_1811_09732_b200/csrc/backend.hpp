@@ -107,6 +107,11 @@ struct BackendConfig {
   unsigned read_threads{8};
   uint64_t arena_bytes{0};  // HBM arena for the fast tier (0 = one cuMem allocation per model)
   std::shared_ptr<Directory> directory;  // multi-GPU: publish sealed segments for peers (null = single GPU)
+  // Keep the host tier in the RESIDENT form: after a converting publish, the
+  // host copy is replaced (async D2H) by the converted blob, so a later warm
+  // reload moves the bf16 bytes over PCIe (half of fp32) and only hashes them.
+  // Off when the host copy is dropped on close anyway (eager reclaim).
+  bool resident_host_tier{true};
 };
 
 // Fast-tier record of one published model: a range of the arena, or a
@@ -154,7 +159,10 @@ class CudaTierBackend : public TierBackend {
     uint8_t* p{nullptr};
     uint64_t bytes{0};
     bool pooled{false};
+    bool resident{false};          // holds the resident (converted) blob, valid once `ready` fires
+    cudaEvent_t ready{nullptr};    // the D2H that wrote it (null: raw artifact bytes)
   };
+  void to_resident_form(uint64_t model_id, const FastRecord& rec, const IngestPlan& plan);
   void free_host(HostBuf& h);
 
   std::shared_ptr<IngestPlan> plan_for(uint64_t model_id, const fmt::Manifest& m);
@@ -183,6 +191,7 @@ class CudaTierBackend : public TierBackend {
   uint8_t* pre_raw_{nullptr};      // from pre_pool_, owned by pre_owner_ until its publish
   cudaMemPool_t pre_pool_{nullptr};
   cudaStream_t pre_stream_{nullptr};
+  cudaStream_t d2h_stream_{nullptr};  // host tier -> resident form
   cudaEvent_t pre_t0_{nullptr}, pre_done_{nullptr}, pre_used_{nullptr};
   double pre_read_ms_{0};
   void release_prestage(uint64_t model_id);

@@ -376,6 +376,7 @@ BackendConfig backend_config(const trims_store_config* cfg) {
   bc.arena_bytes = cfg->arena_bytes == 1 ? 0
                    : cfg->arena_bytes ? cfg->arena_bytes
                                       : cfg->fast_capacity_bytes + cfg->fast_capacity_bytes / 16 + (64ull << 20);
+  bc.resident_host_tier = cfg->eager_reclaim == 0;
   return bc;
 }
 
