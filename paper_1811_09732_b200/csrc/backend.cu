@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <condition_variable>
 #include <cstring>
 #include <filesystem>
 #include <mutex>
@@ -48,40 +49,60 @@ void parallel_pread(int fd, uint8_t* dst, uint64_t len, uint64_t off, unsigned t
 }
 
 // Reads [off, off+len) into the pinned host buffer in 4 MiB pieces handed out
-// to `threads` readers; each reader uploads its piece to `dev` right after
-// reading it (async on `stream`), so the PCIe copy of the blob runs under the
-// file read instead of after it.
+// to `threads` readers, while the calling thread uploads the pieces to `dev`
+// in order as they land (async on `stream`): the PCIe copy of the blob runs
+// under the file read instead of after it, and one thread owns the stream
+// (readers issuing their own copies contended in the driver).
 void parallel_pread_upload(int fd, uint8_t* host, uint8_t* dev, uint64_t len, uint64_t off, unsigned threads,
                            int device, cudaStream_t stream) {
   constexpr uint64_t kPiece = 4ull << 20;
   const uint64_t pieces = (len + kPiece - 1) / kPiece;
   std::atomic<uint64_t> next{0};
   std::atomic<bool> ok{true};
-  std::string err;
-  std::mutex err_mu;
-  auto worker = [&] {
-    try {
-      DeviceGuard g(device);
-      for (uint64_t i; ok.load() && (i = next.fetch_add(1)) < pieces;) {
-        const uint64_t b = i * kPiece, e = std::min(len, b + kPiece);
-        for (uint64_t at = b; at < e;) {
-          ssize_t r = ::pread(fd, host + at, size_t(e - at), off_t(off + at));
-          if (r <= 0) raise(Errc::Corrupt, "blob truncated (short read)");
-          at += uint64_t(r);
+  std::unique_ptr<std::atomic<uint8_t>[]> ready(new std::atomic<uint8_t>[pieces]);
+  for (uint64_t i = 0; i < pieces; ++i) ready[i].store(0, std::memory_order_relaxed);
+  std::mutex mu;
+  std::condition_variable cv;
+  auto reader = [&] {
+    for (uint64_t i; ok.load() && (i = next.fetch_add(1)) < pieces;) {
+      const uint64_t e = std::min(len, (i + 1) * kPiece);
+      for (uint64_t at = i * kPiece; at < e;) {
+        ssize_t r = ::pread(fd, host + at, size_t(e - at), off_t(off + at));
+        if (r <= 0) {
+          ok = false;
+          break;
         }
-        TRIMS_CUDA(cudaMemcpyAsync(dev + b, host + b, e - b, cudaMemcpyHostToDevice, stream));
+        at += uint64_t(r);
       }
-    } catch (const std::exception& x) {
-      std::lock_guard lk(err_mu);
-      if (ok.exchange(false)) err = x.what();
+      {
+        std::lock_guard lk(mu);
+        ready[i].store(1, std::memory_order_release);
+      }
+      cv.notify_one();
     }
   };
   const unsigned n = unsigned(std::clamp<uint64_t>(pieces, 1, std::max(1u, threads)));
   std::vector<std::thread> ts;
-  for (unsigned i = 1; i < n; ++i) ts.emplace_back(worker);
-  worker();
+  for (unsigned i = 0; i < n; ++i) ts.emplace_back(reader);
+  std::string err;
+  try {
+    DeviceGuard g(device);
+    for (uint64_t i = 0; i < pieces && ok.load(); ++i) {
+      {
+        std::unique_lock lk(mu);
+        cv.wait(lk, [&] { return ready[i].load(std::memory_order_acquire) || !ok.load(); });
+      }
+      if (!ok.load()) break;
+      const uint64_t b = i * kPiece, e = std::min(len, b + kPiece);
+      TRIMS_CUDA(cudaMemcpyAsync(dev + b, host + b, e - b, cudaMemcpyHostToDevice, stream));
+    }
+  } catch (const std::exception& x) {
+    ok = false;
+    err = x.what();
+  }
+  cv.notify_all();
   for (auto& t : ts) t.join();
-  if (!ok) raise(Errc::Corrupt, err);
+  if (!ok) raise(Errc::Corrupt, err.empty() ? "blob truncated (short read)" : err);
 }
 
 // ---------------------------------------------------------------------------
