@@ -236,6 +236,17 @@ def run_ours(args):
         alex = C.ARCHS["alexnet"]()
         C.write_arch(alex, work, seed=1)
         lat["alexnet"] = request_latencies(work, alex, dev)  # BASELINE configs[0]: AlexNet cold then hot
+        vgg19 = C.ARCHS["vgg19"]()
+        C.write_arch(vgg19, work, seed=1)
+        lat["vgg19"] = request_latencies(work, vgg19, dev)  # BASELINE configs[3]
+
+    # ---- BASELINE configs[3]: a multi-GB model (large8 vgg16-s4, 6.4 GB)
+    large = None
+    if not args.quick:
+        try:
+            large = large_model(work, dev)
+        except Exception as e:  # report, keep the line
+            large = {"error": repr(e)[:300]}
 
     # ---- BASELINE configs[1]: 16 client processes on one shared HBM copy
     shared = None if args.quick else shared_clients(work, arch, dev, n_clients=16, n_reqs=args.steps * 5)
@@ -279,6 +290,8 @@ def run_ours(args):
         line["shared_clients"] = shared
     if mix:
         line["traces"] = mix
+    if large:
+        line["large_model"] = large
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(src_json, blob, res_json)
     if rank == 0:
@@ -564,6 +577,57 @@ def request_latencies(work: str, arch, dev: int, batch: int = 1, reps: int = 7) 
         out["kernels_per_forward"] = net.launches
         cli.close(v)
     nets["net"].close()
+    return out
+
+
+def large_model(work: str, dev: int, reps: int = 3) -> dict:
+    """BASELINE configs[3]'s multi-GB synthetic model (the reference's large8
+    catalog entry vgg16-s4, 6.408 GB, catalog.cpp:62-66): cold (disk), warm
+    (host tier) and hot (HBM) opens through the public API, each followed by
+    the GPU compute step over every weight byte (the block-checksum pass, the
+    role of Client::touch); identity plan, as the reference stores it."""
+    import statistics
+
+    from paper_1811_09732_b200 import catalog as C
+    from paper_1811_09732_b200 import workload as W
+    from paper_1811_09732_b200.store import Store, StoreOptions
+    d = os.path.join(work, "large8")
+    C.gen_catalog("large8", d, seed=1, only=["vgg16-s4"])
+    m = [x for x in C.catalog("large8")[0] if x.name == "vgg16-s4"][0]
+    key = C.catalog_key(m)
+    touch = W.DeviceTouch(dev)
+    cap = 8 << 30
+    out = {"model": "large8/vgg16-s4", "blob_bytes": None}
+
+    def one(s):
+        t0 = time.perf_counter()
+        ex = s.open(key)
+        t1 = time.perf_counter()
+        touch(ex.dev_ptr, ex.resident_blob_bytes)
+        t2 = time.perf_counter()
+        s.close(key)
+        out["blob_bytes"] = int(ex.resident_blob_bytes)
+        return (t2 - t0) * 1e3, (t1 - t0) * 1e3, (t2 - t1) * 1e3
+
+    with Store(StoreOptions(disk_cache_dir=d, fast_capacity_bytes=cap, host_capacity_bytes=cap, device=dev,
+                            eager_reclaim=True)) as s:
+        cold = [one(s) for _ in range(reps)]
+    with Store(StoreOptions(disk_cache_dir=d, fast_capacity_bytes=cap, host_capacity_bytes=cap, device=dev)) as s:
+        one(s)
+        warm = []
+        for _ in range(reps):
+            s.reclaim(0, cap)
+            warm.append(one(s))
+        hot = [one(s) for _ in range(reps)]
+    med = lambda xs, i: round(statistics.median(x[i] for x in xs), 3)
+    for name, xs in (("cold", cold), ("warm", warm), ("hot", hot)):
+        out[name] = {"e2e_ms": med(xs, 0), "open_ms": med(xs, 1), "compute_ms": med(xs, 2)}
+    b = out["blob_bytes"]
+    out["warm_open_GBps"] = round(b / (out["warm"]["open_ms"] / 1e3) / 1e9, 2)
+    out["cold_open_GBps"] = round(b / (out["cold"]["open_ms"] / 1e3) / 1e9, 2)
+    out["compute_GBps"] = round(b / (out["hot"]["compute_ms"] / 1e3) / 1e9, 1)
+    import shutil
+    shutil.rmtree(d, ignore_errors=True)
     return out
 
 
