@@ -653,6 +653,19 @@ def pcie_h2d_gbs(dev: int) -> float:
     return best
 
 
+def host_info() -> dict:
+    """The box's host CPU (report nproc and the CPU model beside the CPU baseline)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"host_nproc": os.cpu_count(), "host_cpu": model}
+
+
 def cpu_baseline(src_json, blob, res_json) -> dict:
     """Our C port of the same transform (oracle, 1 core) on a bounded sample."""
     import numpy as np
@@ -668,7 +681,7 @@ def cpu_baseline(src_json, blob, res_json) -> dict:
     dt = time.perf_counter() - t0
     return {"value": round(n * blob.size / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",
             "sample": f"{n} full pass(es) of the ResNet-50 fp32 blob through oracle/trims_oracle.c "
-                      f"(convert+permute, numpy glue), {dt:.2f} s"}
+                      f"(convert+permute, numpy glue), {dt:.2f} s", **host_info()}
 
 
 def run_reference(args):
@@ -709,7 +722,8 @@ def run_reference(args):
                    "reference_step": "ShmTierBackend::publish_fast(from_host) host vector -> sealed shm segment "
                                      "(daemon.cpp:160-209); the reference does no dtype/layout conversion"},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
-                         "sample": f"{args.steps} publish_fast calls on the {blob.size} B ResNet-50 blob"},
+                         "sample": f"{args.steps} publish_fast calls on the {blob.size} B ResNet-50 blob",
+                         **host_info()},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "latency_ms": lat,
     }
