@@ -703,7 +703,19 @@ def run_reference(args):
         r = R.ingest(path, 1)
         t.append(r["publish_s"])
     total = sum(t)
-    value = args.steps * blob.size / total / 1e9
+    value_1 = args.steps * blob.size / total / 1e9
+    # all the host threads it can use: the daemon publishes concurrently for
+    # distinct models (one thread per connection); aggregate over T callers
+    cores = 1
+    value = value_1
+    threads = min(os.cpu_count() or 1, 16)
+    while threads > 1:
+        agg, used = R.ingest_parallel(path, threads, max(1, min(args.steps, 5)))
+        if agg:
+            if agg > value:
+                value, cores = agg, used
+            break
+        threads //= 2  # e.g. /dev/shm too small for that many segments
     lat = {}
     from paper_1811_09732_b200 import catalog as C
     key = C.arch_key(arch)
@@ -712,7 +724,6 @@ def run_reference(args):
         lat[f"{mode}_open"] = round(r["open_s"] * 1e3, 3)
         lat[f"{mode}_e2e_with_touch"] = round(r["end_to_end_s"] * 1e3, 3)
     traces = None if args.quick else reference_traces(R)
-    cores = 1
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3),
@@ -722,7 +733,8 @@ def run_reference(args):
                    "reference_step": "ShmTierBackend::publish_fast(from_host) host vector -> sealed shm segment "
                                      "(daemon.cpp:160-209); the reference does no dtype/layout conversion"},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
-                         "sample": f"{args.steps} publish_fast calls on the {blob.size} B ResNet-50 blob",
+                         "sample": f"{args.steps} single-thread publish_fast calls ({value_1:.3f} GB/s) and "
+                                   f"rounds of {cores} concurrent publishes of the {blob.size} B ResNet-50 blob",
                          **host_info()},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "latency_ms": lat,

@@ -170,6 +170,7 @@ class _Ref:
         L.ref_trace.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint32), ctypes.c_uint32,
                                 ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(ctypes.c_double),
                                 _u64p]
+        L.ref_ingest_parallel.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
         L.ref_wire_encode_text.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_uint64, _u64p]
         L.ref_wire_decode_text.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_uint64]
         L.ref_wire_request.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_uint64]
@@ -263,6 +264,11 @@ class _Ref:
         out = (ctypes.c_double * 3)()
         self._check(self.L.ref_ingest(path.encode(), reps, out), "ingest")
         return {"stage_s": out[0], "publish_s": out[1], "blob_bytes": int(out[2])}
+
+    def ingest_parallel(self, path: str, threads: int, reps: int = 3):
+        out = (ctypes.c_double * 2)()
+        rc = self.L.ref_ingest_parallel(path.encode(), threads, reps, out)
+        return (out[0], int(out[1])) if rc == 0 else (None, 0)
 
     def latency(self, dir: str, key, mode: str, reps: int = 5):
         out = (ctypes.c_double * 6)()

@@ -19,6 +19,7 @@
 #include <fstream>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "mrm/bench/catalog.hpp"
@@ -538,6 +539,42 @@ int ref_ingest(const char* path, int reps, double* out) {
     out[0] = st[st.size() / 2];
     out[1] = pu[pu.size() / 2];
     out[2] = double(m.blob_bytes);
+    return 0;
+  });
+}
+
+// The same publish path driven by `threads` concurrent callers, as the
+// reference daemon's per-connection threads would (distinct model ids, one
+// ShmTierBackend): aggregate bytes/second of publish_fast over `reps` rounds.
+// out: [aggregate GB/s of the publishes, threads used]
+int ref_ingest_parallel(const char* path, int threads, int reps, double* out) {
+  return guarded([&] {
+    model::ModelManifest m = model::read_manifest(fs::path(path), false);
+    daemon::ShmTierBackend be(fs::path(path).parent_path().string(), std::nullopt, false);
+    for (int t = 0; t < threads; ++t) be.stage_host(uint64_t(100 + t), m, path);
+    double best = 0;
+    for (int r = 0; r < reps; ++r) {
+      std::vector<std::thread> ts;
+      std::vector<int> ok(size_t(threads), 1);
+      auto t0 = std::chrono::steady_clock::now();
+      for (int t = 0; t < threads; ++t)
+        ts.emplace_back([&, t] {
+          try {
+            be.publish_fast(uint64_t(100 + t), m, true, path);
+          } catch (...) {
+            ok[size_t(t)] = 0;
+          }
+        });
+      for (auto& x : ts) x.join();
+      const double dt = secs_since(t0);
+      for (int t = 0; t < threads; ++t) be.evict_fast(uint64_t(100 + t));
+      for (int v : ok)
+        if (!v) throw std::runtime_error("a parallel publish failed");
+      best = std::max(best, double(threads) * double(m.blob_bytes) / dt / 1e9);
+    }
+    for (int t = 0; t < threads; ++t) be.evict_host(uint64_t(100 + t));
+    out[0] = best;
+    out[1] = threads;
     return 0;
   });
 }
