@@ -9,6 +9,8 @@
 // single lane issues tcgen05.mma (M=128, N=BN, K=16 per instruction), warps
 // 4-7 drain TMEM with tcgen05.ld and run the epilogue.
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -83,22 +85,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Epilogue of tile columns [c_begin, c_end) for tile row rl: fetch(c0, v)
   // yields the 16 fp32 accumulators of columns c0..c0+15; then scale, bias,
   // residual (smem), ReLU, bf16, 32-byte stores.
-  auto store_cols = [&](int c_begin, int c_end, int rl, auto&& fetch) {
+  // Epilogue of tile columns [c_begin, c_end) for tile row rl, CW (16 or 8)
+  // columns at a time: fetch(c0, v) yields the CW fp32 accumulators of
+  // columns c0..c0+CW-1; then scale, bias, residual (smem), ReLU, bf16,
+  // 16-byte stores.
+  auto store_cols = [&](auto cw_tag, int c_begin, int c_end, int rl, auto&& fetch) {
+    constexpr int CW = decltype(cw_tag)::value;
     const int row = row_of(rl);
     uint16_t* drow = D + size_t(row < 0 ? 0 : row) * ldd;
     const bool vec_ok = (ldd % 8 == 0);
 #pragma unroll 1
-    for (int c0 = c_begin; c0 < c_end; c0 += 16) {
-      float v[16];
+    for (int c0 = c_begin; c0 < c_end; c0 += CW) {
+      float v[CW];
       fetch(c0, v);
       const int n = n0 + c0;
       if (row < 0 || n >= N) continue;
-      const uint4* rp = reinterpret_cast<const uint4*>(s_res + rl * L::RES_LD + c0);
-      const uint4 ra = res ? rp[0] : make_uint4(0, 0, 0, 0), rb = res ? rp[1] : make_uint4(0, 0, 0, 0);
-      const uint32_t rw[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-      uint32_t o[8];
+      uint32_t rw[CW / 2];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int q = 0; q < CW / 8; ++q) {
+        const uint4 r4 = res ? reinterpret_cast<const uint4*>(s_res + rl * L::RES_LD + c0)[q] : make_uint4(0, 0, 0, 0);
+        rw[4 * q] = r4.x, rw[4 * q + 1] = r4.y, rw[4 * q + 2] = r4.z, rw[4 * q + 3] = r4.w;
+      }
+      uint32_t o[CW / 2];
+#pragma unroll
+      for (int j = 0; j < CW / 2; ++j) {
         float a = v[2 * j] * s_scale[c0 + 2 * j] + s_bias[c0 + 2 * j];
         float b = v[2 * j + 1] * s_scale[c0 + 2 * j + 1] + s_bias[c0 + 2 * j + 1];
         if (res) {
@@ -111,13 +121,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         o[j] = pack_bf16x2(a, b);
       }
-      if (vec_ok && n + 16 <= N) {
+      if (vec_ok && n + CW <= N) {
         uint4* dp = reinterpret_cast<uint4*>(drow + n);
-        dp[0] = make_uint4(o[0], o[1], o[2], o[3]);
-        dp[1] = make_uint4(o[4], o[5], o[6], o[7]);
+#pragma unroll
+        for (int q = 0; q < CW / 8; ++q) dp[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
       } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
+        for (int j = 0; j < CW; ++j)
           if (n + j < N) drow[n + j] = uint16_t(o[j >> 1] >> (16 * (j & 1)));
       }
     }
@@ -238,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     } else {
       asm volatile("bar.sync 1, 192;" ::: "memory");  // residual / scale / bias in smem
-      store_cols(0, BN, rl, [&](int c0, float (&v)[16]) {
+      store_cols(std::integral_constant<int, 16>{}, 0, BN, rl, [&](int c0, float (&v)[16]) {
         uint32_t r[16];
         tmem_ld16(tq + uint32_t(c0), r);
 #pragma unroll
@@ -256,24 +266,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int rl = (warp & 3) * 32 + lane, cols = BN / splits, cbeg = z * cols;
       const uint32_t local = smem_u32(smem);
       asm volatile("bar.sync 1, 192;" ::: "memory");
-      store_cols(cbeg, cbeg + cols, rl, [&](int c0, float (&v)[16]) {
-        float pv[kMaxSplits][16];
+      auto reduce = [&](auto cw_tag) {
+        constexpr int CW = decltype(cw_tag)::value;
+        store_cols(cw_tag, cbeg, cbeg + cols, rl, [&](int c0, float (&v)[CW]) {
+          float pv[kMaxSplits][CW];
 #pragma unroll
-        for (int zz = 0; zz < kMaxSplits; ++zz) {
-          if (zz < splits) {
-            const uint32_t base = map_shared_rank(local, uint32_t(zz));
+          for (int zz = 0; zz < kMaxSplits; ++zz) {
+            if (zz < splits) {
+              const uint32_t base = map_shared_rank(local, uint32_t(zz));
 #pragma unroll
-            for (int j = 0; j < 16; ++j) pv[zz][j] = ld_dsmem_f32(base + uint32_t(((c0 + j) * BM + rl) * 4));
+              for (int j = 0; j < CW; ++j) pv[zz][j] = ld_dsmem_f32(base + uint32_t(((c0 + j) * BM + rl) * 4));
+            }
           }
-        }
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          v[j] = pv[0][j];
+          for (int j = 0; j < CW; ++j) {
+            v[j] = pv[0][j];
 #pragma unroll
-          for (int zz = 1; zz < kMaxSplits; ++zz)
-            if (zz < splits) v[j] += pv[zz][j];
-        }
-      });
+            for (int zz = 1; zz < kMaxSplits; ++zz)
+              if (zz < splits) v[j] += pv[zz][j];
+          }
+        });
+      };
+      if (cols % 16 == 0) reduce(std::integral_constant<int, 16>{});
+      else reduce(std::integral_constant<int, 8>{});
     }
     cluster_sync();  // no split leaves while its partial may still be read
   }
@@ -380,7 +395,7 @@ Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn) 
 }
 
 void run(const Prepared& p, cudaStream_t stream) {
-  if (p.splits < 1 || p.splits > kMaxSplits || (p.bn / p.splits) % 16)
+  if (p.splits < 1 || p.splits > kMaxSplits || (p.bn / p.splits) % 8)
     raise(Errc::InvalidArgument, "GEMM split count");
   switch (p.bn) {
     case 64: run_bn<64, 6>(p, stream); break;
@@ -391,10 +406,14 @@ void run(const Prepared& p, cudaStream_t stream) {
 
 int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms) {
   // Split K only while the output tiles leave most SMs idle, each split keeps
-  // >= 4 k-blocks and every split's column slice of the tile is >= 16 wide.
+  // >= 4 k-blocks and every split's column slice of the tile is >= 8 wide.
   const uint64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn), kb = (K + BK - 1) / BK;
   int s = 1;
-  while (s < kMaxSplits && bn / (s * 2) >= 16 && tiles * uint64_t(s * 2) <= uint64_t(sms) && kb / uint64_t(s * 2) >= 4)
+  // 8 splits only for the tiniest tile counts (<= 8 tiles, e.g. ResNet-50
+  // layer3/4 3x3 convs at batch 1); measured slower for 16 tiles (VGG-16
+  // conv5), profiles/r03d_split.log.
+  const int max_s = tiles <= 8 ? kMaxSplits : 4;
+  while (s < max_s && bn / (s * 2) >= 8 && tiles * uint64_t(s * 2) <= uint64_t(sms) && kb / uint64_t(s * 2) >= 4)
     s *= 2;
   return s;
 }
