@@ -304,6 +304,14 @@ int trims_net_forward_host(trims_net* net, const float* host_input, float* host_
 /* row softmax of fp32 logits [M, N] (device pointers) */
 int trims_softmax(const float* in, float* out, int M, int N, void* stream);
 
+/* Host-only view of an ingest plan's tile schedule (no device needed): one
+ * "tile op src_off dst_off dst_bytes n_elem tensor" line per logical tile of
+ * the kernel-grouped table, then per group "group kind tiles nbins stride tail
+ * dev_begin dev_count" followed by its device-image entries ("dev ..."; op 255
+ * = bin padding). For tests of the static-bin + dynamic-tail scheduler. */
+int trims_tile_plan_text(const char* src_json, uint32_t plan_flags, uint32_t out_dtype, int sm_count, char* out,
+                         uint64_t cap);
+
 /* ------------------------------------------------------------ daemon
  * The wire-protocol server (proj/src/daemon.cpp:398-560 over
  * proj/src/wire_protocol.cpp's frozen v1 frames): serves OpenRequest /

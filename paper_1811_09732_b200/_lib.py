@@ -139,6 +139,7 @@ _SIGS = {
     "trims_fill_uniform_host": (_c.c_int, [_p, _u64, _u64, _u64, _c.c_float, _c.c_float]),
     "trims_fnv1a": (_u64, [_s]),
     "trims_touch_host": (_c.c_int, [_p, _s, _c.POINTER(_u64)]),
+    "trims_tile_plan_text": (_c.c_int, [_c.c_char_p, _c.c_uint32, _c.c_uint32, _c.c_int, _c.c_char_p, _u64]),
     "trims_server_start": (_c.c_int, [_p, _c.c_char_p, _c.POINTER(_p)]),
     "trims_server_stop": (None, [_p]),
     "trims_server_frames_served": (_u64, [_p]),

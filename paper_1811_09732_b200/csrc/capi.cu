@@ -855,6 +855,28 @@ int trims_plan_create(int device, const char* src_json, uint32_t plan_flags, uin
 
 void trims_plan_destroy(trims_plan* p) { delete p; }
 
+int trims_tile_plan_text(const char* src_json, uint32_t plan_flags, uint32_t out_dtype, int sm_count, char* out,
+                         uint64_t cap) {
+  return guard([&] {
+    const fmt::Manifest src = fmt::manifest_from_json(src_json);
+    const fmt::Plan plan = make_plan(plan_flags, out_dtype);
+    const fmt::Manifest dst = fmt::resident_manifest(src, plan);
+    const ingest::TilePlan t = ingest::build_tiles(src, dst, plan.identity(), 16ull << 20, sm_count);
+    std::ostringstream os;
+    auto tile = [&](const char* tag, const ingest::Tile& x) {
+      os << tag << ' ' << int(x.op) << ' ' << x.src_off << ' ' << x.dst_off << ' ' << x.dst_bytes << ' ' << x.n_elem
+         << ' ' << x.tensor << '\n';
+    };
+    for (const ingest::Tile& x : t.tiles_by_kernel) tile("tile", x);
+    for (const ingest::Group& g : t.groups) {
+      os << "group " << int(g.kind) << ' ' << (g.end - g.begin) << ' ' << g.nbins << ' ' << g.stride << ' ' << g.tail
+         << ' ' << g.dev_begin << ' ' << g.dev_count << '\n';
+      for (uint32_t i = 0; i < g.dev_count; ++i) tile("dev", t.dev_tiles_k[g.dev_begin + i]);
+    }
+    return put(os.str(), out, cap);
+  });
+}
+
 int trims_plan_describe(trims_plan* p, uint64_t out8[8]) {
   return guard([&] {
     const auto& t = p->p->plan;
