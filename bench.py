@@ -292,6 +292,12 @@ def run_ours(args):
         line["traces"] = mix
     if large:
         line["large_model"] = large
+    # warm reload through the store (host tier in resident form: the bf16 bytes
+    # cross PCIe), as artifact bytes per second of publish_fast(from_host)
+    bd = lat.get("resnet50", {}).get("last_publish_breakdown_ms", {})
+    if bd.get("total_ms"):
+        line["e2e"]["warm_reload_artifact_GBps"] = round(src_bytes / (bd["total_ms"] / 1e3) / 1e9, 2)
+        line["e2e"]["warm_reload_pcie_bytes"] = int(bd.get("h2d_bytes", 0))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(src_json, blob, res_json)
     if rank == 0:
