@@ -164,21 +164,29 @@ __global__ void im2col_input_kernel(const float* __restrict__ in, uint16_t* __re
                                     int R, int S, int stride, int pad, int P, int Q, int Kp) {
   pdl_wait();  // the input H2D / previous forward's readers of A
   pdl_trigger();
-  const int RSC = R * S * C, cols8 = Kp / 8;
-  const uint32_t total = uint32_t(N) * P * Q * cols8;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const uint32_t m = i / cols8, col = (i - m * cols8) * 8;
+  // blockIdx.y = one 8-column group: its (c, r, s) taps are decoded once;
+  // threads then walk output pixels (consecutive lanes = consecutive pixels,
+  // so a warp's loads of one tap are stride-apart in one plane row)
+  const int RSC = R * S * C, col = blockIdx.y * 8;
+  int dy[8], dx[8];
+  uint64_t plane[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int k = col + e, rs = k / C, c = k - rs * C;
+    dy[e] = k < RSC ? rs / S : -(1 << 20);  // out of every image: a zero column
+    dx[e] = rs - (rs / S) * S;
+    plane[e] = uint64_t(c) * H * W;
+  }
+  const uint32_t M = uint32_t(N) * P * Q;
+  for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < M; m += gridDim.x * blockDim.x) {
     const uint32_t q = m % Q, pn = m / Q, p = pn % P, n = pn / P;
+    const int y0 = int(p) * stride - pad, x0 = int(q) * stride - pad;
+    const float* img = in + uint64_t(n) * C * H * W;
     uint32_t o[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const int k = int(col) + e;
-      float v = 0.f;
-      if (k < RSC) {
-        const int rs = k / C, c = k - rs * C, r = rs / S, sx = rs - r * S;
-        const int y = int(p) * stride - pad + r, x = int(q) * stride - pad + sx;
-        if (y >= 0 && y < H && x >= 0 && x < W) v = __ldg(in + ((uint64_t(n) * C + c) * H + y) * W + x);
-      }
+      const int y = y0 + dy[e], x = x0 + dx[e];
+      const float v = (y >= 0 && y < H && x >= 0 && x < W) ? __ldg(img + plane[e] + uint64_t(y) * W + x) : 0.f;
       o[e >> 1] |= uint32_t(to_bf(v)) << (16 * (e & 1));
     }
     *reinterpret_cast<uint4*>(A + uint64_t(m) * Kp + col) = make_uint4(o[0], o[1], o[2], o[3]);
@@ -365,8 +373,9 @@ void im2col(const uint16_t* in, uint16_t* A, int N, int H, int W, int Ctot, int 
 void im2col_input(const float* in, uint16_t* A, int N, int C, int H, int W, int R, int S, int stride, int pad, int P,
                   int Q, int Kp, cudaStream_t s) {
   if (Kp % 8) raise(Errc::InvalidArgument, "im2col_input needs Kp % 8 == 0");
-  launch_pdl(im2col_input_kernel, dim3(blocks(uint64_t(N) * P * Q * (Kp / 8))), dim3(256), 0, s, in, A, N, C, H, W, R,
-             S, stride, pad, P, Q, Kp);
+  const uint64_t M = uint64_t(N) * P * Q;
+  launch_pdl(im2col_input_kernel, dim3(unsigned(std::min<uint64_t>((M + 255) / 256, 64)), unsigned(Kp / 8)), dim3(256),
+             0, s, in, A, N, C, H, W, R, S, stride, pad, P, Q, Kp);
 }
 
 void maxpool(const uint16_t* in, uint16_t* out, int N, int H, int W, int C, int k, int stride, int pad, int P, int Q,
