@@ -86,41 +86,57 @@ __global__ void im2col_kernel(const uint16_t* __restrict__ in, uint16_t* __restr
   }
 }
 
-__global__ void maxpool_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out, int N, int H, int W, int C,
-                               int k, int stride, int pad, int P, int Q) {
+// Max pool, 8 channels per thread, 32-bit index math; KS = the window size
+// when it is a compile-time 2 or 3 (all KS*KS loads issued before the max),
+// 0 = generic runtime window.
+template <int KS>
+__global__ void __launch_bounds__(256) maxpool_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out,
+                                                      int N, int H, int W, int C, int k, int stride, int pad, int P,
+                                                      int Q) {
   pdl_wait();  // reads the previous layer's output / writes shared scratch
   pdl_trigger();
-  const int C8 = C / 8;
-  const uint64_t total = uint64_t(N) * P * Q * C8;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
-    const int c = int(i % C8) * 8;
-    uint64_t r = i / C8;
-    const int q = int(r % Q);
-    r /= Q;
-    const int p = int(r % P);
-    const int n = int(r / P);
+  const uint32_t C8 = uint32_t(C) / 8, total = uint32_t(N) * P * Q * C8;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const uint32_t pix = i / C8, c = (i - pix * C8) * 8, q = pix % Q, pn = pix / Q, p = pn % P, n = pn / P;
+    const int y0 = int(p) * stride - pad, x0 = int(q) * stride - pad;
+    const uint16_t* img = in + uint64_t(n) * H * W * C + c;
     float m[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) m[j] = -INFINITY;
-    for (int dy = 0; dy < k; ++dy) {
-      const int y = p * stride - pad + dy;
-      if (y < 0 || y >= H) continue;
-      for (int dx = 0; dx < k; ++dx) {
-        const int x = q * stride - pad + dx;
-        if (x < 0 || x >= W) continue;
-        const uint4 v = *reinterpret_cast<const uint4*>(in + ((uint64_t(n) * H + y) * W + x) * C + c);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    auto fold = [&](const uint4 v) {
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          m[2 * j] = fmaxf(m[2 * j], bf(uint16_t(w[j] & 0xffff)));
-          m[2 * j + 1] = fmaxf(m[2 * j + 1], bf(uint16_t(w[j] >> 16)));
+      for (int j = 0; j < 4; ++j) {
+        m[2 * j] = fmaxf(m[2 * j], bf(uint16_t(w[j] & 0xffff)));
+        m[2 * j + 1] = fmaxf(m[2 * j + 1], bf(uint16_t(w[j] >> 16)));
+      }
+    };
+    if constexpr (KS > 0) {
+      uint4 v[KS * KS];
+      bool ok[KS * KS];
+#pragma unroll
+      for (int t = 0; t < KS * KS; ++t) {
+        const int y = y0 + t / KS, x = x0 + t % KS;
+        ok[t] = y >= 0 && y < H && x >= 0 && x < W;
+        if (ok[t]) v[t] = *reinterpret_cast<const uint4*>(img + (uint64_t(y) * W + x) * C);
+      }
+#pragma unroll
+      for (int t = 0; t < KS * KS; ++t)
+        if (ok[t]) fold(v[t]);
+    } else {
+      for (int dy = 0; dy < k; ++dy) {
+        const int y = y0 + dy;
+        if (y < 0 || y >= H) continue;
+        for (int dx = 0; dx < k; ++dx) {
+          const int x = x0 + dx;
+          if (x >= 0 && x < W) fold(*reinterpret_cast<const uint4*>(img + (uint64_t(y) * W + x) * C));
         }
       }
     }
     uint32_t o[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) o[j] = uint32_t(to_bf(m[2 * j])) | (uint32_t(to_bf(m[2 * j + 1])) << 16);
-    *reinterpret_cast<uint4*>(out + i * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<uint4*>(out + uint64_t(i) * 8) = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -381,7 +397,10 @@ void im2col_input(const float* in, uint16_t* A, int N, int C, int H, int W, int 
 void maxpool(const uint16_t* in, uint16_t* out, int N, int H, int W, int C, int k, int stride, int pad, int P, int Q,
              cudaStream_t s) {
   if (C % 8) raise(Errc::InvalidArgument, "maxpool needs C % 8 == 0");
-  launch_pdl(maxpool_kernel, dim3(blocks(uint64_t(N) * P * Q * C / 8)), dim3(256), 0, s, in, out, N, H, W, C, k, stride, pad, P, Q);
+  const dim3 g(blocks(uint64_t(N) * P * Q * C / 8));
+  if (k == 3) launch_pdl(maxpool_kernel<3>, g, dim3(256), 0, s, in, out, N, H, W, C, k, stride, pad, P, Q);
+  else if (k == 2) launch_pdl(maxpool_kernel<2>, g, dim3(256), 0, s, in, out, N, H, W, C, k, stride, pad, P, Q);
+  else launch_pdl(maxpool_kernel<0>, g, dim3(256), 0, s, in, out, N, H, W, C, k, stride, pad, P, Q);
   TRIMS_CUDA(cudaGetLastError());
 }
 
