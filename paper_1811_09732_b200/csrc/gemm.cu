@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto load_a = [&](void* dst, int kb, uint64_t* bar) {
     if (cg.impl) {
       const int rs = kb / cg.cblocks, cb = kb - rs * cg.cblocks, r = rs / cg.S, s = rs - r * cg.S;
-      tma_load_4d(dst, &tmA, cb * BK, tw * wbox * cg.stride - cg.pad + s, th * cg.hbox * cg.stride - cg.pad + r, ti,
+      tma_load_4d(dst, &tmA, cg.c_off + cb * BK, tw * wbox * cg.stride - cg.pad + s, th * cg.hbox * cg.stride - cg.pad + r, ti,
                   bar);
     } else {
       tma_load_2d(dst, &tmA, kb * BK, m0, bar);
@@ -423,7 +423,8 @@ uint64_t tile_rows(const Prepared& p) {
   return (p.M + BM - 1) / BM * BM;
 }
 
-ConvGeom conv_geom(int N, int H, int W, int C, int R, int S, int stride, int pad, int P, int Q) {
+ConvGeom conv_geom(int N, int H, int W, int C, int R, int S, int stride, int pad, int P, int Q, int cgroup,
+                   int c_off) {
   ConvGeom g;
   g.impl = 1;
   g.N = N, g.H = H, g.W = W, g.C = C, g.R = R, g.S = S, g.stride = stride, g.pad = pad, g.P = P, g.Q = Q;
@@ -435,13 +436,15 @@ ConvGeom conv_geom(int N, int H, int W, int C, int R, int S, int stride, int pad
   g.hbox = BM >> wl;
   g.tiles_w = (Q + (1 << wl) - 1) >> wl;
   g.tiles_h = (P + g.hbox - 1) / g.hbox;
-  g.cblocks = C / BK;
+  g.cblocks = (cgroup ? cgroup : C) / BK;
+  g.c_off = c_off;
   return g;
 }
 
 Prepared prepare_conv(const void* act, const ConvGeom& g, const Operand& B, const Epilogue& e, int bn) {
-  if (!g.impl || g.C % BK || g.hbox * g.stride > 256) raise(Errc::InvalidArgument, "implicit conv geometry");
-  if (B.k != uint64_t(g.R) * g.S * g.C) raise(Errc::InvalidArgument, "implicit conv K mismatch");
+  if (!g.impl || g.C % 8 || g.c_off % BK || g.c_off + g.cblocks * BK > g.C || g.hbox * g.stride > 256)
+    raise(Errc::InvalidArgument, "implicit conv geometry");
+  if (B.k != uint64_t(g.R) * g.S * g.cblocks * BK) raise(Errc::InvalidArgument, "implicit conv K mismatch");
   const uint64_t M = uint64_t(g.N) * g.P * g.Q;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);

@@ -37,8 +37,12 @@ struct ConvGeom {
   int impl{0};
   int N, H, W, C, R, S, stride, pad, P, Q;
   int wbox_log2, hbox, tiles_w, tiles_h, cblocks;
+  int c_off{0};  // grouped conv: first channel of this group (the group has cblocks * 64 channels)
 };
-ConvGeom conv_geom(int N, int H, int W, int C, int R, int S, int stride, int pad, int P, int Q);
+// C = the activation's channels; cg / c_off = this group's channel count and
+// first channel (cg = C, c_off = 0 for an ungrouped conv; cg % 64 == 0).
+ConvGeom conv_geom(int N, int H, int W, int C, int R, int S, int stride, int pad, int P, int Q, int cg = 0,
+                   int c_off = 0);
 int pick_bn(uint64_t M, uint64_t N, int sms);
 
 // A GEMM with its tensor maps encoded once (the executor builds these at

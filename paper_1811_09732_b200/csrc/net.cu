@@ -85,7 +85,7 @@ bool implicit_enabled();
 bool first_conv_fusable(const LayerSpec& l) {
   const int k = l.i("k", 1), groups = l.i("groups", 1);
   const bool direct = k == 1 && l.i("stride", 1) == 1 && l.i("pad", 0) == 0 && groups == 1;
-  const bool implicit = !direct && groups == 1 && l.i("cin") % 64 == 0 && implicit_enabled();
+  const bool implicit = !direct && (l.i("cin") / groups) % 64 == 0 && implicit_enabled();
   return !direct && !implicit && groups == 1;
 }
 
@@ -169,7 +169,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
         conv_shape(in, l, P, Q);
         const int k = l.i("k", 1), groups = l.i("groups", 1), cg = l.i("cin") / groups;
         const bool direct = k == 1 && l.i("stride", 1) == 1 && l.i("pad", 0) == 0 && groups == 1;
-        const bool implicit = !direct && groups == 1 && l.i("cin") % 64 == 0 && implicit_enabled();
+        const bool implicit = !direct && cg % 64 == 0 && implicit_enabled();
         if (!direct && !implicit)
           col_elems = std::max<uint64_t>(col_elems, uint64_t(batch) * P * Q * ((uint64_t(k) * k * cg + 7) / 8 * 8));
         a = {nullptr, batch, P, Q, l.i("cout")};
@@ -257,7 +257,8 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       const bool direct = k == 1 && st == 1 && pad == 0 && groups == 1;
       // Implicit GEMM (A read from the NHWC activation by 4-D TMA, no im2col
       // pass) whenever the channels tile by 64.
-      const bool implicit = !direct && groups == 1 && cin % 64 == 0 && implicit_enabled();
+      // Grouped convs go implicit per group when a group's channels tile by 64.
+      const bool implicit = !direct && cg % 64 == 0 && implicit_enabled();
       // A conv whose output only feeds a later layer by name (the next layer
       // reads its own `src`, e.g. ResNet's downsample shortcut) is an
       // independent branch: it runs on a side stream concurrently with the
@@ -287,7 +288,8 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
         const gemm::Operand Bop{wpad ? wpad : reinterpret_cast<const uint16_t*>(uintptr_t(256)), uint64_t(kg),
                                 uint64_t(kp), uint64_t(kp)};
         auto prep = std::make_shared<gemm::Prepared>(
-            implicit ? gemm::prepare_conv(in.p, gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q), Bop, e)
+            implicit ? gemm::prepare_conv(in.p, gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg),
+                                          Bop, e)
                      : gemm::prepare({A, M, uint64_t(kp), uint64_t(direct ? cin : kp)}, Bop, e));
         if (splitk_enabled())
           prep->splits = gemm::pick_splits(gemm::tile_rows(*prep), uint64_t(kg), uint64_t(kp), prep->bn, sms_);
