@@ -358,25 +358,29 @@ def peer_serve(work: str, arch, dev: int, rank: int, world: int, steps: int) -> 
 
 
 def shared_clients(work: str, arch, dev: int, n_clients: int, n_reqs: int) -> dict:
-    """BASELINE configs[1]: ResNet-50 loaded once into this process's store;
-    `n_clients` spawned client processes map the exported arena read-only,
+    """BASELINE configs[1]: ResNet-50 loaded once into this process's store,
+    served by the wire-protocol daemon; `n_clients` spawned client processes
+    open it over the socket, map the exported arena read-only,
     bind an executor on the shared weights and serve batch-1 requests at once
     (paper_1811_09732_b200/sharing.py). Reports per-request latency
     percentiles, aggregate requests/s, weight copies in HBM and disk reads."""
     import numpy as np
 
     from paper_1811_09732_b200 import catalog as C
+    from paper_1811_09732_b200.daemon import serve
     from paper_1811_09732_b200.models import arch_text
-    from paper_1811_09732_b200.sharing import SharedModel, run_clients
+    from paper_1811_09732_b200.sharing import run_daemon_clients
     from paper_1811_09732_b200.store import Store, StoreOptions
 
     opts = StoreOptions(disk_cache_dir=work, fast_capacity_bytes=2 << 30, host_capacity_bytes=1 << 30,
                         convert_to="bf16", permute_4d=True, device=dev, scan_disk=False)
-    with Store(opts) as s:
-        ex = s.open(C.arch_key(arch))
-        r = run_clients(SharedModel.from_export(ex, arch_text(arch)), ex.fd, n_clients, n_reqs)
+    endpoint = os.path.join(work, "mrmd.sock")
+    with Store(opts) as s, serve(s, endpoint):
+        ex = s.open(C.arch_key(arch))  # loaded once; every client open is a FastHit on this copy
+        r = run_daemon_clients(endpoint, C.arch_key(arch), arch_text(arch), n_clients, n_reqs)
         st = s.stats()
         s.close(C.arch_key(arch))
+    r["transport"] = "v1 wire protocol over a Unix socket (daemon), allocation fd by SCM_RIGHTS"
     logits = r.pop("logits")
     r["identical_logits_across_clients"] = all(np.array_equal(logits[0], l) for l in logits)
     r["hbm_weight_copies"] = round(st["tiers"][0]["used_bytes"] / ex.weights_bytes, 4)

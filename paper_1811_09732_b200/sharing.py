@@ -42,12 +42,12 @@ class SharedModel:
                    bytes(ex.manifest_digest), arch_text)
 
 
-def _client_main(conn, sm: SharedModel, batch: int, n_reqs: int, seed: int) -> None:
+def _serve(conn, sm: SharedModel, fd: int, batch: int, n_reqs: int, seed: int, on_exit=None) -> None:
+    """Attach `fd`'s segment, bind an executor, warm up, then serve n_reqs
+    requests on the parent's "go"; reports latencies and the last logits."""
+    from ._lib import check, lib
+    from .client import import_segment
     try:
-        from ._lib import check, lib
-        from .client import import_segment
-        check(lib.trims_device_init(sm.device))  # context creation is not part of the attach
-        fd = recv_handle(conn)
         t0 = time.perf_counter()
         imp, ptr, res_json = import_segment(sm.device, fd, sm.alloc_bytes, sm.offset, sm.generation,
                                             sm.payload_bytes, sm.digest)
@@ -72,10 +72,62 @@ def _client_main(conn, sm: SharedModel, batch: int, n_reqs: int, seed: int) -> N
         conn.send(("done", lat, t_first, t_last, y.copy()))
         lib.trims_net_destroy(net)
         lib.trims_import_close(imp)
-    except Exception as e:  # reported to the store process
+        if on_exit:
+            on_exit()
+    except Exception as e:  # reported to the parent
         conn.send(("error", repr(e)))
     finally:
         conn.close()
+
+
+def _daemon_client_main(conn, endpoint: str, key: tuple, arch_text: str, batch: int, n_reqs: int,
+                        seed: int) -> None:
+    """A client process of the wire-protocol daemon (daemon.py): opens the
+    model over the socket (the allocation fd arrives with the OpenResponse),
+    attaches, binds an executor and serves; closes its handle at the end."""
+    try:
+        from . import format as F
+        from ._lib import check, lib
+        from .client import import_segment
+        from .daemon import RemoteStore
+        rs = RemoteStore(endpoint)
+        ex = rs.open(F.ModelKey(*key))
+        check(lib.trims_device_init(ex.device))
+        sm = SharedModel(ex.device, ex.alloc_bytes, ex.segment_offset, ex.generation, ex.payload_bytes,
+                         ex.manifest_digest, arch_text)
+        _serve(conn, sm, ex.fd, batch, n_reqs, seed, on_exit=lambda: rs.close(F.ModelKey(*key)))
+    except Exception as e:
+        if not conn.closed:
+            conn.send(("error", repr(e)))
+            conn.close()
+
+
+def _client_main(conn, sm: SharedModel, batch: int, n_reqs: int, seed: int) -> None:
+    try:
+        from ._lib import check, lib
+        check(lib.trims_device_init(sm.device))  # context creation is not part of the attach
+        _serve(conn, sm, recv_handle(conn), batch, n_reqs, seed)
+    except Exception as e:  # reported to the store process
+        if not conn.closed:
+            conn.send(("error", repr(e)))
+            conn.close()
+
+
+def run_daemon_clients(endpoint: str, key, arch_text: str, n_clients: int = 16, n_reqs: int = 20, batch: int = 1,
+                       seed: int = 2, timeout_s: float = 600.0) -> dict:
+    """As run_clients, but every client process gets the model from the
+    daemon at `endpoint` (v1 OpenRequest over the socket, fd by SCM_RIGHTS)."""
+    ctx = mp.get_context("spawn")
+    procs, conns = [], []
+    for i in range(n_clients):
+        parent, child = ctx.Pipe()
+        p = ctx.Process(target=_daemon_client_main,
+                        args=(child, endpoint, (key.ns, key.name, key.version), arch_text, batch, n_reqs, seed),
+                        daemon=True)
+        p.start()
+        procs.append(p)
+        conns.append(parent)
+    return _collect(procs, conns, n_clients, batch, timeout_s)
 
 
 def run_clients(sm: SharedModel, fd: int, n_clients: int = 16, n_reqs: int = 20, batch: int = 1,
@@ -93,6 +145,10 @@ def run_clients(sm: SharedModel, fd: int, n_clients: int = 16, n_reqs: int = 20,
         send_handle(parent, fd, p.pid)
         procs.append(p)
         conns.append(parent)
+    return _collect(procs, conns, n_clients, batch, timeout_s)
+
+
+def _collect(procs, conns, n_clients: int, batch: int, timeout_s: float) -> dict:
     try:
         attach = []
         for c in conns:

@@ -38,3 +38,25 @@ def test_four_clients_one_copy(tmp_path):
         net.close()
         cli.close(v)
         s.close(C.arch_key(arch))
+
+
+def test_daemon_clients_one_copy(tmp_path):
+    """The same through the wire-protocol daemon: clients open over the
+    socket (FastHits on the one copy) and close their handles at the end."""
+    from paper_1811_09732_b200.daemon import serve
+    from paper_1811_09732_b200.sharing import run_daemon_clients
+    arch = C.ARCHS["resnet50"]()
+    C.write_arch(arch, str(tmp_path), seed=1)
+    opts = StoreOptions(disk_cache_dir=str(tmp_path), fast_capacity_bytes=1 << 30, convert_to="bf16",
+                        permute_4d=True, scan_disk=False)
+    ep = str(tmp_path / "mrmd.sock")
+    with Store(opts) as s, serve(s, ep):
+        ex = s.open(C.arch_key(arch))
+        r = run_daemon_clients(ep, C.arch_key(arch), arch_text(arch), n_clients=4, n_reqs=3, seed=5)
+        st = s.stats()
+        assert st["disk_reads"] == 1 and st["tiers"][0]["used_bytes"] == ex.weights_bytes
+        assert st["open_requests"] == 5 and st["tiers"][0]["hits"] == 4  # 4 client opens hit the one copy
+        assert r["requests"] == 12
+        assert all(np.array_equal(y, r["logits"][0]) for y in r["logits"])
+        assert [m["refcount"] for m in st["models"]] == [1]  # only the store's own open remains
+        s.close(C.arch_key(arch))
