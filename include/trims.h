@@ -109,6 +109,7 @@ typedef struct trims_store_config {
   int32_t rank;                  /* this store's row in the directory */
   int32_t world;                 /* stores on the node */
   uint32_t directory_slots;      /* per-rank slots (0 = 1024) */
+  const char* remote_url;        /* daemon.hpp:26: http://... or dir:<path>; NULL = no remote tier */
 } trims_store_config;
 
 /* Reference outcomes (cache_core.hpp:36) + PEER_HIT for the multi-GPU directory. */
@@ -144,10 +145,17 @@ typedef struct trims_export {
 typedef struct trims_backend trims_backend;
 int trims_backend_create(const trims_store_config* cfg, trims_backend** out);
 void trims_backend_destroy(trims_backend* b);
-/* ShmTierBackend::locate (daemon.cpp:128-136); NotFound when absent (no remote tier). */
+/* ShmTierBackend::locate (daemon.cpp:128-136): DiskCache = the path; Remote
+ * (not on disk, remote_url set) = rc 0 with an empty path; NotFound when absent. */
 int trims_backend_locate(trims_backend* b, const char* ns, const char* name, const char* version, char* path_out,
                          uint64_t cap, uint64_t* file_bytes);
-/* ShmTierBackend::read_manifest (daemon.cpp:144-151) */
+/* ShmTierBackend::fetch_remote (daemon.cpp:138-142): remote tier -> disk cache */
+int trims_backend_fetch_remote(trims_backend* b, const char* ns, const char* name, const char* version,
+                               char* path_out, uint64_t cap, uint64_t* file_bytes);
+/* ShmTierBackend::read_manifest (daemon.cpp:144-151). With full_verify the
+ * verified blob stays in pinned memory for the same key's stage_host /
+ * publish_fast (read once, hashed once); trims_backend_load_settled drops it
+ * if the open fails in between (our CacheCore calls it when a load settles). */
 int trims_backend_read_manifest(trims_backend* b, const char* ns, const char* name, const char* version,
                                 const char* path, char* json_out, uint64_t cap, uint8_t checksum_out[32]);
 /* ShmTierBackend::stage_host (daemon.cpp:153-158): disk -> pinned host tier */
@@ -160,6 +168,15 @@ int trims_backend_publish_fast(trims_backend* b, uint64_t model_id, const char* 
 int trims_backend_evict_fast(trims_backend* b, uint64_t model_id);
 int trims_backend_evict_host(trims_backend* b, uint64_t model_id);
 int trims_backend_evict_disk(trims_backend* b, const char* path);
+int trims_backend_load_settled(trims_backend* b, const char* ns, const char* name, const char* version);
+
+/* remote::fetch(make_ref(url, key), dest_dir) (remote_store.cpp:58-120): a
+ * dir:<path> / bare-path store is copied, http://host[:port][/prefix] is
+ * fetched by HTTP/1.1 GET; the download must pass a full verify before it is
+ * renamed to <dest_dir>/<ns>__<name>__<version>.trms. RemoteNotFound,
+ * TransportError, ChecksumMismatch. Host only (no device). */
+int trims_remote_fetch(const char* url, const char* ns, const char* name, const char* version, const char* dest_dir,
+                       char* path_out, uint64_t cap, uint64_t* file_bytes);
 
 /* Daemon::Daemon (daemon.cpp:298-391) minus listeners: builds the backend
  * and the core, optionally scans the disk cache. */

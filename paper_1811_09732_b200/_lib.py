@@ -44,6 +44,7 @@ class Errc:
     NotSealed = 115
     UnknownModel = 120
     RemoteNotFound = 140
+    TransportError = 141
     DaemonUnreachable = 150
     ConnectionLost = 151
     InvalidArgument = 160
@@ -72,6 +73,7 @@ class StoreConfig(ctypes.Structure):
         ("rank", ctypes.c_int32),
         ("world", ctypes.c_int32),
         ("directory_slots", ctypes.c_uint32),
+        ("remote_url", ctypes.c_char_p),
     ]
 
 
@@ -149,6 +151,9 @@ _SIGS = {
     "trims_backend_create": (_c.c_int, [_c.POINTER(StoreConfig), _c.POINTER(_p)]),
     "trims_backend_destroy": (None, [_p]),
     "trims_backend_locate": (_c.c_int, [_p, _s, _s, _s, _s, _u64, _c.POINTER(_u64)]),
+    "trims_backend_fetch_remote": (_c.c_int, [_p, _s, _s, _s, _s, _u64, _c.POINTER(_u64)]),
+    "trims_backend_load_settled": (_c.c_int, [_p, _s, _s, _s]),
+    "trims_remote_fetch": (_c.c_int, [_s, _s, _s, _s, _s, _s, _u64, _c.POINTER(_u64)]),
     "trims_backend_read_manifest": (_c.c_int, [_p, _s, _s, _s, _s, _s, _u64, _p]),
     "trims_backend_stage_host": (_c.c_int, [_p, _u64, _s, _p, _s]),
     "trims_backend_publish_fast": (_c.c_int, [_p, _u64, _s, _c.c_int, _s, _c.POINTER(Export)]),

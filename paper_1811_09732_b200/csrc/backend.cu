@@ -14,6 +14,8 @@
 
 #include "backend.hpp"
 #include "cuda_util.hpp"
+#include "pread.hpp"
+#include "remote.hpp"
 #include "sha256.hpp"
 
 namespace trims {
@@ -23,86 +25,21 @@ namespace fs = std::filesystem;
 void parallel_pread(int fd, uint8_t* dst, uint64_t len, uint64_t off, unsigned threads) {
   // 4 MiB pieces handed out by a counter (measured faster from the page cache
   // than one large piece per thread)
-  constexpr uint64_t kPiece = 4ull << 20;
-  const uint64_t pieces = (len + kPiece - 1) / kPiece;
-  std::atomic<uint64_t> next{0};
-  std::atomic<bool> ok{true};
-  auto worker = [&] {
-    for (uint64_t i; ok.load() && (i = next.fetch_add(1)) < pieces;) {
-      const uint64_t e = std::min(len, (i + 1) * kPiece);
-      for (uint64_t at = i * kPiece; at < e;) {
-        ssize_t r = ::pread(fd, dst + at, size_t(e - at), off_t(off + at));
-        if (r <= 0) {
-          ok = false;
-          return;
-        }
-        at += uint64_t(r);
-      }
-    }
-  };
-  const unsigned n = unsigned(std::clamp<uint64_t>(pieces, 1, std::max(1u, threads)));
-  std::vector<std::thread> ts;
-  for (unsigned i = 1; i < n; ++i) ts.emplace_back(worker);
-  worker();
-  for (auto& t : ts) t.join();
-  if (!ok) raise(Errc::Corrupt, "blob truncated (short read)");
+  pipelined_read(fd, off, len, dst, threads, nullptr);
 }
 
 // Reads [off, off+len) into the pinned host buffer in 4 MiB pieces handed out
 // to `threads` readers, while the calling thread uploads the pieces to `dev`
 // in order as they land (async on `stream`): the PCIe copy of the blob runs
 // under the file read instead of after it, and one thread owns the stream
-// (readers issuing their own copies contended in the driver).
+// (readers issuing their own copies contended in the driver). With `hash`, a
+// further thread hashes the pieces in order under both.
 void parallel_pread_upload(int fd, uint8_t* host, uint8_t* dev, uint64_t len, uint64_t off, unsigned threads,
-                           int device, cudaStream_t stream) {
-  constexpr uint64_t kPiece = 4ull << 20;
-  const uint64_t pieces = (len + kPiece - 1) / kPiece;
-  std::atomic<uint64_t> next{0};
-  std::atomic<bool> ok{true};
-  std::unique_ptr<std::atomic<uint8_t>[]> ready(new std::atomic<uint8_t>[pieces]);
-  for (uint64_t i = 0; i < pieces; ++i) ready[i].store(0, std::memory_order_relaxed);
-  std::mutex mu;
-  std::condition_variable cv;
-  auto reader = [&] {
-    for (uint64_t i; ok.load() && (i = next.fetch_add(1)) < pieces;) {
-      const uint64_t e = std::min(len, (i + 1) * kPiece);
-      for (uint64_t at = i * kPiece; at < e;) {
-        ssize_t r = ::pread(fd, host + at, size_t(e - at), off_t(off + at));
-        if (r <= 0) {
-          ok = false;
-          break;
-        }
-        at += uint64_t(r);
-      }
-      {
-        std::lock_guard lk(mu);
-        ready[i].store(1, std::memory_order_release);
-      }
-      cv.notify_one();
-    }
-  };
-  const unsigned n = unsigned(std::clamp<uint64_t>(pieces, 1, std::max(1u, threads)));
-  std::vector<std::thread> ts;
-  for (unsigned i = 0; i < n; ++i) ts.emplace_back(reader);
-  std::string err;
-  try {
-    DeviceGuard g(device);
-    for (uint64_t i = 0; i < pieces && ok.load(); ++i) {
-      {
-        std::unique_lock lk(mu);
-        cv.wait(lk, [&] { return ready[i].load(std::memory_order_acquire) || !ok.load(); });
-      }
-      if (!ok.load()) break;
-      const uint64_t b = i * kPiece, e = std::min(len, b + kPiece);
-      TRIMS_CUDA(cudaMemcpyAsync(dev + b, host + b, e - b, cudaMemcpyHostToDevice, stream));
-    }
-  } catch (const std::exception& x) {
-    ok = false;
-    err = x.what();
-  }
-  cv.notify_all();
-  for (auto& t : ts) t.join();
-  if (!ok) raise(Errc::Corrupt, err.empty() ? "blob truncated (short read)" : err);
+                           int device, cudaStream_t stream, Sha256* hash) {
+  DeviceGuard g(device);
+  pipelined_read(fd, off, len, host, threads, hash, [&](const uint8_t* p, uint64_t b, uint64_t n) {
+    TRIMS_CUDA(cudaMemcpyAsync(dev + b, p, n, cudaMemcpyHostToDevice, stream));
+  });
 }
 
 // ---------------------------------------------------------------------------
@@ -392,6 +329,8 @@ CudaTierBackend::~CudaTierBackend() {
   fast_.clear();
   for (auto& [id, h] : host_) free_host(h);
   host_.clear();
+  for (auto& [k, h] : verified_) free_host(h);
+  verified_.clear();
   DeviceGuard g(cfg_.device, /*nothrow=*/true);
   if (pre_stream_) cudaStreamSynchronize(pre_stream_);
   if (pre_raw_) cudaFreeAsync(pre_raw_, pre_stream_);
@@ -421,21 +360,80 @@ Located CudaTierBackend::locate(const fmt::ModelKey& key) {
   fs::path p = fs::path(cfg_.disk_cache_dir) / fmt::canonical_filename(key);
   std::error_code ec;
   if (fs::exists(p, ec)) return {Located::Kind::DiskCache, p.string(), uint64_t(fs::file_size(p, ec))};
+  if (!cfg_.remote_url.empty()) return {Located::Kind::Remote, "", 0};
   return {Located::Kind::Absent, "", 0};
 }
 
+// daemon.cpp:138-142: download into the disk cache (remote.cpp)
 FetchResult CudaTierBackend::fetch_remote(const fmt::ModelKey& key) {
-  // The remote tier is outside the B200 hot path.
-  raise(Errc::RemoteNotFound, fmt::to_string(key));
+  if (cfg_.remote_url.empty()) raise(Errc::RemoteNotFound, fmt::to_string(key));
+  std::string p = remote::fetch(remote::make_ref(cfg_.remote_url, key), cfg_.disk_cache_dir);
+  std::error_code ec;
+  return {p, uint64_t(fs::file_size(p, ec))};
 }
 
-// daemon.cpp:144-151
+// daemon.cpp:144-151. With full_verify the blob is read into pinned memory
+// by parallel readers while one thread hashes it in order; the verified bytes
+// are kept for this open's stage_host / publish_fast (take_verified).
 fmt::Manifest CudaTierBackend::read_manifest(const fmt::ModelKey& key, const std::string& path) {
-  fmt::ArtifactInfo a = fmt::read_artifact_info(path, cfg_.full_verify);
+  fmt::ArtifactInfo a = fmt::read_artifact_info(path, false);
   if (a.manifest.key != key)
     raise(Errc::Corrupt, "artifact at " + path + " holds " + fmt::to_string(a.manifest.key) + ", expected " +
                              fmt::to_string(key));
+  if (!cfg_.full_verify) return a.manifest;
+  int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
+  if (fd < 0) raise(Errc::NotFound, path);
+  HostBuf hb;
+  try {
+    hb = alloc_host(a.manifest.blob_bytes);
+    Sha256 h;
+    pipelined_read(fd, a.blob_offset, a.manifest.blob_bytes, hb.p, cfg_.read_threads, &h);
+    if (h.finish() != a.manifest.checksum) raise(Errc::ChecksumMismatch, path);
+  } catch (...) {
+    ::close(fd);
+    free_host(hb);
+    throw;
+  }
+  ::close(fd);
+  std::lock_guard lk(mu_);
+  auto& slot = verified_[fmt::to_string(key)];
+  free_host(slot);  // a stale one from an open that never settled
+  slot = hb;
   return a.manifest;
+}
+
+CudaTierBackend::HostBuf CudaTierBackend::alloc_host(uint64_t bytes) {
+  HostBuf hb;
+  hb.bytes = bytes;
+  if (pool_) hb.p = pool_->alloc(std::max<uint64_t>(bytes, 1));
+  hb.pooled = hb.p != nullptr;
+  if (!hb.p) {
+    DeviceGuard g(cfg_.device);
+    TRIMS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hb.p), std::max<uint64_t>(bytes, 1), cudaHostAllocPortable));
+  }
+  return hb;
+}
+
+bool CudaTierBackend::take_verified(const fmt::ModelKey& key, uint64_t bytes, HostBuf* out) {
+  std::lock_guard lk(mu_);
+  auto it = verified_.find(fmt::to_string(key));
+  if (it == verified_.end()) return false;
+  HostBuf hb = it->second;
+  verified_.erase(it);
+  if (hb.bytes != bytes) {
+    free_host(hb);
+    return false;
+  }
+  *out = hb;
+  return true;
+}
+
+void CudaTierBackend::load_settled(const fmt::ModelKey& key) {
+  std::lock_guard lk(mu_);
+  auto it = verified_.find(fmt::to_string(key));
+  if (it == verified_.end()) return;
+  free_host(it->second);
+  verified_.erase(it);
 }
 
 void CudaTierBackend::free_host(HostBuf& h) {
@@ -452,54 +450,70 @@ void CudaTierBackend::free_host(HostBuf& h) {
 
 // daemon.cpp:153-158: disk -> host tier, here straight into pinned memory.
 void CudaTierBackend::stage_host(uint64_t model_id, const fmt::Manifest& m, const std::string& path) {
-  int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
-  if (fd < 0) raise(Errc::NotFound, path);
   HostBuf hb;
-  try {
-    uint8_t hdr[16];
-    if (::pread(fd, hdr, 16, 0) != 16) raise(Errc::Corrupt, "short read on " + path);
-    uint64_t mlen = 0;
-    for (int i = 0; i < 8; ++i) mlen |= uint64_t(hdr[8 + i]) << (8 * i);
-    const uint64_t off = fmt::blob_file_offset(mlen);
-    hb.bytes = m.blob_bytes;
-    if (pool_) hb.p = pool_->alloc(std::max<uint64_t>(hb.bytes, 1));
-    hb.pooled = hb.p != nullptr;
-    if (!hb.p) {
-      DeviceGuard g(cfg_.device);
-      TRIMS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hb.p), std::max<uint64_t>(hb.bytes, 1), cudaHostAllocPortable));
-    }
-    struct stat st {};
-    ::fstat(fd, &st);
-    if (uint64_t(st.st_size) < off + hb.bytes) raise(Errc::Corrupt, "blob truncated in " + path);
+  if (take_verified(m.key, m.blob_bytes, &hb)) {
+    // read_manifest already read + verified these bytes: only the upload is left
     uint64_t none = kNoOwner;
     if (prestage_enabled() && hb.bytes && pre_owner_.compare_exchange_strong(none, model_id)) {
-      // Read chunk c into the host tier while chunk c-1 uploads to the device.
       try {
         DeviceGuard g(cfg_.device);
-        // stream-ordered from a pool that keeps its memory: a cold open of
-        // any size reuses the blocks of earlier ones (no device-wide sync,
-        // no re-mapping)
         TRIMS_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&pre_raw_), hb.bytes, pre_pool_, pre_stream_));
-        auto r0 = std::chrono::steady_clock::now();
         TRIMS_CUDA(cudaEventRecord(pre_t0_, pre_stream_));
-        parallel_pread_upload(fd, hb.p, pre_raw_, hb.bytes, off, cfg_.read_threads, cfg_.device, pre_stream_);
+        TRIMS_CUDA(cudaMemcpyAsync(pre_raw_, hb.p, hb.bytes, cudaMemcpyHostToDevice, pre_stream_));
         TRIMS_CUDA(cudaEventRecord(pre_done_, pre_stream_));
-        pre_read_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - r0).count();
+        pre_read_ms_ = 0;
       } catch (...) {
         release_prestage(model_id);
+        free_host(hb);
         throw;
       }
-    } else {
-      parallel_pread(fd, hb.p, hb.bytes, off, cfg_.read_threads);
     }
-    if (cfg_.full_verify && Sha256::of(hb.p, hb.bytes) != m.checksum) raise(Errc::ChecksumMismatch, path);
-  } catch (...) {
-    release_prestage(model_id);
+  } else {
+    int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
+    if (fd < 0) raise(Errc::NotFound, path);
+    try {
+      uint8_t hdr[16];
+      if (::pread(fd, hdr, 16, 0) != 16) raise(Errc::Corrupt, "short read on " + path);
+      uint64_t mlen = 0;
+      for (int i = 0; i < 8; ++i) mlen |= uint64_t(hdr[8 + i]) << (8 * i);
+      const uint64_t off = fmt::blob_file_offset(mlen);
+      struct stat st {};
+      ::fstat(fd, &st);
+      if (uint64_t(st.st_size) < off + m.blob_bytes) raise(Errc::Corrupt, "blob truncated in " + path);
+      hb = alloc_host(m.blob_bytes);
+      // verify (daemon.cpp:155 read_model(path, full_verify)) in order under the read + upload
+      Sha256 h;
+      Sha256* hp = cfg_.full_verify ? &h : nullptr;
+      uint64_t none = kNoOwner;
+      if (prestage_enabled() && hb.bytes && pre_owner_.compare_exchange_strong(none, model_id)) {
+        // Read chunk c into the host tier while chunk c-1 uploads to the device.
+        try {
+          DeviceGuard g(cfg_.device);
+          // stream-ordered from a pool that keeps its memory: a cold open of
+          // any size reuses the blocks of earlier ones (no device-wide sync,
+          // no re-mapping)
+          TRIMS_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&pre_raw_), hb.bytes, pre_pool_, pre_stream_));
+          auto r0 = std::chrono::steady_clock::now();
+          TRIMS_CUDA(cudaEventRecord(pre_t0_, pre_stream_));
+          parallel_pread_upload(fd, hb.p, pre_raw_, hb.bytes, off, cfg_.read_threads, cfg_.device, pre_stream_, hp);
+          TRIMS_CUDA(cudaEventRecord(pre_done_, pre_stream_));
+          pre_read_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - r0).count();
+        } catch (...) {
+          release_prestage(model_id);
+          throw;
+        }
+      } else {
+        pipelined_read(fd, off, hb.bytes, hb.p, cfg_.read_threads, hp);
+      }
+      if (hp && h.finish() != m.checksum) raise(Errc::ChecksumMismatch, path);
+    } catch (...) {
+      release_prestage(model_id);
+      ::close(fd);
+      free_host(hb);
+      throw;
+    }
     ::close(fd);
-    free_host(hb);
-    throw;
   }
-  ::close(fd);
   std::lock_guard lk(mu_);
   auto it = host_.find(model_id);
   if (it != host_.end()) free_host(it->second);
@@ -650,6 +664,16 @@ FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Mani
     } else {
       rec->checksum = ing_.from_host(*plan, src, base, &rec->bucket_sums, &rec->stats);
     }
+  } else if (HostBuf vb; take_verified(m.key, m.blob_bytes, &vb)) {
+    // host tier skipped under pressure, but read_manifest holds the verified
+    // bytes: publish from them instead of reading the file again
+    try {
+      rec->checksum = ing_.from_host(*plan, vb.p, base, &rec->bucket_sums, &rec->stats);
+    } catch (...) {
+      free_host(vb);
+      throw;
+    }
+    free_host(vb);
   } else {
     int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
     if (fd < 0) raise(Errc::NotFound, path);

@@ -101,6 +101,7 @@ class Ingestor {
 struct BackendConfig {
   int device{0};
   std::string disk_cache_dir;
+  std::string remote_url;  // daemon.hpp:26 (http://... or dir:<path>; empty = no remote tier)
   bool full_verify{false};
   fmt::Plan plan;
   uint64_t pinned_pool_bytes{0};
@@ -147,6 +148,7 @@ class CudaTierBackend : public TierBackend {
   void evict_fast(uint64_t model_id) override;
   void evict_host(uint64_t model_id) override;
   void evict_disk(const fmt::ModelKey& key, const std::string& path) override;
+  void load_settled(const fmt::ModelKey& key) override;
   FastPublication publish_from_peer(uint64_t model_id, const fmt::Manifest& m, const PeerSource& src) override;
 
   std::shared_ptr<FastRecord> fast_record(uint64_t model_id);
@@ -164,6 +166,8 @@ class CudaTierBackend : public TierBackend {
   };
   void to_resident_form(uint64_t model_id, const FastRecord& rec, const IngestPlan& plan);
   void free_host(HostBuf& h);
+  HostBuf alloc_host(uint64_t bytes);
+  bool take_verified(const fmt::ModelKey& key, uint64_t bytes, HostBuf* out);
 
   std::shared_ptr<IngestPlan> plan_for(uint64_t model_id, const fmt::Manifest& m);
   std::shared_ptr<IngestPlan> pull_plan_for(uint64_t model_id, const fmt::Manifest& resident);
@@ -176,6 +180,11 @@ class CudaTierBackend : public TierBackend {
   std::unique_ptr<DeviceArena> arena_;
   std::mutex mu_;
   std::map<uint64_t, HostBuf> host_;
+  // full_verify: read_manifest reads the blob into pinned memory while hashing
+  // it (one pass, pread.hpp) and keeps the verified bytes here until the same
+  // open stages / publishes them, so they are neither read nor hashed twice
+  // (the reference reads + hashes in read_manifest, then again in read_model).
+  std::map<std::string, HostBuf> verified_;
   std::map<uint64_t, std::shared_ptr<FastRecord>> fast_;
   std::map<uint64_t, std::shared_ptr<IngestPlan>> plans_;  // model_id -> compiled plan (manifests are immutable)
   std::map<uint64_t, std::shared_ptr<IngestPlan>> pull_plans_;  // model_id -> identity plan of the resident blob
@@ -198,6 +207,7 @@ class CudaTierBackend : public TierBackend {
 };
 
 // Multi-threaded pread of [off, off+len) into dst (page cache -> pinned).
+// (parallel_pread_upload, the same with the in-order upload + hash, is local to backend.cu)
 void parallel_pread(int fd, uint8_t* dst, uint64_t len, uint64_t off, unsigned threads);
 
 }  // namespace trims

@@ -108,6 +108,10 @@ class TierBackend {
   // Extension, not part of the reference's eight: fill the fast tier from a
   // peer's sealed segment. The default refuses.
   virtual FastPublication publish_from_peer(uint64_t model_id, const fmt::Manifest& m, const PeerSource& src);
+  // Extension: the open of `key` that called read_manifest has settled
+  // (published or failed). Called under the core mutex; must not block. Lets a
+  // backend drop per-load state, e.g. a blob it read while verifying.
+  virtual void load_settled(const fmt::ModelKey&) {}
 };
 
 struct PlacementResult {

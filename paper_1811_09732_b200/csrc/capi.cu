@@ -21,6 +21,7 @@
 #include "format.hpp"
 #include "gemm.hpp"
 #include "nn.hpp"
+#include "remote.hpp"
 #include "sha256.hpp"
 #include "store_api.hpp"
 
@@ -369,6 +370,7 @@ BackendConfig backend_config(const trims_store_config* cfg) {
   bc.device = cfg->device;
   bc.disk_cache_dir = cfg->disk_cache_dir;
   bc.full_verify = cfg->full_verify != 0;
+  if (cfg->remote_url) bc.remote_url = cfg->remote_url;
   bc.plan = make_plan(cfg->plan_flags, cfg->out_dtype);
   bc.pinned_pool_bytes = cfg->pinned_pool_bytes ? cfg->pinned_pool_bytes : cfg->host_capacity_bytes;
   bc.read_threads = cfg->read_threads ? cfg->read_threads : 8;
@@ -421,6 +423,33 @@ int trims_backend_locate(trims_backend* b, const char* ns, const char* name, con
     if (l.kind == Located::Kind::Absent) raise(Errc::NotFound, std::string(ns) + "/" + name + "@" + version);
     if (file_bytes) *file_bytes = l.file_bytes;
     return put(l.path, path_out, cap);
+  });
+}
+
+int trims_backend_fetch_remote(trims_backend* b, const char* ns, const char* name, const char* version,
+                               char* path_out, uint64_t cap, uint64_t* file_bytes) {
+  return guard([&] {
+    FetchResult f = b->be->fetch_remote({ns, name, version});
+    if (file_bytes) *file_bytes = f.file_bytes;
+    return put(f.path, path_out, cap);
+  });
+}
+
+int trims_backend_load_settled(trims_backend* b, const char* ns, const char* name, const char* version) {
+  return guard([&] {
+    b->be->load_settled({ns, name, version});
+    return 0;
+  });
+}
+
+int trims_remote_fetch(const char* url, const char* ns, const char* name, const char* version, const char* dest_dir,
+                       char* path_out, uint64_t cap, uint64_t* file_bytes) {
+  return guard([&] {
+    if (!url || !dest_dir) raise(Errc::InvalidArgument, "null argument");
+    std::string p = remote::fetch(remote::make_ref(url, {ns, name, version}), dest_dir);
+    std::error_code ec;
+    if (file_bytes) *file_bytes = uint64_t(std::filesystem::file_size(p, ec));
+    return put(p, path_out, cap);
   });
 }
 

@@ -14,6 +14,7 @@
 #include <memory>
 #include <variant>
 
+#include "pread.hpp"
 #include "sha256.hpp"
 
 namespace trims::fmt {
@@ -576,16 +577,8 @@ ArtifactInfo read_artifact_info(const std::string& path, bool full_verify) {
   ArtifactInfo a = parse_head(head.data(), head_len, total);
   pread_all(f.fd, a.manifest.checksum.data(), 32, a.blob_offset + a.manifest.blob_bytes);
   if (full_verify) {
-    Sha256 h;
-    std::vector<uint8_t> buf(4u << 20);
-    uint64_t left = a.manifest.blob_bytes, off = a.blob_offset;
-    while (left) {
-      uint64_t take = std::min<uint64_t>(left, buf.size());
-      pread_all(f.fd, buf.data(), take, off);
-      h.update(buf.data(), take);
-      left -= take;
-      off += take;
-    }
+    Sha256 h;  // readers ahead of one in-order hasher (pread.hpp)
+    pipelined_read(f.fd, a.blob_offset, a.manifest.blob_bytes, nullptr, 8, &h);
     if (h.finish() != a.manifest.checksum) raise(Errc::ChecksumMismatch, path);
   }
   return a;

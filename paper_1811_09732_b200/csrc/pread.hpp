@@ -1,0 +1,27 @@
+// pread.hpp — the disk side of the cold path: a file range read by several
+// threads in 4 MiB pieces, with the pieces handed IN ORDER to a SHA-256 (on
+// its own thread) and to a caller-side sink (the PCIe upload), so a verified
+// load costs max(read, hash, upload) instead of their sum (
+// replaces the reference's ifstream read + separate 1 MiB hash loop,
+// model_format.cpp:370-429).
+#pragma once
+
+#include <cstdint>
+#include <functional>
+
+#include "sha256.hpp"
+
+namespace trims {
+
+constexpr uint64_t kReadPiece = 4ull << 20;
+
+// Reads [off, off+len) of fd. dst != nullptr: the bytes land there. dst ==
+// nullptr: pieces go through a small ring (verify-only). hash (optional) is
+// updated with the range in order on a dedicated thread. in_order (optional)
+// is called on the calling thread for each piece in order, once it has landed:
+// (piece pointer, byte offset within the range, bytes). A short read raises
+// Corrupt; an exception from in_order stops the readers and is rethrown.
+void pipelined_read(int fd, uint64_t off, uint64_t len, uint8_t* dst, unsigned threads, Sha256* hash,
+                    const std::function<void(const uint8_t*, uint64_t, uint64_t)>& in_order = {});
+
+}  // namespace trims

@@ -31,6 +31,7 @@ class StoreOptions:
     policy: int = LRU
     eager_reclaim: bool = False
     full_verify: bool = False
+    remote_url: str | None = None      # daemon.hpp:26: "http://host:port/prefix" or "dir:<path>"
     device: int = 0
     convert_to: str | None = None      # e.g. "bf16": floating tensors converted at ingest
     permute_4d: bool = False           # KCRS -> KRSC (NHWC conv weights) at ingest
@@ -73,6 +74,8 @@ class Store:
         cfg.rank = opts.rank
         cfg.world = opts.world
         cfg.directory_slots = opts.directory_slots
+        self._remote = opts.remote_url.encode() if opts.remote_url else None
+        cfg.remote_url = self._remote
         h = ctypes.c_void_p()
         check(lib.trims_store_create(ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h
