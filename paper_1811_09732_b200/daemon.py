@@ -256,12 +256,15 @@ def main(argv=None) -> int:
     ap.add_argument("--convert-to", default="bf16", help="resident dtype of floating tensors ('' keeps them)")
     ap.add_argument("--no-permute", action="store_true", help="keep 4-D filters KCRS")
     ap.add_argument("--eager-reclaim", action="store_true")
+    ap.add_argument("--full-verify", action="store_true", help="verify the blob SHA-256 on every disk load")
+    ap.add_argument("--remote", default=None, help="remote store: http://host[:port][/prefix] or dir:<path>")
     a = ap.parse_args(argv)
     opts = StoreOptions(disk_cache_dir=a.disk_cache, fast_capacity_bytes=a.fast_capacity,
                         host_capacity_bytes=a.host_capacity, disk_capacity_bytes=a.disk_capacity,
                         policy=0 if a.policy == "lru" else 1, device=a.device,
                         convert_to=a.convert_to or None, permute_4d=not a.no_permute,
-                        eager_reclaim=a.eager_reclaim, scan_disk=True)
+                        eager_reclaim=a.eager_reclaim, scan_disk=True, full_verify=a.full_verify,
+                        remote_url=a.remote)
     stop = threading.Event()
     with Store(opts) as s, serve(s, a.listen):
         signal.signal(signal.SIGINT, lambda *_: stop.set())
