@@ -52,6 +52,26 @@ const RingCfg& ring_cfg() {
 #endif
 constexpr int kConsumerWarps = TRIMS_CONSUMER_WARPS;  // TMA kernel: 1 producer warp + consumer warps
 constexpr int kTmaThreads = 32 * (kConsumerWarps + 1);
+
+#ifdef TRIMS_TRACE
+// Diagnostic build only (make EXTRA=-DTRIMS_TRACE ...; scripts/transform_trace.py):
+// per CTA [start, first stage ready, last push issued, end, staged bytes, tiles,
+// static bin issued, dynamic tiles taken] (times in %globaltimer ns).
+constexpr int kTraceW = 8;
+__device__ unsigned long long g_ttrace[1024 * kTraceW];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE_SET(i, v) (g_ttrace[blockIdx.x * kTraceW + (i)] = (v))
+#define TRACE_MAX(i, v) atomicMax(&g_ttrace[blockIdx.x * kTraceW + (i)], (v))
+#define TRACE_ADD(i, v) (g_ttrace[blockIdx.x * kTraceW + (i)] += (v))
+#else
+#define TRACE_SET(i, v) ((void)0)
+#define TRACE_MAX(i, v) ((void)0)
+#define TRACE_ADD(i, v) ((void)0)
+#endif
 constexpr uint32_t kDescCap = 384;
 constexpr int kDefaultTailPct = 15;  // dynamic share of a TMA group's tile cost  // static-schedule descriptors staged in smem per batch (18 KiB)
 
@@ -551,8 +571,15 @@ __device__ __forceinline__ void consume_tiles(const uint8_t* ring, uint64_t* ful
   uint32_t bucket = ~0u;  // per-warp checksum accumulator, flushed when the tensor changes
   uint64_t wacc = 0;
   uint32_t s = 0, phase = 0;
+#ifdef TRIMS_TRACE
+  bool first = true;
+#endif
   for (;;) {
     mbar_wait(&full[s], phase);
+#ifdef TRIMS_TRACE
+    if (first && cw == 0 && lane == 0) TRACE_SET(1, gtimer());
+    first = false;
+#endif
     const Tile t = staged[s];
     if (t.op == OP_END) break;
     const ST* el = reinterpret_cast<const ST*>(ring + s * stage_alloc + (t.src_off & 15));
@@ -666,6 +693,9 @@ __device__ __forceinline__ void consume_tiles(const uint8_t* ring, uint64_t* ful
     const uint64_t v = warp_sum64(wacc);
     if (lane == 0 && v) atomicAdd(&sums[bucket], (unsigned long long)v);
   }
+#ifdef TRIMS_TRACE
+  if (lane == 0) TRACE_MAX(3, gtimer());
+#endif
 }
 
 // Warp-specialised: warp 0 is the producer (one elected lane issues the bulk
@@ -691,16 +721,29 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
   __shared__ __align__(16) Tile descs[kDescCap];  // static schedule: this CTA's descriptors
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // PDL: let the next launch in the stream start its prologue on SMs as ours
+  // free up. Everything here that touches memory a previous kernel may have
+  // written (src, dst, sums, the ticket counters) happens after the
+  // producer's griddepcontrol.wait below: consumers only act on staged data.
+  pdl_trigger();
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#ifdef TRIMS_TRACE
+    TRACE_SET(0, gtimer());
+    TRACE_SET(3, 0);
+    TRACE_SET(4, 0);
+    TRACE_SET(5, 0);
+    TRACE_SET(7, 0);
+#endif
   }
   __syncthreads();
 
   if (warp == 0) {  // ---------------- producer
+    pdl_wait();
     uint32_t s = 0, round = 0;  // ring slot, and how many times the ring has wrapped
     auto push = [&](const Tile& t) {  // lane 0: stage t's raw bytes into slot s
       if (round) mbar_wait(&empty[s], (round - 1) & 1);
@@ -708,6 +751,8 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
       const uint64_t b = t.src_off & ~15ull, e = (t.src_off + uint64_t(t.n_elem) * SS + 15) & ~15ull;
       mbar_expect_tx(&full[s], uint32_t(e - b));
       bulk_g2s(ring + s * stage_alloc, src + b, uint32_t(e - b), &full[s]);
+      TRACE_ADD(4, e - b);
+      TRACE_ADD(5, 1);
       if (++s == stages) {
         s = 0;
         ++round;
@@ -737,6 +782,7 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
       }
     }
     if (lane == 0) {
+      TRACE_SET(6, gtimer());
       if (sched && tail0 < ntiles) {
         // Dynamic part: tiles [tail0, ntiles) handed out by a ticket counter,
         // so CTAs that ran slow take fewer of them. The next ticket and its
@@ -748,11 +794,13 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
           ti = tail0 + (atomicAdd(sched, 1u) - ticket_base);
           if (ti < ntiles) next = tiles[ti];
           push(t);
+          TRACE_ADD(7, 1);
         }
       } else if (!stride) {  // no schedule at all: static round robin
         for (uint32_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) push(tiles[ti]);
       }
       // end marker: consumers leave
+      TRACE_SET(2, gtimer());
       if (round) mbar_wait(&empty[s], (round - 1) & 1);
       staged[s].op = OP_END;
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
@@ -1166,14 +1214,25 @@ uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, co
       };
       unsigned int* slot = nullptr;
       uint32_t base = 0;
+      static const bool pdl = [] {  // A/B switch: TRIMS_TRANSFORM_PDL=0
+        const char* e = std::getenv("TRIMS_TRANSFORM_PDL");
+        return !(e && std::string(e) == "0");
+      }();
+      auto go = [&](uint32_t ctas, const unsigned int* sl, uint32_t b, uint32_t stride, uint32_t tail0) {
+        if (pdl)
+          launch_pdl(fn, dim3(ctas), dim3(kTmaThreads), size_t(smem), st, t, n, src, dst, d_sums, rc.stages,
+                     rc.stage_alloc(), const_cast<unsigned int*>(sl), b, stride, tail0);
+        else
+          fn<<<ctas, kTmaThreads, smem, st>>>(t, n, src, dst, d_sums, rc.stages, rc.stage_alloc(),
+                                              const_cast<unsigned int*>(sl), b, stride, tail0);
+      };
       if (g.nbins) {  // static schedule: one CTA per bin (+ dynamic tail)
         if (g.tail) take_slot(g.tail, g.nbins, &slot, &base);
-        fn<<<g.nbins, kTmaThreads, smem, st>>>(t, n, src, dst, d_sums, rc.stages, rc.stage_alloc(), slot, base,
-                                               g.stride, g.nbins * g.stride);
+        go(g.nbins, slot, base, g.stride, g.nbins * g.stride);
       } else {
         const uint32_t ctas = std::min<uint32_t>(n, sm_count * rc.ctas_per_sm);
         if (dynamic) take_slot(n, ctas, &slot, &base);
-        fn<<<ctas, kTmaThreads, smem, st>>>(t, n, src, dst, d_sums, rc.stages, rc.stage_alloc(), slot, base, 0u, 0u);
+        go(ctas, slot, base, 0u, 0u);
       }
     } else {
       TransformFn fn = pair_kernel(g.sdt, g.ddt);
@@ -1234,3 +1293,19 @@ void launch_fill_uniform(float* dst, uint64_t n, uint64_t stream_seed, uint64_t 
 }
 
 }  // namespace trims::ingest
+
+#ifdef TRIMS_TRACE
+extern "C" int trims_debug_transform_trace(unsigned long long* out, int n) {
+  return int(cudaMemcpyFromSymbol(out, trims::ingest::g_ttrace, sizeof(unsigned long long) * size_t(n)));
+}
+
+__global__ void trims_debug_empty_kernel() {}
+
+// An empty launch with the transform's shared-memory footprint on every SM:
+// separates the SM carve-out reconfiguration from the transform itself.
+extern "C" int trims_debug_carveout(int smem, int ctas, void* stream) {
+  cudaFuncSetAttribute(trims_debug_empty_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  trims_debug_empty_kernel<<<ctas, 544, smem, static_cast<cudaStream_t>(stream)>>>();
+  return int(cudaGetLastError());
+}
+#endif
