@@ -4,12 +4,12 @@
 #include <unistd.h>
 
 #include <algorithm>
-#include <atomic>
 #include <condition_variable>
 #include <cstdlib>
 #include <exception>
 #include <memory>
 #include <mutex>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -17,30 +17,65 @@
 
 namespace trims {
 
+namespace {
+
+struct Piece {
+  uint64_t begin, bytes;
+};
+
+uint64_t env_kb(const char* name, uint64_t dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::max<uint64_t>(64, std::strtoull(e, nullptr, 10)) << 10 : dflt;
+}
+
+// kReadPiece pieces, except that the last `readers` x kReadPiece bytes are cut
+// 2x finer: the final wave of reads then lands in small pieces, so the upload
+// and hash left after the last read are short.
+std::vector<Piece> cut(uint64_t len, unsigned readers) {
+  static const uint64_t piece = env_kb("TRIMS_READ_PIECE_KB", kReadPiece);
+  static const uint64_t fine = env_kb("TRIMS_READ_FINE_KB", kReadPiece / 2);
+  std::vector<Piece> v;
+  const uint64_t fine_from = len > uint64_t(readers) * piece ? len - uint64_t(readers) * piece : 0;
+  for (uint64_t at = 0; at < len;) {
+    const uint64_t step = at >= fine_from ? fine : piece;
+    const uint64_t n = std::min(step, len - at);
+    v.push_back({at, n});
+    at += n;
+  }
+  return v;
+}
+
+}  // namespace
+
 void pipelined_read(int fd, uint64_t off, uint64_t len, uint8_t* dst, unsigned threads, Sha256* hash,
-                    const std::function<void(const uint8_t*, uint64_t, uint64_t)>& in_order) {
-  const uint64_t pieces = (len + kReadPiece - 1) / kReadPiece;
-  if (!pieces) return;
-  const unsigned readers = unsigned(std::clamp<uint64_t>(pieces, 1, std::max(1u, threads)));
-  // verify-only: a ring of slots, piece i in slot i % ring, reusable once
-  // every consumer is past piece i - ring
-  const uint64_t ring = dst ? pieces : std::min<uint64_t>(pieces, 2 * readers + 2);
+                    const std::function<void(const uint8_t*, uint64_t, uint64_t)>& sink, bool sink_any_order) {
+  if (!len) return;
+  const unsigned want = std::max(1u, threads);
+  const std::vector<Piece> pieces = cut(len, want);
+  const uint64_t np = pieces.size();
+  const unsigned readers = unsigned(std::min<uint64_t>(np, want));
+  if (!dst) sink_any_order = false;
+  // verify-only: a ring of kReadPiece slots, piece i in slot i % ring,
+  // reusable once every consumer is past piece i - ring
+  const uint64_t ring = dst ? np : std::min<uint64_t>(np, 2 * readers + 2);
+  uint64_t slot = 0;
+  for (const Piece& p : pieces) slot = std::max<uint64_t>(slot, (p.bytes + 4095) & ~4095ull);
   std::unique_ptr<uint8_t, void (*)(void*)> ring_mem(nullptr, std::free);
   if (!dst) {
-    ring_mem.reset(static_cast<uint8_t*>(std::aligned_alloc(4096, ring * kReadPiece)));
+    ring_mem.reset(static_cast<uint8_t*>(std::aligned_alloc(4096, ring * slot)));
     if (!ring_mem) raise(Errc::Internal, "read ring allocation failed");
   }
-  auto at = [&](uint64_t i) { return dst ? dst + i * kReadPiece : ring_mem.get() + (i % ring) * kReadPiece; };
-  const bool hashing = hash != nullptr, sinking = bool(in_order);
+  auto at = [&](uint64_t i) { return dst ? dst + pieces[i].begin : ring_mem.get() + (i % ring) * slot; };
+  const bool hashing = hash != nullptr, sinking = bool(sink);
 
   std::mutex mu;
   std::condition_variable cv;
-  std::vector<uint8_t> landed(pieces, 0);
-  uint64_t next = 0, hashed = 0, sunk = 0;  // guarded by mu
+  std::vector<uint8_t> landed(np, 0), sunk_flag(np, 0);
+  uint64_t next = 0, hashed = 0, sunk = 0;  // guarded by mu; sunk = pieces handed to the sink
   bool failed = false;
   std::exception_ptr err;
-  auto retired = [&] {  // pieces every consumer is done with
-    uint64_t r = pieces;
+  auto retired = [&] {  // in-order prefix every consumer is done with (ring mode)
+    uint64_t r = np;
     if (hashing) r = std::min(r, hashed);
     if (sinking) r = std::min(r, sunk);
     return r;
@@ -58,15 +93,15 @@ void pipelined_read(int fd, uint64_t off, uint64_t len, uint8_t* dst, unsigned t
         uint64_t i;
         {
           std::unique_lock lk(mu);
-          if (failed || next >= pieces) return;
+          if (failed || next >= np) return;
           i = next++;
           if (!dst) cv.wait(lk, [&] { return failed || i < retired() + ring; });
           if (failed) return;
         }
-        const uint64_t b = i * kReadPiece, n = std::min(len - b, kReadPiece);
+        const Piece pc = pieces[i];
         uint8_t* p = at(i);
-        for (uint64_t got = 0; got < n;) {
-          ssize_t r = ::pread(fd, p + got, size_t(n - got), off_t(off + b + got));
+        for (uint64_t got = 0; got < pc.bytes;) {
+          ssize_t r = ::pread(fd, p + got, size_t(pc.bytes - got), off_t(off + pc.begin + got));
           if (r <= 0) raise(Errc::Corrupt, "blob truncated (short read)");
           got += uint64_t(r);
         }
@@ -78,21 +113,6 @@ void pipelined_read(int fd, uint64_t off, uint64_t len, uint8_t* dst, unsigned t
       fail(std::current_exception());
     }
   };
-  // one in-order consumer: waits for piece i, runs fn, advances its cursor
-  auto consume = [&](uint64_t& cursor, const std::function<void(const uint8_t*, uint64_t, uint64_t)>& fn) {
-    for (uint64_t i = 0; i < pieces; ++i) {
-      {
-        std::unique_lock lk(mu);
-        cv.wait(lk, [&] { return failed || landed[i]; });
-        if (failed) return;
-      }
-      const uint64_t b = i * kReadPiece;
-      fn(at(i), b, std::min(len - b, kReadPiece));
-      std::lock_guard lk(mu);
-      cursor = i + 1;
-      cv.notify_all();
-    }
-  };
 
   std::vector<std::thread> ts;
   ts.reserve(readers + 1);
@@ -100,7 +120,17 @@ void pipelined_read(int fd, uint64_t off, uint64_t len, uint8_t* dst, unsigned t
   if (hashing) {
     ts.emplace_back([&] {
       try {
-        consume(hashed, [&](const uint8_t* p, uint64_t, uint64_t n) { hash->update(p, n); });
+        for (uint64_t i = 0; i < np; ++i) {
+          {
+            std::unique_lock lk(mu);
+            cv.wait(lk, [&] { return failed || landed[i]; });
+            if (failed) return;
+          }
+          hash->update(at(i), pieces[i].bytes);
+          std::lock_guard lk(mu);
+          hashed = i + 1;
+          cv.notify_all();
+        }
       } catch (...) {
         fail(std::current_exception());
       }
@@ -108,7 +138,36 @@ void pipelined_read(int fd, uint64_t off, uint64_t len, uint8_t* dst, unsigned t
   }
   if (sinking) {
     try {
-      consume(sunk, in_order);
+      uint64_t lo = 0;  // every piece below lo has been sunk
+      for (uint64_t done = 0; done < np; ++done) {
+        uint64_t i = np;
+        {
+          std::unique_lock lk(mu);
+          cv.wait(lk, [&] {
+            if (failed) return true;
+            while (lo < np && sunk_flag[lo]) ++lo;
+            if (!sink_any_order) return lo < np && landed[lo];
+            for (uint64_t j = lo; j < next && j < np; ++j)
+              if (landed[j] && !sunk_flag[j]) return true;
+            return false;
+          });
+          if (failed) break;
+          if (!sink_any_order) {
+            i = lo;
+          } else {
+            for (uint64_t j = lo; j < np; ++j)
+              if (landed[j] && !sunk_flag[j]) {
+                i = j;
+                break;
+              }
+          }
+        }
+        sink(at(i), pieces[i].begin, pieces[i].bytes);
+        std::lock_guard lk(mu);
+        sunk_flag[i] = 1;
+        while (sunk < np && sunk_flag[sunk]) ++sunk;
+        cv.notify_all();
+      }
     } catch (...) {
       fail(std::current_exception());
     }
