@@ -554,10 +554,7 @@ def request_latencies(work: str, arch, dev: int, batch: int = 1, reps: int = 7) 
         t2 = time.perf_counter()
         if logits is None:
             logits = torch.empty(batch, net.classes).pin_memory()
-        net.input_view().copy_(x, non_blocking=True)
-        net.run(stream.cuda_stream, True)
-        logits.copy_(net.logits_view(), non_blocking=True)
-        stream.synchronize()
+        net.infer(x, logits, stream.cuda_stream)  # H2D input -> graph forward -> D2H logits -> sync
         t3 = time.perf_counter()
         cli.close(v)
         t4 = time.perf_counter()
@@ -596,10 +593,7 @@ def request_latencies(work: str, arch, dev: int, batch: int = 1, reps: int = 7) 
         ts = []
         for _ in range(reps * 3):
             t0 = time.perf_counter()
-            net.input_view().copy_(x, non_blocking=True)
-            net.run(stream.cuda_stream, True)
-            logits.copy_(net.logits_view(), non_blocking=True)
-            stream.synchronize()
+            net.infer(x, logits, stream.cuda_stream)
             ts.append((time.perf_counter() - t0) * 1e3)
         out["compute_only"] = round(statistics.median(ts[1:]), 4)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

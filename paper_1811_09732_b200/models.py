@@ -77,6 +77,24 @@ class BoundNet:
     def run(self, stream=None, graph: bool = True) -> None:
         check(lib.trims_net_run(self._h, stream, int(graph)))
 
+    def infer(self, x, out=None, stream=None, graph: bool = True):
+        """One request through the C ABI (trims_net_forward_host): H2D of the
+        host input, the forward (one CUDA graph launch), D2H of the logits,
+        stream sync. x: fp32 NCHW host tensor/array (pinned for full PCIe
+        rate); out: a host [batch, classes] fp32 buffer (allocated if None)."""
+        import numpy as np
+        if out is None:
+            out = np.empty((self.batch, self.classes), np.float32)
+        xp = x.data_ptr() if hasattr(x, "data_ptr") else x.ctypes.data
+        op = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+        n_in = self.batch * 3 * self.input_hw * self.input_hw
+        n = x.numel() if hasattr(x, "numel") else x.size
+        m = out.numel() if hasattr(out, "numel") else out.size
+        if n != n_in or m != self.batch * self.classes:
+            raise ValueError("input / output sizes do not match the bound net")
+        check(lib.trims_net_forward_host(self._h, xp, op, stream, int(graph)))
+        return out
+
     def forward(self, x, graph: bool = True):
         """x: fp32 NCHW (any device). Returns the fp32 logits on the GPU."""
         import torch
