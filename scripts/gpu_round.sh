@@ -1,7 +1,7 @@
 #!/bin/bash
 # One GPU-box pass: gpu tests, a bench line, the ncu launch list of the bench
 # command, and one full ncu capture of the transform kernel.
-# usage: bash scripts/gpu_round.sh <tag> [tests|bench|ncu ...]
+# usage: bash scripts/gpu_round.sh <tag> [tests|bench|reference|multi|ncu ...]
 tag=${1:-r01}; shift
 what=${@:-tests bench ncu}
 mkdir -p gpurun_out
@@ -13,6 +13,8 @@ for w in $what; do
       echo "pytest exit $?" >> gpurun_out/${tag}_pytest_gpu.log ;;
     bench)
       timeout 900 python bench.py > gpurun_out/${tag}_bench.jsonl 2> gpurun_out/${tag}_bench.err ;;
+    reference)
+      timeout 900 python bench.py --impl reference > gpurun_out/${tag}_bench_reference.jsonl 2> gpurun_out/${tag}_bench_reference.err ;;
     multi)
       TRIMS_BENCH_SHARED_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
         --master-addr 127.0.0.1 --master-port 29611 bench.py --gpus 2 --steps 5 --warmup 3 --quick \
