@@ -46,11 +46,17 @@ class CudaTierBackend : public cache::TierBackend {
                                   &bytes);
     if (rc == int(Errc::NotFound)) return {cache::Located::Kind::Absent, "", 0};
     check(rc, "locate");
+    if (!path[0]) return {cache::Located::Kind::Remote, "", 0};  // not on disk, remote_url set
     return {cache::Located::Kind::DiskCache, path, bytes};
   }
 
-  cache::FetchResult fetch_remote(const model::ModelKey& key) override {
-    raise(Errc::RemoteNotFound, model::to_string(key));  // the remote tier is not part of the B200 path
+  cache::FetchResult fetch_remote(const model::ModelKey& key) override {  // daemon.cpp:138-142
+    char path[4096];
+    uint64_t bytes = 0;
+    check(trims_backend_fetch_remote(be_, key.ns.c_str(), key.name.c_str(), key.version.c_str(), path, sizeof path,
+                                     &bytes),
+          "fetch_remote");
+    return {path, bytes};
   }
 
   model::ModelManifest read_manifest(const model::ModelKey& key, const std::string& path) override {
