@@ -111,8 +111,9 @@ class CudaTierBackend : public cache::TierBackend {
 // Test driver: the unmodified reference CacheCore over the CUDA backend.
 // ops: "o <name>" / "c <name>" lines on catalog keys zoo/<name>@1.0.0 in `dir`.
 // Output per op: "<outcome> <fast_used> <host_used> <refcount> <token>".
-extern "C" int refcuda_replay(const char* dir, uint64_t fast_cap, uint64_t host_cap, int eager, const char* ops,
-                              char* out, uint64_t cap) {
+// remote (may be NULL): DaemonConfig::remote_url; full_verify as DaemonConfig.
+extern "C" int refcuda_replay2(const char* dir, const char* remote, int full_verify, uint64_t fast_cap,
+                               uint64_t host_cap, int eager, const char* ops, char* out, uint64_t cap) {
   using namespace mrm;
   try {
     trims_store_config cfg{};
@@ -120,6 +121,8 @@ extern "C" int refcuda_replay(const char* dir, uint64_t fast_cap, uint64_t host_
     cfg.host_capacity_bytes = host_cap;
     cfg.disk_capacity_bytes = 1ull << 40;
     cfg.disk_cache_dir = dir;
+    cfg.remote_url = remote;
+    cfg.full_verify = full_verify != 0;
     mrm_b200::CudaTierBackend be(cfg);
     cache::CoreConfig cc{fast_cap, host_cap, 1ull << 40, cache::Policy::LRU, eager != 0};
     cache::CacheCore core(cc, be);
@@ -155,4 +158,9 @@ extern "C" int refcuda_replay(const char* dir, uint64_t fast_cap, uint64_t host_
   } catch (...) {
     return 7;
   }
+}
+
+extern "C" int refcuda_replay(const char* dir, uint64_t fast_cap, uint64_t host_cap, int eager, const char* ops,
+                              char* out, uint64_t cap) {
+  return refcuda_replay2(dir, nullptr, 0, fast_cap, host_cap, eager, ops, out, cap);
 }
