@@ -72,8 +72,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TRACE_MAX(i, v) ((void)0)
 #define TRACE_ADD(i, v) ((void)0)
 #endif
-constexpr uint32_t kDescCap = 384;
-constexpr int kDefaultTailPct = 15;  // dynamic share of a TMA group's tile cost  // static-schedule descriptors staged in smem per batch (18 KiB)
+constexpr uint32_t kDescCap = 384;  // static-schedule descriptors staged in smem per batch (18 KiB)
+// dynamic share of a TMA group's tile cost: 20 % measured best back to back
+// (ResNet-50 28.3 vs 28.8 us at 15 %, VGG-16 125.7 vs 126.3 us; profiles/r01f/transform_tail_ab.log)
+constexpr int kDefaultTailPct = 20;
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -906,10 +908,17 @@ void schedule_bins(std::vector<Tile>& table, Group& g, uint32_t grid, std::vecto
   const uint32_t n = g.end - g.begin, nb = std::min(n, grid);
   std::vector<uint32_t> order(n);
   std::vector<uint64_t> cost(n);
+  // TRIMS_PERM_WEIGHT (percent, A/B): extra weight of gathered (RS > 1)
+  // permute tiles over streaming ones
+  static const uint64_t perm_w = [] {
+    const char* e = std::getenv("TRIMS_PERM_WEIGHT");
+    return e ? uint64_t(std::clamp(std::atoi(e), 50, 400)) : uint64_t(100);
+  }();
   for (uint32_t i = 0; i < n; ++i) {
     const Tile& t = table[g.begin + i];
     order[i] = i;
     cost[i] = kFixed + t.dst_bytes + uint64_t(t.n_elem) * fmt::element_size(fmt::DType(t.sdt));
+    if (t.op == OP_PERM && t.RS > 1) cost[i] = cost[i] * perm_w / 100;
   }
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cost[a] > cost[b]; });
   // The smallest tiles worth `tail_pct` % of the cost form the dynamic tail
