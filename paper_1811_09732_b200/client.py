@@ -14,6 +14,7 @@ import ctypes
 import json
 import os
 import time
+from collections.abc import Sequence
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -105,7 +106,35 @@ class ModelView:
 _PARSED: dict = {}  # manifest JSON -> parsed tensor records (manifests are immutable)
 
 
-def slice_tensors(manifest_json: str, base_ptr: int) -> list[TensorView]:
+class TensorViews(Sequence):
+    """The views of one attached model, built on first access: a warm open of
+    a new generation then costs no per-tensor Python objects (267 for
+    ResNet-50) until a caller actually walks the tensors."""
+
+    __slots__ = ("_recs", "_base", "_made")
+
+    def __init__(self, recs, base_ptr: int):
+        self._recs, self._base, self._made = recs, base_ptr, {}
+
+    def __len__(self):
+        return len(self._recs)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self._recs)))]
+        if i < 0:
+            i += len(self._recs)
+        v = self._made.get(i)
+        if v is None:
+            n, d, dt, lay, off, nb = self._recs[i]
+            v = self._made[i] = TensorView(n, d, dt, lay, off, nb, self._base + off)
+        return v
+
+    def __eq__(self, other):
+        return list(self) == list(other)
+
+
+def slice_tensors(manifest_json: str, base_ptr: int) -> TensorViews:
     """client.cpp:60-65 with device pointers; the parse is cached per manifest
     (client.cpp:293-307 caches it by digest), so a new generation of a model
     only re-bases the views."""
@@ -116,7 +145,7 @@ def slice_tensors(manifest_json: str, base_ptr: int) -> list[TensorView]:
         if len(_PARSED) > 256:
             _PARSED.clear()
         _PARSED[manifest_json] = recs
-    return [TensorView(n, d, dt, lay, off, nb, base_ptr + off) for n, d, dt, lay, off, nb in recs]
+    return TensorViews(recs, base_ptr)
 
 
 class ImportCache:
@@ -278,7 +307,7 @@ class Client:
             mjson, seen, tensors = hit
         if seen != digest:
             raise TrimsError(Errc.Corrupt, "Corrupt", "manifest digest mismatch on attach")
-        view = ModelView(key, SHARED, "none", mjson, base, list(tensors), ex.model_id, ex.generation,
+        view = ModelView(key, SHARED, "none", mjson, base, tensors, ex.model_id, ex.generation,
                          outcome=_outcome(ex.outcome), export=ex)
         view.timings.rpc_s = t1 - t0
         view.timings.attach_s = time.perf_counter() - t1
