@@ -239,10 +239,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       // Split-K: park this split's fp32 partial tile in the (now idle) ring,
       // column-major so a warp's accesses are contiguous.
       float* part = reinterpret_cast<float*>(smem);
+      // A split can own no k-blocks (ceil(kblocks / splits) * (splits - 1)
+      // >= kblocks): no MMA wrote its accumulator, so its partial is zero.
+      const bool no_k = kb0 >= kb1;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16) {
         uint32_t r[16];
-        tmem_ld16(tq + uint32_t(c0), r);
+        if (no_k) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) r[j] = 0u;
+        } else {
+          tmem_ld16(tq + uint32_t(c0), r);
+        }
 #pragma unroll
         for (int j = 0; j < 16; ++j) part[(c0 + j) * BM + rl] = __uint_as_float(r[j]);
       }
@@ -413,7 +421,11 @@ int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms) {
   // layer3/4 3x3 convs at batch 1); measured slower for 16 tiles (VGG-16
   // conv5), profiles/r03d_split.log.
   const int max_s = tiles <= 8 ? kMaxSplits : 4;
-  while (s < max_s && bn / (s * 2) >= 8 && tiles * uint64_t(s * 2) <= uint64_t(sms) && kb / uint64_t(s * 2) >= 4)
+  static const uint64_t min_kb = [] {  // k-blocks each split keeps at least (A/B: TRIMS_SPLIT_MINKB)
+    const char* e = std::getenv("TRIMS_SPLIT_MINKB");
+    return e ? uint64_t(std::max(1, std::atoi(e))) : uint64_t(4);
+  }();
+  while (s < max_s && bn / (s * 2) >= 8 && tiles * uint64_t(s * 2) <= uint64_t(sms) && kb / uint64_t(s * 2) >= min_kb)
     s *= 2;
   return s;
 }

@@ -13,6 +13,8 @@ pytestmark = pytest.mark.gpu
     (128, 64, 64, 64), (256, 128, 128, 128), (300, 200, 96, 64), (1000, 256, 576, 256),
     (49, 2048, 512, 64), (3136, 64, 576, 64), (17, 1000, 4096, 128), (777, 384, 2304, 128),
     (512, 512, 1024, 256),
+    # 33 k-blocks over 8 splits of ceil(33/8) = 5: the last split owns none
+    (49, 512, 2112, 64), (49, 512, 2112, 128),
 ])
 @pytest.mark.parametrize("epi", ["plain", "full"])
 def test_gemm_matches_fp32_reference(M, N, K, bn, epi):
