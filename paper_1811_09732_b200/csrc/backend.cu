@@ -183,6 +183,9 @@ uint64_t Ingestor::from_host(const IngestPlan& ip, const uint8_t* host_blob, uin
   uint64_t total = finish(p, buckets);
   if (st) {
     float ms = 0;
+    // t1_ sits on the copy stream after the last chunk's event; the compute
+    // stream waited for that event, not for t1_ itself
+    TRIMS_CUDA(cudaEventSynchronize(t1_));
     TRIMS_CUDA(cudaEventElapsedTime(&ms, t0_, t1_));
     st->h2d_ms = ms;
     TRIMS_CUDA(cudaEventElapsedTime(&ms, t0_, c1_));
@@ -235,6 +238,9 @@ uint64_t Ingestor::from_file(const IngestPlan& ip, int fd, uint64_t blob_file_of
   uint64_t total = finish(p, buckets);
   if (st) {
     float ms = 0;
+    // t1_ sits on the copy stream after the last chunk's event; the compute
+    // stream waited for that event, not for t1_ itself
+    TRIMS_CUDA(cudaEventSynchronize(t1_));
     TRIMS_CUDA(cudaEventElapsedTime(&ms, t0_, t1_));
     st->h2d_ms = ms;
     TRIMS_CUDA(cudaEventElapsedTime(&ms, t0_, c1_));
