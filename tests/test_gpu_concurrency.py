@@ -73,3 +73,58 @@ def test_concurrent_clients_under_pressure(tiny_dir, verify, eager):
         assert st["open_requests"] == counts["ok"] and counts["ok"] >= 120
         if eager:
             assert st["tiers"][0]["used_bytes"] == 0  # eager reclaim: nothing resident once closed
+
+
+def _blob_sha(cli, v):
+    import torch
+    from paper_1811_09732_b200.client import TensorView
+    n = v.blob_bytes()
+    t = torch.empty(n, dtype=torch.uint8)
+    t.copy_(TensorView("b", [n], "i8", "native", 0, n, v.base_ptr).torch("cuda:0").view(torch.uint8))
+    return F.sha256(t.numpy())
+
+
+def test_concurrent_converting_store(tiny_dir):
+    """The same under a converting plan (f64 -> bf16 at ingest), so host hits
+    reload the resident-form host copy (async D2H after each publish) while
+    other threads evict and publish: every view must equal a single-threaded
+    load of the same model."""
+    opts = dict(disk_cache_dir=tiny_dir, convert_to="bf16", scan_disk=False)
+    want = {}
+    with Store(StoreOptions(fast_capacity_bytes=64 * MB, host_capacity_bytes=64 * MB, **opts)) as s:
+        cli = Client(s)
+        for name in NAMES:
+            v = cli.open(F.ModelKey("zoo", name, "1.0.0"), force_shared=True)
+            want[name] = _blob_sha(cli, v)
+            cli.close(v)
+    errors = []
+    with Store(StoreOptions(fast_capacity_bytes=5 * MB, host_capacity_bytes=7 * MB, **opts)) as s:
+
+        def worker(wi):
+            rng = random.Random(wi)
+            cli = Client(s)
+            try:
+                for _ in range(30):
+                    name = rng.choice(NAMES)
+                    try:
+                        v = cli.open(F.ModelKey("zoo", name, "1.0.0"), force_shared=True)
+                    except TrimsError as e:
+                        if e.code == Errc.NoEvictableSpace:
+                            continue
+                        raise
+                    try:
+                        assert _blob_sha(cli, v) == want[name], name
+                    finally:
+                        cli.close(v)
+            except Exception as e:  # reported below
+                errors.append(repr(e))
+
+        ts = [threading.Thread(target=worker, args=(i,)) for i in range(6)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        assert not errors, errors[:3]
+        st = s.stats()
+        assert all(m["refcount"] == 0 for m in st["models"])
+        assert st["tiers"][1]["hits"] > 0 and st["tiers"][0]["evictions"] > 0
