@@ -120,3 +120,57 @@ def test_connection_drop_closes_handles(tiny_dir, tmp_path):
             assert all(m["refcount"] == 0 for m in s.stats()["models"])
             with pytest.raises(TrimsError):
                 RemoteStore(ep).close(key("vgg16"))
+
+
+def test_concurrent_connections_under_pressure(tiny_dir, tmp_path):
+    """8 connections at once (one daemon thread each) opening and closing
+    models while the fast tier evicts; half of them drop the connection with
+    handles still open. Afterwards every refcount is back to 0."""
+    import random
+    import threading
+    ep = str(tmp_path / "mrmd4.sock")
+    names = ["alexnet", "resnet50", "vgg16"]
+    errors = []
+    with Store(StoreOptions(disk_cache_dir=tiny_dir, fast_capacity_bytes=13 * MB, host_capacity_bytes=16 * MB)) as s:
+        with serve(s, ep) as srv:
+
+            def worker(wi):
+                rng = random.Random(wi)
+                try:
+                    rs = RemoteStore(ep)
+                    held = []
+                    for _ in range(40):
+                        k = key(rng.choice(names))
+                        if held and rng.random() < 0.5:
+                            rs.close(held.pop())
+                            continue
+                        try:
+                            ex = rs.open(k)
+                        except TrimsError as e:
+                            if e.code in (2, 3):  # TooLargeForFast / NoEvictableSpace: all pinned by others
+                                continue
+                            raise
+                        os.close(ex.fd)
+                        held.append(k)
+                    if wi % 2:
+                        for k in held:
+                            rs.close(k)
+                    rs.close_connection()  # odd workers closed everything; even ones drop with handles open
+                except Exception as e:  # reported below
+                    errors.append(repr(e))
+
+            ts = [threading.Thread(target=worker, args=(i,)) for i in range(8)]
+            for t in ts:
+                t.start()
+            for t in ts:
+                t.join()
+            assert not errors, errors[:3]
+            import time
+            for _ in range(200):
+                if all(m["refcount"] == 0 for m in s.stats()["models"]):
+                    break
+                time.sleep(0.02)
+            st = s.stats()
+            assert all(m["refcount"] == 0 for m in st["models"]), st["models"]
+            assert st["tiers"][0]["used_bytes"] <= 13 * MB
+            assert srv.frames_served() > 100
