@@ -43,6 +43,13 @@ const RingCfg& ring_cfg() {
     // per-tile fixed cost dominates below 32 KiB stages.
     RingCfg r{env("TRIMS_TMA_STAGE_KB", 64) << 10, env("TRIMS_TMA_STAGES", 3), env("TRIMS_TMA_CTAS", 1)};
     r.stages = std::max(2u, std::min<uint32_t>(r.stages, kMaxStages));
+    // the ring + the static descriptor batch (18 KiB) + barriers must fit the
+    // 227 KiB a CTA can opt into: an A/B setting that does not is refused here
+    // with a clear message rather than by cudaFuncSetAttribute
+    constexpr uint64_t kSmemCap = 227u << 10, kStatic = 20u << 10;
+    if (r.stage_bytes < (4u << 10) || uint64_t(r.stages) * r.stage_alloc() + kStatic > kSmemCap)
+      raise(Errc::InvalidArgument, "TRIMS_TMA_STAGES x TRIMS_TMA_STAGE_KB = " + std::to_string(r.stages) + " x " +
+                                       std::to_string(r.stage_bytes >> 10) + " KiB does not fit shared memory");
     return r;
   }();
   return c;
