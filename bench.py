@@ -112,6 +112,9 @@ def dist_setup(n_gpus: int):
             local = 0
             dist.init_process_group("gloo")
         else:
+            if torch.cuda.device_count() < world:
+                raise SystemExit(f"bench.py --gpus {world}: only {torch.cuda.device_count()} GPU(s) visible "
+                                 "(TRIMS_BENCH_SHARED_GPU=1 runs the N>1 code path on one GPU)")
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     return world, rank, local
@@ -131,6 +134,15 @@ def barrier(world: int):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
+
+
+def bench_config(artifact_bytes: int, tensors: int) -> dict:
+    """The workload both arms run (identical dict in both JSON lines)."""
+    return {"workload": WORKLOAD, "artifact_bytes": artifact_bytes, "tensors": tensors,
+            "l2": "value leg not flushed: inputs larger than L2 (rotating src/dst buffer sets, >= 3 x L2 of "
+                  "traffic between reuses); e2e leg: 256 MiB write + 256 MiB read flush before every step",
+            "models": ["resnet50", "alexnet", "vgg16", "vgg19", "small37 seed 1", "large8 vgg16-s4"],
+            "parallelism": "one store shard per GPU, one process per GPU, no collective"}
 
 
 def make_artifact(workdir: str):
@@ -303,12 +315,10 @@ def run_ours(args):
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8/fp32->bf16", "data": "synthetic (seeded uniform init)",
-        "config": {"workload": WORKLOAD, "artifact_bytes": src_bytes, "resident_bytes": res_bytes,
-                   "tensors": len(rb["tensors"]),
-                   "l2": f"not flushed; inputs larger than L2: {R} rotating src/dst buffer sets "
-                         f"({R} x {(src_bytes + res_bytes) / 1e6:.1f} MB >= 4 x L2), each step's buffers last touched "
-                         f"{R - 1} steps earlier; launches back to back",
-                   "parallelism": f"store shard per GPU x{world}"},
+        "config": bench_config(src_bytes, len(rb["tensors"])),
+        "timing": {"resident_bytes": res_bytes, "rotating_buffer_sets": R,
+                   "l2": f"{R} x {(src_bytes + res_bytes) / 1e6:.1f} MB src/dst sets, each step's buffers last "
+                         f"touched {R - 1} steps earlier; launches back to back"},
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": src_bytes,
                 "d2h_bytes_per_step": info["buckets"] * 8, "ms_per_step": round(e2e_max / args.steps, 4),
                 "h2d_gbs_copy_engine": round(h2d_gbs, 2) if h2d_gbs else None},
@@ -345,6 +355,11 @@ def run_ours(args):
         line["e2e"]["warm_reload_pcie_bytes"] = int(bd.get("h2d_bytes", 0))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(src_json, blob, res_json)
+    # compact request-latency summary (ms), last so it survives a truncated tail
+    line["latency_summary_ms"] = {
+        n: {k: (r[k]["e2e"] if isinstance(r.get(k), dict) else r.get(k))
+            for k in ("private", "cold", "warm", "hot", "compute_only", "forward_device_ms")}
+        for n, r in lat.items()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -395,7 +410,11 @@ def peer_serve(work: str, arch, dev: int, rank: int, world: int, steps: int) -> 
         stats = s.stats()
         barrier(world)
     med = statistics.median(gbs) if gbs else 0.0
-    return {"pull_GBps_median": round(med, 1), "pull_GBps_min_over_ranks": round(-barrier_max(-med, world), 1),
+    nvlink = 900.0  # NVLink 5, GB/s per direction per GPU (every rank pulls from one peer at once)
+    lo = -barrier_max(-med, world)
+    return {"pull_GBps_median": round(med, 1), "pull_GBps_min_over_ranks": round(lo, 1),
+            "nvlink_GBps_per_direction": nvlink,
+            "nvlink_frac": None if SHARED_GPU else round(lo / nvlink, 4),
             "open_ms_median": round(statistics.median(open_ms), 3) if open_ms else None,
             "resident_bytes": int(ex.resident_blob_bytes), "outcomes": sorted(set(outcomes)),
             "peer_hits": stats["peer_hits"], "peer_fallbacks": stats["peer_fallbacks"],
@@ -536,21 +555,24 @@ def request_latencies(work: str, arch, dev: int, batch: int = 1, reps: int = 7) 
     logits = None
     stream = torch.cuda.current_stream(dev)
     nets = {}
+    private = False
 
     def request(cli, phases):
         nonlocal logits
         t0 = time.perf_counter()
-        v = cli.open(key, force_shared=True)
+        v = cli.open(key, force_shared=not private, force_private=private)
         t1 = time.perf_counter()
         # A serving client keeps its executor; a new weights generation (after
-        # eviction + reload) only rebinds the weight-dependent state.
+        # eviction + reload, or a fresh private copy) only rebinds the
+        # weight-dependent state.
+        ident = (id(cli), v.generation, v.base_ptr)
         net = nets.get("net")
         if net is None:
             net = nets["net"] = BoundNet(v, arch, batch, dev)
-            nets["gen"] = (id(cli), v.generation)
-        elif nets["gen"] != (id(cli), v.generation):
+            nets["gen"] = ident
+        elif nets["gen"] != ident:
             net.rebind(v)
-            nets["gen"] = (id(cli), v.generation)
+            nets["gen"] = ident
         t2 = time.perf_counter()
         if logits is None:
             logits = torch.empty(batch, net.classes).pin_memory()
@@ -567,6 +589,18 @@ def request_latencies(work: str, arch, dev: int, batch: int = 1, reps: int = 7) 
                 "h2d_forward_d2h": round(med[3], 4)}
 
     out = {"model": arch.name, "batch": batch}
+    # private: no store (the reference's nodaemon baseline, client.cpp:224-241,
+    # harness.cpp:376-399): every request reads the artifact and ingests it into
+    # its own HBM with the same plan, binds, infers and frees it.
+    from paper_1811_09732_b200 import format as F
+    private = True
+    cli = Client(None, model_dirs=[work], device=dev, plan_flags=F.PLAN_CONVERT | F.PLAN_PERMUTE_4D,
+                 out_dtype="bf16")
+    ph = []
+    for _ in range(reps):
+        request(cli, ph)
+    out["private"] = summary(ph)
+    private = False
     with Store(StoreOptions(eager_reclaim=True, **base)) as s:  # cold: every open is a disk load
         cli = Client(s)
         ph = []
@@ -733,7 +767,106 @@ def cpu_baseline(src_json, blob, res_json) -> dict:
                       f"(convert+permute, numpy glue), {dt:.2f} s", **host_info()}
 
 
+def _standalone(mod: str):
+    """paper_1811_09732_b200/<mod>.py loaded on its own (pure Python), so the
+    reference arm describes the same models without importing the package
+    (which would load libtrims.so into the reference process)."""
+    import importlib.util
+    name = f"trims_{mod}"
+    if name in sys.modules:
+        return sys.modules[name]
+    spec = importlib.util.spec_from_file_location(name, os.path.join(ROOT, "paper_1811_09732_b200", f"{mod}.py"))
+    m = importlib.util.module_from_spec(spec)
+    sys.modules[name] = m
+    spec.loader.exec_module(m)
+    return m
+
+
+def _archs():
+    return _standalone("archs")
+
+
+def ref_write_arch(R, P, arch, out_dir: str, seed: int = 1) -> tuple:
+    """The real-shape fp32 artifact of ``arch`` written by the REFERENCE's own
+    writer (model::write_model_file, model_format.cpp:293-305) from the oracle
+    port's uniform generator: byte-identical to catalog.write_arch
+    (tests/test_bench_reference.py), with no product code in the process."""
+    import numpy as np
+    A = _archs()
+    key = A.arch_key_tuple(arch)
+    decls, parts = [], []
+    for name, dims, (lo, hi) in A.arch_tensors(arch):
+        decls.append((name, "f32", dims))
+        stream = (seed ^ P.fnv1a(f"{arch.name}/{name}")) & 0xFFFFFFFFFFFFFFFF
+        parts.append(P.uniform_f32(stream, 0, int(np.prod(dims)), float(np.float32(lo)), float(np.float32(hi))))
+    path = os.path.join(out_dir, f"{key[0]}__{key[1]}__{key[2]}.trms")
+    os.makedirs(out_dir, exist_ok=True)
+    R.write_model(path, key, decls, 0, np.concatenate(parts).tobytes())
+    return key, path
+
+
+def zipf_trace(seed: int, n: int, n_models: int, s: float = 1.1) -> list:
+    """workload.zipf_trace restated for the reference arm (asserted equal in tests/test_bench_reference.py)."""
+    import numpy as np
+    w = 1.0 / np.arange(1, n_models + 1, dtype=np.float64) ** s
+    return [int(i) for i in np.random.default_rng(seed).choice(n_models, size=n, p=w / w.sum())]
+
+
+def nearest_rank(xs, p: float) -> float:
+    """stats_math.cpp:19-27."""
+    import math
+    v = sorted(xs)
+    return v[max(1, int(math.ceil(p / 100.0 * len(v)))) - 1]
+
+
+def ref_catalog(R) -> tuple:
+    """small37 seed 1 written by the reference's own gen_catalog (catalog.cpp:130-159)."""
+    import json as _json
+    names = [row[0] for row in _standalone("catalog_tables").SMALL37]
+    total = 0
+    for n in names:
+        m = _json.loads(R.catalog_manifest_json("small37", n))
+        total += sum(t["nbytes"] for t in m["tensors"])
+    have = set(os.listdir(CATALOG_DIR)) if os.path.isdir(CATALOG_DIR) else set()
+    if not {f"zoo__{n}__1.0.0.trms" for n in names} <= have:
+        R.gen_catalog("small37", CATALOG_DIR, 1, None)
+    return CATALOG_DIR, names, total
+
+
+def ref_workers(R, work: str, key: tuple, n_workers: int, n_reqs: int) -> dict:
+    """BASELINE configs[1] on the reference: one reference daemon (in this
+    process) and ``n_workers`` spawned worker processes, each running the
+    harness worker loop (open force-shared -> touch -> close,
+    harness.cpp:275-349) on the same model: one shared copy, 16 clients."""
+    import json as _json
+    import subprocess as sp
+    blob = os.path.getsize(os.path.join(work, f"{key[0]}__{key[1]}__{key[2]}.trms"))
+    h, ep = R.daemon_start(work, 4 * blob, 4 * blob, 64 * blob)
+    code = ("import json,sys,time; sys.path.insert(0, %r); import oracle; R = oracle.ref(); "
+            "a = json.loads(sys.argv[1]); t0 = time.time(); "
+            "lat, t = R.worker(a['ep'], a['dir'], tuple(a['key']), a['n'], 1); "
+            "print(json.dumps({'lat': lat, 't0': t0, 't1': time.time(), 'touch': t}))") % ROOT
+    arg = _json.dumps({"ep": ep, "dir": work, "key": list(key), "n": n_reqs})
+    try:
+        procs = [sp.Popen([sys.executable, "-c", code, arg], stdout=sp.PIPE, text=True) for _ in range(n_workers)]
+        res = [_json.loads(p.communicate(timeout=900)[0]) for p in procs]
+    finally:
+        st = R.daemon_stop(h)
+    lat = sorted(x * 1e3 for r in res for x in r["lat"])
+    window = max(r["t1"] for r in res) - min(r["t0"] for r in res)
+    return {"clients": n_workers, "requests": len(lat), "p50_ms": round(nearest_rank(lat, 50), 3),
+            "p99_ms": round(nearest_rank(lat, 99), 3), "requests_per_s": round(len(lat) / window, 1),
+            "identical_touch_across_clients": len({r["touch"] for r in res}) == 1,
+            "disk_reads": st["disk_reads"], "fast_used_bytes": st["fast_used_bytes"],
+            "request": "open(force_shared) -> touch (FNV over every weight byte, the reference's compute) -> close",
+            "model": key[1]}
+
+
 def run_reference(args):
+    """The reference's own CPU path (oracle/_ref/libmrm_ref.so, the UNMODIFIED
+    reference compiled from /root/reference) on the same workloads. Only
+    oracle/_ref is loaded in this process: inputs are written by the
+    reference's writer / gen_catalog; nothing from the product package."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -742,72 +875,106 @@ def run_reference(args):
     if not oracle.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmrm_ref.so not built"}))
         return
-    R = oracle.ref()
+    import statistics
+    import threading as _th
+    R, P, A = oracle.ref(), oracle.port(), _archs()
     work = tempfile.mkdtemp(prefix="trims-ref-")
-    arch, path, src_json, blob = make_artifact(work)
+    arches = {n: A.ARCHS[n]() for n in ("resnet50", "alexnet", "vgg16", "vgg19")}
+    paths = {n: ref_write_arch(R, P, a, work) for n, a in arches.items()}
+    path = paths["resnet50"][1]
+    blob_bytes = R.read_manifest(path)[3]
+    n_tensors = len(A.arch_tensors(arches["resnet50"]))
+
+    # ---- value: publish_fast(from_host), the reference's ingest step
     for _ in range(args.warmup):
         R.ingest(path, 1)
-    t = []
-    for _ in range(args.steps):
-        r = R.ingest(path, 1)
-        t.append(r["publish_s"])
-    total = sum(t)
-    value_1 = args.steps * blob.size / total / 1e9
-    # all the host threads it can use: the daemon publishes concurrently for
-    # distinct models (one thread per connection); aggregate over T callers
-    cores = 1
-    value = value_1
+    t = [R.ingest(path, 1)["publish_s"] for _ in range(args.steps)]
+    value_1 = args.steps * blob_bytes / sum(t) / 1e9
+    cores, value = 1, value_1
     threads = min(os.cpu_count() or 1, 16)
-    while threads > 1:
+    while threads > 1:  # all the host threads it can use: concurrent publishes of distinct model ids
         agg, used = R.ingest_parallel(path, threads, max(1, min(args.steps, 5)))
         if agg:
             if agg > value:
                 value, cores = agg, used
             break
         threads //= 2  # e.g. /dev/shm too small for that many segments
+
+    # ---- run_latency {nodaemon, cold, host, warm}, reps = 5 (harness.cpp:99-188)
     lat = {}
-    from paper_1811_09732_b200 import catalog as C
-    key = C.arch_key(arch)
-    for mode in ("cold", "host", "warm"):
-        r = R.latency(work, (key.ns, key.name, key.version), mode, 3)
-        lat[f"{mode}_open"] = round(r["open_s"] * 1e3, 3)
-        lat[f"{mode}_e2e_with_touch"] = round(r["end_to_end_s"] * 1e3, 3)
+    mode_names = {"nodaemon": "private", "cold": "cold", "host": "warm", "warm": "hot"}
+    for n, (key, _) in paths.items():
+        row = {}
+        for mode, ours in mode_names.items():
+            r = R.latency(work, key, mode, 5)
+            row[ours] = round(r["end_to_end_s"] * 1e3, 3)
+            row[f"{ours}_open"] = round(r["open_s"] * 1e3, 3)
+        row["compute_touch"] = round(r["compute_s"] * 1e3, 3)
+        lat[n] = row
+
+    shared = None if args.quick else ref_workers(R, work, paths["resnet50"][0], 16, max(5, args.steps))
     traces = None if args.quick else reference_traces(R)
+    summary = {n: {k: v for k, v in row.items() if k in ("private", "cold", "warm", "hot")} for n, row in lat.items()}
+    config = bench_config(blob_bytes, n_tensors)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3),
+        "steps": args.steps, "warmup": args.warmup,
+        # the value's own step: one artifact published at the aggregate rate
+        "ms_per_step": round(blob_bytes / (value * 1e9) * 1e3, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8 (verbatim bytes)",
-        "data": "synthetic (seeded uniform init)",
-        "config": {"workload": WORKLOAD, "artifact_bytes": blob.size,
-                   "reference_step": "ShmTierBackend::publish_fast(from_host) host vector -> sealed shm segment "
-                                     "(daemon.cpp:160-209); the reference does no dtype/layout conversion"},
+        "data": "synthetic (seeded uniform init)", "config": config,
+        "reference_step": "ShmTierBackend::publish_fast(from_host): host vector -> sealed shm segment "
+                          "(daemon.cpp:160-209); the reference does no dtype/layout conversion",
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
-                         "sample": f"{args.steps} single-thread publish_fast calls ({value_1:.3f} GB/s) and "
-                                   f"rounds of {cores} concurrent publishes of the {blob.size} B ResNet-50 blob",
-                         **host_info()},
+                         "sample": f"{args.steps} single-thread publish_fast calls ({value_1:.3f} GB/s, "
+                                   f"{statistics.median(t) * 1e3:.2f} ms median) and rounds of {cores} concurrent "
+                                   f"publishes of the {blob_bytes} B ResNet-50 blob (value = the {cores}-thread "
+                                   f"aggregate)", **host_info()},
+        "value_single_thread": round(value_1, 4),
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "latency_ms": lat,
+        "latency_note": "run_latency medians of 5 reps (harness.cpp:137-180): private = nodaemon, cold = disk "
+                        "load every open, warm = host-tier hit ('host'), hot = fast-tier hit ('warm'); compute = "
+                        "touch (FNV over every weight byte) on one core",
     }
+    if shared:
+        line["shared_clients"] = shared
     if traces:
         line["traces"] = traces
+    line["latency_summary_ms"] = summary
     print(json.dumps(line), flush=True)
+    import shutil
+    shutil.rmtree(work, ignore_errors=True)
 
 
-def reference_traces(R, n: int = 150) -> dict:
+def reference_traces(R, n: int = 1000) -> dict:
     """configs[2]/[4] through the UNMODIFIED reference daemon + client
     (oracle ref_trace: open force-shared -> touch -> close), same catalog,
-    capacities and request streams as ours; a bounded sample (the first `n`
-    requests) because every request touches the weights on one CPU core."""
-    from paper_1811_09732_b200 import workload as W
-    cat, keys, total = small37_catalog(0, 1)
-    names = [k.name for k in keys]
-    out = {"catalog": "small37 seed 1", "fast_capacity": total // 2, "sample_requests": n}
-    for tname, tr in (("pareto_reference_stream", W.pareto_trace(42, 1000, len(keys))[:n]),
-                      ("faas_zipf_s1.1", W.zipf_trace(42, 1000, len(keys), 1.1)[:n])):
-        lat, st = R.trace(cat, names, tr, max(total // 2, 1 << 20), total + (1 << 20), total * 8 + (64 << 20))
+    capacities and request streams as ours, all 1000 requests. The two traces
+    run at once in two processes (one reference daemon each: two daemons in
+    one process would collide on the shm segment names mrm.<pid>.<seq>)."""
+    import json as _json
+    import subprocess as sp
+    cat, names, total = ref_catalog(R)
+    out = {"catalog": "small37 seed 1", "fast_capacity": total // 2, "requests": n}
+    streams = {"pareto_reference_stream": R.pareto_trace(42, n, 1.0, 1.0, len(names)),
+               "faas_zipf_s1.1": zipf_trace(42, n, len(names), 1.1)}
+    code = ("import json,sys; sys.path.insert(0, %r); import oracle; a = json.loads(sys.stdin.read()); "
+            "print(json.dumps(oracle.ref().trace(*a)))") % ROOT
+    procs = {}
+    for tname, tr in streams.items():
+        p = sp.Popen([sys.executable, "-c", code], stdin=sp.PIPE, stdout=sp.PIPE, text=True)
+        p.stdin.write(_json.dumps([cat, names, tr, max(total // 2, 1 << 20), total + (1 << 20),
+                                   total * 8 + (64 << 20)]))
+        p.stdin.close()
+        procs[tname] = p
+    for tname, p in procs.items():
+        lat, st = _json.loads(p.stdout.read())
+        if p.wait() != 0:
+            raise RuntimeError(f"reference trace {tname} failed")
         acc = st["fast_hits"] + st["fast_misses"]
         out[tname] = {"requests": n, "fast_hit_rate": round(st["fast_hits"] / max(1, acc), 4),
-                      "p50_ms": round(W.percentile(lat, 50) * 1e3, 3), "p99_ms": round(W.percentile(lat, 99) * 1e3, 3),
+                      "p50_ms": round(nearest_rank(lat, 50) * 1e3, 3), "p99_ms": round(nearest_rank(lat, 99) * 1e3, 3),
                       "mean_ms": round(sum(lat) / len(lat) * 1e3, 3), "evictions": st["fast_evictions"]}
     return out
 
@@ -822,6 +989,16 @@ def main():
     ap.add_argument("--quick", action="store_true", help="ResNet-50 latencies only")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # A plain `python bench.py --gpus N`: launch the N ranks ourselves, one
+        # process per GPU, exactly as the driver's torchrun command would.
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        os.execv(sys.executable, cmd)
     if args.impl == "reference":
         run_reference(args)
     else:

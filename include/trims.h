@@ -318,6 +318,12 @@ int trims_net_info(trims_net* net, double out3[3]);
  * -> device, forward, logits (fp32 batch x classes) -> host, synchronised.
  * Pinned host buffers give the full PCIe rate. */
 int trims_net_forward_host(trims_net* net, const float* host_input, float* host_logits, void* stream, int use_graph);
+/* Parity tap: the device buffer architecture layer `layer` (0-based, the
+ * input line excluded) wrote in the last forward, NHWC dims4 = {n, h, w, c},
+ * dtype 0 = bf16, 1 = fp32 (the logits). layer < 0 returns the layer count.
+ * No reference counterpart (the reference has no inference math); it lets the
+ * tests check every layer against the CPU oracle on the device's own inputs. */
+int trims_net_tap(trims_net* net, int layer, const void** ptr, int dims4[4], int* dtype);
 /* row softmax of fp32 logits [M, N] (device pointers) */
 int trims_softmax(const float* in, float* out, int M, int N, void* stream);
 

@@ -174,6 +174,12 @@ class _Ref:
         L.ref_wire_encode_text.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_uint64, _u64p]
         L.ref_wire_decode_text.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_uint64]
         L.ref_wire_request.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_uint64]
+        L.ref_daemon_start.restype = ctypes.c_void_p
+        L.ref_daemon_start.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+                                       ctypes.c_char_p, ctypes.c_uint64]
+        L.ref_daemon_stop.argtypes = [ctypes.c_void_p, _u64p]
+        L.ref_worker.argtypes = [ctypes.c_char_p] * 5 + [ctypes.c_uint32, ctypes.c_uint32,
+                                                         ctypes.POINTER(ctypes.c_double), _u64p]
         self.L = L
 
     # wire_protocol.cpp:319-357 through the shim's text form; (rc, value)
@@ -294,6 +300,28 @@ class _Ref:
                     "trace")
         return list(out), dict(zip(("fast_hits", "fast_misses", "fast_evictions", "open_errors", "disk_reads"),
                                    list(st)))
+
+    def daemon_start(self, dir: str, fast: int, host: int, disk: int, eager: bool = False) -> tuple:
+        """A reference daemon inside this process: (handle, socket path)."""
+        buf = ctypes.create_string_buffer(4096)
+        h = self.L.ref_daemon_start(dir.encode(), fast, host, disk, int(eager), buf, len(buf))
+        if not h:
+            raise RuntimeError("ref_daemon_start failed")
+        return h, buf.value.decode()
+
+    def daemon_stop(self, h) -> dict:
+        st = (ctypes.c_uint64 * 6)()
+        self._check(self.L.ref_daemon_stop(h, st), "daemon_stop")
+        return dict(zip(("fast_hits", "fast_misses", "fast_evictions", "open_errors", "disk_reads",
+                         "fast_used_bytes"), list(st)))
+
+    def worker(self, endpoint: str, dir: str, key, n: int, warmup: int = 1):
+        """bench::run_worker's loop on one key: per-request open+touch seconds, last touch."""
+        out = (ctypes.c_double * max(n, 1))()
+        t = ctypes.c_uint64()
+        self._check(self.L.ref_worker(endpoint.encode(), dir.encode(), *(k.encode() for k in key), n, warmup, out,
+                                      ctypes.byref(t)), "worker")
+        return list(out)[:n], t.value
 
 
 _port = None

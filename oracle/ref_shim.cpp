@@ -10,6 +10,7 @@
 // Each entry point names the reference API it drives.
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <random>
@@ -38,6 +39,14 @@ using namespace mrm;
 namespace fs = std::filesystem;
 
 namespace {
+
+// Unique daemon socket per call (several reference daemons may run at once in
+// one process: the bench's reference arm replays two traces concurrently).
+std::string sock_path(const char* tag) {
+  static std::atomic<uint64_t> seq{0};
+  return "/tmp/mrm-refshim-" + std::string(tag) + "-" + std::to_string(::getpid()) + "-" +
+         std::to_string(seq.fetch_add(1)) + ".sock";
+}
 
 int put_text(const std::string& s, char* out, uint64_t cap) {
   if (!out || cap == 0) return -1;
@@ -605,7 +614,7 @@ int ref_latency(const char* dir, const char* ns, const char* name, const char* v
     std::unique_ptr<daemon::Daemon> dmn;
     if (mode != "nodaemon") {
       daemon::DaemonConfig cfg;
-      cfg.listen_path = "/tmp/mrm-refshim-" + std::to_string(::getpid()) + ".sock";
+      cfg.listen_path = sock_path("lat");
       cfg.disk_cache_dir = dir;
       cfg.startup_calibration = false;
       cfg.workspace_headroom_fraction = 1.0;
@@ -701,7 +710,7 @@ int ref_trace(const char* dir, const char* names_c, const uint32_t* trace, uint3
     std::string nm;
     while (is >> nm) keys.push_back({"zoo", nm, "1.0.0"});
     daemon::DaemonConfig cfg;
-    cfg.listen_path = "/tmp/mrm-refshim-trace-" + std::to_string(::getpid()) + ".sock";
+    cfg.listen_path = sock_path("trace");
     cfg.disk_cache_dir = dir;
     cfg.startup_calibration = false;
     cfg.workspace_headroom_fraction = 1.0;
@@ -732,6 +741,79 @@ int ref_trace(const char* dir, const char* names_c, const uint32_t* trace, uint3
     stats[4] = st.disk_reads;
     dmn.request_stop();
     dmn.join();
+    return 0;
+  });
+}
+
+// A reference daemon (daemon::Daemon, daemon.cpp:398-601) running inside this
+// process for external worker processes (ref_worker): the harness's
+// run_workers setup (harness.cpp:275-349) without its CLI11 executable.
+// Returns an opaque handle; the socket path is written to endpoint_out.
+void* ref_daemon_start(const char* dir, uint64_t fast_cap, uint64_t host_cap, uint64_t disk_cap, int eager,
+                       char* endpoint_out, uint64_t cap) {
+  try {
+    daemon::DaemonConfig cfg;
+    cfg.listen_path = sock_path("srv");
+    cfg.disk_cache_dir = dir;
+    cfg.startup_calibration = false;
+    cfg.workspace_headroom_fraction = 1.0;
+    cfg.fast_capacity_bytes = fast_cap;
+    cfg.host_capacity_bytes = host_cap;
+    cfg.disk_capacity_bytes = disk_cap;
+    cfg.eager_reclaim = eager != 0;
+    auto d = std::make_unique<daemon::Daemon>(cfg);
+    d->start();
+    if (put_text(cfg.listen_path, endpoint_out, cap) != 0) return nullptr;
+    return d.release();
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "ref_shim: %s\n", e.what());
+    return nullptr;
+  }
+}
+
+// Stops the daemon; stats: fast hits, fast misses, fast evictions,
+// open_errors, disk_reads, fast used bytes.
+int ref_daemon_stop(void* h, uint64_t* stats) {
+  return guarded([&] {
+    std::unique_ptr<daemon::Daemon> d(static_cast<daemon::Daemon*>(h));
+    cache::StatsSnapshot st = d->stats();
+    if (stats) {
+      stats[0] = st.tiers[0].hits;
+      stats[1] = st.tiers[0].misses;
+      stats[2] = st.tiers[0].evictions;
+      stats[3] = st.open_errors;
+      stats[4] = st.disk_reads;
+      stats[5] = st.tiers[0].used_bytes;
+    }
+    d->request_stop();
+    d->join();
+    return 0;
+  });
+}
+
+// The reference worker's request loop (bench::run_worker, harness.cpp:297-322)
+// for one model key: open(force_shared) -> touch -> close, `warmup` untimed
+// then `n` timed requests. out_s[i] = open + touch seconds (the harness's
+// total_ns); touch_out = the last touch value.
+int ref_worker(const char* endpoint, const char* dir, const char* ns, const char* name, const char* version,
+               uint32_t n, uint32_t warmup, double* out_s, uint64_t* touch_out) {
+  return guarded([&] {
+    client::ClientConfig cc;
+    cc.endpoint = endpoint;
+    cc.model_dirs = {dir};
+    client::Client cli(cc);
+    client::OpenOptions opts;
+    opts.force_shared = true;
+    model::ModelKey key{ns, name, version};
+    for (uint32_t i = 0; i < warmup + n; ++i) {
+      auto t0 = std::chrono::steady_clock::now();
+      client::ModelView v = cli.open(key, opts);
+      const uint64_t t = cli.touch(v);
+      auto t1 = std::chrono::steady_clock::now();
+      cli.close(v);
+      if (touch_out) *touch_out = t;
+      if (i >= warmup) out_s[i - warmup] = std::chrono::duration<double>(t1 - t0).count();
+    }
     return 0;
   });
 }

@@ -1083,6 +1083,23 @@ int trims_net_info(trims_net* net, double out3[3]) {
   });
 }
 
+int trims_net_tap(trims_net* net, int layer, const void** ptr, int dims4[4], int* dtype) {
+  return guard([&] {
+    if (!net) raise(Errc::InvalidArgument, "null net");
+    if (layer < 0) return net->net->layers();
+    const auto& t = net->net->tap(layer);
+    if (ptr) *ptr = t.p;
+    if (dims4) {
+      dims4[0] = t.n;
+      dims4[1] = t.h;
+      dims4[2] = t.w;
+      dims4[3] = t.c;
+    }
+    if (dtype) *dtype = t.dtype;
+    return 0;
+  });
+}
+
 int trims_softmax(const float* in, float* out, int M, int N, void* stream) {
   return guard([&] {
     nn::softmax(in, out, M, N, static_cast<cudaStream_t>(stream));

@@ -193,6 +193,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
   for (size_t li = 0; li < layers.size(); ++li) {
     const LayerSpec& l = layers[li];
     const size_t first_step = steps_.size();
+    Act produced;  // this layer's output buffer (the parity tap)
     std::vector<int> joins;
     for (const char* ref : {"src", "res"}) {
       auto it = branch_of.find(l.s(ref));
@@ -307,6 +308,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
         first_group = false;
       }
       flops_ += 2.0 * double(M) * cout * rsc;
+      produced = out;
       if (branch) branch_of[l.s("out")] = nbranches_++;
       if (!l.s("out").empty()) named[l.s("out")] = out;
       if (!branch) cur = out;
@@ -388,6 +390,11 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       raise(Errc::InvalidArgument, "unknown layer kind " + l.kind);
     }
     attach_joins();
+    if (l.kind != "input") {
+      if (l.kind == "fc" && int(li) == last_fc) taps_.push_back({logits_, batch, 1, 1, classes_, 1});
+      else if (l.kind == "conv") taps_.push_back({produced.p, produced.n, produced.h, produced.w, produced.c, 0});
+      else taps_.push_back({cur.p, cur.n, cur.h, cur.w, cur.c, 0});
+    }
   }
   if (!branch_of.empty()) raise(Errc::InvalidArgument, "a branch output is never consumed");
   if (!logits_) raise(Errc::InvalidArgument, "architecture has no fc output");
@@ -414,6 +421,11 @@ Net::~Net() {
   for (auto* v : {&fork_ev_, &join_ev_})
     for (auto e : *v) cudaEventDestroy(e);
   for (void* p : owned_) cudaFree(p);
+}
+
+const Net::Tap& Net::tap(int i) const {
+  if (i < 0 || i >= int(taps_.size())) raise(Errc::InvalidArgument, "no such layer " + std::to_string(i));
+  return taps_[size_t(i)];
 }
 
 void Net::rebind(const uint8_t* weights) {

@@ -63,6 +63,16 @@ class Net {
   // Point the executor at another generation of the same resident model
   // (identical manifest, new segment): recomputes weight-dependent state only.
   void rebind(const uint8_t* weights);
+  // Output buffer of architecture layer `i` (0-based, the input line excluded)
+  // as written by the last forward: NHWC [n, h, w, c]; dtype 0 = bf16, 1 = fp32
+  // (the logits). Every layer owns its output buffer, so all taps of one
+  // forward stay readable until the next one. For parity tests.
+  struct Tap {
+    const void* p{nullptr};
+    int n{0}, h{0}, w{0}, c{0}, dtype{0};
+  };
+  const Tap& tap(int i) const;
+  int layers() const { return int(taps_.size()); }
   double flops() const { return flops_; }
   uint32_t launches() const { return launches_; }
   uint64_t workspace_bytes() const { return ws_bytes_; }
@@ -76,6 +86,7 @@ class Net {
   const uint8_t* wbase_{nullptr};  // current weights generation (resident blob base)
   int in_hw_{224}, in_c_{3}, classes_{1000};
   std::vector<std::unique_ptr<Step>> steps_;
+  std::vector<Tap> taps_;
   std::vector<void*> owned_;
   float* input_{nullptr};
   float* logits_{nullptr};

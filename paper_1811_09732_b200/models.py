@@ -67,6 +67,23 @@ class BoundNet:
         return TensorView("logits", [self.batch, self.classes], "f32", "native", 0, self.batch * self.classes * 4,
                           self.logits_ptr).torch(f"cuda:{self.device}")
 
+    def layer_count(self) -> int:
+        return int(lib.trims_net_tap(self._h, -1, None, None, None))
+
+    def tap(self, layer: int):
+        """Device view of what architecture layer `layer` wrote in the last forward
+        (NCHW-permuted torch view of the NHWC buffer; bf16, or fp32 logits)."""
+        import torch
+        from .client import TensorView
+        p, dims, dt = ctypes.c_void_p(), (ctypes.c_int * 4)(), ctypes.c_int()
+        check(lib.trims_net_tap(self._h, layer, ctypes.byref(p), dims, ctypes.byref(dt)))
+        n, h, w, c = dims
+        es = 4 if dt.value else 2
+        t = TensorView(f"layer{layer}", [n * h * w * c * es], "i8", "native", 0, n * h * w * c * es,
+                       int(p.value)).torch(f"cuda:{self.device}").view(torch.uint8)
+        t = t.view(torch.float32 if dt.value else torch.bfloat16).view(n, h, w, c)
+        return t.permute(0, 3, 1, 2)
+
     def rebind(self, view) -> None:
         """Follow the model to a new segment (same resident manifest, new generation)."""
         if view.manifest_json != self.view.manifest_json:
@@ -83,6 +100,17 @@ class BoundNet:
         stream sync. x: fp32 NCHW host tensor/array (pinned for full PCIe
         rate); out: a host [batch, classes] fp32 buffer (allocated if None)."""
         import numpy as np
+        for a, what in ((x, "x"), (out, "out")):
+            if a is None:
+                continue
+            dt = str(getattr(a, "dtype", ""))
+            if dt not in ("float32", "torch.float32"):
+                raise ValueError(f"{what} must be float32, got {dt}")
+            contig = a.is_contiguous() if hasattr(a, "is_contiguous") else a.flags["C_CONTIGUOUS"]
+            if not contig:
+                raise ValueError(f"{what} must be contiguous")
+            if hasattr(a, "device") and getattr(a.device, "type", "cpu") != "cpu":
+                raise ValueError(f"{what} must be a host buffer")
         if out is None:
             out = np.empty((self.batch, self.classes), np.float32)
         xp = x.data_ptr() if hasattr(x, "data_ptr") else x.ctypes.data

@@ -51,8 +51,11 @@ def test_identity_ingest_catalog_bytes_and_checksum(torch):
         assert F.touch_host(out, res_json) == e["touch"]              # == the reference's own touch
 
 
-@pytest.mark.parametrize("arch", ["alexnet", "resnet50"])
+@pytest.mark.parametrize("arch", ["alexnet", "resnet50", "vgg16", "vgg19"])
 def test_convert_permute_bit_exact(torch, arch):
+    """Every real-shape net the bench reports, fp32 KCRS -> bf16 KRSC. VGG's
+    411 MB fc6 and its 512-channel k-slices take different tile paths from
+    ResNet-50's (elementwise chunks vs whole k-slices vs the direct kernel)."""
     a = C.ARCHS[arch]()
     src_json, blob = C.arch_blob(a, seed=1)
     flags = F.PLAN_CONVERT | F.PLAN_PERMUTE_4D
