@@ -110,6 +110,9 @@ typedef struct trims_store_config {
   int32_t world;                 /* stores on the node */
   uint32_t directory_slots;      /* per-rank slots (0 = 1024) */
   const char* remote_url;        /* daemon.hpp:26: http://... or dir:<path>; NULL = no remote tier */
+  double workspace_headroom_fraction; /* daemon.hpp:29 (in [0, 1]; published in stats for the client's
+                                         workspace-reservation fallback, client.cpp:192-204) */
+  uint32_t startup_calibration;  /* daemon.hpp:33: measure q/o/s at creation (daemon.cpp:342-390) */
 } trims_store_config;
 
 /* Reference outcomes (cache_core.hpp:36) + PEER_HIT for the multi-GPU directory. */

@@ -174,6 +174,9 @@ class _Ref:
         L.ref_wire_encode_text.argtypes = [ctypes.c_char_p, ctypes.c_void_p, ctypes.c_uint64, _u64p]
         L.ref_wire_decode_text.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_uint64]
         L.ref_wire_request.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_uint64]
+        L.ref_client_decision.argtypes = [ctypes.c_char_p] * 4 + [ctypes.c_int, ctypes.c_uint64, ctypes.c_int] + \
+            [ctypes.c_double] * 3 + [ctypes.c_uint64, ctypes.c_double, ctypes.c_int, ctypes.c_char_p, ctypes.c_uint64,
+                                     ctypes.POINTER(ctypes.c_double)]
         L.ref_daemon_start.restype = ctypes.c_void_p
         L.ref_daemon_start.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
                                        ctypes.c_char_p, ctypes.c_uint64]
@@ -300,6 +303,17 @@ class _Ref:
                     "trace")
         return list(out), dict(zip(("fast_hits", "fast_misses", "fast_evictions", "open_errors", "disk_reads"),
                                    list(st)))
+
+    def client_decision(self, dir: str, key, gran_kind: int, block_bytes: int, params, fast_cap: int,
+                        headroom: float, calibrate: bool):
+        """Client::open's origin / fallback reason against a reference daemon, + its published calibration."""
+        buf = ctypes.create_string_buffer(256)
+        st = (ctypes.c_double * 4)()
+        q, o, s = params if params else (0.0, 0.0, 0.0)
+        self._check(self.L.ref_client_decision(dir.encode(), *(k.encode() for k in key), gran_kind, block_bytes,
+                                               int(params is not None), q, o, s, fast_cap, headroom, int(calibrate),
+                                               buf, len(buf), st), "client_decision")
+        return buf.value.decode(), (bool(st[0]), st[1], st[2], st[3])
 
     def daemon_start(self, dir: str, fast: int, host: int, disk: int, eager: bool = False) -> tuple:
         """A reference daemon inside this process: (handle, socket path)."""

@@ -818,6 +818,53 @@ int ref_worker(const char* endpoint, const char* dir, const char* ns, const char
   });
 }
 
+// Client::open's placement decision (client.cpp:148-222) against a reference
+// daemon configured with (fast_cap, headroom, startup_calibration): opens the
+// key with the given granularity (kind 0 model / 1 layer / 2 block) and, when
+// has_params, explicit CostModelParams; writes "shared" or "private <reason>"
+// and the daemon's published stats (has_calibration, q, o, s).
+int ref_client_decision(const char* dir, const char* ns, const char* name, const char* version, int gran_kind,
+                        uint64_t block_bytes, int has_params, double q, double o, double s, uint64_t fast_cap,
+                        double headroom, int calibrate, char* out, uint64_t cap, double* stats4) {
+  return guarded([&] {
+    daemon::DaemonConfig cfg;
+    cfg.listen_path = sock_path("dec");
+    cfg.disk_cache_dir = dir;
+    cfg.startup_calibration = calibrate != 0;
+    cfg.workspace_headroom_fraction = headroom;
+    cfg.fast_capacity_bytes = fast_cap;
+    cfg.host_capacity_bytes = fast_cap;
+    cfg.disk_capacity_bytes = 64ull << 30;
+    daemon::Daemon dmn(cfg);
+    dmn.start();
+    client::ClientConfig cc;
+    cc.endpoint = cfg.listen_path;
+    cc.model_dirs = {dir};
+    client::Client cli(cc);
+    client::OpenOptions opts;
+    opts.granularity = gran_kind == 0   ? shm::ShareGranularity::model()
+                       : gran_kind == 1 ? shm::ShareGranularity::layer()
+                                        : shm::ShareGranularity::block(block_bytes);
+    if (has_params) opts.params = client::CostModelParams{q, o, s};
+    std::string res;
+    {
+      client::ModelView v = cli.open({ns, name, version}, opts);
+      res = v.origin() == client::Origin::Shared ? "shared"
+                                                 : std::string("private ") + client::fallback_reason_name(
+                                                                                 v.fallback_reason());
+      cli.close(v);
+    }
+    wire::StatsResponse st = cli.stats();
+    stats4[0] = st.has_calibration ? 1 : 0;
+    stats4[1] = st.calib_q;
+    stats4[2] = st.calib_o;
+    stats4[3] = st.calib_s;
+    dmn.request_stop();
+    dmn.join();
+    return put_text(res, out, cap);
+  });
+}
+
 // wire_protocol.cpp:319-357 encode/decode through the text form
 int ref_wire_encode_text(const char* text, uint8_t* out, uint64_t cap, uint64_t* n) {
   return guarded([&] {

@@ -74,6 +74,8 @@ class StoreConfig(ctypes.Structure):
         ("world", ctypes.c_int32),
         ("directory_slots", ctypes.c_uint32),
         ("remote_url", ctypes.c_char_p),
+        ("workspace_headroom_fraction", ctypes.c_double),
+        ("startup_calibration", ctypes.c_uint32),
     ]
 
 

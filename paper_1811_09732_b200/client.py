@@ -216,6 +216,7 @@ class Client:
         self.plan_flags = plan_flags if plan_flags is not None else (opts.plan_flags if opts else 0)
         self.out_dtype = out_dtype or (opts.convert_to if opts and opts.convert_to else "bf16")
         self.imports = ImportCache()
+        self.cached_stats = None  # client.hpp cached_stats_: the last StatsResponse
         self._local = {}  # (model_id, generation) -> (resident json, digest, tensor views)
 
     # client.cpp:94-106
@@ -228,36 +229,86 @@ class Client:
                 return p
         return None
 
-    def open(self, key: F.ModelKey, force_private: bool = False, force_shared: bool = False,
-             granularity: int | None = None, params: CostModelParams | None = None,
-             local_path: str | None = None) -> ModelView:
-        """client.cpp:148-222."""
-        local = self.resolve_local(key, local_path)
+    # client.cpp:124-135
+    def stats(self) -> dict:
+        """Fetch (and cache) the store's stats: tiers, counters, the workspace
+        headroom and the published calibration."""
+        st = self.store.stats()
+        self.cached_stats = st
+        return st
 
-        def private(reason):
-            if not local:
-                raise TrimsError(Errc.NotFound, "NotFound", f"{key} (no daemon, no local artifact)")
-            return self.open_private(key, local, reason)
+    # client.cpp:137-142
+    def effective_params(self, params: CostModelParams | None = None) -> CostModelParams:
+        if params:
+            return params
+        if self.params:
+            return self.params
+        cs = self.cached_stats
+        if cs and cs.get("has_calibration"):
+            return CostModelParams(cs["calib_q"], cs["calib_o"], cs["calib_s"])
+        return CostModelParams()
 
+    def decide(self, key: F.ModelKey, local: str | None, force_private: bool = False, force_shared: bool = False,
+               granularity: int | None = None, params: CostModelParams | None = None,
+               block_bytes: int = 2 << 20) -> tuple[str, object]:
+        """The placement decision of Client::open (client.cpp:148-205), before
+        any data moves: (PRIVATE, fallback reason) or (SHARED, granularity).
+        1. forced / disabled -> private;
+        2. with a local artifact and no force_shared: rho = b/q - n(o+s) with
+           the caller's params, else the store's published calibration (stats
+           fetched once; unreachable -> private), else kDefaultParams; Layer
+           falls back to Model when only that pays; rho <= 0 -> private;
+        3. workspace reservation: the artifact's workspace_bytes must fit the
+           store's advertised headroom (workspace_headroom x fast capacity),
+           else private."""
         if force_private:
-            return private("forced")
+            return PRIVATE, "forced"
         if self.disabled:
-            return private("disabled")
+            return PRIVATE, "disabled"
         if self.store is None:
-            return private("daemon_unreachable")
+            return PRIVATE, "daemon_unreachable"
         g = self.granularity if granularity is None else granularity
         if local and not force_shared:
             info = F.read_manifest(local)
+            manifest = json.loads(info.manifest_json)
             b = os.path.getsize(local)
-            p = params or self.params or CostModelParams()
-            n = len(F.layout_for(info.manifest_json, g))
+            if not params and not self.params and self.cached_stats is None:
+                try:
+                    self.stats()
+                except (TrimsError, OSError):
+                    return PRIVATE, "daemon_unreachable"
+            p = self.effective_params(params)
+            n = len(F.layout_for(info.manifest_json, g, block_bytes))
             if share_benefit(b, n, p) <= 0:
                 if g == F.LAYER and share_benefit(b, 1, p) > 0:
                     g = F.MODEL
                 else:
-                    return private("benefit_non_positive")
+                    return PRIVATE, "benefit_non_positive"
+            ws = int(manifest.get("workspace_bytes", 0))
+            if ws > 0 and self.cached_stats is None:
+                try:
+                    self.stats()
+                except (TrimsError, OSError):
+                    return PRIVATE, "daemon_unreachable"
+            cs = self.cached_stats
+            if cs is not None and "workspace_headroom" in cs:
+                headroom = cs["workspace_headroom"] * float(cs["tiers"][0]["capacity_bytes"])
+                if float(ws) > headroom:
+                    return PRIVATE, "workspace_reservation"
+        return SHARED, g
+
+    def open(self, key: F.ModelKey, force_private: bool = False, force_shared: bool = False,
+             granularity: int | None = None, params: CostModelParams | None = None,
+             local_path: str | None = None, block_bytes: int = 2 << 20) -> ModelView:
+        """client.cpp:148-222."""
+        local = self.resolve_local(key, local_path)
+        origin, what = self.decide(key, local, force_private, force_shared, granularity, params, block_bytes)
+        if origin == PRIVATE:
+            if not local:
+                raise TrimsError(Errc.NotFound, "NotFound", f"{key} (no daemon, no local artifact)")
+            return self.open_private(key, local, what)
         try:
-            return self.open_shared(key, g)
+            return self.open_shared(key, what, block_bytes)
         except TrimsError as e:
             if local and e.code in (Errc.NotFound, Errc.RemoteNotFound, Errc.NoEvictableSpace,
                                     Errc.TooLargeForFast, Errc.Internal, Errc.DaemonUnreachable,
@@ -265,10 +316,46 @@ class Client:
                 return self.open_private(key, local, "daemon_error")
             raise
 
-    def open_shared(self, key: F.ModelKey, granularity: int = F.MODEL) -> ModelView:
+    def calibrate(self, sample: F.ModelKey) -> CostModelParams:
+        """Client::calibrate (client.cpp:361-423): q = one sequential read of the
+        sample artifact; o = the store's export time per open (handle_export
+        counter deltas) and s = the local attach time, medians of 32 warm
+        force-shared opens."""
+        local = self.resolve_local(sample)
+        if not local:
+            raise TrimsError(Errc.NotFound, "NotFound", "calibration sample not found locally")
+        t0 = time.perf_counter()
+        total = 0
+        with open(local, "rb", buffering=0) as f:
+            while True:
+                chunk = f.read(1 << 20)
+                if not chunk:
+                    break
+                total += len(chunk)
+        dt = time.perf_counter() - t0
+        if dt <= 0 or total == 0:
+            raise TrimsError(Errc.Internal, "Internal", "calibration read failed")
+        q = total / dt
+        exports, attaches = [], []
+        before = self.stats()
+        prev_export, prev_opens = before["export_ns"], before["open_requests"]
+        for _ in range(32):
+            v = self.open(sample, force_shared=True)
+            if v.origin != SHARED:
+                raise TrimsError(Errc.DaemonUnreachable, "DaemonUnreachable", "calibration needs the store")
+            attaches.append(v.timings.attach_s)
+            self.close(v)
+            after = self.stats()
+            if after["open_requests"] > prev_opens:
+                exports.append((after["export_ns"] - prev_export) / 1e9 / (after["open_requests"] - prev_opens))
+            prev_export, prev_opens = after["export_ns"], after["open_requests"]
+        med = lambda v: sorted(v)[len(v) // 2] if v else 0.0
+        return CostModelParams(q, med(exports), med(attaches))
+
+    def open_shared(self, key: F.ModelKey, granularity: int = F.MODEL, block_bytes: int = 2 << 20) -> ModelView:
         """client.cpp:243-315: RPC, attach, digest, slice."""
         t0 = time.perf_counter()
-        ex = self.store.open(key, granularity)
+        ex = self.store.open(key, granularity, block_bytes)
         t1 = time.perf_counter()
         token = ex.token.decode() if isinstance(ex.token, bytes) else ex.token
         remote = getattr(ex, "remote", False)

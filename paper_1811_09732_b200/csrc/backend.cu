@@ -553,6 +553,75 @@ std::shared_ptr<IngestPlan> CudaTierBackend::plan_for(uint64_t model_id, const f
   return plans_.emplace(model_id, std::move(p)).first->second;
 }
 
+std::optional<Calibration> CudaTierBackend::calibrate() {
+  using clock = std::chrono::steady_clock;
+  auto secs = [](clock::time_point a) { return std::chrono::duration<double>(clock::now() - a).count(); };
+  Calibration cal;
+  // q: one full sequential read (1 MiB reads) of the largest artifact in the
+  // disk cache (daemon.cpp:343-364); nothing >= 1 MiB -> no calibration.
+  std::filesystem::path biggest;
+  uintmax_t biggest_size = 0;
+  std::error_code ec;
+  for (const auto& e : std::filesystem::directory_iterator(cfg_.disk_cache_dir, ec)) {
+    if (!e.is_regular_file(ec)) continue;
+    const uintmax_t sz = e.file_size(ec);
+    if (!ec && sz > biggest_size) {
+      biggest_size = sz;
+      biggest = e.path();
+    }
+  }
+  if (biggest_size < (1u << 20)) return std::nullopt;
+  {
+    const int fd = ::open(biggest.c_str(), O_RDONLY | O_CLOEXEC);
+    if (fd < 0) return std::nullopt;
+    std::vector<char> buf(1 << 20);
+    const auto t0 = clock::now();
+    uint64_t total = 0;
+    for (;;) {
+      const ssize_t n = ::read(fd, buf.data(), buf.size());
+      if (n <= 0) break;
+      total += uint64_t(n);
+    }
+    const double dt = secs(t0);
+    ::close(fd);
+    if (dt <= 0 || total == 0) return std::nullopt;
+    cal.q = double(total) / dt;
+  }
+  // o and s: medians over 32 export / attach reps of a 64 KiB segment
+  // (daemon.cpp:366-385): export = place it in the fast tier and seal its
+  // tail; attach = read the sealed tail back and validate it, which is what
+  // an importer does per object (trims_import_attach).
+  DeviceGuard g(cfg_.device);
+  std::vector<double> exports, attaches;
+  for (int i = 0; i < 32; ++i) {
+    auto rec = std::make_shared<FastRecord>();
+    const uint64_t payload = 64 * 1024;
+    auto e0 = clock::now();
+    place(*rec, payload);
+    SegTail t{};
+    t.magic = kSegMagic;
+    t.generation = rec->generation;
+    t.length = payload;
+    t.sealed = 1;
+    t.device = uint32_t(cfg_.device);
+    TRIMS_CUDA(cudaMemcpy(rec->base() + payload, &t, sizeof t, cudaMemcpyHostToDevice));
+    exports.push_back(secs(e0));
+    auto a0 = clock::now();
+    SegTail back{};
+    TRIMS_CUDA(cudaMemcpy(&back, rec->base() + payload, sizeof back, cudaMemcpyDeviceToHost));
+    if (back.magic != kSegMagic || back.generation != t.generation || !back.sealed)
+      raise(Errc::Internal, "calibration segment tail did not read back");
+    attaches.push_back(secs(a0));
+  }
+  auto median = [](std::vector<double>& v) {
+    std::sort(v.begin(), v.end());
+    return v[v.size() / 2];
+  };
+  cal.o = median(exports);
+  cal.s = median(attaches);
+  return cal;
+}
+
 void CudaTierBackend::place(FastRecord& rec, uint64_t payload) {
   auto a0 = std::chrono::steady_clock::now();
   uint64_t off = 0, reserved = 0;

@@ -10,6 +10,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -134,6 +135,16 @@ struct FastRecord {
   IngestStats stats;
 };
 
+// Startup calibration of the share-benefit cost model (daemon.hpp:42-46,
+// Daemon::run_startup_calibration daemon.cpp:342-390), measured on the B200
+// path: q = artifact read rate, o = per-object export (place + seal a
+// segment), s = per-object attach (read back + validate its sealed tail).
+struct Calibration {
+  double q{0};  // disk bytes/second
+  double o{0};  // per-object export seconds
+  double s{0};  // per-object attach seconds
+};
+
 class CudaTierBackend : public TierBackend {
  public:
   explicit CudaTierBackend(BackendConfig cfg);
@@ -152,6 +163,8 @@ class CudaTierBackend : public TierBackend {
   FastPublication publish_from_peer(uint64_t model_id, const fmt::Manifest& m, const PeerSource& src) override;
 
   std::shared_ptr<FastRecord> fast_record(uint64_t model_id);
+  // nullopt when the disk cache holds no artifact of >= 1 MiB to time (as the reference)
+  std::optional<Calibration> calibrate();
   const uint8_t* host_buffer(uint64_t model_id, uint64_t* bytes);
   Ingestor& ingestor() { return ing_; }
   const BackendConfig& config() const { return cfg_; }

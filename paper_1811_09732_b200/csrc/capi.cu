@@ -31,6 +31,12 @@ namespace {
 
 thread_local std::string g_last_error;
 
+std::string f64(double v) {  // round-trippable JSON number
+  char b[40];
+  std::snprintf(b, sizeof b, "%.17g", v);
+  return b;
+}
+
 template <class F>
 int guard(F&& f) {
   try {
@@ -119,6 +125,10 @@ struct trims_store {
   std::atomic<uint64_t> clock{0};
   // multi-GPU
   std::shared_ptr<Directory> dir;
+  // DaemonConfig::workspace_headroom_fraction (daemon.hpp:29) and the startup
+  // calibration published in StatsResponse (daemon.cpp:535-539)
+  double workspace_headroom{0.25};
+  std::optional<Calibration> calibration;
   PeerCounters peers;
   std::mutex peer_mu;
   std::map<std::tuple<int, int, uint64_t>, std::shared_ptr<Import>> peer_arenas;  // (pid, fd, bytes) -> mapping
@@ -518,6 +528,10 @@ int trims_store_create(const trims_store_config* cfg, trims_store** out) {
                                cfg->directory_slots ? cfg->directory_slots : 1024);
       bc.directory = s->dir;
     }
+    // validate_config (daemon.cpp): the headroom is a fraction
+    if (!(cfg->workspace_headroom_fraction >= 0.0 && cfg->workspace_headroom_fraction <= 1.0))
+      raise(Errc::InvalidArgument, "workspace_headroom_fraction must be in [0, 1]");
+    s->workspace_headroom = cfg->workspace_headroom_fraction;
     s->be = std::make_unique<CudaTierBackend>(std::move(bc));
     CoreConfig cc{cfg->fast_capacity_bytes, cfg->host_capacity_bytes, cfg->disk_capacity_bytes,
                   Policy(cfg->policy ? 1 : 0), cfg->eager_reclaim != 0};
@@ -532,6 +546,7 @@ int trims_store_create(const trims_store_config* cfg, trims_store** out) {
         if (key) s->core->register_disk_file(*key, p.string(), std::filesystem::file_size(p));
       }
     }
+    if (cfg->startup_calibration) s->calibration = s->be->calibrate();  // daemon.cpp:334
     *out = s.release();
     return 0;
   });
@@ -630,7 +645,12 @@ int trims_store_stats_json(trims_store* s, char* out, uint64_t cap) {
        << ",\"copy_ns\":" << st.cumulative.host_to_fast_copy_ns << ",\"export_ns\":" << st.cumulative.handle_export_ns
        << ",\"peer_hits\":" << st.peer_hits << ",\"peer_attempts\":" << s->peers.attempts.load()
        << ",\"peer_fallbacks\":" << s->peers.fallbacks.load() << ",\"rank\":" << (s->dir ? s->dir->rank() : 0)
-       << ",\"world\":" << (s->dir ? s->dir->world() : 1) << "}";
+       << ",\"world\":" << (s->dir ? s->dir->world() : 1) << ",\"workspace_headroom\":" << f64(s->workspace_headroom)
+       << ",\"has_calibration\":" << (s->calibration ? "true" : "false");
+    if (s->calibration)
+      os << ",\"calib_q\":" << f64(s->calibration->q) << ",\"calib_o\":" << f64(s->calibration->o)
+         << ",\"calib_s\":" << f64(s->calibration->s);
+    os << "}";
     return put(os.str(), out, cap);
   });
 }
@@ -1134,5 +1154,9 @@ StatsSnapshot stats(trims_store* s) { return s->core->stats(); }
 std::shared_ptr<FastRecord> fast_record(trims_store* s, uint64_t model_id) { return s->be->fast_record(model_id); }
 
 void set_last_error(const std::string& what) { g_last_error = what; }
+
+double workspace_headroom(trims_store* s) { return s->workspace_headroom; }
+
+std::optional<Calibration> calibration(trims_store* s) { return s->calibration; }
 
 }  // namespace trims::store_api

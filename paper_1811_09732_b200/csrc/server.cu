@@ -108,8 +108,8 @@ struct trims_server {
     return {q.model_id, store_api::close(store, key)};
   }
 
-  // daemon.cpp:515-542 (no calibration: the B200 client's share decision
-  // uses its own cost-model parameters)
+  // daemon.cpp:515-542, with the store's workspace headroom and its startup
+  // calibration (measured on the B200 path at store creation)
   wire::StatsResp stats() {
     const StatsSnapshot st = store_api::stats(store);
     wire::StatsResp m;
@@ -126,6 +126,13 @@ struct trims_server {
     m.disk_read_ns = st.cumulative.disk_read_ns;
     m.copy_ns = st.cumulative.host_to_fast_copy_ns;
     m.export_ns = st.cumulative.handle_export_ns;
+    m.workspace_headroom = store_api::workspace_headroom(store);
+    if (const auto cal = store_api::calibration(store)) {
+      m.has_calibration = true;
+      m.calib_q = cal->q;
+      m.calib_o = cal->o;
+      m.calib_s = cal->s;
+    }
     return m;
   }
 

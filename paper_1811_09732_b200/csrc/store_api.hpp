@@ -5,6 +5,7 @@
 #pragma once
 
 #include <memory>
+#include <optional>
 
 #include "backend.hpp"
 #include "cache_core.hpp"
@@ -19,6 +20,10 @@ uint64_t close(trims_store* s, const fmt::ModelKey& key);
 StatsSnapshot stats(trims_store* s);
 // The published fast-tier record (resident manifest, segment coordinates).
 std::shared_ptr<FastRecord> fast_record(trims_store* s, uint64_t model_id);
+// DaemonConfig::workspace_headroom_fraction and the startup calibration the
+// daemon publishes in StatsResponse (daemon.cpp:535-539).
+double workspace_headroom(trims_store* s);
+std::optional<Calibration> calibration(trims_store* s);
 // The C ABI's per-thread error text (trims_last_error).
 void set_last_error(const std::string& what);
 

@@ -229,6 +229,12 @@ class RemoteStore:
                  "copy_ns", "export_ns")
         out = {"tiers": tiers, "models": models}
         out.update({k: int(v) for k, v in zip(names, t[at:at + 8])})
+        at += 8
+        if at < len(t):  # wire_protocol.hpp StatsResponse tail: headroom, calibration
+            out["workspace_headroom"] = float(t[at])
+            out["has_calibration"] = t[at + 1] == "1"
+            if out["has_calibration"]:
+                out.update(zip(("calib_q", "calib_o", "calib_s"), (float(x) for x in t[at + 2:at + 5])))
         return out
 
     def close_connection(self) -> None:

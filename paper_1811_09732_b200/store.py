@@ -44,6 +44,8 @@ class StoreOptions:
     rank: int = 0
     world: int = 1
     directory_slots: int = 0           # 0 = 1024 per rank
+    workspace_headroom_fraction: float = 0.25  # daemon.hpp:29 (published to clients in stats)
+    startup_calibration: bool = True   # daemon.hpp:33: q/o/s measured at creation, published in stats
 
     @property
     def plan_flags(self) -> int:
@@ -76,6 +78,8 @@ class Store:
         cfg.directory_slots = opts.directory_slots
         self._remote = opts.remote_url.encode() if opts.remote_url else None
         cfg.remote_url = self._remote
+        cfg.workspace_headroom_fraction = opts.workspace_headroom_fraction
+        cfg.startup_calibration = int(opts.startup_calibration)
         h = ctypes.c_void_p()
         check(lib.trims_store_create(ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h
