@@ -257,6 +257,24 @@ int trims_import_verify(trims_import* im, uint64_t offset, uint64_t generation, 
                         uint64_t* checksum_out);
 void trims_import_close(trims_import* im);
 
+/* View lifetime (shared_segment.cpp:212-245 + test_shared_segment.cpp:99-110:
+ * an attached view survives the owner's destruction of the segment). With
+ * every model in one HBM arena, a reader holds the range it reads:
+ *  - in the store's process, a pin keeps the published record (and its arena
+ *    range) alive after eviction until released;
+ *  - in another process, a lease row in the arena's shared lease table
+ *    ("/<token>.leases") keeps the owner from reusing the range until it is
+ *    released or the reader dies. Acquire while the model is open (the open
+ *    handle guarantees the generation is current). A token without a lease
+ *    table (a dedicated segment) yields *out = NULL: the mapping itself keeps
+ *    the pages alive. */
+typedef struct trims_pin trims_pin;
+typedef struct trims_lease trims_lease;
+int trims_store_pin(trims_store* s, uint64_t model_id, uint64_t generation, trims_pin** out);
+void trims_pin_release(trims_pin* p);
+int trims_lease_acquire(const char* token, uint64_t offset, uint64_t generation, trims_lease** out);
+void trims_lease_release(trims_lease* l);
+
 /* ------------------------------------------- ingest kernels (K1..K5) raw */
 
 /* Pinned/pageable host raw blob -> resident blob on the device (what

@@ -212,6 +212,10 @@ _SIGS = {
     "trims_net_rebind": (_c.c_int, [_p, _p]),
     "trims_net_info": (_c.c_int, [_p, _c.POINTER(_c.c_double)]),
     "trims_net_forward_host": (_c.c_int, [_p, _p, _p, _p, _c.c_int]),
+    "trims_store_pin": (_c.c_int, [_p, _u64, _u64, _c.POINTER(_p)]),
+    "trims_pin_release": (None, [_p]),
+    "trims_lease_acquire": (_c.c_int, [_s, _u64, _u64, _c.POINTER(_p)]),
+    "trims_lease_release": (None, [_p]),
     "trims_net_tap": (_c.c_int, [_p, _c.c_int, _c.POINTER(_p), _c.POINTER(_c.c_int), _c.POINTER(_c.c_int)]),
     "trims_softmax": (_c.c_int, [_p, _p, _c.c_int, _c.c_int, _p]),
 }

@@ -46,6 +46,7 @@ class TensorView:
     offset: int
     nbytes: int
     dev_ptr: int
+    _keep: object = field(default=None, repr=False, compare=False)  # what keeps dev_ptr's bytes valid
 
     def torch(self, device=None):
         """Zero-copy torch view of the (read-only) device bytes."""
@@ -85,6 +86,7 @@ class ModelView:
     is_open: bool = True
     _import: object = None          # trims_import* for imported mappings
     _private: object = None         # owning torch buffer of a private view
+    _hold: object = None            # ViewHold of a shared view (keeps its bytes valid)
     _release: object = None
 
     @property
@@ -111,10 +113,14 @@ class TensorViews(Sequence):
     a new generation then costs no per-tensor Python objects (267 for
     ResNet-50) until a caller actually walks the tensors."""
 
-    __slots__ = ("_recs", "_base", "_made")
+    __slots__ = ("_recs", "_base", "_made", "_keep")
 
-    def __init__(self, recs, base_ptr: int):
-        self._recs, self._base, self._made = recs, base_ptr, {}
+    def __init__(self, recs, base_ptr: int, keep=None):
+        self._recs, self._base, self._made, self._keep = recs, base_ptr, {}, keep
+
+    def held_by(self, keep) -> "TensorViews":
+        """The same views for one open, holding that open's pin / lease."""
+        return TensorViews(self._recs, self._base, keep)
 
     def __len__(self):
         return len(self._recs)
@@ -127,7 +133,7 @@ class TensorViews(Sequence):
         v = self._made.get(i)
         if v is None:
             n, d, dt, lay, off, nb = self._recs[i]
-            v = self._made[i] = TensorView(n, d, dt, lay, off, nb, self._base + off)
+            v = self._made[i] = TensorView(n, d, dt, lay, off, nb, self._base + off, self._keep)
         return v
 
     def __eq__(self, other):
@@ -146,6 +152,43 @@ def slice_tensors(manifest_json: str, base_ptr: int) -> TensorViews:
             _PARSED.clear()
         _PARSED[manifest_json] = recs
     return TensorViews(recs, base_ptr)
+
+
+class ViewHold:
+    """Keeps an attached view's bytes valid for as long as any object that can
+    read them (the ModelView, its TensorViews, a BoundNet) is alive — also
+    after close() and after the store evicts the model, as an attached POSIX
+    shm view outlives its owner (proj/tests/test_shared_segment.cpp:99-110):
+    an in-process pin on the published record, or a lease row in the owner's
+    arena lease table (trims_store_pin / trims_lease_acquire)."""
+
+    __slots__ = ("_h", "_release")
+
+    def __init__(self, h, release):
+        self._h, self._release = h, release
+
+    @classmethod
+    def pin(cls, store, model_id: int, generation: int) -> "ViewHold":
+        h = ctypes.c_void_p()
+        check(lib.trims_store_pin(store._h, model_id, generation, ctypes.byref(h)))
+        return cls(h, lib.trims_pin_release)
+
+    @classmethod
+    def lease(cls, token: str, offset: int, generation: int) -> "ViewHold":
+        h = ctypes.c_void_p()
+        check(lib.trims_lease_acquire(token.encode(), offset, generation, ctypes.byref(h)))
+        return cls(h if h.value else None, lib.trims_lease_release)
+
+    def release(self) -> None:
+        if self._h:
+            self._release(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
 
 
 class ImportCache:
@@ -380,6 +423,7 @@ class Client:
             elif remote and ex.fd >= 0:
                 os.close(ex.fd)
             base, mjson, seen, tensors = hit
+            hold = ViewHold.lease(token, ex.segment_offset, ex.generation)
         else:
             # same process: the segment is already mapped; the manifest is
             # fetched, digest-checked and sliced once per (model, generation)
@@ -392,10 +436,12 @@ class Client:
                 hit = (mjson, digest, slice_tensors(mjson, base))
                 self._local[(ex.model_id, ex.generation)] = hit
             mjson, seen, tensors = hit
+            hold = ViewHold.pin(self.store, ex.model_id, ex.generation)
         if seen != digest:
             raise TrimsError(Errc.Corrupt, "Corrupt", "manifest digest mismatch on attach")
-        view = ModelView(key, SHARED, "none", mjson, base, tensors, ex.model_id, ex.generation,
+        view = ModelView(key, SHARED, "none", mjson, base, tensors.held_by(hold), ex.model_id, ex.generation,
                          outcome=_outcome(ex.outcome), export=ex)
+        view._hold = hold
         view.timings.rpc_s = t1 - t0
         view.timings.attach_s = time.perf_counter() - t1
         return view
@@ -420,7 +466,7 @@ class Client:
         cs = ctypes.c_uint64()
         check(lib.trims_ingest_host(self.device, host.data_ptr(), info.manifest_json.encode(), self.plan_flags,
                                     F.DTYPE_CODE[self.out_dtype], dev.data_ptr(), ctypes.byref(cs), None))
-        view = ModelView(key, PRIVATE, reason, rj, dev.data_ptr(), slice_tensors(rj, dev.data_ptr()))
+        view = ModelView(key, PRIVATE, reason, rj, dev.data_ptr(), slice_tensors(rj, dev.data_ptr()).held_by(dev))
         view._private = dev
         view.timings.private_load_s = time.perf_counter() - t0
         return view

@@ -322,7 +322,10 @@ bool prestage_enabled() {
 CudaTierBackend::CudaTierBackend(BackendConfig cfg) : cfg_(std::move(cfg)), ing_(cfg_.device) {
   DeviceGuard g(cfg_.device);
   if (cfg_.pinned_pool_bytes) pool_ = std::make_unique<PinnedPool>(cfg_.pinned_pool_bytes);
-  if (cfg_.arena_bytes) arena_ = std::make_unique<DeviceArena>(cfg_.device, cfg_.arena_bytes);
+  if (cfg_.arena_bytes)
+    arena_ = std::make_unique<DeviceArena>(cfg_.device, cfg_.arena_bytes,
+                                           "trims." + std::to_string(::getpid()) + ".arena" +
+                                               std::to_string(cfg_.device));
   TRIMS_CUDA(cudaStreamCreateWithFlags(&pre_stream_, cudaStreamNonBlocking));
   TRIMS_CUDA(cudaStreamCreateWithFlags(&d2h_stream_, cudaStreamNonBlocking));
   cudaMemPoolProps pp{};
@@ -671,7 +674,7 @@ FastPublication CudaTierBackend::seal(uint64_t model_id, std::shared_ptr<FastRec
   es.fd = rec->arena ? rec->arena->fd() : rec->seg.fd();
   es.alloc_bytes = rec->arena ? rec->arena->size() : rec->seg.size();
   es.offset = rec->offset;
-  if (rec->arena) es.token = "trims." + std::to_string(::getpid()) + ".arena" + std::to_string(cfg_.device);
+  if (rec->arena) es.token = rec->arena->token();
   es.resident_blob_bytes = rb;
   es.ingest_checksum = rec->checksum;
   pub.segments.push_back(es);

@@ -210,6 +210,19 @@ struct trims_import {
   int device{0};
 };
 
+// In-process view lifetime: holds the published record, so its arena range
+// is neither freed nor reused while the view may be read.
+struct trims_pin {
+  std::shared_ptr<FastRecord> rec;
+};
+
+// Cross-process view lifetime: one row of the owner's lease table.
+struct trims_lease {
+  std::shared_ptr<LeaseTable> table;
+  int row{-1};
+  uint64_t offset{0}, generation{0};
+};
+
 extern "C" {
 
 const char* trims_errc_name(int code) { return errc_name(Errc(code)); }
@@ -653,6 +666,41 @@ int trims_store_stats_json(trims_store* s, char* out, uint64_t cap) {
     os << "}";
     return put(os.str(), out, cap);
   });
+}
+
+int trims_store_pin(trims_store* s, uint64_t model_id, uint64_t generation, trims_pin** out) {
+  return guard([&] {
+    if (!s || !out) raise(Errc::InvalidArgument, "null argument");
+    auto rec = s->be->fast_record(model_id);
+    if (!rec) raise(Errc::NoSuchSegment, "model " + std::to_string(model_id) + " is not fast-resident");
+    if (rec->generation != generation) raise(Errc::StaleGeneration, "pin of a replaced generation");
+    *out = new trims_pin{std::move(rec)};
+    return 0;
+  });
+}
+
+void trims_pin_release(trims_pin* p) { delete p; }
+
+int trims_lease_acquire(const char* token, uint64_t offset, uint64_t generation, trims_lease** out) {
+  return guard([&] {
+    if (!token || !out) raise(Errc::InvalidArgument, "null argument");
+    *out = nullptr;
+    auto t = LeaseTable::open(token);
+    if (!t) return 0;  // a dedicated segment (no arena): the mapping itself keeps the pages
+    auto l = std::make_unique<trims_lease>();
+    l->row = t->acquire(offset, generation);
+    l->table = std::move(t);
+    l->offset = offset;
+    l->generation = generation;
+    *out = l.release();
+    return 0;
+  });
+}
+
+void trims_lease_release(trims_lease* l) {
+  if (!l) return;
+  if (l->table) l->table->release(l->row, l->offset, l->generation);
+  delete l;
 }
 
 int trims_store_resident_json(trims_store* s, uint64_t model_id, char* out, uint64_t cap) {

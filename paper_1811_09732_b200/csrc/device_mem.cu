@@ -1,7 +1,12 @@
 // device_mem.cu — cuMem VMM segments (export/import) and the pinned host pool.
+#include <fcntl.h>
+#include <signal.h>
+#include <sys/mman.h>
 #include <unistd.h>
 
 #include <algorithm>
+#include <cerrno>
+#include <cstring>
 
 #include "cuda_util.hpp"
 #include "device_mem.hpp"
@@ -176,14 +181,117 @@ Import::~Import() {
   }
 }
 
-DeviceArena::DeviceArena(int device, uint64_t bytes) {
+// ------------------------------------------------------------ LeaseTable
+
+LeaseTable::~LeaseTable() {
+  if (rows_) ::munmap(rows_, sizeof(Row) * kRows);
+  if (owner_) ::shm_unlink(name_.c_str());
+}
+
+std::unique_ptr<LeaseTable> LeaseTable::create(const std::string& token) {
+  auto t = std::make_unique<LeaseTable>();
+  t->name_ = shm_name(token);
+  ::shm_unlink(t->name_.c_str());  // a stale table of a dead owner with the same pid
+  const int fd = ::shm_open(t->name_.c_str(), O_CREAT | O_EXCL | O_RDWR | O_CLOEXEC, 0600);
+  if (fd < 0) raise(Errc::Internal, "shm_open " + t->name_ + ": " + std::strerror(errno));
+  if (::ftruncate(fd, off_t(sizeof(Row) * kRows)) != 0) {
+    ::close(fd);
+    ::shm_unlink(t->name_.c_str());
+    raise(Errc::Internal, "ftruncate " + t->name_);
+  }
+  void* p = ::mmap(nullptr, sizeof(Row) * kRows, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  ::close(fd);
+  if (p == MAP_FAILED) {
+    ::shm_unlink(t->name_.c_str());
+    raise(Errc::Internal, "mmap " + t->name_);
+  }
+  t->rows_ = static_cast<Row*>(p);  // zero-filled by ftruncate: every row free
+  t->owner_ = true;
+  return t;
+}
+
+std::shared_ptr<LeaseTable> LeaseTable::open(const std::string& token) {
+  static std::mutex mu;
+  static std::map<std::string, std::weak_ptr<LeaseTable>> cache;
+  std::lock_guard lk(mu);
+  auto& w = cache[token];
+  if (auto t = w.lock()) return t;
+  auto t = std::make_shared<LeaseTable>();
+  t->name_ = shm_name(token);
+  const int fd = ::shm_open(t->name_.c_str(), O_RDWR | O_CLOEXEC, 0);
+  if (fd < 0) return nullptr;  // the owner has no table (no arena) or is gone
+  void* p = ::mmap(nullptr, sizeof(Row) * kRows, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  ::close(fd);
+  if (p == MAP_FAILED) return nullptr;
+  t->rows_ = static_cast<Row*>(p);
+  w = t;
+  return t;
+}
+
+int LeaseTable::acquire(uint64_t offset, uint64_t generation) {
+  const uint32_t me = uint32_t(::getpid());
+  for (uint32_t pass = 0; pass < 2; ++pass) {
+    for (uint32_t i = 0; i < kRows; ++i) {
+      Row& r = rows_[i];
+      uint32_t cur = r.pid.load(std::memory_order_relaxed);
+      if (cur != 0) {
+        if (pass == 0 || ::kill(pid_t(cur), 0) == 0 || errno != ESRCH) continue;
+        // a dead reader's row: reclaim it
+        if (!r.pid.compare_exchange_strong(cur, 0)) continue;
+        cur = 0;
+      }
+      // Claim with a sentinel pid first so the owner never sees a half-written row.
+      uint32_t zero = 0;
+      if (!r.pid.compare_exchange_strong(zero, ~0u)) continue;
+      r.offset.store(offset, std::memory_order_relaxed);
+      r.generation.store(generation, std::memory_order_relaxed);
+      r.pid.store(me, std::memory_order_seq_cst);
+      return int(i);
+    }
+  }
+  raise(Errc::Internal, "lease table " + name_ + " is full");
+}
+
+void LeaseTable::release(int row, uint64_t offset, uint64_t generation) {
+  if (row < 0 || uint32_t(row) >= kRows) return;
+  Row& r = rows_[row];
+  if (r.offset.load() == offset && r.generation.load() == generation) r.pid.store(0, std::memory_order_seq_cst);
+}
+
+bool LeaseTable::held(uint64_t offset) {
+  for (uint32_t i = 0; i < kRows; ++i) {
+    Row& r = rows_[i];
+    uint32_t pid = r.pid.load(std::memory_order_seq_cst);
+    if (pid == 0) continue;
+    if (pid == ~0u) return true;  // being claimed: be conservative
+    if (r.offset.load() != offset) continue;
+    if (::kill(pid_t(pid), 0) != 0 && errno == ESRCH) {
+      r.pid.compare_exchange_strong(pid, 0);  // dead reader
+      continue;
+    }
+    return true;
+  }
+  return false;
+}
+
+uint32_t LeaseTable::live_rows() {
+  uint32_t n = 0;
+  for (uint32_t i = 0; i < kRows; ++i) n += rows_[i].pid.load() != 0;
+  return n;
+}
+
+// ------------------------------------------------------------ DeviceArena
+
+DeviceArena::DeviceArena(int device, uint64_t bytes, const std::string& token) : token_(token) {
   seg_ = DeviceSegment::create(device, std::max<uint64_t>(bytes, kGranule));
   free_[0] = seg_.size();
+  leases_ = LeaseTable::create(token);
 }
 
 bool DeviceArena::alloc(uint64_t bytes, uint64_t* offset, uint64_t* reserved) {
   const uint64_t need = std::max<uint64_t>(kGranule, (bytes + kGranule - 1) / kGranule * kGranule);
   std::lock_guard lk(mu_);
+  sweep();
   for (auto it = free_.begin(); it != free_.end(); ++it) {
     if (it->second < need) continue;
     const uint64_t off = it->first, len = it->second;
@@ -201,8 +309,35 @@ void DeviceArena::free(uint64_t off) {
   std::lock_guard lk(mu_);
   auto u = used_.find(off);
   if (u == used_.end()) return;
-  uint64_t len = u->second;
+  const uint64_t len = u->second;
   used_.erase(u);
+  if (leases_ && leases_->held(off)) {
+    retired_[off] = len;  // a reader still holds a view of this range
+    return;
+  }
+  insert_free(off, len);
+}
+
+void DeviceArena::sweep() {
+  for (auto it = retired_.begin(); it != retired_.end();) {
+    if (leases_ && leases_->held(it->first)) {
+      ++it;
+      continue;
+    }
+    insert_free(it->first, it->second);
+    it = retired_.erase(it);
+  }
+}
+
+uint64_t DeviceArena::retired_bytes() {
+  std::lock_guard lk(mu_);
+  sweep();
+  uint64_t r = 0;
+  for (auto& [o, l] : retired_) r += l;
+  return r;
+}
+
+void DeviceArena::insert_free(uint64_t off, uint64_t len) {
   auto next = free_.lower_bound(off);
   if (next != free_.end() && next->first == off + len) {
     len += next->second;

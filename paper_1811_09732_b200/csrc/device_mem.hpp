@@ -16,8 +16,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 
@@ -85,28 +87,68 @@ class DeviceSegment {
   int device_{0};
 };
 
+// Attach leases of one arena, in POSIX shared memory ("/<arena token>.leases").
+// A reader process that attaches a model segment of the arena holds a row
+// {pid, offset, generation} for as long as its view may be read; the owner
+// does not hand a freed range to another model while a live row names it.
+// This is how an attached view survives the owner's eviction
+// (proj/tests/test_shared_segment.cpp:99-110: a POSIX shm mapping outlives
+// shm_unlink) although every model lives in one shared allocation. Rows of
+// dead processes are reclaimed (kill(pid, 0) == ESRCH).
+class LeaseTable {
+ public:
+  static constexpr uint32_t kRows = 4096;
+  struct Row {
+    std::atomic<uint32_t> pid;  // 0 = free
+    uint32_t pad;
+    std::atomic<uint64_t> offset;
+    std::atomic<uint64_t> generation;
+  };
+  ~LeaseTable();
+  static std::string shm_name(const std::string& token) { return "/" + token + ".leases"; }
+  static std::unique_ptr<LeaseTable> create(const std::string& token);  // owner
+  static std::shared_ptr<LeaseTable> open(const std::string& token);    // reader (cached per process)
+  int acquire(uint64_t offset, uint64_t generation);  // row index; raises ResourceExhausted when full
+  void release(int row, uint64_t offset, uint64_t generation);
+  bool held(uint64_t offset);  // a live row names this range (any generation)
+  uint32_t live_rows();
+
+ private:
+  Row* rows_{nullptr};
+  std::string name_;
+  bool owner_{false};
+};
+
 // The fast tier's HBM arena: ONE exportable cuMem allocation sized to the
 // tier's capacity, carved first-fit into model segments. Publishing a model
 // costs no driver allocation call, and a client process maps the arena once
-// (one fd, read-only) and then reaches every model by offset. Reuse of a
-// freed range is detected by importers through the tail's generation
-// (the reference's StaleGeneration check, shared_segment.cpp:233-237).
+// (one fd, read-only) and then reaches every model by offset. A freed range
+// whose model is still leased by a reader (LeaseTable) is retired, not
+// reused, until the last lease goes; an importer holding a stale
+// (offset, generation) without a lease is refused through the tail's
+// generation (the reference's StaleGeneration check, shared_segment.cpp:233-237).
 class DeviceArena {
  public:
   static constexpr uint64_t kGranule = 64ull << 10;
-  DeviceArena(int device, uint64_t bytes);
+  DeviceArena(int device, uint64_t bytes, const std::string& token);
   // Returns false when no free extent fits (caller falls back to a dedicated segment).
   bool alloc(uint64_t bytes, uint64_t* offset, uint64_t* reserved);
   void free(uint64_t offset);
   uint8_t* base() const { return seg_.ptr(); }
   uint64_t size() const { return seg_.size(); }
   int fd() const { return seg_.fd(); }
+  const std::string& token() const { return token_; }
   uint64_t free_bytes();
+  uint64_t retired_bytes();
 
  private:
+  void insert_free(uint64_t off, uint64_t len);  // coalescing; mu_ held
+  void sweep();                                  // retired ranges whose leases are gone -> free; mu_ held
   DeviceSegment seg_;
+  std::string token_;
+  std::unique_ptr<LeaseTable> leases_;
   std::mutex mu_;
-  std::map<uint64_t, uint64_t> free_, used_;
+  std::map<uint64_t, uint64_t> free_, used_, retired_;
 };
 
 // Client-side read-only mapping of an exported segment.
