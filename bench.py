@@ -759,7 +759,7 @@ def cpu_baseline(src_json, blob, res_json) -> dict:
     while True:
         expected_resident(src_json, blob, res_json)
         n += 1
-        if time.perf_counter() - t0 > 3.0 or n >= 3:
+        if time.perf_counter() - t0 > 10.0:  # a bounded ~10 s sample of CPU work
             break
     dt = time.perf_counter() - t0
     return {"value": round(n * blob.size / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "port",

@@ -282,6 +282,14 @@ uint64_t Ingestor::from_staged(const IngestPlan& ip, const uint8_t* d_raw, cudaE
   return total;
 }
 
+void Ingestor::drain() {
+  DeviceGuard g(device_, /*nothrow=*/true);
+  if (copy_) cudaStreamSynchronize(copy_);
+  if (compute_) cudaStreamSynchronize(compute_);
+  if (side_.stream) cudaStreamSynchronize(side_.stream);
+  cudaGetLastError();
+}
+
 uint64_t Ingestor::pull(const IngestPlan& ip, const uint8_t* d_src, uint8_t* d_dst, std::vector<uint64_t>* buckets,
                         IngestStats* st) {
   if (!ip.identity) raise(Errc::Internal, "peer pull needs an identity plan");
@@ -323,7 +331,7 @@ CudaTierBackend::CudaTierBackend(BackendConfig cfg) : cfg_(std::move(cfg)), ing_
   DeviceGuard g(cfg_.device);
   if (cfg_.pinned_pool_bytes) pool_ = std::make_unique<PinnedPool>(cfg_.pinned_pool_bytes);
   if (cfg_.arena_bytes)
-    arena_ = std::make_unique<DeviceArena>(cfg_.device, cfg_.arena_bytes,
+    arena_ = std::make_shared<DeviceArena>(cfg_.device, cfg_.arena_bytes,
                                            "trims." + std::to_string(::getpid()) + ".arena" +
                                                std::to_string(cfg_.device));
   TRIMS_CUDA(cudaStreamCreateWithFlags(&pre_stream_, cudaStreamNonBlocking));
@@ -333,7 +341,7 @@ CudaTierBackend::CudaTierBackend(BackendConfig cfg) : cfg_(std::move(cfg)), ing_
   pp.location.type = cudaMemLocationTypeDevice;
   pp.location.id = cfg_.device;
   TRIMS_CUDA(cudaMemPoolCreate(&pre_pool_, &pp));
-  uint64_t keep = ~0ull;
+  uint64_t keep = kPrestageKeep;  // parked between cold opens; the rest is released at the next sync point
   TRIMS_CUDA(cudaMemPoolSetAttribute(pre_pool_, cudaMemPoolAttrReleaseThreshold, &keep));
   TRIMS_CUDA(cudaEventCreate(&pre_t0_));
   TRIMS_CUDA(cudaEventCreate(&pre_done_));
@@ -368,8 +376,44 @@ void CudaTierBackend::release_prestage(uint64_t model_id) {
     cudaFreeAsync(pre_raw_, pre_stream_);
     pre_raw_ = nullptr;
   }
+  pre_rec_.reset();  // a segment placed for an identity stream that was never published
   uint64_t want = model_id;
   pre_owner_.compare_exchange_strong(want, kNoOwner);
+}
+
+uint8_t* CudaTierBackend::claim_prestage(uint64_t model_id, const fmt::Manifest& m, uint64_t bytes) {
+  uint64_t none = kNoOwner;
+  if (!prestage_enabled() || !bytes || !pre_owner_.compare_exchange_strong(none, model_id)) return nullptr;
+  try {
+    DeviceGuard g(cfg_.device);
+    std::shared_ptr<IngestPlan> plan = plan_for(model_id, m);
+    if (plan->identity) {
+      // The resident blob IS the raw blob: stream it straight into the
+      // fast-tier segment (placed now, sealed by publish_fast) -- no second
+      // copy of the weights in HBM, no device-to-device pass.
+      auto rec = std::make_shared<FastRecord>();
+      rec->resident = plan->dst;
+      rec->json = plan->dst_json;
+      place(*rec, rec->resident.blob_bytes + rec->json.size() + 8);
+      pre_rec_ = std::move(rec);
+      return pre_rec_->base();
+    }
+    // A converting plan reads the raw blob from a transient buffer. Its pool
+    // parks at most kPrestageKeep bytes between cold opens; larger buffers go
+    // back to the driver after the publish (release_prestage).
+    const cudaError_t e =
+        cudaMallocFromPoolAsync(reinterpret_cast<void**>(&pre_raw_), bytes, pre_pool_, pre_stream_);
+    if (e != cudaSuccess) {
+      cudaGetLastError();  // out of memory for the overlap buffer: the plain path needs none
+      pre_raw_ = nullptr;
+      release_prestage(model_id);
+      return nullptr;
+    }
+    return pre_raw_;
+  } catch (...) {
+    release_prestage(model_id);
+    throw;
+  }
 }
 
 // daemon.cpp:128-136
@@ -470,13 +514,18 @@ void CudaTierBackend::stage_host(uint64_t model_id, const fmt::Manifest& m, cons
   HostBuf hb;
   if (take_verified(m.key, m.blob_bytes, &hb)) {
     // read_manifest already read + verified these bytes: only the upload is left
-    uint64_t none = kNoOwner;
-    if (prestage_enabled() && hb.bytes && pre_owner_.compare_exchange_strong(none, model_id)) {
+    uint8_t* target = nullptr;
+    try {
+      target = claim_prestage(model_id, m, hb.bytes);
+    } catch (...) {
+      free_host(hb);
+      throw;
+    }
+    if (target) {
       try {
         DeviceGuard g(cfg_.device);
-        TRIMS_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&pre_raw_), hb.bytes, pre_pool_, pre_stream_));
         TRIMS_CUDA(cudaEventRecord(pre_t0_, pre_stream_));
-        TRIMS_CUDA(cudaMemcpyAsync(pre_raw_, hb.p, hb.bytes, cudaMemcpyHostToDevice, pre_stream_));
+        TRIMS_CUDA(cudaMemcpyAsync(target, hb.p, hb.bytes, cudaMemcpyHostToDevice, pre_stream_));
         TRIMS_CUDA(cudaEventRecord(pre_done_, pre_stream_));
         pre_read_ms_ = 0;
       } catch (...) {
@@ -501,18 +550,14 @@ void CudaTierBackend::stage_host(uint64_t model_id, const fmt::Manifest& m, cons
       // verify (daemon.cpp:155 read_model(path, full_verify)) in order under the read + upload
       Sha256 h;
       Sha256* hp = cfg_.full_verify ? &h : nullptr;
-      uint64_t none = kNoOwner;
-      if (prestage_enabled() && hb.bytes && pre_owner_.compare_exchange_strong(none, model_id)) {
-        // Read chunk c into the host tier while chunk c-1 uploads to the device.
+      if (uint8_t* target = claim_prestage(model_id, m, hb.bytes)) {
+        // Read chunk c into the host tier while chunk c-1 uploads to the
+        // device (into the segment itself for an identity plan).
         try {
           DeviceGuard g(cfg_.device);
-          // stream-ordered from a pool that keeps its memory: a cold open of
-          // any size reuses the blocks of earlier ones (no device-wide sync,
-          // no re-mapping)
-          TRIMS_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&pre_raw_), hb.bytes, pre_pool_, pre_stream_));
           auto r0 = std::chrono::steady_clock::now();
           TRIMS_CUDA(cudaEventRecord(pre_t0_, pre_stream_));
-          parallel_pread_upload(fd, hb.p, pre_raw_, hb.bytes, off, cfg_.read_threads, cfg_.device, pre_stream_, hp);
+          parallel_pread_upload(fd, hb.p, target, hb.bytes, off, cfg_.read_threads, cfg_.device, pre_stream_, hp);
           TRIMS_CUDA(cudaEventRecord(pre_done_, pre_stream_));
           pre_read_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - r0).count();
         } catch (...) {
@@ -629,7 +674,7 @@ void CudaTierBackend::place(FastRecord& rec, uint64_t payload) {
   auto a0 = std::chrono::steady_clock::now();
   uint64_t off = 0, reserved = 0;
   if (arena_ && arena_->alloc(payload + sizeof(SegTail), &off, &reserved)) {
-    rec.arena = arena_.get();
+    rec.arena = arena_;
     rec.offset = off;
     rec.reserved = reserved;
   } else {
@@ -705,76 +750,93 @@ FastPublication CudaTierBackend::seal(uint64_t model_id, std::shared_ptr<FastRec
 // 64-byte SegTail.
 FastPublication CudaTierBackend::publish_fast(uint64_t model_id, const fmt::Manifest& m, bool from_host,
                                               const std::string& path) {
-  auto rec = std::make_shared<FastRecord>();
   std::shared_ptr<IngestPlan> plan = plan_for(model_id, m);
-  rec->resident = plan->dst;
-  rec->json = plan->dst_json;
-  place(*rec, rec->resident.blob_bytes + rec->json.size() + 8);
+  const bool staged = from_host && pre_owner_.load() == model_id;
+  std::shared_ptr<FastRecord> rec;
+  if (staged && pre_rec_) {
+    rec = std::move(pre_rec_);  // the identity stream already filled this segment
+  } else {
+    rec = std::make_shared<FastRecord>();
+    rec->resident = plan->dst;
+    rec->json = plan->dst_json;
+    place(*rec, rec->resident.blob_bytes + rec->json.size() + 8);
+  }
   uint8_t* const base = rec->base();
   const double alloc_ms = rec->stats.alloc_ms;
 
-  if (from_host && pre_owner_.load() == model_id) {
-    // stage_host already streamed the raw blob to pre_raw_: transform only
-    try {
-      rec->checksum = ing_.from_staged(*plan, pre_raw_, pre_done_, base, &rec->bucket_sums, &rec->stats);
-      TRIMS_CUDA(cudaEventRecord(pre_used_, pre_stream_));  // from_staged returned: the reads are done
-      float ms = 0;
-      TRIMS_CUDA(cudaEventElapsedTime(&ms, pre_t0_, pre_done_));
-      rec->stats.h2d_ms = ms;  // overlapped with the file read
-      rec->stats.read_ms = pre_read_ms_;
-      rec->stats.h2d_bytes = m.blob_bytes;
-    } catch (...) {
+  // Any failure below: wait for queued ingest work before `rec` (and with it
+  // the arena range) is released by the unwinding.
+  try {
+    if (staged) {
+      // stage_host already streamed the raw blob to the device: transform only
+      // (an identity plan: hash the segment in place -- the fused copy+hash
+      // kernel with source == destination rewrites every word with itself)
+      const uint8_t* raw = pre_raw_ ? pre_raw_ : base;
+      try {
+        rec->checksum = ing_.from_staged(*plan, raw, pre_done_, base, &rec->bucket_sums, &rec->stats);
+        TRIMS_CUDA(cudaEventRecord(pre_used_, pre_stream_));  // from_staged returned: the reads are done
+        float ms = 0;
+        TRIMS_CUDA(cudaEventElapsedTime(&ms, pre_t0_, pre_done_));
+        rec->stats.h2d_ms = ms;  // overlapped with the file read
+        rec->stats.read_ms = pre_read_ms_;
+        rec->stats.h2d_bytes = m.blob_bytes;
+      } catch (...) {
+        ing_.drain();  // no queued kernel may still touch the buffers freed below
+        release_prestage(model_id);
+        throw;
+      }
       release_prestage(model_id);
-      throw;
-    }
-    release_prestage(model_id);
-  } else if (from_host) {
-    const uint8_t* src = nullptr;
-    bool resident = false;
-    cudaEvent_t ready = nullptr;
-    {
-      std::lock_guard lk(mu_);
-      auto it = host_.find(model_id);
-      if (it == host_.end()) raise(Errc::Internal, "host buffer missing for publish");
-      if (it->second.bytes != m.blob_bytes) raise(Errc::Internal, "host buffer size mismatch");
-      src = it->second.p;  // single-flight pins the entry while loading
-      resident = it->second.resident;
-      ready = it->second.ready;
-    }
-    if (resident) {
-      // The host tier already holds the resident blob: copy it straight into
-      // the segment and hash it (the identity plan of the resident manifest).
-      if (ready) TRIMS_CUDA(cudaEventSynchronize(ready));
-      std::shared_ptr<IngestPlan> ident = pull_plan_for(model_id, rec->resident);
-      rec->checksum = ing_.from_host(*ident, src, base, &rec->bucket_sums, &rec->stats);
-    } else {
-      rec->checksum = ing_.from_host(*plan, src, base, &rec->bucket_sums, &rec->stats);
-    }
-  } else if (HostBuf vb; take_verified(m.key, m.blob_bytes, &vb)) {
-    // host tier skipped under pressure, but read_manifest holds the verified
-    // bytes: publish from them instead of reading the file again
-    try {
-      rec->checksum = ing_.from_host(*plan, vb.p, base, &rec->bucket_sums, &rec->stats);
-    } catch (...) {
+    } else if (from_host) {
+      const uint8_t* src = nullptr;
+      bool resident = false;
+      cudaEvent_t ready = nullptr;
+      {
+        std::lock_guard lk(mu_);
+        auto it = host_.find(model_id);
+        if (it == host_.end()) raise(Errc::Internal, "host buffer missing for publish");
+        if (it->second.bytes != m.blob_bytes) raise(Errc::Internal, "host buffer size mismatch");
+        src = it->second.p;  // single-flight pins the entry while loading
+        resident = it->second.resident;
+        ready = it->second.ready;
+      }
+      if (resident) {
+        // The host tier already holds the resident blob: copy it straight into
+        // the segment and hash it (the identity plan of the resident manifest).
+        if (ready) TRIMS_CUDA(cudaEventSynchronize(ready));
+        std::shared_ptr<IngestPlan> ident = pull_plan_for(model_id, rec->resident);
+        rec->checksum = ing_.from_host(*ident, src, base, &rec->bucket_sums, &rec->stats);
+      } else {
+        rec->checksum = ing_.from_host(*plan, src, base, &rec->bucket_sums, &rec->stats);
+      }
+    } else if (HostBuf vb; take_verified(m.key, m.blob_bytes, &vb)) {
+      // host tier skipped under pressure, but read_manifest holds the verified
+      // bytes: publish from them instead of reading the file again
+      try {
+        rec->checksum = ing_.from_host(*plan, vb.p, base, &rec->bucket_sums, &rec->stats);
+      } catch (...) {
+        free_host(vb);
+        throw;
+      }
       free_host(vb);
-      throw;
-    }
-    free_host(vb);
-  } else {
-    int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
-    if (fd < 0) raise(Errc::NotFound, path);
-    try {
-      uint8_t hdr[16];
-      if (::pread(fd, hdr, 16, 0) != 16) raise(Errc::Corrupt, "short read on " + path);
-      uint64_t mlen = 0;
-      for (int i = 0; i < 8; ++i) mlen |= uint64_t(hdr[8 + i]) << (8 * i);
-      rec->checksum = ing_.from_file(*plan, fd, fmt::blob_file_offset(mlen), base, &rec->bucket_sums,
-                                     &rec->stats);
-    } catch (...) {
+    } else {
+      int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
+      if (fd < 0) raise(Errc::NotFound, path);
+      try {
+        uint8_t hdr[16];
+        if (::pread(fd, hdr, 16, 0) != 16) raise(Errc::Corrupt, "short read on " + path);
+        uint64_t mlen = 0;
+        for (int i = 0; i < 8; ++i) mlen |= uint64_t(hdr[8 + i]) << (8 * i);
+        rec->checksum = ing_.from_file(*plan, fd, fmt::blob_file_offset(mlen), base, &rec->bucket_sums,
+                                       &rec->stats);
+      } catch (...) {
+        ::close(fd);
+        throw;
+      }
       ::close(fd);
-      throw;
     }
-    ::close(fd);
+  } catch (...) {
+    ing_.drain();
+    throw;
   }
   rec->stats.alloc_ms = alloc_ms;
   if (cfg_.resident_host_tier && !plan->identity) to_resident_form(model_id, *rec, *plan);
@@ -829,7 +891,12 @@ FastPublication CudaTierBackend::publish_from_peer(uint64_t model_id, const fmt:
   if (peer_json != rec->json) raise(Errc::InvalidArgument, "peer resident manifest differs (plan mismatch)");
   place(*rec, payload);
   std::shared_ptr<IngestPlan> ident = pull_plan_for(model_id, rec->resident);
-  rec->checksum = ing_.pull(*ident, src.payload, rec->base(), &rec->bucket_sums, &rec->stats);
+  try {
+    rec->checksum = ing_.pull(*ident, src.payload, rec->base(), &rec->bucket_sums, &rec->stats);
+  } catch (...) {
+    ing_.drain();  // the pull may still be writing the range `rec` releases
+    throw;
+  }
   read_tail(nullptr);
   if (rec->checksum != src.checksum)
     raise(Errc::ChecksumMismatch, "peer pull of " + fmt::to_string(m.key) + ": checksum " +

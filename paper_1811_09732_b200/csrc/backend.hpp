@@ -77,6 +77,9 @@ class Ingestor {
   // segment mapped here) to d_dst, copied and hashed by one fused kernel.
   uint64_t pull(const IngestPlan& p, const uint8_t* d_src, uint8_t* d_dst, std::vector<uint64_t>* buckets,
                 IngestStats* st);
+  // Waits for everything queued on the ingest streams (error paths: before
+  // buffers a failed ingest may still be touching are freed). Never throws.
+  void drain();
 
  private:
   uint8_t* staging(uint64_t bytes);
@@ -120,7 +123,7 @@ struct BackendConfig {
 // dedicated segment when the arena has no fitting extent.
 struct FastRecord {
   DeviceSegment seg;             // dedicated allocation (arena == nullptr)
-  DeviceArena* arena{nullptr};   // arena range [offset, offset + reserved)
+  std::shared_ptr<DeviceArena> arena;  // arena range [offset, offset + reserved); kept alive by pinned records
   uint64_t offset{0}, reserved{0};
   uint8_t* base() const { return arena ? arena->base() + offset : seg.ptr(); }
   ~FastRecord() {
@@ -190,7 +193,7 @@ class CudaTierBackend : public TierBackend {
   BackendConfig cfg_;
   Ingestor ing_;
   std::unique_ptr<PinnedPool> pool_;
-  std::unique_ptr<DeviceArena> arena_;
+  std::shared_ptr<DeviceArena> arena_;  // shared with every record placed in it (a pin may outlive the backend)
   std::mutex mu_;
   std::map<uint64_t, HostBuf> host_;
   // full_verify: read_manifest reads the blob into pinned memory while hashing
@@ -209,8 +212,11 @@ class CudaTierBackend : public TierBackend {
   // transforms. One model at a time owns the buffer (pre_owner_); a
   // concurrent cold open takes the plain path.
   static constexpr uint64_t kNoOwner = ~0ull;
+  static constexpr uint64_t kPrestageKeep = 256ull << 20;  // pool memory parked between cold opens
   std::atomic<uint64_t> pre_owner_{kNoOwner};
-  uint8_t* pre_raw_{nullptr};      // from pre_pool_, owned by pre_owner_ until its publish
+  uint8_t* pre_raw_{nullptr};      // from pre_pool_, owned by pre_owner_ until its publish (converting plans)
+  std::shared_ptr<FastRecord> pre_rec_;  // identity plans: the placed segment the file streams into
+  uint8_t* claim_prestage(uint64_t model_id, const fmt::Manifest& m, uint64_t bytes);
   cudaMemPool_t pre_pool_{nullptr};
   cudaStream_t pre_stream_{nullptr};
   cudaStream_t d2h_stream_{nullptr};  // host tier -> resident form

@@ -158,6 +158,11 @@ std::vector<Candidate> evict_candidates(Policy p, std::vector<Candidate> c);
 
 class CacheCore {
  public:
+  // A peer attempt that failed for good (open_with_peers rethrows it): one user-level open error.
+  void note_open_error() {
+    std::lock_guard lk(mu_);
+    ++open_errors_;
+  }
   CacheCore(CoreConfig cfg, TierBackend& backend);
   // `peer` (multi-GPU extension): a peer copy to serve a fast-tier miss from;
   // nullptr is exactly the reference's open.

@@ -144,7 +144,12 @@ struct trims_store {
       auto it = manifests.find(key);
       if (it != manifests.end()) return it->second;
     }
-    auto m = std::make_shared<const fmt::Manifest>(be->read_manifest(key, l.path));
+    // The manifest only (no full_verify pass over the blob): a PeerHit never
+    // reads the local artifact's bytes, and the pulled copy is checked
+    // against the holder's sealed checksum instead.
+    fmt::ArtifactInfo a = fmt::read_artifact_info(l.path, false);
+    if (a.manifest.key != key) raise(Errc::Corrupt, "artifact at " + l.path + " holds " + fmt::to_string(a.manifest.key));
+    auto m = std::make_shared<const fmt::Manifest>(std::move(a.manifest));
     std::lock_guard lk(peer_mu);
     return manifests.emplace(key, std::move(m)).first->second;
   }

@@ -226,7 +226,10 @@ PlacementResult open_with_peers(CacheCore& core, const Directory* dir, const fmt
         if (peer_rank && r.outcome == Outcome::PeerHit) *peer_rank = c.rank;
         return r;
       } catch (const Error& e) {
-        if (!peer_retryable(e.code())) throw;
+        if (!peer_retryable(e.code())) {
+          core.note_open_error();
+          throw;
+        }
         if (ctr) ++ctr->fallbacks;
       }
     }

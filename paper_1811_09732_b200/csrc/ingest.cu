@@ -1221,12 +1221,23 @@ uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, co
       }();
       // Ticket counters are never reset: a launch draws exactly (dynamic
       // tiles + CTAs) tickets (every CTA ends on one failing draw), so the
-      // host advances the slot's base by that and passes it in.
+      // host advances the slot's base by that and passes it in -- only once
+      // the launch is accepted (commit_slot): a launch that never ran drew
+      // nothing, and the slot's base must stay equal to its device counter.
+      int pending_k = -1;
+      uint32_t pending_adv = 0;
       auto take_slot = [&](uint32_t dyn_tiles, uint32_t ctas, unsigned int** slot, uint32_t* base) {
-        const uint32_t k = side->sched_next++ % kSchedSlots;
+        const uint32_t k = side->sched_next % kSchedSlots;
         *slot = side->sched + 2 * k;
         *base = side->sched_base[k];
-        side->sched_base[k] += dyn_tiles + ctas;
+        pending_k = int(k);
+        pending_adv = dyn_tiles + ctas;
+      };
+      auto commit_slot = [&] {
+        if (pending_k < 0) return;
+        side->sched_base[pending_k] += pending_adv;
+        ++side->sched_next;
+        pending_k = -1;
       };
       unsigned int* slot = nullptr;
       uint32_t base = 0;
@@ -1250,6 +1261,8 @@ uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, co
         if (dynamic) take_slot(n, ctas, &slot, &base);
         go(ctas, slot, base, 0u, 0u);
       }
+      TRIMS_CUDA(cudaGetLastError());
+      commit_slot();
     } else {
       TransformFn fn = pair_kernel(g.sdt, g.ddt);
       if (!fn) raise(Errc::InvalidArgument, "unsupported dtype pair in plan");

@@ -93,8 +93,11 @@ TilePlan build_tiles(const fmt::Manifest& src, const fmt::Manifest& dst, bool id
 // Launch context of an Ingestor: an optional second stream for concurrent
 // groups (fork/join through the events), and a ring of tile-scheduler
 // counters in device memory for the TMA kernel's dynamic (work-stealing) tile
-// order. Each launch takes the next slot; the kernel's last CTA re-zeroes it,
-// so stream-ordered reuse is safe (slots >> launches in flight).
+// order. Each launch takes the next slot. The counters are never reset: a
+// launch draws exactly (dynamic tiles + CTAs) tickets, so the host keeps each
+// slot's base (the counter value the next launch on it starts from) and
+// advances it only after the launch is accepted; stream-ordered reuse is safe
+// (slots >> launches in flight).
 struct SideStream {
   cudaStream_t stream{nullptr};
   cudaEvent_t fork{nullptr}, join{nullptr};
