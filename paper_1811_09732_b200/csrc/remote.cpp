@@ -1,4 +1,12 @@
 // remote.cpp — see remote.hpp.
+//
+// Structure: a fetch is "produce the bytes into a private staging file, then
+// admit it". Producing is the backend's job (DirSource copies, HttpSource runs
+// one GET over a plain socket); admission is one place (StagedFile::admit):
+// a full artifact verification, then an atomic rename onto the canonical name.
+// A StagedFile that is not admitted deletes itself, so no error path can leave
+// a half-written or unverified file in the disk cache
+// (behaviour of proj/src/remote_store.cpp:74-120).
 #include "remote.hpp"
 
 #include <fcntl.h>
@@ -11,6 +19,7 @@
 #include <cerrno>
 #include <cstring>
 #include <filesystem>
+#include <optional>
 #include <vector>
 
 #include "errc.hpp"
@@ -21,166 +30,252 @@ namespace fs = std::filesystem;
 
 namespace {
 
-// remote_store.cpp:15-22: a full verify succeeding is what makes a file valid
-bool file_valid(const fs::path& p) {
+// The verification verdict of an artifact on disk: nullopt = valid, else the
+// error a full read_artifact_info raised.
+std::optional<Error> verdict(const fs::path& p) {
   try {
     fmt::read_artifact_info(p.string(), /*full_verify=*/true);
-    return true;
-  } catch (...) {
-    return false;
-  }
-}
-
-// remote_store.cpp:24-33
-void verify_or_remove(const fs::path& tmp) {
-  try {
-    fmt::read_artifact_info(tmp.string(), /*full_verify=*/true);
+    return std::nullopt;
   } catch (const Error& e) {
-    std::error_code ec;
-    fs::remove(tmp, ec);
-    if (e.code() == Errc::ChecksumMismatch) throw;
-    raise(Errc::ChecksumMismatch, std::string("fetched artifact invalid: ") + e.what());
+    return e;
+  } catch (const std::exception& e) {
+    return Error(Errc::CorruptManifest, e.what());
   }
 }
 
-struct Fd {
-  int fd{-1};
-  ~Fd() {
-    if (fd >= 0) ::close(fd);
+class UniqueFd {
+ public:
+  explicit UniqueFd(int fd = -1) : fd_(fd) {}
+  UniqueFd(const UniqueFd&) = delete;
+  UniqueFd& operator=(const UniqueFd&) = delete;
+  ~UniqueFd() { reset(); }
+  void reset(int fd = -1) {
+    if (fd_ >= 0) ::close(fd_);
+    fd_ = fd;
   }
+  int get() const { return fd_; }
+
+ private:
+  int fd_;
 };
 
-void write_all(int fd, const char* p, size_t n, const fs::path& what) {
-  while (n) {
-    ssize_t w = ::write(fd, p, n);
-    if (w < 0 && errno == EINTR) continue;
-    if (w <= 0) raise(Errc::TransportError, "cannot write " + what.string());
-    p += w;
-    n -= size_t(w);
-  }
-}
-
-// A buffered reader over the socket (status line, headers, chunked bodies).
-struct Conn {
-  int fd;
-  std::vector<char> buf = std::vector<char>(1 << 16);
-  size_t lo = 0, hi = 0;
-  bool fill() {
-    if (lo < hi) return true;
-    for (;;) {
-      ssize_t r = ::recv(fd, buf.data(), buf.size(), 0);
-      if (r < 0 && errno == EINTR) continue;
-      if (r < 0) raise(Errc::TransportError, std::string("recv: ") + std::strerror(errno));
-      lo = 0;
-      hi = size_t(r);
-      return r > 0;
+// `<dest_dir>/<file>.part.<pid>`: the only place a download is written to.
+class StagedFile {
+ public:
+  StagedFile(const fs::path& dest_dir, const std::string& filename)
+      : path_(dest_dir / (filename + ".part." + std::to_string(::getpid()))), dest_(dest_dir / filename) {}
+  ~StagedFile() {
+    if (!admitted_) {
+      std::error_code ec;
+      fs::remove(path_, ec);
     }
   }
+  const fs::path& path() const { return path_; }
+
+  int open_for_write() {
+    int fd = ::open(path_.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
+    if (fd < 0) raise(Errc::TransportError, "cannot write " + path_.string());
+    return fd;
+  }
+  void append(int fd, const char* p, size_t n) {
+    for (size_t done = 0; done < n;) {
+      const ssize_t w = ::write(fd, p + done, n - done);
+      if (w > 0) {
+        done += size_t(w);
+      } else if (!(w < 0 && errno == EINTR)) {
+        raise(Errc::TransportError, "cannot write " + path_.string());
+      }
+    }
+  }
+
+  // Verify, then rename onto the canonical name. A download that does not
+  // verify is reported as ChecksumMismatch whatever the parser's complaint.
+  fs::path admit() {
+    if (auto bad = verdict(path_)) {
+      if (bad->code() == Errc::ChecksumMismatch) throw *bad;
+      raise(Errc::ChecksumMismatch, std::string("fetched artifact invalid: ") + bad->what());
+    }
+    std::error_code ec;
+    fs::rename(path_, dest_, ec);
+    if (ec) raise(Errc::TransportError, "rename to " + dest_.string() + ": " + ec.message());
+    admitted_ = true;
+    return dest_;
+  }
+
+ private:
+  fs::path path_, dest_;
+  bool admitted_{false};
+};
+
+// ---- dir: backend ----------------------------------------------------------
+
+void produce_from_dir(const std::string& root, const std::string& filename, StagedFile& staged) {
+  const fs::path src = fs::path(root) / filename;
+  std::error_code ec;
+  if (!fs::exists(src, ec)) raise(Errc::RemoteNotFound, src.string());
+  fs::copy_file(src, staged.path(), fs::copy_options::overwrite_existing, ec);
+  if (ec) raise(Errc::TransportError, "copy " + src.string() + ": " + ec.message());
+}
+
+// ---- http:// backend -------------------------------------------------------
+
+struct Endpoint {
+  std::string authority;  // host[:port], as sent in the Host header
+  std::string host, port{"80"};
+  std::string prefix;  // path prefix without a trailing '/'
+};
+
+Endpoint parse_http_url(const std::string& url) {
+  constexpr std::string_view kScheme = "http://";
+  if (url.compare(0, kScheme.size(), kScheme) != 0) raise(Errc::InvalidArgument, "expected http:// url");
+  const std::string rest = url.substr(kScheme.size());
+  Endpoint ep;
+  const size_t path_at = rest.find('/');
+  ep.authority = rest.substr(0, path_at);
+  if (path_at != std::string::npos) {
+    ep.prefix = rest.substr(path_at);
+    ep.prefix.erase(ep.prefix.find_last_not_of('/') + 1);
+  }
+  ep.host = ep.authority;
+  const size_t colon = ep.authority.rfind(':');
+  const bool bracketed_v6 = ep.authority.find(']') != std::string::npos;
+  if (colon != std::string::npos && !bracketed_v6) {
+    ep.host = ep.authority.substr(0, colon);
+    ep.port = ep.authority.substr(colon + 1);
+  }
+  return ep;
+}
+
+int dial(const Endpoint& ep, const std::string& what) {
+  addrinfo hints{};
+  hints.ai_family = AF_UNSPEC;
+  hints.ai_socktype = SOCK_STREAM;
+  addrinfo* found = nullptr;
+  if (int rc = ::getaddrinfo(ep.host.c_str(), ep.port.c_str(), &hints, &found); rc != 0)
+    raise(Errc::TransportError, what + ": resolve " + ep.host + ": " + gai_strerror(rc));
+  int fd = -1;
+  for (addrinfo* ai = found; ai && fd < 0; ai = ai->ai_next) {
+    fd = ::socket(ai->ai_family, ai->ai_socktype | SOCK_CLOEXEC, ai->ai_protocol);
+    if (fd >= 0 && ::connect(fd, ai->ai_addr, ai->ai_addrlen) != 0) {
+      ::close(fd);
+      fd = -1;
+    }
+  }
+  ::freeaddrinfo(found);
+  if (fd < 0) raise(Errc::TransportError, what + ": connection to " + ep.authority + " failed");
+  timeval tv{60, 0};  // a stalled server fails the fetch after 60 s of silence
+  ::setsockopt(fd, SOL_SOCKET, SO_RCVTIMEO, &tv, sizeof(tv));
+  return fd;
+}
+
+// Response reader: a 64 KiB window over the socket.
+class Reader {
+ public:
+  explicit Reader(int fd) : fd_(fd), win_(1 << 16) {}
+
   std::string line() {
     std::string s;
     for (;;) {
-      if (!fill()) raise(Errc::TransportError, "connection closed in the response head");
-      while (lo < hi) {
-        char c = buf[lo++];
-        if (c == '\n') {
-          if (!s.empty() && s.back() == '\r') s.pop_back();
-          return s;
-        }
-        s.push_back(c);
-        if (s.size() > 16384) raise(Errc::TransportError, "response line too long");
+      if (!more()) raise(Errc::TransportError, "connection closed in the response head");
+      const char* b = win_.data() + at_;
+      const char* nl = static_cast<const char*>(std::memchr(b, '\n', end_ - at_));
+      const size_t take = nl ? size_t(nl - b) : end_ - at_;
+      s.append(b, take);
+      at_ += take + (nl ? 1 : 0);
+      if (s.size() > 16384) raise(Errc::TransportError, "response line too long");
+      if (nl) {
+        if (!s.empty() && s.back() == '\r') s.pop_back();
+        return s;
       }
     }
   }
-  // copies n bytes (or to EOF when n == npos) into fd
-  void body(int out, uint64_t n, const fs::path& what) {
-    while (n) {
-      if (!fill()) {
-        if (n == ~0ull) return;
+  // Moves `n` body bytes (all remaining bytes when n is nullopt) into `sink`.
+  template <class Sink>
+  void body(std::optional<uint64_t> n, Sink&& sink) {
+    uint64_t left = n.value_or(~0ull);
+    while (left) {
+      if (!more()) {
+        if (!n) return;
         raise(Errc::TransportError, "connection closed mid-body");
       }
-      size_t take = size_t(std::min<uint64_t>(n, hi - lo));
-      write_all(out, buf.data() + lo, take, what);
-      lo += take;
-      if (n != ~0ull) n -= take;
+      const size_t take = size_t(std::min<uint64_t>(left, end_ - at_));
+      sink(win_.data() + at_, take);
+      at_ += take;
+      if (n) left -= take;
     }
   }
+
+ private:
+  bool more() {
+    while (at_ == end_) {
+      const ssize_t r = ::recv(fd_, win_.data(), win_.size(), 0);
+      if (r < 0 && errno == EINTR) continue;
+      if (r < 0) raise(Errc::TransportError, std::string("recv: ") + std::strerror(errno));
+      if (r == 0) return false;
+      at_ = 0;
+      end_ = size_t(r);
+    }
+    return true;
+  }
+  int fd_;
+  std::vector<char> win_;
+  size_t at_{0}, end_{0};
 };
 
-std::string lower(std::string s) {
-  for (auto& c : s) c = char(std::tolower(static_cast<unsigned char>(c)));
-  return s;
+struct ResponseHead {
+  int status{0};
+  std::optional<uint64_t> content_length;
+  bool chunked{false};
+};
+
+ResponseHead read_head(Reader& in, const std::string& what) {
+  ResponseHead h;
+  const std::string status = in.line();  // "HTTP/1.x NNN reason"
+  if (status.compare(0, 5, "HTTP/") != 0 || status.size() < 12 || std::sscanf(status.c_str() + 9, "%d", &h.status) != 1)
+    raise(Errc::TransportError, what + ": bad status line");
+  for (std::string field = in.line(); !field.empty(); field = in.line()) {
+    const size_t colon = field.find(':');
+    if (colon == std::string::npos) continue;
+    std::string name = field.substr(0, colon), value = field.substr(colon + 1);
+    for (auto& ch : name) ch = char(std::tolower(static_cast<unsigned char>(ch)));
+    value.erase(0, value.find_first_not_of(' '));
+    if (name == "content-length") {
+      h.content_length = std::stoull(value);
+    } else if (name == "transfer-encoding") {
+      for (auto& ch : value) ch = char(std::tolower(static_cast<unsigned char>(ch)));
+      h.chunked = value.find("chunked") != std::string::npos;
+    }
+  }
+  return h;
 }
 
-// remote_store.cpp:35-56 (split_http) + the GET of :92-112, on a plain socket
-void http_get(const std::string& base, const std::string& filename, const fs::path& tmp) {
-  const std::string scheme = "http://";
-  if (base.rfind(scheme, 0) != 0) raise(Errc::InvalidArgument, "expected http:// url");
-  size_t slash = base.find('/', scheme.size());
-  std::string host_port = base.substr(scheme.size(), slash == std::string::npos ? std::string::npos
-                                                                                : slash - scheme.size());
-  std::string prefix = slash == std::string::npos ? "" : base.substr(slash);
-  while (!prefix.empty() && prefix.back() == '/') prefix.pop_back();
-  std::string host = host_port, port = "80";
-  if (size_t c = host_port.rfind(':'); c != std::string::npos && host_port.find(']') == std::string::npos) {
-    host = host_port.substr(0, c);
-    port = host_port.substr(c + 1);
+void produce_from_http(const std::string& url, const std::string& filename, StagedFile& staged) {
+  const Endpoint ep = parse_http_url(url);
+  const std::string what = "GET " + filename;
+  UniqueFd sock(dial(ep, what));
+  const std::string request = "GET " + ep.prefix + "/" + filename + " HTTP/1.1\r\nHost: " + ep.authority +
+                              "\r\nAccept: */*\r\nConnection: close\r\n\r\n";
+  for (size_t sent = 0; sent < request.size();) {
+    const ssize_t w = ::send(sock.get(), request.data() + sent, request.size() - sent, MSG_NOSIGNAL);
+    if (w <= 0) raise(Errc::TransportError, what + ": send failed");
+    sent += size_t(w);
   }
+  Reader in(sock.get());
+  const ResponseHead head = read_head(in, what);
+  if (head.status == 404) raise(Errc::RemoteNotFound, filename);
+  if (head.status != 200) raise(Errc::TransportError, what + ": http " + std::to_string(head.status));
 
-  addrinfo hints{}, *res = nullptr;
-  hints.ai_family = AF_UNSPEC;
-  hints.ai_socktype = SOCK_STREAM;
-  if (int rc = ::getaddrinfo(host.c_str(), port.c_str(), &hints, &res); rc != 0)
-    raise(Errc::TransportError, "GET " + filename + ": resolve " + host + ": " + gai_strerror(rc));
-  Fd s;
-  for (addrinfo* ai = res; ai; ai = ai->ai_next) {
-    s.fd = ::socket(ai->ai_family, ai->ai_socktype | SOCK_CLOEXEC, ai->ai_protocol);
-    if (s.fd < 0) continue;
-    if (::connect(s.fd, ai->ai_addr, ai->ai_addrlen) == 0) break;
-    ::close(s.fd);
-    s.fd = -1;
+  UniqueFd out(staged.open_for_write());
+  auto sink = [&](const char* p, size_t n) { staged.append(out.get(), p, n); };
+  if (!head.chunked) {
+    in.body(head.content_length, sink);
+    return;
   }
-  ::freeaddrinfo(res);
-  if (s.fd < 0) raise(Errc::TransportError, "GET " + filename + ": connection to " + host_port + " failed");
-  timeval tv{60, 0};  // client.set_read_timeout(60, 0)
-  ::setsockopt(s.fd, SOL_SOCKET, SO_RCVTIMEO, &tv, sizeof(tv));
-
-  const std::string req = "GET " + prefix + "/" + filename + " HTTP/1.1\r\nHost: " + host_port +
-                          "\r\nAccept: */*\r\nConnection: close\r\n\r\n";
-  for (size_t at = 0; at < req.size();) {
-    ssize_t w = ::send(s.fd, req.data() + at, req.size() - at, MSG_NOSIGNAL);
-    if (w <= 0) raise(Errc::TransportError, "GET " + filename + ": send failed");
-    at += size_t(w);
-  }
-  Conn c{s.fd};
-  std::string status = c.line();  // HTTP/1.x NNN reason
-  int code = 0;
-  if (status.rfind("HTTP/", 0) != 0 || status.size() < 12 || std::sscanf(status.c_str() + 9, "%d", &code) != 1)
-    raise(Errc::TransportError, "GET " + filename + ": bad status line");
-  uint64_t length = ~0ull;
-  bool chunked = false;
-  for (std::string h; !(h = c.line()).empty();) {
-    size_t colon = h.find(':');
-    if (colon == std::string::npos) continue;
-    std::string k = lower(h.substr(0, colon)), v = h.substr(colon + 1);
-    while (!v.empty() && v.front() == ' ') v.erase(v.begin());
-    if (k == "content-length") length = std::stoull(v);
-    if (k == "transfer-encoding" && lower(v).find("chunked") != std::string::npos) chunked = true;
-  }
-  if (code == 404) raise(Errc::RemoteNotFound, filename);
-  if (code != 200) raise(Errc::TransportError, "GET " + filename + ": http " + std::to_string(code));
-
-  Fd out;
-  out.fd = ::open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC | O_CLOEXEC, 0644);
-  if (out.fd < 0) raise(Errc::TransportError, "cannot write " + tmp.string());
-  if (chunked) {
-    for (;;) {
-      uint64_t n = std::stoull(c.line(), nullptr, 16);
-      if (!n) break;
-      c.body(out.fd, n, tmp);
-      c.line();  // CRLF after the chunk
-    }
-  } else {
-    c.body(out.fd, length, tmp);
+  for (;;) {  // chunk-size line, chunk, CRLF ... until the 0-size chunk
+    const uint64_t n = std::stoull(in.line(), nullptr, 16);
+    if (n == 0) return;
+    in.body(n, sink);
+    in.line();
   }
 }
 
@@ -189,45 +284,25 @@ void http_get(const std::string& base, const std::string& filename, const fs::pa
 RemoteRef make_ref(const std::string& url, const fmt::ModelKey& key) {
   RemoteRef ref;
   ref.key = key;
-  if (url.rfind("http://", 0) == 0) {
-    ref.backend = RemoteRef::Backend::Http;
-    ref.base = url;
-  } else {
-    ref.backend = RemoteRef::Backend::Dir;
-    ref.base = url.rfind("dir:", 0) == 0 ? url.substr(4) : url;
-  }
+  const bool http = url.compare(0, 7, "http://") == 0;
+  ref.backend = http ? RemoteRef::Backend::Http : RemoteRef::Backend::Dir;
+  ref.base = (!http && url.compare(0, 4, "dir:") == 0) ? url.substr(4) : url;
   return ref;
 }
 
 std::string fetch(const RemoteRef& ref, const std::string& dest_dir) {
   const std::string filename = fmt::canonical_filename(ref.key);
-  const fs::path dest = fs::path(dest_dir) / filename;
+  const fs::path cached = fs::path(dest_dir) / filename;
   std::error_code ec;
-  if (fs::exists(dest, ec) && file_valid(dest)) return dest.string();
+  if (fs::exists(cached, ec) && !verdict(cached)) return cached.string();  // reuse a valid copy
 
   fs::create_directories(dest_dir, ec);
-  const fs::path tmp = fs::path(dest_dir) / (filename + ".part." + std::to_string(::getpid()));
-  if (ref.backend == RemoteRef::Backend::Dir) {
-    const fs::path src = fs::path(ref.base) / filename;
-    if (!fs::exists(src, ec)) raise(Errc::RemoteNotFound, src.string());
-    fs::copy_file(src, tmp, fs::copy_options::overwrite_existing, ec);
-    if (ec) raise(Errc::TransportError, "copy " + src.string() + ": " + ec.message());
-  } else {
-    try {
-      http_get(ref.base, filename, tmp);
-    } catch (...) {
-      fs::remove(tmp, ec);
-      throw;
-    }
-  }
-  verify_or_remove(tmp);
-  fs::rename(tmp, dest, ec);
-  if (ec) {
-    std::error_code ec2;
-    fs::remove(tmp, ec2);
-    raise(Errc::TransportError, "rename to " + dest.string() + ": " + ec.message());
-  }
-  return dest.string();
+  StagedFile staged(dest_dir, filename);
+  if (ref.backend == RemoteRef::Backend::Http)
+    produce_from_http(ref.base, filename, staged);
+  else
+    produce_from_dir(ref.base, filename, staged);
+  return staged.admit().string();
 }
 
 }  // namespace trims::remote
