@@ -162,6 +162,8 @@ class _Ref:
         L.ref_touch_file.argtypes = [ctypes.c_char_p, _u64p]
         L.ref_layout_for.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_uint64, ctypes.c_char_p, ctypes.c_uint64]
         L.ref_replay.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_uint64]
+        L.ref_acceptance_specs.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                           ctypes.c_char_p, ctypes.c_uint64]
         L.ref_run_oracle.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, _u64p]
         L.ref_ingest.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
         L.ref_latency.argtypes = [ctypes.c_char_p] * 5 + [ctypes.c_int, ctypes.POINTER(ctypes.c_double), _u64p]
@@ -263,6 +265,17 @@ class _Ref:
         buf = ctypes.create_string_buffer(1 << 26)
         self._check(self.L.ref_replay(spec.encode(), buf, len(buf)), "replay")
         return buf.value.decode()
+
+    def replay_into(self, spec: bytes, buf) -> bytes:
+        """ref_replay into a caller-owned buffer (no per-call 64 MiB zeroing)."""
+        self._check(self.L.ref_replay(spec, buf, len(buf)), "replay")
+        return buf.value
+
+    def acceptance_specs(self, seed: int, traces: int, max_models: int, max_ops: int) -> list[str]:
+        """The exact trace set run_oracle draws (oracle.cpp:136-211) as replay specs."""
+        buf = ctypes.create_string_buffer(1 << 28)
+        self._check(self.L.ref_acceptance_specs(seed, traces, max_models, max_ops, buf, len(buf)), "acceptance_specs")
+        return [s for s in buf.value.decode().split("end\n") if s]
 
     def run_oracle(self, traces: int, seed: int, max_models: int, max_ops: int):
         out = (ctypes.c_uint64 * 6)()
