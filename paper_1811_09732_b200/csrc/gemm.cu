@@ -13,6 +13,7 @@
 #include <type_traits>
 #include <map>
 #include <mutex>
+#include <string>
 #include <tuple>
 
 #include "cuda_util.hpp"
@@ -26,7 +27,31 @@ using namespace trims::sm100;
 
 namespace {
 
-constexpr int BM = 128, BK = 64, kThreads = 256, kMaxSplits = 8;
+// 12 warps: 0 TMA producer, 1 MMA issuer (+ TMEM owner), 2-3 folded-BN
+// scale/bias, 4-11 epilogue (two warps per TMEM lane quarter, each taking
+// half of the tile's columns: at batch 1 the epilogue is latency-bound, so a
+// second warp per scheduler halves it).
+constexpr int BM = 128, BK = 64, kThreads = 384, kMaxSplits = 8;
+
+#ifdef TRIMS_GEMM_TRACE
+// Diagnostic build only (make EXTRA=-DTRIMS_GEMM_TRACE ...; scripts/gemm_trace.py):
+// per CTA [M<<32|N, K<<32|z<<16|y, start, producer past pdl_wait, first stage
+// full (MMA), accumulator full (epilogue), end, smid | x<<32, operand warps
+// done, epilogue operands ready, epilogue stores done, split-K: partial
+// parked, past the first cluster barrier, reduction done] (%globaltimer ns).
+constexpr int kGTW = 16, kGTCap = 16384;
+__device__ unsigned long long g_gtrace[kGTCap * kGTW];
+__device__ unsigned int g_gtrace_n;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define GT_SET(slot, i, v) \
+  do {                     \
+    if ((slot) < kGTCap) g_gtrace[(slot) * kGTW + (i)] = (v); \
+  } while (0)
+#endif
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
@@ -36,38 +61,59 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 __device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
 
-// Shared-memory plan of one CTA: the TMA ring, then the epilogue operands
-// (residual tile, folded-BN scale and bias) prefetched during the mainloop.
-template <int BN, int STAGES>
+// Shared-memory plan of one CTA: the TMA ring, the residual tile (staged by
+// TMA in SWIZZLE_128B boxes of 64 channels x 128 rows), for split-K launches
+// the receive buffer of this CTA's column slice, then folded-BN scale/bias.
+template <int BN, int STAGES, bool SPLIT>
 struct Smem {
   static constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr uint32_t RES_LD = BN + 8;  // bf16 elements per residual row (+16 B: spreads banks)
   static constexpr uint32_t RING = STAGES * STAGE_BYTES;
-  static constexpr uint32_t RES = RING, RES_BYTES = BM * RES_LD * 2;
-  static constexpr uint32_t SCALE = RES + RES_BYTES, BIAS = SCALE + BN * 4;
+  // split-K: only the 64-channel box holding this CTA's slice
+  static constexpr uint32_t RES = RING, RES_BYTES = SPLIT ? BM * 128 : BM * BN * 2;
+  // split z's partial of slice j lands at recv[z][row][0..cw) of CTA j;
+  // rows padded by 16 B so v4 accesses of 8 consecutive rows hit 8 bank groups
+  static constexpr uint32_t RECV = RES + RES_BYTES, RECV_BYTES = SPLIT ? BM * 4 * (BN + 4 * kMaxSplits) : 0;
+  static constexpr uint32_t SCALE = RECV + RECV_BYTES, BIAS = SCALE + BN * 4;
   static constexpr uint32_t TOTAL = BIAS + BN * 4 + 1024;  // + 1 KiB realignment slack
+  // split-K: the idle ring holds the outgoing partial blocks
+  static_assert(!SPLIT || RING >= BM * 4 * (BN + 4 * kMaxSplits), "split-K outgoing blocks exceed the ring");
 };
 
-template <int BN, int STAGES>
+// SPLIT = false: one CTA per output tile. SPLIT = true: grid.z = S splits of
+// K, the S CTAs of a tile form one (1, 1, S) cluster; split z owns output
+// columns [z*BN/S, (z+1)*BN/S) of the tile. Every split pushes each owner its
+// fp32 partial of that owner's slice straight from TMEM into the owner's
+// shared memory (st.async, completing bytes on the owner's mbarrier), so
+// nobody waits on a remote load; an owner sums the S partials in split order
+// (deterministic) and runs the epilogue of its slice.
+template <int BN, int STAGES, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, uint16_t* D,
-                   int M, int N, int K, int ldd, const float* __restrict__ scale, const float* __restrict__ bias,
-                   const uint16_t* __restrict__ res, int ldr, int relu, int kper, const ConvGeom cg) {
-  using L = Smem<BN, STAGES>;
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmR, uint16_t* D, int M, int N, int K, int ldd,
+                   const float* __restrict__ scale, const float* __restrict__ bias, int has_res, int relu, int kper,
+                   const ConvGeom cg) {
+  using L = Smem<BN, STAGES, SPLIT>;
   constexpr uint32_t TMEM_COLS = BN;  // 64 / 128 / 256: powers of two >= 32
   extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], accum_full;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], accum_full, res_full, recv_full;
   __shared__ uint32_t tmem_base;
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint16_t* s_res = reinterpret_cast<uint16_t*>(smem + L::RES);
+  // 1 KiB-aligned base for the SWIZZLE_128B tiles, derived from smem_raw by
+  // pointer arithmetic (an integer round trip would drop the shared address
+  // space and turn every epilogue smem access into a generic load)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* s_recv = reinterpret_cast<float*>(smem + L::RECV);
   float* s_scale = reinterpret_cast<float*>(smem + L::SCALE);
   float* s_bias = reinterpret_cast<float*>(smem + L::BIAS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  const int splits = gridDim.z, z = blockIdx.z;
+  const int splits = SPLIT ? int(gridDim.z) : 1, z = SPLIT ? int(blockIdx.z) : 0;
+  const int cw = BN / splits;  // split-K: this CTA's column slice [z*cw, (z+1)*cw)
+  const int rstride = cw + 4;  // receive-buffer row stride (floats)
   const int kblocks = (K + BK - 1) / BK;
   const int kb0 = z * kper, kb1 = min(kblocks, kb0 + kper);  // this split's k-blocks
+  // residual boxes staged: all BN/64 of the tile, or the one holding the slice
+  const int rbox0 = SPLIT ? (z * cw) / 64 : 0, rboxes = SPLIT ? 1 : (BN + 63) / 64;
   // Implicit conv: this tile = image ti, output rows [th*hbox, +hbox), cols [tw*wbox, +wbox).
   int ti = 0, th = 0, tw = 0;
   if (cg.impl) {
@@ -82,36 +128,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int h = th * cg.hbox + (rl >> cg.wbox_log2), w = tw * wbox + (rl & (wbox - 1));
     return (h < cg.P && w < cg.Q) ? (ti * cg.P + h) * cg.Q + w : -1;
   };
-  // Epilogue of tile columns [c_begin, c_end) for tile row rl: fetch(c0, v)
-  // yields the 16 fp32 accumulators of columns c0..c0+15; then scale, bias,
-  // residual (smem), ReLU, bf16, 32-byte stores.
-  // Epilogue of tile columns [c_begin, c_end) for tile row rl, CW (16 or 8)
-  // columns at a time: fetch(c0, v) yields the CW fp32 accumulators of
-  // columns c0..c0+CW-1; then scale, bias, residual (smem), ReLU, bf16,
-  // 16-byte stores.
-  auto store_cols = [&](auto cw_tag, int c_begin, int c_end, int rl, auto&& fetch) {
+  // Epilogue of CW (8 or 16) tile columns c0.. of tile row rl: scale, bias,
+  // residual, ReLU, bf16 -> back into the staging tile (the residual's
+  // swizzled smem box, in place: each 16-byte chunk is read and rewritten by
+  // the same thread). copy_out then writes the tile rows to global memory
+  // whole: a thread per row storing its own 16-byte chunks puts every chunk
+  // of a warp store in a different line (one L1 wavefront per 16 bytes, ~1
+  // cycle each: ~1000 cycles for a 128 x 64 tile); row-major copy-out packs
+  // a warp store into 128-byte row segments.
+  uint16_t* s_out = reinterpret_cast<uint16_t*>(smem + L::RES);
+  auto stage_at = [&](int rl, int c) {  // staging address of tile (row rl, column c), c % 8 == 0
+    const int box = c / 64 - rbox0, chunk = ((c & 63) >> 3) ^ (rl & 7);
+    return s_out + box * BM * 64 + rl * 64 + chunk * 8;
+  };
+  auto finish = [&](int rl, int c0, auto cw_tag, const float* v) {
     constexpr int CW = decltype(cw_tag)::value;
-    const int row = row_of(rl);
-    uint16_t* drow = D + size_t(row < 0 ? 0 : row) * ldd;
-    const bool vec_ok = (ldd % 8 == 0);
-#pragma unroll 1
-    for (int c0 = c_begin; c0 < c_end; c0 += CW) {
-      float v[CW];
-      fetch(c0, v);
-      const int n = n0 + c0;
-      if (row < 0 || n >= N) continue;
-      uint32_t rw[CW / 2];
 #pragma unroll
-      for (int q = 0; q < CW / 8; ++q) {
-        const uint4 r4 = res ? reinterpret_cast<const uint4*>(s_res + rl * L::RES_LD + c0)[q] : make_uint4(0, 0, 0, 0);
-        rw[4 * q] = r4.x, rw[4 * q + 1] = r4.y, rw[4 * q + 2] = r4.z, rw[4 * q + 3] = r4.w;
-      }
-      uint32_t o[CW / 2];
+    for (int q = 0; q < CW / 8; ++q) {
+      uint4* sp = reinterpret_cast<uint4*>(stage_at(rl, c0 + 8 * q));
+      const uint4 r4 = has_res ? *sp : make_uint4(0, 0, 0, 0);
+      const uint32_t rw[4] = {r4.x, r4.y, r4.z, r4.w};
+      const float4 sc0 = *reinterpret_cast<const float4*>(s_scale + c0 + 8 * q);
+      const float4 sc1 = *reinterpret_cast<const float4*>(s_scale + c0 + 8 * q + 4);
+      const float4 bi0 = *reinterpret_cast<const float4*>(s_bias + c0 + 8 * q);
+      const float4 bi1 = *reinterpret_cast<const float4*>(s_bias + c0 + 8 * q + 4);
+      const float sc[8] = {sc0.x, sc0.y, sc0.z, sc0.w, sc1.x, sc1.y, sc1.z, sc1.w};
+      const float bi[8] = {bi0.x, bi0.y, bi0.z, bi0.w, bi1.x, bi1.y, bi1.z, bi1.w};
+      uint32_t o[4];
 #pragma unroll
-      for (int j = 0; j < CW / 2; ++j) {
-        float a = v[2 * j] * s_scale[c0 + 2 * j] + s_bias[c0 + 2 * j];
-        float b = v[2 * j + 1] * s_scale[c0 + 2 * j + 1] + s_bias[c0 + 2 * j + 1];
-        if (res) {
+      for (int j = 0; j < 4; ++j) {
+        float a = v[8 * q + 2 * j] * sc[2 * j] + bi[2 * j];
+        float b = v[8 * q + 2 * j + 1] * sc[2 * j + 1] + bi[2 * j + 1];
+        if (has_res) {
           a += bf16_lo(rw[j]);
           b += bf16_hi(rw[j]);
         }
@@ -121,14 +169,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         o[j] = pack_bf16x2(a, b);
       }
-      if (vec_ok && n + CW <= N) {
-        uint4* dp = reinterpret_cast<uint4*>(drow + n);
-#pragma unroll
-        for (int q = 0; q < CW / 8; ++q) dp[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+      *sp = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  };
+  // Staged tile columns [cbeg, cbeg + W) -> D, row-major: consecutive
+  // threads take consecutive 16-byte chunks of a row. 256 epilogue threads.
+  auto copy_out = [&](int t, int cbeg, int W) {
+    const int lg = __ffs(W / 8) - 1;  // chunks per row = W / 8, a power of two
+#pragma unroll 4
+    for (int k = t; k < (BM << lg); k += 256) {
+      const int rl = k >> lg, c = cbeg + (k & ((1 << lg) - 1)) * 8;
+      const int row = row_of(rl), n = n0 + c;
+      if (row < 0 || n >= N) continue;
+      const uint4 v = *reinterpret_cast<const uint4*>(stage_at(rl, c));
+      uint16_t* dp = D + size_t(row) * ldd + n;
+      if (ldd % 8 == 0 && n + 8 <= N) {
+        *reinterpret_cast<uint4*>(dp) = v;
       } else {
-#pragma unroll
-        for (int j = 0; j < CW; ++j)
-          if (n + j < N) drow[n + j] = uint16_t(o[j >> 1] >> (16 * (j & 1)));
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        for (int j = 0; j < 8 && n + j < N; ++j) dp[j] = uint16_t(w[j >> 1] >> (16 * (j & 1)));
       }
     }
   };
@@ -142,21 +201,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   };
 
+#ifdef TRIMS_GEMM_TRACE
+  __shared__ unsigned int gt_slot;
+  if (threadIdx.x == 0) {
+    gt_slot = atomicAdd(&g_gtrace_n, 1u);
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    GT_SET(gt_slot, 0, (uint64_t(M) << 32) | uint32_t(N));
+    GT_SET(gt_slot, 1, (uint64_t(K) << 32) | (blockIdx.z << 16) | blockIdx.y);
+    GT_SET(gt_slot, 2, gtimer());
+    GT_SET(gt_slot, 7, smid | (uint64_t(blockIdx.x) << 32));
+  }
+#endif
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(&accum_full, 1);
+    mbar_init(&res_full, 1);
+    mbar_init(&recv_full, 1);
     fence_barrier_init();
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    if (has_res) prefetch_tmap(&tmR);
+    // the other splits' partials of this CTA's slice, in bytes
+    if (SPLIT) mbar_expect_tx(&recv_full, uint32_t((splits - 1) * BM * (cw + 4) * 4));
   }
   if (warp == 1) tmem_alloc<TMEM_COLS>(&tmem_base);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   pdl_trigger();  // the next layer's CTAs may start their prologue now
+  // every split's receive barrier is initialised before anyone pushes into it
+  // (off the critical path: this runs under the previous layer's tail)
+  if (SPLIT) cluster_sync();
   const uint32_t tmem = tmem_base;
 
   if (warp == 0) {
@@ -170,7 +249,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(sa + L::A_BYTES, &tmB, (kb0 + i) * BK, n0, &full[i]);
       }
       pdl_wait();
+#ifdef TRIMS_GEMM_TRACE
+      GT_SET(gt_slot, 3, gtimer());
+#endif
       for (int i = 0; i < pre; ++i) load_a(smem + i * L::STAGE_BYTES, kb0 + i, &full[i]);
+      if (has_res) {  // the residual tile rides the same engine, behind the first A tiles
+        mbar_expect_tx(&res_full, uint32_t(rboxes * BM * 128));
+        for (int b = 0; b < rboxes; ++b) {
+          uint8_t* dst = smem + L::RES + b * BM * 128;
+          const int c = n0 + (rbox0 + b) * 64;
+          if (cg.impl) tma_load_4d(dst, &tmR, c, tw * wbox, th * cg.hbox, ti, &res_full);
+          else tma_load_2d(dst, &tmR, c, m0, &res_full);
+        }
+      }
       for (int kb = kb0 + pre, i = pre; kb < kb1; ++kb, ++i) {
         const int s = i % STAGES;
         mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
@@ -186,6 +277,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
         const int s = i % STAGES;
         mbar_wait(&full[s], (i / STAGES) & 1);
+#ifdef TRIMS_GEMM_TRACE
+        if (i == 0) GT_SET(gt_slot, 4, gtimer());
+#endif
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES), sb = sa + L::A_BYTES;
 #pragma unroll
@@ -195,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mma_commit(&accum_full);
     }
-  } else if (warp < 4) {  // ---- epilogue operands -> smem, during the mainloop
+  } else if (warp < 4) {  // ---- folded-BN scale / bias -> smem (bind-time constants)
     const int t = threadIdx.x - 64;  // 64 threads
 #pragma unroll
     for (int j = t; j < BN; j += 64) {
@@ -203,105 +297,150 @@ __global__ void __launch_bounds__(kThreads, 1)
       s_scale[j] = (scale && n < N) ? __ldg(scale + n) : 1.f;
       s_bias[j] = (bias && n < N) ? __ldg(bias + n) : 0.f;
     }
-    pdl_wait();
-    if (res) {  // residual tile, 16-byte pieces (ldr % 8 == 0 checked on the host), 8 loads in flight
-      constexpr int PR = BN / 8, PIECES = BM * PR / 64, BATCH = PIECES < 8 ? PIECES : 8;
-#pragma unroll 1
-      for (int b = 0; b < PIECES; b += BATCH) {
-        uint4 v[BATCH];
-#pragma unroll
-        for (int u = 0; u < BATCH; ++u) {
-          const int i = t + (b + u) * 64, r = i / PR, c = (i - r * PR) * 8, gr = row_of(r);
-          v[u] = make_uint4(0, 0, 0, 0);
-          if (gr >= 0 && n0 + c + 8 <= N) {
-            v[u] = *reinterpret_cast<const uint4*>(res + size_t(gr) * ldr + n0 + c);
-          } else if (gr >= 0) {
-            for (int q = 0; q < 8 && n0 + c + q < N; ++q)
-              reinterpret_cast<uint16_t*>(&v[u])[q] = res[size_t(gr) * ldr + n0 + c + q];
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < BATCH; ++u) {
-          const int i = t + (b + u) * 64, r = i / PR, c = (i - r * PR) * 8;
-          *reinterpret_cast<uint4*>(s_res + r * L::RES_LD + c) = v[u];
-        }
-      }
-    }
-    asm volatile("bar.arrive 1, 192;" ::: "memory");  // operands ready for warps 4-7
+#ifdef TRIMS_GEMM_TRACE
+    if (t == 0) GT_SET(gt_slot, 8, gtimer());
+#endif
+    asm volatile("bar.arrive 1, 320;" ::: "memory");  // operands ready for warps 4-11
   } else {  // ---- epilogue: TMEM -> registers -> bf16 global
     pdl_wait();
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int q = warp & 3;          // TMEM lane quarter this warp may access
+    const int half = (warp - 4) >> 2;  // which half of the columns
     const int rl = q * 32 + lane;
     const uint32_t tq = tmem + (uint32_t(q * 32) << 16);
     mbar_wait(&accum_full, 0);
+#ifdef TRIMS_GEMM_TRACE
+    if (threadIdx.x == 128) GT_SET(gt_slot, 5, gtimer());
+#endif
     tc_fence_after();
-    if (splits > 1) {
-      // Split-K: park this split's fp32 partial tile in the (now idle) ring,
-      // column-major so a warp's accesses are contiguous.
-      float* part = reinterpret_cast<float*>(smem);
+    if (!SPLIT) {
+      asm volatile("bar.sync 1, 320;" ::: "memory");  // scale / bias in smem
+      if (has_res) mbar_wait(&res_full, 0);
+#ifdef TRIMS_GEMM_TRACE
+      if (threadIdx.x == 128) GT_SET(gt_slot, 9, gtimer());
+#endif
+      // this warp's BN/2 columns, 32 per TMEM round trip
+#pragma unroll 1
+      for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
+        uint32_t r[32];
+#ifdef TRIMS_GEMM_TRACE
+        const long long k0 = clock64();
+#endif
+        tmem_ld16_nw(tq + uint32_t(c0), r);
+        tmem_ld16_nw(tq + uint32_t(c0 + 16), r + 16);
+        tmem_wait_ld();
+#ifdef TRIMS_GEMM_TRACE
+        const long long k1 = clock64();
+#endif
+        finish(rl, c0, std::integral_constant<int, 16>{}, reinterpret_cast<const float*>(r));
+        finish(rl, c0 + 16, std::integral_constant<int, 16>{}, reinterpret_cast<const float*>(r + 16));
+#ifdef TRIMS_GEMM_TRACE
+        if (threadIdx.x == 128 && c0 == 0) GT_SET(gt_slot, 13, uint64_t(clock64() - k1));
+        if (c0 == 0 && !has_res) {  // diagnostic: the same work again, now with warm instruction caches
+          const long long k2 = clock64();
+          finish(rl, c0, std::integral_constant<int, 16>{}, reinterpret_cast<const float*>(r));
+          finish(rl, c0 + 16, std::integral_constant<int, 16>{}, reinterpret_cast<const float*>(r + 16));
+          if (threadIdx.x == 128) GT_SET(gt_slot, 14, uint64_t(clock64() - k2));
+        }
+        if (threadIdx.x == 128 && c0 == 0) GT_SET(gt_slot, 15, uint64_t(k1 - k0));
+#endif
+      }
+      asm volatile("bar.sync 2, 256;" ::: "memory");  // the whole tile is staged
+      copy_out(threadIdx.x - 128, 0, BN);
+#ifdef TRIMS_GEMM_TRACE
+      if (threadIdx.x == 128) GT_SET(gt_slot, 10, gtimer());
+#endif
+    } else {
       // A split can own no k-blocks (ceil(kblocks / splits) * (splits - 1)
       // >= kblocks): no MMA wrote its accumulator, so its partial is zero.
       const bool no_k = kb0 >= kb1;
+      const uint32_t recv_local = smem_u32(s_recv), bar_local = smem_u32(&recv_full);
+      // push: slice j of this row -> row rl of block j of the outgoing buffer
+      // (the ring, idle once the accumulator is complete), or straight into
+      // my own receive slot z for my own slice; the two warps of a lane
+      // quarter take alternate owners, one TMEM round trip per owner. Then
+      // one thread ships each block to its owner with one bulk copy (DSMEM
+      // through the copy engine; per-thread remote stores measured ~100-400
+      // cycles each).
+      float* s_out32 = reinterpret_cast<float*>(smem);  // [splits][BM][rstride]
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t r[16];
+      for (int j = half; j < splits; j += 2) {
+        uint32_t r[64];
         if (no_k) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) r[j] = 0u;
+          for (int u = 0; u < 64; ++u) r[u] = 0u;
         } else {
-          tmem_ld16(tq + uint32_t(c0), r);
+          if (cw == 8) tmem_ld8_nw(tq + uint32_t(j * cw), r);
+#pragma unroll
+          for (int c = 0; c < 64; c += 16)
+            if (c < cw && cw >= 16) tmem_ld16_nw(tq + uint32_t(j * cw + c), r + c);
+          tmem_wait_ld();
         }
+        float4* p = reinterpret_cast<float4*>((j == z ? s_recv : s_out32) + ((j * BM) + rl) * rstride);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) part[(c0 + j) * BM + rl] = __uint_as_float(r[j]);
+        for (int c = 0; c < 64; c += 4)
+          if (c < cw)
+            p[c / 4] = make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]), __uint_as_float(r[c + 2]),
+                                   __uint_as_float(r[c + 3]));
       }
-    } else {
-      asm volatile("bar.sync 1, 192;" ::: "memory");  // residual / scale / bias in smem
-      store_cols(std::integral_constant<int, 16>{}, 0, BN, rl, [&](int c0, float (&v)[16]) {
-        uint32_t r[16];
-        tmem_ld16(tq + uint32_t(c0), r);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-      });
-    }
-  }
-  if (splits > 1) {
-    // The splits of a tile form one thread-block cluster. After a cluster
-    // barrier, split z reduces columns [z*BN/S, (z+1)*BN/S) of the tile by
-    // reading every split's partial from distributed shared memory in split
-    // order (deterministic), and runs the epilogue for that slice.
-    cluster_sync();
-    if (warp >= 4) {
-      const int rl = (warp & 3) * 32 + lane, cols = BN / splits, cbeg = z * cols;
-      const uint32_t local = smem_u32(smem);
-      asm volatile("bar.sync 1, 192;" ::: "memory");
-      auto reduce = [&](auto cw_tag) {
-        constexpr int CW = decltype(cw_tag)::value;
-        store_cols(cw_tag, cbeg, cbeg + cols, rl, [&](int c0, float (&v)[CW]) {
-          float pv[kMaxSplits][CW];
+      fence_proxy_async_smem();
+      asm volatile("bar.sync 2, 256;" ::: "memory");  // all outgoing blocks written
+      if (threadIdx.x == 128) {
+        const uint32_t block = uint32_t(BM * rstride * 4);
+#pragma unroll 1
+        for (int j = 0; j < splits; ++j)
+          if (j != z)
+            bulk_copy_to_cluster(map_shared_rank(recv_local + uint32_t(z) * block, uint32_t(j)),
+                                 smem_u32(s_out32) + uint32_t(j) * block, block,
+                                 map_shared_rank(bar_local, uint32_t(j)));
+      }
+#ifdef TRIMS_GEMM_TRACE
+      if (threadIdx.x == 128) GT_SET(gt_slot, 11, gtimer());
+#endif
+      // every other split's partial of my slice has landed (bulk-copied data
+      // is visible to the observers of its mbarrier's phase completion, like
+      // a TMA load's: no cluster-scope acquire, which would invalidate L1 on
+      // every poll)
+      mbar_wait(&recv_full, 0);
+#ifdef TRIMS_GEMM_TRACE
+      if (threadIdx.x == 128) GT_SET(gt_slot, 12, gtimer());
+#endif
+      asm volatile("bar.sync 1, 320;" ::: "memory");  // scale / bias in smem; own partials written
+      if (has_res) mbar_wait(&res_full, 0);
+      // reduce this warp's part of the slice: v = p0 + p1 + ... in split
+      // order (deterministic); a slice of 8 columns is one warp's
+      const int hw = cw >= 16 ? cw / 2 : cw, cbeg = cw >= 16 ? half * hw : 0;
+      if (cw >= 16 || half == 0) {
+#pragma unroll 1
+        for (int c = cbeg; c < cbeg + hw; c += 8) {
+          float v[8];
 #pragma unroll
           for (int zz = 0; zz < kMaxSplits; ++zz) {
             if (zz < splits) {
-              const uint32_t base = map_shared_rank(local, uint32_t(zz));
+              const float4* p = reinterpret_cast<const float4*>(s_recv + ((zz * BM) + rl) * rstride + c);
+              const float4 a = p[0], b = p[1];
+              const float pv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-              for (int j = 0; j < CW; ++j) pv[zz][j] = ld_dsmem_f32(base + uint32_t(((c0 + j) * BM + rl) * 4));
+              for (int u = 0; u < 8; ++u) v[u] = zz ? v[u] + pv[u] : pv[u];
             }
           }
-#pragma unroll
-          for (int j = 0; j < CW; ++j) {
-            v[j] = pv[0][j];
-#pragma unroll
-            for (int zz = 1; zz < kMaxSplits; ++zz)
-              if (zz < splits) v[j] += pv[zz][j];
-          }
-        });
-      };
-      if (cols % 16 == 0) reduce(std::integral_constant<int, 16>{});
-      else reduce(std::integral_constant<int, 8>{});
+          finish(rl, z * cw + c, std::integral_constant<int, 8>{}, v);
+        }
+      }
+      asm volatile("bar.sync 2, 256;" ::: "memory");  // the slice is staged
+      copy_out(threadIdx.x - 128, z * cw, cw);
+#ifdef TRIMS_GEMM_TRACE
+      if (threadIdx.x == 128) GT_SET(gt_slot, 13, gtimer());
+#endif
     }
-    cluster_sync();  // no split leaves while its partial may still be read
   }
+  // split-K: no CTA leaves while a bulk copy may still be reading its
+  // outgoing blocks (every owner has received all its bytes past this point)
+  if (SPLIT) cluster_sync();
   tc_fence_before();
   __syncthreads();
+#ifdef TRIMS_GEMM_TRACE
+  if (threadIdx.x == 0) GT_SET(gt_slot, 6, gtimer());
+#endif
   if (warp == 1) {
     tc_fence_after();
     tmem_free<TMEM_COLS>(tmem);
@@ -321,13 +460,13 @@ EncodeTiled encode_fn() {
   return fn;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool SPLIT>
 void run_bn(const Prepared& p, cudaStream_t stream) {
-  constexpr size_t smem = Smem<BN, STAGES>::TOTAL;
+  constexpr size_t smem = Smem<BN, STAGES, SPLIT>::TOTAL;
   static_assert(smem <= 227 * 1024, "GEMM shared memory");
   static bool smem_set = false;
   if (!smem_set) {
-    TRIMS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TRIMS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(smem)));
     smem_set = true;
   }
@@ -349,9 +488,38 @@ void run_bn(const Prepared& p, cudaStream_t stream) {
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = unsigned(p.splits);
   cfg.attrs = attr;
-  cfg.numAttrs = p.splits > 1 ? 2 : 1;
-  TRIMS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES>, p.ta, p.tb, e.out, int(p.M), int(p.N), int(p.K),
-                                int(e.ldo), e.scale, e.bias, e.residual, int(e.ldr), e.relu ? 1 : 0, kper, p.g));
+  cfg.numAttrs = SPLIT ? 2 : 1;
+  TRIMS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, SPLIT>, p.ta, p.tb, p.tr, e.out, int(p.M), int(p.N),
+                                int(p.K), int(e.ldo), e.scale, e.bias, e.residual ? 1 : 0, e.relu ? 1 : 0, kper, p.g));
+}
+
+// Residual tile maps: bf16 [rows][ldr] (or NHWC [n][P][Q][ldr] for an
+// implicit conv), N channels wide, SWIZZLE_128B boxes of 64 channels x the
+// tile's 128 rows. Out-of-range rows / channels are zero-filled.
+CUtensorMap residual_map_2d(const Epilogue& e, uint64_t M, uint64_t N) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {N, M};
+  cuuint64_t strides[1] = {e.ldr * 2};
+  cuuint32_t box[2] = {64, uint32_t(BM)};
+  cuuint32_t estr[2] = {1, 1};
+  cu_check(encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(e.residual), dims, strides, box,
+                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+           "cuTensorMapEncodeTiled (residual)");
+  return m;
+}
+
+CUtensorMap residual_map_conv(const Epilogue& e, const ConvGeom& g, uint64_t N) {
+  CUtensorMap m;
+  cuuint64_t dims[4] = {N, cuuint64_t(g.Q), cuuint64_t(g.P), cuuint64_t(g.N)};
+  cuuint64_t strides[3] = {e.ldr * 2, cuuint64_t(g.Q) * e.ldr * 2, cuuint64_t(g.P) * g.Q * e.ldr * 2};
+  cuuint32_t box[4] = {64, uint32_t(1 << g.wbox_log2), uint32_t(g.hbox), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  cu_check(encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(e.residual), dims, strides, box,
+                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+           "cuTensorMapEncodeTiled (conv residual)");
+  return m;
 }
 
 }  // namespace
@@ -372,12 +540,26 @@ CUtensorMap make_tmap(const void* ptr, uint64_t rows, uint64_t k, uint64_t ld, u
 }
 
 int pick_bn(uint64_t M, uint64_t N, int sms) {
+  static const int forced = [] {  // A/B switch: TRIMS_GEMM_BN=64|128|256
+    const char* e = std::getenv("TRIMS_GEMM_BN");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 64 || forced == 128 || (forced == 256 && N % 256 == 0)) return forced;
   // Enough CTAs to cover the SMs first, then the widest tile.
   const uint64_t mt = (M + BM - 1) / BM;
   if (N <= 64) return 64;
   if (mt * ((N + 255) / 256) >= uint64_t(sms) && N % 256 == 0) return 256;
-  if (mt * ((N + 127) / 128) >= uint64_t(sms) / 2 || N <= 128) return 128;
-  return 64;
+  // 64-wide tiles whenever they still fit one wave: there latency (batch-1
+  // layers) wins with more, narrower CTAs (ResNet-50 b1 forward 0.294 vs
+  // 0.307 ms, AlexNet 0.100 vs 0.107, same box); multi-wave layers keep the
+  // wider tile (VGG-16). TRIMS_GEMM_PICK=old keeps the previous rule.
+  static const bool old_rule = [] {
+    const char* e = std::getenv("TRIMS_GEMM_PICK");
+    return e && std::string(e) == "old";
+  }();
+  if (old_rule) return (mt * ((N + 127) / 128) >= uint64_t(sms) / 2 || N <= 128) ? 128 : 64;
+  if (mt * ((N + 63) / 64) <= uint64_t(sms)) return 64;  // 64-wide tiles still fit one wave
+  return (mt * ((N + 127) / 128) >= uint64_t(sms) / 2 || N <= 128) ? 128 : 64;
 }
 
 Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn) {
@@ -399,16 +581,18 @@ Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn) 
   p.K = A.k;
   p.bn = bn;
   p.e = e;
+  if (e.residual) p.tr = residual_map_2d(e, p.M, p.N);
   return p;
 }
 
 void run(const Prepared& p, cudaStream_t stream) {
-  if (p.splits < 1 || p.splits > kMaxSplits || (p.bn / p.splits) % 8)
+  if (p.splits < 1 || p.splits > kMaxSplits || (p.bn / p.splits) % 8 || (p.bn == 256 && p.splits > 1))
     raise(Errc::InvalidArgument, "GEMM split count");
+  const bool split = p.splits > 1;
   switch (p.bn) {
-    case 64: run_bn<64, 6>(p, stream); break;
-    case 128: run_bn<128, 5>(p, stream); break;
-    default: run_bn<256, 3>(p, stream); break;
+    case 64: split ? run_bn<64, 4, true>(p, stream) : run_bn<64, 6, false>(p, stream); break;
+    case 128: split ? run_bn<128, 3, true>(p, stream) : run_bn<128, 5, false>(p, stream); break;
+    default: run_bn<256, 3, false>(p, stream); break;
   }
 }
 
@@ -417,6 +601,7 @@ int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms) {
   // >= 4 k-blocks and every split's column slice of the tile is >= 8 wide.
   const uint64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn), kb = (K + BK - 1) / BK;
   int s = 1;
+  if (bn == 256) return 1;  // no split variant of the widest tile (shared memory)
   // 8 splits only for the tiniest tile counts (<= 8 tiles, e.g. ResNet-50
   // layer3/4 3x3 convs at batch 1); measured slower for 16 tiles (VGG-16
   // conv5), profiles/r03d_split.log.
@@ -475,6 +660,7 @@ Prepared prepare_conv(const void* act, const ConvGeom& g, const Operand& B, cons
   cu_check(r, "cuTensorMapEncodeTiled (conv)");
   p.ta = m;
   p.g = g;
+  if (e.residual) p.tr = residual_map_conv(e, g, p.N);
   return p;
 }
 
@@ -483,3 +669,20 @@ void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t 
 }
 
 }  // namespace trims::gemm
+
+#ifdef TRIMS_GEMM_TRACE
+// Copies out up to `cap` records (16 u64 each) and returns how many CTAs
+// recorded since the last reset; reset != 0 zeroes the counter afterwards.
+extern "C" int trims_debug_gemm_trace(unsigned long long* out, int cap, int reset) {
+  unsigned int n = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&n, trims::gemm::g_gtrace_n, sizeof(n));
+  const int take = int(std::min<unsigned>(n, unsigned(std::min(cap, trims::gemm::kGTCap))));
+  if (out && take) cudaMemcpyFromSymbol(out, trims::gemm::g_gtrace, sizeof(unsigned long long) * trims::gemm::kGTW * size_t(take));
+  if (reset) {
+    unsigned int z = 0;
+    cudaMemcpyToSymbol(trims::gemm::g_gtrace_n, &z, sizeof(z));
+  }
+  return int(n);
+}
+#endif

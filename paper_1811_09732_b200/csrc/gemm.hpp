@@ -49,6 +49,10 @@ int pick_bn(uint64_t M, uint64_t N, int sms);
 // bind time so a forward pass costs only kernel launches).
 struct Prepared {
   CUtensorMap ta, tb;
+  // Residual tile loader (e.residual != nullptr): SWIZZLE_128B boxes of 64
+  // channels x the tile's 128 output rows (2-D rows, or the implicit conv's
+  // Wbox x Hbox pixel block), staged by TMA during the mainloop.
+  CUtensorMap tr;
   uint64_t M{0}, N{0}, K{0};
   int bn{128};
   Epilogue e;
