@@ -62,18 +62,22 @@ constexpr int kTmaThreads = 32 * (kConsumerWarps + 1);
 
 #ifdef TRIMS_TRACE
 // Diagnostic build only (make EXTRA=-DTRIMS_TRACE ...; scripts/transform_trace.py):
-// per CTA [start, first stage ready, last push issued, end, staged bytes, tiles,
-// static bin issued, dynamic tiles taken] (times in %globaltimer ns).
-constexpr int kTraceW = 8;
-__device__ unsigned long long g_ttrace[1024 * kTraceW];
+// one record per CTA launch, appended in start order (so back-to-back
+// launches are all kept): [start, first stage ready, last push issued, end,
+// staged bytes, tiles, static bin issued, dynamic tiles taken, launch ticket
+// base (distinct per launch), blockIdx.x] (times in %globaltimer ns).
+constexpr int kTraceW = 10, kTraceCap = 16384;
+__device__ unsigned long long g_ttrace[kTraceCap * kTraceW];
+__device__ unsigned int g_tslot_n;
+__shared__ unsigned int g_tslot;  // this CTA's record
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-#define TRACE_SET(i, v) (g_ttrace[blockIdx.x * kTraceW + (i)] = (v))
-#define TRACE_MAX(i, v) atomicMax(&g_ttrace[blockIdx.x * kTraceW + (i)], (v))
-#define TRACE_ADD(i, v) (g_ttrace[blockIdx.x * kTraceW + (i)] += (v))
+#define TRACE_SET(i, v) (g_tslot < kTraceCap ? (void)(g_ttrace[g_tslot * kTraceW + (i)] = (v)) : (void)0)
+#define TRACE_MAX(i, v) (g_tslot < kTraceCap ? (void)atomicMax(&g_ttrace[g_tslot * kTraceW + (i)], (v)) : (void)0)
+#define TRACE_ADD(i, v) (g_tslot < kTraceCap ? (void)(g_ttrace[g_tslot * kTraceW + (i)] += (v)) : (void)0)
 #else
 #define TRACE_SET(i, v) ((void)0)
 #define TRACE_MAX(i, v) ((void)0)
@@ -580,6 +584,7 @@ __device__ __forceinline__ void consume_tiles(const uint8_t* ring, uint64_t* ful
   uint32_t bucket = ~0u;  // per-warp checksum accumulator, flushed when the tensor changes
   uint64_t wacc = 0;
   uint32_t s = 0, phase = 0;
+  pdl_wait();  // no write (dst, sums) before the previous grid completes
 #ifdef TRIMS_TRACE
   bool first = true;
 #endif
@@ -720,7 +725,7 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
                                                                     uint32_t stages, uint32_t stage_alloc,
                                                                     unsigned int* __restrict__ sched,
                                                                     uint32_t ticket_base, uint32_t stride,
-                                                                    uint32_t tail0) {
+                                                                    uint32_t tail0, uint32_t early) {
   using ST = typename Bits<S>::T;
   constexpr int DS = esize<D>(), SS = esize<S>(), EPW = 8 / DS;
   constexpr uint32_t kC = kConsumerWarps * 32;  // consumer threads
@@ -742,7 +747,10 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 #ifdef TRIMS_TRACE
+    g_tslot = atomicAdd(&g_tslot_n, 1u);
     TRACE_SET(0, gtimer());
+    TRACE_SET(8, ticket_base);
+    TRACE_SET(9, blockIdx.x);
     TRACE_SET(3, 0);
     TRACE_SET(4, 0);
     TRACE_SET(5, 0);
@@ -752,7 +760,21 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
   __syncthreads();
 
   if (warp == 0) {  // ---------------- producer
-    pdl_wait();
+    // early != 0: the host guarantees no kernel that triggers its dependents
+    // early (a transform, a forward-pass kernel) writes this launch's source
+    // (sources are filled by DMA copies or by non-PDL fill kernels), so the
+    // first ring fill is requested BEFORE griddepcontrol.wait, while the
+    // previous launch drains: consecutive ingests keep HBM busy across the
+    // launch boundary. Everything that writes (consumers: dst, sums) and the
+    // ticket draws still wait for the previous grid.
+    if (!early) pdl_wait();
+    bool gated = !early;
+    auto gate = [&] {
+      if (!gated) {
+        pdl_wait();
+        gated = true;
+      }
+    };
     uint32_t s = 0, round = 0;  // ring slot, and how many times the ring has wrapped
     auto push = [&](const Tile& t) {  // lane 0: stage t's raw bytes into slot s
       if (round) mbar_wait(&empty[s], (round - 1) & 1);
@@ -792,6 +814,7 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
     }
     if (lane == 0) {
       TRACE_SET(6, gtimer());
+      gate();
       if (sched && tail0 < ntiles) {
         // Dynamic part: tiles [tail0, ntiles) handed out by a ticket counter,
         // so CTAs that ran slow take fewer of them. The next ticket and its
@@ -821,7 +844,7 @@ __global__ void __launch_bounds__(kTmaThreads) transform_tma_kernel(const Tile* 
 
 using TransformFn = void (*)(const Tile*, uint32_t, const uint8_t*, uint8_t*, unsigned long long*);
 using TmaFn = void (*)(const Tile*, uint32_t, const uint8_t*, uint8_t*, unsigned long long*, uint32_t, uint32_t,
-                       unsigned int*, uint32_t, uint32_t, uint32_t);
+                       unsigned int*, uint32_t, uint32_t, uint32_t, uint32_t);
 
 TmaFn pair_tma_kernel(int s, int d) {
   switch (s * 8 + d) {
@@ -1245,13 +1268,19 @@ uint32_t launch_groups(const Tile* d_tiles, const std::vector<Group>& groups, co
         const char* e = std::getenv("TRIMS_TRANSFORM_PDL");
         return !(e && std::string(e) == "0");
       }();
+      // Early ring fill (see transform_tma_kernel): transform sources are only
+      // ever written by DMA copies or non-PDL kernels. A/B: TRIMS_TRANSFORM_EARLY=0.
+      static const uint32_t early = [] {
+        const char* e = std::getenv("TRIMS_TRANSFORM_EARLY");
+        return (e && std::string(e) == "0") ? 0u : 1u;
+      }();
       auto go = [&](uint32_t ctas, const unsigned int* sl, uint32_t b, uint32_t stride, uint32_t tail0) {
         if (pdl)
           launch_pdl(fn, dim3(ctas), dim3(kTmaThreads), size_t(smem), st, t, n, src, dst, d_sums, rc.stages,
-                     rc.stage_alloc(), const_cast<unsigned int*>(sl), b, stride, tail0);
+                     rc.stage_alloc(), const_cast<unsigned int*>(sl), b, stride, tail0, early);
         else
           fn<<<ctas, kTmaThreads, smem, st>>>(t, n, src, dst, d_sums, rc.stages, rc.stage_alloc(),
-                                              const_cast<unsigned int*>(sl), b, stride, tail0);
+                                              const_cast<unsigned int*>(sl), b, stride, tail0, 0u);
       };
       if (g.nbins) {  // static schedule: one CTA per bin (+ dynamic tail)
         if (g.tail) take_slot(g.tail, g.nbins, &slot, &base);
@@ -1324,8 +1353,17 @@ void launch_fill_uniform(float* dst, uint64_t n, uint64_t stream_seed, uint64_t 
 }  // namespace trims::ingest
 
 #ifdef TRIMS_TRACE
+// Copies out up to n words (kTraceW = 10 per CTA record) and resets the
+// record counter; returns the number of records since the last reset, or -1.
 extern "C" int trims_debug_transform_trace(unsigned long long* out, int n) {
-  return int(cudaMemcpyFromSymbol(out, trims::ingest::g_ttrace, sizeof(unsigned long long) * size_t(n)));
+  unsigned int recs = 0, zero = 0;
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  cudaMemcpyFromSymbol(&recs, trims::ingest::g_tslot_n, sizeof(recs));
+  const size_t words = std::min<size_t>(size_t(n), size_t(recs) * trims::ingest::kTraceW);
+  if (words && cudaMemcpyFromSymbol(out, trims::ingest::g_ttrace, sizeof(unsigned long long) * words) != cudaSuccess)
+    return -1;
+  cudaMemcpyToSymbol(trims::ingest::g_tslot_n, &zero, sizeof(zero));
+  return int(recs);
 }
 
 __global__ void trims_debug_empty_kernel() {}
