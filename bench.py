@@ -433,17 +433,33 @@ def shared_clients(work: str, arch, dev: int, n_clients: int, n_reqs: int) -> di
     from paper_1811_09732_b200 import catalog as C
     from paper_1811_09732_b200.daemon import serve
     from paper_1811_09732_b200.models import arch_text
-    from paper_1811_09732_b200.sharing import run_daemon_clients
+    from paper_1811_09732_b200.sharing import mps_session, run_daemon_clients
     from paper_1811_09732_b200.store import Store, StoreOptions
 
     opts = StoreOptions(disk_cache_dir=work, fast_capacity_bytes=2 << 30, host_capacity_bytes=1 << 30,
                         convert_to="bf16", permute_4d=True, device=dev, scan_disk=False)
     endpoint = os.path.join(work, "mrmd.sock")
+    key, text = C.arch_key(arch), arch_text(arch)
     with Store(opts) as s, serve(s, endpoint):
-        ex = s.open(C.arch_key(arch))  # loaded once; every client open is a FastHit on this copy
-        r = run_daemon_clients(endpoint, C.arch_key(arch), arch_text(arch), n_clients, n_reqs)
+        ex = s.open(key)  # loaded once; every client open is a FastHit on this copy
+        one = run_daemon_clients(endpoint, key, text, 1, n_reqs)  # the single-client rate
+        # 16 CUDA contexts time-slicing the GPU (no MPS)
+        sliced = run_daemon_clients(endpoint, key, text, n_clients, n_reqs)
+        # the same clients as MPS clients: their kernels run concurrently
+        with mps_session() as env:
+            r = run_daemon_clients(endpoint, key, text, n_clients, n_reqs, env=env) if env else None
         st = s.stats()
-        s.close(C.arch_key(arch))
+        s.close(key)
+    single_rps = one["requests_per_s"]
+    if r is None:
+        r, mps = sliced, "unavailable (no nvidia-cuda-mps-control, or it failed to start)"
+    else:
+        mps = "on (client processes are MPS clients; the store/daemon process is not)"
+        sliced.pop("logits", None)
+        r["without_mps"] = {k: sliced[k] for k in ("p50_ms", "p99_ms", "requests_per_s", "attach_ms_median")}
+    r["mps"] = mps
+    r["single_client_requests_per_s"] = single_rps
+    r["aggregate_over_single_client"] = round(r["requests_per_s"] / single_rps, 2)
     r["transport"] = "v1 wire protocol over a Unix socket (daemon), allocation fd by SCM_RIGHTS"
     logits = r.pop("logits")
     r["identical_logits_across_clients"] = all(np.array_equal(logits[0], l) for l in logits)

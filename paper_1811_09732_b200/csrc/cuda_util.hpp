@@ -1,6 +1,8 @@
 // cuda_util.hpp — error plumbing between the CUDA runtime and trims::Error.
 #pragma once
 
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include <string>
@@ -54,6 +56,18 @@ struct DeviceGuard {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// TRIMS_PDL=0 launches without the attribute (kernels still call
+// griddepcontrol, which is then a no-op): under MPS many clients share the
+// SMs, and CTAs launched early only to sit in griddepcontrol.wait hold SMs
+// another client's kernel could run on.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TRIMS_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args&&... args) {
   cudaLaunchConfig_t cfg{};
@@ -65,7 +79,7 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   TRIMS_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 #endif

@@ -487,8 +487,9 @@ void run_bn(const Prepared& p, cudaStream_t stream) {
   attr[1].val.clusterDim.x = 1;
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = unsigned(p.splits);
+  if (!pdl_enabled()) attr[0] = attr[1];  // keep only the cluster shape
   cfg.attrs = attr;
-  cfg.numAttrs = SPLIT ? 2 : 1;
+  cfg.numAttrs = (SPLIT ? 2 : 1) - (pdl_enabled() ? 0 : 1);
   TRIMS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, SPLIT>, p.ta, p.tb, p.tr, e.out, int(p.M), int(p.N),
                                 int(p.K), int(e.ldo), e.scale, e.bias, e.residual ? 1 : 0, e.relu ? 1 : 0, kper, p.g));
 }

@@ -15,8 +15,13 @@ costs a CUDA context plus its activation workspace.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import multiprocessing as mp
+import os
+import shutil
+import subprocess
+import tempfile
 import time
 from dataclasses import dataclass
 from multiprocessing.reduction import recv_handle, send_handle
@@ -113,20 +118,72 @@ def _client_main(conn, sm: SharedModel, batch: int, n_reqs: int, seed: int) -> N
             conn.close()
 
 
+@contextlib.contextmanager
+def mps_session():
+    """An MPS control daemon for the CLIENT processes (the store process keeps
+    its own context): with MPS the clients' kernels share the GPU
+    concurrently instead of time-slicing 16 contexts. Yields the environment
+    a client needs (pipe / log directories), or None when MPS is not
+    available on this host (no nvidia-cuda-mps-control, or it fails to start;
+    e.g. a GPU in exclusive-process mode owned by another process)."""
+    exe = shutil.which("nvidia-cuda-mps-control")
+    if not exe:
+        yield None
+        return
+    root = tempfile.mkdtemp(prefix="trims-mps-")
+    env = {"CUDA_MPS_PIPE_DIRECTORY": os.path.join(root, "pipe"), "CUDA_MPS_LOG_DIRECTORY": os.path.join(root, "log")}
+    for d in env.values():
+        os.makedirs(d, exist_ok=True)
+    full = {**os.environ, **env}
+    try:
+        started = subprocess.run([exe, "-d"], env=full, timeout=30).returncode == 0
+    except (OSError, subprocess.SubprocessError):
+        started = False
+    if not started:
+        shutil.rmtree(root, ignore_errors=True)
+        yield None
+        return
+    try:
+        yield env
+    finally:
+        try:
+            subprocess.run([exe], input=b"quit\n", env=full, timeout=60)
+        except (OSError, subprocess.SubprocessError):
+            pass
+        shutil.rmtree(root, ignore_errors=True)
+
+
+@contextlib.contextmanager
+def _child_env(env: dict | None):
+    """Environment inherited by processes spawned inside the block."""
+    saved = {k: os.environ.get(k) for k in (env or {})}
+    os.environ.update(env or {})
+    try:
+        yield
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
 def run_daemon_clients(endpoint: str, key, arch_text: str, n_clients: int = 16, n_reqs: int = 20, batch: int = 1,
-                       seed: int = 2, timeout_s: float = 600.0) -> dict:
+                       seed: int = 2, timeout_s: float = 600.0, env: dict | None = None) -> dict:
     """As run_clients, but every client process gets the model from the
-    daemon at `endpoint` (v1 OpenRequest over the socket, fd by SCM_RIGHTS)."""
+    daemon at `endpoint` (v1 OpenRequest over the socket, fd by SCM_RIGHTS).
+    `env` (e.g. mps_session()'s) is set in the clients' environment."""
     ctx = mp.get_context("spawn")
     procs, conns = [], []
-    for i in range(n_clients):
-        parent, child = ctx.Pipe()
-        p = ctx.Process(target=_daemon_client_main,
-                        args=(child, endpoint, (key.ns, key.name, key.version), arch_text, batch, n_reqs, seed),
-                        daemon=True)
-        p.start()
-        procs.append(p)
-        conns.append(parent)
+    with _child_env(env):
+        for i in range(n_clients):
+            parent, child = ctx.Pipe()
+            p = ctx.Process(target=_daemon_client_main,
+                            args=(child, endpoint, (key.ns, key.name, key.version), arch_text, batch, n_reqs, seed),
+                            daemon=True)
+            p.start()
+            procs.append(p)
+            conns.append(parent)
     return _collect(procs, conns, n_clients, batch, timeout_s)
 
 
