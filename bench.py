@@ -514,6 +514,7 @@ def mix_traces(dev: int, rank: int, world: int, n_requests: int = 1000) -> dict:
         info = F.read_manifest(path)
         blob = np.fromfile(path, dtype=np.uint8, count=info.blob_bytes, offset=info.blob_offset)
         d = torch.from_numpy(blob).to(f"cuda:{dev}")
+        torch.cuda.current_stream(dev).synchronize()  # the touch runs on its own stream
         touch(d.data_ptr(), d.numel())
         base[k] = time.perf_counter() - t0
         del d, blob

@@ -44,6 +44,7 @@ def baselines(catalog_dir: str, keys, total_weights: int, device: int = 0, reps:
             info = F.read_manifest(path)
             blob = np.fromfile(path, dtype=np.uint8, count=info.blob_bytes, offset=info.blob_offset)
             d = torch.from_numpy(blob).to(f"cuda:{device}")
+            torch.cuda.current_stream(device).synchronize()  # the touch runs on its own stream
             touch(d.data_ptr(), d.numel())
             ts.append(time.perf_counter() - t0)
         base[k] = W.percentile(ts, 50)

@@ -105,13 +105,20 @@ class DeviceTouch:
         import torch
         self.torch = torch
         self.out = torch.zeros(1, dtype=torch.int64, device=f"cuda:{device}")
-        self.stream = torch.cuda.current_stream(device)
+        self.host = torch.zeros(1, dtype=torch.int64).pin_memory()
+        # a stream of its own: concurrent workers (grid.py threads) must not
+        # queue behind each other's kernels and synchronisations on one stream
+        self.stream = torch.cuda.Stream(device)
 
     def __call__(self, dev_ptr: int, nbytes: int) -> int:
-        self.out.zero_()
-        check(lib.trims_checksum_device(ctypes.c_void_p(dev_ptr), nbytes, 0, ctypes.c_void_p(self.out.data_ptr()),
-                                        ctypes.c_void_p(self.stream.cuda_stream)))
-        return int(self.out.item()) & _M64  # .item() synchronises: the request includes the kernel
+        with self.torch.cuda.stream(self.stream):
+            self.out.zero_()
+            check(lib.trims_checksum_device(ctypes.c_void_p(dev_ptr), nbytes, 0,
+                                            ctypes.c_void_p(self.out.data_ptr()),
+                                            ctypes.c_void_p(self.stream.cuda_stream)))
+            self.host.copy_(self.out, non_blocking=True)
+        self.stream.synchronize()  # the request includes the kernel
+        return int(self.host.item()) & _M64
 
 
 def run_trace(store, keys: list[F.ModelKey], trace: list[int], device: int = 0, private_baseline: dict | None = None,

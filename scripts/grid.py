@@ -1,5 +1,5 @@
-"""The oversubscription grid on the tiny catalog:
-    python scripts/grid.py [out.json] [requests]"""
+"""The oversubscription grid on the tiny or the full small37
+catalog: python scripts/grid.py [out.json] [requests] [tiny|small37]"""
 import json
 import os
 import sys
@@ -13,13 +13,14 @@ from paper_1811_09732_b200.grid import run_grid
 
 out = sys.argv[1] if len(sys.argv) > 1 else None
 reqs = int(sys.argv[2]) if len(sys.argv) > 2 else 400
-models, div = C.catalog("tiny")
+cat = sys.argv[3] if len(sys.argv) > 3 else "tiny"
+models, div = C.catalog(cat)
 keys = [C.catalog_key(m) for m in models]
 total = sum(C.scaled_weights_bytes(m, div) for m in models)
 d = tempfile.mkdtemp()
-C.gen_catalog("tiny", d, seed=1)
+C.gen_catalog(cat, d, seed=1)
 res = run_grid(d, keys, total, requests=reqs)
-res["catalog"] = "tiny (small37 / 64), seed 1"
+res["catalog"] = ("tiny (small37 / 64)" if cat == "tiny" else cat) + ", seed 1"
 txt = json.dumps(res, indent=1)
 print(txt)
 if out:
