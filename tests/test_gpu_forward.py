@@ -10,7 +10,7 @@ Tolerances (stated here, per north_star's "within a stated fp tolerance"):
   previous layers' device outputs, read through ``trims_net_tap``) and compared
   with the device's output:
   - bf16 outputs: every element within ONE bf16 ulp of the oracle
-    (|d| <= ulp(max(|a|, |b|)) + 2^-20 * max|layer|, the absolute floor covering
+    (|d| <= ulp(max(|a|, |b|)) + 2^-16 * max|layer|, the absolute floor covering
     values that cancel to ~0), and at most 0.2 % of the elements not
     bit-identical. A 1-ulp flip happens only where the device's fp32 summation
     order lands the accumulator across a bf16 rounding boundary: measured on
