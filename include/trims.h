@@ -317,6 +317,13 @@ int trims_fill_uniform_device(float* dev, uint64_t n, uint64_t stream_seed, uint
 int trims_gemm_bf16(const void* A, uint64_t M, uint64_t K, uint64_t lda, const void* B, uint64_t N, uint64_t ldb,
                     void* D, uint64_t ldd, const float* scale, const float* bias, const void* residual, uint64_t ldr,
                     int relu, int bn, void* stream);
+/* The same with an explicit split-K count: splits = 1, 2, 4 or 8 (the S
+ * splits of an output tile run as one thread-block cluster and reduce their
+ * fp32 partials in split order through distributed shared memory), or 0 to
+ * pick it as the network executor does. */
+int trims_gemm_bf16_split(const void* A, uint64_t M, uint64_t K, uint64_t lda, const void* B, uint64_t N,
+                          uint64_t ldb, void* D, uint64_t ldd, const float* scale, const float* bias,
+                          const void* residual, uint64_t ldr, int relu, int bn, int splits, void* stream);
 
 /* The compute on shared weights (replaces Client::touch, client.cpp:338-359):
  * a CNN bound to a resident manifest whose bf16 KRSC weights start at

@@ -1087,6 +1087,17 @@ int trims_gemm_bf16(const void* A, uint64_t M, uint64_t K, uint64_t lda, const v
   });
 }
 
+int trims_gemm_bf16_split(const void* A, uint64_t M, uint64_t K, uint64_t lda, const void* B, uint64_t N,
+                          uint64_t ldb, void* D, uint64_t ldd, const float* scale, const float* bias,
+                          const void* residual, uint64_t ldr, int relu, int bn, int splits, void* stream) {
+  return guard([&] {
+    gemm::Epilogue e{static_cast<uint16_t*>(D), ldd, scale, bias, static_cast<const uint16_t*>(residual), ldr,
+                     relu != 0};
+    gemm::launch({A, M, K, lda}, {B, N, K, ldb}, e, static_cast<cudaStream_t>(stream), bn, splits);
+    return 0;
+  });
+}
+
 struct trims_net {
   std::unique_ptr<nn::Net> net;
 };

@@ -63,36 +63,48 @@ __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v 
 
 // Shared-memory plan of one CTA: the TMA ring, the residual tile (staged by
 // TMA in SWIZZLE_128B boxes of 64 channels x 128 rows), for split-K launches
-// the receive buffer of this CTA's column slice, then folded-BN scale/bias.
-template <int BN, int STAGES, bool SPLIT>
+// the receive buffer (S partial blocks of this CTA's column slice), then
+// folded-BN scale/bias.
+template <int BN, int STAGES, int S>
 struct Smem {
   static constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t RING = STAGES * STAGE_BYTES;
   // split-K: only the 64-channel box holding this CTA's slice
-  static constexpr uint32_t RES = RING, RES_BYTES = SPLIT ? BM * 128 : BM * BN * 2;
-  // split z's partial of slice j lands at recv[z][row][0..cw) of CTA j;
-  // rows padded by 16 B so v4 accesses of 8 consecutive rows hit 8 bank groups
-  static constexpr uint32_t RECV = RES + RES_BYTES, RECV_BYTES = SPLIT ? BM * 4 * (BN + 4 * kMaxSplits) : 0;
+  static constexpr uint32_t RES = RING, RES_BYTES = S > 1 ? BM * 128 : BM * BN * 2;
+  // split z's partial of slice j (<= 128 rows x BN/S fp32) lands in block z of CTA j
+  static constexpr uint32_t RECV = RES + RES_BYTES, RECV_BYTES = S > 1 ? BM * BN * 4 : 0;
   static constexpr uint32_t SCALE = RECV + RECV_BYTES, BIAS = SCALE + BN * 4;
   static constexpr uint32_t TOTAL = BIAS + BN * 4 + 1024;  // + 1 KiB realignment slack
   // split-K: the idle ring holds the outgoing partial blocks
-  static_assert(!SPLIT || RING >= BM * 4 * (BN + 4 * kMaxSplits), "split-K outgoing blocks exceed the ring");
+  static_assert(S == 1 || RING >= BM * BN * 4, "split-K outgoing blocks exceed the ring");
 };
 
-// SPLIT = false: one CTA per output tile. SPLIT = true: grid.z = S splits of
-// K, the S CTAs of a tile form one (1, 1, S) cluster; split z owns output
-// columns [z*BN/S, (z+1)*BN/S) of the tile. Every split pushes each owner its
-// fp32 partial of that owner's slice straight from TMEM into the owner's
-// shared memory (st.async, completing bytes on the owner's mbarrier), so
-// nobody waits on a remote load; an owner sums the S partials in split order
-// (deterministic) and runs the epilogue of its slice.
-template <int BN, int STAGES, bool SPLIT>
+// S = 1: one CTA per output tile. S > 1: grid.z = S splits of K, the S CTAs
+// of a tile form one (1, 1, S) cluster and split z owns output columns
+// [z*CW, (z+1)*CW), CW = BN / S. Measured building blocks in one 8-CTA
+// cluster (scripts/dsmem_bench.cu, profiles/r3/dsmem_bench.jsonl): a relaxed
+// cluster barrier 124 cycles, a release/acquire one after global stores
+// ~1000 (it drains the stores), tcgen05.ld x16 x2 25 cycles, per-thread
+// remote stores (st.async) ~245 cycles EACH (serialised), per-thread remote
+// loads worse, and bulk DSMEM copies the cheapest way to move a block. So:
+// every split parks its partial of each owner's slice in its (idle) ring as
+// one compact block (only the tile's valid rows, chunk-major: [CW/4][rows][4]
+// floats, conflict-free for both sides), S-1 warps each ship one block with
+// one bulk copy completing bytes on the owner's mbarrier, the owner sums the
+// S partials in split order (deterministic) and stores its slice to global
+// straight from registers. A relaxed cluster barrier (arrive once my inputs
+// have landed, wait at exit) keeps every source alive until its blocks are
+// read.
+template <int BN, int STAGES, int S>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmR, uint16_t* D, int M, int N, int K, int ldd,
                    const float* __restrict__ scale, const float* __restrict__ bias, int has_res, int relu, int kper,
                    const ConvGeom cg) {
-  using L = Smem<BN, STAGES, SPLIT>;
+  constexpr bool SPLIT = S > 1;
+  constexpr int CW = BN / S;  // split-K: columns of the slice this CTA owns
+  static_assert(CW % 8 == 0, "split slices are >= 8 columns");
+  using L = Smem<BN, STAGES, S>;
   constexpr uint32_t TMEM_COLS = BN;  // 64 / 128 / 256: powers of two >= 32
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], accum_full, res_full, recv_full;
@@ -101,19 +113,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   // pointer arithmetic (an integer round trip would drop the shared address
   // space and turn every epilogue smem access into a generic load)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  float* s_recv = reinterpret_cast<float*>(smem + L::RECV);
   float* s_scale = reinterpret_cast<float*>(smem + L::SCALE);
   float* s_bias = reinterpret_cast<float*>(smem + L::BIAS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  const int splits = SPLIT ? int(gridDim.z) : 1, z = SPLIT ? int(blockIdx.z) : 0;
-  const int cw = BN / splits;  // split-K: this CTA's column slice [z*cw, (z+1)*cw)
-  const int rstride = cw + 4;  // receive-buffer row stride (floats)
+  const int z = SPLIT ? int(blockIdx.z) : 0;
   const int kblocks = (K + BK - 1) / BK;
   const int kb0 = z * kper, kb1 = min(kblocks, kb0 + kper);  // this split's k-blocks
   // residual boxes staged: all BN/64 of the tile, or the one holding the slice
-  const int rbox0 = SPLIT ? (z * cw) / 64 : 0, rboxes = SPLIT ? 1 : (BN + 63) / 64;
+  const int rbox0 = SPLIT ? (z * CW) / 64 : 0, rboxes = SPLIT ? 1 : (BN + 63) / 64;
   // Implicit conv: this tile = image ti, output rows [th*hbox, +hbox), cols [tw*wbox, +wbox).
   int ti = 0, th = 0, tw = 0;
   if (cg.impl) {
@@ -128,6 +137,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int h = th * cg.hbox + (rl >> cg.wbox_log2), w = tw * wbox + (rl & (wbox - 1));
     return (h < cg.P && w < cg.Q) ? (ti * cg.P + h) * cg.Q + w : -1;
   };
+  // Valid rows of the tile (hv x qv box of the output; qv = 1 for a plain
+  // GEMM) and tile row -> compact index among them (-1 if outside).
+  const int hv = cg.impl ? min(cg.hbox, cg.P - th * cg.hbox) : min(BM, M - m0);
+  const int qv = cg.impl ? min(wbox, cg.Q - tw * wbox) : 1;
+  const int nvalid = hv * qv;
+  auto cidx = [&](int rl) -> int {
+    if (!cg.impl) return rl < hv ? rl : -1;
+    const int hr = rl >> cg.wbox_log2, wc = rl & (wbox - 1);
+    return (hr < hv && wc < qv) ? hr * qv + wc : -1;
+  };
   // Epilogue of CW (8 or 16) tile columns c0.. of tile row rl: scale, bias,
   // residual, ReLU, bf16 -> back into the staging tile (the residual's
   // swizzled smem box, in place: each 16-byte chunk is read and rewritten by
@@ -141,35 +160,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int box = c / 64 - rbox0, chunk = ((c & 63) >> 3) ^ (rl & 7);
     return s_out + box * BM * 64 + rl * 64 + chunk * 8;
   };
-  auto finish = [&](int rl, int c0, auto cw_tag, const float* v) {
-    constexpr int CW = decltype(cw_tag)::value;
+  // scale, bias, residual, ReLU of 8 values at tile column c of row rl -> 4 bf16 pairs
+  auto epi8 = [&](int rl, int c, const float* v, uint32_t* o) {
+    const uint4 r4 = has_res ? *reinterpret_cast<const uint4*>(stage_at(rl, c)) : make_uint4(0, 0, 0, 0);
+    const uint32_t rw[4] = {r4.x, r4.y, r4.z, r4.w};
+    const float4 sc0 = *reinterpret_cast<const float4*>(s_scale + c);
+    const float4 sc1 = *reinterpret_cast<const float4*>(s_scale + c + 4);
+    const float4 bi0 = *reinterpret_cast<const float4*>(s_bias + c);
+    const float4 bi1 = *reinterpret_cast<const float4*>(s_bias + c + 4);
+    const float sc[8] = {sc0.x, sc0.y, sc0.z, sc0.w, sc1.x, sc1.y, sc1.z, sc1.w};
+    const float bi[8] = {bi0.x, bi0.y, bi0.z, bi0.w, bi1.x, bi1.y, bi1.z, bi1.w};
 #pragma unroll
-    for (int q = 0; q < CW / 8; ++q) {
-      uint4* sp = reinterpret_cast<uint4*>(stage_at(rl, c0 + 8 * q));
-      const uint4 r4 = has_res ? *sp : make_uint4(0, 0, 0, 0);
-      const uint32_t rw[4] = {r4.x, r4.y, r4.z, r4.w};
-      const float4 sc0 = *reinterpret_cast<const float4*>(s_scale + c0 + 8 * q);
-      const float4 sc1 = *reinterpret_cast<const float4*>(s_scale + c0 + 8 * q + 4);
-      const float4 bi0 = *reinterpret_cast<const float4*>(s_bias + c0 + 8 * q);
-      const float4 bi1 = *reinterpret_cast<const float4*>(s_bias + c0 + 8 * q + 4);
-      const float sc[8] = {sc0.x, sc0.y, sc0.z, sc0.w, sc1.x, sc1.y, sc1.z, sc1.w};
-      const float bi[8] = {bi0.x, bi0.y, bi0.z, bi0.w, bi1.x, bi1.y, bi1.z, bi1.w};
-      uint32_t o[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float a = v[8 * q + 2 * j] * sc[2 * j] + bi[2 * j];
-        float b = v[8 * q + 2 * j + 1] * sc[2 * j + 1] + bi[2 * j + 1];
-        if (has_res) {
-          a += bf16_lo(rw[j]);
-          b += bf16_hi(rw[j]);
-        }
-        if (relu) {
-          a = fmaxf(a, 0.f);
-          b = fmaxf(b, 0.f);
-        }
-        o[j] = pack_bf16x2(a, b);
+    for (int j = 0; j < 4; ++j) {
+      float a = v[2 * j] * sc[2 * j] + bi[2 * j];
+      float b = v[2 * j + 1] * sc[2 * j + 1] + bi[2 * j + 1];
+      if (has_res) {
+        a += bf16_lo(rw[j]);
+        b += bf16_hi(rw[j]);
       }
-      *sp = make_uint4(o[0], o[1], o[2], o[3]);
+      if (relu) {
+        a = fmaxf(a, 0.f);
+        b = fmaxf(b, 0.f);
+      }
+      o[j] = pack_bf16x2(a, b);
+    }
+  };
+  auto finish = [&](int rl, int c0, auto cw_tag, const float* v) {
+    constexpr int W = decltype(cw_tag)::value;
+#pragma unroll
+    for (int q = 0; q < W / 8; ++q) {
+      uint32_t o[4];
+      epi8(rl, c0 + 8 * q, v + 8 * q, o);
+      *reinterpret_cast<uint4*>(stage_at(rl, c0 + 8 * q)) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  };
+  // 8 finished columns of tile row rl -> D (one 16-byte store when aligned)
+  auto store8 = [&](int row, int n, const uint32_t* o) {
+    uint16_t* dp = D + size_t(row) * ldd + n;
+    if (ldd % 8 == 0 && n + 8 <= N) {
+      *reinterpret_cast<uint4*>(dp) = make_uint4(o[0], o[1], o[2], o[3]);
+    } else {
+      for (int j = 0; j < 8 && n + j < N; ++j) dp[j] = uint16_t(o[j >> 1] >> (16 * (j & 1)));
     }
   };
   // Staged tile columns [cbeg, cbeg + W) -> D, row-major: consecutive
@@ -182,13 +213,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = row_of(rl), n = n0 + c;
       if (row < 0 || n >= N) continue;
       const uint4 v = *reinterpret_cast<const uint4*>(stage_at(rl, c));
-      uint16_t* dp = D + size_t(row) * ldd + n;
-      if (ldd % 8 == 0 && n + 8 <= N) {
-        *reinterpret_cast<uint4*>(dp) = v;
-      } else {
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-        for (int j = 0; j < 8 && n + j < N; ++j) dp[j] = uint16_t(w[j >> 1] >> (16 * (j & 1)));
-      }
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      store8(row, n, w);
     }
   };
   auto load_a = [&](void* dst, int kb, uint64_t* bar) {
@@ -225,8 +251,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     if (has_res) prefetch_tmap(&tmR);
-    // the other splits' partials of this CTA's slice, in bytes
-    if (SPLIT) mbar_expect_tx(&recv_full, uint32_t((splits - 1) * BM * (cw + 4) * 4));
+    // the other splits' blocks of this CTA's slice, in bytes
+    if (SPLIT) mbar_expect_tx(&recv_full, uint32_t((S - 1) * nvalid * CW * 4));
   }
   if (warp == 1) tmem_alloc<TMEM_COLS>(&tmem_base);
   tc_fence_before();
@@ -235,7 +261,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_trigger();  // the next layer's CTAs may start their prologue now
   // every split's receive barrier is initialised before anyone pushes into it
   // (off the critical path: this runs under the previous layer's tail)
-  if (SPLIT) cluster_sync();
+  if (SPLIT) {
+    cluster_arrive_relaxed();
+    cluster_wait();
+  }
   const uint32_t tmem = tmem_base;
 
   if (warp == 0) {
@@ -312,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 128) GT_SET(gt_slot, 5, gtimer());
 #endif
     tc_fence_after();
-    if (!SPLIT) {
+    if constexpr (!SPLIT) {
       asm volatile("bar.sync 1, 320;" ::: "memory");  // scale / bias in smem
       if (has_res) mbar_wait(&res_full, 0);
 #ifdef TRIMS_GEMM_TRACE
@@ -322,27 +351,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
         uint32_t r[32];
-#ifdef TRIMS_GEMM_TRACE
-        const long long k0 = clock64();
-#endif
         tmem_ld16_nw(tq + uint32_t(c0), r);
         tmem_ld16_nw(tq + uint32_t(c0 + 16), r + 16);
         tmem_wait_ld();
-#ifdef TRIMS_GEMM_TRACE
-        const long long k1 = clock64();
-#endif
         finish(rl, c0, std::integral_constant<int, 16>{}, reinterpret_cast<const float*>(r));
         finish(rl, c0 + 16, std::integral_constant<int, 16>{}, reinterpret_cast<const float*>(r + 16));
-#ifdef TRIMS_GEMM_TRACE
-        if (threadIdx.x == 128 && c0 == 0) GT_SET(gt_slot, 13, uint64_t(clock64() - k1));
-        if (c0 == 0 && !has_res) {  // diagnostic: the same work again, now with warm instruction caches
-          const long long k2 = clock64();
-          finish(rl, c0, std::integral_constant<int, 16>{}, reinterpret_cast<const float*>(r));
-          finish(rl, c0 + 16, std::integral_constant<int, 16>{}, reinterpret_cast<const float*>(r + 16));
-          if (threadIdx.x == 128) GT_SET(gt_slot, 14, uint64_t(clock64() - k2));
-        }
-        if (threadIdx.x == 128 && c0 == 0) GT_SET(gt_slot, 15, uint64_t(k1 - k0));
-#endif
       }
       asm volatile("bar.sync 2, 256;" ::: "memory");  // the whole tile is staged
       copy_out(threadIdx.x - 128, 0, BN);
@@ -350,92 +363,97 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (threadIdx.x == 128) GT_SET(gt_slot, 10, gtimer());
 #endif
     } else {
-      // A split can own no k-blocks (ceil(kblocks / splits) * (splits - 1)
-      // >= kblocks): no MMA wrote its accumulator, so its partial is zero.
-      const bool no_k = kb0 >= kb1;
-      const uint32_t recv_local = smem_u32(s_recv), bar_local = smem_u32(&recv_full);
-      // push: slice j of this row -> row rl of block j of the outgoing buffer
-      // (the ring, idle once the accumulator is complete), or straight into
-      // my own receive slot z for my own slice; the two warps of a lane
-      // quarter take alternate owners, one TMEM round trip per owner. Then
-      // one thread ships each block to its owner with one bulk copy (DSMEM
-      // through the copy engine; per-thread remote stores measured ~100-400
-      // cycles each).
-      float* s_out32 = reinterpret_cast<float*>(smem);  // [splits][BM][rstride]
-#pragma unroll 1
-      for (int j = half; j < splits; j += 2) {
-        uint32_t r[64];
-        if (no_k) {
+      // This warp's half of the accumulator row in one TMEM round trip. A
+      // split can own no k-blocks (ceil(kblocks / S) * (S - 1) >= kblocks):
+      // no MMA wrote its accumulator, so its partial is zero.
+      constexpr int HC = BN / 2;
+      uint32_t r[HC];
+      if (kb0 >= kb1) {
 #pragma unroll
-          for (int u = 0; u < 64; ++u) r[u] = 0u;
-        } else {
-          if (cw == 8) tmem_ld8_nw(tq + uint32_t(j * cw), r);
+        for (int u = 0; u < HC; ++u) r[u] = 0u;
+      } else {
 #pragma unroll
-          for (int c = 0; c < 64; c += 16)
-            if (c < cw && cw >= 16) tmem_ld16_nw(tq + uint32_t(j * cw + c), r + c);
-          tmem_wait_ld();
-        }
-        float4* p = reinterpret_cast<float4*>((j == z ? s_recv : s_out32) + ((j * BM) + rl) * rstride);
-#pragma unroll
-        for (int c = 0; c < 64; c += 4)
-          if (c < cw)
-            p[c / 4] = make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]), __uint_as_float(r[c + 2]),
-                                   __uint_as_float(r[c + 3]));
+        for (int c = 0; c < HC; c += 16) tmem_ld16_nw(tq + uint32_t(half * HC + c), r + c);
+        tmem_wait_ld();
       }
+      // park: column group c (4 floats) of owner j -> block j, chunk (c % CW) / 4,
+      // compact row; my own slice goes straight into my receive block z
+      const uint32_t blk = uint32_t(nvalid) * CW * 4;
+      const int ci = cidx(rl);
+      if (ci >= 0) {
+#pragma unroll
+        for (int c = 0; c < HC; c += 4) {
+          const int col = half * HC + c, j = col / CW, kk = (col % CW) / 4;
+          uint8_t* base = j == z ? smem + L::RECV + uint32_t(z) * blk : smem + uint32_t(j) * blk;
+          *reinterpret_cast<float4*>(base + (uint32_t(kk) * nvalid + ci) * 16) =
+              make_float4(__uint_as_float(r[c]), __uint_as_float(r[c + 1]), __uint_as_float(r[c + 2]),
+                          __uint_as_float(r[c + 3]));
+        }
+      }
+#ifdef TRIMS_GEMM_TRACE
+      if (threadIdx.x == 128) GT_SET(gt_slot, 14, gtimer());
+#endif
       fence_proxy_async_smem();
       asm volatile("bar.sync 2, 256;" ::: "memory");  // all outgoing blocks written
-      if (threadIdx.x == 128) {
-        const uint32_t block = uint32_t(BM * rstride * 4);
-#pragma unroll 1
-        for (int j = 0; j < splits; ++j)
-          if (j != z)
-            bulk_copy_to_cluster(map_shared_rank(recv_local + uint32_t(z) * block, uint32_t(j)),
-                                 smem_u32(s_out32) + uint32_t(j) * block, block,
-                                 map_shared_rank(bar_local, uint32_t(j)));
+#ifdef TRIMS_GEMM_TRACE
+      if (threadIdx.x == 128) GT_SET(gt_slot, 15, gtimer());
+#endif
+      // warp 4 + i ships block (z + 1 + i) % S: S - 1 bulk copies issued in parallel
+      if (lane == 0 && warp - 4 < S - 1) {
+        const uint32_t j = uint32_t(z + 1 + warp - 4) % S;
+        bulk_copy_to_cluster(map_shared_rank(smem_u32(smem + L::RECV) + uint32_t(z) * blk, j),
+                             smem_u32(smem) + j * blk, blk, map_shared_rank(smem_u32(&recv_full), j));
       }
 #ifdef TRIMS_GEMM_TRACE
       if (threadIdx.x == 128) GT_SET(gt_slot, 11, gtimer());
 #endif
-      // every other split's partial of my slice has landed (bulk-copied data
-      // is visible to the observers of its mbarrier's phase completion, like
-      // a TMA load's: no cluster-scope acquire, which would invalidate L1 on
-      // every poll)
+      // every other split's block of my slice has landed (bulk-copied data is
+      // visible to the observers of its mbarrier's phase completion, like a
+      // TMA load's); from here on nobody reads my outgoing blocks but me...
       mbar_wait(&recv_full, 0);
+      // ...and my peers' blocks are read: they may leave once all owners say so
+      cluster_arrive_relaxed();
 #ifdef TRIMS_GEMM_TRACE
       if (threadIdx.x == 128) GT_SET(gt_slot, 12, gtimer());
 #endif
       asm volatile("bar.sync 1, 320;" ::: "memory");  // scale / bias in smem; own partials written
       if (has_res) mbar_wait(&res_full, 0);
-      // reduce this warp's part of the slice: v = p0 + p1 + ... in split
-      // order (deterministic); a slice of 8 columns is one warp's
-      const int hw = cw >= 16 ? cw / 2 : cw, cbeg = cw >= 16 ? half * hw : 0;
-      if (cw >= 16 || half == 0) {
-#pragma unroll 1
-        for (int c = cbeg; c < cbeg + hw; c += 8) {
+      // reduce: thread t takes tile row t % 128 and 8-column groups t / 128,
+      // + 2, ... of the slice; v = p0 + p1 + ... in split order (deterministic)
+      const int t = threadIdx.x - 128, rr = t & (BM - 1), cr = cidx(rr), row = row_of(rr);
+      const uint8_t* recv = smem + L::RECV;
+      if (cr >= 0) {
+#pragma unroll
+        for (int g = t >> 7; g < CW / 8; g += 2) {
           float v[8];
 #pragma unroll
-          for (int zz = 0; zz < kMaxSplits; ++zz) {
-            if (zz < splits) {
-              const float4* p = reinterpret_cast<const float4*>(s_recv + ((zz * BM) + rl) * rstride + c);
-              const float4 a = p[0], b = p[1];
-              const float pv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+          for (int zz = 0; zz < S; ++zz) {
+            const float4 a = *reinterpret_cast<const float4*>(recv + zz * blk + (uint32_t(2 * g) * nvalid + cr) * 16);
+            const float4 b =
+                *reinterpret_cast<const float4*>(recv + zz * blk + (uint32_t(2 * g + 1) * nvalid + cr) * 16);
+            const float pv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-              for (int u = 0; u < 8; ++u) v[u] = zz ? v[u] + pv[u] : pv[u];
-            }
+            for (int u = 0; u < 8; ++u) v[u] = zz ? v[u] + pv[u] : pv[u];
           }
-          finish(rl, z * cw + c, std::integral_constant<int, 8>{}, v);
+          const int c = z * CW + 8 * g;
+          if (n0 + c < N) {
+            uint32_t o[4];
+            epi8(rr, c, v, o);
+            store8(row, n0 + c, o);
+          }
         }
       }
-      asm volatile("bar.sync 2, 256;" ::: "memory");  // the slice is staged
-      copy_out(threadIdx.x - 128, z * cw, cw);
 #ifdef TRIMS_GEMM_TRACE
       if (threadIdx.x == 128) GT_SET(gt_slot, 13, gtimer());
 #endif
     }
   }
   // split-K: no CTA leaves while a bulk copy may still be reading its
-  // outgoing blocks (every owner has received all its bytes past this point)
-  if (SPLIT) cluster_sync();
+  // outgoing blocks (every owner arrived after receiving all its bytes)
+  if constexpr (SPLIT) {
+    if (warp < 4) cluster_arrive_relaxed();
+    cluster_wait();
+  }
   tc_fence_before();
   __syncthreads();
 #ifdef TRIMS_GEMM_TRACE
@@ -460,20 +478,20 @@ EncodeTiled encode_fn() {
   return fn;
 }
 
-template <int BN, int STAGES, bool SPLIT>
+template <int BN, int STAGES, int S>
 void run_bn(const Prepared& p, cudaStream_t stream) {
-  constexpr size_t smem = Smem<BN, STAGES, SPLIT>::TOTAL;
+  constexpr size_t smem = Smem<BN, STAGES, S>::TOTAL;
   static_assert(smem <= 227 * 1024, "GEMM shared memory");
   static bool smem_set = false;
   if (!smem_set) {
-    TRIMS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TRIMS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(smem)));
     smem_set = true;
   }
   const Epilogue& e = p.e;
   const int kblocks = int((p.K + BK - 1) / BK);
-  const int kper = (kblocks + p.splits - 1) / p.splits;
-  dim3 grid(unsigned(tile_rows(p) / BM), unsigned((p.N + BN - 1) / BN), unsigned(p.splits));
+  const int kper = (kblocks + S - 1) / S;
+  dim3 grid(unsigned(tile_rows(p) / BM), unsigned((p.N + BN - 1) / BN), unsigned(S));
   // PDL always; split-K launches the splits of a tile as one (1, 1, S) cluster
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
@@ -486,11 +504,11 @@ void run_bn(const Prepared& p, cudaStream_t stream) {
   attr[1].id = cudaLaunchAttributeClusterDimension;
   attr[1].val.clusterDim.x = 1;
   attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = unsigned(p.splits);
+  attr[1].val.clusterDim.z = unsigned(S);
   if (!pdl_enabled()) attr[0] = attr[1];  // keep only the cluster shape
   cfg.attrs = attr;
-  cfg.numAttrs = (SPLIT ? 2 : 1) - (pdl_enabled() ? 0 : 1);
-  TRIMS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, SPLIT>, p.ta, p.tb, p.tr, e.out, int(p.M), int(p.N),
+  cfg.numAttrs = (S > 1 ? 2 : 1) - (pdl_enabled() ? 0 : 1);
+  TRIMS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, S>, p.ta, p.tb, p.tr, e.out, int(p.M), int(p.N),
                                 int(p.K), int(e.ldo), e.scale, e.bias, e.residual ? 1 : 0, e.relu ? 1 : 0, kper, p.g));
 }
 
@@ -587,13 +605,19 @@ Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn) 
 }
 
 void run(const Prepared& p, cudaStream_t stream) {
-  if (p.splits < 1 || p.splits > kMaxSplits || (p.bn / p.splits) % 8 || (p.bn == 256 && p.splits > 1))
+  if (p.splits < 1 || p.splits > kMaxSplits || (p.splits & (p.splits - 1)) || (p.bn / p.splits) % 8 ||
+      (p.bn == 256 && p.splits > 1))
     raise(Errc::InvalidArgument, "GEMM split count");
-  const bool split = p.splits > 1;
-  switch (p.bn) {
-    case 64: split ? run_bn<64, 4, true>(p, stream) : run_bn<64, 6, false>(p, stream); break;
-    case 128: split ? run_bn<128, 3, true>(p, stream) : run_bn<128, 5, false>(p, stream); break;
-    default: run_bn<256, 3, false>(p, stream); break;
+  switch (p.bn * 16 + p.splits) {
+    case 64 * 16 + 1: run_bn<64, 6, 1>(p, stream); break;
+    case 64 * 16 + 2: run_bn<64, 6, 2>(p, stream); break;
+    case 64 * 16 + 4: run_bn<64, 6, 4>(p, stream); break;
+    case 64 * 16 + 8: run_bn<64, 6, 8>(p, stream); break;
+    case 128 * 16 + 1: run_bn<128, 5, 1>(p, stream); break;
+    case 128 * 16 + 2: run_bn<128, 4, 2>(p, stream); break;
+    case 128 * 16 + 4: run_bn<128, 4, 4>(p, stream); break;
+    case 128 * 16 + 8: run_bn<128, 4, 8>(p, stream); break;
+    default: run_bn<256, 3, 1>(p, stream); break;
   }
 }
 
@@ -665,8 +689,16 @@ Prepared prepare_conv(const void* act, const ConvGeom& g, const Operand& B, cons
   return p;
 }
 
-void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn) {
-  run(prepare(A, B, e, bn), stream);
+void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn, int splits) {
+  Prepared p = prepare(A, B, e, bn);
+  if (splits == 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    splits = pick_splits(tile_rows(p), p.N, p.K, p.bn, sms);
+  }
+  p.splits = splits;
+  run(p, stream);
 }
 
 }  // namespace trims::gemm

@@ -69,7 +69,8 @@ uint64_t tile_rows(const Prepared& p);
 void run(const Prepared& p, cudaStream_t stream);
 // Split count for a GEMM shape on `sms` SMs.
 int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms);
-// D = epi(A . B^T); bn = 0 picks the tile width.
-void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn = 0);
+// D = epi(A . B^T); bn = 0 picks the tile width; splits = split-K count
+// (1, 2, 4, 8; 0 picks it as the executor does).
+void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn = 0, int splits = 1);
 
 }  // namespace trims::gemm

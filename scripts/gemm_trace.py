@@ -91,9 +91,17 @@ with Store(StoreOptions(disk_cache_dir=d, fast_capacity_bytes=4 << 30, host_capa
                       "span_us": round((prev_end - t0) / 1e3, 2)}))
     for r in out:
         print(json.dumps(r))
-    # split launches: push-phase cycles (TMEM loads, remote stores) of thread 128
+    # per-CTA phase durations (median over the launch's CTAs, µs): split
+    # launches mma | stage partials | bar | bulk issue | recv wait | reduce+store | tail
     for g in groups:
         R = np.array(g["rows"])
+        med = lambda a, b: round(float(np.median(R[:, b] - R[:, a])) / 1e3, 3)
+        sig = [int(R[0, 0] >> 32), int(R[0, 0] & 0xffffffff), int(R[0, 1] >> 32)]
         if (R[:, 1] >> 16 & 0xffff).max() > 0:
-            print(json.dumps({"split_push": [int(R[0, 0] >> 32), int(R[0, 0] & 0xffffffff), int(R[0, 1] >> 32)],
-                              "ldtm_cyc_med": float(np.median(R[:, 9])), "st_async_cyc_med": float(np.median(R[:, 10]))}))
+            print(json.dumps({"split_phases": sig, "splits": int(R[:, 1].max() >> 16 & 0xffff) + 1,
+                              "wait_to_full": med(3, 4), "mma": med(4, 5), "stage": med(5, 14), "bar": med(14, 15),
+                              "issue": med(15, 11), "recv_wait": med(11, 12), "reduce_store": med(12, 13),
+                              "tail": med(13, 6), "cta_total": med(2, 6)}))
+        else:
+            print(json.dumps({"phases": sig, "wait_to_full": med(3, 4), "mma": med(4, 5),
+                              "epi": med(5, 10), "tail": med(10, 6), "cta_total": med(2, 6)}))

@@ -41,3 +41,53 @@ def test_gemm_matches_fp32_reference(M, N, K, bn, epi):
     err = (out - ref).abs()
     tol = ref.abs() * 2 ** -8 + 1e-3 * ref.abs().max()
     assert (err <= tol).all(), f"max err {err.max().item()} (ref max {ref.abs().max().item()})"
+
+
+@pytest.mark.parametrize("M,N,K,bn,splits", [
+    (49, 512, 4608, 64, 8), (49, 512, 2048, 128, 8), (196, 256, 2304, 64, 8), (196, 256, 1024, 128, 4),
+    (784, 128, 1152, 128, 4), (3136, 64, 576, 64, 2), (300, 200, 1024, 64, 4), (17, 1000, 4096, 128, 2),
+    # 33 k-blocks over 8 splits of ceil(33/8) = 5: the last split owns none
+    (49, 512, 2112, 64, 8), (49, 512, 2112, 128, 8),
+])
+@pytest.mark.parametrize("epi", ["plain", "full"])
+def test_gemm_split_k_matches_fp32_reference(M, N, K, bn, splits, epi):
+    """Split-K through the C ABI (trims_gemm_bf16_split): the S splits of a
+    tile reduce their fp32 partials in split order inside one cluster. Same
+    tolerance as above; two launches are bit-identical (deterministic order)."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(M * 5 + N + K + splits)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    scale = bias = res = None
+    ref = A.float() @ B.float().T
+    if epi == "full":
+        scale = torch.rand(N, device="cuda", generator=g) + 0.5
+        bias = torch.randn(N, device="cuda", generator=g)
+        res = torch.randn(M, N, device="cuda", generator=g).to(torch.bfloat16)
+        ref = torch.relu(ref * scale + bias + res.float())
+    outs = []
+    for _ in range(2):
+        D = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+        check(lib.trims_gemm_bf16_split(A.data_ptr(), M, K, K, B.data_ptr(), N, K, D.data_ptr(), N,
+                                        scale.data_ptr() if scale is not None else None,
+                                        bias.data_ptr() if bias is not None else None,
+                                        res.data_ptr() if res is not None else None, N, int(epi == "full"), bn,
+                                        splits, torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        outs.append(D)
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
+    out = outs[0].float()
+    assert torch.isfinite(out).all()
+    err = (out - ref).abs()
+    tol = ref.abs() * 2 ** -8 + 1e-3 * ref.abs().max()
+    assert (err <= tol).all(), f"max err {err.max().item()} (ref max {ref.abs().max().item()})"
+
+
+def test_gemm_split_count_validated():
+    import torch
+    A = torch.zeros(128, 64, device="cuda", dtype=torch.bfloat16)
+    D = torch.zeros(128, 64, device="cuda", dtype=torch.bfloat16)
+    for bn, splits in ((64, 3), (64, 16), (256, 2)):
+        rc = lib.trims_gemm_bf16_split(A.data_ptr(), 128, 64, 64, A.data_ptr(), 64, 64, D.data_ptr(), 64, None, None,
+                                       None, 64, 0, bn, splits, None)
+        assert rc != 0
