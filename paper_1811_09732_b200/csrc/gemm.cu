@@ -98,9 +98,9 @@ struct Smem {
 template <int BN, int STAGES, int S>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmR, uint16_t* D, int M, int N, int K, int ldd,
-                   const float* __restrict__ scale, const float* __restrict__ bias, int has_res, int relu, int kper,
-                   const ConvGeom cg) {
+                   const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmD, uint16_t* D,
+                   int M, int N, int K, int ldd, const float* __restrict__ scale, const float* __restrict__ bias,
+                   int has_res, int relu, int kper, int tma_out, const ConvGeom cg) {
   constexpr bool SPLIT = S > 1;
   constexpr int CW = BN / S;  // split-K: columns of the slice this CTA owns
   static_assert(CW % 8 == 0, "split slices are >= 8 columns");
@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     if (has_res) prefetch_tmap(&tmR);
+    if (!SPLIT && tma_out) prefetch_tmap(&tmD);
     // the other splits' blocks of this CTA's slice, in bytes
     if (SPLIT) mbar_expect_tx(&recv_full, uint32_t((S - 1) * nvalid * CW * 4));
   }
@@ -347,6 +348,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef TRIMS_GEMM_TRACE
       if (threadIdx.x == 128) GT_SET(gt_slot, 9, gtimer());
 #endif
+#ifdef TRIMS_EPI_COMPACT
+      // A/B: one 8-column group per TMEM round trip (tcgen05.ld ~25 cycles),
+      // one copy of the epilogue code (the epilogue runs once per CTA, so
+      // its instructions are fetched cold; a compact loop fetches them once)
+#pragma unroll 1
+      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 8) {
+        uint32_t r[8], o[4];
+        tmem_ld8_nw(tq + uint32_t(c), r);
+        tmem_wait_ld();
+        epi8(rl, c, reinterpret_cast<const float*>(r), o);
+        *reinterpret_cast<uint4*>(stage_at(rl, c)) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+      asm volatile("bar.sync 2, 256;" ::: "memory");  // the whole tile is staged
+      {
+        constexpr int lg = BN == 64 ? 3 : BN == 128 ? 4 : 5;  // 16-byte chunks per row
+#pragma unroll 1
+        for (int k = threadIdx.x - 128; k < (BM << lg); k += 256) {
+          const int rr = k >> lg, c = (k & ((1 << lg) - 1)) * 8;
+          const int row = row_of(rr), n = n0 + c;
+          if (row < 0 || n >= N) continue;
+          const uint4 v = *reinterpret_cast<const uint4*>(stage_at(rr, c));
+          const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+          store8(row, n, w);
+        }
+      }
+#else
       // this warp's BN/2 columns, 32 per TMEM round trip
 #pragma unroll 1
       for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
@@ -357,8 +384,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         finish(rl, c0, std::integral_constant<int, 16>{}, reinterpret_cast<const float*>(r));
         finish(rl, c0 + 16, std::integral_constant<int, 16>{}, reinterpret_cast<const float*>(r + 16));
       }
+#ifdef TRIMS_GEMM_TRACE
+      if (threadIdx.x == 128) GT_SET(gt_slot, 14, gtimer());
+#endif
+      if (tma_out) fence_proxy_async_smem();  // staged tile -> async proxy (the TMA store reads it)
       asm volatile("bar.sync 2, 256;" ::: "memory");  // the whole tile is staged
-      copy_out(threadIdx.x - 128, 0, BN);
+#ifdef TRIMS_GEMM_TRACE
+      if (threadIdx.x == 128) GT_SET(gt_slot, 15, gtimer());
+#endif
+      if (tma_out) {
+        // one TMA store per 64-channel box; the engine clips rows / channels
+        // outside the output. The CTA stays until the boxes are read out.
+        if (threadIdx.x == 128) {
+#pragma unroll
+          for (int b = 0; b < BN / 64; ++b) {
+            const uint16_t* src = s_out + b * BM * 64;
+            if (cg.impl) tma_store_4d(&tmD, src, n0 + b * 64, tw * wbox, th * cg.hbox, ti);
+            else tma_store_2d(&tmD, src, n0 + b * 64, m0);
+          }
+          bulk_commit();
+          bulk_wait_read();
+        }
+      } else {
+        copy_out(threadIdx.x - 128, 0, BN);
+      }
+#endif
 #ifdef TRIMS_GEMM_TRACE
       if (threadIdx.x == 128) GT_SET(gt_slot, 10, gtimer());
 #endif
@@ -508,37 +558,52 @@ void run_bn(const Prepared& p, cudaStream_t stream) {
   if (!pdl_enabled()) attr[0] = attr[1];  // keep only the cluster shape
   cfg.attrs = attr;
   cfg.numAttrs = (S > 1 ? 2 : 1) - (pdl_enabled() ? 0 : 1);
-  TRIMS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, S>, p.ta, p.tb, p.tr, e.out, int(p.M), int(p.N),
-                                int(p.K), int(e.ldo), e.scale, e.bias, e.residual ? 1 : 0, e.relu ? 1 : 0, kper, p.g));
+  TRIMS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, S>, p.ta, p.tb, p.tr, p.td, e.out, int(p.M),
+                                int(p.N), int(p.K), int(e.ldo), e.scale, e.bias, e.residual ? 1 : 0, e.relu ? 1 : 0,
+                                kper, p.tma_out, p.g));
 }
 
 // Residual tile maps: bf16 [rows][ldr] (or NHWC [n][P][Q][ldr] for an
 // implicit conv), N channels wide, SWIZZLE_128B boxes of 64 channels x the
 // tile's 128 rows. Out-of-range rows / channels are zero-filled.
-CUtensorMap residual_map_2d(const Epilogue& e, uint64_t M, uint64_t N) {
+CUtensorMap tile_map_2d(const uint16_t* ptr, uint64_t ld, uint64_t M, uint64_t N) {
   CUtensorMap m;
   cuuint64_t dims[2] = {N, M};
-  cuuint64_t strides[1] = {e.ldr * 2};
+  cuuint64_t strides[1] = {ld * 2};
   cuuint32_t box[2] = {64, uint32_t(BM)};
   cuuint32_t estr[2] = {1, 1};
-  cu_check(encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(e.residual), dims, strides, box,
+  cu_check(encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(ptr), dims, strides, box,
                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
-           "cuTensorMapEncodeTiled (residual)");
+           "cuTensorMapEncodeTiled (tile)");
   return m;
 }
 
-CUtensorMap residual_map_conv(const Epilogue& e, const ConvGeom& g, uint64_t N) {
+CUtensorMap tile_map_conv(const uint16_t* ptr, uint64_t ld, const ConvGeom& g, uint64_t N) {
   CUtensorMap m;
   cuuint64_t dims[4] = {N, cuuint64_t(g.Q), cuuint64_t(g.P), cuuint64_t(g.N)};
-  cuuint64_t strides[3] = {e.ldr * 2, cuuint64_t(g.Q) * e.ldr * 2, cuuint64_t(g.P) * g.Q * e.ldr * 2};
+  cuuint64_t strides[3] = {ld * 2, cuuint64_t(g.Q) * ld * 2, cuuint64_t(g.P) * g.Q * ld * 2};
   cuuint32_t box[4] = {64, uint32_t(1 << g.wbox_log2), uint32_t(g.hbox), 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  cu_check(encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(e.residual), dims, strides, box,
+  cu_check(encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(ptr), dims, strides, box,
                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
-           "cuTensorMapEncodeTiled (conv residual)");
+           "cuTensorMapEncodeTiled (conv tile)");
   return m;
+}
+
+// TRIMS_TMA_OUT=0: the staged output tile leaves by thread stores (A/B switch).
+bool tma_out_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("TRIMS_TMA_OUT");
+    return !(v && std::string(v) == "0");
+  }();
+  return on;
+}
+
+// TMA stores need 16-byte aligned rows and base.
+bool tma_out_ok(const Epilogue& e) {
+  return tma_out_enabled() && e.ldo % 8 == 0 && reinterpret_cast<uintptr_t>(e.out) % 16 == 0;
 }
 
 }  // namespace
@@ -600,7 +665,9 @@ Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn) 
   p.K = A.k;
   p.bn = bn;
   p.e = e;
-  if (e.residual) p.tr = residual_map_2d(e, p.M, p.N);
+  if (e.residual) p.tr = tile_map_2d(e.residual, e.ldr, p.M, p.N);
+  p.tma_out = tma_out_ok(e) ? 1 : 0;
+  if (p.tma_out) p.td = tile_map_2d(e.out, e.ldo, p.M, p.N);
   return p;
 }
 
@@ -685,7 +752,8 @@ Prepared prepare_conv(const void* act, const ConvGeom& g, const Operand& B, cons
   cu_check(r, "cuTensorMapEncodeTiled (conv)");
   p.ta = m;
   p.g = g;
-  if (e.residual) p.tr = residual_map_conv(e, g, p.N);
+  if (e.residual) p.tr = tile_map_conv(e.residual, e.ldr, g, p.N);
+  if (p.tma_out) p.td = tile_map_conv(e.out, e.ldo, g, p.N);
   return p;
 }
 

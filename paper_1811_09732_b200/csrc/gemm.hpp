@@ -53,6 +53,10 @@ struct Prepared {
   // channels x the tile's 128 output rows (2-D rows, or the implicit conv's
   // Wbox x Hbox pixel block), staged by TMA during the mainloop.
   CUtensorMap tr;
+  // Output tile store map (same box shape as the residual map) when the
+  // output rows are 16-byte aligned: the staged bf16 tile leaves by TMA.
+  CUtensorMap td;
+  int tma_out{0};
   uint64_t M{0}, N{0}, K{0};
   int bn{128};
   Epilogue e;
