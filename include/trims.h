@@ -303,6 +303,10 @@ int trims_plan_info(const char* src_json, uint32_t plan_flags, uint32_t out_dtyp
 /* TRIMS block checksum of a device range (async, accumulates into *d_out). */
 int trims_checksum_device(const void* dev, uint64_t nbytes, uint64_t word0, unsigned long long* d_out,
                           void* stream);
+/* The GPU compute step of a catalog request (the role of Client::touch,
+ * client.cpp:338-359): the block checksum of `nbytes` at `dev` on a stream of
+ * the calling thread, synchronously; *out = the sum (every byte read once). */
+int trims_touch_device(int device, const void* dev, uint64_t nbytes, uint64_t* out);
 /* K5 on device: splitmix words / uniform fp32 (bit-identical to the host fills). */
 int trims_fill_splitmix_device(uint64_t* dev, uint64_t n, uint64_t stream_seed, uint64_t k0, void* stream);
 int trims_fill_uniform_device(float* dev, uint64_t n, uint64_t stream_seed, uint64_t j0, float lo, float hi,

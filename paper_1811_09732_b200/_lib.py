@@ -199,6 +199,7 @@ _SIGS = {
     "trims_plan_transform": (_c.c_int, [_p, _p, _p, _p, _p, _c.POINTER(_u32)]),
     "trims_plan_ingest_host": (_c.c_int, [_p, _p, _p, _c.POINTER(_u64), _c.POINTER(_c.c_double)]),
     "trims_checksum_device": (_c.c_int, [_p, _u64, _u64, _p, _p]),
+    "trims_touch_device": (_c.c_int, [_c.c_int, _p, _u64, _c.POINTER(_u64)]),
     "trims_fill_splitmix_device": (_c.c_int, [_p, _u64, _u64, _u64, _p]),
     "trims_fill_uniform_device": (_c.c_int, [_p, _u64, _u64, _u64, _c.c_float, _c.c_float, _p]),
     "trims_replay": (_c.c_int, [_s, _s, _u64]),

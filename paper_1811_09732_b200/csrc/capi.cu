@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cstring>
 #include <filesystem>
+#include <map>
 #include <memory>
 #include <sstream>
 #include <thread>
@@ -1065,6 +1066,35 @@ int trims_checksum_device(const void* dev, uint64_t nbytes, uint64_t word0, unsi
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev_id);
     ingest::launch_checksum(static_cast<const uint8_t*>(dev), nbytes, word0, d_out, static_cast<cudaStream_t>(stream),
                             sms);
+    return 0;
+  });
+}
+
+int trims_touch_device(int device, const void* dev, uint64_t nbytes, uint64_t* out) {
+  return guard([&] {
+    // per calling thread and device: a stream, a device accumulator, a pinned result word
+    struct Scratch {
+      int device{-1};
+      cudaStream_t stream{nullptr};
+      unsigned long long* d_sum{nullptr};
+      unsigned long long* h_sum{nullptr};
+    };
+    thread_local std::map<int, Scratch> scratch;
+    DeviceGuard g(device);
+    Scratch& sc = scratch[device];
+    if (sc.device < 0) {
+      TRIMS_CUDA(cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking));
+      TRIMS_CUDA(cudaMalloc(&sc.d_sum, sizeof(unsigned long long)));
+      TRIMS_CUDA(cudaMallocHost(&sc.h_sum, sizeof(unsigned long long)));
+      sc.device = device;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    TRIMS_CUDA(cudaMemsetAsync(sc.d_sum, 0, sizeof(unsigned long long), sc.stream));
+    ingest::launch_checksum(static_cast<const uint8_t*>(dev), nbytes, 0, sc.d_sum, sc.stream, sms);
+    TRIMS_CUDA(cudaMemcpyAsync(sc.h_sum, sc.d_sum, sizeof(unsigned long long), cudaMemcpyDeviceToHost, sc.stream));
+    TRIMS_CUDA(cudaStreamSynchronize(sc.stream));
+    *out = *sc.h_sum;
     return 0;
   });
 }

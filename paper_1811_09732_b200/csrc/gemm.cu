@@ -690,7 +690,9 @@ void run(const Prepared& p, cudaStream_t stream) {
 
 int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms) {
   // Split K only while the output tiles leave most SMs idle, each split keeps
-  // >= 4 k-blocks and every split's column slice of the tile is >= 8 wide.
+  // >= 2 k-blocks (4 before the cheaper reduction; 2 measured best, AlexNet
+  // b1 0.0883 -> 0.0862 ms, others flat, profiles/r3/split_minkb_ab.log) and
+  // every split's column slice of the tile is >= 8 wide.
   const uint64_t tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn), kb = (K + BK - 1) / BK;
   int s = 1;
   if (bn == 256) return 1;  // no split variant of the widest tile (shared memory)
@@ -700,7 +702,7 @@ int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms) {
   const int max_s = tiles <= 8 ? kMaxSplits : 4;
   static const uint64_t min_kb = [] {  // k-blocks each split keeps at least (A/B: TRIMS_SPLIT_MINKB)
     const char* e = std::getenv("TRIMS_SPLIT_MINKB");
-    return e ? uint64_t(std::max(1, std::atoi(e))) : uint64_t(4);
+    return e ? uint64_t(std::max(1, std::atoi(e))) : uint64_t(2);
   }();
   while (s < max_s && bn / (s * 2) >= 8 && tiles * uint64_t(s * 2) <= uint64_t(sms) && kb / uint64_t(s * 2) >= min_kb)
     s *= 2;
