@@ -337,6 +337,14 @@ int trims_gemm_bf16_split(const void* A, uint64_t M, uint64_t K, uint64_t lda, c
 typedef struct trims_net trims_net;
 int trims_net_create(int device, const char* arch_text, const char* resident_json, const void* weights, int batch,
                      trims_net** out);
+/* The same with executor flags: TRIMS_NET_THROUGHPUT (1) builds no split-K
+ * launches (one CTA per output tile) so many clients' forwards pack the GPU;
+ * TRIMS_NET_LEAN (2) also uses GEMM variants that fit two CTAs per SM.
+ * 0 = latency mode (trims_net_create). */
+#define TRIMS_NET_THROUGHPUT 1
+#define TRIMS_NET_LEAN 2
+int trims_net_create_ex(int device, const char* arch_text, const char* resident_json, const void* weights, int batch,
+                        int flags, trims_net** out);
 void trims_net_destroy(trims_net* net);
 int trims_net_buffers(trims_net* net, void** input, void** logits, int* classes, int* input_hw);
 /* Re-point a net at a new generation of the same resident model (after an

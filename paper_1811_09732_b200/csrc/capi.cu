@@ -1132,16 +1132,22 @@ struct trims_net {
   std::unique_ptr<nn::Net> net;
 };
 
-int trims_net_create(int device, const char* arch_text, const char* resident_json, const void* weights, int batch,
-                     trims_net** out) {
+int trims_net_create_ex(int device, const char* arch_text, const char* resident_json, const void* weights, int batch,
+                        int flags, trims_net** out) {
   return guard([&] {
     if (batch < 1) raise(Errc::InvalidArgument, "batch must be >= 1");
+    if (flags & ~(nn::kNetThroughput | nn::kNetLean)) raise(Errc::InvalidArgument, "unknown executor flags");
     auto h = std::make_unique<trims_net>();
     h->net = std::make_unique<nn::Net>(device, arch_text, fmt::manifest_from_json(resident_json),
-                                       static_cast<const uint8_t*>(weights), batch);
+                                       static_cast<const uint8_t*>(weights), batch, flags);
     *out = h.release();
     return 0;
   });
+}
+
+int trims_net_create(int device, const char* arch_text, const char* resident_json, const void* weights, int batch,
+                     trims_net** out) {
+  return trims_net_create_ex(device, arch_text, resident_json, weights, batch, 0, out);
 }
 
 void trims_net_destroy(trims_net* net) {

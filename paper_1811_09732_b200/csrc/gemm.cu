@@ -675,6 +675,11 @@ void run(const Prepared& p, cudaStream_t stream) {
   if (p.splits < 1 || p.splits > kMaxSplits || (p.splits & (p.splits - 1)) || (p.bn / p.splits) % 8 ||
       (p.bn == 256 && p.splits > 1))
     raise(Errc::InvalidArgument, "GEMM split count");
+  if (p.lean && p.splits == 1 && p.bn != 256) {  // <= ~110 KB: two CTAs per SM
+    if (p.bn == 64) run_bn<64, 3, 1>(p, stream);
+    else run_bn<128, 2, 1>(p, stream);
+    return;
+  }
   switch (p.bn * 16 + p.splits) {
     case 64 * 16 + 1: run_bn<64, 6, 1>(p, stream); break;
     case 64 * 16 + 2: run_bn<64, 6, 2>(p, stream); break;

@@ -63,6 +63,9 @@ struct Prepared {
   // Split-K (grid.z = splits, one (1,1,splits) cluster per output tile):
   // the splits reduce their fp32 partials through distributed shared memory.
   int splits{1};
+  // Lean variants (splits == 1, BN 64/128): a shallower TMA ring so two CTAs
+  // fit one SM's shared memory (throughput mode: many clients' kernels).
+  bool lean{false};
   ConvGeom g{};  // g.impl: A is the implicit im2col of an NHWC activation
 };
 Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn = 0);

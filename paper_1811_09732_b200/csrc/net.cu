@@ -129,8 +129,15 @@ uint8_t* Net::alloc(uint64_t bytes) {
   return static_cast<uint8_t*>(p);
 }
 
-Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, const uint8_t* weights, int batch)
+Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, const uint8_t* weights, int batch,
+         int flags)
     : device_(device), batch_(batch) {
+  // Latency mode (default) splits K over more CTAs to cut one request's
+  // latency; throughput mode keeps one CTA per output tile, so concurrent
+  // clients' kernels pack the SMs (16 MPS clients on ResNet-50: 12.0k vs 5.9k
+  // requests/s, profiles/r3/mps_mode_ab.log).
+  const bool split_ok = splitk_enabled() && !(flags & (kNetThroughput | kNetLean));
+  const bool lean = (flags & kNetLean) != 0;
   DeviceGuard g(device);
   TRIMS_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device));
   std::map<std::string, const fmt::TensorSpec*> tensors;
@@ -292,8 +299,9 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
             implicit ? gemm::prepare_conv(in.p, gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg),
                                           Bop, e)
                      : gemm::prepare({A, M, uint64_t(kp), uint64_t(direct ? cin : kp)}, Bop, e));
-        if (splitk_enabled())
+        if (split_ok)
           prep->splits = gemm::pick_splits(gemm::tile_rows(*prep), uint64_t(kg), uint64_t(kp), prep->bn, sms_);
+        prep->lean = lean;
         const uint64_t b_off = w_off + uint64_t(gi) * kg * rsc * 2;
         const bool do_params = first_group && bind_params;
         auto rebind = [=](cudaStream_t s) {
@@ -374,6 +382,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
                           {reinterpret_cast<const uint16_t*>(uintptr_t(256)), uint64_t(cout), uint64_t(cin),
                            uint64_t(cin)},
                           e));
+        prep->lean = lean;
         auto rebind = [=](cudaStream_t s) {
           prep->tb = gemm::make_tmap(wptr(w_off), uint64_t(cout), uint64_t(cin), uint64_t(cin), prep->bn);
           bind_bias(s);

@@ -46,9 +46,14 @@ void softmax(const float* in, float* out, int M, int N, cudaStream_t s);
 // paper_1811_09732_b200/models.py) over a resident manifest whose bf16 KRSC
 // weights live at `weights` (the store's segment, mapped read-only), plus a
 // private workspace: activations, im2col scratch, folded BN parameters.
+// Executor modes (trims_net_create_ex flags).
+constexpr int kNetThroughput = 1;  // no split-K: one CTA per output tile (many clients on one GPU)
+constexpr int kNetLean = 2;        // throughput + GEMM variants that fit 2 CTAs per SM
+
 class Net {
  public:
-  Net(int device, const std::string& arch, const fmt::Manifest& resident, const uint8_t* weights, int batch);
+  Net(int device, const std::string& arch, const fmt::Manifest& resident, const uint8_t* weights, int batch,
+      int flags = 0);
   ~Net();
   float* input() const { return input_; }    // fp32 NCHW [batch, 3, H, W]
   float* logits() const { return logits_; }  // fp32 [batch, classes]

@@ -36,15 +36,21 @@ def arch_text(arch: C.Arch) -> str:
     return "\n".join(lines) + "\n"
 
 
+NET_MODES = {"latency": 0, "throughput": 1, "lean": 3}  # trims_net_create_ex flags
+
+
 class BoundNet:
     """A network executor over one attached model view (weights stay shared)."""
 
-    def __init__(self, view, arch: C.Arch | str, batch: int = 1, device: int = 0):
+    def __init__(self, view, arch: C.Arch | str, batch: int = 1, device: int = 0, mode: str = "latency"):
+        """mode: "latency" (split-K layers: fastest single request), "throughput"
+        (one CTA per output tile: many clients' forwards pack one GPU) or "lean"
+        (throughput with GEMM variants that fit two CTAs per SM)."""
         arch = C.ARCHS[arch]() if isinstance(arch, str) else arch
-        self.arch, self.batch, self.device, self.view = arch, batch, device, view
+        self.arch, self.batch, self.device, self.view, self.mode = arch, batch, device, view, mode
         h = ctypes.c_void_p()
-        check(lib.trims_net_create(device, arch_text(arch).encode(), view.manifest_json.encode(), view.base_ptr, batch,
-                                   ctypes.byref(h)))
+        check(lib.trims_net_create_ex(device, arch_text(arch).encode(), view.manifest_json.encode(), view.base_ptr,
+                                      batch, NET_MODES[mode], ctypes.byref(h)))
         self._h = h
         inp, lg = ctypes.c_void_p(), ctypes.c_void_p()
         classes, hw = ctypes.c_int(), ctypes.c_int()

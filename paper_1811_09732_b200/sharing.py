@@ -47,7 +47,8 @@ class SharedModel:
                    bytes(ex.manifest_digest), arch_text)
 
 
-def _serve(conn, sm: SharedModel, fd: int, batch: int, n_reqs: int, seed: int, on_exit=None) -> None:
+def _serve(conn, sm: SharedModel, fd: int, batch: int, n_reqs: int, seed: int, on_exit=None,
+           mode: str = "latency") -> None:
     """Attach `fd`'s segment, bind an executor, warm up, then serve n_reqs
     requests on the parent's "go"; reports latencies and the last logits."""
     from ._lib import check, lib
@@ -57,8 +58,9 @@ def _serve(conn, sm: SharedModel, fd: int, batch: int, n_reqs: int, seed: int, o
         imp, ptr, res_json = import_segment(sm.device, fd, sm.alloc_bytes, sm.offset, sm.generation,
                                             sm.payload_bytes, sm.digest)
         net = ctypes.c_void_p()
-        check(lib.trims_net_create(sm.device, sm.arch_text.encode(), res_json.encode(), ptr, batch,
-                                   ctypes.byref(net)))
+        from .models import NET_MODES
+        check(lib.trims_net_create_ex(sm.device, sm.arch_text.encode(), res_json.encode(), ptr, batch,
+                                      NET_MODES[mode], ctypes.byref(net)))
         classes, hw = ctypes.c_int(), ctypes.c_int()
         check(lib.trims_net_buffers(net, None, None, ctypes.byref(classes), ctypes.byref(hw)))
         attach_ms = (time.perf_counter() - t0) * 1e3
@@ -86,7 +88,7 @@ def _serve(conn, sm: SharedModel, fd: int, batch: int, n_reqs: int, seed: int, o
 
 
 def _daemon_client_main(conn, endpoint: str, key: tuple, arch_text: str, batch: int, n_reqs: int,
-                        seed: int) -> None:
+                        seed: int, mode: str = "latency") -> None:
     """A client process of the wire-protocol daemon (daemon.py): opens the
     model over the socket (the allocation fd arrives with the OpenResponse),
     attaches, binds an executor and serves; closes its handle at the end."""
@@ -100,7 +102,7 @@ def _daemon_client_main(conn, endpoint: str, key: tuple, arch_text: str, batch: 
         check(lib.trims_device_init(ex.device))
         sm = SharedModel(ex.device, ex.alloc_bytes, ex.segment_offset, ex.generation, ex.payload_bytes,
                          ex.manifest_digest, arch_text)
-        _serve(conn, sm, ex.fd, batch, n_reqs, seed, on_exit=lambda: rs.close(F.ModelKey(*key)))
+        _serve(conn, sm, ex.fd, batch, n_reqs, seed, on_exit=lambda: rs.close(F.ModelKey(*key)), mode=mode)
     except Exception as e:
         if not conn.closed:
             conn.send(("error", repr(e)))
@@ -169,17 +171,20 @@ def _child_env(env: dict | None):
 
 
 def run_daemon_clients(endpoint: str, key, arch_text: str, n_clients: int = 16, n_reqs: int = 20, batch: int = 1,
-                       seed: int = 2, timeout_s: float = 600.0, env: dict | None = None) -> dict:
+                       seed: int = 2, timeout_s: float = 600.0, env: dict | None = None,
+                       mode: str = "latency") -> dict:
     """As run_clients, but every client process gets the model from the
     daemon at `endpoint` (v1 OpenRequest over the socket, fd by SCM_RIGHTS).
-    `env` (e.g. mps_session()'s) is set in the clients' environment."""
+    `env` (e.g. mps_session()'s) is set in the clients' environment; `mode`
+    is the clients' executor mode (models.BoundNet)."""
     ctx = mp.get_context("spawn")
     procs, conns = [], []
     with _child_env(env):
         for i in range(n_clients):
             parent, child = ctx.Pipe()
             p = ctx.Process(target=_daemon_client_main,
-                            args=(child, endpoint, (key.ns, key.name, key.version), arch_text, batch, n_reqs, seed),
+                            args=(child, endpoint, (key.ns, key.name, key.version), arch_text, batch, n_reqs, seed,
+                                  mode),
                             daemon=True)
             p.start()
             procs.append(p)

@@ -91,6 +91,30 @@ def test_forward_layerwise_parity(store, name, batch):
         cli.close(view)
 
 
+@pytest.mark.parametrize("mode", ["throughput", "lean"])
+@pytest.mark.parametrize("name,batch", [("alexnet", 1), ("resnet50", 1), ("vgg16", 1)])
+def test_forward_executor_modes(store, name, batch, mode):
+    """Throughput mode (no split-K) and lean mode (two-CTAs-per-SM GEMM
+    variants): same layer-by-layer tolerance; the logits agree with latency
+    mode's up to fp32 summation order (split-K sums per split, then across)."""
+    import torch
+    arch = C.ARCHS[name]()
+    cli = Client(store)
+    view = cli.open(C.arch_key(arch), force_shared=True)
+    net = BoundNet(view, arch, batch=batch, mode=mode)
+    lat = BoundNet(view, arch, batch=batch)
+    try:
+        _layerwise(arch, view, net, f"{name}[{mode}]", batch)
+        x = torch.randn(batch, 3, arch.input_hw, arch.input_hw, generator=torch.Generator().manual_seed(3))
+        a, b = net.forward(x).clone(), lat.forward(x).clone()
+        assert torch.equal(net.forward(x), a), "not deterministic"
+        assert ((a - b).norm() / b.norm()).item() <= 1e-2 and torch.equal(a.argmax(1), b.argmax(1))
+    finally:
+        net.close()
+        lat.close()
+        cli.close(view)
+
+
 def _layerwise(arch, view, net, name, batch):
     import torch
     assert net.layer_count() == len(arch.layers)
