@@ -113,6 +113,11 @@ typedef struct trims_store_config {
   double workspace_headroom_fraction; /* daemon.hpp:29 (in [0, 1]; published in stats for the client's
                                          workspace-reservation fallback, client.cpp:192-204) */
   uint32_t startup_calibration;  /* daemon.hpp:33: measure q/o/s at creation (daemon.cpp:342-390) */
+  /* Cold loads read the artifact with O_DIRECT straight into the pinned host
+   * tier (no page-cache copy): 0 = buffered reads, 1 = direct, 2 = auto
+   * (direct when most of the blob is not in the page cache). Filesystems
+   * without O_DIRECT fall back to buffered reads. */
+  uint32_t direct_io;
 } trims_store_config;
 
 /* Reference outcomes (cache_core.hpp:36) + PEER_HIT for the multi-GPU directory. */

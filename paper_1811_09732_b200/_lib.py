@@ -76,6 +76,7 @@ class StoreConfig(ctypes.Structure):
         ("remote_url", ctypes.c_char_p),
         ("workspace_headroom_fraction", ctypes.c_double),
         ("startup_calibration", ctypes.c_uint32),
+        ("direct_io", ctypes.c_uint32),
     ]
 
 

@@ -36,7 +36,7 @@ void parallel_pread(int fd, uint8_t* dst, uint64_t len, uint64_t off, unsigned t
 // in the order they land, not in file order. With `hash`, a further thread
 // hashes the pieces in file order under both.
 void parallel_pread_upload(int fd, uint8_t* host, uint8_t* dev, uint64_t len, uint64_t off, unsigned threads,
-                           int device, cudaStream_t stream, Sha256* hash) {
+                           int device, cudaStream_t stream, Sha256* hash, int direct_fd) {
   DeviceGuard g(device);
   static const bool any_order = [] {  // A/B switch: TRIMS_UPLOAD_IN_ORDER=1
     const char* e = std::getenv("TRIMS_UPLOAD_IN_ORDER");
@@ -47,7 +47,7 @@ void parallel_pread_upload(int fd, uint8_t* host, uint8_t* dev, uint64_t len, ui
       [&](const uint8_t* p, uint64_t b, uint64_t n) {
         TRIMS_CUDA(cudaMemcpyAsync(dev + b, p, n, cudaMemcpyHostToDevice, stream));
       },
-      any_order);
+      any_order, direct_fd);
 }
 
 // ---------------------------------------------------------------------------
@@ -445,17 +445,21 @@ fmt::Manifest CudaTierBackend::read_manifest(const fmt::ModelKey& key, const std
   int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
   if (fd < 0) raise(Errc::NotFound, path);
   HostBuf hb;
+  const int dfd = direct_fd_for(path, fd, a.blob_offset, a.manifest.blob_bytes);
+  if (dfd >= 0) direct_loads_.fetch_add(1);
   try {
-    hb = alloc_host(a.manifest.blob_bytes);
+    hb = alloc_host(a.manifest.blob_bytes, dfd >= 0 ? a.blob_offset % 4096 : 0, dfd >= 0);
     Sha256 h;
-    pipelined_read(fd, a.blob_offset, a.manifest.blob_bytes, hb.p, cfg_.read_threads, &h);
+    pipelined_read(fd, a.blob_offset, a.manifest.blob_bytes, hb.p, cfg_.read_threads, &h, {}, false, dfd);
     if (h.finish() != a.manifest.checksum) raise(Errc::ChecksumMismatch, path);
   } catch (...) {
     ::close(fd);
+    if (dfd >= 0) ::close(dfd);
     free_host(hb);
     throw;
   }
   ::close(fd);
+  if (dfd >= 0) ::close(dfd);
   std::lock_guard lk(mu_);
   auto& slot = verified_[fmt::to_string(key)];
   free_host(slot);  // a stale one from an open that never settled
@@ -463,16 +467,26 @@ fmt::Manifest CudaTierBackend::read_manifest(const fmt::ModelKey& key, const std
   return a.manifest;
 }
 
-CudaTierBackend::HostBuf CudaTierBackend::alloc_host(uint64_t bytes) {
+CudaTierBackend::HostBuf CudaTierBackend::alloc_host(uint64_t bytes, uint64_t head, bool direct) {
   HostBuf hb;
   hb.bytes = bytes;
-  if (pool_) hb.p = pool_->alloc(std::max<uint64_t>(bytes, 1));
-  hb.pooled = hb.p != nullptr;
-  if (!hb.p) {
+  const uint64_t total = std::max<uint64_t>(bytes + head + (head || direct ? 4096 : 0), 1);
+  if (pool_) hb.base = pool_->alloc(total);
+  hb.pooled = hb.base != nullptr;
+  if (!hb.base) {
     DeviceGuard g(cfg_.device);
-    TRIMS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hb.p), std::max<uint64_t>(bytes, 1), cudaHostAllocPortable));
+    TRIMS_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hb.base), total, cudaHostAllocPortable));
   }
+  hb.p = hb.base + head;
   return hb;
+}
+
+// Cold-load read mode for one artifact (cfg_.direct_io): an O_DIRECT fd of
+// the same file, or -1 for buffered reads.
+int CudaTierBackend::direct_fd_for(const std::string& path, int fd, uint64_t off, uint64_t len) {
+  if (cfg_.direct_io == 0) return -1;
+  if (cfg_.direct_io == 2 && page_cache_fraction(fd, off, len) > 0.5) return -1;  // mostly cached: buffered
+  return ::open(path.c_str(), O_RDONLY | O_CLOEXEC | O_DIRECT);  // -1 where unsupported: buffered
 }
 
 bool CudaTierBackend::take_verified(const fmt::ModelKey& key, uint64_t bytes, HostBuf* out) {
@@ -503,10 +517,10 @@ void CudaTierBackend::free_host(HostBuf& h) {
     cudaEventDestroy(h.ready);
     h.ready = nullptr;
   }
-  if (!h.p) return;
-  if (h.pooled) pool_->free(h.p);
-  else cudaFreeHost(h.p);
-  h.p = nullptr;
+  if (!h.base) return;
+  if (h.pooled) pool_->free(h.base);
+  else cudaFreeHost(h.base);
+  h.p = h.base = nullptr;
 }
 
 // daemon.cpp:153-158: disk -> host tier, here straight into pinned memory.
@@ -537,6 +551,7 @@ void CudaTierBackend::stage_host(uint64_t model_id, const fmt::Manifest& m, cons
   } else {
     int fd = ::open(path.c_str(), O_RDONLY | O_CLOEXEC);
     if (fd < 0) raise(Errc::NotFound, path);
+    int dfd = -1;
     try {
       uint8_t hdr[16];
       if (::pread(fd, hdr, 16, 0) != 16) raise(Errc::Corrupt, "short read on " + path);
@@ -546,7 +561,9 @@ void CudaTierBackend::stage_host(uint64_t model_id, const fmt::Manifest& m, cons
       struct stat st {};
       ::fstat(fd, &st);
       if (uint64_t(st.st_size) < off + m.blob_bytes) raise(Errc::Corrupt, "blob truncated in " + path);
-      hb = alloc_host(m.blob_bytes);
+      dfd = direct_fd_for(path, fd, off, m.blob_bytes);
+      hb = alloc_host(m.blob_bytes, dfd >= 0 ? off % 4096 : 0, dfd >= 0);
+      if (dfd >= 0) direct_loads_.fetch_add(1);
       // verify (daemon.cpp:155 read_model(path, full_verify)) in order under the read + upload
       Sha256 h;
       Sha256* hp = cfg_.full_verify ? &h : nullptr;
@@ -557,7 +574,8 @@ void CudaTierBackend::stage_host(uint64_t model_id, const fmt::Manifest& m, cons
           DeviceGuard g(cfg_.device);
           auto r0 = std::chrono::steady_clock::now();
           TRIMS_CUDA(cudaEventRecord(pre_t0_, pre_stream_));
-          parallel_pread_upload(fd, hb.p, target, hb.bytes, off, cfg_.read_threads, cfg_.device, pre_stream_, hp);
+          parallel_pread_upload(fd, hb.p, target, hb.bytes, off, cfg_.read_threads, cfg_.device, pre_stream_, hp,
+                                dfd);
           TRIMS_CUDA(cudaEventRecord(pre_done_, pre_stream_));
           pre_read_ms_ = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - r0).count();
         } catch (...) {
@@ -565,16 +583,18 @@ void CudaTierBackend::stage_host(uint64_t model_id, const fmt::Manifest& m, cons
           throw;
         }
       } else {
-        pipelined_read(fd, off, hb.bytes, hb.p, cfg_.read_threads, hp);
+        pipelined_read(fd, off, hb.bytes, hb.p, cfg_.read_threads, hp, {}, false, dfd);
       }
       if (hp && h.finish() != m.checksum) raise(Errc::ChecksumMismatch, path);
     } catch (...) {
       release_prestage(model_id);
       ::close(fd);
+      if (dfd >= 0) ::close(dfd);
       free_host(hb);
       throw;
     }
     ::close(fd);
+    if (dfd >= 0) ::close(dfd);
   }
   std::lock_guard lk(mu_);
   auto it = host_.find(model_id);

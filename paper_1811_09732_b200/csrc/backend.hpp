@@ -110,6 +110,9 @@ struct BackendConfig {
   fmt::Plan plan;
   uint64_t pinned_pool_bytes{0};
   unsigned read_threads{8};
+  // Cold-load reads into the pinned host tier: 0 buffered, 1 O_DIRECT, 2 auto
+  // (O_DIRECT when most of the blob is not in the page cache).
+  int direct_io{0};
   uint64_t arena_bytes{0};  // HBM arena for the fast tier (0 = one cuMem allocation per model)
   std::shared_ptr<Directory> directory;  // multi-GPU: publish sealed segments for peers (null = single GPU)
   // Keep the host tier in the RESIDENT form: after a converting publish, the
@@ -171,10 +174,12 @@ class CudaTierBackend : public TierBackend {
   const uint8_t* host_buffer(uint64_t model_id, uint64_t* bytes);
   Ingestor& ingestor() { return ing_; }
   const BackendConfig& config() const { return cfg_; }
+  uint64_t direct_loads() const { return direct_loads_.load(); }
 
  private:
   struct HostBuf {
-    uint8_t* p{nullptr};
+    uint8_t* p{nullptr};           // the blob
+    uint8_t* base{nullptr};        // the allocation (p - head: direct reads keep p congruent to the file offset)
     uint64_t bytes{0};
     bool pooled{false};
     bool resident{false};          // holds the resident (converted) blob, valid once `ready` fires
@@ -182,7 +187,11 @@ class CudaTierBackend : public TierBackend {
   };
   void to_resident_form(uint64_t model_id, const FastRecord& rec, const IngestPlan& plan);
   void free_host(HostBuf& h);
-  HostBuf alloc_host(uint64_t bytes);
+  // head: bytes before the blob in the allocation (< 4096); a head or direct
+  // read also reserves 4 KiB after it (the last aligned block)
+  HostBuf alloc_host(uint64_t bytes, uint64_t head = 0, bool direct = false);
+  int direct_fd_for(const std::string& path, int fd, uint64_t off, uint64_t len);
+  std::atomic<uint64_t> direct_loads_{0};  // disk reads done with O_DIRECT
   bool take_verified(const fmt::ModelKey& key, uint64_t bytes, HostBuf* out);
 
   std::shared_ptr<IngestPlan> plan_for(uint64_t model_id, const fmt::Manifest& m);

@@ -403,6 +403,8 @@ BackendConfig backend_config(const trims_store_config* cfg) {
   bc.plan = make_plan(cfg->plan_flags, cfg->out_dtype);
   bc.pinned_pool_bytes = cfg->pinned_pool_bytes ? cfg->pinned_pool_bytes : cfg->host_capacity_bytes;
   bc.read_threads = cfg->read_threads ? cfg->read_threads : 8;
+  bc.direct_io = int(cfg->direct_io);
+  if (const char* e = std::getenv("TRIMS_DIRECT_IO")) bc.direct_io = std::atoi(e);  // A/B override
   // arena: 0 = auto (capacity + 1/16 + 64 MiB for per-segment rounding and tails), 1 = off
   bc.arena_bytes = cfg->arena_bytes == 1 ? 0
                    : cfg->arena_bytes ? cfg->arena_bytes
@@ -663,7 +665,8 @@ int trims_store_stats_json(trims_store* s, char* out, uint64_t cap) {
        << ",\"fetch_ns\":" << st.cumulative.fetch_ns << ",\"disk_read_ns\":" << st.cumulative.disk_read_ns
        << ",\"copy_ns\":" << st.cumulative.host_to_fast_copy_ns << ",\"export_ns\":" << st.cumulative.handle_export_ns
        << ",\"peer_hits\":" << st.peer_hits << ",\"peer_attempts\":" << s->peers.attempts.load()
-       << ",\"peer_fallbacks\":" << s->peers.fallbacks.load() << ",\"rank\":" << (s->dir ? s->dir->rank() : 0)
+       << ",\"peer_fallbacks\":" << s->peers.fallbacks.load() << ",\"direct_reads\":" << s->be->direct_loads()
+       << ",\"rank\":" << (s->dir ? s->dir->rank() : 0)
        << ",\"world\":" << (s->dir ? s->dir->world() : 1) << ",\"workspace_headroom\":" << f64(s->workspace_headroom)
        << ",\"has_calibration\":" << (s->calibration ? "true" : "false");
     if (s->calibration)

@@ -24,8 +24,20 @@ constexpr uint64_t kReadPiece = 2ull << 20;  // measured: 2 MiB 4.3-4.4 ms vs 4 
 // range, bytes) -- in range order, or in landing order when sink_any_order
 // (dst != nullptr only). A short read raises Corrupt; an exception from the
 // sink stops the readers and is rethrown.
+//
+// direct_fd >= 0 (the same file opened O_DIRECT) with dst != nullptr: dst
+// must be congruent to `off` modulo 4096 and the caller's allocation must
+// span [dst - off % 4096, dst + len + 4096): the readers then read whole
+// aligned 4 KiB blocks with O_DIRECT (DMA from the device into dst's pages,
+// no page-cache copy; the bytes around the blob land in the slack). A piece
+// the filesystem refuses (EINVAL) is read buffered instead. Hash and sink see
+// exactly the blob range either way.
 void pipelined_read(int fd, uint64_t off, uint64_t len, uint8_t* dst, unsigned threads, Sha256* hash,
                     const std::function<void(const uint8_t*, uint64_t, uint64_t)>& sink = {},
-                    bool sink_any_order = false);
+                    bool sink_any_order = false, int direct_fd = -1);
+
+// Fraction of [off, off + len) of fd resident in the page cache (mincore over
+// a sample of up to 256 pages); 1.0 when it cannot tell.
+double page_cache_fraction(int fd, uint64_t off, uint64_t len);
 
 }  // namespace trims

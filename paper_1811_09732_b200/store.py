@@ -46,6 +46,7 @@ class StoreOptions:
     directory_slots: int = 0           # 0 = 1024 per rank
     workspace_headroom_fraction: float = 0.25  # daemon.hpp:29 (published to clients in stats)
     startup_calibration: bool = True   # daemon.hpp:33: q/o/s measured at creation, published in stats
+    direct_io: str = "auto"            # cold-load reads: "buffered", "direct" (O_DIRECT) or "auto"
 
     @property
     def plan_flags(self) -> int:
@@ -70,6 +71,7 @@ class Store:
         cfg.pinned_pool_bytes = opts.pinned_pool_bytes
         cfg.scan_disk = int(opts.scan_disk)
         cfg.read_threads = opts.read_threads
+        cfg.direct_io = {"buffered": 0, "direct": 1, "auto": 2}[opts.direct_io]
         cfg.arena_bytes = opts.arena_bytes
         self._dirname = opts.directory.encode() if opts.directory else None
         cfg.directory = self._dirname

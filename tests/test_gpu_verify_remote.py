@@ -40,6 +40,47 @@ def gold():
     return {e["name"]: e for e in load("catalog.json.gz")["tiny_seed1"]}
 
 
+def _o_direct_supported(d: str) -> bool:
+    path = os.path.join(d, "odirect.probe")
+    with open(path, "wb") as f:
+        f.write(b"\0" * 8192)
+    try:
+        fd = os.open(path, os.O_RDONLY | os.O_DIRECT)
+        os.close(fd)
+        return True
+    except OSError:
+        return False
+    finally:
+        os.unlink(path)
+
+
+@pytest.mark.parametrize("mode", ["direct", "buffered", "auto"])
+@pytest.mark.parametrize("verify", [False, True])
+def test_direct_io_cold_loads_bit_exact(tiny_dir, gold, mode, verify):
+    """Cold loads with O_DIRECT reads into the pinned host tier (blob offsets
+    are 64-aligned, not 4 KiB-aligned: the host buffer is placed congruent to
+    the file offset and whole blocks are read around the blob): identical
+    resident bytes, trailer SHA and touch; host-tier reloads identical too."""
+    import torch
+    with Store(StoreOptions(disk_cache_dir=tiny_dir, fast_capacity_bytes=20 * MB, host_capacity_bytes=64 * MB,
+                            full_verify=verify, direct_io=mode)) as s:
+        cli = Client(s)
+        for rnd in range(2):
+            for name in ("alexnet", "resnet50", "vgg16"):
+                v = cli.open(key(name), force_shared=True)
+                assert v.outcome == ("disk_load" if rnd == 0 else "host_hit")
+                assert F.sha256(d2h(v, torch)).hex() == gold[name]["trailer"]
+                assert cli.touch(v) == gold[name]["touch"]
+                cli.close(v)
+            s.reclaim(0, 20 * MB)  # drop the fast tier: round 2 reloads from the host tier
+        st = s.stats()
+        assert st["open_errors"] == 0
+        if mode == "direct" and _o_direct_supported(tiny_dir):
+            assert st["direct_reads"] == 3
+        if mode == "buffered":
+            assert st["direct_reads"] == 0
+
+
 @pytest.mark.parametrize("host_mb", [64, 1])  # 1 MB: host staging skipped, publish from the verified read
 def test_full_verify_loads_bit_exact(tiny_dir, gold, host_mb):
     import torch
