@@ -26,6 +26,22 @@ for w in $what; do
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:transform -c 2 \
         -f -o gpurun_out/${tag}_transform python scripts/prof_transform.py resnet50 1 \
         > gpurun_out/${tag}_ncu_transform.log 2>&1 ;;
+    fwdncu)
+      ARCHS="resnet50 vgg16 alexnet vgg19" timeout 1500 bash scripts/gpu_fwd_ncu.sh ${tag}
+      for a in resnet50 vgg16 alexnet vgg19; do
+        python scripts/ncu_forward_summary.py gpurun_out/${tag}_fwd_${a}.csv gpurun_out/${tag}_ncu_forward_${a}.json > /dev/null 2>&1
+      done ;;
+    refmaps)  # which shared objects the reference arm's process maps (must be oracle/_ref only)
+      timeout 900 python -c "
+import runpy, sys, os
+sys.argv = ['bench.py', '--impl', 'reference', '--quick', '--steps', '3', '--warmup', '3']
+try:
+    runpy.run_path('bench.py', run_name='__main__')
+finally:
+    maps = open('/proc/self/maps').read().split()
+    sos = sorted({m for m in maps if m.endswith('.so') and ('repo' in m or 'graft' in m or 'oracle' in m)})
+    print('REFERENCE_ARM_MAPS', sos)
+" > gpurun_out/${tag}_refmaps.log 2>&1 ;;
   esac
 done
 ls -la gpurun_out
