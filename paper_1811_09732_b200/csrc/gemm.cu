@@ -95,12 +95,41 @@ struct Smem {
 // straight from registers. A relaxed cluster barrier (arrive once my inputs
 // have landed, wait at exit) keeps every source alive until its blocks are
 // read.
+//
+// A launch runs one GEMM, or two independent GEMMs of the same tile width
+// and split count side by side (a job table in the kernel parameters: blocks
+// [0, t0) run job 0, the rest job 1) -- ResNet's downsample and the first
+// 1x1 conv of a stage read the same input, so they share one launch instead
+// of adding a dependent step to the chain.
+struct alignas(64) Job {
+  CUtensorMap ta, tb, tr, td;  // A, B, residual, output tile maps
+  uint16_t* D;
+  const float* scale;
+  const float* bias;
+  int M, N, K, ldd, has_res, relu, kper, tma_out, tiles_m;
+  ConvGeom cg;
+};
+struct Jobs {
+  Job j[2];
+  int t0;  // output tiles of job 0 (blocks >= t0 belong to job 1)
+};
+
 template <int BN, int STAGES, int S>
-__global__ void __launch_bounds__(kThreads, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmD, uint16_t* D,
-                   int M, int N, int K, int ldd, const float* __restrict__ scale, const float* __restrict__ bias,
-                   int has_res, int relu, int kper, int tma_out, const ConvGeom cg) {
+__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ Jobs jobs) {
+  const int jb = int(blockIdx.x) < jobs.t0 ? 0 : 1;
+  const Job& J = jobs.j[jb];
+  const CUtensorMap& tmA = J.ta;
+  const CUtensorMap& tmB = J.tb;
+  const CUtensorMap& tmR = J.tr;
+  const CUtensorMap& tmD = J.td;
+  uint16_t* const D = J.D;
+  const float* __restrict__ scale = J.scale;
+  const float* __restrict__ bias = J.bias;
+  const int M = J.M, N = J.N, K = J.K, ldd = J.ldd, has_res = J.has_res, relu = J.relu, kper = J.kper,
+            tma_out = J.tma_out;
+  const ConvGeom& cg = J.cg;
+  const int tile = int(blockIdx.x) - (jb ? jobs.t0 : 0);  // this job's output tile: M-tile fastest
+  const int mt = tile % J.tiles_m, nt = tile / J.tiles_m;
   constexpr bool SPLIT = S > 1;
   constexpr int CW = BN / S;  // split-K: columns of the slice this CTA owns
   static_assert(CW % 8 == 0, "split slices are >= 8 columns");
@@ -117,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* s_bias = reinterpret_cast<float*>(smem + L::BIAS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int m0 = mt * BM, n0 = nt * BN;
   const int z = SPLIT ? int(blockIdx.z) : 0;
   const int kblocks = (K + BK - 1) / BK;
   const int kb0 = z * kper, kb1 = min(kblocks, kb0 + kper);  // this split's k-blocks
@@ -126,9 +155,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Implicit conv: this tile = image ti, output rows [th*hbox, +hbox), cols [tw*wbox, +wbox).
   int ti = 0, th = 0, tw = 0;
   if (cg.impl) {
-    tw = blockIdx.x % cg.tiles_w;
-    th = (blockIdx.x / cg.tiles_w) % cg.tiles_h;
-    ti = blockIdx.x / (cg.tiles_w * cg.tiles_h);
+    tw = mt % cg.tiles_w;
+    th = (mt / cg.tiles_w) % cg.tiles_h;
+    ti = mt / (cg.tiles_w * cg.tiles_h);
   }
   const int wbox = 1 << cg.wbox_log2;
   // Global output row of tile row rl, or -1 outside the output.
@@ -234,9 +263,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     unsigned smid;
     asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
     GT_SET(gt_slot, 0, (uint64_t(M) << 32) | uint32_t(N));
-    GT_SET(gt_slot, 1, (uint64_t(K) << 32) | (blockIdx.z << 16) | blockIdx.y);
+    GT_SET(gt_slot, 1, (uint64_t(K) << 32) | (blockIdx.z << 16) | uint32_t(nt));
     GT_SET(gt_slot, 2, gtimer());
-    GT_SET(gt_slot, 7, smid | (uint64_t(blockIdx.x) << 32));
+    GT_SET(gt_slot, 7, smid | (uint64_t(mt) << 32));
   }
 #endif
   if (threadIdx.x == 0) {
@@ -528,8 +557,30 @@ EncodeTiled encode_fn() {
   return fn;
 }
 
+void fill_job(Job& j, const Prepared& p, int S) {
+  const Epilogue& e = p.e;
+  j.ta = p.ta;
+  j.tb = p.tb;
+  j.tr = p.tr;
+  j.td = p.td;
+  j.D = e.out;
+  j.scale = e.scale;
+  j.bias = e.bias;
+  j.M = int(p.M);
+  j.N = int(p.N);
+  j.K = int(p.K);
+  j.ldd = int(e.ldo);
+  j.has_res = e.residual ? 1 : 0;
+  j.relu = e.relu ? 1 : 0;
+  const int kblocks = int((p.K + BK - 1) / BK);
+  j.kper = (kblocks + S - 1) / S;
+  j.tma_out = p.tma_out;
+  j.tiles_m = int(tile_rows(p) / BM);
+  j.cg = p.g;
+}
+
 template <int BN, int STAGES, int S>
-void run_bn(const Prepared& p, cudaStream_t stream) {
+void run_bn(const Prepared& p, const Prepared* q, cudaStream_t stream) {
   constexpr size_t smem = Smem<BN, STAGES, S>::TOTAL;
   static_assert(smem <= 227 * 1024, "GEMM shared memory");
   static bool smem_set = false;
@@ -538,10 +589,15 @@ void run_bn(const Prepared& p, cudaStream_t stream) {
                                     int(smem)));
     smem_set = true;
   }
-  const Epilogue& e = p.e;
-  const int kblocks = int((p.K + BK - 1) / BK);
-  const int kper = (kblocks + S - 1) / S;
-  dim3 grid(unsigned(tile_rows(p) / BM), unsigned((p.N + BN - 1) / BN), unsigned(S));
+  Jobs jobs{};
+  fill_job(jobs.j[0], p, S);
+  jobs.t0 = jobs.j[0].tiles_m * int((p.N + BN - 1) / BN);
+  int tiles = jobs.t0;
+  if (q) {
+    fill_job(jobs.j[1], *q, S);
+    tiles += jobs.j[1].tiles_m * int((q->N + BN - 1) / BN);
+  }
+  dim3 grid(unsigned(tiles), 1, unsigned(S));
   // PDL always; split-K launches the splits of a tile as one (1, 1, S) cluster
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
@@ -558,9 +614,7 @@ void run_bn(const Prepared& p, cudaStream_t stream) {
   if (!pdl_enabled()) attr[0] = attr[1];  // keep only the cluster shape
   cfg.attrs = attr;
   cfg.numAttrs = (S > 1 ? 2 : 1) - (pdl_enabled() ? 0 : 1);
-  TRIMS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, S>, p.ta, p.tb, p.tr, p.td, e.out, int(p.M),
-                                int(p.N), int(p.K), int(e.ldo), e.scale, e.bias, e.residual ? 1 : 0, e.relu ? 1 : 0,
-                                kper, p.tma_out, p.g));
+  TRIMS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, S>, jobs));
 }
 
 // Residual tile maps: bf16 [rows][ldr] (or NHWC [n][P][Q][ldr] for an
@@ -671,25 +725,29 @@ Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn) 
   return p;
 }
 
-void run(const Prepared& p, cudaStream_t stream) {
+void run(const Prepared& p, cudaStream_t stream) { run_pair(p, nullptr, stream); }
+
+void run_pair(const Prepared& p, const Prepared* q, cudaStream_t stream) {
   if (p.splits < 1 || p.splits > kMaxSplits || (p.splits & (p.splits - 1)) || (p.bn / p.splits) % 8 ||
       (p.bn == 256 && p.splits > 1))
     raise(Errc::InvalidArgument, "GEMM split count");
+  if (q && (q->bn != p.bn || q->splits != p.splits || q->lean != p.lean))
+    raise(Errc::InvalidArgument, "grouped GEMMs need the same tile width, split count and variant");
   if (p.lean && p.splits == 1 && p.bn != 256) {  // <= ~110 KB: two CTAs per SM
-    if (p.bn == 64) run_bn<64, 3, 1>(p, stream);
-    else run_bn<128, 2, 1>(p, stream);
+    if (p.bn == 64) run_bn<64, 3, 1>(p, q, stream);
+    else run_bn<128, 2, 1>(p, q, stream);
     return;
   }
   switch (p.bn * 16 + p.splits) {
-    case 64 * 16 + 1: run_bn<64, 6, 1>(p, stream); break;
-    case 64 * 16 + 2: run_bn<64, 6, 2>(p, stream); break;
-    case 64 * 16 + 4: run_bn<64, 6, 4>(p, stream); break;
-    case 64 * 16 + 8: run_bn<64, 6, 8>(p, stream); break;
-    case 128 * 16 + 1: run_bn<128, 5, 1>(p, stream); break;
-    case 128 * 16 + 2: run_bn<128, 4, 2>(p, stream); break;
-    case 128 * 16 + 4: run_bn<128, 4, 4>(p, stream); break;
-    case 128 * 16 + 8: run_bn<128, 4, 8>(p, stream); break;
-    default: run_bn<256, 3, 1>(p, stream); break;
+    case 64 * 16 + 1: run_bn<64, 6, 1>(p, q, stream); break;
+    case 64 * 16 + 2: run_bn<64, 6, 2>(p, q, stream); break;
+    case 64 * 16 + 4: run_bn<64, 6, 4>(p, q, stream); break;
+    case 64 * 16 + 8: run_bn<64, 6, 8>(p, q, stream); break;
+    case 128 * 16 + 1: run_bn<128, 5, 1>(p, q, stream); break;
+    case 128 * 16 + 2: run_bn<128, 4, 2>(p, q, stream); break;
+    case 128 * 16 + 4: run_bn<128, 4, 4>(p, q, stream); break;
+    case 128 * 16 + 8: run_bn<128, 4, 8>(p, q, stream); break;
+    default: run_bn<256, 3, 1>(p, q, stream); break;
   }
 }
 

@@ -74,6 +74,8 @@ Prepared prepare_conv(const void* act, const ConvGeom& g, const Operand& B, cons
 // Output-tile rows of a prepared GEMM (M rounded up to whole tiles).
 uint64_t tile_rows(const Prepared& p);
 void run(const Prepared& p, cudaStream_t stream);
+// Two independent GEMMs (same bn, splits and variant) in one launch.
+void run_pair(const Prepared& p, const Prepared* q, cudaStream_t stream);
 // Split count for a GEMM shape on `sms` SMs.
 int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms);
 // D = epi(A . B^T); bn = 0 picks the tile width; splits = split-K count

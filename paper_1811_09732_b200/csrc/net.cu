@@ -11,6 +11,7 @@
 #include <cmath>
 #include <functional>
 #include <map>
+#include <optional>
 #include <sstream>
 
 #include "cuda_util.hpp"
@@ -110,6 +111,16 @@ bool branches_enabled() {
   return on;
 }
 
+// TRIMS_PAIR=0 launches ResNet's downsample and the stage's first 1x1 conv
+// (same input, independent) separately instead of as one grouped launch.
+bool pairing_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TRIMS_PAIR");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
 // TRIMS_SPLITK=0 turns split-K off (A/B switch).
 bool splitk_enabled() {
   static const bool on = [] {
@@ -197,6 +208,13 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
   Act cur;
 
   std::map<std::string, int> branch_of;  // named output -> side branch producing it
+  // A GEMM held back to share the next layer's launch (an independent conv
+  // reading the same input): its prepared GEMM and rebind.
+  struct Pending {
+    std::shared_ptr<gemm::Prepared> prep;
+    std::function<void(cudaStream_t)> rebind;
+  };
+  std::optional<Pending> pending;
   for (size_t li = 0; li < layers.size(); ++li) {
     const LayerSpec& l = layers[li];
     const size_t first_step = steps_.size();
@@ -311,7 +329,38 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
                                          prep->bn);
           if (do_params) bind_params(s);
         };
-        steps_.push_back(std::make_unique<Step>(Step{[prep](cudaStream_t s) { gemm::run(*prep, s); }, rebind}));
+        // Pair with the next layer when it is an independent conv on the same
+        // input (ResNet: downsample + the stage's first 1x1 conv).
+        const bool pair_first = pairing_enabled() && !branches_enabled() && groups == 1 && !l.s("src").empty() &&
+                                li + 1 < layers.size() && layers[li + 1].kind == "conv" &&
+                                layers[li + 1].s("src") == l.s("src") && layers[li + 1].i("groups", 1) == 1 &&
+                                !pending;
+        if (pending && groups == 1) {
+          auto a = pending->prep;
+          auto rb_a = pending->rebind;
+          pending.reset();
+          if (a->bn == prep->bn && a->lean == prep->lean) {
+            // one split count for both; the launch must stay one wave
+            int sp = std::min(a->splits, prep->splits);
+            const uint64_t t = tile_rows(*a) / 128 * ((a->N + a->bn - 1) / a->bn) +
+                               gemm::tile_rows(*prep) / 128 * ((prep->N + prep->bn - 1) / prep->bn);
+            while (sp > 1 && t * uint64_t(sp) > uint64_t(sms_)) sp /= 2;
+            a->splits = prep->splits = sp;
+            auto both = [rb_a, rebind](cudaStream_t s) {
+              rb_a(s);
+              rebind(s);
+            };
+            steps_.push_back(std::make_unique<Step>(
+                Step{[a, prep](cudaStream_t s) { gemm::run_pair(*a, prep.get(), s); }, both}));
+          } else {
+            steps_.push_back(std::make_unique<Step>(Step{[a](cudaStream_t s) { gemm::run(*a, s); }, rb_a}));
+            steps_.push_back(std::make_unique<Step>(Step{[prep](cudaStream_t s) { gemm::run(*prep, s); }, rebind}));
+          }
+        } else if (pair_first) {
+          pending = Pending{prep, rebind};
+        } else {
+          steps_.push_back(std::make_unique<Step>(Step{[prep](cudaStream_t s) { gemm::run(*prep, s); }, rebind}));
+        }
         if (branch) steps_.back()->branch = nbranches_;
         first_group = false;
       }
