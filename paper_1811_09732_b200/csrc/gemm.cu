@@ -118,6 +118,7 @@ template <int BN, int STAGES, int S>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ Jobs jobs) {
   const int jb = int(blockIdx.x) < jobs.t0 ? 0 : 1;
   const Job& J = jobs.j[jb];
+  const int tile = int(blockIdx.x) - (jb ? jobs.t0 : 0);  // this job's output tile: M-tile fastest
   const CUtensorMap& tmA = J.ta;
   const CUtensorMap& tmB = J.tb;
   const CUtensorMap& tmR = J.tr;
@@ -127,8 +128,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   const float* __restrict__ bias = J.bias;
   const int M = J.M, N = J.N, K = J.K, ldd = J.ldd, has_res = J.has_res, relu = J.relu, kper = J.kper,
             tma_out = J.tma_out;
-  const ConvGeom& cg = J.cg;
-  const int tile = int(blockIdx.x) - (jb ? jobs.t0 : 0);  // this job's output tile: M-tile fastest
+  // by value: the producer's per-k-block address math reads these from
+  // registers (a reference into the runtime-indexed job made each an indexed
+  // constant load in that loop: VGG-16 +4.5 %)
+  const ConvGeom cg = J.cg;
   const int mt = tile % J.tiles_m, nt = tile / J.tiles_m;
   constexpr bool SPLIT = S > 1;
   constexpr int CW = BN / S;  // split-K: columns of the slice this CTA owns
@@ -770,6 +773,38 @@ int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms) {
   while (s < max_s && bn / (s * 2) >= 8 && tiles * uint64_t(s * 2) <= uint64_t(sms) && kb / uint64_t(s * 2) >= min_kb)
     s *= 2;
   return s;
+}
+
+void choose_tiles(uint64_t rows, uint64_t N, uint64_t K, int sms, int* bn_out, int* splits_out) {
+  // Cost model of one batch-1 layer (per-CTA phases measured by
+  // scripts/gemm_trace.py): each CTA streams ceil(kblocks / S) stages of
+  // (16 KiB A + BN x 128 B of B) from L2 at ~95 KB/us per SM, plus ~2 us of
+  // fixed cost per wave (dependent-launch release, first tile, epilogue) and
+  // ~0.8 us more for a split-K reduction. Candidates: BN 64/128/256 (256 only
+  // unsplit, N % 256 == 0), S 1/2/4/8 with slices >= 8 columns, >= 2 k-blocks
+  // per split and split launches within one wave.
+  const double bw = 95.0, c_wave = 2.0, c_split = 0.8;
+  const uint64_t mt = (rows + BM - 1) / BM, kb = (K + BK - 1) / BK;
+  double best = 1e30;
+  int bb = 64, bs = 1;
+  for (int bn : {64, 128, 256}) {
+    if (bn == 256 && N % 256) continue;
+    for (int sp : {1, 2, 4, 8}) {
+      if ((bn == 256 && sp > 1) || bn / sp < 8 || (sp > 1 && kb / uint64_t(sp) < 2)) continue;
+      const uint64_t ctas = mt * ((N + bn - 1) / bn) * uint64_t(sp);
+      if (sp > 1 && ctas > uint64_t(sms)) continue;
+      const double waves = double((ctas + uint64_t(sms) - 1) / uint64_t(sms));
+      const double per_kb = (16.0 + bn * 128.0 / 1024.0);  // KB per stage
+      const double c = waves * (c_wave + double((kb + sp - 1) / sp) * per_kb / bw) + (sp > 1 ? c_split : 0.0);
+      if (c < best - 1e-9) {
+        best = c;
+        bb = bn;
+        bs = sp;
+      }
+    }
+  }
+  *bn_out = bb;
+  *splits_out = bs;
 }
 
 uint64_t tile_rows(const Prepared& p) {

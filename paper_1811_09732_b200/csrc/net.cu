@@ -121,6 +121,16 @@ bool pairing_enabled() {
   return on;
 }
 
+// TRIMS_TILE_PICK=rule keeps the older tile-width / split rules instead of
+// gemm::choose_tiles' cost model (A/B switch).
+bool tile_model_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TRIMS_TILE_PICK");
+    return !(e && std::string(e) == "rule");
+  }();
+  return on;
+}
+
 // TRIMS_SPLITK=0 turns split-K off (A/B switch).
 bool splitk_enabled() {
   static const bool on = [] {
@@ -317,8 +327,29 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
             implicit ? gemm::prepare_conv(in.p, gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg),
                                           Bop, e)
                      : gemm::prepare({A, M, uint64_t(kp), uint64_t(direct ? cin : kp)}, Bop, e));
-        if (split_ok)
+        // the same GEMM prepared with another tile width
+        auto remake = [&](int bn) {
+          return std::make_shared<gemm::Prepared>(
+              implicit ? gemm::prepare_conv(in.p,
+                                            gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg),
+                                            Bop, e, bn)
+                       : gemm::prepare({A, M, uint64_t(kp), uint64_t(direct ? cin : kp)}, Bop, e, bn));
+        };
+        if (split_ok && tile_model_enabled()) {
+          int bn = 0, sp = 1;
+          gemm::choose_tiles(gemm::tile_rows(*prep), uint64_t(kg), uint64_t(kp), sms_, &bn, &sp);
+          if (bn != prep->bn) prep = remake(bn);
+          prep->splits = sp;
+        } else if (split_ok) {
           prep->splits = gemm::pick_splits(gemm::tile_rows(*prep), uint64_t(kg), uint64_t(kp), prep->bn, sms_);
+        }
+        // second GEMM of a grouped launch: the first one's tile width
+        if (pending && groups == 1 && pending->prep->bn != prep->bn &&
+            !(pending->prep->bn == 256 && prep->N % 256)) {
+          const int sp = prep->splits;
+          prep = remake(pending->prep->bn);
+          prep->splits = pending->prep->bn == 256 ? 1 : sp;
+        }
         prep->lean = lean;
         const uint64_t b_off = w_off + uint64_t(gi) * kg * rsc * 2;
         const bool do_params = first_group && bind_params;
@@ -339,7 +370,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
           auto a = pending->prep;
           auto rb_a = pending->rebind;
           pending.reset();
-          if (a->bn == prep->bn && a->lean == prep->lean) {
+          if (a->bn == prep->bn && a->lean == prep->lean && (a->bn != 256 || (a->splits == 1 && prep->splits == 1))) {
             // one split count for both; the launch must stay one wave
             int sp = std::min(a->splits, prep->splits);
             const uint64_t t = tile_rows(*a) / 128 * ((a->N + a->bn - 1) / a->bn) +

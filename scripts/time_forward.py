@@ -23,7 +23,7 @@ with Store(StoreOptions(disk_cache_dir=d, fast_capacity_bytes=4 << 30, host_capa
                         convert_to="bf16", permute_4d=True)) as s:
     cli = Client(s)
     v = cli.open(C.arch_key(arch), force_shared=True)
-    net = BoundNet(v, arch, batch)
+    net = BoundNet(v, arch, batch, mode=os.environ.get("TRIMS_NET_MODE", "latency"))
     x = torch.randn(batch, 3, arch.input_hw, arch.input_hw).pin_memory()
     st = torch.cuda.current_stream()
     for _ in range(5):
