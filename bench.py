@@ -701,8 +701,8 @@ def request_latencies(work: str, arch, dev: int, batch: int = 1, reps: int = 7) 
                            "hot_frac": round(out["compute_only"] / out["hot"]["e2e"], 4),
                            "forward_ideal_ms": round(fwd_ideal, 4),
                            "forward_frac": round(fwd_ideal / out["forward_device_ms"], 4),
-                           "forward_note": "batch 1: per-layer latency bound (57/23/22 dependent kernels), not "
-                                           "HBM or tensor bound"}
+                           "forward_note": f"batch 1: per-layer latency bound ({net.launches} dependent kernels), "
+                                           "not HBM or tensor bound"}
         out["kernels_per_forward"] = net.launches
         cli.close(v)
     nets["net"].close()

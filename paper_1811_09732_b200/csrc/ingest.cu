@@ -148,19 +148,16 @@ __device__ __forceinline__ uint32_t f64_to_f32(uint64_t u) {
   return __float_as_uint(__double2float_rn(__longlong_as_double((long long)u)));
 }
 
+// f16 -> f32 is exact; the hardware widening convert handles normals and
+// subnormals in one instruction (the software normalisation loop it replaces
+// made the f16 transform variants spill). Inf/NaN keep their payload bits
+// verbatim, as the oracle does (the hardware would quiet a signalling NaN).
 __device__ __forceinline__ uint32_t f16_to_f32(uint16_t hbits) {
-  uint32_t h = hbits, sign = (h & 0x8000u) << 16, e = (h >> 10) & 0x1f, m = h & 0x3ff;
-  if (e == 0x1f) return sign | 0x7f800000u | (m << 13);
-  if (e == 0) {
-    if (m == 0) return sign;
-    int ex = -1;
-    do {
-      m <<= 1;
-      ++ex;
-    } while (!(m & 0x400));
-    return sign | (uint32_t(127 - 15 - ex) << 23) | ((m & 0x3ff) << 13);
-  }
-  return sign | ((e + 112) << 23) | (m << 13);
+  if ((hbits & 0x7c00u) == 0x7c00u)
+    return (uint32_t(hbits & 0x8000u) << 16) | 0x7f800000u | (uint32_t(hbits & 0x3ffu) << 13);
+  float f;
+  asm("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"(hbits));
+  return __float_as_uint(f);
 }
 
 template <int S, int D>
@@ -331,7 +328,9 @@ __device__ uint64_t tile_pull(const Tile& t, const uint8_t* src, uint8_t* dst) {
 constexpr int kCvtUnroll = 8;
 template <int S, int D>
 __device__ uint64_t tile_cvt(const Tile& t, const uint8_t* src, uint8_t* dst) {
-  constexpr int kUnroll = kCvtUnroll;
+  // f64 sources: a word is 32 source bytes, so half the groups keep the same
+  // bytes in flight without spilling
+  constexpr int kUnroll = S == 0 ? kCvtUnroll / 2 : kCvtUnroll;
   using ST = typename Bits<S>::T;
   using DT = typename Bits<D>::T;
   constexpr int DS = esize<D>(), SS = esize<S>(), EPW = 8 / DS;
@@ -472,7 +471,7 @@ __device__ uint64_t tile_perm(const Tile& t, const uint8_t* src, uint8_t* dst, u
 // pressure at what that pair needs; tiles of other pairs in the same range are
 // skipped (the host launches one kernel per pair present, usually exactly one).
 template <int S, int D>
-__global__ void __launch_bounds__(kThreads, 3) transform_kernel(const Tile* __restrict__ tiles, uint32_t ntiles,
+__global__ void __launch_bounds__(kThreads, 2) transform_kernel(const Tile* __restrict__ tiles, uint32_t ntiles,
                                                              const uint8_t* __restrict__ src,
                                                              uint8_t* __restrict__ dst,
                                                              unsigned long long* __restrict__ sums) {
