@@ -218,6 +218,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
   Act cur;
 
   std::map<std::string, int> branch_of;  // named output -> side branch producing it
+  bool flat_done = false;                // a pool wrote its output flattened (NCHW) for the next flatten
   // A GEMM held back to share the next layer's launch (an independent conv
   // reading the same input): its prepared GEMM and rebind.
   struct Pending {
@@ -405,11 +406,25 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       const Act in = cur;
       const int P = (in.h + 2 * pad - k) / st + 1, Q = (in.w + 2 * pad - k) / st + 1;
       const Act out{reinterpret_cast<uint16_t*>(alloc(uint64_t(batch) * P * Q * in.c * 2)), batch, P, Q, in.c};
+      // A pool feeding a flatten writes NCHW itself (the flatten step is then
+      // free): one launch less for VGG / AlexNet. TRIMS_POOL_NCHW=0: A/B.
+      static const bool pool_nchw_on = [] {
+        const char* e = std::getenv("TRIMS_POOL_NCHW");
+        return !(e && std::string(e) == "0");
+      }();
+      const bool nchw = pool_nchw_on && P * Q > 1 && l.s("out").empty() && li + 1 < layers.size() &&
+                        layers[li + 1].kind == "flatten";
       steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) {
-        nn::maxpool(in.p, out.p, in.n, in.h, in.w, in.c, k, st, pad, P, Q, s);
+        nn::maxpool(in.p, out.p, in.n, in.h, in.w, in.c, k, st, pad, P, Q, s, nchw);
       }}));
       if (!l.s("out").empty()) named[l.s("out")] = out;
-      cur = out;
+      if (nchw) {
+        cur = {out.p, batch, 1, 1, P * Q * in.c};  // already flattened (NCHW order)
+        flat_done = true;
+        produced = cur;
+      } else {
+        cur = out;
+      }
     } else if (l.kind == "pool_avg") {
       const Act in = cur;
       const Act out{reinterpret_cast<uint16_t*>(alloc(uint64_t(batch) * in.c * 2)), batch, 1, 1, in.c};
@@ -419,7 +434,9 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       cur = out;
     } else if (l.kind == "flatten") {
       const Act in = cur;
-      if (in.h * in.w > 1) {  // FC weights expect torch's NCHW flatten order
+      if (flat_done) {  // the pool before already wrote the NCHW-flattened vector
+        flat_done = false;
+      } else if (in.h * in.w > 1) {  // FC weights expect torch's NCHW flatten order
         const Act out{reinterpret_cast<uint16_t*>(alloc(in.elems() * 2)), batch, 1, 1, in.h * in.w * in.c};
         steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) {
           nn::flatten_nchw(in.p, out.p, in.n, in.h * in.w, in.c, s);
@@ -481,7 +498,8 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
     attach_joins();
     if (l.kind != "input") {
       if (l.kind == "fc" && int(li) == last_fc) taps_.push_back({logits_, batch, 1, 1, classes_, 1});
-      else if (l.kind == "conv") taps_.push_back({produced.p, produced.n, produced.h, produced.w, produced.c, 0});
+      else if (l.kind == "conv" || (l.kind == "pool_max" && produced.p))
+        taps_.push_back({produced.p, produced.n, produced.h, produced.w, produced.c, 0});
       else taps_.push_back({cur.p, cur.n, cur.h, cur.w, cur.c, 0});
     }
   }

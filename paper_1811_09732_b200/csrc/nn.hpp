@@ -18,8 +18,9 @@ namespace trims::nn {
 void input_prep(const float* in_nchw, uint16_t* out_nhwc, int N, int C, int H, int W, cudaStream_t s);
 void im2col(const uint16_t* in, uint16_t* A, int N, int H, int W, int Ctot, int c_off, int Cg, int R, int S, int stride,
             int pad, int P, int Q, int Kp, cudaStream_t s);
+// nchw: write NCHW (the flatten order of a following FC) instead of NHWC.
 void maxpool(const uint16_t* in, uint16_t* out, int N, int H, int W, int C, int k, int stride, int pad, int P, int Q,
-             cudaStream_t s);
+             cudaStream_t s, bool nchw = false);
 void avgpool_global(const uint16_t* in, uint16_t* out, int N, int HW, int C, cudaStream_t s);
 // im2col straight from the fp32 NCHW network input (the first conv): fuses the
 // input layout/precision prep into the column build. Columns in (r, s, c)

@@ -89,10 +89,12 @@ __global__ void im2col_kernel(const uint16_t* __restrict__ in, uint16_t* __restr
 // Max pool, 8 channels per thread, 32-bit index math; KS = the window size
 // when it is a compile-time 2 or 3 (all KS*KS loads issued before the max),
 // 0 = generic runtime window.
+// nchw != 0: write the output in NCHW order (torch's flatten order for a
+// following FC layer), so no separate flatten pass is needed.
 template <int KS>
 __global__ void __launch_bounds__(256) maxpool_kernel(const uint16_t* __restrict__ in, uint16_t* __restrict__ out,
                                                       int N, int H, int W, int C, int k, int stride, int pad, int P,
-                                                      int Q) {
+                                                      int Q, int nchw) {
   pdl_wait();  // reads the previous layer's output / writes shared scratch
   pdl_trigger();
   const uint32_t C8 = uint32_t(C) / 8, total = uint32_t(N) * P * Q * C8;
@@ -132,6 +134,12 @@ __global__ void __launch_bounds__(256) maxpool_kernel(const uint16_t* __restrict
           if (x >= 0 && x < W) fold(*reinterpret_cast<const uint4*>(img + (uint64_t(y) * W + x) * C));
         }
       }
+    }
+    if (nchw) {  // 8 channels of one pixel -> 8 planes
+      uint16_t* o = out + (uint64_t(n) * C + c) * P * Q + uint64_t(p) * Q + q;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[uint64_t(j) * P * Q] = to_bf(m[j]);
+      continue;
     }
     uint32_t o[4];
 #pragma unroll
@@ -395,12 +403,13 @@ void im2col_input(const float* in, uint16_t* A, int N, int C, int H, int W, int 
 }
 
 void maxpool(const uint16_t* in, uint16_t* out, int N, int H, int W, int C, int k, int stride, int pad, int P, int Q,
-             cudaStream_t s) {
+             cudaStream_t s, bool nchw) {
   if (C % 8) raise(Errc::InvalidArgument, "maxpool needs C % 8 == 0");
   const dim3 g(blocks(uint64_t(N) * P * Q * C / 8));
-  if (k == 3) launch_pdl(maxpool_kernel<3>, g, dim3(256), 0, s, in, out, N, H, W, C, k, stride, pad, P, Q);
-  else if (k == 2) launch_pdl(maxpool_kernel<2>, g, dim3(256), 0, s, in, out, N, H, W, C, k, stride, pad, P, Q);
-  else launch_pdl(maxpool_kernel<0>, g, dim3(256), 0, s, in, out, N, H, W, C, k, stride, pad, P, Q);
+  const int o = nchw ? 1 : 0;
+  if (k == 3) launch_pdl(maxpool_kernel<3>, g, dim3(256), 0, s, in, out, N, H, W, C, k, stride, pad, P, Q, o);
+  else if (k == 2) launch_pdl(maxpool_kernel<2>, g, dim3(256), 0, s, in, out, N, H, W, C, k, stride, pad, P, Q, o);
+  else launch_pdl(maxpool_kernel<0>, g, dim3(256), 0, s, in, out, N, H, W, C, k, stride, pad, P, Q, o);
   TRIMS_CUDA(cudaGetLastError());
 }
 
