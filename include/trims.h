@@ -333,6 +333,12 @@ int trims_gemm_bf16(const void* A, uint64_t M, uint64_t K, uint64_t lda, const v
 int trims_gemm_bf16_split(const void* A, uint64_t M, uint64_t K, uint64_t lda, const void* B, uint64_t N,
                           uint64_t ldb, void* D, uint64_t ldd, const float* scale, const float* bias,
                           const void* residual, uint64_t ldr, int relu, int bn, int splits, void* stream);
+/* The same with weight multicast: mc = 1, 2, 4 or 8 consecutive M-tiles form
+ * one thread-block cluster dimension and share every weight (B) stage by TMA
+ * multicast (splits * mc <= 8; bn 64 or 128). */
+int trims_gemm_bf16_ex(const void* A, uint64_t M, uint64_t K, uint64_t lda, const void* B, uint64_t N, uint64_t ldb,
+                       void* D, uint64_t ldd, const float* scale, const float* bias, const void* residual,
+                       uint64_t ldr, int relu, int bn, int splits, int mc, void* stream);
 
 /* The compute on shared weights (replaces Client::touch, client.cpp:338-359):
  * a CNN bound to a resident manifest whose bf16 KRSC weights start at

@@ -1081,6 +1081,14 @@ int trims_touch_device(int device, const void* dev, uint64_t nbytes, uint64_t* o
       cudaStream_t stream{nullptr};
       unsigned long long* d_sum{nullptr};
       unsigned long long* h_sum{nullptr};
+      ~Scratch() {  // thread exit (errors ignored: the context may already be gone at process exit)
+        if (device < 0) return;
+        cudaSetDevice(device);
+        cudaStreamDestroy(stream);
+        cudaFree(d_sum);
+        cudaFreeHost(h_sum);
+        cudaGetLastError();
+      }
     };
     thread_local std::map<int, Scratch> scratch;
     DeviceGuard g(device);
@@ -1127,6 +1135,18 @@ int trims_gemm_bf16_split(const void* A, uint64_t M, uint64_t K, uint64_t lda, c
     gemm::Epilogue e{static_cast<uint16_t*>(D), ldd, scale, bias, static_cast<const uint16_t*>(residual), ldr,
                      relu != 0};
     gemm::launch({A, M, K, lda}, {B, N, K, ldb}, e, static_cast<cudaStream_t>(stream), bn, splits);
+    return 0;
+  });
+}
+
+int trims_gemm_bf16_ex(const void* A, uint64_t M, uint64_t K, uint64_t lda, const void* B, uint64_t N, uint64_t ldb,
+                       void* D, uint64_t ldd, const float* scale, const float* bias, const void* residual,
+                       uint64_t ldr, int relu, int bn, int splits, int mc, void* stream) {
+  return guard([&] {
+    if (mc != 1 && mc != 2 && mc != 4 && mc != 8) raise(Errc::InvalidArgument, "multicast group of 1, 2, 4 or 8");
+    gemm::Epilogue e{static_cast<uint16_t*>(D), ldd, scale, bias, static_cast<const uint16_t*>(residual), ldr,
+                     relu != 0};
+    gemm::launch({A, M, K, lda}, {B, N, K, ldb}, e, static_cast<cudaStream_t>(stream), bn, splits, mc);
     return 0;
   });
 }

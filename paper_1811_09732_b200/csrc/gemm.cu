@@ -114,7 +114,13 @@ struct Jobs {
   int t0;  // output tiles of job 0 (blocks >= t0 belong to job 1)
 };
 
-template <int BN, int STAGES, int S>
+// MC > 1: the MC CTAs of consecutive M-tiles (same N-tile, same split) form
+// the cluster's x dimension and share every B (weight) stage by TMA
+// multicast: each loads BN/MC rows of it into all MC CTAs, so L2 serves each
+// weight tile once per MC tiles. A stage is refilled only when all MC CTAs'
+// MMAs released it (multicast commits). Off by default (pick_mc): at batch 1
+// it measured slower.
+template <int BN, int STAGES, int S, int MC>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ Jobs jobs) {
   const int jb = int(blockIdx.x) < jobs.t0 ? 0 : 1;
   const Job& J = jobs.j[jb];
@@ -133,6 +139,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   // constant load in that loop: VGG-16 +4.5 %)
   const ConvGeom cg = J.cg;
   const int mt = tile % J.tiles_m, nt = tile / J.tiles_m;
+  const uint32_t cx = uint32_t(mt % MC);  // rank along the cluster's multicast dimension
+  // cluster ranks: x (multicast group) fastest, then the split z
+  auto crank = [&](uint32_t x, uint32_t zz) { return x + uint32_t(MC) * zz; };
   constexpr bool SPLIT = S > 1;
   constexpr int CW = BN / S;  // split-K: columns of the slice this CTA owns
   static_assert(CW % 8 == 0, "split slices are >= 8 columns");
@@ -171,8 +180,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   };
   // Valid rows of the tile (hv x qv box of the output; qv = 1 for a plain
   // GEMM) and tile row -> compact index among them (-1 if outside).
-  const int hv = cg.impl ? min(cg.hbox, cg.P - th * cg.hbox) : min(BM, M - m0);
-  const int qv = cg.impl ? min(wbox, cg.Q - tw * wbox) : 1;
+  // (a padding tile of a multicast group has none)
+  const int hv = max(0, cg.impl ? min(cg.hbox, cg.P - th * cg.hbox) : min(BM, M - m0));
+  const int qv = max(0, cg.impl ? min(wbox, cg.Q - tw * wbox) : 1);
   const int nvalid = hv * qv;
   auto cidx = [&](int rl) -> int {
     if (!cg.impl) return rl < hv ? rl : -1;
@@ -274,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC);  // released by the MMAs of all MC CTAs sharing the stage
     }
     mbar_init(&accum_full, 1);
     mbar_init(&res_full, 1);
@@ -294,12 +304,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   pdl_trigger();  // the next layer's CTAs may start their prologue now
   // every split's receive barrier is initialised before anyone pushes into it
   // (off the critical path: this runs under the previous layer's tail)
-  if (SPLIT) {
+  if (SPLIT || MC > 1) {
     cluster_arrive_relaxed();
     cluster_wait();
   }
   const uint32_t tmem = tmem_base;
 
+  // multicast group of this CTA (same split z): cluster ranks z*MC .. z*MC+MC-1
+  const uint16_t mc_mask = uint16_t(((1u << MC) - 1u) << (uint32_t(MC) * uint32_t(z)));
+  // B stage of k-block kb: whole (MC = 1), or this CTA's BN/MC rows to the group
+  auto load_b = [&](uint8_t* sa, int kb, uint64_t* bar) {
+    if constexpr (MC == 1) {
+      tma_load_2d(sa + L::A_BYTES, &tmB, kb * BK, n0, bar);
+    } else {
+      constexpr int SR = BN / MC;  // rows per slice (>= 16: 1 KiB-aligned swizzle atoms)
+      tma_load_2d_mc(sa + L::A_BYTES + cx * SR * 128, &tmB, kb * BK, n0 + int(cx) * SR, bar, mc_mask);
+    }
+  };
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
       // Weights (B) do not depend on the previous kernel: the first stages'
@@ -308,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       for (int i = 0; i < pre; ++i) {
         uint8_t* sa = smem + i * L::STAGE_BYTES;
         mbar_expect_tx(&full[i], L::STAGE_BYTES);
-        tma_load_2d(sa + L::A_BYTES, &tmB, (kb0 + i) * BK, n0, &full[i]);
+        load_b(sa, kb0 + i, &full[i]);
       }
       pdl_wait();
 #ifdef TRIMS_GEMM_TRACE
@@ -330,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         uint8_t* sa = smem + s * L::STAGE_BYTES;
         mbar_expect_tx(&full[s], L::STAGE_BYTES);
         load_a(sa, kb, &full[s]);
-        tma_load_2d(sa + L::A_BYTES, &tmB, kb * BK, n0, &full[s]);
+        load_b(sa, kb, &full[s]);
       }
     }
   } else if (warp == 1) {
@@ -347,7 +368,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)
           mma_bf16(tmem, smem_desc_sw128(sa + k * 32), smem_desc_sw128(sb + k * 32), idesc, (i | k) != 0);
-        mma_commit(&empty[s]);  // the stage is free once these MMAs have read it
+        // the stage is free once these MMAs have read it; with multicast every
+        // CTA of the group refills it, so each needs this CTA's release --
+        // except for the last STAGES k-blocks, whose stages are never refilled
+        // (no release arrives at a peer that may already have exited)
+        if constexpr (MC == 1) mma_commit(&empty[s]);
+        else if (i + STAGES < kb1 - kb0) mma_commit_mc(&empty[s], mc_mask);
       }
       mma_commit(&accum_full);
     }
@@ -483,8 +509,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       // warp 4 + i ships block (z + 1 + i) % S: S - 1 bulk copies issued in parallel
       if (lane == 0 && warp - 4 < S - 1) {
         const uint32_t j = uint32_t(z + 1 + warp - 4) % S;
-        bulk_copy_to_cluster(map_shared_rank(smem_u32(smem + L::RECV) + uint32_t(z) * blk, j),
-                             smem_u32(smem) + j * blk, blk, map_shared_rank(smem_u32(&recv_full), j));
+        if (blk)  // (a padding tile of a multicast group has no rows)
+          bulk_copy_to_cluster(map_shared_rank(smem_u32(smem + L::RECV) + uint32_t(z) * blk, crank(cx, j)),
+                               smem_u32(smem) + j * blk, blk, map_shared_rank(smem_u32(&recv_full), crank(cx, j)));
       }
 #ifdef TRIMS_GEMM_TRACE
       if (threadIdx.x == 128) GT_SET(gt_slot, 11, gtimer());
@@ -535,6 +562,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
   if constexpr (SPLIT) {
     if (warp < 4) cluster_arrive_relaxed();
     cluster_wait();
+  } else if constexpr (MC > 1) {
+    // no CTA leaves while a group peer's multicast loads / releases may still
+    // target it (every peer arrives once its own MMAs are complete)
+    cluster_arrive_relaxed();
+    cluster_wait();
   }
   tc_fence_before();
   __syncthreads();
@@ -578,20 +610,23 @@ void fill_job(Job& j, const Prepared& p, int S) {
   const int kblocks = int((p.K + BK - 1) / BK);
   j.kper = (kblocks + S - 1) / S;
   j.tma_out = p.tma_out;
-  j.tiles_m = int(tile_rows(p) / BM);
+  const int mc = std::max(1, p.mc);
+  j.tiles_m = (int(tile_rows(p) / BM) + mc - 1) / mc * mc;  // whole multicast groups (padding tiles have no rows)
   j.cg = p.g;
 }
 
-template <int BN, int STAGES, int S>
+template <int BN, int STAGES, int S, int MC = 1>
 void run_bn(const Prepared& p, const Prepared* q, cudaStream_t stream) {
   constexpr size_t smem = Smem<BN, STAGES, S>::TOTAL;
   static_assert(smem <= 227 * 1024, "GEMM shared memory");
+  static_assert(S * MC <= 8, "portable cluster size");
   static bool smem_set = false;
   if (!smem_set) {
-    TRIMS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TRIMS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, S, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(smem)));
     smem_set = true;
   }
+  if (MC > 1 && q) raise(Errc::InvalidArgument, "multicast GEMMs run alone");
   Jobs jobs{};
   fill_job(jobs.j[0], p, S);
   jobs.t0 = jobs.j[0].tiles_m * int((p.N + BN - 1) / BN);
@@ -601,7 +636,8 @@ void run_bn(const Prepared& p, const Prepared* q, cudaStream_t stream) {
     tiles += jobs.j[1].tiles_m * int((q->N + BN - 1) / BN);
   }
   dim3 grid(unsigned(tiles), 1, unsigned(S));
-  // PDL always; split-K launches the splits of a tile as one (1, 1, S) cluster
+  // PDL always; split-K / multicast launch (MC, 1, S) clusters: the MC
+  // consecutive M-tiles of one N-tile x the S splits of each
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kThreads);
@@ -611,13 +647,13 @@ void run_bn(const Prepared& p, const Prepared* q, cudaStream_t stream) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = 1;
+  attr[1].val.clusterDim.x = unsigned(MC);
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = unsigned(S);
   if (!pdl_enabled()) attr[0] = attr[1];  // keep only the cluster shape
   cfg.attrs = attr;
-  cfg.numAttrs = (S > 1 ? 2 : 1) - (pdl_enabled() ? 0 : 1);
-  TRIMS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, S>, jobs));
+  cfg.numAttrs = (S > 1 || MC > 1 ? 2 : 1) - (pdl_enabled() ? 0 : 1);
+  TRIMS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, S, MC>, jobs));
 }
 
 // Residual tile maps: bf16 [rows][ldr] (or NHWC [n][P][Q][ldr] for an
@@ -728,6 +764,19 @@ Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn) 
   return p;
 }
 
+// TMA ring depths (stages in flight per CTA: at batch 1 a CTA's k-loop is
+// bound by bytes in flight / L2 latency, so deeper is faster while it fits).
+#ifndef TRIMS_ST64
+#define TRIMS_ST64 6
+#endif
+#ifndef TRIMS_ST64S
+#define TRIMS_ST64S 6
+#endif
+#ifndef TRIMS_ST128
+#define TRIMS_ST128 5
+#endif
+constexpr int kSt64 = TRIMS_ST64, kSt64S = TRIMS_ST64S, kSt128 = TRIMS_ST128;
+
 void run(const Prepared& p, cudaStream_t stream) { run_pair(p, nullptr, stream); }
 
 void run_pair(const Prepared& p, const Prepared* q, cudaStream_t stream) {
@@ -736,22 +785,110 @@ void run_pair(const Prepared& p, const Prepared* q, cudaStream_t stream) {
     raise(Errc::InvalidArgument, "GEMM split count");
   if (q && (q->bn != p.bn || q->splits != p.splits || q->lean != p.lean))
     raise(Errc::InvalidArgument, "grouped GEMMs need the same tile width, split count and variant");
+  if (p.mc > 1) {  // weight-multicast groups (single GEMM launches, latency mode)
+    switch (p.bn * 1000 + p.splits * 10 + p.mc) {
+      case 64 * 1000 + 14: run_bn<64, kSt64, 1, 4>(p, q, stream); return;
+      case 64 * 1000 + 18: run_bn<64, kSt64, 1, 8>(p, q, stream); return;
+      case 64 * 1000 + 24: run_bn<64, kSt64S, 2, 4>(p, q, stream); return;
+      case 64 * 1000 + 42: run_bn<64, kSt64S, 4, 2>(p, q, stream); return;
+      case 128 * 1000 + 14: run_bn<128, kSt128, 1, 4>(p, q, stream); return;
+      case 128 * 1000 + 18: run_bn<128, kSt128, 1, 8>(p, q, stream); return;
+      case 128 * 1000 + 24: run_bn<128, 4, 2, 4>(p, q, stream); return;
+      case 128 * 1000 + 42: run_bn<128, 4, 4, 2>(p, q, stream); return;
+      default: raise(Errc::InvalidArgument, "no multicast variant for this tile width / split count");
+    }
+  }
   if (p.lean && p.splits == 1 && p.bn != 256) {  // <= ~110 KB: two CTAs per SM
     if (p.bn == 64) run_bn<64, 3, 1>(p, q, stream);
     else run_bn<128, 2, 1>(p, q, stream);
     return;
   }
   switch (p.bn * 16 + p.splits) {
-    case 64 * 16 + 1: run_bn<64, 6, 1>(p, q, stream); break;
-    case 64 * 16 + 2: run_bn<64, 6, 2>(p, q, stream); break;
-    case 64 * 16 + 4: run_bn<64, 6, 4>(p, q, stream); break;
-    case 64 * 16 + 8: run_bn<64, 6, 8>(p, q, stream); break;
-    case 128 * 16 + 1: run_bn<128, 5, 1>(p, q, stream); break;
+    case 64 * 16 + 1: run_bn<64, kSt64, 1>(p, q, stream); break;
+    case 64 * 16 + 2: run_bn<64, kSt64S, 2>(p, q, stream); break;
+    case 64 * 16 + 4: run_bn<64, kSt64S, 4>(p, q, stream); break;
+    case 64 * 16 + 8: run_bn<64, kSt64S, 8>(p, q, stream); break;
+    case 128 * 16 + 1: run_bn<128, kSt128, 1>(p, q, stream); break;
     case 128 * 16 + 2: run_bn<128, 4, 2>(p, q, stream); break;
     case 128 * 16 + 4: run_bn<128, 4, 4>(p, q, stream); break;
     case 128 * 16 + 8: run_bn<128, 4, 8>(p, q, stream); break;
     default: run_bn<256, 3, 1>(p, q, stream); break;
   }
+}
+
+uint32_t b_box_rows(const Prepared& p) { return uint32_t(p.bn / std::max(1, p.mc)); }
+
+namespace {
+// Co-resident (MC, 1, S) clusters of one GEMM variant on this device.
+template <int BN, int STAGES, int S, int MC>
+int max_clusters() {
+  static const int n = [] {
+    constexpr size_t smem = Smem<BN, STAGES, S>::TOTAL;
+    cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, S, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(MC * 64), 1, unsigned(S));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute a{};
+    a.id = cudaLaunchAttributeClusterDimension;
+    a.val.clusterDim.x = unsigned(MC);
+    a.val.clusterDim.y = 1;
+    a.val.clusterDim.z = unsigned(S);
+    cfg.attrs = &a;
+    cfg.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, gemm_tc_kernel<BN, STAGES, S, MC>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    return c;
+  }();
+  return n;
+}
+
+int mc_capacity(int bn, int splits, int mc) {
+  switch (bn * 1000 + splits * 10 + mc) {
+    case 64 * 1000 + 14: return max_clusters<64, kSt64, 1, 4>();
+    case 64 * 1000 + 18: return max_clusters<64, kSt64, 1, 8>();
+    case 64 * 1000 + 24: return max_clusters<64, kSt64S, 2, 4>();
+    case 64 * 1000 + 42: return max_clusters<64, kSt64S, 4, 2>();
+    case 128 * 1000 + 14: return max_clusters<128, kSt128, 1, 4>();
+    case 128 * 1000 + 18: return max_clusters<128, kSt128, 1, 8>();
+    case 128 * 1000 + 24: return max_clusters<128, 4, 2, 4>();
+    case 128 * 1000 + 42: return max_clusters<128, 4, 4, 2>();
+    default: return 0;
+  }
+}
+}  // namespace
+
+int pick_mc(const Prepared& p, int sms) {
+  // Off by default: measured slower at batch 1 (VGG-16 0.2147 -> 0.2198 ms
+  // with groups of 4, 0.2204 with 8; ResNet-50 0.2141 -> 0.2150; AlexNet flat;
+  // profiles/r3/weight_multicast_ab.log): the k-loops are bound by each SM's
+  // own ingress, not by L2 egress, and a shared stage refills only when the
+  // slowest CTA of the group released it. TRIMS_MC=N enables groups <= N.
+  static const int forced = [] {
+    const char* e = std::getenv("TRIMS_MC");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (forced <= 1 || p.lean || p.bn == 256 || p.splits > 4) return 1;
+  const uint64_t tm = tile_rows(p) / BM, tn = (p.N + p.bn - 1) / p.bn, kb = (p.K + BK - 1) / BK;
+  if (kb / uint64_t(p.splits) < 4) return 1;  // a short k-loop gains nothing from sharing its few stages
+  const uint64_t ctas = tm * tn * uint64_t(p.splits);
+  for (int mc : {8, 4, 2}) {
+    if (mc > forced || p.splits * mc > 8 || tm < uint64_t(mc)) continue;
+    const uint64_t pad = (tm + mc - 1) / mc * mc;
+    if ((pad - tm) * 8 > pad) continue;  // <= 1/8 of the tiles padding
+    const int cap = mc_capacity(p.bn, p.splits, mc);
+    if (cap <= 0) continue;
+    const uint64_t clusters = pad * tn / uint64_t(mc);
+    // one wave stays one wave (a multi-wave launch keeps its wave count)
+    const uint64_t waves_before = (ctas + uint64_t(sms) - 1) / uint64_t(sms);
+    const uint64_t waves_after = (clusters + uint64_t(cap) - 1) / uint64_t(cap);
+    if (waves_after > waves_before) continue;
+    return mc;
+  }
+  return 1;
 }
 
 int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms) {
@@ -857,8 +994,12 @@ Prepared prepare_conv(const void* act, const ConvGeom& g, const Operand& B, cons
   return p;
 }
 
-void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn, int splits) {
+void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn, int splits, int mc) {
   Prepared p = prepare(A, B, e, bn);
+  if (mc > 1) {
+    p.mc = mc;
+    p.tb = make_tmap(B.ptr, B.rows, B.k, B.ld, b_box_rows(p));
+  }
   if (splits == 0) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

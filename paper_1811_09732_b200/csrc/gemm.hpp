@@ -27,6 +27,12 @@ struct Epilogue {
 };
 
 CUtensorMap make_tmap(const void* ptr, uint64_t rows, uint64_t k, uint64_t ld, uint32_t box_rows);
+struct Prepared;
+// Rows of the B (weight) TMA box of a prepared GEMM: BN, or BN / mc.
+uint32_t b_box_rows(const Prepared& p);
+// Weight-multicast group size for a prepared GEMM (its tile width and split
+// count set): 1 when it does not pay or does not fit one wave of clusters.
+int pick_mc(const Prepared& p, int sms);
 
 // Implicit-GEMM convolution geometry: A is read straight from the NHWC bf16
 // activation [N][H][W][C] by 4-D TMA boxes of 64 channels x Wbox x Hbox output
@@ -66,6 +72,10 @@ struct Prepared {
   // Lean variants (splits == 1, BN 64/128): a shallower TMA ring so two CTAs
   // fit one SM's shared memory (throughput mode: many clients' kernels).
   bool lean{false};
+  // Weight multicast: MC consecutive M-tiles (one cluster dimension) share
+  // each B stage by TMA multicast, BN/MC rows loaded by each (the B tensor
+  // map's box is then BN/MC rows: b_box_rows()). 1 = off.
+  int mc{1};
   ConvGeom g{};  // g.impl: A is the implicit im2col of an NHWC activation
 };
 Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn = 0);
@@ -83,6 +93,8 @@ void choose_tiles(uint64_t rows, uint64_t N, uint64_t K, int sms, int* bn, int* 
 int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms);
 // D = epi(A . B^T); bn = 0 picks the tile width; splits = split-K count
 // (1, 2, 4, 8; 0 picks it as the executor does).
-void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn = 0, int splits = 1);
+// mc: weight-multicast group size (1 = off; 2 / 4 / 8 with splits * mc <= 8).
+void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn = 0, int splits = 1,
+            int mc = 1);
 
 }  // namespace trims::gemm

@@ -352,22 +352,26 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
           prep->splits = pending->prep->bn == 256 ? 1 : sp;
         }
         prep->lean = lean;
-        const uint64_t b_off = w_off + uint64_t(gi) * kg * rsc * 2;
-        const bool do_params = first_group && bind_params;
-        auto rebind = [=](cudaStream_t s) {
-          if (first_group && wpad) pad_rows(wptr(w_off), cout, rsc, wpad, kp, s);
-          if (!wpad) prep->tb = gemm::make_tmap(wptr(b_off), uint64_t(kg), uint64_t(kp), uint64_t(kp), prep->bn);
-          else prep->tb = gemm::make_tmap(wpad + uint64_t(gi) * kg * kp, uint64_t(kg), uint64_t(kp), uint64_t(kp),
-                                         prep->bn);
-          if (do_params) bind_params(s);
-        };
         // Pair with the next layer when it is an independent conv on the same
         // input (ResNet: downsample + the stage's first 1x1 conv).
         const bool pair_first = pairing_enabled() && !branches_enabled() && groups == 1 && !l.s("src").empty() &&
                                 li + 1 < layers.size() && layers[li + 1].kind == "conv" &&
                                 layers[li + 1].s("src") == l.s("src") && layers[li + 1].i("groups", 1) == 1 &&
                                 !pending;
-        if (pending && groups == 1) {
+        const bool pair_second = pending && groups == 1;
+        // weight multicast across M-tiles for a GEMM launched alone (latency mode)
+        if (split_ok && !pair_first && !pair_second) prep->mc = gemm::pick_mc(*prep, sms_);
+        const uint64_t b_off = w_off + uint64_t(gi) * kg * rsc * 2;
+        const bool do_params = first_group && bind_params;
+        auto rebind = [=](cudaStream_t s) {
+          if (first_group && wpad) pad_rows(wptr(w_off), cout, rsc, wpad, kp, s);
+          if (!wpad)
+            prep->tb = gemm::make_tmap(wptr(b_off), uint64_t(kg), uint64_t(kp), uint64_t(kp), gemm::b_box_rows(*prep));
+          else prep->tb = gemm::make_tmap(wpad + uint64_t(gi) * kg * kp, uint64_t(kg), uint64_t(kp), uint64_t(kp),
+                                         gemm::b_box_rows(*prep));
+          if (do_params) bind_params(s);
+        };
+        if (pair_second) {
           auto a = pending->prep;
           auto rb_a = pending->rebind;
           pending.reset();
@@ -481,7 +485,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
                           e));
         prep->lean = lean;
         auto rebind = [=](cudaStream_t s) {
-          prep->tb = gemm::make_tmap(wptr(w_off), uint64_t(cout), uint64_t(cin), uint64_t(cin), prep->bn);
+          prep->tb = gemm::make_tmap(wptr(w_off), uint64_t(cout), uint64_t(cin), uint64_t(cin), gemm::b_box_rows(*prep));
           bind_bias(s);
         };
         steps_.push_back(std::make_unique<Step>(Step{[prep](cudaStream_t s) { gemm::run(*prep, s); }, rebind}));
@@ -503,6 +507,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       else taps_.push_back({cur.p, cur.n, cur.h, cur.w, cur.c, 0});
     }
   }
+  if (pending) raise(Errc::Internal, "a grouped GEMM was never launched");
   if (!branch_of.empty()) raise(Errc::InvalidArgument, "a branch output is never consumed");
   if (!logits_) raise(Errc::InvalidArgument, "architecture has no fc output");
   for (const auto& s : steps_) launches_ += s->launches;

@@ -91,3 +91,42 @@ def test_gemm_split_count_validated():
         rc = lib.trims_gemm_bf16_split(A.data_ptr(), 128, 64, 64, A.data_ptr(), 64, 64, D.data_ptr(), 64, None, None,
                                        None, 64, 0, bn, splits, None)
         assert rc != 0
+
+
+@pytest.mark.parametrize("M,N,K,bn,splits,mc", [
+    (3136, 256, 2304, 128, 2, 4), (784, 512, 4608, 128, 4, 2), (12544, 128, 1152, 128, 1, 4),
+    (12544, 64, 576, 64, 1, 8), (3000, 200, 1024, 64, 2, 4), (700, 96, 640, 64, 1, 4),
+    # tile rows not a multiple of the group: padding tiles (no rows) take part in the multicast
+    (300, 256, 1024, 64, 2, 4), (1000, 128, 576, 128, 1, 8),
+])
+@pytest.mark.parametrize("epi", ["plain", "full"])
+def test_gemm_weight_multicast_matches_fp32_reference(M, N, K, bn, splits, mc, epi):
+    """Weight multicast (trims_gemm_bf16_ex): mc consecutive M-tiles share each
+    B stage by TMA multicast; same tolerance, equal to the unshared launch."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(M + N * 3 + K + mc)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    scale = bias = res = None
+    ref = A.float() @ B.float().T
+    if epi == "full":
+        scale = torch.rand(N, device="cuda", generator=g) + 0.5
+        bias = torch.randn(N, device="cuda", generator=g)
+        res = torch.randn(M, N, device="cuda", generator=g).to(torch.bfloat16)
+        ref = torch.relu(ref * scale + bias + res.float())
+    outs = []
+    for m in (mc, 1):
+        D = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+        check(lib.trims_gemm_bf16_ex(A.data_ptr(), M, K, K, B.data_ptr(), N, K, D.data_ptr(), N,
+                                     scale.data_ptr() if scale is not None else None,
+                                     bias.data_ptr() if bias is not None else None,
+                                     res.data_ptr() if res is not None else None, N, int(epi == "full"), bn,
+                                     splits, m, torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        outs.append(D)
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16)), "multicast changed the result"
+    out = outs[0].float()
+    assert torch.isfinite(out).all()
+    err = (out - ref).abs()
+    tol = ref.abs() * 2 ** -8 + 1e-3 * ref.abs().max()
+    assert (err <= tol).all(), f"max err {err.max().item()} (ref max {ref.abs().max().item()})"
