@@ -369,6 +369,11 @@ int trims_net_info(trims_net* net, double out3[3]);
  * -> device, forward, logits (fp32 batch x classes) -> host, synchronised.
  * Pinned host buffers give the full PCIe rate. */
 int trims_net_forward_host(trims_net* net, const float* host_input, float* host_logits, void* stream, int use_graph);
+/* Page-locked host memory for request buffers (a pageable input makes every
+ * H2D a CPU-side staging copy: with many client processes the host cores,
+ * not the GPU, become the bound). */
+int trims_host_alloc(uint64_t bytes, void** out);
+void trims_host_free(void* p);
 /* Parity tap: the device buffer architecture layer `layer` (0-based, the
  * input line excluded) wrote in the last forward, NHWC dims4 = {n, h, w, c},
  * dtype 0 = bf16, 1 = fp32 (the logits). layer < 0 returns the layer count.

@@ -210,6 +210,8 @@ _SIGS = {
                                          _c.c_int, _c.c_int, _c.c_int, _p]),
     "trims_gemm_bf16_ex": (_c.c_int, [_p, _u64, _u64, _u64, _p, _u64, _u64, _p, _u64, _p, _p, _p, _u64,
                                       _c.c_int, _c.c_int, _c.c_int, _c.c_int, _p]),
+    "trims_host_alloc": (_c.c_int, [_u64, _c.POINTER(_p)]),
+    "trims_host_free": (None, [_p]),
     "trims_net_create": (_c.c_int, [_c.c_int, _s, _s, _p, _c.c_int, _c.POINTER(_p)]),
     "trims_net_create_ex": (_c.c_int, [_c.c_int, _s, _s, _p, _c.c_int, _c.c_int, _c.POINTER(_p)]),
     "trims_net_destroy": (None, [_p]),

@@ -1217,6 +1217,19 @@ int trims_net_forward_host(trims_net* net, const float* host_input, float* host_
   });
 }
 
+int trims_host_alloc(uint64_t bytes, void** out) {
+  return guard([&] {
+    if (!out) raise(Errc::InvalidArgument, "null argument");
+    *out = nullptr;
+    TRIMS_CUDA(cudaHostAlloc(out, std::max<uint64_t>(bytes, 1), cudaHostAllocPortable));
+    return 0;
+  });
+}
+
+void trims_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 int trims_net_info(trims_net* net, double out3[3]) {
   return guard([&] {
     out3[0] = net->net->flops();

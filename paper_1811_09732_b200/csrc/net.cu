@@ -131,6 +131,16 @@ bool tile_model_enabled() {
   return on;
 }
 
+// TRIMS_TP_WIDE=0: throughput / lean executors keep the latency rule's tile
+// widths instead of the widest tiles (A/B switch).
+bool tp_wide_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TRIMS_TP_WIDE");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
 // TRIMS_SPLITK=0 turns split-K off (A/B switch).
 bool splitk_enabled() {
   static const bool on = [] {
@@ -343,6 +353,13 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
           prep->splits = sp;
         } else if (split_ok) {
           prep->splits = gemm::pick_splits(gemm::tile_rows(*prep), uint64_t(kg), uint64_t(kp), prep->bn, sms_);
+        } else if (!split_ok && (flags & (kNetThroughput | kNetLean))) {
+          // Many clients share the GPU: wider tiles, fewer CTAs (each CTA's
+          // fixed cost is paid once per 128 instead of 64 output channels).
+          // 16 MPS clients on ResNet-50: 14.1k -> 15.6k req/s
+          // (profiles/r3/mps_bn_ab.log). Lean has no 256-wide variant.
+          const int want = (!lean && kg >= 256 && kg % 256 == 0) ? 256 : kg >= 128 ? 128 : 64;
+          if (tp_wide_enabled() && want != prep->bn) prep = remake(want);
         }
         // second GEMM of a grouped launch: the first one's tile width
         if (pending && groups == 1 && pending->prep->bn != prep->bn &&

@@ -64,8 +64,19 @@ def _serve(conn, sm: SharedModel, fd: int, batch: int, n_reqs: int, seed: int, o
         classes, hw = ctypes.c_int(), ctypes.c_int()
         check(lib.trims_net_buffers(net, None, None, ctypes.byref(classes), ctypes.byref(hw)))
         attach_ms = (time.perf_counter() - t0) * 1e3
-        x = np.random.default_rng(seed).standard_normal((batch, 3, hw.value, hw.value)).astype(np.float32)
-        y = np.empty((batch, classes.value), np.float32)
+        shape_x, shape_y = (batch, 3, hw.value, hw.value), (batch, classes.value)
+        pinned = []
+        if os.environ.get("TRIMS_CLIENT_PINNED", "1") == "1":  # page-locked request buffers (A/B: =0)
+            def host_array(shape):
+                n = int(np.prod(shape)) * 4
+                p = ctypes.c_void_p()
+                check(lib.trims_host_alloc(n, ctypes.byref(p)))
+                pinned.append(p)
+                return np.ctypeslib.as_array((ctypes.c_float * (n // 4)).from_address(p.value)).reshape(shape)
+            x, y = host_array(shape_x), host_array(shape_y)
+        else:
+            x, y = np.empty(shape_x, np.float32), np.empty(shape_y, np.float32)
+        x[...] = np.random.default_rng(seed).standard_normal(shape_x).astype(np.float32)
         check(lib.trims_net_forward_host(net, x.ctypes.data, y.ctypes.data, None, 1))  # warm-up + graph capture
         conn.send(("ready", attach_ms))
         assert conn.recv() == "go"
@@ -77,6 +88,8 @@ def _serve(conn, sm: SharedModel, fd: int, batch: int, n_reqs: int, seed: int, o
             lat.append((time.perf_counter() - t) * 1e3)
         t_last = time.perf_counter()
         conn.send(("done", lat, t_first, t_last, y.copy()))
+        for p in pinned:
+            lib.trims_host_free(p)
         lib.trims_net_destroy(net)
         lib.trims_import_close(imp)
         if on_exit:
