@@ -345,9 +345,21 @@ def run_ours(args):
             large = {"error": repr(e)[:300]}
 
     # ---- BASELINE configs[1]: 16 client processes on one shared HBM copy
-    shared = None if args.quick else shared_clients(work, arch, dev, n_clients=16, n_reqs=args.steps * 5)
+    # (rank 0 only: a single-GPU config; N ranks would start N MPS control
+    # daemons and N x 16 client processes on one node)
+    shared = None
+    if not args.quick and rank == 0:
+        try:
+            shared = shared_clients(work, arch, dev, n_clients=16, n_reqs=args.steps * 5)
+        except Exception as e:  # report, keep the line (the driver needs it)
+            shared = {"error": repr(e)[:300]}
     # ---- BASELINE configs[2] + [4]: 37-model mix / FaaS traces under memory pressure
-    mix = None if args.quick else mix_traces(dev, rank, world)
+    mix = None
+    if not args.quick:
+        try:
+            mix = mix_traces(dev, rank, world)
+        except Exception as e:  # report, keep the line
+            mix = {"error": repr(e)[:300]}
 
     peer = None
     if world > 1:
