@@ -336,6 +336,13 @@ def run_ours(args):
         C.write_arch(vgg19, work, seed=1)
         lat["vgg19"] = request_latencies(work, vgg19, dev)  # BASELINE configs[3]
 
+    batched = None
+    if not args.quick:
+        try:
+            batched = forward_batched(work, dev)
+        except Exception as e:  # report, keep the line
+            batched = {"error": repr(e)[:300]}
+
     # ---- BASELINE configs[3]: a multi-GB model (large8 vgg16-s4, 6.4 GB)
     large = None
     if not args.quick:
@@ -415,6 +422,8 @@ def run_ours(args):
         line["large_model"] = large
     if other_transforms:
         line["transform_by_model"] = other_transforms
+    if batched:
+        line["forward_batched"] = batched
     # warm reload through the store (host tier in resident form: the bf16 bytes
     # cross PCIe), as artifact bytes per second of publish_fast(from_host)
     bd = lat.get("resnet50", {}).get("last_publish_breakdown_ms", {})
@@ -645,6 +654,54 @@ def ncu_traffic() -> dict:
         return {"traffic": None}
     doc = json.load(open(files[-1]))
     return {"traffic": int(doc["step"]["dram_bytes"]), "traffic_source": os.path.relpath(files[-1], ROOT)}
+
+
+def forward_batched(work: str, dev: int, cases=(("resnet50", 32), ("vgg16", 32))) -> dict:
+    """The forward at batch > 1 (the tensor cores' regime; batch 1 is a chain
+    of latency-bound layers): device time of one graph-replayed forward on the
+    store-lent weights, issued TFLOP/s and its fraction of the measured dense
+    bf16 peak (MEASURED_PEAKS.json, burst)."""
+    import torch
+
+    from paper_1811_09732_b200 import catalog as C
+    from paper_1811_09732_b200.client import Client
+    from paper_1811_09732_b200.models import BoundNet
+    from paper_1811_09732_b200.store import Store, StoreOptions
+    try:
+        peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"]
+        peak_src = "MEASURED_PEAKS.json bf16_tflops (cuBLAS 8192^3, burst)"
+    except (OSError, KeyError, ValueError):
+        peak, peak_src = 2250.0, "nominal dense bf16 (no MEASURED_PEAKS.json)"
+    out = {"peak_tflops": peak, "peak_source": peak_src}
+    with Store(StoreOptions(disk_cache_dir=work, fast_capacity_bytes=4 << 30, host_capacity_bytes=4 << 30,
+                            device=dev, convert_to="bf16", permute_4d=True)) as s:
+        cli = Client(s, device=dev)
+        for name, batch in cases:
+            arch = C.ARCHS[name]()
+            if not os.path.exists(os.path.join(work, C.arch_key(arch).filename)):
+                C.write_arch(arch, work, seed=1)
+            v = cli.open(C.arch_key(arch), force_shared=True)
+            net = BoundNet(v, arch, batch, device=dev)
+            st = torch.cuda.current_stream(dev)
+            x = torch.randn(batch, 3, arch.input_hw, arch.input_hw, device=f"cuda:{dev}")
+            net.input_view().copy_(x)
+            for _ in range(3):
+                net.run(st.cuda_stream, True)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            n = 10
+            e0.record(st)
+            for _ in range(n):
+                net.run(st.cuda_stream, True)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / n
+            tf = net.flops / (ms / 1e3) / 1e12
+            out[f"{name}_b{batch}"] = {"ms": round(ms, 4), "tflops": round(tf, 1), "frac": round(tf / peak, 4),
+                                       "gflop": round(net.flops / 1e9, 2), "launches": net.launches,
+                                       "images_per_s": round(batch / (ms / 1e3), 1)}
+            net.close()
+            cli.close(v)
+    return out
 
 
 def request_latencies(work: str, arch, dev: int, batch: int = 1, reps: int = 7) -> dict:
