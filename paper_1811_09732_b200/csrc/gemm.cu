@@ -120,8 +120,13 @@ struct Jobs {
 // weight tile once per MC tiles. A stage is refilled only when all MC CTAs'
 // MMAs released it (multicast commits). Off by default (pick_mc): at batch 1
 // it measured slower.
+// Lean variants (BN <= 128, <= 3 stages, no split) must fit two CTAs per SM:
+// registers capped at 65536 / (2 x 384) = 85 per thread.
+template <int BN, int STAGES, int S>
+constexpr int min_ctas() { return (BN <= 128 && STAGES <= 3 && S == 1) ? 2 : 1; }
+
 template <int BN, int STAGES, int S, int MC>
-__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ Jobs jobs) {
+__global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_kernel(const __grid_constant__ Jobs jobs) {
   const int jb = int(blockIdx.x) < jobs.t0 ? 0 : 1;
   const Job& J = jobs.j[jb];
   const int tile = int(blockIdx.x) - (jb ? jobs.t0 : 0);  // this job's output tile: M-tile fastest
@@ -202,14 +207,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     const int box = c / 64 - rbox0, chunk = ((c & 63) >> 3) ^ (rl & 7);
     return s_out + box * BM * 64 + rl * 64 + chunk * 8;
   };
-  // scale, bias, residual, ReLU of 8 values at tile column c of row rl -> 4 bf16 pairs
-  auto epi8 = [&](int rl, int c, const float* v, uint32_t* o) {
-    const uint4 r4 = has_res ? *reinterpret_cast<const uint4*>(stage_at(rl, c)) : make_uint4(0, 0, 0, 0);
+  // scale, bias, residual (r4: its 8 bf16 values), ReLU of 8 values at tile
+  // column c of row rl -> 4 bf16 pairs. Scale/bias are read with loads the
+  // compiler may hoist above earlier shared-memory stores (they are never
+  // written in the epilogue): C++ loads would each wait behind the previous
+  // chunk's staging store (possible aliasing), a serial chain of round trips.
+  auto epi8r = [&](int c, const float* v, uint32_t* o, const uint4 r4) {
     const uint32_t rw[4] = {r4.x, r4.y, r4.z, r4.w};
-    const float4 sc0 = *reinterpret_cast<const float4*>(s_scale + c);
-    const float4 sc1 = *reinterpret_cast<const float4*>(s_scale + c + 4);
-    const float4 bi0 = *reinterpret_cast<const float4*>(s_bias + c);
-    const float4 bi1 = *reinterpret_cast<const float4*>(s_bias + c + 4);
+    const float4 sc0 = lds_f4(s_scale + c), sc1 = lds_f4(s_scale + c + 4);
+    const float4 bi0 = lds_f4(s_bias + c), bi1 = lds_f4(s_bias + c + 4);
     const float sc[8] = {sc0.x, sc0.y, sc0.z, sc0.w, sc1.x, sc1.y, sc1.z, sc1.w};
     const float bi[8] = {bi0.x, bi0.y, bi0.z, bi0.w, bi1.x, bi1.y, bi1.z, bi1.w};
 #pragma unroll
@@ -227,12 +233,21 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       o[j] = pack_bf16x2(a, b);
     }
   };
+  auto epi8 = [&](int rl, int c, const float* v, uint32_t* o) {
+    epi8r(c, v, o, has_res ? *reinterpret_cast<const uint4*>(stage_at(rl, c)) : make_uint4(0, 0, 0, 0));
+  };
+  // W staged columns: every residual chunk is read before the first
+  // in-place store, then converted and stored chunk by chunk
   auto finish = [&](int rl, int c0, auto cw_tag, const float* v) {
     constexpr int W = decltype(cw_tag)::value;
+    uint4 res[W / 8];
+#pragma unroll
+    for (int q = 0; q < W / 8; ++q)
+      res[q] = has_res ? *reinterpret_cast<const uint4*>(stage_at(rl, c0 + 8 * q)) : make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int q = 0; q < W / 8; ++q) {
       uint32_t o[4];
-      epi8(rl, c0 + 8 * q, v + 8 * q, o);
+      epi8r(c0 + 8 * q, v + 8 * q, o, res[q]);
       *reinterpret_cast<uint4*>(stage_at(rl, c0 + 8 * q)) = make_uint4(o[0], o[1], o[2], o[3]);
     }
   };
@@ -435,12 +450,30 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
       // this warp's BN/2 columns, 32 per TMEM round trip
 #pragma unroll 1
       for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
+#ifdef TRIMS_GEMM_TRACE
+        const long long q0 = clock64();
+#endif
         uint32_t r[32];
         tmem_ld16_nw(tq + uint32_t(c0), r);
         tmem_ld16_nw(tq + uint32_t(c0 + 16), r + 16);
         tmem_wait_ld();
+#ifdef TRIMS_GEMM_TRACE
+        {  // diagnostic: consume the loaded registers (data actually arrived)
+          uint32_t x = 0;
+#pragma unroll
+          for (int u = 0; u < 32; ++u) x ^= r[u];
+          asm volatile("" ::"r"(x));
+        }
+        const long long q1 = clock64();
+#endif
         finish(rl, c0, std::integral_constant<int, 16>{}, reinterpret_cast<const float*>(r));
         finish(rl, c0 + 16, std::integral_constant<int, 16>{}, reinterpret_cast<const float*>(r + 16));
+#ifdef TRIMS_GEMM_TRACE
+        if (threadIdx.x == 128 && c0 == 0) {  // cycles: TMEM loads until consumed, then the two finishes
+          GT_SET(gt_slot, 12, uint64_t(q1 - q0));
+          GT_SET(gt_slot, 13, uint64_t(clock64() - q1));
+        }
+#endif
       }
 #ifdef TRIMS_GEMM_TRACE
       if (threadIdx.x == 128) GT_SET(gt_slot, 14, gtimer());

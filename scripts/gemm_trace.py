@@ -106,4 +106,5 @@ with Store(StoreOptions(disk_cache_dir=d, fast_capacity_bytes=4 << 30, host_capa
             print(json.dumps({"phases": sig, "wait_to_full": med(3, 4), "mma": med(4, 5),
                               "epi": med(5, 10), "epi_ready": med(5, 9), "ldtm_finish": med(9, 14),
                               "bar": med(14, 15), "copy_out": med(15, 10), "tail": med(10, 6),
+                              "ldtm_cyc": float(np.median(R[:, 12])), "finish_cyc": float(np.median(R[:, 13])),
                               "cta_total": med(2, 6)}))
