@@ -212,7 +212,11 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
   // compiler may hoist above earlier shared-memory stores (they are never
   // written in the epilogue): C++ loads would each wait behind the previous
   // chunk's staging store (possible aliasing), a serial chain of round trips.
-  auto epi8r = [&](int c, const float* v, uint32_t* o, const uint4 r4) {
+  // HR / RL: compile-time residual / ReLU (the unsplit epilogue runs a
+  // specialised copy: predicated-off adds and max still cost issue slots,
+  // and with two warps per scheduler the epilogue is issue-bound)
+  auto epi8t = [&](int c, const float* v, uint32_t* o, const uint4 r4, auto hr_tag, auto rl_tag) {
+    constexpr bool HR = decltype(hr_tag)::value, RL = decltype(rl_tag)::value;
     const uint32_t rw[4] = {r4.x, r4.y, r4.z, r4.w};
     const float4 sc0 = lds_f4(s_scale + c), sc1 = lds_f4(s_scale + c + 4);
     const float4 bi0 = lds_f4(s_bias + c), bi1 = lds_f4(s_bias + c + 4);
@@ -222,15 +226,26 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
     for (int j = 0; j < 4; ++j) {
       float a = v[2 * j] * sc[2 * j] + bi[2 * j];
       float b = v[2 * j + 1] * sc[2 * j + 1] + bi[2 * j + 1];
-      if (has_res) {
+      if constexpr (HR) {
         a += bf16_lo(rw[j]);
         b += bf16_hi(rw[j]);
       }
-      if (relu) {
+      if constexpr (RL) {
         a = fmaxf(a, 0.f);
         b = fmaxf(b, 0.f);
       }
       o[j] = pack_bf16x2(a, b);
+    }
+  };
+  auto epi8r = [&](int c, const float* v, uint32_t* o, const uint4 r4) {  // runtime flags (split path)
+    using T = std::true_type;
+    using F = std::false_type;
+    if (has_res) {
+      if (relu) epi8t(c, v, o, r4, T{}, T{});
+      else epi8t(c, v, o, r4, T{}, F{});
+    } else {
+      if (relu) epi8t(c, v, o, r4, F{}, T{});
+      else epi8t(c, v, o, r4, F{}, F{});
     }
   };
   auto epi8 = [&](int rl, int c, const float* v, uint32_t* o) {
@@ -238,17 +253,21 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
   };
   // W staged columns: every residual chunk is read before the first
   // in-place store, then converted and stored chunk by chunk
-  auto finish = [&](int rl, int c0, auto cw_tag, const float* v) {
+  auto finish_t = [&](int rl, int c0, auto cw_tag, const float* v, auto hr_tag, auto rl_tag) {
     constexpr int W = decltype(cw_tag)::value;
+    constexpr bool HR = decltype(hr_tag)::value;
+    // the row's staging address once; chunk q of the 16-byte chunks at (chunk0 + q) ^ (rl & 7)
+    uint16_t* srow = s_out + (c0 / 64 - rbox0) * BM * 64 + rl * 64;
+    const int chunk0 = (c0 & 63) >> 3, sw = rl & 7;
     uint4 res[W / 8];
 #pragma unroll
     for (int q = 0; q < W / 8; ++q)
-      res[q] = has_res ? *reinterpret_cast<const uint4*>(stage_at(rl, c0 + 8 * q)) : make_uint4(0, 0, 0, 0);
+      res[q] = HR ? *reinterpret_cast<const uint4*>(srow + (((chunk0 + q) ^ sw) << 3)) : make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int q = 0; q < W / 8; ++q) {
       uint32_t o[4];
-      epi8r(c0 + 8 * q, v + 8 * q, o, res[q]);
-      *reinterpret_cast<uint4*>(stage_at(rl, c0 + 8 * q)) = make_uint4(o[0], o[1], o[2], o[3]);
+      epi8t(c0 + 8 * q, v + 8 * q, o, res[q], hr_tag, rl_tag);
+      *reinterpret_cast<uint4*>(srow + (((chunk0 + q) ^ sw) << 3)) = make_uint4(o[0], o[1], o[2], o[3]);
     }
   };
   // 8 finished columns of tile row rl -> D (one 16-byte store when aligned)
@@ -466,8 +485,20 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
         }
         const long long q1 = clock64();
 #endif
-        finish(rl, c0, std::integral_constant<int, 16>{}, reinterpret_cast<const float*>(r));
-        finish(rl, c0 + 16, std::integral_constant<int, 16>{}, reinterpret_cast<const float*>(r + 16));
+        {
+          auto both = [&](auto hr, auto rlu) {
+            finish_t(rl, c0, std::integral_constant<int, 32>{}, reinterpret_cast<const float*>(r), hr, rlu);
+          };
+          using T = std::true_type;
+          using F = std::false_type;
+          if (has_res) {
+            if (relu) both(T{}, T{});
+            else both(T{}, F{});
+          } else {
+            if (relu) both(F{}, T{});
+            else both(F{}, F{});
+          }
+        }
 #ifdef TRIMS_GEMM_TRACE
         if (threadIdx.x == 128 && c0 == 0) {  // cycles: TMEM loads until consumed, then the two finishes
           GT_SET(gt_slot, 12, uint64_t(q1 - q0));
