@@ -336,8 +336,10 @@ def run_ours(args):
         C.write_arch(vgg19, work, seed=1)
         lat["vgg19"] = request_latencies(work, vgg19, dev)  # BASELINE configs[3]
 
+    # single-GPU extras (rank 0 only: the line is rank 0's; N ranks would
+    # e.g. each write their own 6.4 GB artifact)
     batched = None
-    if not args.quick:
+    if not args.quick and rank == 0:
         try:
             batched = forward_batched(work, dev)
         except Exception as e:  # report, keep the line
@@ -345,7 +347,7 @@ def run_ours(args):
 
     # ---- BASELINE configs[3]: a multi-GB model (large8 vgg16-s4, 6.4 GB)
     large = None
-    if not args.quick:
+    if not args.quick and rank == 0:
         try:
             large = large_model(work, dev)
         except Exception as e:  # report, keep the line
@@ -377,7 +379,7 @@ def run_ours(args):
 
     hbm_peak, peak_kind = peaks()
     other_transforms = None
-    if not args.quick:
+    if not args.quick and rank == 0:
         try:
             other_transforms = transform_by_model(dev, args.steps, hbm_peak)
         except Exception as e:  # report, keep the line
