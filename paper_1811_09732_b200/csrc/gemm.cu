@@ -58,6 +58,22 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2).
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)),
+        "l"(*reinterpret_cast<uint64_t*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+  return *reinterpret_cast<float2*>(&d);
+}
 __device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
 
@@ -224,17 +240,16 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
     const float bi[8] = {bi0.x, bi0.y, bi0.z, bi0.w, bi1.x, bi1.y, bi1.z, bi1.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      float a = v[2 * j] * sc[2 * j] + bi[2 * j];
-      float b = v[2 * j + 1] * sc[2 * j + 1] + bi[2 * j + 1];
-      if constexpr (HR) {
-        a += bf16_lo(rw[j]);
-        b += bf16_hi(rw[j]);
-      }
+      // packed pairs (FFMA2 / FADD2: two independent round-to-nearest fp32
+      // ops, bit-identical to the scalar fma + add, half the issue slots)
+      float2 ab = fma2(make_float2(v[2 * j], v[2 * j + 1]), make_float2(sc[2 * j], sc[2 * j + 1]),
+                       make_float2(bi[2 * j], bi[2 * j + 1]));
+      if constexpr (HR) ab = add2(ab, make_float2(bf16_lo(rw[j]), bf16_hi(rw[j])));
       if constexpr (RL) {
-        a = fmaxf(a, 0.f);
-        b = fmaxf(b, 0.f);
+        ab.x = fmaxf(ab.x, 0.f);
+        ab.y = fmaxf(ab.y, 0.f);
       }
-      o[j] = pack_bf16x2(a, b);
+      o[j] = pack_bf16x2(ab.x, ab.y);
     }
   };
   auto epi8r = [&](int c, const float* v, uint32_t* o, const uint4 r4) {  // runtime flags (split path)
