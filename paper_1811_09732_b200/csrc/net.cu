@@ -8,6 +8,8 @@
 // across store evictions/reloads and only pays a few microseconds per layer
 // when a new generation of the model is published.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <functional>
 #include <map>
@@ -559,9 +561,12 @@ const Net::Tap& Net::tap(int i) const {
 
 void Net::rebind(const uint8_t* weights) {
   DeviceGuard g(device_);
+  static const bool prof = std::getenv("TRIMS_REBIND_PROFILE") != nullptr;  // diagnostic: phase times to stderr
+  const auto t0 = std::chrono::steady_clock::now();
   wbase_ = weights;
   for (const auto& s : steps_)
     if (s->rebind) s->rebind(capture_stream_);
+  const auto t1 = std::chrono::steady_clock::now();
   if (!folds_.empty()) {
     std::vector<FoldJob> jobs;
     jobs.reserve(folds_.size());
@@ -572,10 +577,16 @@ void Net::rebind(const uint8_t* weights) {
     nn::bn_fold_batched(d_jobs_, int(jobs.size()), max_fold_c_, 1e-5f, capture_stream_);
   }
   TRIMS_CUDA(cudaStreamSynchronize(capture_stream_));
+  const auto t2 = std::chrono::steady_clock::now();
   // Kernel parameters (tensor maps, pointers) changed: re-record the graph
   // and update the instantiated one in place (same topology) instead of
   // instantiating a new executable graph.
   if (exec_) capture_graph();
+  if (prof) {
+    const auto t3 = std::chrono::steady_clock::now();
+    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    std::fprintf(stderr, "rebind_us steps=%.1f fold_sync=%.1f graph=%.1f\n", us(t0, t1), us(t1, t2), us(t2, t3));
+  }
 }
 
 void Net::capture_graph() {
