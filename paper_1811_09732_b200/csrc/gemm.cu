@@ -81,9 +81,11 @@ __device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v 
 // TMA in SWIZZLE_128B boxes of 64 channels x 128 rows), for split-K launches
 // the receive buffer (S partial blocks of this CTA's column slice), then
 // folded-BN scale/bias.
-template <int BN, int STAGES, int S>
+template <int BN, int STAGES, int S, bool PAIR = false>
 struct Smem {
-  static constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
+  // PAIR (2-SM MMA): this CTA holds half of every B stage (BN/2 rows)
+  static constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2,
+                            STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t RING = STAGES * STAGE_BYTES;
   // split-K: only the 64-channel box holding this CTA's slice
   static constexpr uint32_t RES = RING, RES_BYTES = S > 1 ? BM * 128 : BM * BN * 2;
@@ -143,6 +145,12 @@ constexpr int min_ctas() { return (BN <= 128 && STAGES <= 3 && S == 1) ? 2 : 1; 
 
 template <int BN, int STAGES, int S, int MC>
 __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_kernel(const __grid_constant__ Jobs jobs) {
+  // MC < 0: a 2-SM pair (tcgen05 cta_group::2): the two CTAs of consecutive
+  // M-tiles form a (2, 1, 1) cluster; the leader issues M = 256 MMAs over both
+  // CTAs' A tiles and B halves, each CTA's TMEM holds its 128 rows of D.
+  constexpr bool PAIR = MC < 0;
+  constexpr int CX = PAIR ? -MC : MC;  // cluster x extent
+  static_assert(!PAIR || (S == 1 && MC == -2 && BN >= 128), "2-SM pairs: unsplit, BN >= 128");
   const int jb = int(blockIdx.x) < jobs.t0 ? 0 : 1;
   const Job& J = jobs.j[jb];
   const int tile = int(blockIdx.x) - (jb ? jobs.t0 : 0);  // this job's output tile: M-tile fastest
@@ -160,13 +168,13 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
   // constant load in that loop: VGG-16 +4.5 %)
   const ConvGeom cg = J.cg;
   const int mt = tile % J.tiles_m, nt = tile / J.tiles_m;
-  const uint32_t cx = uint32_t(mt % MC);  // rank along the cluster's multicast dimension
+  const uint32_t cx = uint32_t(mt % CX);  // rank along the cluster's x dimension (multicast group / pair)
   // cluster ranks: x (multicast group) fastest, then the split z
-  auto crank = [&](uint32_t x, uint32_t zz) { return x + uint32_t(MC) * zz; };
+  auto crank = [&](uint32_t x, uint32_t zz) { return x + uint32_t(CX) * zz; };
   constexpr bool SPLIT = S > 1;
   constexpr int CW = BN / S;  // split-K: columns of the slice this CTA owns
   static_assert(CW % 8 == 0, "split slices are >= 8 columns");
-  using L = Smem<BN, STAGES, S>;
+  using L = Smem<BN, STAGES, S, PAIR>;
   constexpr uint32_t TMEM_COLS = BN;  // 64 / 128 / 256: powers of two >= 32
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], accum_full, res_full, recv_full;
@@ -311,10 +319,16 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
   auto load_a = [&](void* dst, int kb, uint64_t* bar) {
     if (cg.impl) {
       const int rs = kb / cg.cblocks, cb = kb - rs * cg.cblocks, r = rs / cg.S, s = rs - r * cg.S;
-      tma_load_4d(dst, &tmA, cg.c_off + cb * BK, tw * wbox * cg.stride - cg.pad + s, th * cg.hbox * cg.stride - cg.pad + r, ti,
-                  bar);
+      const int c0 = cg.c_off + cb * BK, c1 = tw * wbox * cg.stride - cg.pad + s,
+                c2 = th * cg.hbox * cg.stride - cg.pad + r;
+      if constexpr (MC < 0) {
+        tma_load_4d_pair(dst, &tmA, c0, c1, c2, ti, map_shared_rank(smem_u32(bar), 0u));  // leader = rank 0
+      } else {
+        tma_load_4d(dst, &tmA, c0, c1, c2, ti, bar);
+      }
     } else {
-      tma_load_2d(dst, &tmA, kb * BK, m0, bar);
+      if constexpr (MC < 0) tma_load_2d_pair(dst, &tmA, kb * BK, m0, map_shared_rank(smem_u32(bar), 0u));
+      else tma_load_2d(dst, &tmA, kb * BK, m0, bar);
     }
   };
 
@@ -333,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MC);  // released by the MMAs of all MC CTAs sharing the stage
+      mbar_init(&empty[s], MC > 1 ? MC : 1);  // released by the MMAs of all MC CTAs sharing the stage
     }
     mbar_init(&accum_full, 1);
     mbar_init(&res_full, 1);
@@ -346,14 +360,17 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
     // the other splits' blocks of this CTA's slice, in bytes
     if (SPLIT) mbar_expect_tx(&recv_full, uint32_t((S - 1) * nvalid * CW * 4));
   }
-  if (warp == 1) tmem_alloc<TMEM_COLS>(&tmem_base);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_alloc_pair<TMEM_COLS>(&tmem_base);
+    else tmem_alloc<TMEM_COLS>(&tmem_base);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   pdl_trigger();  // the next layer's CTAs may start their prologue now
   // every split's receive barrier is initialised before anyone pushes into it
   // (off the critical path: this runs under the previous layer's tail)
-  if (SPLIT || MC > 1) {
+  if (SPLIT || MC > 1 || PAIR) {
     cluster_arrive_relaxed();
     cluster_wait();
   }
@@ -362,8 +379,12 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
   // multicast group of this CTA (same split z): cluster ranks z*MC .. z*MC+MC-1
   const uint16_t mc_mask = uint16_t(((1u << MC) - 1u) << (uint32_t(MC) * uint32_t(z)));
   // B stage of k-block kb: whole (MC = 1), or this CTA's BN/MC rows to the group
+  // pair: every load completes on the LEADER's barrier (its MMA consumes both CTAs' stages)
+  auto pair_bar = [&](uint64_t* bar) { return map_shared_rank(smem_u32(bar), crank(0, uint32_t(z))); };
   auto load_b = [&](uint8_t* sa, int kb, uint64_t* bar) {
-    if constexpr (MC == 1) {
+    if constexpr (PAIR) {
+      tma_load_2d_pair(sa + L::A_BYTES, &tmB, kb * BK, n0 + int(cx) * (BN / 2), pair_bar(bar));
+    } else if constexpr (MC == 1) {
       tma_load_2d(sa + L::A_BYTES, &tmB, kb * BK, n0, bar);
     } else {
       constexpr int SR = BN / MC;  // rows per slice (>= 16: 1 KiB-aligned swizzle atoms)
@@ -375,9 +396,17 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
       // Weights (B) do not depend on the previous kernel: the first stages'
       // B tiles are requested before waiting on it, the activations after.
       const int pre = min(STAGES, kb1 - kb0);
+      // pair: the leader's barrier counts both CTAs' bytes; the peer only loads
+      auto expect = [&](uint64_t* bar) {
+        if constexpr (PAIR) {
+          if (cx == 0) mbar_expect_tx(bar, 2 * L::STAGE_BYTES);
+        } else {
+          mbar_expect_tx(bar, L::STAGE_BYTES);
+        }
+      };
       for (int i = 0; i < pre; ++i) {
         uint8_t* sa = smem + i * L::STAGE_BYTES;
-        mbar_expect_tx(&full[i], L::STAGE_BYTES);
+        expect(&full[i]);
         load_b(sa, kb0 + i, &full[i]);
       }
       pdl_wait();
@@ -398,14 +427,14 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
         const int s = i % STAGES;
         mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
         uint8_t* sa = smem + s * L::STAGE_BYTES;
-        mbar_expect_tx(&full[s], L::STAGE_BYTES);
+        expect(&full[s]);
         load_a(sa, kb, &full[s]);
         load_b(sa, kb, &full[s]);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer
-      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+    if (lane == 0 && (!PAIR || cx == 0)) {  // ---- MMA issuer (a pair's leader only)
+      constexpr uint32_t idesc = idesc_bf16_f32(PAIR ? 2 * BM : BM, BN);
       for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
         const int s = i % STAGES;
         mbar_wait(&full[s], (i / STAGES) & 1);
@@ -415,16 +444,26 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES), sb = sa + L::A_BYTES;
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          mma_bf16(tmem, smem_desc_sw128(sa + k * 32), smem_desc_sw128(sb + k * 32), idesc, (i | k) != 0);
+        for (int k = 0; k < BK / 16; ++k) {
+          if constexpr (PAIR)
+            mma_bf16_pair(tmem, smem_desc_sw128(sa + k * 32), smem_desc_sw128(sb + k * 32), idesc, (i | k) != 0);
+          else
+            mma_bf16(tmem, smem_desc_sw128(sa + k * 32), smem_desc_sw128(sb + k * 32), idesc, (i | k) != 0);
+        }
         // the stage is free once these MMAs have read it; with multicast every
         // CTA of the group refills it, so each needs this CTA's release --
         // except for the last STAGES k-blocks, whose stages are never refilled
         // (no release arrives at a peer that may already have exited)
-        if constexpr (MC == 1) mma_commit(&empty[s]);
-        else if (i + STAGES < kb1 - kb0) mma_commit_mc(&empty[s], mc_mask);
+        if constexpr (PAIR) {
+          if (i + STAGES < kb1 - kb0) mma_commit_pair(&empty[s], uint16_t(3));  // both CTAs' stage s
+        } else if constexpr (MC == 1) {
+          mma_commit(&empty[s]);
+        } else if (i + STAGES < kb1 - kb0) {
+          mma_commit_mc(&empty[s], mc_mask);
+        }
       }
-      mma_commit(&accum_full);
+      if constexpr (PAIR) mma_commit_pair(&accum_full, uint16_t(3));  // each CTA's 128 rows of D
+      else mma_commit(&accum_full);
     }
   } else if (warp < 4) {  // ---- folded-BN scale / bias -> smem (bind-time constants)
     const int t = threadIdx.x - 64;  // 64 threads
@@ -641,9 +680,10 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
   if constexpr (SPLIT) {
     if (warp < 4) cluster_arrive_relaxed();
     cluster_wait();
-  } else if constexpr (MC > 1) {
+  } else if constexpr (MC > 1 || PAIR) {
     // no CTA leaves while a group peer's multicast loads / releases may still
-    // target it (every peer arrives once its own MMAs are complete)
+    // target it (every peer arrives once its own MMAs are complete); a pair
+    // also frees its TMEM together
     cluster_arrive_relaxed();
     cluster_wait();
   }
@@ -654,7 +694,8 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
 #endif
   if (warp == 1) {
     tc_fence_after();
-    tmem_free<TMEM_COLS>(tmem);
+    if constexpr (PAIR) tmem_free_pair<TMEM_COLS>(tmem);
+    else tmem_free<TMEM_COLS>(tmem);
   }
 }
 
@@ -689,23 +730,24 @@ void fill_job(Job& j, const Prepared& p, int S) {
   const int kblocks = int((p.K + BK - 1) / BK);
   j.kper = (kblocks + S - 1) / S;
   j.tma_out = p.tma_out;
-  const int mc = std::max(1, p.mc);
-  j.tiles_m = (int(tile_rows(p) / BM) + mc - 1) / mc * mc;  // whole multicast groups (padding tiles have no rows)
+  const int mc = p.pair ? 2 : std::max(1, p.mc);
+  j.tiles_m = (int(tile_rows(p) / BM) + mc - 1) / mc * mc;  // whole groups / pairs (padding tiles have no rows)
   j.cg = p.g;
 }
 
 template <int BN, int STAGES, int S, int MC = 1>
 void run_bn(const Prepared& p, const Prepared* q, cudaStream_t stream) {
-  constexpr size_t smem = Smem<BN, STAGES, S>::TOTAL;
+  constexpr int CX = MC < 0 ? -MC : MC;
+  constexpr size_t smem = Smem<BN, STAGES, S, (MC < 0)>::TOTAL;
   static_assert(smem <= 227 * 1024, "GEMM shared memory");
-  static_assert(S * MC <= 8, "portable cluster size");
+  static_assert(S * CX <= 8, "portable cluster size");
   static bool smem_set = false;
   if (!smem_set) {
     TRIMS_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, S, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(smem)));
     smem_set = true;
   }
-  if (MC > 1 && q) raise(Errc::InvalidArgument, "multicast GEMMs run alone");
+  if (CX > 1 && q) raise(Errc::InvalidArgument, "multicast / paired GEMMs run alone");
   Jobs jobs{};
   fill_job(jobs.j[0], p, S);
   jobs.t0 = jobs.j[0].tiles_m * int((p.N + BN - 1) / BN);
@@ -726,12 +768,12 @@ void run_bn(const Prepared& p, const Prepared* q, cudaStream_t stream) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = unsigned(MC);
+  attr[1].val.clusterDim.x = unsigned(CX);
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = unsigned(S);
   if (!pdl_enabled()) attr[0] = attr[1];  // keep only the cluster shape
   cfg.attrs = attr;
-  cfg.numAttrs = (S > 1 || MC > 1 ? 2 : 1) - (pdl_enabled() ? 0 : 1);
+  cfg.numAttrs = (S > 1 || CX > 1 ? 2 : 1) - (pdl_enabled() ? 0 : 1);
   TRIMS_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, STAGES, S, MC>, jobs));
 }
 
@@ -864,6 +906,12 @@ void run_pair(const Prepared& p, const Prepared* q, cudaStream_t stream) {
     raise(Errc::InvalidArgument, "GEMM split count");
   if (q && (q->bn != p.bn || q->splits != p.splits || q->lean != p.lean))
     raise(Errc::InvalidArgument, "grouped GEMMs need the same tile width, split count and variant");
+  if (p.pair) {  // 2-SM pairs (cta_group::2): unsplit, BN 128 / 256
+    if (p.splits != 1 || p.mc > 1 || p.lean || p.bn < 128) raise(Errc::InvalidArgument, "2-SM pair variant");
+    if (p.bn == 128) run_bn<128, 6, 1, -2>(p, q, stream);
+    else run_bn<256, 4, 1, -2>(p, q, stream);
+    return;
+  }
   if (p.mc > 1) {  // weight-multicast groups (single GEMM launches, latency mode)
     switch (p.bn * 1000 + p.splits * 10 + p.mc) {
       case 64 * 1000 + 14: run_bn<64, kSt64, 1, 4>(p, q, stream); return;
@@ -895,14 +943,14 @@ void run_pair(const Prepared& p, const Prepared* q, cudaStream_t stream) {
   }
 }
 
-uint32_t b_box_rows(const Prepared& p) { return uint32_t(p.bn / std::max(1, p.mc)); }
+uint32_t b_box_rows(const Prepared& p) { return uint32_t(p.bn / (p.pair ? 2 : std::max(1, p.mc))); }
 
 namespace {
 // Co-resident (MC, 1, S) clusters of one GEMM variant on this device.
 template <int BN, int STAGES, int S, int MC>
 int max_clusters() {
   static const int n = [] {
-    constexpr size_t smem = Smem<BN, STAGES, S>::TOTAL;
+    constexpr size_t smem = Smem<BN, STAGES, S, (MC < 0)>::TOTAL;
     cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, S, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(MC * 64), 1, unsigned(S));
@@ -1075,8 +1123,9 @@ Prepared prepare_conv(const void* act, const ConvGeom& g, const Operand& B, cons
 
 void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn, int splits, int mc) {
   Prepared p = prepare(A, B, e, bn);
-  if (mc > 1) {
-    p.mc = mc;
+  if (mc > 1 || mc == -2) {
+    if (mc == -2) p.pair = true;
+    else p.mc = mc;
     p.tb = make_tmap(B.ptr, B.rows, B.k, B.ld, b_box_rows(p));
   }
   if (splits == 0) {

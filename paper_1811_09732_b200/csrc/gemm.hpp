@@ -76,6 +76,9 @@ struct Prepared {
   // each B stage by TMA multicast, BN/MC rows loaded by each (the B tensor
   // map's box is then BN/MC rows: b_box_rows()). 1 = off.
   int mc{1};
+  // 2-SM pair (tcgen05 cta_group::2, M = 256 over two CTAs; each loads half
+  // of B: b_box_rows() = BN / 2). Unsplit, BN 128 / 256.
+  bool pair{false};
   ConvGeom g{};  // g.impl: A is the implicit im2col of an NHWC activation
 };
 Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn = 0);
@@ -93,7 +96,8 @@ void choose_tiles(uint64_t rows, uint64_t N, uint64_t K, int sms, int* bn, int* 
 int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms);
 // D = epi(A . B^T); bn = 0 picks the tile width; splits = split-K count
 // (1, 2, 4, 8; 0 picks it as the executor does).
-// mc: weight-multicast group size (1 = off; 2 / 4 / 8 with splits * mc <= 8).
+// mc: weight-multicast group size (1 = off; 2 / 4 / 8 with splits * mc <= 8);
+// mc = -2: a 2-SM pair (cta_group::2; splits 1, bn 128 / 256).
 void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn = 0, int splits = 1,
             int mc = 1);
 

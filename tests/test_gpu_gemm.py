@@ -130,3 +130,41 @@ def test_gemm_weight_multicast_matches_fp32_reference(M, N, K, bn, splits, mc, e
     err = (out - ref).abs()
     tol = ref.abs() * 2 ** -8 + 1e-3 * ref.abs().max()
     assert (err <= tol).all(), f"max err {err.max().item()} (ref max {ref.abs().max().item()})"
+
+
+@pytest.mark.parametrize("M,N,K,bn", [
+    (256, 128, 64, 128), (512, 256, 576, 256), (3136, 128, 1152, 128), (1000, 256, 2304, 256),
+    # an odd number of M-tiles: the last pair has a padding CTA with no rows
+    (300, 128, 512, 128), (12544, 64 * 3, 576, 128),
+])
+@pytest.mark.parametrize("epi", ["plain", "full"])
+def test_gemm_two_sm_pair_matches_fp32_reference(M, N, K, bn, epi):
+    """2-SM pairs (trims_gemm_bf16_ex with mc = -2): tcgen05.mma.cta_group::2
+    with M = 256 over two CTAs of one cluster, each loading its 128 rows of A
+    and half of B; same tolerance, bit-identical to the single-CTA launch."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(M * 11 + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    scale = bias = res = None
+    ref = A.float() @ B.float().T
+    if epi == "full":
+        scale = torch.rand(N, device="cuda", generator=g) + 0.5
+        bias = torch.randn(N, device="cuda", generator=g)
+        res = torch.randn(M, N, device="cuda", generator=g).to(torch.bfloat16)
+        ref = torch.relu(ref * scale + bias + res.float())
+    outs = []
+    for m in (-2, 1):
+        D = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+        check(lib.trims_gemm_bf16_ex(A.data_ptr(), M, K, K, B.data_ptr(), N, K, D.data_ptr(), N,
+                                     scale.data_ptr() if scale is not None else None,
+                                     bias.data_ptr() if bias is not None else None,
+                                     res.data_ptr() if res is not None else None, N, int(epi == "full"), bn,
+                                     1, m, torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        outs.append(D)
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16)), "the pair changed the result"
+    out = outs[0].float()
+    err = (out - ref).abs()
+    tol = ref.abs() * 2 ** -8 + 1e-3 * ref.abs().max()
+    assert (err <= tol).all(), f"max err {err.max().item()} (ref max {ref.abs().max().item()})"
