@@ -998,7 +998,7 @@ int pick_mc(const Prepared& p, int sms) {
     const char* e = std::getenv("TRIMS_MC");
     return e ? std::atoi(e) : 1;
   }();
-  if (forced <= 1 || p.lean || p.bn == 256 || p.splits > 4) return 1;
+  if (forced <= 1 || p.lean || p.pair || p.bn == 256 || p.splits > 4) return 1;
   const uint64_t tm = tile_rows(p) / BM, tn = (p.N + p.bn - 1) / p.bn, kb = (p.K + BK - 1) / BK;
   if (kb / uint64_t(p.splits) < 4) return 1;  // a short k-loop gains nothing from sharing its few stages
   const uint64_t ctas = tm * tn * uint64_t(p.splits);
@@ -1039,7 +1039,7 @@ int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms) {
   return s;
 }
 
-void choose_tiles(uint64_t rows, uint64_t N, uint64_t K, int sms, int* bn_out, int* splits_out) {
+void choose_tiles(uint64_t rows, uint64_t N, uint64_t K, int sms, int* bn_out, int* splits_out, bool* pair_out) {
   // Cost model of one batch-1 layer (per-CTA phases measured by
   // scripts/gemm_trace.py): each CTA streams ceil(kblocks / S) stages of
   // (16 KiB A + BN x 128 B of B) from L2 at ~95 KB/us per SM, plus ~2 us of
@@ -1067,6 +1067,33 @@ void choose_tiles(uint64_t rows, uint64_t N, uint64_t K, int sms, int* bn_out, i
       }
     }
   }
+  // 2-SM pairs (unsplit, BN 128 / 256): each SM streams 16 KiB of A and only
+  // half of B per stage; M-tiles padded to whole pairs
+  bool bp = false;
+  // Default: 256-wide pairs only (VGG-16 b32 2.249 -> 2.162 ms, b8 0.848 ->
+  // 0.824; ResNet-50 b32 +0.7 %; batch 1 flat; 128-wide pairs lost on
+  // ResNet-50: profiles/r3/pair_sm_ab.log). TRIMS_PAIR_SM=0 off, =1 all widths.
+  static const int pairs_on = [] {
+    const char* e = std::getenv("TRIMS_PAIR_SM");
+    return e ? std::atoi(e) : 256;
+  }();
+  if (pair_out && pairs_on && mt >= 2) {
+    for (int bn : {128, 256}) {
+      if (pairs_on == 256 && bn != 256) continue;
+      if (bn == 256 && N % 256) continue;
+      const uint64_t ctas = (mt + 1) / 2 * 2 * ((N + bn - 1) / bn);
+      const double waves = double((ctas + uint64_t(sms) - 1) / uint64_t(sms));
+      const double per_kb = 16.0 + bn * 64.0 / 1024.0;
+      const double c = waves * (c_wave + double(kb) * per_kb / bw);
+      if (c < best - 1e-9) {
+        best = c;
+        bb = bn;
+        bs = 1;
+        bp = true;
+      }
+    }
+  }
+  if (pair_out) *pair_out = bp;
   *bn_out = bb;
   *splits_out = bs;
 }

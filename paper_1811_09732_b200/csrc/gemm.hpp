@@ -91,7 +91,7 @@ void run(const Prepared& p, cudaStream_t stream);
 void run_pair(const Prepared& p, const Prepared* q, cudaStream_t stream);
 // Tile width and split count from a per-CTA cost model (L2 -> SMEM stage
 // bytes, per-wave fixed cost, split-K reduction cost); `rows` = tile rows.
-void choose_tiles(uint64_t rows, uint64_t N, uint64_t K, int sms, int* bn, int* splits);
+void choose_tiles(uint64_t rows, uint64_t N, uint64_t K, int sms, int* bn, int* splits, bool* pair = nullptr);
 // Split count for a GEMM shape on `sms` SMs.
 int pick_splits(uint64_t M, uint64_t N, uint64_t K, int bn, int sms);
 // D = epi(A . B^T); bn = 0 picks the tile width; splits = split-K count

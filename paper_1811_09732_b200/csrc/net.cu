@@ -350,9 +350,11 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
         };
         if (split_ok && tile_model_enabled()) {
           int bn = 0, sp = 1;
-          gemm::choose_tiles(gemm::tile_rows(*prep), uint64_t(kg), uint64_t(kp), sms_, &bn, &sp);
+          bool pr = false;
+          gemm::choose_tiles(gemm::tile_rows(*prep), uint64_t(kg), uint64_t(kp), sms_, &bn, &sp, &pr);
           if (bn != prep->bn) prep = remake(bn);
           prep->splits = sp;
+          prep->pair = pr;
         } else if (split_ok) {
           prep->splits = gemm::pick_splits(gemm::tile_rows(*prep), uint64_t(kg), uint64_t(kp), prep->bn, sms_);
         } else if (!split_ok && (flags & (kNetThroughput | kNetLean))) {
@@ -378,6 +380,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
                                 layers[li + 1].s("src") == l.s("src") && layers[li + 1].i("groups", 1) == 1 &&
                                 !pending;
         const bool pair_second = pending && groups == 1;
+        if (pair_first || pair_second) prep->pair = false;  // grouped launches run single-CTA GEMMs
         // weight multicast across M-tiles for a GEMM launched alone (latency mode)
         if (split_ok && !pair_first && !pair_second) prep->mc = gemm::pick_mc(*prep, sms_);
         const uint64_t b_off = w_off + uint64_t(gi) * kg * rsc * 2;
