@@ -91,6 +91,21 @@ def test_forward_layerwise_parity(store, name, batch):
         cli.close(view)
 
 
+def test_forward_layerwise_batched_vgg16_two_sm_pairs(store):
+    """VGG-16 at batch 8: the cost model runs the 256-wide 3x3 convs as 2-SM
+    pairs (cta_group::2, implicit-GEMM A tiles by cta_group::2 4-D TMA), so
+    this case covers that path layer by layer at the same tolerance."""
+    arch = C.ARCHS["vgg16"]()
+    cli = Client(store)
+    view = cli.open(C.arch_key(arch), force_shared=True)
+    net = BoundNet(view, arch, batch=8)
+    try:
+        _layerwise(arch, view, net, "vgg16", 8)
+    finally:
+        net.close()
+        cli.close(view)
+
+
 @pytest.mark.parametrize("mode", ["throughput", "lean"])
 @pytest.mark.parametrize("name,batch", [("alexnet", 1), ("resnet50", 1), ("vgg16", 1)])
 def test_forward_executor_modes(store, name, batch, mode):
