@@ -7,7 +7,12 @@
 // One CTA per 128 x BN output tile: warp 0 issues TMA (SWIZZLE_128B boxes
 // of 64 x rows) into a STAGES-deep mbarrier ring, warp 1 allocates TMEM and a
 // single lane issues tcgen05.mma (M=128, N=BN, K=16 per instruction), warps
-// 4-7 drain TMEM with tcgen05.ld and run the epilogue.
+// 2-3 stage folded-BN scale/bias, warps 4-11 drain TMEM with tcgen05.ld and
+// run the epilogue; the staged bf16 tile leaves by TMA store. Variants (all
+// template parameters): split-K over an (1,1,S) cluster reducing through
+// DSMEM bulk copies; 2-SM pairs (cta_group::2, M = 256 over a (2,1,1)
+// cluster); weight multicast across M-tiles (off by default); a job table
+// that runs two independent GEMMs in one launch; lean 2-CTA/SM variants.
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
