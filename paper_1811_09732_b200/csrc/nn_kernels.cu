@@ -248,7 +248,10 @@ __global__ void __launch_bounds__(256) gemv_kernel(const uint16_t* __restrict__ 
                                                    int ldo, int R) {
   __shared__ float red[kGemvRows][8][MB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * R, rows = min(R, N - n0);
+  // R > 0: R rows per block. R == 0: rows spread evenly over the grid (a
+  // multiple of the SM count: every SM streams the same share of W)
+  const int n0 = R ? int(blockIdx.x) * R : int(uint64_t(blockIdx.x) * N / gridDim.x);
+  const int rows = R ? min(R, N - n0) : int(uint64_t(blockIdx.x + 1) * N / gridDim.x) - n0;
   const int ppr = K / 256, pieces = rows * ppr;  // 256-element pieces per row / in the block
   const uint16_t* base = Wt + uint64_t(n0) * K;
   for (int i = threadIdx.x; i < kGemvRows * 8 * MB; i += blockDim.x) reinterpret_cast<float*>(red)[i] = 0.f;
@@ -430,10 +433,19 @@ void gemv(const uint16_t* x, int M, int K, const uint16_t* W, int N, const float
   // (TRIMS_GEMV_R / TRIMS_GEMV_U override rows per block / loads in flight)
   static const int r_env = std::getenv("TRIMS_GEMV_R") ? std::atoi(std::getenv("TRIMS_GEMV_R")) : 0;
   static const int u_env = std::getenv("TRIMS_GEMV_U") ? std::atoi(std::getenv("TRIMS_GEMV_U")) : 8;
-  int R = kGemvRows;
-  while (R > 2 && (N + R - 1) / R < 2 * sms) R /= 2;
-  if (r_env >= 1 && r_env <= kGemvRows) R = r_env;
-  const unsigned grid = unsigned((N + R - 1) / R);
+  // Balanced (default): b blocks per SM, b = the fewest that keep a block
+  // <= kGemvRows rows (>= 2), rows spread evenly: every SM streams the same
+  // share of W (fixed R rows per block left up to a third of the SMs with
+  // one block more than the rest). TRIMS_GEMV_R=n: n rows per block (A/B).
+  int R = 0;
+  unsigned grid = 0;
+  if (r_env >= 1 && r_env <= kGemvRows) {
+    R = r_env;
+    grid = unsigned((N + R - 1) / R);
+  } else {
+    const int per_sm = std::max(2, (N + sms * kGemvRows - 1) / (sms * kGemvRows));
+    grid = unsigned(std::min(N, sms * per_sm));
+  }
   auto go = [&](auto k) { launch_pdl(k, dim3(grid), dim3(256), 0, s, x, M, K, W, N, bias, relu, out_bf, out_f32, ldo, R); };
   if (M > 8) raise(Errc::InvalidArgument, "gemv is for M <= 8");
   if (u_env == 4) {
