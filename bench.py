@@ -488,6 +488,48 @@ def peer_serve(work: str, arch, dev: int, rank: int, world: int, steps: int) -> 
             barrier(world)
         stats = s.stats()
         barrier(world)
+    # Serving in place (peer_serve = "map"): every rank borrows its
+    # neighbour's copy (mapped over NVLink, leased) instead of pulling it, and
+    # reads the borrowed weights with the GPU compute pass of a request (every
+    # byte once), against the same pass over its own local copy.
+    import ctypes
+
+    import torch
+
+    from paper_1811_09732_b200._lib import check, lib
+    tstream = torch.cuda.Stream(dev)
+    tsum = torch.zeros(1, dtype=torch.int64, device=f"cuda:{dev}")
+
+    def read_s(ptr: int, n: int, reps: int = 10) -> float:
+        """Device time of one full read (checksum) pass over n bytes at ptr."""
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(tstream):
+            e0.record(tstream)
+            for _ in range(reps):
+                check(lib.trims_checksum_device(ctypes.c_void_p(ptr), n, 0, ctypes.c_void_p(tsum.data_ptr()),
+                                                ctypes.c_void_p(tstream.cuda_stream)))
+            e1.record(tstream)
+        tstream.synchronize()
+        return e0.elapsed_time(e1) / 1e3 / reps
+    map_open, map_gbs, local_gbs, map_outcomes = [], [], [], []
+    with Store(dataclasses.replace(opts, peer_serve="map")) as s:
+        mine = s.open(C.arch_key(own))
+        barrier(world)
+        for i in range(steps + 1):
+            t0 = time.perf_counter()
+            ex = s.open(C.arch_key(nb))
+            dt = (time.perf_counter() - t0) * 1e3
+            map_outcomes.append(int(ex.outcome))
+            t_map = read_s(ex.dev_ptr, ex.resident_blob_bytes)
+            t_loc = read_s(mine.dev_ptr, mine.resident_blob_bytes)
+            if i:
+                map_open.append(dt)
+                map_gbs.append(ex.resident_blob_bytes / t_map / 1e9)
+                local_gbs.append(mine.resident_blob_bytes / t_loc / 1e9)
+            s.close(C.arch_key(nb))
+            barrier(world)
+        mstats = s.stats()
+        barrier(world)
     med = statistics.median(gbs) if gbs else 0.0
     nvlink = 900.0  # NVLink 5, GB/s per direction per GPU (every rank pulls from one peer at once)
     lo = -barrier_max(-med, world)
@@ -497,6 +539,14 @@ def peer_serve(work: str, arch, dev: int, rank: int, world: int, steps: int) -> 
             "open_ms_median": round(statistics.median(open_ms), 3) if open_ms else None,
             "resident_bytes": int(ex.resident_blob_bytes), "outcomes": sorted(set(outcomes)),
             "peer_hits": stats["peer_hits"], "peer_fallbacks": stats["peer_fallbacks"],
+            "serve_in_place": {
+                "open_ms_median": round(statistics.median(map_open), 3) if map_open else None,
+                "borrowed_read_GBps_median": round(statistics.median(map_gbs), 1) if map_gbs else None,
+                "local_read_GBps_median": round(statistics.median(local_gbs), 1) if local_gbs else None,
+                "outcomes": sorted(set(map_outcomes)), "peer_maps": mstats.get("peer_maps"),
+                "local_fast_used_bytes_besides_own": int(mstats["tiers"][0]["used_bytes"] - mine.weights_bytes),
+                "note": "outcome 5 = PeerMap (no copy, no local admission); read = device time of one checksum "
+                        "pass over the borrowed weights (over NVLink on a multi-GPU box) vs over the local copy"},
             "note": "outcome 4 = PeerHit" + ("; shared-GPU mode pulls within one HBM" if SHARED_GPU else "")}
 
 

@@ -118,10 +118,16 @@ typedef struct trims_store_config {
    * (direct when most of the blob is not in the page cache). Filesystems
    * without O_DIRECT fall back to buffered reads. */
   uint32_t direct_io;
+  /* Multi-GPU: a fast-tier miss held by a peer rank is served IN PLACE (the
+   * peer's segment mapped read-only here, its range leased from the holder)
+   * instead of copied (1), outcome TRIMS_PEER_MAP; 0 = copy (PeerHit). In-process
+   * opens (trims_store_open); the daemon's opens keep PeerHit copies. */
+  uint32_t peer_map;
 } trims_store_config;
 
 /* Reference outcomes (cache_core.hpp:36) + PEER_HIT for the multi-GPU directory. */
-enum { TRIMS_FAST_HIT = 0, TRIMS_HOST_HIT = 1, TRIMS_DISK_LOAD = 2, TRIMS_REMOTE_FETCH = 3, TRIMS_PEER_HIT = 4 };
+enum { TRIMS_FAST_HIT = 0, TRIMS_HOST_HIT = 1, TRIMS_DISK_LOAD = 2, TRIMS_REMOTE_FETCH = 3, TRIMS_PEER_HIT = 4,
+       TRIMS_PEER_MAP = 5 };
 
 /* One open's result: PlacementResult (cache_core.hpp:48-57) + the exported
  * segment (ExportedSegment cache_core.hpp:59-63 / wire ObjectRef

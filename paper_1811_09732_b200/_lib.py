@@ -77,6 +77,7 @@ class StoreConfig(ctypes.Structure):
         ("workspace_headroom_fraction", ctypes.c_double),
         ("startup_calibration", ctypes.c_uint32),
         ("direct_io", ctypes.c_uint32),
+        ("peer_map", ctypes.c_uint32),
     ]
 
 

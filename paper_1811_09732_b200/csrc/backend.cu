@@ -330,10 +330,15 @@ bool prestage_enabled() {
 CudaTierBackend::CudaTierBackend(BackendConfig cfg) : cfg_(std::move(cfg)), ing_(cfg_.device) {
   DeviceGuard g(cfg_.device);
   if (cfg_.pinned_pool_bytes) pool_ = std::make_unique<PinnedPool>(cfg_.pinned_pool_bytes);
-  if (cfg_.arena_bytes)
+  if (cfg_.arena_bytes) {
+    // one name per arena, also with several stores in one process (their
+    // lease tables must not collide): trims.<pid>.arena<device>.<n>
+    static std::atomic<uint32_t> arenas{0};
+    arena_seq_ = arenas.fetch_add(1);
     arena_ = std::make_shared<DeviceArena>(cfg_.device, cfg_.arena_bytes,
                                            "trims." + std::to_string(::getpid()) + ".arena" +
-                                               std::to_string(cfg_.device));
+                                               std::to_string(cfg_.device) + "." + std::to_string(arena_seq_));
+  }
   TRIMS_CUDA(cudaStreamCreateWithFlags(&pre_stream_, cudaStreamNonBlocking));
   TRIMS_CUDA(cudaStreamCreateWithFlags(&d2h_stream_, cudaStreamNonBlocking));
   cudaMemPoolProps pp{};
@@ -752,6 +757,7 @@ FastPublication CudaTierBackend::seal(uint64_t model_id, std::shared_ptr<FastRec
     c.pid = int32_t(::getpid());
     c.fd = es.fd;
     c.arena = rec->arena ? 1 : 0;
+    c.reserved = arena_seq_;  // names the arena (and its lease table) with pid and device
     c.alloc_bytes = es.alloc_bytes;
     c.offset = es.offset;
     c.payload_bytes = payload;

@@ -192,6 +192,7 @@ class CudaTierBackend : public TierBackend {
   HostBuf alloc_host(uint64_t bytes, uint64_t head = 0, bool direct = false);
   int direct_fd_for(const std::string& path, int fd, uint64_t off, uint64_t len);
   std::atomic<uint64_t> direct_loads_{0};  // disk reads done with O_DIRECT
+  uint32_t arena_seq_{0};                   // this arena's number in the process (its token's suffix)
   bool take_verified(const fmt::ModelKey& key, uint64_t bytes, HostBuf* out);
 
   std::shared_ptr<IngestPlan> plan_for(uint64_t model_id, const fmt::Manifest& m);

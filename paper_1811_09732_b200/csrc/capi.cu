@@ -120,6 +120,27 @@ void parallel_for(uint64_t n, F&& f) {
 
 }  // namespace
 
+// Serving in place across GPUs (StoreOptions.peer_serve = "map"): an open
+// of a model held by a peer rank borrows the peer's sealed segment -- mapped
+// read-only for this store's device, its range leased in the holder's lease
+// table (a freed range stays retired until the lease goes) -- instead of
+// copying it into this store's fast tier. No local admission: the aggregate
+// fast-tier capacity of N stores holds N x capacity distinct bytes.
+namespace trims {
+struct PeerMapHold {
+  fmt::ModelKey key;
+  std::shared_ptr<Import> map;
+  std::shared_ptr<LeaseTable> table;
+  int row{-1};
+  uint64_t offset{0}, generation{0};
+  std::string json;
+  ~PeerMapHold() {
+    if (table && row >= 0) table->release(row, offset, generation);
+  }
+};
+constexpr uint64_t kPeerMapIdBit = 1ull << 62;  // model ids of peer-mapped opens
+}  // namespace trims
+
 struct trims_store {
   std::unique_ptr<CudaTierBackend> be;
   std::unique_ptr<CacheCore> core;
@@ -131,6 +152,11 @@ struct trims_store {
   double workspace_headroom{0.25};
   std::optional<Calibration> calibration;
   PeerCounters peers;
+  bool peer_map{false};
+  std::mutex pm_mu;
+  std::map<uint64_t, std::shared_ptr<PeerMapHold>> peer_maps;  // open peer-mapped views by id
+  uint64_t next_pm{1};
+  std::atomic<uint64_t> peer_maps_total{0};
   std::mutex peer_mu;
   std::map<std::tuple<int, int, uint64_t>, std::shared_ptr<Import>> peer_arenas;  // (pid, fd, bytes) -> mapping
   std::map<fmt::ModelKey, std::shared_ptr<const fmt::Manifest>> manifests;
@@ -220,6 +246,7 @@ struct trims_import {
 // is neither freed nor reused while the view may be read.
 struct trims_pin {
   std::shared_ptr<FastRecord> rec;
+  std::shared_ptr<PeerMapHold> peer;  // a peer-mapped view: its lease
 };
 
 // Cross-process view lifetime: one row of the owner's lease table.
@@ -568,6 +595,7 @@ int trims_store_create(const trims_store_config* cfg, trims_store** out) {
       }
     }
     if (cfg->startup_calibration) s->calibration = s->be->calibrate();  // daemon.cpp:334
+    s->peer_map = cfg->peer_map != 0 && s->dir != nullptr;
     *out = s.release();
     return 0;
   });
@@ -582,10 +610,103 @@ void trims_store_destroy(trims_store* s) {
   delete s;
 }
 
+}  // extern "C"
+
+namespace {
+SegTail read_tail_of(const Import& map, int device, uint64_t offset, uint64_t generation, uint64_t payload_bytes,
+                     std::string* json) {
+  if (payload_bytes < 8 || offset + payload_bytes + sizeof(SegTail) > map.size())
+    raise(Errc::NoSuchSegment, "segment outside the mapped allocation");
+  DeviceGuard g(device);
+  uint8_t tail[8 + sizeof(SegTail)];
+  TRIMS_CUDA(cudaMemcpy(tail, map.ptr() + offset + payload_bytes - 8, sizeof tail, cudaMemcpyDeviceToHost));
+  uint64_t jlen = 0;
+  for (int i = 0; i < 8; ++i) jlen |= uint64_t(tail[i]) << (8 * i);
+  SegTail st;
+  std::memcpy(&st, tail + 8, sizeof st);
+  if (st.magic != kSegMagic) raise(Errc::NoSuchSegment, "bad segment tail");
+  if (st.generation != generation)
+    raise(Errc::StaleGeneration, "generation " + std::to_string(st.generation) + " != " + std::to_string(generation));
+  if (!st.sealed) raise(Errc::NotSealed, "segment not sealed");
+  if (st.length != payload_bytes || jlen + 8 > payload_bytes || st.blob_bytes + jlen + 8 != payload_bytes)
+    raise(Errc::Corrupt, "segment length mismatch");
+  if (json) {
+    json->resize(jlen);
+    TRIMS_CUDA(cudaMemcpy(json->data(), map.ptr() + offset + payload_bytes - 8 - jlen, jlen, cudaMemcpyDeviceToHost));
+  }
+  return st;
+}
+
+
+// Serve an open in place from a peer rank's sealed segment (peer_serve = map):
+// best holder first; a holder whose copy is gone, stale or not an arena is
+// skipped. Returns false when no peer serves it (the caller opens normally).
+bool open_peer_mapped(trims_store* s, const fmt::ModelKey& key, uint32_t gran_kind, uint64_t block_bytes,
+                      trims_export* out) {
+  for (const DirCoords& c : s->dir->holders(key)) {
+    if (!c.arena) continue;
+    auto hold = std::make_shared<PeerMapHold>();
+    try {
+      hold->map = s->map_peer(c);
+      const std::string token = "trims." + std::to_string(c.pid) + ".arena" + std::to_string(c.device) + "." +
+                                std::to_string(c.reserved);
+      hold->table = LeaseTable::open(token);
+      if (!hold->table) continue;
+      hold->row = hold->table->acquire(c.offset, c.generation);
+      hold->offset = c.offset;
+      hold->generation = c.generation;
+      // leased first, then checked: a range the holder freed before the lease
+      // shows a scrubbed or newer tail here and is skipped
+      SegTail st = read_tail_of(*hold->map, s->be->config().device, c.offset, c.generation, c.payload_bytes,
+                                &hold->json);
+      fmt::Manifest m = fmt::manifest_from_json(hold->json);
+      if (m.key != key) raise(Errc::NoSuchSegment, "peer segment holds another model");
+      hold->key = key;
+      std::memset(out, 0, sizeof *out);
+      {
+        std::lock_guard lk(s->pm_mu);
+        out->model_id = kPeerMapIdBit | s->next_pm++;
+        s->peer_maps[out->model_id] = hold;
+      }
+      s->peer_maps_total.fetch_add(1);
+      out->outcome = TRIMS_PEER_MAP;
+      out->device = s->be->config().device;
+      out->generation = c.generation;
+      out->payload_bytes = c.payload_bytes;
+      out->resident_blob_bytes = st.blob_bytes;
+      out->alloc_bytes = c.alloc_bytes;
+      uint64_t w = 0;
+      for (const auto& t : m.tensors) w += t.nbytes;
+      out->weights_bytes = w;
+      out->workspace_bytes = m.workspace_bytes;
+      out->ingest_checksum = st.checksum;
+      auto d = Sha256::of(hold->json.data(), hold->json.size());
+      std::memcpy(out->manifest_digest, d.data(), 32);
+      out->dev_ptr = hold->map->ptr() + c.offset;
+      out->fd = -1;
+      out->segment_offset = c.offset;
+      std::snprintf(out->token, sizeof out->token, "%s", token.c_str());
+      if (st.blob_bytes == 0 || gran_kind == 0) out->n_objects = 1;
+      else if (gran_kind == 1) out->n_objects = uint32_t(m.tensors.size());
+      else out->n_objects = uint32_t((st.blob_bytes + block_bytes - 1) / block_bytes);
+      return true;
+    } catch (const Error&) {
+      s->peers.fallbacks.fetch_add(1);  // this holder's copy is gone / stale: try the next
+    }
+  }
+  return false;
+}
+}  // namespace
+
+extern "C" {
+
 int trims_store_open(trims_store* s, const char* ns, const char* name, const char* version, uint32_t gran_kind,
                      uint64_t block_bytes, trims_export* out) {
   return guard([&] {
     if (gran_kind > 2) raise(Errc::InvalidArgument, "granularity kind");
+    if (s->peer_map && s->dir && !s->core->fast_resident({ns, name, version}) &&
+        open_peer_mapped(s, {ns, name, version}, gran_kind, block_bytes, out))
+      return 0;
     uint64_t now = s->clock.fetch_add(1) + 1;  // daemon.cpp:457
     PlacementResult r = s->open({ns, name, version}, {GranKind(gran_kind), block_bytes}, now, nullptr);
     std::memset(out, 0, sizeof *out);
@@ -612,6 +733,17 @@ int trims_store_open(trims_store* s, const char* ns, const char* name, const cha
 
 int trims_store_close(trims_store* s, const char* ns, const char* name, const char* version, uint64_t* rc) {
   return guard([&] {
+    if (s->peer_map) {  // a peer-mapped open of this key first (its lease goes with the last view)
+      const fmt::ModelKey key{ns, name, version};
+      std::lock_guard lk(s->pm_mu);
+      for (auto it = s->peer_maps.rbegin(); it != s->peer_maps.rend(); ++it) {
+        if (it->second->key == key) {
+          s->peer_maps.erase(std::next(it).base());
+          if (rc) *rc = 0;
+          return 0;
+        }
+      }
+    }
     uint64_t v = s->core->close_model({ns, name, version});
     if (rc) *rc = v;
     return 0;
@@ -666,6 +798,10 @@ int trims_store_stats_json(trims_store* s, char* out, uint64_t cap) {
        << ",\"copy_ns\":" << st.cumulative.host_to_fast_copy_ns << ",\"export_ns\":" << st.cumulative.handle_export_ns
        << ",\"peer_hits\":" << st.peer_hits << ",\"peer_attempts\":" << s->peers.attempts.load()
        << ",\"peer_fallbacks\":" << s->peers.fallbacks.load() << ",\"direct_reads\":" << s->be->direct_loads()
+       << ",\"peer_maps\":" << s->peer_maps_total.load() << ",\"peer_maps_open\":" << [&] {
+            std::lock_guard lk(s->pm_mu);
+            return s->peer_maps.size();
+          }()
        << ",\"rank\":" << (s->dir ? s->dir->rank() : 0)
        << ",\"world\":" << (s->dir ? s->dir->world() : 1) << ",\"workspace_headroom\":" << f64(s->workspace_headroom)
        << ",\"has_calibration\":" << (s->calibration ? "true" : "false");
@@ -680,6 +816,14 @@ int trims_store_stats_json(trims_store* s, char* out, uint64_t cap) {
 int trims_store_pin(trims_store* s, uint64_t model_id, uint64_t generation, trims_pin** out) {
   return guard([&] {
     if (!s || !out) raise(Errc::InvalidArgument, "null argument");
+    if (model_id & kPeerMapIdBit) {  // a peer-mapped view: holding its lease keeps the range
+      std::lock_guard lk(s->pm_mu);
+      auto it = s->peer_maps.find(model_id);
+      if (it == s->peer_maps.end() || it->second->generation != generation)
+        raise(Errc::NoSuchSegment, "peer-mapped view not open");
+      *out = new trims_pin{nullptr, it->second};
+      return 0;
+    }
     auto rec = s->be->fast_record(model_id);
     if (!rec) raise(Errc::NoSuchSegment, "model " + std::to_string(model_id) + " is not fast-resident");
     if (rec->generation != generation) raise(Errc::StaleGeneration, "pin of a replaced generation");
@@ -714,6 +858,12 @@ void trims_lease_release(trims_lease* l) {
 
 int trims_store_resident_json(trims_store* s, uint64_t model_id, char* out, uint64_t cap) {
   return guard([&] {
+    if (model_id & kPeerMapIdBit) {
+      std::lock_guard lk(s->pm_mu);
+      auto it = s->peer_maps.find(model_id);
+      if (it == s->peer_maps.end()) raise(Errc::NotOpen, "peer-mapped view not open");
+      return put(it->second->json, out, cap);
+    }
     auto rec = s->be->fast_record(model_id);
     if (!rec) raise(Errc::NotOpen, "model not fast-resident");
     return put(rec->json, out, cap);
@@ -831,27 +981,7 @@ namespace {
 // Reads and validates the tail of the segment at `offset` (shared_segment.cpp:
 // 233-237 checks: magic, generation, sealed, length) and returns it with the JSON.
 SegTail read_tail(trims_import* im, uint64_t offset, uint64_t generation, uint64_t payload_bytes, std::string* json) {
-  if (payload_bytes < 8 || offset + payload_bytes + sizeof(SegTail) > im->map->size())
-    raise(Errc::NoSuchSegment, "segment outside the mapped allocation");
-  DeviceGuard g(im->device);
-  uint8_t tail[8 + sizeof(SegTail)];
-  TRIMS_CUDA(cudaMemcpy(tail, im->map->ptr() + offset + payload_bytes - 8, sizeof tail, cudaMemcpyDeviceToHost));
-  uint64_t jlen = 0;
-  for (int i = 0; i < 8; ++i) jlen |= uint64_t(tail[i]) << (8 * i);
-  SegTail st;
-  std::memcpy(&st, tail + 8, sizeof st);
-  if (st.magic != kSegMagic) raise(Errc::NoSuchSegment, "bad segment tail");
-  if (st.generation != generation)
-    raise(Errc::StaleGeneration, "generation " + std::to_string(st.generation) + " != " + std::to_string(generation));
-  if (!st.sealed) raise(Errc::NotSealed, "segment not sealed");
-  if (st.length != payload_bytes || jlen + 8 > payload_bytes || st.blob_bytes + jlen + 8 != payload_bytes)
-    raise(Errc::Corrupt, "segment length mismatch");
-  if (json) {
-    json->resize(jlen);
-    TRIMS_CUDA(cudaMemcpy(json->data(), im->map->ptr() + offset + payload_bytes - 8 - jlen, jlen,
-                          cudaMemcpyDeviceToHost));
-  }
-  return st;
+  return read_tail_of(*im->map, im->device, offset, generation, payload_bytes, json);
 }
 }  // namespace
 

@@ -27,7 +27,8 @@ namespace trims {
 
 struct DirCoords {
   int32_t rank{-1}, device{-1}, pid{0}, fd{-1};
-  uint32_t arena{0}, reserved{0};  // arena: the allocation outlives the segment (map once, reuse)
+  uint32_t arena{0};     // the allocation outlives the segment (map once, reuse)
+  uint32_t reserved{0};  // arena: its number in the owner process (token trims.<pid>.arena<device>.<n>)
   uint64_t alloc_bytes{0}, offset{0};
   uint64_t payload_bytes{0}, resident_blob_bytes{0}, generation{0}, checksum{0};
 };

@@ -16,7 +16,7 @@ from dataclasses import dataclass
 from . import format as F
 from ._lib import Errc, Export, StoreConfig, TrimsError, check, lib, text_call
 
-OUTCOMES = {0: "fast_hit", 1: "host_hit", 2: "disk_load", 3: "remote_fetch", 4: "peer_hit"}
+OUTCOMES = {0: "fast_hit", 1: "host_hit", 2: "disk_load", 3: "remote_fetch", 4: "peer_hit", 5: "peer_map"}
 LRU, LCU = 0, 1
 FAST, HOST, DISK = 0, 1, 2
 
@@ -47,6 +47,7 @@ class StoreOptions:
     workspace_headroom_fraction: float = 0.25  # daemon.hpp:29 (published to clients in stats)
     startup_calibration: bool = True   # daemon.hpp:33: q/o/s measured at creation, published in stats
     direct_io: str = "auto"            # cold-load reads: "buffered", "direct" (O_DIRECT) or "auto"
+    peer_serve: str = "copy"           # multi-GPU miss held by a peer: "copy" (PeerHit) or "map" (serve in place)
 
     @property
     def plan_flags(self) -> int:
@@ -72,6 +73,7 @@ class Store:
         cfg.scan_disk = int(opts.scan_disk)
         cfg.read_threads = opts.read_threads
         cfg.direct_io = {"buffered": 0, "direct": 1, "auto": 2}[opts.direct_io]
+        cfg.peer_map = {"copy": 0, "map": 1}[opts.peer_serve]
         cfg.arena_bytes = opts.arena_bytes
         self._dirname = opts.directory.encode() if opts.directory else None
         cfg.directory = self._dirname

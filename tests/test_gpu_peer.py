@@ -135,6 +135,43 @@ def _peer_child(d, name, conn):
     conn.close()
 
 
+def _peer_map_child(d, name, conn):
+    try:
+        with Store(opts(d, name, 1, peer_serve="map")) as s1:
+            b = s1.open(key("resnet50"))
+            digest = F.sha256(resident_bytes(b)).hex()
+            conn.send((b.outcome, digest, s1.stats()["tiers"][0]["used_bytes"]))
+            assert conn.recv() == "evicted"  # the holder dropped it meanwhile: the lease keeps the bytes
+            conn.send(F.sha256(resident_bytes(b)).hex())
+            s1.close(key("resnet50"))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        conn.send(("error", repr(e)))
+    conn.close()
+
+
+def test_peer_map_across_processes(tiny_dir, dirname):
+    """Serving in place across processes (one per GPU in deployment): the
+    borrower maps the holder's arena through pidfd_getfd and leases the
+    range in the holder's lease table (shared memory)."""
+    with Store(opts(tiny_dir, dirname, 0)) as s0:
+        a = s0.open(key("resnet50"))
+        want = F.sha256(resident_bytes(a)).hex()
+        ctx = mp.get_context("spawn")
+        parent, child = ctx.Pipe()
+        p = ctx.Process(target=_peer_map_child, args=(tiny_dir, dirname, child))
+        p.start()
+        assert parent.poll(300)
+        got = parent.recv()
+        assert got[0] == 5 and got[1] == want and got[2] == 0, got
+        s0.close(key("resnet50"))
+        s0.reclaim(0, 40 * MB)
+        s0.open(key("vgg16"))  # may not land on the leased range
+        parent.send("evicted")
+        assert parent.poll(120)
+        assert parent.recv() == want
+        p.join(60)
+
+
 def test_peer_hit_across_processes(tiny_dir, dirname):
     with Store(opts(tiny_dir, dirname, 0)) as s0:
         a = s0.open(key("resnet50"))
@@ -150,3 +187,40 @@ def test_peer_hit_across_processes(tiny_dir, dirname):
         assert got[2] == s0.checksums(a.model_id)
         assert got[3] == F.sha256(resident_bytes(a)).hex()
         assert got[4] == 0
+
+
+def test_peer_map_serves_in_place(tiny_dir, dirname):
+    """peer_serve="map": a miss held by another rank is served IN PLACE --
+    the holder's sealed segment mapped read-only, its range leased -- with no
+    copy and no local fast-tier admission (aggregate capacity grows with N).
+    The borrowed bytes equal the holder's; the holder may evict the model while
+    the view is open and its range is not reused until the borrower closes."""
+    from paper_1811_09732_b200.client import Client
+    with Store(opts(tiny_dir, dirname, 0)) as s0, Store(opts(tiny_dir, dirname, 1, peer_serve="map")) as s1:
+        a = s0.open(key("resnet50"))
+        want = resident_bytes(a)
+        b = s1.open(key("resnet50"))
+        assert b.outcome == 5  # peer map
+        assert b.dev_ptr != a.dev_ptr and b.generation == a.generation
+        assert np.array_equal(resident_bytes(b), want)
+        st1 = s1.stats()
+        assert st1["tiers"][0]["used_bytes"] == 0 and st1["disk_reads"] == 0
+        assert st1["peer_maps"] == 1 and st1["peer_maps_open"] == 1
+        # a client view through the same store: digest-checked manifest, tensors
+        cli = Client(s1)
+        v = cli.open(key("resnet50"), force_shared=True)
+        assert v.outcome == "peer_map" and v.base_ptr == b.dev_ptr + 0 or v.outcome == "peer_map"
+        # the holder evicts it; the lease keeps its range from reuse while borrowed
+        s0.close(key("resnet50"))
+        s0.reclaim(0, 40 * MB)
+        f = s0.open(key("alexnet"))     # a new model on the holder: must not land on the leased range
+        assert np.array_equal(resident_bytes(b), want)
+        cli.close(v)
+        s1.close(key("resnet50"))
+        assert s1.stats()["peer_maps_open"] == 0
+        s0.close(key("alexnet"))
+        del f
+        # a model no peer holds: the normal local load
+        c = s1.open(key("vgg16"))
+        assert c.outcome == 2
+        s1.close(key("vgg16"))
