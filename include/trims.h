@@ -343,7 +343,9 @@ int trims_gemm_bf16_split(const void* A, uint64_t M, uint64_t K, uint64_t lda, c
  * one thread-block cluster dimension and share every weight (B) stage by TMA
  * multicast (splits * mc <= 8; bn 64 or 128); mc = -2: a 2-SM pair, tcgen05
  * cta_group::2 MMAs of M = 256 over two CTAs that each load half of B
- * (splits 1; bn 128 or 256). */
+ * (splits 1; bn 128 or 256); mc = -3: persistent (one CTA per SM over all
+ * output tiles, two TMEM accumulators so a tile's epilogue overlaps the next
+ * tile's k-loop; splits ignored, 16-byte aligned output rows). */
 int trims_gemm_bf16_ex(const void* A, uint64_t M, uint64_t K, uint64_t lda, const void* B, uint64_t N, uint64_t ldb,
                        void* D, uint64_t ldd, const float* scale, const float* bias, const void* residual,
                        uint64_t ldr, int relu, int bn, int splits, int mc, void* stream);

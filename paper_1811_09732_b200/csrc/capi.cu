@@ -1273,8 +1273,8 @@ int trims_gemm_bf16_ex(const void* A, uint64_t M, uint64_t K, uint64_t lda, cons
                        void* D, uint64_t ldd, const float* scale, const float* bias, const void* residual,
                        uint64_t ldr, int relu, int bn, int splits, int mc, void* stream) {
   return guard([&] {
-    if (mc != 1 && mc != 2 && mc != 4 && mc != 8 && mc != -2)
-      raise(Errc::InvalidArgument, "multicast group of 1, 2, 4 or 8, or -2 (2-SM pair)");
+    if (mc != 1 && mc != 2 && mc != 4 && mc != 8 && mc != -2 && mc != -3)
+      raise(Errc::InvalidArgument, "multicast group of 1, 2, 4 or 8, -2 (2-SM pair) or -3 (persistent)");
     gemm::Epilogue e{static_cast<uint16_t*>(D), ldd, scale, bias, static_cast<const uint16_t*>(residual), ldr,
                      relu != 0};
     gemm::launch({A, M, K, lda}, {B, N, K, ldb}, e, static_cast<cudaStream_t>(stream), bn, splits, mc);

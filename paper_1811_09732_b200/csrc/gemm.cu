@@ -495,6 +495,8 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
     tc_fence_after();
     if constexpr (!SPLIT) {
       asm volatile("bar.sync 1, 320;" ::: "memory");  // scale / bias in smem
+      s_scale = after_here(s_scale);  // the clobber-free scale / bias loads stay below the barrier
+      s_bias = after_here(s_bias);
       if (has_res) mbar_wait(&res_full, 0);
 #ifdef TRIMS_GEMM_TRACE
       if (threadIdx.x == 128) GT_SET(gt_slot, 9, gtimer());
@@ -649,6 +651,8 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
       if (threadIdx.x == 128) GT_SET(gt_slot, 12, gtimer());
 #endif
       asm volatile("bar.sync 1, 320;" ::: "memory");  // scale / bias in smem; own partials written
+      s_scale = after_here(s_scale);  // the clobber-free scale / bias loads stay below the barrier
+      s_bias = after_here(s_bias);
       if (has_res) mbar_wait(&res_full, 0);
       // reduce: thread t takes tile row t % 128 and 8-column groups t / 128,
       // + 2, ... of the slice; v = p0 + p1 + ... in split order (deterministic)
@@ -701,6 +705,236 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
     tc_fence_after();
     if constexpr (PAIR) tmem_free_pair<TMEM_COLS>(tmem);
     else tmem_free<TMEM_COLS>(tmem);
+  }
+}
+
+// Persistent variant for multi-wave layers (batch > 1; VGG's first layers at
+// batch 1): one CTA per SM walks the output tiles t = blockIdx.x,
+// + gridDim.x, ... (M-tile fastest, so co-running CTAs share the weight
+// tile). The TMA ring runs on across tiles, and TWO TMEM accumulators let
+// tile i's epilogue (TMEM -> bf16 staging -> TMA store) overlap tile i+1's
+// k-loop: the one-tile-per-CTA kernel leaves the tensor pipe idle for each
+// tile's prologue and epilogue, which dominates short k-loops (K = 64..576).
+// Unsplit, one GEMM per launch, TMA-store epilogue, same arithmetic as
+// gemm_tc_kernel (bit-identical outputs).
+template <int BN, int STAGES>
+struct PSmem {
+  static constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t RING = STAGES * STAGE_BYTES;
+  static constexpr uint32_t OUT = RING, OUT_BYTES = BM * BN * 2;  // staging tile (residual in, bf16 out)
+  static constexpr uint32_t SCALE = OUT + OUT_BYTES, BIAS = SCALE + BN * 4;
+  static constexpr uint32_t TOTAL = BIAS + BN * 4 + 1024;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1) gemm_persist_kernel(const __grid_constant__ Job J) {
+  using L = PSmem<BN, STAGES>;
+  constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulators
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], acc_full[2], acc_empty[2], res_full;
+  __shared__ uint32_t tmem_base;
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* s_scale = reinterpret_cast<float*>(smem + L::SCALE);
+  float* s_bias = reinterpret_cast<float*>(smem + L::BIAS);
+  uint16_t* s_out = reinterpret_cast<uint16_t*>(smem + L::OUT);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int M = J.M, N = J.N, K = J.K, has_res = J.has_res, relu = J.relu;
+  const ConvGeom cg = J.cg;
+  const int kblocks = (K + BK - 1) / BK;
+  const int tiles_m = J.tiles_m, tiles = tiles_m * ((N + BN - 1) / BN);
+  const int wbox = 1 << cg.wbox_log2;
+  (void)M;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 8);  // one arrive per epilogue warp
+    }
+    mbar_init(&res_full, 1);
+    fence_barrier_init();
+    prefetch_tmap(&J.ta);
+    prefetch_tmap(&J.tb);
+    if (has_res) prefetch_tmap(&J.tr);
+    prefetch_tmap(&J.td);
+  }
+  if (warp == 1) tmem_alloc<TMEM_COLS>(&tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_trigger();
+  const uint32_t tmem = tmem_base;
+
+  // tile -> (m-tile, n-tile) and, for an implicit conv, (image, row box, col box)
+  struct T {
+    int m0, n0, ti, th, tw;
+  };
+  auto tile_of = [&](int t) {
+    T r;
+    const int mt = t % tiles_m, nt = t / tiles_m;
+    r.m0 = mt * BM;
+    r.n0 = nt * BN;
+    r.ti = r.th = r.tw = 0;
+    if (cg.impl) {
+      r.tw = mt % cg.tiles_w;
+      r.th = (mt / cg.tiles_w) % cg.tiles_h;
+      r.ti = mt / (cg.tiles_w * cg.tiles_h);
+    }
+    return r;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer: the ring continues across tiles
+      pdl_wait();
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const T tl = tile_of(t);
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const uint32_t s = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+          uint8_t* sa = smem + s * L::STAGE_BYTES;
+          mbar_expect_tx(&full[s], L::STAGE_BYTES);
+          if (cg.impl) {
+            const int rs = kb / cg.cblocks, cb = kb - rs * cg.cblocks, r = rs / cg.S, ss = rs - r * cg.S;
+            tma_load_4d(sa, &J.ta, cg.c_off + cb * BK, tl.tw * wbox * cg.stride - cg.pad + ss,
+                        tl.th * cg.hbox * cg.stride - cg.pad + r, tl.ti, &full[s]);
+          } else {
+            tma_load_2d(sa, &J.ta, kb * BK, tl.m0, &full[s]);
+          }
+          tma_load_2d(sa + L::A_BYTES, &J.tb, kb * BK, tl.n0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer: accumulator lt & 1 for local tile lt
+      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+      uint32_t it = 0, lt = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+        const uint32_t b = lt & 1;
+        if (lt >= 2) mbar_wait(&acc_empty[b], ((lt >> 1) - 1) & 1);  // its previous tile's epilogue drained it
+        tc_fence_after();
+        const uint32_t acc = tmem + b * BN;
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const uint32_t s = it % STAGES;
+          mbar_wait(&full[s], (it / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES), sb = sa + L::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16(acc, smem_desc_sw128(sa + k * 32), smem_desc_sw128(sb + k * 32), idesc, (kb | k) != 0);
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&acc_full[b]);
+      }
+    }
+  } else if (warp >= 4) {  // ---- epilogue: 8 warps, two per TMEM lane quarter
+    const int q = warp & 3, half = (warp - 4) >> 2, rl = q * 32 + lane, et = threadIdx.x - 128;
+    const uint32_t tq = tmem + (uint32_t(q * 32) << 16);
+    pdl_wait();  // the residual may be the previous kernel's output
+    uint32_t lt = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++lt) {
+      const T tl = tile_of(t);
+      const uint32_t b = lt & 1;
+      // the staging tile is free once the previous tile's TMA store has read it
+      if (et == 0) {
+        bulk_wait_read();
+        if (has_res) {
+          mbar_expect_tx(&res_full, uint32_t((BN / 64) * BM * 128));
+#pragma unroll
+          for (int bx = 0; bx < BN / 64; ++bx) {
+            uint8_t* dst = smem + L::OUT + bx * BM * 128;
+            if (cg.impl) tma_load_4d(dst, &J.tr, tl.n0 + bx * 64, tl.tw * wbox, tl.th * cg.hbox, tl.ti, &res_full);
+            else tma_load_2d(dst, &J.tr, tl.n0 + bx * 64, tl.m0, &res_full);
+          }
+        }
+      }
+      if (et < BN) {
+        const int n = tl.n0 + et;
+        s_scale[et] = (J.scale && n < N) ? __ldg(J.scale + n) : 1.f;
+        s_bias[et] = (J.bias && n < N) ? __ldg(J.bias + n) : 0.f;
+      }
+      asm volatile("bar.sync 2, 256;" ::: "memory");  // scale / bias staged; staging tile free
+      // scale / bias are rewritten every tile: their clobber-free loads must
+      // stay below this barrier (not be hoisted out of the tile loop)
+      const float* tsc = after_here(s_scale);
+      const float* tbi = after_here(s_bias);
+      mbar_wait(&acc_full[b], (lt >> 1) & 1);
+      tc_fence_after();
+      if (has_res) mbar_wait(&res_full, lt & 1);
+      auto fin = [&](auto hr_tag, auto rl_tag) {
+        constexpr bool HR = decltype(hr_tag)::value, RL = decltype(rl_tag)::value;
+#pragma unroll 1
+        for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
+          uint32_t r[32];
+          tmem_ld16_nw(tq + b * BN + uint32_t(c0), r);
+          tmem_ld16_nw(tq + b * BN + uint32_t(c0 + 16), r + 16);
+          tmem_wait_ld();
+          const float* v = reinterpret_cast<const float*>(r);
+          uint16_t* srow = s_out + (c0 / 64) * BM * 64 + rl * 64;
+          const int chunk0 = (c0 & 63) >> 3, sw = rl & 7;
+          uint4 res[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            res[u] = HR ? *reinterpret_cast<const uint4*>(srow + (((chunk0 + u) ^ sw) << 3)) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = c0 + 8 * u;
+            const uint32_t rw[4] = {res[u].x, res[u].y, res[u].z, res[u].w};
+            const float4 sc0 = lds_f4(tsc + c), sc1 = lds_f4(tsc + c + 4);
+            const float4 bi0 = lds_f4(tbi + c), bi1 = lds_f4(tbi + c + 4);
+            const float sc[8] = {sc0.x, sc0.y, sc0.z, sc0.w, sc1.x, sc1.y, sc1.z, sc1.w};
+            const float bi[8] = {bi0.x, bi0.y, bi0.z, bi0.w, bi1.x, bi1.y, bi1.z, bi1.w};
+            uint32_t o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float2 ab = fma2(make_float2(v[8 * u + 2 * j], v[8 * u + 2 * j + 1]), make_float2(sc[2 * j], sc[2 * j + 1]),
+                               make_float2(bi[2 * j], bi[2 * j + 1]));
+              if constexpr (HR) ab = add2(ab, make_float2(bf16_lo(rw[j]), bf16_hi(rw[j])));
+              if constexpr (RL) {
+                ab.x = fmaxf(ab.x, 0.f);
+                ab.y = fmaxf(ab.y, 0.f);
+              }
+              o[j] = pack_bf16x2(ab.x, ab.y);
+            }
+            *reinterpret_cast<uint4*>(srow + (((chunk0 + u) ^ sw) << 3)) = make_uint4(o[0], o[1], o[2], o[3]);
+          }
+        }
+      };
+      using Tt = std::true_type;
+      using Ff = std::false_type;
+      if (has_res) {
+        if (relu) fin(Tt{}, Tt{});
+        else fin(Tt{}, Ff{});
+      } else {
+        if (relu) fin(Ff{}, Tt{});
+        else fin(Ff{}, Ff{});
+      }
+      // accumulator b is drained: the MMA warp may start tile lt + 2 in it
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
+      fence_proxy_async_smem();                       // staged tile -> async proxy
+      asm volatile("bar.sync 2, 256;" ::: "memory");  // the whole tile is staged
+      if (et == 0) {
+#pragma unroll
+        for (int bx = 0; bx < BN / 64; ++bx) {
+          const uint16_t* src = s_out + bx * BM * 64;
+          if (cg.impl) tma_store_4d(&J.td, src, tl.n0 + bx * 64, tl.tw * wbox, tl.th * cg.hbox, tl.ti);
+          else tma_store_2d(&J.td, src, tl.n0 + bx * 64, tl.m0);
+        }
+        bulk_commit();
+      }
+    }
+    if (et == 0) bulk_wait_read();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free<TMEM_COLS>(tmem);
   }
 }
 
@@ -890,6 +1124,37 @@ Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn) 
   return p;
 }
 
+namespace {
+template <int BN, int STAGES>
+void run_persist(const Prepared& p, cudaStream_t stream) {
+  constexpr size_t smem = PSmem<BN, STAGES>::TOTAL;
+  static_assert(smem <= 227 * 1024, "persistent GEMM shared memory");
+  static bool smem_set = false;
+  if (!smem_set) {
+    TRIMS_CUDA(cudaFuncSetAttribute(gemm_persist_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(smem)));
+    smem_set = true;
+  }
+  Job j{};
+  fill_job(j, p, 1);
+  const int tiles = j.tiles_m * int((p.N + BN - 1) / BN);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(std::min(tiles, sms)));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  TRIMS_CUDA(cudaLaunchKernelEx(&cfg, gemm_persist_kernel<BN, STAGES>, j));
+}
+}  // namespace
+
 // TMA ring depths (stages in flight per CTA: at batch 1 a CTA's k-loop is
 // bound by bytes in flight / L2 latency, so deeper is faster while it fits).
 #ifndef TRIMS_ST64
@@ -911,6 +1176,13 @@ void run_pair(const Prepared& p, const Prepared* q, cudaStream_t stream) {
     raise(Errc::InvalidArgument, "GEMM split count");
   if (q && (q->bn != p.bn || q->splits != p.splits || q->lean != p.lean))
     raise(Errc::InvalidArgument, "grouped GEMMs need the same tile width, split count and variant");
+  if (p.persist) {  // persistent, double-buffered accumulators: unsplit, single GEMM, TMA-store output
+    if (q || p.splits != 1 || p.pair || p.mc > 1 || !p.tma_out) raise(Errc::InvalidArgument, "persistent GEMM variant");
+    if (p.bn == 64) run_persist<64, 6>(p, stream);
+    else if (p.bn == 128) run_persist<128, 5>(p, stream);
+    else run_persist<256, 3>(p, stream);
+    return;
+  }
   if (p.pair) {  // 2-SM pairs (cta_group::2): unsplit, BN 128 / 256
     if (p.splits != 1 || p.mc > 1 || p.lean || p.bn < 128) raise(Errc::InvalidArgument, "2-SM pair variant");
     if (p.bn == 128) run_bn<128, 6, 1, -2>(p, q, stream);
@@ -947,6 +1219,7 @@ void run_pair(const Prepared& p, const Prepared* q, cudaStream_t stream) {
     default: run_bn<256, 3, 1>(p, q, stream); break;
   }
 }
+
 
 uint32_t b_box_rows(const Prepared& p) { return uint32_t(p.bn / (p.pair ? 2 : std::max(1, p.mc))); }
 
@@ -1155,7 +1428,10 @@ Prepared prepare_conv(const void* act, const ConvGeom& g, const Operand& B, cons
 
 void launch(const Operand& A, const Operand& B, const Epilogue& e, cudaStream_t stream, int bn, int splits, int mc) {
   Prepared p = prepare(A, B, e, bn);
-  if (mc > 1 || mc == -2) {
+  if (mc == -3) {
+    p.persist = true;
+    splits = 1;
+  } else if (mc > 1 || mc == -2) {
     if (mc == -2) p.pair = true;
     else p.mc = mc;
     p.tb = make_tmap(B.ptr, B.rows, B.k, B.ld, b_box_rows(p));

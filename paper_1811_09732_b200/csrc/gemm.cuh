@@ -112,6 +112,14 @@ __device__ __forceinline__ float4 lds_f4(const float* p) {
   return v;
 }
 
+// p, made opaque at this point of the program: an lds_f4 through the result
+// cannot be scheduled above the volatile asm (e.g. a barrier) before it.
+template <class T>
+__device__ __forceinline__ T* after_here(T* p) {
+  asm volatile("" : "+l"(p));
+  return p;
+}
+
 // ---- clusters / distributed shared memory
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");

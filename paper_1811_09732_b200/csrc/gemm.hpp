@@ -79,6 +79,10 @@ struct Prepared {
   // 2-SM pair (tcgen05 cta_group::2, M = 256 over two CTAs; each loads half
   // of B: b_box_rows() = BN / 2). Unsplit, BN 128 / 256.
   bool pair{false};
+  // Persistent (one CTA per SM over all output tiles, two TMEM accumulators:
+  // a tile's epilogue overlaps the next tile's k-loop). Unsplit, single GEMM,
+  // TMA-store output; for multi-wave layers.
+  bool persist{false};
   ConvGeom g{};  // g.impl: A is the implicit im2col of an NHWC activation
 };
 Prepared prepare(const Operand& A, const Operand& B, const Epilogue& e, int bn = 0);

@@ -143,6 +143,18 @@ bool tp_wide_enabled() {
   return on;
 }
 
+// TRIMS_PERSIST: 0 = no persistent GEMMs, 1 = for multi-wave layers except
+// long-k-loop 2-SM pairs, 2 = every multi-wave layer launched alone (default:
+// VGG-16 b32 2.166 -> 1.624 ms, ResNet-50 b32 1.176 -> 1.043, VGG-16 b1
+// 0.2125 -> 0.2048; mode 1 within 1 %; profiles/r3/persist_ab.log).
+int persist_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("TRIMS_PERSIST");
+    return e ? std::atoi(e) : 2;
+  }();
+  return m;
+}
+
 // TRIMS_SPLITK=0 turns split-K off (A/B switch).
 bool splitk_enabled() {
   static const bool on = [] {
@@ -383,6 +395,19 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
         if (pair_first || pair_second) prep->pair = false;  // grouped launches run single-CTA GEMMs
         // weight multicast across M-tiles for a GEMM launched alone (latency mode)
         if (split_ok && !pair_first && !pair_second) prep->mc = gemm::pick_mc(*prep, sms_);
+        // a multi-wave GEMM launched alone runs persistent CTAs (one per SM,
+        // double-buffered accumulators: each tile's epilogue overlaps the next
+        // tile's k-loop), in place of a 2-SM pair too (mode 1: only when the
+        // pair's k-loop is short)
+        if (!pair_first && !pair_second && !lean && prep->splits == 1 && prep->mc <= 1 && prep->tma_out) {
+          const uint64_t tiles = gemm::tile_rows(*prep) / 128 * ((prep->N + prep->bn - 1) / prep->bn);
+          const uint64_t kb = (uint64_t(kp) + 63) / 64;
+          const int mode = persist_mode();
+          if (mode && tiles > uint64_t(sms_) && (!prep->pair || mode == 2 || kb <= 8)) {
+            prep->pair = false;
+            prep->persist = true;
+          }
+        }
         const uint64_t b_off = w_off + uint64_t(gi) * kg * rsc * 2;
         const bool do_params = first_group && bind_params;
         auto rebind = [=](cudaStream_t s) {

@@ -168,3 +168,44 @@ def test_gemm_two_sm_pair_matches_fp32_reference(M, N, K, bn, epi):
     err = (out - ref).abs()
     tol = ref.abs() * 2 ** -8 + 1e-3 * ref.abs().max()
     assert (err <= tol).all(), f"max err {err.max().item()} (ref max {ref.abs().max().item()})"
+
+
+@pytest.mark.parametrize("M,N,K,bn", [
+    (256, 128, 64, 128),            # fewer tiles than SMs: one tile per CTA
+    (40000, 256, 64, 256),          # 313 tiles: 2-3 per CTA, both accumulators, K = one k-block
+    (25088, 512, 256, 256),         # 392 tiles
+    (100352, 64, 576, 64),          # 784 tiles, ring phases wrap across tiles
+    (3000, 128, 1152, 128),         # ragged last M-tile
+    (20000, 192, 128, 128),         # partial last N-tile
+])
+@pytest.mark.parametrize("epi", ["plain", "full"])
+def test_gemm_persistent_matches_fp32_reference(M, N, K, bn, epi):
+    """Persistent launch (trims_gemm_bf16_ex with mc = -3): one CTA per SM over
+    all output tiles, two TMEM accumulators (tile i's epilogue overlaps tile
+    i+1's k-loop); same tolerance, bit-identical to one CTA per tile."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).to(torch.bfloat16)
+    scale = bias = res = None
+    ref = A.float() @ B.float().T
+    if epi == "full":
+        scale = torch.rand(N, device="cuda", generator=g) + 0.5
+        bias = torch.randn(N, device="cuda", generator=g)
+        res = torch.randn(M, N, device="cuda", generator=g).to(torch.bfloat16)
+        ref = torch.relu(ref * scale + bias + res.float())
+    outs = []
+    for m in (-3, 1):
+        D = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+        check(lib.trims_gemm_bf16_ex(A.data_ptr(), M, K, K, B.data_ptr(), N, K, D.data_ptr(), N,
+                                     scale.data_ptr() if scale is not None else None,
+                                     bias.data_ptr() if bias is not None else None,
+                                     res.data_ptr() if res is not None else None, N, int(epi == "full"), bn,
+                                     1, m, torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        outs.append(D)
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16)), "the persistent launch changed the result"
+    out = outs[0].float()
+    err = (out - ref).abs()
+    tol = ref.abs() * 2 ** -8 + 1e-3 * ref.abs().max()
+    assert (err <= tol).all(), f"max err {err.max().item()} (ref max {ref.abs().max().item()})"
