@@ -89,7 +89,7 @@ bool first_conv_fusable(const LayerSpec& l) {
   const int k = l.i("k", 1), groups = l.i("groups", 1);
   const bool direct = k == 1 && l.i("stride", 1) == 1 && l.i("pad", 0) == 0 && groups == 1;
   const bool implicit = !direct && (l.i("cin") / groups) % 64 == 0 && implicit_enabled();
-  return !direct && !implicit && groups == 1;
+  return !direct && !implicit && groups == 1 && k * k * l.i("cin") <= 504;  // im2col_input: Kp <= 512
 }
 
 bool implicit_enabled() {
@@ -531,6 +531,11 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
                            uint64_t(cin)},
                           e));
         prep->lean = lean;
+        // batch > 8: few output tiles (one M-tile per 128 images), each
+        // streaming a K-long weight slab: split K so the weights stream on
+        // most SMs (VGG-16 b32 fc6: 64 CTAs -> 128); latency mode only, as for convs
+        if (split_ok)
+          prep->splits = gemm::pick_splits(gemm::tile_rows(*prep), uint64_t(cout), uint64_t(cin), prep->bn, sms_);
         auto rebind = [=](cudaStream_t s) {
           prep->tb = gemm::make_tmap(wptr(w_off), uint64_t(cout), uint64_t(cin), uint64_t(cin), gemm::b_box_rows(*prep));
           bind_bias(s);

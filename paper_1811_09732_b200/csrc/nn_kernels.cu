@@ -182,38 +182,47 @@ __global__ void __launch_bounds__(256) avgpool_kernel(const uint16_t* __restrict
   }
 }
 
-// A[m, (r*S + s)*C + c] = bf16(in[n, c, y, x]) for the first conv, 8 columns
-// (one 16-byte store) per thread.
-__global__ void im2col_input_kernel(const float* __restrict__ in, uint16_t* __restrict__ A, int N, int C, int H, int W,
-                                    int R, int S, int stride, int pad, int P, int Q, int Kp) {
+// A[m, (r*S + s)*C + c] = bf16(in[n, c, y, x]) for the first conv. Thread i
+// fills 16-byte chunk i of A (row i / G, columns 8 (i % G) .., G = Kp / 8):
+// consecutive lanes write consecutive chunks, so a warp's stores are one
+// contiguous run of A (a thread per row put every chunk of a warp store in
+// a different row: 1.8x the DRAM writes, ResNet-50 b32 142 us). Each
+// column's tap (plane offset, dy, dx) is decoded once per block into shared
+// memory; the scattered input loads hit L1 (a pixel feeds up to R*S/stride^2
+// rows of the block).
+constexpr int kIm2colMaxK = 512;
+__global__ void __launch_bounds__(256) im2col_input_kernel(const float* __restrict__ in, uint16_t* __restrict__ A,
+                                                           int N, int C, int H, int W, int R, int S, int stride,
+                                                           int pad, int P, int Q, int Kp) {
+  __shared__ int s_plane[kIm2colMaxK];
+  __shared__ short s_dy[kIm2colMaxK], s_dx[kIm2colMaxK];
+  const int RSC = R * S * C;
+  for (int k = threadIdx.x; k < Kp; k += blockDim.x) {
+    const int rs = k / C, c = k - rs * C;
+    s_dy[k] = short(k < RSC ? rs / S : -16384);  // out of every image: a zero column
+    s_dx[k] = short(rs - (rs / S) * S);
+    s_plane[k] = c * H * W;
+  }
   pdl_wait();  // the input H2D / previous forward's readers of A
   pdl_trigger();
-  // blockIdx.y = one 8-column group: its (c, r, s) taps are decoded once;
-  // threads then walk output pixels (consecutive lanes = consecutive pixels,
-  // so a warp's loads of one tap are stride-apart in one plane row)
-  const int RSC = R * S * C, col = blockIdx.y * 8;
-  int dy[8], dx[8];
-  uint64_t plane[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int k = col + e, rs = k / C, c = k - rs * C;
-    dy[e] = k < RSC ? rs / S : -(1 << 20);  // out of every image: a zero column
-    dx[e] = rs - (rs / S) * S;
-    plane[e] = uint64_t(c) * H * W;
-  }
-  const uint32_t M = uint32_t(N) * P * Q;
-  for (uint32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < M; m += gridDim.x * blockDim.x) {
+  __syncthreads();
+  const uint32_t G = uint32_t(Kp) / 8;
+  const uint64_t chunks = uint64_t(N) * P * Q * G;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < chunks; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t m = uint32_t(i / G), col = uint32_t(i - uint64_t(m) * G) * 8;
     const uint32_t q = m % Q, pn = m / Q, p = pn % P, n = pn / P;
     const int y0 = int(p) * stride - pad, x0 = int(q) * stride - pad;
     const float* img = in + uint64_t(n) * C * H * W;
-    uint32_t o[4] = {0, 0, 0, 0};
+    float v[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const int y = y0 + dy[e], x = x0 + dx[e];
-      const float v = (y >= 0 && y < H && x >= 0 && x < W) ? __ldg(img + plane[e] + uint64_t(y) * W + x) : 0.f;
-      o[e >> 1] |= uint32_t(to_bf(v)) << (16 * (e & 1));
+      const int y = y0 + s_dy[col + e], x = x0 + s_dx[col + e];
+      v[e] = (y >= 0 && y < H && x >= 0 && x < W) ? __ldg(img + s_plane[col + e] + y * W + x) : 0.f;
     }
-    *reinterpret_cast<uint4*>(A + uint64_t(m) * Kp + col) = make_uint4(o[0], o[1], o[2], o[3]);
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = uint32_t(to_bf(v[2 * j])) | (uint32_t(to_bf(v[2 * j + 1])) << 16);
+    *reinterpret_cast<uint4*>(A + i * 8) = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 
@@ -399,10 +408,10 @@ void im2col(const uint16_t* in, uint16_t* A, int N, int H, int W, int Ctot, int 
 
 void im2col_input(const float* in, uint16_t* A, int N, int C, int H, int W, int R, int S, int stride, int pad, int P,
                   int Q, int Kp, cudaStream_t s) {
-  if (Kp % 8) raise(Errc::InvalidArgument, "im2col_input needs Kp % 8 == 0");
-  const uint64_t M = uint64_t(N) * P * Q;
-  launch_pdl(im2col_input_kernel, dim3(unsigned(std::min<uint64_t>((M + 255) / 256, 64)), unsigned(Kp / 8)), dim3(256),
-             0, s, in, A, N, C, H, W, R, S, stride, pad, P, Q, Kp);
+  if (Kp % 8 || Kp > kIm2colMaxK) raise(Errc::InvalidArgument, "im2col_input needs Kp % 8 == 0, Kp <= 512");
+  const uint64_t chunks = uint64_t(N) * P * Q * (Kp / 8);
+  launch_pdl(im2col_input_kernel, dim3(unsigned(std::min<uint64_t>((chunks + 255) / 256, 148 * 16))), dim3(256), 0, s,
+             in, A, N, C, H, W, R, S, stride, pad, P, Q, Kp);
 }
 
 void maxpool(const uint16_t* in, uint16_t* out, int N, int H, int W, int C, int k, int stride, int pad, int P, int Q,
