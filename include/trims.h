@@ -386,7 +386,9 @@ int trims_host_alloc(uint64_t bytes, void** out);
 void trims_host_free(void* p);
 /* Parity tap: the device buffer architecture layer `layer` (0-based, the
  * input line excluded) wrote in the last forward, NHWC dims4 = {n, h, w, c},
- * dtype 0 = bf16, 1 = fp32 (the logits). layer < 0 returns the layer count.
+ * dtype 0 = bf16, 1 = fp32 (the logits), 2 = not kept (a conv whose 2x2 max
+ * pool ran in its epilogue: *ptr = NULL, the pool layer's tap holds the
+ * pooled result). layer < 0 returns the layer count.
  * No reference counterpart (the reference has no inference math); it lets the
  * tests check every layer against the CPU oracle on the device's own inputs. */
 int trims_net_tap(trims_net* net, int layer, const void** ptr, int dims4[4], int* dtype);

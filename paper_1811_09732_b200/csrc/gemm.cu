@@ -102,6 +102,41 @@ struct Smem {
   static_assert(S == 1 || RING >= BM * BN * 4, "split-K outgoing blocks exceed the ring");
 };
 
+// Fused 2x2 / stride-2 max pool of a staged bf16 tile (128 rows = Hbox x
+// Wbox pixels, row hr * Wbox + wc; BN channels in SWIZZLE_128B boxes of 64
+// channels x 128 rows): pooled row ph * Wbox/2 + pw = the max of rows
+// 2ph * Wbox + 2pw + {0, 1, Wbox, Wbox + 1}, written in place to rows
+// [0, 32) of the same boxes (every thread's reads precede every write). The
+// max of bf16 values is one of them: bit-identical to pooling the stored
+// tile. 256 threads (t), named barrier 2.
+template <int BN>
+__device__ __forceinline__ void pool_staged_tile(uint16_t* s_out, int t, int wl) {
+  constexpr int CPR = BN / 8, PER = BN / 64;  // 16-byte chunks per row; pooled chunks per thread
+  auto at = [&](int r, int c) {
+    return reinterpret_cast<uint4*>(s_out + (c >> 6) * BM * 64 + r * 64 + ((((c & 63) >> 3) ^ (r & 7)) << 3));
+  };
+  auto mx = [](uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    const float lo = fmaxf(fmaxf(bf16_lo(a), bf16_lo(b)), fmaxf(bf16_lo(c), bf16_lo(d)));
+    const float hi = fmaxf(fmaxf(bf16_hi(a), bf16_hi(b)), fmaxf(bf16_hi(c), bf16_hi(d)));
+    return pack_bf16x2(lo, hi);
+  };
+  uint4 v[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int i = t + k * 256, pr = i / CPR, c = (i % CPR) * 8;
+    const int ph = pr >> (wl - 1), pw = pr & ((1 << (wl - 1)) - 1);
+    const int r = ((2 * ph) << wl) + 2 * pw;
+    const uint4 a = *at(r, c), b = *at(r + 1, c), d = *at(r + (1 << wl), c), e = *at(r + (1 << wl) + 1, c);
+    v[k] = make_uint4(mx(a.x, b.x, d.x, e.x), mx(a.y, b.y, d.y, e.y), mx(a.z, b.z, d.z, e.z), mx(a.w, b.w, d.w, e.w));
+  }
+  asm volatile("bar.sync 2, 256;" ::: "memory");  // every window read before any pooled row is written
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int i = t + k * 256;
+    *at(i / CPR, (i % CPR) * 8) = v[k];
+  }
+}
+
 // S = 1: one CTA per output tile. S > 1: grid.z = S splits of K, the S CTAs
 // of a tile form one (1, 1, S) cluster and split z owns output columns
 // [z*CW, (z+1)*CW), CW = BN / S. Measured building blocks in one 8-CTA
@@ -575,14 +610,20 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
 #ifdef TRIMS_GEMM_TRACE
       if (threadIdx.x == 128) GT_SET(gt_slot, 15, gtimer());
 #endif
+      if (cg.pool) {  // fused 2x2 max pool: the pooled tile replaces rows [0, 32)
+        pool_staged_tile<BN>(s_out, threadIdx.x - 128, cg.wbox_log2);
+        fence_proxy_async_smem();
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+      }
       if (tma_out) {
         // one TMA store per 64-channel box; the engine clips rows / channels
         // outside the output. The CTA stays until the boxes are read out.
         if (threadIdx.x == 128) {
+          const int pl = cg.pool;  // pooled: box coordinates halve
 #pragma unroll
           for (int b = 0; b < BN / 64; ++b) {
             const uint16_t* src = s_out + b * BM * 64;
-            if (cg.impl) tma_store_4d(&tmD, src, n0 + b * 64, tw * wbox, th * cg.hbox, ti);
+            if (cg.impl) tma_store_4d(&tmD, src, n0 + b * 64, (tw * wbox) >> pl, (th * cg.hbox) >> pl, ti);
             else tma_store_2d(&tmD, src, n0 + b * 64, m0);
           }
           bulk_commit();
@@ -918,11 +959,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_persist_kernel(const __grid_
       if (lane == 0) mbar_arrive(&acc_empty[b]);
       fence_proxy_async_smem();                       // staged tile -> async proxy
       asm volatile("bar.sync 2, 256;" ::: "memory");  // the whole tile is staged
+      if (cg.pool) {  // fused 2x2 max pool: the pooled tile replaces rows [0, 32)
+        pool_staged_tile<BN>(s_out, et, cg.wbox_log2);
+        fence_proxy_async_smem();
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+      }
       if (et == 0) {
+        const int pl = cg.pool;  // pooled: box coordinates halve
 #pragma unroll
         for (int bx = 0; bx < BN / 64; ++bx) {
           const uint16_t* src = s_out + bx * BM * 64;
-          if (cg.impl) tma_store_4d(&J.td, src, tl.n0 + bx * 64, tl.tw * wbox, tl.th * cg.hbox, tl.ti);
+          if (cg.impl)
+            tma_store_4d(&J.td, src, tl.n0 + bx * 64, (tl.tw * wbox) >> pl, (tl.th * cg.hbox) >> pl, tl.ti);
           else tma_store_2d(&J.td, src, tl.n0 + bx * 64, tl.m0);
         }
         bulk_commit();
@@ -1042,6 +1090,21 @@ CUtensorMap tile_map_conv(const uint16_t* ptr, uint64_t ld, const ConvGeom& g, u
                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
            "cuTensorMapEncodeTiled (conv tile)");
+  return m;
+}
+
+// Pooled output map of a conv with a fused 2x2 / 2 max pool: NHWC
+// [n][P/2][Q/2][ld], boxes of 64 channels x (Wbox/2 x Hbox/2) pooled pixels.
+CUtensorMap tile_map_pool(const uint16_t* ptr, uint64_t ld, const ConvGeom& g, uint64_t N) {
+  CUtensorMap m;
+  cuuint64_t dims[4] = {N, cuuint64_t(g.Q / 2), cuuint64_t(g.P / 2), cuuint64_t(g.N)};
+  cuuint64_t strides[3] = {ld * 2, cuuint64_t(g.Q / 2) * ld * 2, cuuint64_t(g.P / 2) * (g.Q / 2) * ld * 2};
+  cuuint32_t box[4] = {64, uint32_t(1 << (g.wbox_log2 - 1)), uint32_t(g.hbox / 2), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  cu_check(encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(ptr), dims, strides, box,
+                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+           "cuTensorMapEncodeTiled (pool tile)");
   return m;
 }
 
@@ -1174,6 +1237,8 @@ void run_pair(const Prepared& p, const Prepared* q, cudaStream_t stream) {
   if (p.splits < 1 || p.splits > kMaxSplits || (p.splits & (p.splits - 1)) || (p.bn / p.splits) % 8 ||
       (p.bn == 256 && p.splits > 1))
     raise(Errc::InvalidArgument, "GEMM split count");
+  if ((p.g.pool || (q && q->g.pool)) && (p.splits != 1 || p.pair || p.mc > 1 || !p.tma_out))
+    raise(Errc::InvalidArgument, "a fused pool needs an unsplit, TMA-stored GEMM");
   if (q && (q->bn != p.bn || q->splits != p.splits || q->lean != p.lean))
     raise(Errc::InvalidArgument, "grouped GEMMs need the same tile width, split count and variant");
   if (p.persist) {  // persistent, double-buffered accumulators: unsplit, single GEMM, TMA-store output
@@ -1382,12 +1447,28 @@ uint64_t tile_rows(const Prepared& p) {
 }
 
 ConvGeom conv_geom(int N, int H, int W, int C, int R, int S, int stride, int pad, int P, int Q, int cgroup,
-                   int c_off) {
+                   int c_off, bool pool_box) {
   ConvGeom g;
   g.impl = 1;
   g.N = N, g.H = H, g.W = W, g.C = C, g.R = R, g.S = S, g.stride = stride, g.pad = pad, g.P = P, g.Q = Q;
   int wl = 0;
   while ((1 << wl) < Q && wl < 7) ++wl;   // Wbox = next power of two >= Q, at most 128
+  if (pool_box) {
+    // even box sides: Wbox <= 64 (Hbox >= 2); the widest Wbox that tiles Q
+    // exactly, else the one wasting the fewest columns
+    int best = -1;
+    uint64_t waste_best = ~0ull;
+    for (int w = std::min(wl, 6); w >= 1; --w) {
+      if ((BM >> w) * stride > 256 || (1 << w) * stride > 256) continue;
+      const uint64_t waste = uint64_t(((Q + (1 << w) - 1) >> w) << w) - uint64_t(Q);
+      if (waste < waste_best) {
+        waste_best = waste;
+        best = w;
+      }
+    }
+    if (best < 0) raise(Errc::InvalidArgument, "no pooling tile box for this conv");
+    wl = best;
+  }
   while ((1 << wl) * stride > 256) --wl;  // TMA box dims are <= 256 elements
   while ((BM >> wl) * stride > 256) ++wl;
   g.wbox_log2 = wl;
@@ -1422,7 +1503,13 @@ Prepared prepare_conv(const void* act, const ConvGeom& g, const Operand& B, cons
   p.ta = m;
   p.g = g;
   if (e.residual) p.tr = tile_map_conv(e.residual, e.ldr, g, p.N);
-  if (p.tma_out) p.td = tile_map_conv(e.out, e.ldo, g, p.N);
+  if (g.pool) {
+    if (!p.tma_out || g.P % 2 || g.Q % 2 || g.wbox_log2 < 1 || g.hbox % 2)
+      raise(Errc::InvalidArgument, "fused pool: even output / tile sides and a TMA-stored output");
+    p.td = tile_map_pool(e.out, e.ldo, g, p.N);
+  } else if (p.tma_out) {
+    p.td = tile_map_conv(e.out, e.ldo, g, p.N);
+  }
   return p;
 }
 

@@ -44,11 +44,17 @@ struct ConvGeom {
   int N, H, W, C, R, S, stride, pad, P, Q;
   int wbox_log2, hbox, tiles_w, tiles_h, cblocks;
   int c_off{0};  // grouped conv: first channel of this group (the group has cblocks * 64 channels)
+  // 1: a 2x2 / stride-2 max pool is fused into the epilogue (the output is
+  // the pooled P/2 x Q/2 map; unsplit launches, TMA-store output)
+  int pool{0};
 };
 // C = the activation's channels; cg / c_off = this group's channel count and
 // first channel (cg = C, c_off = 0 for an ungrouped conv; cg % 64 == 0).
+// pool_box: a tile box with an even number of rows and columns (>= 2 each)
+// that tiles Q exactly where possible, so every 2x2 pooling window lies
+// inside one tile.
 ConvGeom conv_geom(int N, int H, int W, int C, int R, int S, int stride, int pad, int P, int Q, int cg = 0,
-                   int c_off = 0);
+                   int c_off = 0, bool pool_box = false);
 int pick_bn(uint64_t M, uint64_t N, int sms);
 
 // A GEMM with its tensor maps encoded once (the executor builds these at

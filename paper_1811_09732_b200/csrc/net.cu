@@ -155,6 +155,15 @@ int persist_mode() {
   return m;
 }
 
+// TRIMS_POOL_FUSE=0: 2x2 max pools stay separate launches (A/B switch).
+bool pool_fuse_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TRIMS_POOL_FUSE");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
 // TRIMS_SPLITK=0 turns split-K off (A/B switch).
 bool splitk_enabled() {
   static const bool on = [] {
@@ -250,8 +259,14 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
     std::function<void(cudaStream_t)> rebind;
   };
   std::optional<Pending> pending;
+  bool pool_fused = false;  // the previous conv wrote this pool layer's output
   for (size_t li = 0; li < layers.size(); ++li) {
     const LayerSpec& l = layers[li];
+    if (pool_fused) {
+      pool_fused = false;
+      taps_.push_back({cur.p, cur.n, cur.h, cur.w, cur.c, 0});
+      continue;
+    }
     const size_t first_step = steps_.size();
     Act produced;  // this layer's output buffer (the parity tap)
     std::vector<int> joins;
@@ -326,6 +341,17 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       // main path and is joined by the first layer that references it.
       const bool branch = branches_enabled() && groups == 1 && (direct || implicit) && !l.s("out").empty() &&
                           li + 1 < layers.size() && !layers[li + 1].s("src").empty();
+      // A 2x2 / 2 max pool right after this conv runs in the GEMM's epilogue
+      // when the GEMM is unsplit (one dependent launch less; VGG). Not before
+      // a flatten: that pool writes NCHW itself.
+      const LayerSpec* nx = li + 1 < layers.size() ? &layers[li + 1] : nullptr;
+      const bool pool_cand = pool_fuse_enabled() && implicit && groups == 1 && !branch && l.s("out").empty() &&
+                             l.s("res").empty() && nx && nx->kind == "pool_max" && nx->i("k") == 2 &&
+                             nx->i("stride", 2) == 2 && nx->i("pad", 0) == 0 && nx->s("out").empty() &&
+                             nx->s("src").empty() && P % 2 == 0 && Q % 2 == 0 &&
+                             !(li + 2 < layers.size() && layers[li + 2].kind == "flatten");
+      bool fused_here = false;
+      Act pout{};
       bool first_group = true;
       for (int gi = 0; gi < groups; ++gi) {
         const uint16_t* A = direct ? in.p : col;
@@ -349,15 +375,16 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
         const gemm::Operand Bop{wpad ? wpad : reinterpret_cast<const uint16_t*>(uintptr_t(256)), uint64_t(kg),
                                 uint64_t(kp), uint64_t(kp)};
         auto prep = std::make_shared<gemm::Prepared>(
-            implicit ? gemm::prepare_conv(in.p, gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg),
-                                          Bop, e)
+            implicit ? gemm::prepare_conv(
+                           in.p, gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg, pool_cand),
+                           Bop, e)
                      : gemm::prepare({A, M, uint64_t(kp), uint64_t(direct ? cin : kp)}, Bop, e));
         // the same GEMM prepared with another tile width
         auto remake = [&](int bn) {
           return std::make_shared<gemm::Prepared>(
-              implicit ? gemm::prepare_conv(in.p,
-                                            gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg),
-                                            Bop, e, bn)
+              implicit ? gemm::prepare_conv(
+                             in.p, gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg, pool_cand),
+                             Bop, e, bn)
                        : gemm::prepare({A, M, uint64_t(kp), uint64_t(direct ? cin : kp)}, Bop, e, bn));
         };
         if (split_ok && tile_model_enabled()) {
@@ -408,6 +435,20 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
             prep->persist = true;
           }
         }
+        if (pool_cand && !pair_first && !pair_second && prep->splits == 1 && !prep->pair && prep->mc <= 1 &&
+            prep->tma_out) {
+          pout = {reinterpret_cast<uint16_t*>(alloc(uint64_t(batch) * (P / 2) * (Q / 2) * cout * 2)), batch, P / 2,
+                  Q / 2, cout};
+          gemm::ConvGeom g = gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg, true);
+          g.pool = 1;
+          gemm::Epilogue ep = e;
+          ep.out = pout.p;
+          auto np = std::make_shared<gemm::Prepared>(gemm::prepare_conv(in.p, g, Bop, ep, prep->bn));
+          np->persist = prep->persist;
+          np->lean = prep->lean;
+          prep = np;
+          fused_here = true;
+        }
         const uint64_t b_off = w_off + uint64_t(gi) * kg * rsc * 2;
         const bool do_params = first_group && bind_params;
         auto rebind = [=](cudaStream_t s) {
@@ -452,6 +493,11 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       if (branch) branch_of[l.s("out")] = nbranches_++;
       if (!l.s("out").empty()) named[l.s("out")] = out;
       if (!branch) cur = out;
+      if (fused_here) {  // this conv's tap is the pooled map (the next layer's); its own is not kept
+        produced = {};
+        cur = pout;
+        pool_fused = true;
+      }
     } else if (l.kind == "pool_max") {
       const int k = l.i("k"), st = l.i("stride", k), pad = l.i("pad", 0);
       const Act in = cur;
@@ -554,6 +600,8 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
     attach_joins();
     if (l.kind != "input") {
       if (l.kind == "fc" && int(li) == last_fc) taps_.push_back({logits_, batch, 1, 1, classes_, 1});
+      else if (l.kind == "conv" && !produced.p)
+        taps_.push_back({nullptr, 0, 0, 0, 0, 2});  // fused: the following pool's tap holds the result
       else if (l.kind == "conv" || (l.kind == "pool_max" && produced.p))
         taps_.push_back({produced.p, produced.n, produced.h, produced.w, produced.c, 0});
       else taps_.push_back({cur.p, cur.n, cur.h, cur.w, cur.c, 0});

@@ -78,11 +78,15 @@ class BoundNet:
 
     def tap(self, layer: int):
         """Device view of what architecture layer `layer` wrote in the last forward
-        (NCHW-permuted torch view of the NHWC buffer; bf16, or fp32 logits)."""
+        (NCHW-permuted torch view of the NHWC buffer; bf16, or fp32 logits), or
+        None for a conv whose 2x2 max pool was fused into it (the next layer's
+        tap is the pooled map)."""
         import torch
         from .client import TensorView
         p, dims, dt = ctypes.c_void_p(), (ctypes.c_int * 4)(), ctypes.c_int()
         check(lib.trims_net_tap(self._h, layer, ctypes.byref(p), dims, ctypes.byref(dt)))
+        if dt.value == 2:  # a conv whose 2x2 max pool ran in its epilogue: the pool layer holds the result
+            return None
         n, h, w, c = dims
         es = 4 if dt.value else 2
         t = TensorView(f"layer{layer}", [n * h * w * c * es], "i8", "native", 0, n * h * w * c * es,

@@ -62,10 +62,13 @@ def main():
     # utilisation (the realtime tensor-active counters read n/a on this ncu).
     import re
     for l in launches:
-        m = re.search(r"gemm_tc_kernel<(\d+),", l["kernel"])
+        # gemm_tc_kernel<BN, STAGES, S, MC> (MC = -2: a 2-SM pair, M = 256
+        # per instruction) or gemm_persist_kernel<BN, STAGES>
+        m = re.search(r"gemm_(?:tc|persist)_kernel<(\d+),\s*\d+(?:,\s*\d+,\s*(-?\d+))?", l["kernel"])
         if m and l["tc_inst"] and l["us"]:
             bn = int(m.group(1))
-            fl = float(l["tc_inst"]) * 128 * bn * 16 * 2
+            rows = 256 if m.group(2) == "-2" else 128
+            fl = float(l["tc_inst"]) * rows * bn * 16 * 2
             l["mma_flop_issued"] = fl
             l["mma_tflops_issued"] = round(fl / (l["us"] * 1e-6) / 1e12, 2)
             l["tensor_pipe_frac_of_2250tf"] = round(fl / (l["us"] * 1e-6) / 2.25e15, 4)

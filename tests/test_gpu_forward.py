@@ -137,11 +137,19 @@ def _layerwise(arch, view, net, name, batch):
     net.forward(x, graph=True)
     torch.cuda.synchronize()
     W = _resident_weights(view)
-    dev = [net.tap(i).float().cpu() for i in range(len(arch.layers))]
+    taps = [net.tap(i) for i in range(len(arch.layers))]
+    dev = [t.float().cpu() if t is not None else None for t in taps]
     named, cur = {}, torch_ref._bf(x)
     report = []
     for i, l in enumerate(arch.layers):
         want = torch_ref.apply_layer_bf16(arch, i, W, cur, named, batch)
+        if dev[i] is None:  # conv with its 2x2 max pool fused: checked through the pool layer's tap
+            assert l.kind == "conv" and arch.layers[i + 1].kind == "pool_max", f"layer {i} has no tap"
+            report.append((i, l.kind, l.name, "fused"))
+            cur = want
+            if l.out:
+                named[l.out] = cur
+            continue
         got = dev[i].reshape(want.shape)
         if i == len(arch.layers) - 1 and batch <= 8:  # fp32 logits straight from the GEMV
             err = ((got - want).abs().max() / want.abs().max()).item()
