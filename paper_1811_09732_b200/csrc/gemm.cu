@@ -109,16 +109,21 @@ struct Smem {
 // [0, 32) of the same boxes (every thread's reads precede every write). The
 // max of bf16 values is one of them: bit-identical to pooling the stored
 // tile. 256 threads (t), named barrier 2.
+// 8 bf16 channels: the max of four pixels' 16-byte chunks
+__device__ __forceinline__ uint4 max4_bf16x8(uint4 a, uint4 b, uint4 c, uint4 d) {
+  auto mx = [](uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    const float lo = fmaxf(fmaxf(bf16_lo(a), bf16_lo(b)), fmaxf(bf16_lo(c), bf16_lo(d)));
+    const float hi = fmaxf(fmaxf(bf16_hi(a), bf16_hi(b)), fmaxf(bf16_hi(c), bf16_hi(d)));
+    return pack_bf16x2(lo, hi);
+  };
+  return make_uint4(mx(a.x, b.x, c.x, d.x), mx(a.y, b.y, c.y, d.y), mx(a.z, b.z, c.z, d.z), mx(a.w, b.w, c.w, d.w));
+}
+
 template <int BN>
 __device__ __forceinline__ void pool_staged_tile(uint16_t* s_out, int t, int wl) {
   constexpr int CPR = BN / 8, PER = BN / 64;  // 16-byte chunks per row; pooled chunks per thread
   auto at = [&](int r, int c) {
     return reinterpret_cast<uint4*>(s_out + (c >> 6) * BM * 64 + r * 64 + ((((c & 63) >> 3) ^ (r & 7)) << 3));
-  };
-  auto mx = [](uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    const float lo = fmaxf(fmaxf(bf16_lo(a), bf16_lo(b)), fmaxf(bf16_lo(c), bf16_lo(d)));
-    const float hi = fmaxf(fmaxf(bf16_hi(a), bf16_hi(b)), fmaxf(bf16_hi(c), bf16_hi(d)));
-    return pack_bf16x2(lo, hi);
   };
   uint4 v[PER];
 #pragma unroll
@@ -126,8 +131,7 @@ __device__ __forceinline__ void pool_staged_tile(uint16_t* s_out, int t, int wl)
     const int i = t + k * 256, pr = i / CPR, c = (i % CPR) * 8;
     const int ph = pr >> (wl - 1), pw = pr & ((1 << (wl - 1)) - 1);
     const int r = ((2 * ph) << wl) + 2 * pw;
-    const uint4 a = *at(r, c), b = *at(r + 1, c), d = *at(r + (1 << wl), c), e = *at(r + (1 << wl) + 1, c);
-    v[k] = make_uint4(mx(a.x, b.x, d.x, e.x), mx(a.y, b.y, d.y, e.y), mx(a.z, b.z, d.z, e.z), mx(a.w, b.w, d.w, e.w));
+    v[k] = max4_bf16x8(*at(r, c), *at(r + 1, c), *at(r + (1 << wl), c), *at(r + (1 << wl) + 1, c));
   }
   asm volatile("bar.sync 2, 256;" ::: "memory");  // every window read before any pooled row is written
 #pragma unroll
@@ -716,7 +720,29 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
           if (n0 + c < N) {
             uint32_t o[4];
             epi8(rr, c, v, o);
-            store8(row, n0 + c, o);
+            if (cg.pool)  // staged (the residual box is free: no residual with a fused pool)
+              *reinterpret_cast<uint4*>(smem + L::RES + (uint32_t(rr) * (CW / 8) + g) * 16) =
+                  make_uint4(o[0], o[1], o[2], o[3]);
+            else
+              store8(row, n0 + c, o);
+          }
+        }
+      }
+      if (cg.pool) {  // fused 2x2 max pool of my slice: 32 pooled rows x CW / 8 chunks
+        asm volatile("bar.sync 2, 256;" ::: "memory");  // every row of the slice staged
+        constexpr int CH = CW / 8;
+        if (t < 32 * CH) {
+          const int pr = t / CH, gch = t % CH, wl = cg.wbox_log2;
+          const int ph = pr >> (wl - 1), pw = pr & ((1 << (wl - 1)) - 1), r = ((2 * ph) << wl) + 2 * pw;
+          const int P2 = cg.P / 2, Q2 = cg.Q / 2, py = th * (cg.hbox / 2) + ph, px = tw * (wbox / 2) + pw;
+          const int c = z * CW + 8 * gch;
+          if (py < P2 && px < Q2 && n0 + c < N) {  // a valid pooled pixel's window rows are all valid
+            auto at = [&](int rw) {
+              return *reinterpret_cast<const uint4*>(smem + L::RES + (uint32_t(rw) * CH + gch) * 16);
+            };
+            const uint4 m = max4_bf16x8(at(r), at(r + 1), at(r + wbox), at(r + wbox + 1));
+            const uint32_t o[4] = {m.x, m.y, m.z, m.w};
+            store8((ti * P2 + py) * Q2 + px, n0 + c, o);
           }
         }
       }
@@ -1237,8 +1263,8 @@ void run_pair(const Prepared& p, const Prepared* q, cudaStream_t stream) {
   if (p.splits < 1 || p.splits > kMaxSplits || (p.splits & (p.splits - 1)) || (p.bn / p.splits) % 8 ||
       (p.bn == 256 && p.splits > 1))
     raise(Errc::InvalidArgument, "GEMM split count");
-  if ((p.g.pool || (q && q->g.pool)) && (p.splits != 1 || p.pair || p.mc > 1 || !p.tma_out))
-    raise(Errc::InvalidArgument, "a fused pool needs an unsplit, TMA-stored GEMM");
+  if ((p.g.pool || (q && q->g.pool)) && (p.pair || p.mc > 1 || (p.splits == 1 && !p.tma_out)))
+    raise(Errc::InvalidArgument, "a fused pool needs a single-CTA (split or TMA-stored) GEMM");
   if (q && (q->bn != p.bn || q->splits != p.splits || q->lean != p.lean))
     raise(Errc::InvalidArgument, "grouped GEMMs need the same tile width, split count and variant");
   if (p.persist) {  // persistent, double-buffered accumulators: unsplit, single GEMM, TMA-store output
@@ -1504,8 +1530,8 @@ Prepared prepare_conv(const void* act, const ConvGeom& g, const Operand& B, cons
   p.g = g;
   if (e.residual) p.tr = tile_map_conv(e.residual, e.ldr, g, p.N);
   if (g.pool) {
-    if (!p.tma_out || g.P % 2 || g.Q % 2 || g.wbox_log2 < 1 || g.hbox % 2)
-      raise(Errc::InvalidArgument, "fused pool: even output / tile sides and a TMA-stored output");
+    if (!p.tma_out || g.P % 2 || g.Q % 2 || g.wbox_log2 < 1 || g.hbox % 2 || e.residual)
+      raise(Errc::InvalidArgument, "fused pool: even output / tile sides, a TMA-stored output, no residual");
     p.td = tile_map_pool(e.out, e.ldo, g, p.N);
   } else if (p.tma_out) {
     p.td = tile_map_conv(e.out, e.ldo, g, p.N);

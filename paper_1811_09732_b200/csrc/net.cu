@@ -342,8 +342,9 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       const bool branch = branches_enabled() && groups == 1 && (direct || implicit) && !l.s("out").empty() &&
                           li + 1 < layers.size() && !layers[li + 1].s("src").empty();
       // A 2x2 / 2 max pool right after this conv runs in the GEMM's epilogue
-      // when the GEMM is unsplit (one dependent launch less; VGG). Not before
-      // a flatten: that pool writes NCHW itself.
+      // (one dependent launch less; VGG): on the staged tile, or on each
+      // split-K owner's reduced slice. Not before a flatten: that pool writes
+      // NCHW itself.
       const LayerSpec* nx = li + 1 < layers.size() ? &layers[li + 1] : nullptr;
       const bool pool_cand = pool_fuse_enabled() && implicit && groups == 1 && !branch && l.s("out").empty() &&
                              l.s("res").empty() && nx && nx->kind == "pool_max" && nx->i("k") == 2 &&
@@ -435,8 +436,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
             prep->persist = true;
           }
         }
-        if (pool_cand && !pair_first && !pair_second && prep->splits == 1 && !prep->pair && prep->mc <= 1 &&
-            prep->tma_out) {
+        if (pool_cand && !pair_first && !pair_second && !prep->pair && prep->mc <= 1 && prep->tma_out) {
           pout = {reinterpret_cast<uint16_t*>(alloc(uint64_t(batch) * (P / 2) * (Q / 2) * cout * 2)), batch, P / 2,
                   Q / 2, cout};
           gemm::ConvGeom g = gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg, true);
@@ -446,6 +446,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
           auto np = std::make_shared<gemm::Prepared>(gemm::prepare_conv(in.p, g, Bop, ep, prep->bn));
           np->persist = prep->persist;
           np->lean = prep->lean;
+          np->splits = prep->splits;
           prep = np;
           fused_here = true;
         }
