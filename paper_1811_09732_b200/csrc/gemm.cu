@@ -742,7 +742,12 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
             };
             const uint4 m = max4_bf16x8(at(r), at(r + 1), at(r + wbox), at(r + wbox + 1));
             const uint32_t o[4] = {m.x, m.y, m.z, m.w};
-            store8((ti * P2 + py) * Q2 + px, n0 + c, o);
+            if (cg.pool == 2) {  // NCHW (torch's flatten order for the FC layer that follows)
+              uint16_t* dp = D + (size_t(ti) * ldd + n0 + c) * P2 * Q2 + size_t(py) * Q2 + px;
+              for (int j = 0; j < 8 && n0 + c + j < N; ++j) dp[size_t(j) * P2 * Q2] = uint16_t(o[j >> 1] >> (16 * (j & 1)));
+            } else {
+              store8((ti * P2 + py) * Q2 + px, n0 + c, o);
+            }
           }
         }
       }
@@ -1263,7 +1268,8 @@ void run_pair(const Prepared& p, const Prepared* q, cudaStream_t stream) {
   if (p.splits < 1 || p.splits > kMaxSplits || (p.splits & (p.splits - 1)) || (p.bn / p.splits) % 8 ||
       (p.bn == 256 && p.splits > 1))
     raise(Errc::InvalidArgument, "GEMM split count");
-  if ((p.g.pool || (q && q->g.pool)) && (p.pair || p.mc > 1 || (p.splits == 1 && !p.tma_out)))
+  if ((p.g.pool || (q && q->g.pool)) &&
+      (p.pair || p.mc > 1 || (p.splits == 1 && (!p.tma_out || p.g.pool == 2 || (q && q->g.pool == 2)))))
     raise(Errc::InvalidArgument, "a fused pool needs a single-CTA (split or TMA-stored) GEMM");
   if (q && (q->bn != p.bn || q->splits != p.splits || q->lean != p.lean))
     raise(Errc::InvalidArgument, "grouped GEMMs need the same tile width, split count and variant");
@@ -1473,20 +1479,29 @@ uint64_t tile_rows(const Prepared& p) {
 }
 
 ConvGeom conv_geom(int N, int H, int W, int C, int R, int S, int stride, int pad, int P, int Q, int cgroup,
-                   int c_off, bool pool_box) {
+                   int c_off, int pool_box) {
   ConvGeom g;
   g.impl = 1;
   g.N = N, g.H = H, g.W = W, g.C = C, g.R = R, g.S = S, g.stride = stride, g.pad = pad, g.P = P, g.Q = Q;
   int wl = 0;
   while ((1 << wl) < Q && wl < 7) ++wl;   // Wbox = next power of two >= Q, at most 128
   if (pool_box) {
-    // even box sides: Wbox <= 64 (Hbox >= 2); the widest Wbox that tiles Q
-    // exactly, else the one wasting the fewest columns
+    // even box sides: Wbox <= 64 (Hbox >= 2); pool_box 1: the box whose
+    // tiles cover the fewest pixels outside the P x Q map, 2: the fewest
+    // columns outside it (taller boxes); the widest on a tie
     int best = -1;
     uint64_t waste_best = ~0ull;
     for (int w = std::min(wl, 6); w >= 1; --w) {
       if ((BM >> w) * stride > 256 || (1 << w) * stride > 256) continue;
-      const uint64_t waste = uint64_t(((Q + (1 << w) - 1) >> w) << w) - uint64_t(Q);
+      const uint64_t hb = uint64_t(BM >> w);
+      static const int forced = [] {  // A/B: TRIMS_POOL_BOX=area|col
+        const char* e = std::getenv("TRIMS_POOL_BOX");
+        return !e ? 0 : std::string(e) == "col" ? 2 : std::string(e) == "area" ? 1 : 0;
+      }();
+      const bool col_rule = (forced ? forced : pool_box) == 2;
+      const uint64_t waste = col_rule ? uint64_t(((Q + (1 << w) - 1) >> w) << w) - uint64_t(Q)
+                                      : uint64_t(((Q + (1 << w) - 1) >> w) << w) * ((uint64_t(P) + hb - 1) / hb * hb) -
+                                            uint64_t(P) * uint64_t(Q);
       if (waste < waste_best) {
         waste_best = waste;
         best = w;

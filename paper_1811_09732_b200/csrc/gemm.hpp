@@ -45,16 +45,18 @@ struct ConvGeom {
   int wbox_log2, hbox, tiles_w, tiles_h, cblocks;
   int c_off{0};  // grouped conv: first channel of this group (the group has cblocks * 64 channels)
   // 1: a 2x2 / stride-2 max pool is fused into the epilogue (the output is
-  // the pooled P/2 x Q/2 map; unsplit launches, TMA-store output)
+  // the pooled P/2 x Q/2 map, NHWC); 2: the same written NCHW (a flatten
+  // follows; split-K launches only)
   int pool{0};
 };
 // C = the activation's channels; cg / c_off = this group's channel count and
 // first channel (cg = C, c_off = 0 for an ungrouped conv; cg % 64 == 0).
-// pool_box: a tile box with an even number of rows and columns (>= 2 each)
-// that tiles Q exactly where possible, so every 2x2 pooling window lies
-// inside one tile.
+// pool_box != 0: a tile box with an even number of rows and columns (>= 2
+// each), so every 2x2 pooling window lies inside one tile: 1 = the least
+// padded tile area, 2 = the fewest padded columns (taller boxes; measured
+// faster for single-wave layers, 1 for multi-wave ones).
 ConvGeom conv_geom(int N, int H, int W, int C, int R, int S, int stride, int pad, int P, int Q, int cg = 0,
-                   int c_off = 0, bool pool_box = false);
+                   int c_off = 0, int pool_box = 0);
 int pick_bn(uint64_t M, uint64_t N, int sms);
 
 // A GEMM with its tensor maps encoded once (the executor builds these at

@@ -349,8 +349,20 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       const bool pool_cand = pool_fuse_enabled() && implicit && groups == 1 && !branch && l.s("out").empty() &&
                              l.s("res").empty() && nx && nx->kind == "pool_max" && nx->i("k") == 2 &&
                              nx->i("stride", 2) == 2 && nx->i("pad", 0) == 0 && nx->s("out").empty() &&
-                             nx->s("src").empty() && P % 2 == 0 && Q % 2 == 0 &&
-                             !(li + 2 < layers.size() && layers[li + 2].kind == "flatten");
+                             nx->s("src").empty() && P % 2 == 0 && Q % 2 == 0;
+      // ... before a flatten only on a split-K launch (its owners store the
+      // pooled slice NCHW, torch's flatten order, with thread stores)
+      const bool pool_flat = li + 2 < layers.size() && layers[li + 2].kind == "flatten" && P * Q > 4;
+      // Off by default: the NCHW thread stores made VGG-16 b1 slower than the
+      // separate pool (0.1885 -> 0.1933 ms, profiles/r3/pool_box_flat_ab.log).
+      static const bool flat_fuse = [] {  // A/B: TRIMS_POOL_FLAT=1 fuses it
+        const char* e = std::getenv("TRIMS_POOL_FLAT");
+        return e && std::string(e) == "1";
+      }();
+      // tile box for a fused pool: taller boxes for a single-wave layer
+      // (VGG-16 b1 0.1885 -> 0.1862 ms), least padding for multi-wave ones
+      // (b32 1.483 -> 1.399)
+      const int pool_box = !pool_cand ? 0 : uint64_t(batch) * P * Q <= uint64_t(sms_) * 128 ? 2 : 1;
       bool fused_here = false;
       Act pout{};
       bool first_group = true;
@@ -377,14 +389,14 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
                                 uint64_t(kp), uint64_t(kp)};
         auto prep = std::make_shared<gemm::Prepared>(
             implicit ? gemm::prepare_conv(
-                           in.p, gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg, pool_cand),
+                           in.p, gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg, pool_box),
                            Bop, e)
                      : gemm::prepare({A, M, uint64_t(kp), uint64_t(direct ? cin : kp)}, Bop, e));
         // the same GEMM prepared with another tile width
         auto remake = [&](int bn) {
           return std::make_shared<gemm::Prepared>(
               implicit ? gemm::prepare_conv(
-                             in.p, gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg, pool_cand),
+                             in.p, gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg, pool_box),
                              Bop, e, bn)
                        : gemm::prepare({A, M, uint64_t(kp), uint64_t(direct ? cin : kp)}, Bop, e, bn));
         };
@@ -436,11 +448,12 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
             prep->persist = true;
           }
         }
-        if (pool_cand && !pair_first && !pair_second && !prep->pair && prep->mc <= 1 && prep->tma_out) {
+        if (pool_cand && !pair_first && !pair_second && !prep->pair && prep->mc <= 1 && prep->tma_out &&
+            (!pool_flat || (prep->splits > 1 && flat_fuse))) {
           pout = {reinterpret_cast<uint16_t*>(alloc(uint64_t(batch) * (P / 2) * (Q / 2) * cout * 2)), batch, P / 2,
                   Q / 2, cout};
-          gemm::ConvGeom g = gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg, true);
-          g.pool = 1;
+          gemm::ConvGeom g = gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg, pool_box);
+          g.pool = pool_flat ? 2 : 1;
           gemm::Epilogue ep = e;
           ep.out = pout.p;
           auto np = std::make_shared<gemm::Prepared>(gemm::prepare_conv(in.p, g, Bop, ep, prep->bn));
@@ -498,6 +511,10 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
         produced = {};
         cur = pout;
         pool_fused = true;
+        if (pool_flat) {  // written NCHW: the flatten step is free
+          cur = {pout.p, batch, 1, 1, pout.h * pout.w * pout.c};
+          flat_done = true;
+        }
       }
     } else if (l.kind == "pool_max") {
       const int k = l.i("k"), st = l.i("stride", k), pad = l.i("pad", 0);
