@@ -720,7 +720,14 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
           if (n0 + c < N) {
             uint32_t o[4];
             epi8(rr, c, v, o);
-            if (cg.pool)  // staged (the residual box is free: no residual with a fused pool)
+            if (cg.pool == 3) {  // global average pool: bf16 outputs as fp32 [pixel][CW] in the idle ring
+              float* st = reinterpret_cast<float*>(smem + uint32_t(S) * uint32_t(nvalid) * CW * 4) + cr * CW + 8 * g;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                st[2 * u] = bf16_lo(o[u]);
+                st[2 * u + 1] = bf16_hi(o[u]);
+              }
+            } else if (cg.pool)  // staged (the residual box is free: no residual with a fused pool)
               *reinterpret_cast<uint4*>(smem + L::RES + (uint32_t(rr) * (CW / 8) + g) * 16) =
                   make_uint4(o[0], o[1], o[2], o[3]);
             else
@@ -728,7 +735,44 @@ __global__ void __launch_bounds__(kThreads, min_ctas<BN, STAGES, S>()) gemm_tc_k
           }
         }
       }
-      if (cg.pool) {  // fused 2x2 max pool of my slice: 32 pooled rows x CW / 8 chunks
+      if (cg.pool == 3) {
+        // fused global average pool: the tile holds whole images (host-checked:
+        // an implicit conv's tile = one image ti; a 1x1 conv's single M-tile =
+        // all M / HW images), its compact rows are the pixels in order. Thread
+        // q averages column q % CW of image q / CW in nn::avgpool_kernel's exact
+        // summation order (32 pixel slices j = k, k + 32, ..., then the slices
+        // in order, / HW): bit-identical to pooling the stored map. The staging
+        // sits past my outgoing blocks in the ring (host-checked:
+        // (S + 1) * rows <= 128 * S).
+        asm volatile("bar.sync 2, 256;" ::: "memory");  // every pixel of the slice staged
+        const float* st = reinterpret_cast<const float*>(smem + uint32_t(S) * uint32_t(nvalid) * CW * 4);
+        const int HW = cg.P * cg.Q, imgs = nvalid / HW;
+        // slice sums (image, k, column) into the receive blocks (every partial
+        // was read before the barrier above), 256 in parallel...
+        float* slc = reinterpret_cast<float*>(smem + L::RECV);
+        for (int q = t; q < 32 * CW * imgs; q += 256) {
+          const int col = q % CW, k = (q / CW) % 32, im = q / (32 * CW);
+          const float* sp = st + im * HW * CW + col;
+          float sl = 0.f;
+          for (int j = k; j < HW; j += 32) sl += sp[j * CW];
+          slc[q] = sl;
+        }
+        asm volatile("bar.sync 2, 256;" ::: "memory");
+        // ...then each (image, column) adds its 32 slices in order (independent
+        // loads first, one dependent add chain)
+        for (int q = t; q < CW * imgs; q += 256) {
+          const int col = q % CW, im = q / CW;
+          float v[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) v[k] = slc[(im * 32 + k) * CW + col];
+          float tot = 0.f;
+#pragma unroll
+          for (int k = 0; k < 32; ++k) tot += v[k];
+          if (n0 + z * CW + col < N)
+            D[size_t(cg.impl ? ti : im) * ldd + n0 + z * CW + col] =
+                uint16_t(pack_bf16x2(tot / float(HW), 0.f) & 0xffffu);
+        }
+      } else if (cg.pool) {  // fused 2x2 max pool of my slice: 32 pooled rows x CW / 8 chunks
         asm volatile("bar.sync 2, 256;" ::: "memory");  // every row of the slice staged
         constexpr int CH = CW / 8;
         if (t < 32 * CH) {
@@ -1271,6 +1315,14 @@ void run_pair(const Prepared& p, const Prepared* q, cudaStream_t stream) {
   if ((p.g.pool || (q && q->g.pool)) &&
       (p.pair || p.mc > 1 || (p.splits == 1 && (!p.tma_out || p.g.pool == 2 || (q && q->g.pool == 2)))))
     raise(Errc::InvalidArgument, "a fused pool needs a single-CTA (split or TMA-stored) GEMM");
+  for (const Prepared* x : {&p, q})
+    if (x && x->g.pool == 3) {
+      const uint64_t hw = uint64_t(x->g.P) * x->g.Q, rows = x->g.impl ? hw : x->M;  // rows of the one tile
+      if (x->splits < 2 || uint64_t(x->splits + 1) * rows > uint64_t(128) * x->splits ||
+          (!x->g.impl && (hw == 0 || x->M > 128 || x->M % hw)))
+        raise(Errc::InvalidArgument,
+              "a fused global average pool needs a split-K launch over whole images with (S + 1) * rows <= 128 * S");
+    }
   if (q && (q->bn != p.bn || q->splits != p.splits || q->lean != p.lean))
     raise(Errc::InvalidArgument, "grouped GEMMs need the same tile width, split count and variant");
   if (p.persist) {  // persistent, double-buffered accumulators: unsplit, single GEMM, TMA-store output
@@ -1544,7 +1596,10 @@ Prepared prepare_conv(const void* act, const ConvGeom& g, const Operand& B, cons
   p.ta = m;
   p.g = g;
   if (e.residual) p.tr = tile_map_conv(e.residual, e.ldr, g, p.N);
-  if (g.pool) {
+  if (g.pool == 3) {  // global average pool in the split-K owners' epilogue: one tile = one whole image
+    if (!g.impl || g.tiles_w != 1 || g.tiles_h != 1)
+      raise(Errc::InvalidArgument, "fused global average pool: one tile per image");
+  } else if (g.pool) {
     if (!p.tma_out || g.P % 2 || g.Q % 2 || g.wbox_log2 < 1 || g.hbox % 2 || e.residual)
       raise(Errc::InvalidArgument, "fused pool: even output / tile sides, a TMA-stored output, no residual");
     p.td = tile_map_pool(e.out, e.ldo, g, p.N);

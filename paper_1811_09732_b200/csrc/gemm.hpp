@@ -46,7 +46,8 @@ struct ConvGeom {
   int c_off{0};  // grouped conv: first channel of this group (the group has cblocks * 64 channels)
   // 1: a 2x2 / stride-2 max pool is fused into the epilogue (the output is
   // the pooled P/2 x Q/2 map, NHWC); 2: the same written NCHW (a flatten
-  // follows; split-K launches only)
+  // follows; split-K launches only); 3: a global average pool (output
+  // [N][Cout]; split-K launches whose tile is one whole image)
   int pool{0};
 };
 // C = the activation's channels; cg / c_off = this group's channel count and

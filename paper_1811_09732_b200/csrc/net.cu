@@ -362,6 +362,21 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       // tile box for a fused pool: taller boxes for a single-wave layer
       // (VGG-16 b1 0.1885 -> 0.1862 ms), least padding for multi-wave ones
       // (b32 1.483 -> 1.399)
+      // TRIMS_AVG_FUSE=0: the global average pool stays a separate launch (A/B)
+      static const bool avg_fuse = [] {
+        const char* e = std::getenv("TRIMS_AVG_FUSE");
+        return !(e && std::string(e) == "0");
+      }();
+      // (a named output is fine when no later layer reads it: ResNet's last
+      // block names its output for a residual nobody takes)
+      const bool out_unread = [&] {
+        const std::string o = l.s("out");
+        for (size_t j = li + 1; !o.empty() && j < layers.size(); ++j)
+          if (layers[j].s("src") == o || layers[j].s("res") == o) return false;
+        return true;
+      }();
+      const bool avg_cand = avg_fuse && (implicit || direct) && groups == 1 && !branch && out_unread && nx &&
+                            nx->kind == "pool_avg" && nx->s("out").empty() && nx->s("src").empty();
       const int pool_box = !pool_cand ? 0 : uint64_t(batch) * P * Q <= uint64_t(sms_) * 128 ? 2 : 1;
       bool fused_here = false;
       Act pout{};
@@ -463,6 +478,36 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
           prep = np;
           fused_here = true;
         }
+        // A global average pool right after the last conv (ResNet) runs in
+        // that GEMM's split-K owners: each tile is one whole image, so an owner
+        // holds every pixel of its column slice (one dependent launch less).
+        if (avg_cand && !pair_first && !pair_second && !prep->pair && prep->mc <= 1 && !prep->persist &&
+            prep->splits > 1 && uint64_t(prep->splits + 1) * P * Q <= uint64_t(128) * prep->splits) {
+          gemm::ConvGeom g{};
+          if (implicit) g = gemm::conv_geom(batch, in.h, in.w, cin, k, k, st, pad, P, Q, cg, gi * cg, 0);
+          if (implicit ? g.tiles_w == 1 && g.tiles_h == 1 : M <= 128) {
+            pout = {reinterpret_cast<uint16_t*>(alloc(uint64_t(batch) * cout * 2)), batch, 1, 1, cout};
+            gemm::Epilogue ep = e;
+            ep.out = pout.p;
+            ep.ldo = uint64_t(cout);
+            std::shared_ptr<gemm::Prepared> np;
+            if (implicit) {
+              g.pool = 3;
+              np = std::make_shared<gemm::Prepared>(gemm::prepare_conv(in.p, g, Bop, ep, prep->bn));
+            } else {  // a 1x1 conv: one plain M-tile holding all M / HW images
+              np = std::make_shared<gemm::Prepared>(
+                  gemm::prepare({A, M, uint64_t(kp), uint64_t(cin)}, Bop, ep, prep->bn));
+              np->g.pool = 3;
+              np->g.P = P;
+              np->g.Q = Q;
+              np->g.N = batch;
+            }
+            np->lean = prep->lean;
+            np->splits = prep->splits;
+            prep = np;
+            fused_here = true;
+          }
+        }
         const uint64_t b_off = w_off + uint64_t(gi) * kg * rsc * 2;
         const bool do_params = first_group && bind_params;
         auto rebind = [=](cudaStream_t s) {
@@ -511,7 +556,9 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
         produced = {};
         cur = pout;
         pool_fused = true;
-        if (pool_flat) {  // written NCHW: the flatten step is free
+        if (avg_cand) {  // the pooled [N][C] vector (the next layer, pool_avg, is skipped)
+          cur = pout;
+        } else if (pool_flat) {  // written NCHW: the flatten step is free
           cur = {pout.p, batch, 1, 1, pout.h * pout.w * pout.c};
           flat_done = true;
         }

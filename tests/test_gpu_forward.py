@@ -37,7 +37,7 @@ from tests import torch_ref
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("alexnet", 1), ("alexnet", 2), ("resnet50", 1), ("resnet50", 4), ("resnet50", 16), ("vgg16", 1),
+CASES = [("alexnet", 1), ("alexnet", 2), ("resnet50", 1), ("resnet50", 2), ("resnet50", 4), ("resnet50", 16), ("vgg16", 1),
          ("vgg19", 1)]
 
 
@@ -143,8 +143,8 @@ def _layerwise(arch, view, net, name, batch):
     report = []
     for i, l in enumerate(arch.layers):
         want = torch_ref.apply_layer_bf16(arch, i, W, cur, named, batch)
-        if dev[i] is None:  # conv with its 2x2 max pool fused: checked through the pool layer's tap
-            assert l.kind == "conv" and arch.layers[i + 1].kind == "pool_max", f"layer {i} has no tap"
+        if dev[i] is None:  # conv with its 2x2 max / global average pool fused: checked through the pool's tap
+            assert l.kind == "conv" and arch.layers[i + 1].kind in ("pool_max", "pool_avg"), f"layer {i} has no tap"
             report.append((i, l.kind, l.name, "fused"))
             cur = want
             if l.out:
