@@ -447,14 +447,24 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
                                 layers[li + 1].s("src") == l.s("src") && layers[li + 1].i("groups", 1) == 1 &&
                                 !pending;
         const bool pair_second = pending && groups == 1;
-        if (pair_first || pair_second) prep->pair = false;  // grouped launches run single-CTA GEMMs
+        // The two groups of a 2-group implicit conv (AlexNet conv4/conv5) are
+        // independent GEMMs on disjoint input channels and output columns: one
+        // launch runs both (TRIMS_GROUP_PAIR=0: A/B).
+        static const bool gpair_on = [] {
+          const char* e = std::getenv("TRIMS_GROUP_PAIR");
+          return !(e && std::string(e) == "0");
+        }();
+        const bool gpair_first = gpair_on && groups == 2 && implicit && gi == 0 && !pending && !pool_cand && !avg_cand;
+        const bool gpair_second = groups == 2 && implicit && gi == 1 && bool(pending);
+        if (pair_first || pair_second || gpair_first || gpair_second) prep->pair = false;  // grouped launches run single-CTA GEMMs
         // weight multicast across M-tiles for a GEMM launched alone (latency mode)
-        if (split_ok && !pair_first && !pair_second) prep->mc = gemm::pick_mc(*prep, sms_);
+        if (split_ok && !pair_first && !pair_second && !gpair_first && !gpair_second) prep->mc = gemm::pick_mc(*prep, sms_);
         // a multi-wave GEMM launched alone runs persistent CTAs (one per SM,
         // double-buffered accumulators: each tile's epilogue overlaps the next
         // tile's k-loop), in place of a 2-SM pair too (mode 1: only when the
         // pair's k-loop is short)
-        if (!pair_first && !pair_second && !lean && prep->splits == 1 && prep->mc <= 1 && prep->tma_out) {
+        if (!pair_first && !pair_second && !gpair_first && !gpair_second && !lean && prep->splits == 1 && prep->mc <= 1 &&
+            prep->tma_out) {
           const uint64_t tiles = gemm::tile_rows(*prep) / 128 * ((prep->N + prep->bn - 1) / prep->bn);
           const uint64_t kb = (uint64_t(kp) + 63) / 64;
           const int mode = persist_mode();
@@ -518,7 +528,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
                                          gemm::b_box_rows(*prep));
           if (do_params) bind_params(s);
         };
-        if (pair_second) {
+        if (pair_second || gpair_second) {
           auto a = pending->prep;
           auto rb_a = pending->rebind;
           pending.reset();
@@ -539,7 +549,7 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
             steps_.push_back(std::make_unique<Step>(Step{[a](cudaStream_t s) { gemm::run(*a, s); }, rb_a}));
             steps_.push_back(std::make_unique<Step>(Step{[prep](cudaStream_t s) { gemm::run(*prep, s); }, rebind}));
           }
-        } else if (pair_first) {
+        } else if (pair_first || gpair_first) {
           pending = Pending{prep, rebind};
         } else {
           steps_.push_back(std::make_unique<Step>(Step{[prep](cudaStream_t s) { gemm::run(*prep, s); }, rebind}));
