@@ -113,6 +113,16 @@ bool branches_enabled() {
   return on;
 }
 
+// TRIMS_GROUP_PAIR=0: the two groups of a 2-group conv launch separately
+// (A/B switch; on: one paired GEMM launch, and one im2col for both groups).
+bool group_pair_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("TRIMS_GROUP_PAIR");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
 // TRIMS_PAIR=0 launches ResNet's downsample and the stage's first 1x1 conv
 // (same input, independent) separately instead of as one grouped launch.
 bool pairing_enabled() {
@@ -231,8 +241,9 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
         const int k = l.i("k", 1), groups = l.i("groups", 1), cg = l.i("cin") / groups;
         const bool direct = k == 1 && l.i("stride", 1) == 1 && l.i("pad", 0) == 0 && groups == 1;
         const bool implicit = !direct && cg % 64 == 0 && implicit_enabled();
-        if (!direct && !implicit)
-          col_elems = std::max<uint64_t>(col_elems, uint64_t(batch) * P * Q * ((uint64_t(k) * k * cg + 7) / 8 * 8));
+        if (!direct && !implicit)  // a 2-group conv keeps both groups' columns (one im2col, one paired GEMM launch)
+          col_elems = std::max<uint64_t>(col_elems, uint64_t(groups == 2 ? 2 : 1) * batch * P * Q *
+                                                        ((uint64_t(k) * k * cg + 7) / 8 * 8));
         a = {nullptr, batch, P, Q, l.i("cout")};
         if (!l.s("out").empty()) named[l.s("out")] = a;
       } else if (l.kind == "pool_max") {
@@ -381,9 +392,20 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
       bool fused_here = false;
       Act pout{};
       bool first_group = true;
+      // both groups of a 2-group im2col conv (AlexNet conv2): one im2col launch
+      // into side-by-side column buffers, then one paired GEMM launch
+      const bool gcol = group_pair_enabled() && groups == 2 && !direct && !implicit &&
+                        !(li == 1 && layers[0].kind == "input" && l.s("src").empty() && first_conv_fusable(l));
       for (int gi = 0; gi < groups; ++gi) {
-        const uint16_t* A = direct ? in.p : col;
-        if (!direct && !implicit) {
+        const uint16_t* A = direct ? in.p : gcol ? col + uint64_t(gi) * M * kp : col;
+        if (gcol) {
+          if (gi == 0) {
+            const Act src = in;
+            steps_.push_back(std::make_unique<Step>(Step{[=](cudaStream_t s) {
+              nn::im2col(src.p, col, src.n, src.h, src.w, src.c, 0, cg, k, k, st, pad, P, Q, kp, s, 2);
+            }}));
+          }
+        } else if (!direct && !implicit) {
           const Act src = in;
           if (li == 1 && layers[0].kind == "input" && l.s("src").empty() && first_conv_fusable(l)) {
             const float* x = input_;
@@ -450,12 +472,9 @@ Net::Net(int device, const std::string& arch, const fmt::Manifest& resident, con
         // The two groups of a 2-group implicit conv (AlexNet conv4/conv5) are
         // independent GEMMs on disjoint input channels and output columns: one
         // launch runs both (TRIMS_GROUP_PAIR=0: A/B).
-        static const bool gpair_on = [] {
-          const char* e = std::getenv("TRIMS_GROUP_PAIR");
-          return !(e && std::string(e) == "0");
-        }();
-        const bool gpair_first = gpair_on && groups == 2 && implicit && gi == 0 && !pending && !pool_cand && !avg_cand;
-        const bool gpair_second = groups == 2 && implicit && gi == 1 && bool(pending);
+        const bool gpair_first =
+            group_pair_enabled() && groups == 2 && (implicit || gcol) && gi == 0 && !pending && !pool_cand && !avg_cand;
+        const bool gpair_second = groups == 2 && (implicit || gcol) && gi == 1 && bool(pending);
         if (pair_first || pair_second || gpair_first || gpair_second) prep->pair = false;  // grouped launches run single-CTA GEMMs
         // weight multicast across M-tiles for a GEMM launched alone (latency mode)
         if (split_ok && !pair_first && !pair_second && !gpair_first && !gpair_second) prep->mc = gemm::pick_mc(*prep, sms_);

@@ -16,8 +16,10 @@
 namespace trims::nn {
 
 void input_prep(const float* in_nchw, uint16_t* out_nhwc, int N, int C, int H, int W, cudaStream_t s);
+// groups > 1: that many consecutive channel groups (from c_off) in one launch,
+// group g's columns at A + g * N*P*Q * Kp
 void im2col(const uint16_t* in, uint16_t* A, int N, int H, int W, int Ctot, int c_off, int Cg, int R, int S, int stride,
-            int pad, int P, int Q, int Kp, cudaStream_t s);
+            int pad, int P, int Q, int Kp, cudaStream_t s, int groups = 1);
 // nchw: write NCHW (the flatten order of a following FC) instead of NHWC.
 void maxpool(const uint16_t* in, uint16_t* out, int N, int H, int W, int C, int k, int stride, int pad, int P, int Q,
              cudaStream_t s, bool nchw = false);

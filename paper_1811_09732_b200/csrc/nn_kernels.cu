@@ -46,6 +46,9 @@ __global__ void im2col_kernel(const uint16_t* __restrict__ in, uint16_t* __restr
   const int RSC = R * S * Cg;
   const bool vec = (Cg % 8 == 0) && (Ctot % 8 == 0) && (c_off % 8 == 0) && (Kp % 8 == 0);
   const uint64_t M = uint64_t(N) * P * Q;
+  // grid.y = channel groups written side by side: group g's columns go to A + g * M * Kp
+  c_off += int(blockIdx.y) * Cg;
+  A += uint64_t(blockIdx.y) * M * Kp;
   if (vec) {
     const int cols8 = Kp / 8;
     const uint64_t total = M * cols8;
@@ -400,9 +403,10 @@ void input_prep(const float* in, uint16_t* out, int N, int C, int H, int W, cuda
 }
 
 void im2col(const uint16_t* in, uint16_t* A, int N, int H, int W, int Ctot, int c_off, int Cg, int R, int S, int stride,
-            int pad, int P, int Q, int Kp, cudaStream_t s) {
+            int pad, int P, int Q, int Kp, cudaStream_t s, int groups) {
   const uint64_t work = uint64_t(N) * P * Q * ((Cg % 8 == 0 && Ctot % 8 == 0 && c_off % 8 == 0 && Kp % 8 == 0) ? Kp / 8 : R);
-  launch_pdl(im2col_kernel, dim3(blocks(work)), dim3(256), 0, s, in, A, N, H, W, Ctot, c_off, Cg, R, S, stride, pad, P, Q, Kp);
+  launch_pdl(im2col_kernel, dim3(blocks(work), unsigned(groups)), dim3(256), 0, s, in, A, N, H, W, Ctot, c_off, Cg, R, S,
+             stride, pad, P, Q, Kp);
   TRIMS_CUDA(cudaGetLastError());
 }
 
